@@ -1,0 +1,228 @@
+/*
+ * dflb200 -- B200-native solve phase of subdomain-deflated Krylov solvers
+ * preconditioned by per-subdomain smoothed-aggregation AMG (arXiv 1710.03940).
+ *
+ * C ABI of libdflb200.so.  Plain pointers and sizes only; no torch / C++
+ * types cross this boundary.  Every function returns 0 on success or a
+ * negative DFL_E_* status; the message of the last failure of a context is
+ * returned by dfl_last_error(ctx) (dfl_last_setup_error() for context-free
+ * setup calls).  Status codes map 1:1 onto the reference's exception classes
+ * (pkg/src/deflamg/errors.py:4-37).
+ *
+ * The entry points replace, in the reference package deflamg 0.1.0:
+ *
+ *   host setup (stays on the CPU, timed separately, native C++ here):
+ *     dfl_hier_build        <- amg.py:217-250 build_hierarchy (+ strength_filter :70-84,
+ *                              aggregate :87-125, smooth_prolongation :136-157,
+ *                              spai0_weights :160-166, dense_lu sparse.py:226-244)
+ *     dfl_basis_az          <- deflation.py:140-149 (AZ = spgemm(A, Z) and the
+ *                              per-subdomain rows of E = Z'AZ)
+ *     dfl_dense_inverse     <- sparse.py:226-244 dense_lu (+ singularity check)
+ *
+ *   device solve (sm_100a kernels):
+ *     dfl_ctx_set_operator  <- runtime.py:117-152 split_matrix output (SubdomainView)
+ *                              and runtime.py:246-271 halo_exchange plan
+ *     dfl_ctx_add_hierarchy <- deflation.py:208 (one AmgHierarchy per subdomain)
+ *     dfl_ctx_set_deflation <- deflation.py:83-163 DeflationBasis (Z, AZ, E factor)
+ *     dfl_solve             <- deflation.py:254-312 DeflatedSolver.solve, with
+ *                              krylov.py:95-145 cg / krylov.py:148-285 bicgstab2
+ *     dfl_op_apply          <- runtime.py:283-292 DistributedOperator.apply
+ *     dfl_precond_apply     <- deflation.py:239-250 preconditioner -> amg.py:201-212
+ *     dfl_project           <- deflation.py:230-233 DeflatedSolver.project
+ *     dfl_coarse_lift       <- deflation.py:235-237 DeflatedSolver.coarse_lift
+ *     dfl_dot               <- runtime.py:297-304 partition_dot
+ *     dfl_spmv_csr          <- _kernels.pyx:11-23 spmv_rows (the reference's plugin
+ *                              seam, backend.py:126-146, as one device call)
+ */
+#ifndef DFLB200_H
+#define DFLB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DFLB200_ABI_VERSION 1
+
+/* status codes */
+#define DFL_OK 0
+#define DFL_E_DIMENSION (-1)   /* DimensionError */
+#define DFL_E_STRUCTURE (-2)   /* StructureError */
+#define DFL_E_SINGULAR (-3)    /* SingularMatrixError */
+#define DFL_E_PARTITION (-4)   /* PartitionError */
+#define DFL_E_COMM (-5)        /* CommunicatorError (NCCL / halo) */
+#define DFL_E_CONFIG (-6)      /* ConfigError */
+#define DFL_E_CUDA (-7)        /* CUDA runtime failure */
+#define DFL_E_STATE (-8)       /* call out of order (e.g. solve before finalize) */
+
+/* relaxation kinds (precond.relax.type) */
+#define DFL_RELAX_DAMPED_JACOBI 0
+#define DFL_RELAX_SPAI0 1
+
+/* solver kinds (solver.type) */
+#define DFL_SOLVER_CG 0
+#define DFL_SOLVER_BICGSTAB2 1
+
+/* which matrix of a hierarchy level */
+#define DFL_LEVEL_A 0
+#define DFL_LEVEL_P 1
+#define DFL_LEVEL_R 2
+
+/* pointer residency for dfl_solve / unit ops */
+#define DFL_PTR_HOST 0
+#define DFL_PTR_DEVICE 1
+
+/* breakdown codes of dfl_report.breakdown (strings: dfl_breakdown_string) */
+#define DFL_BRK_NONE 0
+#define DFL_BRK_CURVATURE 1      /* cg: non-positive curvature p'Ap */
+#define DFL_BRK_RZ 2             /* cg: preconditioned residual product degenerated */
+#define DFL_BRK_RHO 3            /* bicgstab2: rho degenerated in the BiCG stage */
+#define DFL_BRK_SHADOW 4         /* bicgstab2: shadow product degenerated */
+#define DFL_BRK_MR 5             /* bicgstab2: minimal-residual basis degenerated */
+#define DFL_BRK_OMEGA 6          /* bicgstab2: stabilization weight vanished */
+
+/* host CSR view: int64 indices, fp64 values (the reference's SparseMatrix
+ * layout, sparse.py:50-58) */
+typedef struct {
+    int64_t nrows;
+    int64_t ncols;
+    const int64_t *row_ptr; /* nrows + 1 */
+    const int64_t *col_idx; /* row_ptr[nrows] */
+    const double *values;   /* row_ptr[nrows] */
+} dfl_csr;
+
+/* AmgOptions (amg.py:43-67) */
+typedef struct {
+    double eps_strong;     /* 0.08 */
+    double omega;          /* 2/3 */
+    double damping;        /* 0.8 */
+    int32_t relax;         /* DFL_RELAX_* */
+    int32_t max_levels;    /* 25 */
+    int64_t coarse_enough; /* 500 */
+} dfl_amg_options;
+
+typedef struct {
+    int32_t solver;       /* DFL_SOLVER_* */
+    int32_t maxiter;      /* solver.maxiter */
+    int32_t refresh_every;/* 50 (krylov.py:41) */
+    int32_t deflated;     /* 0: plain block-AMG Krylov (deflation.py:287-290) */
+    double tol;           /* solver.tol: atol = tol * ||b|| (deflation.py:266-270) */
+} dfl_solve_params;
+
+typedef struct {
+    int32_t iterations;
+    int32_t converged;
+    int32_t breakdown;          /* DFL_BRK_* */
+    int32_t device_loop;        /* 1: the Krylov loop ran as a device-side graph loop */
+    double bnorm;
+    double resnorm;             /* final recurrence residual norm */
+    double relative_residual;   /* true ||b - A x|| / ||b|| (deflation.py:293-297) */
+    double solve_seconds;       /* device time of the solve phase (Krylov + lift) */
+    double h2d_seconds;
+    double d2h_seconds;
+    int64_t kernel_launches;    /* kernels of this library launched by the solve */
+} dfl_report;
+
+typedef struct dfl_matrix dfl_matrix; /* host CSR produced by setup */
+typedef struct dfl_hier dfl_hier;     /* host AMG hierarchy */
+typedef struct dfl_ctx dfl_ctx;       /* device solve context (one rank) */
+
+/* ---- library ----------------------------------------------------------- */
+int dfl_abi_version(void);
+const char *dfl_last_setup_error(void);
+const char *dfl_breakdown_string(int code);
+
+/* ---- host setup (C++) ----------------------------------------------------- */
+int dfl_hier_build(const dfl_csr *A, const dfl_amg_options *opts, dfl_hier **out);
+int dfl_hier_num_levels(const dfl_hier *h);
+/* shape of level l's A / P / R (P and R absent at the bottom level: nnz = -1) */
+int dfl_hier_level_shape(const dfl_hier *h, int level, int which, int64_t *nrows,
+                         int64_t *ncols, int64_t *nnz);
+int dfl_hier_level_copy(const dfl_hier *h, int level, int which, int64_t *row_ptr,
+                        int64_t *col_idx, double *values);
+/* relaxation weights w of level l: (damping * 1/a_ii) or SPAI-0 a_ii / sum a_ij^2 */
+int dfl_hier_level_weights(const dfl_hier *h, int level, double *w);
+/* bottom level: dense inverse (n x n, row-major) of the LU-factorised block */
+int dfl_hier_bottom_inverse(const dfl_hier *h, double *inv);
+void dfl_hier_free(dfl_hier *h);
+
+/* AZ rows of this rank (deflation.py:140) and its rows of E = Z'AZ.
+ *   A      : n_local x n_ext rows of the global operator, columns [0, n_local)
+ *            own, [n_local, n_ext) ghosts, entries in the global CSR order
+ *   zext   : n_ext x k values of Z on every extended column (row-major)
+ *   owner  : n_ext global subdomain index of every extended column
+ *   rowsub : n_local global subdomain index of every own row
+ *   K      : global coarse dimension m*k
+ * Outputs: *AZ (n_local x K, exact zeros dropped unless keep_zeros) and
+ * E_rows (nsub_local*k x K, row-major) for subdomains [sub0, sub0+nsub). */
+int dfl_basis_az(const dfl_csr *A, int32_t k, const double *zext, const int32_t *owner,
+                 const int32_t *rowsub, int64_t K, int32_t sub0, int32_t nsub, int32_t keep_zeros,
+                 dfl_matrix **AZ, double *E_rows);
+int dfl_matrix_shape(const dfl_matrix *m, int64_t *nrows, int64_t *ncols, int64_t *nnz);
+int dfl_matrix_copy(const dfl_matrix *m, int64_t *row_ptr, int64_t *col_idx, double *values);
+void dfl_matrix_free(dfl_matrix *m);
+
+/* LU with partial pivoting; DFL_E_SINGULAR with the reference's criterion
+ * (min |u_ii| <= 1e-14 max |u_ii|, sparse.py:236-241); writes inv (n x n). */
+int dfl_dense_inverse(int64_t n, const double *a, double *inv);
+
+/* ---- device context ----------------------------------------------------------- */
+int dfl_ctx_create(int device, dfl_ctx **out);
+void dfl_ctx_destroy(dfl_ctx *ctx);
+const char *dfl_last_error(const dfl_ctx *ctx);
+
+/* multi-process (one rank per GPU) communicator over NCCL; nccl_id is the
+ * 128-byte ncclUniqueId produced on rank 0 by dfl_nccl_unique_id */
+int dfl_nccl_unique_id(void *nccl_id_128);
+int dfl_ctx_set_comm(dfl_ctx *ctx, int nranks, int rank, const void *nccl_id_128);
+
+/* Operator rows of this rank (all its subdomains), columns renumbered as in
+ * dfl_basis_az, entries in the global CSR order.
+ *   sub_offsets : nsub+1 rank-local row offsets of the rank's subdomains
+ *   halo plan   : for each neighbour rank q (ascending): recv_counts[q] ghost
+ *                 values arrive (they fill the ghost columns in ascending
+ *                 global order), send_counts[q] values go out, taken from own
+ *                 rows send_idx[...] (concatenated in neighbour order). */
+int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int64_t *sub_offsets,
+                         int32_t nnbr, const int32_t *nbr_rank, const int64_t *recv_counts,
+                         const int64_t *send_counts, const int64_t *send_idx);
+/* the AMG hierarchy of local subdomain `sub` (uploaded, host copy not kept) */
+int dfl_ctx_add_hierarchy(dfl_ctx *ctx, int32_t sub, const dfl_hier *h);
+/* deflation data of this rank: k columns per subdomain; zcols = n_local x (k-1)
+ * non-constant columns (row-major, NULL when k == 1); AZ = n_local x K;
+ * Einv = K x K inverse of E (row-major); first_sub = global index of the
+ * rank's first subdomain. */
+int dfl_ctx_set_deflation(dfl_ctx *ctx, int32_t k, const double *zcols, const dfl_csr *AZ,
+                          int64_t K, const double *Einv, int32_t first_sub);
+/* converts layouts, builds launch plans; call once after the uploads */
+int dfl_ctx_finalize(dfl_ctx *ctx);
+
+/* device bytes held by the context */
+int64_t dfl_ctx_device_bytes(const dfl_ctx *ctx);
+
+/* ---- solve phase ------------------------------------------------------------------- */
+int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *x, int ptr_kind,
+              dfl_report *rep);
+
+/* unit operations on this rank's vectors (n_local), host or device pointers */
+int dfl_op_apply(dfl_ctx *ctx, const double *x, double *y, int ptr_kind);
+int dfl_precond_apply(dfl_ctx *ctx, const double *r, double *z, int ptr_kind);
+int dfl_project(dfl_ctx *ctx, const double *r, double *out, int ptr_kind);
+int dfl_coarse_lift(dfl_ctx *ctx, const double *r, double *out, int ptr_kind);
+int dfl_dot(dfl_ctx *ctx, const double *a, const double *b, int ptr_kind, double *out);
+
+/* stand-alone CSR SpMV on the device (rows of A; x has A->ncols entries) --
+ * the per-kernel seam of the reference (backend.py:126-146) */
+int dfl_spmv_csr(const dfl_csr *A, const double *x, double *y, int device);
+
+/* timing of the unit operations for the roofline: runs `reps` back-to-back
+ * launches of the named kernel family on the context's data and returns the
+ * mean device milliseconds per launch and the algorithmic bytes per launch.
+ *   what: 0 = operator SpMV (fine A), 1 = V-cycle, 2 = CG iteration */
+int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms_per_launch, double *bytes_per_launch);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DFLB200_H */

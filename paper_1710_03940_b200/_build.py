@@ -1,0 +1,68 @@
+"""Build libdflb200.so in-tree: nvcc for the sm_100a kernels, g++ for the host
+setup (no FMA contraction, so the AMG hierarchy matches the reference bit for
+bit).  Invoked by ``__graft_entry__.build()`` and ``python -m
+paper_1710_03940_b200._build``."""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libdflb200.so")
+BUILD = os.path.join(REPO, "build", "dflb200")
+
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+CU_SOURCES = ["ctx.cu"]
+CXX_SOURCES = ["host_setup.cpp"]
+
+
+def _nvcc() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _sources():
+    hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
+    hdrs.append(os.path.join(REPO, "include", "dflb200.h"))
+    return [os.path.join(CSRC, f) for f in CU_SOURCES + CXX_SOURCES] + hdrs
+
+
+def up_to_date() -> bool:
+    if not os.path.exists(LIB):
+        return False
+    t = os.path.getmtime(LIB)
+    return all(os.path.getmtime(s) <= t for s in _sources())
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and up_to_date():
+        return LIB
+    os.makedirs(BUILD, exist_ok=True)
+    nvcc = _nvcc()
+    objs = []
+    run = lambda cmd: subprocess.run(cmd, check=True, stdout=None if verbose else subprocess.DEVNULL)
+    for f in CXX_SOURCES:
+        o = os.path.join(BUILD, f + ".o")
+        run(["g++", "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
+             "-I", os.path.join(REPO, "include"), "-c", os.path.join(CSRC, f), "-o", o])
+        objs.append(o)
+    for f in CU_SOURCES:
+        o = os.path.join(BUILD, f + ".o")
+        run([nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-Xcompiler", "-ffp-contract=off", "-I", os.path.join(REPO, "include"),
+             "-c", os.path.join(CSRC, f), "-o", o])
+        objs.append(o)
+    tmp = LIB + ".tmp"
+    run([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-ldl", "-lpthread"])
+    os.replace(tmp, LIB)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose=True))

@@ -1,0 +1,331 @@
+"""ctypes binding of libdflb200.so (include/dflb200.h).
+
+The library is required: importing this module on a machine where it cannot
+be loaded raises :class:`~paper_1710_03940_b200.errors.DeviceError` -- there is
+no CPU fallback for the solve.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from .errors import DeviceError, raise_for_status
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libdflb200.so")
+
+c_i64 = ctypes.c_int64
+c_i32 = ctypes.c_int32
+c_dbl = ctypes.c_double
+c_vp = ctypes.c_void_p
+
+DFL_RELAX = {"damped_jacobi": 0, "spai0": 1}
+DFL_SOLVER = {"cg": 0, "bicgstab2": 1}
+PTR_HOST, PTR_DEVICE = 0, 1
+LEVEL_A, LEVEL_P, LEVEL_R = 0, 1, 2
+
+
+class Csr(ctypes.Structure):
+    _fields_ = [("nrows", c_i64), ("ncols", c_i64), ("row_ptr", c_vp), ("col_idx", c_vp), ("values", c_vp)]
+
+
+class AmgOptions(ctypes.Structure):
+    _fields_ = [("eps_strong", c_dbl), ("omega", c_dbl), ("damping", c_dbl), ("relax", c_i32),
+                ("max_levels", c_i32), ("coarse_enough", c_i64)]
+
+
+class SolveParams(ctypes.Structure):
+    _fields_ = [("solver", c_i32), ("maxiter", c_i32), ("refresh_every", c_i32), ("deflated", c_i32),
+                ("tol", c_dbl)]
+
+
+class Report(ctypes.Structure):
+    _fields_ = [("iterations", c_i32), ("converged", c_i32), ("breakdown", c_i32), ("device_loop", c_i32),
+                ("bnorm", c_dbl), ("resnorm", c_dbl), ("relative_residual", c_dbl),
+                ("solve_seconds", c_dbl), ("h2d_seconds", c_dbl), ("d2h_seconds", c_dbl),
+                ("kernel_launches", c_i64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdflb200.so (built in-tree by ``paper_1710_03940_b200._build``)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(
+            f"{LIB_PATH} is missing: build it with `python -m paper_1710_03940_b200._build` "
+            "(there is no CPU fallback for the solve)"
+        )
+    try:
+        L = ctypes.CDLL(LIB_PATH)
+    except OSError as exc:
+        raise DeviceError(f"cannot load {LIB_PATH}: {exc}") from exc
+    P = ctypes.POINTER
+    sig = {
+        "dfl_abi_version": ([], c_i32),
+        "dfl_last_setup_error": ([], ctypes.c_char_p),
+        "dfl_breakdown_string": ([c_i32], ctypes.c_char_p),
+        "dfl_hier_build": ([P(Csr), P(AmgOptions), P(c_vp)], c_i32),
+        "dfl_hier_num_levels": ([c_vp], c_i32),
+        "dfl_hier_level_shape": ([c_vp, c_i32, c_i32, P(c_i64), P(c_i64), P(c_i64)], c_i32),
+        "dfl_hier_level_copy": ([c_vp, c_i32, c_i32, c_vp, c_vp, c_vp], c_i32),
+        "dfl_hier_level_weights": ([c_vp, c_i32, c_vp], c_i32),
+        "dfl_hier_bottom_inverse": ([c_vp, c_vp], c_i32),
+        "dfl_hier_free": ([c_vp], None),
+        "dfl_basis_az": ([P(Csr), c_i32, c_vp, c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, P(c_vp), c_vp], c_i32),
+        "dfl_matrix_shape": ([c_vp, P(c_i64), P(c_i64), P(c_i64)], c_i32),
+        "dfl_matrix_copy": ([c_vp, c_vp, c_vp, c_vp], c_i32),
+        "dfl_matrix_free": ([c_vp], None),
+        "dfl_dense_inverse": ([c_i64, c_vp, c_vp], c_i32),
+        "dfl_ctx_create": ([c_i32, P(c_vp)], c_i32),
+        "dfl_ctx_destroy": ([c_vp], None),
+        "dfl_last_error": ([c_vp], ctypes.c_char_p),
+        "dfl_nccl_unique_id": ([c_vp], c_i32),
+        "dfl_ctx_set_comm": ([c_vp, c_i32, c_i32, c_vp], c_i32),
+        "dfl_ctx_set_operator": ([c_vp, P(Csr), c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp], c_i32),
+        "dfl_ctx_add_hierarchy": ([c_vp, c_i32, c_vp], c_i32),
+        "dfl_ctx_set_deflation": ([c_vp, c_i32, c_vp, P(Csr), c_i64, c_vp, c_i32], c_i32),
+        "dfl_ctx_finalize": ([c_vp], c_i32),
+        "dfl_ctx_device_bytes": ([c_vp], c_i64),
+        "dfl_solve": ([c_vp, P(SolveParams), c_vp, c_vp, c_i32, P(Report)], c_i32),
+        "dfl_op_apply": ([c_vp, c_vp, c_vp, c_i32], c_i32),
+        "dfl_precond_apply": ([c_vp, c_vp, c_vp, c_i32], c_i32),
+        "dfl_project": ([c_vp, c_vp, c_vp, c_i32], c_i32),
+        "dfl_coarse_lift": ([c_vp, c_vp, c_vp, c_i32], c_i32),
+        "dfl_dot": ([c_vp, c_vp, c_vp, c_i32, P(c_dbl)], c_i32),
+        "dfl_spmv_csr": ([P(Csr), c_vp, c_vp, c_i32], c_i32),
+        "dfl_ctx_time": ([c_vp, c_i32, c_i32, P(c_dbl), P(c_dbl)], c_i32),
+    }
+    for name, (args, res) in sig.items():
+        fn = getattr(L, name)
+        fn.argtypes = args
+        fn.restype = res
+    _lib = L
+    return L
+
+
+EXPORTED = None  # filled lazily by exported_symbols()
+
+
+def exported_symbols():
+    """The dfl_* functions include/dflb200.h declares."""
+    import re
+
+    hdr = os.path.join(os.path.dirname(_PKG), "include", "dflb200.h")
+    with open(hdr) as fh:
+        text = fh.read()
+    return sorted(set(re.findall(r"\b(dfl_[a-z0-9_]+)\s*\(", text)))
+
+
+def _ptr(a: np.ndarray):
+    return c_vp(a.ctypes.data) if a is not None else None
+
+
+def setup_error() -> str:
+    return (lib().dfl_last_setup_error() or b"").decode()
+
+
+def check(rc: int, ctx=None) -> None:
+    if rc != 0:
+        msg = (lib().dfl_last_error(ctx) if ctx is not None else lib().dfl_last_setup_error()) or b""
+        raise_for_status(rc, msg.decode())
+
+
+class CsrArrays:
+    """Keeps numpy buffers alive for a ctypes Csr view."""
+
+    def __init__(self, nrows, ncols, row_ptr, col_idx, values):
+        self.row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int64)
+        self.col_idx = np.ascontiguousarray(col_idx, dtype=np.int64)
+        self.values = np.ascontiguousarray(values, dtype=np.float64)
+        self.s = Csr(int(nrows), int(ncols), _ptr(self.row_ptr), _ptr(self.col_idx), _ptr(self.values))
+
+
+class Hierarchy:
+    """Host AMG hierarchy built by the native setup (dfl_hier_build)."""
+
+    def __init__(self, A: CsrArrays, opts: AmgOptions):
+        h = c_vp()
+        check(lib().dfl_hier_build(ctypes.byref(A.s), ctypes.byref(opts), ctypes.byref(h)))
+        self.h = h
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.dfl_hier_free(self.h)
+            self.h = None
+
+    @property
+    def nlevels(self) -> int:
+        return lib().dfl_hier_num_levels(self.h)
+
+    def level_shape(self, level: int, which: int = LEVEL_A):
+        r, c, z = c_i64(), c_i64(), c_i64()
+        check(lib().dfl_hier_level_shape(self.h, level, which, ctypes.byref(r), ctypes.byref(c), ctypes.byref(z)))
+        return r.value, c.value, z.value
+
+    @property
+    def level_sizes(self):
+        return [self.level_shape(l)[0] for l in range(self.nlevels)]
+
+    def level_nnz(self):
+        return [self.level_shape(l)[2] for l in range(self.nlevels)]
+
+    def matrix(self, level: int, which: int = LEVEL_A):
+        nr, nc, nnz = self.level_shape(level, which)
+        if nnz < 0:
+            return None
+        ptr = np.empty(nr + 1, dtype=np.int64)
+        col = np.empty(nnz, dtype=np.int64)
+        val = np.empty(nnz, dtype=np.float64)
+        check(lib().dfl_hier_level_copy(self.h, level, which, _ptr(ptr), _ptr(col), _ptr(val)))
+        return nr, nc, ptr, col, val
+
+    def weights(self, level: int) -> np.ndarray:
+        n = self.level_shape(level)[0]
+        w = np.empty(n)
+        check(lib().dfl_hier_level_weights(self.h, level, _ptr(w)))
+        return w
+
+    def bottom_inverse(self) -> np.ndarray:
+        n = self.level_shape(self.nlevels - 1)[0]
+        inv = np.empty((n, n))
+        check(lib().dfl_hier_bottom_inverse(self.h, _ptr(inv)))
+        return inv
+
+
+def basis_az(A: CsrArrays, k: int, zext: np.ndarray, owner: np.ndarray, rowsub: np.ndarray, K: int,
+             sub0: int, nsub: int, keep_zeros: bool = False):
+    zext = np.ascontiguousarray(zext, dtype=np.float64)
+    owner = np.ascontiguousarray(owner, dtype=np.int32)
+    rowsub = np.ascontiguousarray(rowsub, dtype=np.int32)
+    E_rows = np.zeros((nsub * k, K))
+    m = c_vp()
+    check(lib().dfl_basis_az(ctypes.byref(A.s), k, _ptr(zext), _ptr(owner), _ptr(rowsub), K, sub0, nsub,
+                             1 if keep_zeros else 0, ctypes.byref(m), _ptr(E_rows)))
+    try:
+        r, c, z = c_i64(), c_i64(), c_i64()
+        check(lib().dfl_matrix_shape(m, ctypes.byref(r), ctypes.byref(c), ctypes.byref(z)))
+        ptr = np.empty(r.value + 1, dtype=np.int64)
+        col = np.empty(z.value, dtype=np.int64)
+        val = np.empty(z.value)
+        check(lib().dfl_matrix_copy(m, _ptr(ptr), _ptr(col), _ptr(val)))
+    finally:
+        lib().dfl_matrix_free(m)
+    return (r.value, c.value, ptr, col, val), E_rows
+
+
+def dense_inverse(a: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    n = a.shape[0]
+    inv = np.empty((n, n))
+    check(lib().dfl_dense_inverse(n, _ptr(a), _ptr(inv)))
+    return inv
+
+
+class DeviceContext:
+    """One rank's device state (dfl_ctx)."""
+
+    def __init__(self, device: int = 0):
+        h = c_vp()
+        check(lib().dfl_ctx_create(int(device), ctypes.byref(h)))
+        self.h = h
+        self.device = device
+
+    def close(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.dfl_ctx_destroy(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def _c(self, rc):
+        check(rc, self.h)
+
+    def set_comm(self, nranks: int, rank: int, nccl_id: bytes):
+        buf = ctypes.create_string_buffer(nccl_id, 128)
+        self._c(lib().dfl_ctx_set_comm(self.h, nranks, rank, buf))
+
+    def set_operator(self, A: CsrArrays, sub_offsets, nbr, recv_counts, send_counts, send_idx):
+        self._keep_sub = np.ascontiguousarray(sub_offsets, dtype=np.int64)
+        nbr = np.ascontiguousarray(nbr, dtype=np.int32)
+        rc_ = np.ascontiguousarray(recv_counts, dtype=np.int64)
+        sc_ = np.ascontiguousarray(send_counts, dtype=np.int64)
+        si = np.ascontiguousarray(send_idx, dtype=np.int64)
+        self._c(lib().dfl_ctx_set_operator(self.h, ctypes.byref(A.s), len(self._keep_sub) - 1,
+                                           _ptr(self._keep_sub), len(nbr), _ptr(nbr), _ptr(rc_), _ptr(sc_),
+                                           _ptr(si)))
+
+    def add_hierarchy(self, sub: int, h: Hierarchy):
+        self._c(lib().dfl_ctx_add_hierarchy(self.h, sub, h.h))
+
+    def set_deflation(self, k: int, zcols, AZ: CsrArrays, K: int, Einv, first_sub: int):
+        zc = np.ascontiguousarray(zcols, dtype=np.float64) if zcols is not None and k > 1 else None
+        Ei = np.ascontiguousarray(Einv, dtype=np.float64)
+        self._c(lib().dfl_ctx_set_deflation(self.h, k, _ptr(zc) if zc is not None else None,
+                                            ctypes.byref(AZ.s), K, _ptr(Ei), first_sub))
+
+    def finalize(self):
+        self._c(lib().dfl_ctx_finalize(self.h))
+
+    @property
+    def device_bytes(self) -> int:
+        return lib().dfl_ctx_device_bytes(self.h)
+
+    def solve(self, params: SolveParams, b, x, ptr_kind: int = PTR_HOST) -> Report:
+        rep = Report()
+        bp = _ptr(b) if ptr_kind == PTR_HOST else c_vp(b)
+        xp = _ptr(x) if ptr_kind == PTR_HOST else c_vp(x)
+        self._c(lib().dfl_solve(self.h, ctypes.byref(params), bp, xp, ptr_kind, ctypes.byref(rep)))
+        return rep
+
+    def _unary(self, fn, v: np.ndarray) -> np.ndarray:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.empty_like(v)
+        self._c(fn(self.h, _ptr(v), _ptr(out), PTR_HOST))
+        return out
+
+    def op_apply(self, v):
+        return self._unary(lib().dfl_op_apply, v)
+
+    def precond_apply(self, v):
+        return self._unary(lib().dfl_precond_apply, v)
+
+    def project(self, v):
+        return self._unary(lib().dfl_project, v)
+
+    def coarse_lift(self, v):
+        return self._unary(lib().dfl_coarse_lift, v)
+
+    def dot(self, a, b) -> float:
+        a = np.ascontiguousarray(a, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        out = c_dbl()
+        self._c(lib().dfl_dot(self.h, _ptr(a), _ptr(b), PTR_HOST, ctypes.byref(out)))
+        return out.value
+
+    def time(self, what: int, reps: int):
+        ms, by = c_dbl(), c_dbl()
+        self._c(lib().dfl_ctx_time(self.h, what, reps, ctypes.byref(ms), ctypes.byref(by)))
+        return ms.value, by.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    check(lib().dfl_nccl_unique_id(buf))
+    return buf.raw
+
+
+def spmv_device(A: CsrArrays, x: np.ndarray, device: int = 0) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.empty(A.s.nrows)
+    check(lib().dfl_spmv_csr(ctypes.byref(A.s), _ptr(x), _ptr(y), device))
+    return y
+
+
+def breakdown_string(code: int) -> str:
+    return (lib().dfl_breakdown_string(code) or b"").decode()

@@ -1,0 +1,1356 @@
+// Device context of one rank: uploads the host setup products into
+// device-resident layouts and runs the solve phase (deflation.py:254-312)
+// entirely on the GPU.  The Krylov loop is a CUDA graph with a device-side
+// while-conditional, so a whole CG solve is a handful of launches and no
+// host round trip per iteration (single rank); with several ranks the loop is
+// host-driven with NCCL collectives between kernels.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/dflb200.h"
+#include "host_setup.hpp"
+#include "kernels.cuh"
+
+using namespace dfl;
+
+// ---------------------------------------------------------------------------
+// minimal NCCL surface, loaded lazily (no link-time dependency)
+namespace {
+typedef struct {
+    char internal[128];
+} NcclId;
+typedef void *NcclComm;
+enum { ncclDouble_ = 8 };
+struct Nccl {
+    void *h = nullptr;
+    int (*GetUniqueId)(NcclId *) = nullptr;
+    int (*CommInitRank)(NcclComm *, int, NcclId, int) = nullptr;
+    int (*CommDestroy)(NcclComm) = nullptr;
+    int (*AllGather)(const void *, void *, size_t, int, NcclComm, cudaStream_t) = nullptr;
+    int (*Send)(const void *, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+    int (*Recv)(void *, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+    int (*GroupStart)() = nullptr;
+    int (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(int) = nullptr;
+    bool load(std::string &err) {
+        if (h) return true;
+        const char *names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char *n : names)
+            if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!h) {
+            err = "cannot load libnccl.so.2";
+            return false;
+        }
+#define LD(f, s)                                            \
+    f = reinterpret_cast<decltype(f)>(dlsym(h, s));         \
+    if (!f) {                                               \
+        err = std::string("libnccl lacks ") + s;            \
+        return false;                                       \
+    }
+        LD(GetUniqueId, "ncclGetUniqueId");
+        LD(CommInitRank, "ncclCommInitRank");
+        LD(CommDestroy, "ncclCommDestroy");
+        LD(AllGather, "ncclAllGather");
+        LD(Send, "ncclSend");
+        LD(Recv, "ncclRecv");
+        LD(GroupStart, "ncclGroupStart");
+        LD(GroupEnd, "ncclGroupEnd");
+        LD(GetErrorString, "ncclGetErrorString");
+#undef LD
+        return true;
+    }
+};
+Nccl g_nccl;
+}  // namespace
+
+// ---------------------------------------------------------------------------
+
+struct DLevel {
+    DMat A, P, R;
+    double *w = nullptr;
+    int64_t n = 0, nc = 0;
+    double *rv = nullptr;  // level right-hand side (l >= 1)
+    double *t = nullptr;   // residual / prolongation scratch
+    double *xv = nullptr;  // level solution (l >= 1)
+};
+
+struct VGroup {
+    int sub0 = 0, nsub = 0;
+    int64_t row0 = 0, row1 = 0;
+    std::vector<DLevel> lv;          // smoothing levels
+    int64_t nb = 0;                  // bottom rows (all subdomains of the group)
+    double *rb = nullptr, *xb = nullptr;
+    double *binvT = nullptr;
+    int64_t *binv_off = nullptr;     // per subdomain offset into binvT
+    int64_t *b_off = nullptr;        // nsub + 1 row offsets in rb
+    int max_nb = 0;
+    // host-side statistics
+    std::vector<int64_t> nnzA, nnzP, rows;
+};
+
+struct dfl_ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    std::string err;
+    std::vector<void *> allocs;
+    int64_t bytes = 0;
+    // comm
+    int nranks = 1, rank = 0;
+    NcclComm comm = nullptr;
+    // operator
+    bool have_op = false, finalized = false;
+    int64_t n = 0, n_ghost = 0;
+    int nsub = 0;
+    std::vector<int64_t> sub_off;
+    DMat Aop;
+    std::vector<int64_t> op_nnz_rows;  // host stats
+    int64_t op_nnz = 0;
+    // tiles (per subdomain, rows per tile = op rows per block)
+    Tiles tiles{};
+    int64_t ntiles = 0;
+    int *tile_sub = nullptr;
+    int64_t *sub_tiles = nullptr;       // device nsub + 1
+    std::vector<int64_t> h_sub_tiles;
+    // halo
+    std::vector<int> nbr;
+    std::vector<int64_t> recv_cnt, send_cnt;
+    int *send_idx = nullptr;
+    int64_t nsend = 0;
+    double *sendbuf = nullptr;
+    // hierarchies
+    std::vector<dfl::Hierarchy> pending;
+    std::vector<int> pending_set;
+    std::vector<VGroup> groups;
+    int relax = DFL_RELAX_DAMPED_JACOBI;
+    // deflation
+    bool deflation = false;
+    int k = 0;
+    int64_t K = 0;
+    int first_sub = 0;
+    double *zcols = nullptr;
+    int *az_ptr = nullptr, *az_col = nullptr;
+    double *az_val = nullptr;
+    int64_t az_nnz = 0;
+    double *Einv = nullptr;
+    double *tvec = nullptr, *t2 = nullptr;
+    double *zt_part = nullptr;
+    double *tgather = nullptr;  // nranks * maxsub * k
+    int max_nsub = 0;
+    std::vector<int> rank_nsub;  // subdomains per rank (runtime.rank_subdomains)
+    // work vectors (n, or n + n_ghost for operator inputs)
+    double *b = nullptr, *bp = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr,
+           *w = nullptr, *tmp = nullptr, *xin = nullptr, *yout = nullptr;
+    double *dpart = nullptr;
+    int64_t nblk = 0;
+    double *scal = nullptr;     // [0..7] local reduced scalars
+    double *sgather = nullptr;  // nranks * 8
+    KState *state = nullptr;
+    KState *h_state = nullptr;  // pinned
+    // graph
+    cudaGraphExec_t loop_exec = nullptr;
+    int loop_key = -1;
+    int64_t body_kernels = 0;
+    int64_t launches = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+};
+
+#define CK(call)                                                                             \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess) {                                                             \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                  \
+            return DFL_E_CUDA;                                                               \
+        }                                                                                    \
+    } while (0)
+#define RC(call)                       \
+    do {                               \
+        int r_ = (call);               \
+        if (r_ != DFL_OK) return r_;   \
+    } while (0)
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+template <class T>
+static int dalloc(dfl_ctx *ctx, T **p, int64_t count) {
+    *p = nullptr;
+    if (count <= 0) count = 1;
+    void *q = nullptr;
+    CK(cudaMalloc(&q, sizeof(T) * (size_t)count));
+    ctx->allocs.push_back(q);
+    ctx->bytes += sizeof(T) * count;
+    *p = static_cast<T *>(q);
+    return DFL_OK;
+}
+
+template <class T>
+static int upload(dfl_ctx *ctx, T **p, const T *h, int64_t count) {
+    RC(dalloc(ctx, p, count));
+    if (count > 0) CK(cudaMemcpy(*p, h, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice));
+    return DFL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// matrix upload with format selection
+
+struct HostRows {
+    int64_t nrows, ncols;
+    const int64_t *ptr;
+    const int64_t *col;
+    const double *val;
+};
+
+static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, bool allow_ell = true) {
+    m = DMat{};
+    m.nrows = h.nrows;
+    m.ncols = h.ncols;
+    m.nnz = h.ptr[h.nrows] - h.ptr[0];
+    if (h.ncols >= INT32_MAX || m.nnz >= INT32_MAX) {
+        ctx->err = "matrix too large for int32 device indices";
+        return DFL_E_DIMENSION;
+    }
+    const int64_t nsl = cdiv(h.nrows, 32);
+    std::vector<int64_t> soff(nsl + 1, 0);
+    int64_t maxlen = 0;
+    for (int64_t s = 0; s < nsl; ++s) {
+        int64_t wmax = 0;
+        for (int64_t i = s * 32; i < std::min(h.nrows, s * 32 + 32); ++i) wmax = std::max(wmax, h.ptr[i + 1] - h.ptr[i]);
+        maxlen = std::max(maxlen, wmax);
+        soff[s + 1] = soff[s] + 32 * wmax;
+    }
+    const double mean = h.nrows ? (double)m.nnz / (double)h.nrows : 0.0;
+    const bool ell = allow_ell && maxlen <= 32 && (double)soff[nsl] <= 1.2 * (double)m.nnz + 64.0;
+    if (ell) {
+        m.fmt = FMT_ELL;
+        m.stored = soff[nsl];
+        std::vector<int> col(m.stored);
+        std::vector<double> val(m.stored, 0.0);
+        for (int64_t s = 0; s < nsl; ++s) {
+            const int64_t wdt = (soff[s + 1] - soff[s]) / 32;
+            for (int64_t i = s * 32; i < std::min(h.nrows, s * 32 + 32); ++i) {
+                const int lane = (int)(i - s * 32);
+                const int64_t b = h.ptr[i], e = h.ptr[i + 1];
+                const int pad_col = e > b ? (int)h.col[e - 1] : 0;
+                for (int64_t k = 0; k < wdt; ++k) {
+                    const int64_t dst = soff[s] + k * 32 + lane;
+                    if (b + k < e) {
+                        col[dst] = (int)h.col[b + k];
+                        val[dst] = h.val[b + k];
+                    } else {
+                        col[dst] = pad_col;
+                        val[dst] = 0.0;
+                    }
+                }
+            }
+            for (int64_t i = std::min(h.nrows, s * 32 + 32); i < s * 32 + 32; ++i)  // rows past the end
+                for (int64_t k = 0; k < wdt; ++k) col[soff[s] + k * 32 + (i - s * 32)] = 0;
+        }
+        int64_t *d_soff;
+        int *d_col;
+        double *d_val;
+        RC(upload(ctx, &d_soff, soff.data(), nsl + 1));
+        RC(upload(ctx, &d_col, col.data(), m.stored));
+        RC(upload(ctx, &d_val, val.data(), m.stored));
+        m.slice_off = d_soff;
+        m.col = d_col;
+        m.val = d_val;
+    } else {
+        m.fmt = FMT_CSR;
+        m.stored = m.nnz;
+        int g = 1;
+        if (mean > 8.0) {
+            const int want = (int)std::ceil(mean / 2.0);
+            g = 2;
+            while (g < want && g < 32) g *= 2;
+        }
+        m.group = g;
+        std::vector<int> ptr(h.nrows + 1), col(m.nnz);
+        for (int64_t i = 0; i <= h.nrows; ++i) ptr[i] = (int)(h.ptr[i] - h.ptr[0]);
+        for (int64_t k = 0; k < m.nnz; ++k) col[k] = (int)h.col[h.ptr[0] + k];
+        int *d_ptr, *d_col;
+        double *d_val;
+        RC(upload(ctx, &d_ptr, ptr.data(), h.nrows + 1));
+        RC(upload(ctx, &d_col, col.data(), m.nnz));
+        RC(upload(ctx, &d_val, h.val + h.ptr[0], m.nnz));
+        m.ptr = d_ptr;
+        m.col = d_col;
+        m.val = d_val;
+    }
+    return DFL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// kernel launch helpers
+
+static int rows_per_block(const DMat &A) { return A.fmt == FMT_ELL ? kBlock : kBlock / A.group; }
+
+static int64_t nblocks_for(const DMat &A) { return cdiv(A.nrows, rows_per_block(A)); }
+
+template <int MODE, bool DOT>
+static void launch_csr_mode(const DMat &A, const RowArgs &a, cudaStream_t st) {
+    const dim3 grid((unsigned)nblocks_for(A));
+    switch (A.group) {
+        case 1: k_csr<1, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
+        case 2: k_csr<2, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
+        case 4: k_csr<4, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
+        case 8: k_csr<8, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
+        case 16: k_csr<16, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
+        default: k_csr<32, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
+    }
+}
+
+template <int MODE, bool DOT>
+static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
+    if (A.nrows == 0) return;
+    if (A.fmt == FMT_ELL)
+        k_ell<MODE, DOT><<<(unsigned)nblocks_for(A), kBlock, 0, ctx->st>>>(A, a);
+    else
+        launch_csr_mode<MODE, DOT>(A, a, ctx->st);
+    ctx->launches++;
+}
+
+template <int OPMODE>
+static void launch_op(dfl_ctx *ctx, const OpArgs &a) {
+    const DMat &A = ctx->Aop;
+    const unsigned grid = (unsigned)ctx->ntiles;
+    if (grid == 0) return;
+    if (A.fmt == FMT_ELL) {
+        k_op_ell<OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a);
+    } else {
+        switch (A.group) {
+            case 1: k_op_csr<1, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a); break;
+            case 2: k_op_csr<2, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a); break;
+            case 4: k_op_csr<4, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a); break;
+            case 8: k_op_csr<8, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a); break;
+            case 16: k_op_csr<16, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a); break;
+            default: k_op_csr<32, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a); break;
+        }
+    }
+    ctx->launches++;
+}
+
+// ---------------------------------------------------------------------------
+// communication (no-ops on a single rank)
+
+static int nccl_check(dfl_ctx *ctx, int rc, const char *what) {
+    if (rc != 0) {
+        ctx->err = std::string(what) + ": " + (g_nccl.GetErrorString ? g_nccl.GetErrorString(rc) : "nccl error");
+        return DFL_E_COMM;
+    }
+    return DFL_OK;
+}
+
+// fill the ghost part v[n .. n+n_ghost) from the neighbours (runtime.py:246-271)
+static int halo(dfl_ctx *ctx, double *v) {
+    if (ctx->nranks == 1 || ctx->nbr.empty()) return DFL_OK;
+    if (ctx->nsend > 0) {
+        k_gather<<<(unsigned)cdiv(ctx->nsend, kBlock), kBlock, 0, ctx->st>>>(v, ctx->send_idx, ctx->nsend,
+                                                                              ctx->sendbuf);
+        ctx->launches++;
+    }
+    RC(nccl_check(ctx, g_nccl.GroupStart(), "ncclGroupStart"));
+    int64_t so = 0, ro = 0;
+    for (size_t q = 0; q < ctx->nbr.size(); ++q) {
+        if (ctx->send_cnt[q] > 0)
+            RC(nccl_check(ctx, g_nccl.Send(ctx->sendbuf + so, ctx->send_cnt[q], ncclDouble_, ctx->nbr[q], ctx->comm, ctx->st),
+                          "ncclSend"));
+        if (ctx->recv_cnt[q] > 0)
+            RC(nccl_check(ctx, g_nccl.Recv(v + ctx->n + ro, ctx->recv_cnt[q], ncclDouble_, ctx->nbr[q], ctx->comm, ctx->st),
+                          "ncclRecv"));
+        so += ctx->send_cnt[q];
+        ro += ctx->recv_cnt[q];
+    }
+    RC(nccl_check(ctx, g_nccl.GroupEnd(), "ncclGroupEnd"));
+    return DFL_OK;
+}
+
+// Z' v partials -> t (global numbering) -> t2 = E^-1 t on every rank
+static int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh) {
+    if (ctx->nranks == 1) {
+        k_zt_finish<<<1, 256, 0, ctx->st>>>(ctx->zt_part, ctx->sub_tiles, ctx->nsub, ctx->k, ctx->tvec, 0, ctx->Einv,
+                                            ctx->K, ctx->t2, st, need_refresh);
+        ctx->launches++;
+        return DFL_OK;
+    }
+    // local entries into a padded slot, allgather, unpack, solve
+    const int64_t slot = (int64_t)ctx->max_nsub * ctx->k;
+    double *mine = ctx->tgather + (int64_t)ctx->rank * slot;
+    k_zt_finish<<<1, 256, 0, ctx->st>>>(ctx->zt_part, ctx->sub_tiles, ctx->nsub, ctx->k, mine, 0, nullptr, ctx->K,
+                                        nullptr, st, need_refresh);
+    RC(nccl_check(ctx, g_nccl.AllGather(mine, ctx->tgather, slot, ncclDouble_, ctx->comm, ctx->st), "ncclAllGather"));
+    // unpack rank slots into t: rank q owns a contiguous subdomain range
+    int64_t pos = 0;
+    for (int q = 0; q < ctx->nranks; ++q) {
+        const int64_t cnt = (int64_t)ctx->rank_nsub[q] * ctx->k;
+        if (cnt > 0) CK(cudaMemcpyAsync(ctx->tvec + pos, ctx->tgather + q * slot, cnt * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, ctx->st));
+        pos += cnt;
+    }
+    k_esolve<<<1, 256, 0, ctx->st>>>(ctx->Einv, ctx->K, ctx->tvec, ctx->t2, st, need_refresh);
+    ctx->launches += 2;
+    return DFL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Krylov scalar steps (single block).  With several ranks the per-rank sums
+// arrive allgathered in `gath` (stride 8) and are added in rank order, which
+// mirrors the ascending-order allreduce of runtime.py:214-219.
+
+__device__ __forceinline__ double scalar_in(const double *part, int64_t nparts, const double *gath, int nranks,
+                                            int slot) {
+    if (gath == nullptr) return reduce_parts(part, nparts);
+    double s = 0.0;
+    for (int q = 0; q < nranks; ++q) s += gath[q * 8 + slot];
+    return s;
+}
+
+// bnorm = ||b|| (deflation.py:266), atol = tol * bnorm
+__global__ void k_cg_start(KState *st, const double *part, int64_t nparts, const double *gath, int nranks,
+                           double tol, int maxiter, int refresh) {
+    const double bb = scalar_in(part, nparts, gath, nranks, 0);
+    if (threadIdx.x != 0) return;
+    KState s{};
+    s.bnorm = sqrt(fmax(bb, 0.0));
+    s.target = tol * s.bnorm;
+    s.maxiter = maxiter;
+    s.refresh_every = refresh;
+    if (s.bnorm == 0.0) {
+        s.done = 1;
+        s.converged = 1;
+    }
+    *st = s;
+}
+
+// ||b'|| of the projected rhs: zero -> zero solution; r = b' meets the target
+// -> converged at 0 iterations (krylov.py:101-113)
+__global__ void k_cg_init_r(KState *st, const double *part, int64_t nparts, const double *gath, int nranks) {
+    if (st->done) return;
+    const double bb = scalar_in(part, nparts, gath, nranks, 0);
+    if (threadIdx.x != 0) return;
+    const double bn = sqrt(fmax(bb, 0.0));
+    st->resnorm = bn;
+    if (bn == 0.0 || bn <= st->target) {
+        st->done = 1;
+        st->converged = 1;
+    } else if (st->maxiter <= 0) {
+        st->done = 1;
+    }
+}
+
+__global__ void k_cg_init_rz(KState *st, const double *part, int64_t nparts, const double *gath, int nranks) {
+    if (st->done) return;
+    const double rz = scalar_in(part, nparts, gath, nranks, 0);
+    if (threadIdx.x == 0) st->rz = rz;
+}
+
+// iters += 1; pAp (krylov.py:119-126)
+__global__ void k_cg_pq(KState *st, const double *part, int64_t nparts, const double *gath, int nranks) {
+    if (st->done) return;
+    const double pq = scalar_in(part, nparts, gath, nranks, 0);
+    if (threadIdx.x != 0) return;
+    st->iters += 1;
+    st->pq = pq;
+    if (pq <= 0.0 || !isfinite(pq)) {
+        st->breakdown = DFL_BRK_CURVATURE;
+        st->done = 1;
+        return;
+    }
+    st->alpha = st->rz / pq;
+    st->refresh_now = (st->iters % st->refresh_every) == 0;
+}
+
+// resnorm test (krylov.py:132-136)
+__global__ void k_cg_rr(KState *st, const double *part, int64_t nparts, const double *gath, int nranks) {
+    if (st->done) return;
+    const double rr = scalar_in(part, nparts, gath, nranks, 0);
+    if (threadIdx.x != 0) return;
+    st->rr = rr;
+    st->resnorm = sqrt(fmax(rr, 0.0));
+    if (st->resnorm <= st->target) {
+        st->converged = 1;
+        st->done = 1;
+    }
+}
+
+// beta (krylov.py:138-143)
+__global__ void k_cg_rz(KState *st, const double *part, int64_t nparts, const double *gath, int nranks) {
+    if (st->done) return;
+    const double rz = scalar_in(part, nparts, gath, nranks, 0);
+    if (threadIdx.x != 0) return;
+    if (rz == 0.0 || !isfinite(rz)) {
+        st->breakdown = DFL_BRK_RZ;
+        st->done = 1;
+        return;
+    }
+    st->beta = rz / st->rz;
+    st->rz = rz;
+}
+
+__global__ void k_cg_end(KState *st, cudaGraphConditionalHandle h, int use_cond) {
+    if (threadIdx.x != 0) return;
+    if (!st->done && st->iters >= st->maxiter) st->done = 1;
+    if (use_cond) cudaGraphSetConditional(h, st->done ? 0u : 1u);
+}
+
+// ---------------------------------------------------------------------------
+// reductions across ranks: returns the pointer the scalar kernel reads
+static int rank_scalar(dfl_ctx *ctx, const double *part, int64_t nparts, int slot, const double **gath) {
+    *gath = nullptr;
+    if (ctx->nranks == 1) return DFL_OK;
+    k_reduce<<<1, 256, 0, ctx->st>>>(part, nparts, ctx->scal + slot);
+    ctx->launches++;
+    RC(nccl_check(ctx, g_nccl.AllGather(ctx->scal, ctx->sgather, 8, ncclDouble_, ctx->comm, ctx->st), "ncclAllGather"));
+    *gath = ctx->sgather;
+    return DFL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// V-cycle over all groups: z = M r  (deflation.py:239-250 -> amg.py:201-212).
+// With dot_part != nullptr the last kernel of every group also emits the
+// per-block partials of r.z; *nparts receives their count.
+static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *dot_part, int64_t *nparts) {
+    int64_t poff = 0;
+    for (VGroup &g : ctx->groups) {
+        const double *rin = r + g.row0;
+        double *zout = z + g.row0;
+        const int L = (int)g.lv.size();
+        for (int l = 0; l < L; ++l) {
+            DLevel &v = g.lv[l];
+            const double *in = l == 0 ? rin : v.rv;
+            double *next = (l + 1 < L) ? g.lv[l + 1].rv : g.rb;
+            RowArgs a{nullptr, v.w, in, nullptr, v.t, nullptr, st};
+            launch_rows<MODE_RESID, false>(ctx, v.A, a);
+            RowArgs b{v.t, nullptr, nullptr, nullptr, next, nullptr, st};
+            launch_rows<MODE_PLAIN, false>(ctx, v.R, b);
+        }
+        {
+            const double *rb = L == 0 ? rin : g.rb;
+            double *xb = L == 0 ? zout : g.xb;
+            const int threads = std::min(512, std::max(32, (g.max_nb + 31) / 32 * 32));
+            k_bottom<<<g.nsub, threads, sizeof(double) * g.max_nb, ctx->st>>>(g.binvT, g.binv_off, g.b_off, rb, xb, st);
+            ctx->launches++;
+        }
+        for (int l = L - 1; l >= 0; --l) {
+            DLevel &v = g.lv[l];
+            const double *in = l == 0 ? rin : v.rv;
+            const double *e = (l + 1 < L) ? g.lv[l + 1].xv : g.xb;
+            double *out = l == 0 ? zout : v.xv;
+            RowArgs a{e, v.w, in, nullptr, v.t, nullptr, st};
+            launch_rows<MODE_PROLONG, false>(ctx, v.P, a);
+            if (l == 0 && dot_part) {
+                RowArgs b{v.t, v.w, in, v.t, out, dot_part + poff, st};
+                launch_rows<MODE_POST, true>(ctx, v.A, b);
+                poff += nblocks_for(v.A);
+            } else {
+                RowArgs b{v.t, v.w, in, v.t, out, nullptr, st};
+                launch_rows<MODE_POST, false>(ctx, v.A, b);
+            }
+        }
+        if (L == 0 && dot_part) {
+            // bottom-only group: explicit partial dot of this group's rows
+            const int64_t rows = g.row1 - g.row0;
+            const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(rows, kBlock), 64));
+            k_dot<<<nb, kBlock, 0, ctx->st>>>(rin, zout, rows, dot_part + poff, st);
+            ctx->launches++;
+            poff += nb;
+        }
+    }
+    if (nparts) *nparts = poff;
+    return DFL_OK;
+}
+
+// y = A x (opmode 0) or y = b - A x (opmode 1); with zt the Z'y tile partials
+static int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double *b, bool zt,
+                        const KState *st, int need_refresh) {
+    RC(halo(ctx, xin));
+    OpArgs a{xin, b, y, ctx->zcols, ctx->n, zt ? ctx->k : 0, ctx->zt_part, st, need_refresh};
+    if (opmode == 0)
+        launch_op<0>(ctx, a);
+    else
+        launch_op<1>(ctx, a);
+    return DFL_OK;
+}
+
+static ProjArgs proj_args(dfl_ctx *ctx, const double *in, double *out, const KState *st) {
+    ProjArgs a{};
+    if (ctx->deflation) {
+        a.az_ptr = ctx->az_ptr;
+        a.az_col = ctx->az_col;
+        a.az_val = ctx->az_val;
+    }
+    a.t2 = ctx->t2;
+    a.K = ctx->deflation ? ctx->K : 0;
+    a.n = ctx->n;
+    a.in = in;
+    a.out = out;
+    a.st = st;
+    return a;
+}
+
+template <int MODE>
+static void launch_project(dfl_ctx *ctx, const ProjArgs &a) {
+    k_project<MODE><<<(unsigned)ctx->nblk, kBlock, sizeof(double) * std::max<int64_t>(1, a.K), ctx->st>>>(a);
+    ctx->launches++;
+}
+
+// out = project(v) = v - AZ E^-1 Z' v   (deflation.py:230-233)
+static int project_dev(dfl_ctx *ctx, const double *v, double *out, const KState *st, int dotmode) {
+    k_zt_vec<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, v, ctx->zcols, ctx->n, ctx->k, ctx->zt_part);
+    ctx->launches++;
+    RC(zt_to_t2(ctx, nullptr, 0));
+    ProjArgs a = proj_args(ctx, v, out, st);
+    a.dotmode = dotmode;
+    a.dot_part = ctx->dpart;
+    launch_project<0>(ctx, a);
+    return DFL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// one CG iteration (krylov.py:119-143) on the projected operator
+static int cg_body(dfl_ctx *ctx, bool deflated, cudaGraphConditionalHandle h, int use_cond) {
+    KState *st = ctx->state;
+    const double *gath;
+    // w = A p, Z'w ; t2 ; q = w - AZ t2 ; p.q
+    RC(op_apply_dev(ctx, ctx->p, ctx->w, 0, nullptr, deflated, st, 0));
+    if (deflated) RC(zt_to_t2(ctx, st, 0));
+    {
+        ProjArgs a = proj_args(ctx, ctx->w, ctx->w, st);
+        if (!deflated) a.az_ptr = nullptr, a.K = 0;
+        a.dotmode = 1;
+        a.dotv = ctx->p;
+        a.dot_part = ctx->dpart;
+        launch_project<0>(ctx, a);
+    }
+    RC(rank_scalar(ctx, ctx->dpart, ctx->nblk, 0, &gath));
+    k_cg_pq<<<1, 256, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks);
+    ctx->launches++;
+    // x += alpha p ; r -= alpha q (regular iterations)
+    k_cg_update<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->x, ctx->r, ctx->p, ctx->w, ctx->n, ctx->dpart, st);
+    ctx->launches++;
+    // refresh iterations: r = b' - project(A x)   (krylov.py:128-129)
+    RC(op_apply_dev(ctx, ctx->x, ctx->tmp, 0, nullptr, deflated, st, 1));
+    if (deflated) RC(zt_to_t2(ctx, st, 1));
+    {
+        ProjArgs a = proj_args(ctx, ctx->tmp, ctx->r, st);
+        if (!deflated) a.az_ptr = nullptr, a.K = 0;
+        a.base = ctx->bp;
+        a.dotmode = 2;
+        a.dot_part = ctx->dpart;
+        a.need_refresh = 1;
+        launch_project<1>(ctx, a);
+    }
+    RC(rank_scalar(ctx, ctx->dpart, ctx->nblk, 0, &gath));
+    k_cg_rr<<<1, 256, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks);
+    ctx->launches++;
+    // z = M r, r.z
+    int64_t np = 0;
+    RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
+    RC(rank_scalar(ctx, ctx->dpart, np, 0, &gath));
+    k_cg_rz<<<1, 256, 0, ctx->st>>>(st, ctx->dpart, np, gath, ctx->nranks);
+    ctx->launches++;
+    k_cg_p<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->p, ctx->z, ctx->n, st);
+    ctx->launches++;
+    k_cg_end<<<1, 32, 0, ctx->st>>>(st, h, use_cond);
+    ctx->launches++;
+    return DFL_OK;
+}
+
+static int build_loop_graph(dfl_ctx *ctx, bool deflated) {
+    const int key = deflated ? 1 : 0;
+    if (ctx->loop_exec && ctx->loop_key == key) return DFL_OK;
+    if (ctx->loop_exec) {
+        cudaGraphExecDestroy(ctx->loop_exec);
+        ctx->loop_exec = nullptr;
+    }
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    CK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CK(cudaStreamBeginCaptureToGraph(ctx->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    const int64_t before = ctx->launches;
+    int rc = cg_body(ctx, deflated, h, 1);
+    cudaGraph_t captured = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(ctx->st, &captured);
+    if (rc != DFL_OK) return rc;
+    CK(ce);
+    ctx->body_kernels = ctx->launches - before;
+    ctx->launches = before;
+    CK(cudaGraphInstantiate(&ctx->loop_exec, g, 0));
+    cudaGraphDestroy(g);
+    ctx->loop_key = key;
+    return DFL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// the whole solve on the device: b, x in ctx->b / ctx->xin
+static int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
+    KState *st = ctx->state;
+    const bool defl = p->deflated != 0;
+    const double *gath;
+    // x = 0 (y of the deflated system)
+    k_fill<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->x, 0.0, ctx->n);
+    // ||b||
+    k_dot<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->b, ctx->b, ctx->n, ctx->dpart, nullptr);
+    ctx->launches += 2;
+    RC(rank_scalar(ctx, ctx->dpart, ctx->nblk, 0, &gath));
+    k_cg_start<<<1, 256, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks, p->tol, p->maxiter,
+                                      std::max(1, p->refresh_every));
+    ctx->launches++;
+    // b' = project(b) and ||b'||^2
+    if (defl) {
+        RC(project_dev(ctx, ctx->b, ctx->bp, nullptr, 2));
+    } else {
+        ProjArgs a = proj_args(ctx, ctx->b, ctx->bp, nullptr);
+        a.az_ptr = nullptr;
+        a.K = 0;
+        a.dotmode = 2;
+        a.dot_part = ctx->dpart;
+        launch_project<0>(ctx, a);
+    }
+    RC(rank_scalar(ctx, ctx->dpart, ctx->nblk, 0, &gath));
+    k_cg_init_r<<<1, 256, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks);
+    k_copy<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->r, ctx->bp, ctx->n);
+    ctx->launches += 2;
+    int64_t np = 0;
+    RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
+    RC(rank_scalar(ctx, ctx->dpart, np, 0, &gath));
+    k_cg_init_rz<<<1, 256, 0, ctx->st>>>(st, ctx->dpart, np, gath, ctx->nranks);
+    k_copy<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->p, ctx->z, ctx->n);
+    ctx->launches += 2;
+    // the loop
+    if (use_graph) {
+        RC(build_loop_graph(ctx, defl));
+        CK(cudaGraphLaunch(ctx->loop_exec, ctx->st));
+    } else {
+        for (;;) {
+            RC(cg_body(ctx, defl, 0, 0));
+            CK(cudaMemcpyAsync(ctx->h_state, st, sizeof(KState), cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaStreamSynchronize(ctx->st));
+            if (ctx->h_state->done) break;
+        }
+    }
+    // x = y + Z E^-1 Z'(b - A y)   (deflation.py:285)
+    if (defl) {
+        RC(op_apply_dev(ctx, ctx->x, ctx->tmp, 1, ctx->b, true, nullptr, 0));
+        RC(zt_to_t2(ctx, nullptr, 0));
+        k_lift<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, ctx->tile_sub, ctx->x, ctx->zcols, ctx->n,
+                                                              ctx->k, ctx->t2, (int64_t)ctx->first_sub * ctx->k,
+                                                              ctx->xin, 1);
+    } else {
+        k_copy<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->xin, ctx->x, ctx->n);
+    }
+    ctx->launches++;
+    return DFL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// upload helpers for finalize
+
+struct OwnedRows {
+    int64_t nrows = 0, ncols = 0;
+    std::vector<int64_t> ptr{0}, col;
+    std::vector<double> val;
+    HostRows view() const { return HostRows{nrows, ncols, ptr.data(), col.data(), val.data()}; }
+};
+
+// block-diagonal concatenation: part j contributes rows at row offset, columns
+// shifted by col offset
+static OwnedRows merge_blocks(const std::vector<const dfl::Csr *> &parts, const std::vector<int64_t> &coff) {
+    OwnedRows m;
+    int64_t nnz = 0;
+    for (auto *p : parts) nnz += p->nnz(), m.nrows += p->nrows;
+    m.ncols = coff.back();
+    m.ptr.reserve(m.nrows + 1);
+    m.col.reserve(nnz);
+    m.val.reserve(nnz);
+    for (size_t j = 0; j < parts.size(); ++j) {
+        const dfl::Csr &p = *parts[j];
+        for (int64_t i = 0; i < p.nrows; ++i) {
+            for (int64_t k = p.ptr[i]; k < p.ptr[i + 1]; ++k) {
+                m.col.push_back(p.col[k] + coff[j]);
+                m.val.push_back(p.val[k]);
+            }
+            m.ptr.push_back((int64_t)m.col.size());
+        }
+    }
+    return m;
+}
+
+static int build_groups(dfl_ctx *ctx) {
+    ctx->groups.clear();
+    int s = 0;
+    while (s < ctx->nsub) {
+        const size_t depth = ctx->pending[s].levels.size();
+        int e = s + 1;
+        while (e < ctx->nsub && ctx->pending[e].levels.size() == depth) ++e;
+        VGroup g;
+        g.sub0 = s;
+        g.nsub = e - s;
+        g.row0 = ctx->sub_off[s];
+        g.row1 = ctx->sub_off[e];
+        const int L = (int)depth - 1;
+        for (int j = s; j < e; ++j)
+            if (ctx->pending[j].levels[0].A.nrows != ctx->sub_off[j + 1] - ctx->sub_off[j]) {
+                ctx->err = "hierarchy of subdomain " + std::to_string(j) + " does not match its row range";
+                return DFL_E_DIMENSION;
+            }
+        for (int l = 0; l < L; ++l) {
+            DLevel v;
+            std::vector<const dfl::Csr *> As, Ps, Rs;
+            std::vector<int64_t> fo{0}, co{0};
+            std::vector<double> w;
+            for (int j = s; j < e; ++j) {
+                const dfl::Level &lv = ctx->pending[j].levels[l];
+                As.push_back(&lv.A);
+                Ps.push_back(&lv.P);
+                Rs.push_back(&lv.R);
+                fo.push_back(fo.back() + lv.A.nrows);
+                co.push_back(co.back() + lv.P.ncols);
+                w.insert(w.end(), lv.w.begin(), lv.w.end());
+            }
+            OwnedRows A = merge_blocks(As, fo), P = merge_blocks(Ps, co), R = merge_blocks(Rs, fo);
+            RC(upload_matrix(ctx, A.view(), v.A));
+            RC(upload_matrix(ctx, P.view(), v.P));
+            RC(upload_matrix(ctx, R.view(), v.R));
+            RC(upload(ctx, &v.w, w.data(), (int64_t)w.size()));
+            v.n = fo.back();
+            v.nc = co.back();
+            RC(dalloc(ctx, &v.t, v.n));
+            if (l > 0) {
+                RC(dalloc(ctx, &v.rv, v.n));
+                RC(dalloc(ctx, &v.xv, v.n));
+            }
+            g.nnzA.push_back(A.ptr.back());
+            g.nnzP.push_back(P.ptr.back());
+            g.rows.push_back(v.n);
+            g.lv.push_back(v);
+        }
+        // bottom level
+        std::vector<int64_t> boff{0}, ioff{0};
+        std::vector<double> invT;
+        for (int j = s; j < e; ++j) {
+            const dfl::Level &bl = ctx->pending[j].levels.back();
+            const int64_t nb = bl.A.nrows;
+            boff.push_back(boff.back() + nb);
+            ioff.push_back(ioff.back() + nb * nb);
+            g.max_nb = std::max<int>(g.max_nb, (int)nb);
+            for (int64_t c = 0; c < nb; ++c)
+                for (int64_t i = 0; i < nb; ++i) invT.push_back(bl.bottom_inv[i * nb + c]);
+        }
+        g.nb = boff.back();
+        g.rows.push_back(g.nb);
+        RC(upload(ctx, &g.binvT, invT.data(), (int64_t)invT.size()));
+        RC(upload(ctx, &g.binv_off, ioff.data(), (int64_t)ioff.size()));
+        RC(upload(ctx, &g.b_off, boff.data(), (int64_t)boff.size()));
+        if (L > 0) {
+            RC(dalloc(ctx, &g.rb, g.nb));
+            RC(dalloc(ctx, &g.xb, g.nb));
+        }
+        if (g.max_nb > 6000) {
+            ctx->err = "bottom level too large for shared-memory staging";
+            return DFL_E_DIMENSION;
+        }
+        ctx->groups.push_back(std::move(g));
+        s = e;
+    }
+    return DFL_OK;
+}
+
+static int build_tiles(dfl_ctx *ctx) {
+    const int rpt = rows_per_block(ctx->Aop);
+    std::vector<int64_t> r0, r1, subt{0};
+    std::vector<int> ts;
+    for (int s = 0; s < ctx->nsub; ++s) {
+        for (int64_t i = ctx->sub_off[s]; i < ctx->sub_off[s + 1]; i += rpt) {
+            r0.push_back(i);
+            r1.push_back(std::min(i + rpt, ctx->sub_off[s + 1]));
+            ts.push_back(s);
+        }
+        subt.push_back((int64_t)r0.size());
+    }
+    ctx->ntiles = (int64_t)r0.size();
+    int64_t *d0, *d1;
+    RC(upload(ctx, &d0, r0.data(), ctx->ntiles));
+    RC(upload(ctx, &d1, r1.data(), ctx->ntiles));
+    RC(upload(ctx, &ctx->tile_sub, ts.data(), ctx->ntiles));
+    RC(upload(ctx, &ctx->sub_tiles, subt.data(), (int64_t)subt.size()));
+    ctx->h_sub_tiles = subt;
+    ctx->tiles = Tiles{d0, d1, ctx->ntiles};
+    return DFL_OK;
+}
+
+static int stage_in(dfl_ctx *ctx, double *dst, const double *src, int ptr_kind) {
+    CK(cudaMemcpyAsync(dst, src, sizeof(double) * ctx->n,
+                       ptr_kind == DFL_PTR_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, ctx->st));
+    return DFL_OK;
+}
+
+static int stage_out(dfl_ctx *ctx, double *dst, const double *src, int ptr_kind) {
+    CK(cudaMemcpyAsync(dst, src, sizeof(double) * ctx->n,
+                       ptr_kind == DFL_PTR_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    return DFL_OK;
+}
+
+static int ready(dfl_ctx *ctx) {
+    if (!ctx) return DFL_E_STATE;
+    if (!ctx->finalized) {
+        ctx->err = "context not finalized";
+        return DFL_E_STATE;
+    }
+    CK(cudaSetDevice(ctx->device));
+    return DFL_OK;
+}
+
+static int rank_dot(dfl_ctx *ctx, const double *a, const double *b, double *out) {
+    const unsigned nb = (unsigned)std::min<int64_t>(std::max<int64_t>(1, ctx->nblk), 4 * 148);
+    k_dot<<<nb, kBlock, 0, ctx->st>>>(a, b, ctx->n, ctx->dpart, nullptr);
+    k_reduce<<<1, 256, 0, ctx->st>>>(ctx->dpart, nb, ctx->scal);
+    ctx->launches += 2;
+    if (ctx->nranks > 1) {
+        RC(nccl_check(ctx, g_nccl.AllGather(ctx->scal, ctx->sgather, 8, ncclDouble_, ctx->comm, ctx->st), "ncclAllGather"));
+        k_rank_sum<<<1, 32, 0, ctx->st>>>(ctx->sgather, ctx->nranks, 8, 1, ctx->scal + 1);
+        ctx->launches++;
+        CK(cudaMemcpyAsync(out, ctx->scal + 1, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    } else {
+        CK(cudaMemcpyAsync(out, ctx->scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
+    }
+    CK(cudaStreamSynchronize(ctx->st));
+    return DFL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+const char *dfl_breakdown_string(int code) {
+    switch (code) {
+        case DFL_BRK_NONE: return "";
+        case DFL_BRK_CURVATURE: return "non-positive curvature p'Ap";
+        case DFL_BRK_RZ: return "preconditioned residual product degenerated";
+        case DFL_BRK_RHO: return "rho degenerated in the BiCG stage";
+        case DFL_BRK_SHADOW: return "shadow product degenerated in the BiCG stage";
+        case DFL_BRK_MR: return "minimal-residual basis degenerated";
+        case DFL_BRK_OMEGA: return "stabilization weight vanished";
+        default: return "unknown breakdown";
+    }
+}
+
+int dfl_ctx_create(int device, dfl_ctx **out) {
+    if (!out) return DFL_E_STATE;
+    *out = nullptr;
+    auto *ctx = new dfl_ctx;
+    ctx->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
+    if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_state, sizeof(KState));
+    if (e != cudaSuccess) {
+        dfl::set_setup_error(std::string("CUDA context creation failed: ") + cudaGetErrorString(e));
+        delete ctx;
+        return DFL_E_CUDA;
+    }
+    *out = ctx;
+    return DFL_OK;
+}
+
+void dfl_ctx_destroy(dfl_ctx *ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->st) cudaStreamSynchronize(ctx->st);
+    if (ctx->loop_exec) cudaGraphExecDestroy(ctx->loop_exec);
+    for (void *p : ctx->allocs) cudaFree(p);
+    if (ctx->h_state) cudaFreeHost(ctx->h_state);
+    if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+    if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+    if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
+    if (ctx->st) cudaStreamDestroy(ctx->st);
+    delete ctx;
+}
+
+const char *dfl_last_error(const dfl_ctx *ctx) { return ctx ? ctx->err.c_str() : dfl::setup_error(); }
+
+int64_t dfl_ctx_device_bytes(const dfl_ctx *ctx) { return ctx ? ctx->bytes : 0; }
+
+int dfl_nccl_unique_id(void *id) {
+    std::string err;
+    if (!g_nccl.load(err)) {
+        dfl::set_setup_error(err);
+        return DFL_E_COMM;
+    }
+    int rc = g_nccl.GetUniqueId(static_cast<NcclId *>(id));
+    if (rc != 0) {
+        dfl::set_setup_error(std::string("ncclGetUniqueId: ") + g_nccl.GetErrorString(rc));
+        return DFL_E_COMM;
+    }
+    return DFL_OK;
+}
+
+int dfl_ctx_set_comm(dfl_ctx *ctx, int nranks, int rank, const void *id) {
+    if (!ctx) return DFL_E_STATE;
+    if (nranks < 1 || rank < 0 || rank >= nranks) {
+        ctx->err = "bad rank / world size";
+        return DFL_E_PARTITION;
+    }
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    if (nranks == 1) return DFL_OK;
+    if (!g_nccl.load(ctx->err)) return DFL_E_COMM;
+    CK(cudaSetDevice(ctx->device));
+    NcclId nid;
+    std::memcpy(&nid, id, sizeof nid);
+    return nccl_check(ctx, g_nccl.CommInitRank(&ctx->comm, nranks, nid, rank), "ncclCommInitRank");
+}
+
+int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int64_t *sub_offsets, int32_t nnbr,
+                         const int32_t *nbr_rank, const int64_t *recv_counts, const int64_t *send_counts,
+                         const int64_t *send_idx) {
+    if (!ctx || !A || nsub < 1 || !sub_offsets) return DFL_E_STATE;
+    CK(cudaSetDevice(ctx->device));
+    if (sub_offsets[0] != 0 || sub_offsets[nsub] != A->nrows) {
+        ctx->err = "subdomain offsets do not span the operator rows";
+        return DFL_E_PARTITION;
+    }
+    for (int s = 0; s < nsub; ++s)
+        if (sub_offsets[s + 1] <= sub_offsets[s]) {
+            ctx->err = "empty subdomain";
+            return DFL_E_PARTITION;
+        }
+    ctx->n = A->nrows;
+    ctx->n_ghost = A->ncols - A->nrows;
+    if (ctx->n_ghost < 0) {
+        ctx->err = "operator has fewer columns than rows";
+        return DFL_E_DIMENSION;
+    }
+    ctx->nsub = nsub;
+    ctx->sub_off.assign(sub_offsets, sub_offsets + nsub + 1);
+    HostRows h{A->nrows, A->ncols, A->row_ptr, A->col_idx, A->values};
+    RC(upload_matrix(ctx, h, ctx->Aop));
+    ctx->op_nnz = ctx->Aop.nnz;
+    int64_t nrecv = 0;
+    ctx->nbr.clear();
+    ctx->recv_cnt.clear();
+    ctx->send_cnt.clear();
+    ctx->nsend = 0;
+    for (int q = 0; q < nnbr; ++q) {
+        ctx->nbr.push_back(nbr_rank[q]);
+        ctx->recv_cnt.push_back(recv_counts[q]);
+        ctx->send_cnt.push_back(send_counts[q]);
+        nrecv += recv_counts[q];
+        ctx->nsend += send_counts[q];
+    }
+    if (nrecv != ctx->n_ghost) {
+        ctx->err = "halo plan receives " + std::to_string(nrecv) + " values for " + std::to_string(ctx->n_ghost) +
+                   " ghost columns";
+        return DFL_E_COMM;
+    }
+    if (ctx->nsend > 0) {
+        std::vector<int> si(send_idx, send_idx + ctx->nsend);
+        for (int v : si)
+            if (v < 0 || v >= ctx->n) {
+                ctx->err = "halo send index out of range";
+                return DFL_E_COMM;
+            }
+        RC(upload(ctx, &ctx->send_idx, si.data(), ctx->nsend));
+        RC(dalloc(ctx, &ctx->sendbuf, ctx->nsend));
+    }
+    ctx->pending.assign(nsub, dfl::Hierarchy{});
+    ctx->pending_set.assign(nsub, 0);
+    ctx->have_op = true;
+    ctx->finalized = false;
+    return DFL_OK;
+}
+
+int dfl_ctx_add_hierarchy(dfl_ctx *ctx, int32_t sub, const dfl_hier *h) {
+    if (!ctx || !h) return DFL_E_STATE;
+    if (!ctx->have_op || sub < 0 || sub >= ctx->nsub) {
+        ctx->err = "hierarchy for an unknown subdomain (set the operator first)";
+        return DFL_E_STATE;
+    }
+    const dfl::Hierarchy &src = h->h;
+    if (sub > 0 && src.relax != ctx->relax) {
+        ctx->err = "all subdomains must use the same relaxation";
+        return DFL_E_CONFIG;
+    }
+    ctx->relax = src.relax;
+    ctx->pending[sub] = src;
+    ctx->pending_set[sub] = 1;
+    return DFL_OK;
+}
+
+int dfl_ctx_set_deflation(dfl_ctx *ctx, int32_t k, const double *zcols, const dfl_csr *AZ, int64_t K,
+                          const double *Einv, int32_t first_sub) {
+    if (!ctx || !AZ || !Einv) return DFL_E_STATE;
+    if (!ctx->have_op) {
+        ctx->err = "set the operator before the deflation basis";
+        return DFL_E_STATE;
+    }
+    if (k < 1 || k > kKmax || K % k != 0 || AZ->nrows != ctx->n || AZ->ncols != K) {
+        ctx->err = "inconsistent deflation dimensions";
+        return DFL_E_DIMENSION;
+    }
+    CK(cudaSetDevice(ctx->device));
+    ctx->k = k;
+    ctx->K = K;
+    ctx->first_sub = first_sub;
+    const int m = (int)(K / k);
+    ctx->rank_nsub.assign(ctx->nranks, 0);
+    for (int q = 0; q < ctx->nranks; ++q) ctx->rank_nsub[q] = m / ctx->nranks + (q < m % ctx->nranks ? 1 : 0);
+    ctx->max_nsub = *std::max_element(ctx->rank_nsub.begin(), ctx->rank_nsub.end());
+    if (ctx->rank_nsub[ctx->rank] != ctx->nsub) {
+        ctx->err = "rank owns " + std::to_string(ctx->nsub) + " subdomains, placement expects " +
+                   std::to_string(ctx->rank_nsub[ctx->rank]);
+        return DFL_E_PARTITION;
+    }
+    // Z columns 1..k-1, column-major for coalesced loads
+    std::vector<double> zc((size_t)std::max(1, k - 1) * ctx->n, 0.0);
+    for (int c = 1; c < k; ++c)
+        for (int64_t i = 0; i < ctx->n; ++i) zc[(size_t)(c - 1) * ctx->n + i] = zcols[i * (k - 1) + (c - 1)];
+    RC(upload(ctx, &ctx->zcols, zc.data(), (int64_t)zc.size()));
+    std::vector<int> ptr(ctx->n + 1), col(AZ->row_ptr[ctx->n]);
+    for (int64_t i = 0; i <= ctx->n; ++i) ptr[i] = (int)AZ->row_ptr[i];
+    for (size_t j = 0; j < col.size(); ++j) col[j] = (int)AZ->col_idx[j];
+    ctx->az_nnz = (int64_t)col.size();
+    RC(upload(ctx, &ctx->az_ptr, ptr.data(), (int64_t)ptr.size()));
+    RC(upload(ctx, &ctx->az_col, col.data(), ctx->az_nnz));
+    RC(upload(ctx, &ctx->az_val, AZ->values, ctx->az_nnz));
+    RC(upload(ctx, &ctx->Einv, Einv, K * K));
+    RC(dalloc(ctx, &ctx->tvec, K));
+    RC(dalloc(ctx, &ctx->t2, K));
+    RC(dalloc(ctx, &ctx->tgather, (int64_t)ctx->nranks * ctx->max_nsub * k));
+    ctx->deflation = true;
+    return DFL_OK;
+}
+
+int dfl_ctx_finalize(dfl_ctx *ctx) {
+    if (!ctx) return DFL_E_STATE;
+    if (!ctx->have_op) {
+        ctx->err = "no operator uploaded";
+        return DFL_E_STATE;
+    }
+    for (int s = 0; s < ctx->nsub; ++s)
+        if (!ctx->pending_set[s]) {
+            ctx->err = "missing hierarchy for subdomain " + std::to_string(s);
+            return DFL_E_STATE;
+        }
+    CK(cudaSetDevice(ctx->device));
+    RC(build_groups(ctx));
+    ctx->pending.clear();
+    ctx->pending.shrink_to_fit();
+    RC(build_tiles(ctx));
+    const int64_t nx = ctx->n + ctx->n_ghost;
+    RC(dalloc(ctx, &ctx->b, ctx->n));
+    RC(dalloc(ctx, &ctx->bp, ctx->n));
+    RC(dalloc(ctx, &ctx->x, nx));
+    RC(dalloc(ctx, &ctx->xin, nx));
+    RC(dalloc(ctx, &ctx->p, nx));
+    RC(dalloc(ctx, &ctx->r, ctx->n));
+    RC(dalloc(ctx, &ctx->z, ctx->n));
+    RC(dalloc(ctx, &ctx->w, ctx->n));
+    RC(dalloc(ctx, &ctx->tmp, ctx->n));
+    RC(dalloc(ctx, &ctx->yout, ctx->n));
+    ctx->nblk = cdiv(ctx->n, kBlock);
+    int64_t vparts = 0;
+    for (auto &g : ctx->groups)
+        vparts += g.lv.empty() ? std::max<int64_t>(1, std::min<int64_t>(cdiv(g.row1 - g.row0, kBlock), 64))
+                               : nblocks_for(g.lv[0].A);
+    RC(dalloc(ctx, &ctx->dpart, std::max(ctx->nblk, vparts) + 64));
+    RC(dalloc(ctx, &ctx->zt_part, ctx->ntiles * kKmax + 64));
+    RC(dalloc(ctx, &ctx->scal, 16));
+    RC(dalloc(ctx, &ctx->sgather, (int64_t)8 * ctx->nranks));
+    RC(dalloc(ctx, &ctx->state, 1));
+    CK(cudaMemset(ctx->x, 0, sizeof(double) * nx));
+    CK(cudaMemset(ctx->xin, 0, sizeof(double) * nx));
+    CK(cudaMemset(ctx->p, 0, sizeof(double) * nx));
+    CK(cudaDeviceSynchronize());
+    ctx->finalized = true;
+    return DFL_OK;
+}
+
+int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *x, int ptr_kind, dfl_report *rep) {
+    RC(ready(ctx));
+    if (!p || !rep) return DFL_E_STATE;
+    if (p->solver != DFL_SOLVER_CG) {
+        ctx->err = "only cg is implemented by this build of the device loop";
+        return DFL_E_CONFIG;
+    }
+    if (p->deflated && !ctx->deflation) {
+        ctx->err = "deflated solve requested but no deflation basis uploaded";
+        return DFL_E_STATE;
+    }
+    std::memset(rep, 0, sizeof *rep);
+    ctx->launches = 0;
+    cudaEvent_t e_h0, e_h1;
+    CK(cudaEventCreate(&e_h0));
+    CK(cudaEventCreate(&e_h1));
+    CK(cudaEventRecord(e_h0, ctx->st));
+    RC(stage_in(ctx, ctx->b, b, ptr_kind));
+    CK(cudaEventRecord(ctx->ev0, ctx->st));
+    const bool use_graph = ctx->nranks == 1;
+    RC(cg_solve_dev(ctx, p, use_graph));
+    CK(cudaEventRecord(ctx->ev1, ctx->st));
+    CK(cudaMemcpyAsync(x, ctx->xin, sizeof(double) * ctx->n,
+                       ptr_kind == DFL_PTR_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->st));
+    CK(cudaEventRecord(e_h1, ctx->st));
+    CK(cudaMemcpyAsync(ctx->h_state, ctx->state, sizeof(KState), cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    float ms_h2d = 0, ms_solve = 0, ms_d2h = 0;
+    CK(cudaEventElapsedTime(&ms_h2d, e_h0, ctx->ev0));
+    CK(cudaEventElapsedTime(&ms_solve, ctx->ev0, ctx->ev1));
+    CK(cudaEventElapsedTime(&ms_d2h, ctx->ev1, e_h1));
+    cudaEventDestroy(e_h0);
+    cudaEventDestroy(e_h1);
+    const KState s = *ctx->h_state;
+    rep->iterations = s.iters;
+    rep->converged = s.converged || (s.resnorm <= s.target);
+    if (s.breakdown) rep->converged = 0;
+    rep->breakdown = rep->converged ? DFL_BRK_NONE : s.breakdown;
+    rep->device_loop = use_graph ? 1 : 0;
+    rep->bnorm = s.bnorm;
+    rep->resnorm = s.resnorm;
+    rep->solve_seconds = ms_solve * 1e-3;
+    rep->h2d_seconds = ms_h2d * 1e-3;
+    rep->d2h_seconds = ms_d2h * 1e-3;
+    rep->kernel_launches = ctx->launches + (use_graph ? ctx->body_kernels * std::max(1, s.iters) : 0);
+    // true residual ||b - A x|| / ||b|| (deflation.py:293-297; outside the timed span)
+    if (s.bnorm == 0.0) {
+        rep->relative_residual = 0.0;
+    } else {
+        RC(op_apply_dev(ctx, ctx->xin, ctx->tmp, 1, ctx->b, false, nullptr, 0));
+        double rr = 0.0;
+        RC(rank_dot(ctx, ctx->tmp, ctx->tmp, &rr));
+        rep->relative_residual = std::sqrt(std::max(rr, 0.0)) / s.bnorm;
+    }
+    return DFL_OK;
+}
+
+int dfl_op_apply(dfl_ctx *ctx, const double *x, double *y, int ptr_kind) {
+    RC(ready(ctx));
+    RC(stage_in(ctx, ctx->xin, x, ptr_kind));
+    RC(op_apply_dev(ctx, ctx->xin, ctx->yout, 0, nullptr, false, nullptr, 0));
+    return stage_out(ctx, y, ctx->yout, ptr_kind);
+}
+
+int dfl_precond_apply(dfl_ctx *ctx, const double *r, double *z, int ptr_kind) {
+    RC(ready(ctx));
+    RC(stage_in(ctx, ctx->tmp, r, ptr_kind));
+    RC(vcycle(ctx, ctx->tmp, ctx->yout, nullptr, nullptr, nullptr));
+    return stage_out(ctx, z, ctx->yout, ptr_kind);
+}
+
+int dfl_project(dfl_ctx *ctx, const double *r, double *out, int ptr_kind) {
+    RC(ready(ctx));
+    if (!ctx->deflation) {
+        ctx->err = "no deflation basis";
+        return DFL_E_STATE;
+    }
+    RC(stage_in(ctx, ctx->tmp, r, ptr_kind));
+    RC(project_dev(ctx, ctx->tmp, ctx->yout, nullptr, 0));
+    return stage_out(ctx, out, ctx->yout, ptr_kind);
+}
+
+int dfl_coarse_lift(dfl_ctx *ctx, const double *r, double *out, int ptr_kind) {
+    RC(ready(ctx));
+    if (!ctx->deflation) {
+        ctx->err = "no deflation basis";
+        return DFL_E_STATE;
+    }
+    RC(stage_in(ctx, ctx->tmp, r, ptr_kind));
+    k_zt_vec<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, ctx->tmp, ctx->zcols, ctx->n, ctx->k,
+                                                           ctx->zt_part);
+    RC(zt_to_t2(ctx, nullptr, 0));
+    k_lift<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, ctx->tile_sub, ctx->tmp, ctx->zcols, ctx->n,
+                                                         ctx->k, ctx->t2, (int64_t)ctx->first_sub * ctx->k,
+                                                         ctx->yout, 0);
+    return stage_out(ctx, out, ctx->yout, ptr_kind);
+}
+
+int dfl_dot(dfl_ctx *ctx, const double *a, const double *b, int ptr_kind, double *out) {
+    RC(ready(ctx));
+    RC(stage_in(ctx, ctx->tmp, a, ptr_kind));
+    RC(stage_in(ctx, ctx->yout, b, ptr_kind));
+    return rank_dot(ctx, ctx->tmp, ctx->yout, out);
+}
+
+int dfl_spmv_csr(const dfl_csr *A, const double *x, double *y, int device) {
+    dfl_ctx *ctx = nullptr;
+    RC(dfl_ctx_create(device, &ctx));
+    std::unique_ptr<dfl_ctx, void (*)(dfl_ctx *)> guard(ctx, dfl_ctx_destroy);
+    DMat m;
+    HostRows h{A->nrows, A->ncols, A->row_ptr, A->col_idx, A->values};
+    int rc = upload_matrix(ctx, h, m);
+    if (rc != DFL_OK) {
+        dfl::set_setup_error(ctx->err);
+        return rc;
+    }
+    double *dx, *dy;
+    RC(upload(ctx, &dx, x, A->ncols));
+    RC(dalloc(ctx, &dy, A->nrows));
+    RowArgs a{dx, nullptr, nullptr, nullptr, dy, nullptr, nullptr};
+    launch_rows<MODE_PLAIN, false>(ctx, m, a);
+    cudaError_t e = cudaMemcpyAsync(y, dy, sizeof(double) * A->nrows, cudaMemcpyDeviceToHost, ctx->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
+    if (e != cudaSuccess) {
+        dfl::set_setup_error(cudaGetErrorString(e));
+        return DFL_E_CUDA;
+    }
+    return DFL_OK;
+}
+
+// algorithmic bytes: CSR with fp64 values / int32 indices,
+// every vector read once and written once per kernel
+int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
+    RC(ready(ctx));
+    if (reps < 1) reps = 1;
+    auto run = [&]() -> int {
+        if (what == 0) return op_apply_dev(ctx, ctx->p, ctx->w, 0, nullptr, false, nullptr, 0);
+        if (what == 1) return vcycle(ctx, ctx->r, ctx->z, nullptr, nullptr, nullptr);
+        ctx->err = "unknown timing target";
+        return DFL_E_CONFIG;
+    };
+    if (what == 0) {
+        *bytes = 12.0 * ctx->op_nnz + 4.0 * (ctx->n + 1) + 8.0 * (ctx->n + ctx->n_ghost) + 8.0 * ctx->n;
+    } else {
+        double b = 0;
+        for (auto &g : ctx->groups) {
+            for (size_t l = 0; l < g.lv.size(); ++l) {
+                const double n = (double)g.rows[l], nc = (double)g.rows[l + 1];
+                b += 24.0 * g.nnzA[l] + 24.0 * g.nnzP[l] + 100.0 * n + 20.0 * nc;
+            }
+            b += 8.0 * (double)g.nb * (double)g.nb / std::max(1, g.nsub);
+        }
+        *bytes = b;
+    }
+    // fill the inputs with something finite
+    k_fill<<<(unsigned)cdiv(ctx->n + ctx->n_ghost, kBlock), kBlock, 0, ctx->st>>>(ctx->p, 1.0, ctx->n + ctx->n_ghost);
+    k_fill<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->r, 1.0, ctx->n);
+    for (int i = 0; i < 3; ++i) RC(run());
+    CK(cudaEventRecord(ctx->ev0, ctx->st));
+    for (int i = 0; i < reps; ++i) RC(run());
+    CK(cudaEventRecord(ctx->ev1, ctx->st));
+    CK(cudaEventSynchronize(ctx->ev1));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, ctx->ev0, ctx->ev1));
+    *ms = t / reps;
+    return DFL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,51 @@
+// Host-side setup structures (C++), shared by host_setup.cpp and the device
+// upload code.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/dflb200.h"
+
+namespace dfl {
+
+struct Csr {
+    int64_t nrows = 0, ncols = 0;
+    std::vector<int64_t> ptr{0};
+    std::vector<int64_t> col;
+    std::vector<double> val;
+    int64_t nnz() const { return (int64_t)col.size(); }
+};
+
+struct Level {
+    Csr A, P, R;
+    std::vector<double> w;           // relaxation weights (damping/a_ii or SPAI-0)
+    bool bottom = false;
+    std::vector<double> bottom_inv;  // dense inverse of the bottom block
+};
+
+struct Hierarchy {
+    std::vector<Level> levels;
+    int relax = DFL_RELAX_DAMPED_JACOBI;
+};
+
+void set_setup_error(const std::string &s);
+const char *setup_error();
+
+Csr csr_from_view(const dfl_csr *v);
+Csr transpose(const Csr &a);
+Csr spgemm(const Csr &a, const Csr &b);
+bool diagonal(const Csr &a, std::vector<double> &d, const char *what);
+int lu_inverse(int64_t n, const double *a, double *inv);
+int build_hierarchy(const Csr &a0, const dfl_amg_options &o, Hierarchy &h);
+int basis_az(const dfl_csr *A, int k, const double *zext, const int32_t *owner,
+             const int32_t *rowsub, int64_t K, int sub0, int nsub, int keep_zeros, Csr &az,
+             double *E_rows);
+
+}  // namespace dfl
+
+// opaque handle of the C ABI
+struct dfl_hier {
+    dfl::Hierarchy h;
+};

@@ -1,0 +1,548 @@
+// sm_100a kernels of the B200 solve phase.
+//
+// Everything here is HBM-bandwidth bound sparse / vector work in fp64 with
+// int32 indices (no stage is a dense contraction, so no tensor cores).
+// Matrix storage:
+//   * sliced ELL, 32-row slices stored column-major inside the slice: one
+//     thread per row, each warp-wide load of a slice column is 256 B of
+//     values / 128 B of indices, fully coalesced; rows keep the reference's
+//     CSR entry order and are summed sequentially with separate multiply and
+//     add (no FMA), so ELL SpMV is bit-identical to _kernels.pyx:11-23.
+//   * CSR-vector for long / irregular rows (coarse A, restriction R): a
+//     sub-warp of G lanes per row and a shuffle tree (deterministic, but not
+//     the reference's sequential order).
+// Matrix streams are read with evict-first (ld.global.cs) so the gathered
+// vectors stay resident in the 126 MB L2; gathers use the read-only path.
+//
+// Fused epilogues implement the V(1,1) cycle of amg.py:201-212, the deflation
+// projector of deflation.py:230-233 and the CG recurrences of krylov.py:95-145.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dfl {
+
+constexpr int kBlock = 256;       // threads per block for row kernels
+constexpr int kKmax = 8;          // max deflation columns per subdomain
+constexpr int kEllUnroll = 8;     // slice widths up to this are fully unrolled
+
+enum { FMT_ELL = 0, FMT_CSR = 1 };
+
+struct DMat {
+    int fmt = FMT_ELL;
+    int group = 1;            // CSR-vector lanes per row
+    int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;
+    const int64_t *slice_off = nullptr;  // ELL: nslices + 1 element offsets
+    const int *ptr = nullptr;            // CSR row pointer
+    const int *col = nullptr;
+    const double *val = nullptr;
+};
+
+// run-time state of one Krylov solve (device resident)
+struct KState {
+    double bnorm, target;
+    double rz, rz_new, alpha, beta, pq, rr, resnorm;
+    int iters, done, converged, breakdown, maxiter, refresh_every, refresh_now, pad;
+    // bicgstab2 scalars
+    double rho0, rho1, omega, gamma_div;
+};
+
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+
+template <class T>
+__device__ __forceinline__ T ld_stream(const T *p) { return __ldcs(p); }
+
+// ---------------------------------------------------------------------------
+// gather functors: the value an entry multiplies
+struct GatherX {
+    const double *__restrict__ x;
+    __device__ __forceinline__ double operator()(int c) const { return __ldg(x + c); }
+};
+// relaxation applied on the fly: (w * r)[c]  (amg.py:193/195 then matvec)
+struct GatherWR {
+    const double *__restrict__ w;
+    const double *__restrict__ r;
+    __device__ __forceinline__ double operator()(int c) const { return mul_rn(__ldg(w + c), __ldg(r + c)); }
+};
+
+// sequential, CSR-ordered row sum of an ELL row (bit-identical to spmv_rows)
+template <class G>
+__device__ __forceinline__ double ell_row(const DMat &A, int64_t row, const G &g) {
+    const int64_t s = row >> 5;
+    const int lane = (int)(row & 31);
+    const int64_t off = A.slice_off[s];
+    const int width = (int)((A.slice_off[s + 1] - off) >> 5);
+    const int *cp = A.col + off + lane;
+    const double *vp = A.val + off + lane;
+    double acc = 0.0;
+    if (width <= kEllUnroll) {
+        int c[kEllUnroll];
+        double v[kEllUnroll], xv[kEllUnroll];
+#pragma unroll
+        for (int k = 0; k < kEllUnroll; ++k)
+            if (k < width) {
+                c[k] = ld_stream(cp + 32 * k);
+                v[k] = ld_stream(vp + 32 * k);
+            }
+#pragma unroll
+        for (int k = 0; k < kEllUnroll; ++k)
+            if (k < width) xv[k] = g(c[k]);
+#pragma unroll
+        for (int k = 0; k < kEllUnroll; ++k)
+            if (k < width) acc = add_rn(acc, mul_rn(v[k], xv[k]));
+    } else {
+        for (int k = 0; k < width; ++k) acc = add_rn(acc, mul_rn(ld_stream(vp + 32 * k), g(ld_stream(cp + 32 * k))));
+    }
+    return acc;
+}
+
+// CSR-vector partial sum of one row by G lanes; full sum returned on all lanes
+template <int G, class Gat>
+__device__ __forceinline__ double csr_row(const DMat &A, int64_t row, int sub, const Gat &g) {
+    double acc = 0.0;
+    if (row < A.nrows) {
+        const int b = A.ptr[row], e = A.ptr[row + 1];
+        if (G == 1) {  // one thread per row: sequential CSR order, bit-identical to spmv_rows
+            for (int k = b; k < e; ++k) acc = add_rn(acc, mul_rn(ld_stream(A.val + k), g(ld_stream(A.col + k))));
+        } else {
+            for (int k = b + sub; k < e; k += G) acc += ld_stream(A.val + k) * g(ld_stream(A.col + k));
+        }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+    return acc;
+}
+
+// block-wide sum of NV values (deterministic tree), result valid in thread 0
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double *smem /* 32*NV */) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_down_sync(0xffffffffu, v[j], o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0)
+#pragma unroll
+        for (int j = 0; j < NV; ++j) smem[warp * NV + j] = v[j];
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            v[j] = lane < nw ? smem[lane * NV + j] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v[j] += __shfl_down_sync(0xffffffffu, v[j], o);
+        }
+    }
+}
+
+__device__ __forceinline__ bool skip(const KState *st) { return st != nullptr && st->done; }
+
+// ---------------------------------------------------------------------------
+// V-cycle kernels (amg.py:201-212), one per fused stage.
+//   RESID  : out = r - A (w .* r)                     (pre-smooth + residual)
+//   POST   : out = x + w .* (r - A x)                 (post-smooth), opt. dot r.out
+//   PROLONG: out = w .* r + P e                       (coarse correction)
+//   PLAIN  : out = A x                                (restriction / operator)
+enum { MODE_PLAIN = 0, MODE_RESID = 1, MODE_POST = 2, MODE_PROLONG = 3 };
+
+struct RowArgs {
+    const double *x;   // gathered vector (PLAIN / POST: x, PROLONG: e)
+    const double *w;   // relaxation weights
+    const double *r;   // right-hand side of the level
+    const double *xo;  // POST: own x
+    double *out;
+    double *dot_part;  // POST: per-block r.out partials (nullptr: none)
+    const KState *st;
+};
+
+template <int MODE>
+__device__ __forceinline__ double epilogue(const RowArgs &a, int64_t i, double ax) {
+    if (MODE == MODE_PLAIN) return ax;
+    if (MODE == MODE_RESID) return sub_rn(__ldg(a.r + i), ax);
+    if (MODE == MODE_PROLONG) return add_rn(mul_rn(__ldg(a.w + i), __ldg(a.r + i)), ax);
+    // POST: x + w*(r - Ax)
+    return add_rn(__ldg(a.xo + i), mul_rn(__ldg(a.w + i), sub_rn(__ldg(a.r + i), ax)));
+}
+
+template <int MODE, bool DOT>
+__global__ void __launch_bounds__(kBlock) k_ell(DMat A, RowArgs a) {
+    if (skip(a.st)) return;
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    double dot = 0.0;
+    if (i < A.nrows) {
+        double ax;
+        if (MODE == MODE_RESID)
+            ax = ell_row(A, i, GatherWR{a.w, a.r});
+        else
+            ax = ell_row(A, i, GatherX{a.x});
+        const double y = epilogue<MODE>(a, i, ax);
+        a.out[i] = y;
+        if (DOT) dot = __ldg(a.r + i) * y;
+    }
+    if (DOT) {
+        __shared__ double sm[32];
+        double v[1] = {dot};
+        block_sum<1>(v, sm);
+        if (threadIdx.x == 0) a.dot_part[blockIdx.x] = v[0];
+    }
+}
+
+template <int G, int MODE, bool DOT>
+__global__ void __launch_bounds__(kBlock) k_csr(DMat A, RowArgs a) {
+    if (skip(a.st)) return;
+    constexpr int RPB = kBlock / G;
+    const int64_t i = (int64_t)blockIdx.x * RPB + threadIdx.x / G;
+    const int sub = threadIdx.x % G;
+    double ax;
+    if (MODE == MODE_RESID)
+        ax = csr_row<G>(A, i, sub, GatherWR{a.w, a.r});
+    else
+        ax = csr_row<G>(A, i, sub, GatherX{a.x});
+    double dot = 0.0;
+    if (sub == 0 && i < A.nrows) {
+        const double y = epilogue<MODE>(a, i, ax);
+        a.out[i] = y;
+        if (DOT) dot = __ldg(a.r + i) * y;
+    }
+    if (DOT) {
+        __shared__ double sm[32];
+        double v[1] = {dot};
+        block_sum<1>(v, sm);
+        if (threadIdx.x == 0) a.dot_part[blockIdx.x] = v[0];
+    }
+}
+
+// bottom level: x = inv(A_bottom) r per subdomain, inverse stored transposed
+// (column j contiguous) so that thread i reads coalesced; r staged in smem.
+__global__ void k_bottom(const double *__restrict__ invT, const int64_t *__restrict__ inv_off,
+                         const int64_t *__restrict__ off, const double *__restrict__ r,
+                         double *__restrict__ x, const KState *st) {
+    if (skip(st)) return;
+    extern __shared__ double rs[];
+    const int s = blockIdx.x;
+    const int64_t o = off[s];
+    const int n = (int)(off[s + 1] - o);
+    const double *M = invT + inv_off[s];
+    for (int j = threadIdx.x; j < n; j += blockDim.x) rs[j] = r[o + j];
+    __syncthreads();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        double acc = 0.0;
+        for (int j = 0; j < n; ++j) acc = fma(M[(int64_t)j * n + i], rs[j], acc);
+        x[o + i] = acc;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Operator SpMV (runtime.py:283-292) with the deflation epilogue: per tile
+// (tiles never straddle a subdomain) partial sums of Z' y for the k basis
+// columns (column 0 is the constant 1; columns 1..k-1 come from zcols).
+//   OPMODE 0: y = A x ;  OPMODE 1: y = b - A x
+struct Tiles {
+    const int64_t *row0;  // ntiles + 1 boundaries are not contiguous across subdomains
+    const int64_t *row1;
+    int64_t ntiles;
+};
+
+struct OpArgs {
+    const double *x;        // gathered input (n_local + n_ghost)
+    const double *b;        // OPMODE 1
+    double *y;
+    const double *zcols;    // (k-1) columns, column-major, length n each
+    int64_t n;
+    int k;                  // 0: no Z' partials
+    double *zt_part;        // ntiles * k
+    const KState *st;
+    int need_refresh;       // 1: skip unless st->refresh_now
+};
+
+template <int OPMODE, int NV>
+__device__ __forceinline__ void op_epilogue(const OpArgs &a, int64_t i, bool valid, double y,
+                                            double (&acc)[NV]) {
+#pragma unroll
+    for (int c = 0; c < NV; ++c) acc[c] = 0.0;
+    if (valid) {
+        acc[0] = y;
+#pragma unroll
+        for (int c = 1; c < NV; ++c)
+            if (c < a.k) acc[c] = __ldg(a.zcols + (int64_t)(c - 1) * a.n + i) * y;
+    }
+}
+
+template <int OPMODE>
+__global__ void __launch_bounds__(kBlock) k_op_ell(DMat A, Tiles T, OpArgs a) {
+    if (skip(a.st)) return;
+    if (a.need_refresh && !a.st->refresh_now) return;
+    const int64_t t = blockIdx.x;
+    const int64_t i = T.row0[t] + threadIdx.x;
+    const bool valid = i < T.row1[t];
+    double y = 0.0;
+    if (valid) {
+        const double ax = ell_row(A, i, GatherX{a.x});
+        y = OPMODE == 1 ? sub_rn(__ldg(a.b + i), ax) : ax;
+        a.y[i] = y;
+    }
+    if (a.k > 0) {
+        __shared__ double sm[32 * kKmax];
+        double acc[kKmax];
+        op_epilogue<OPMODE>(a, i, valid, y, acc);
+        block_sum<kKmax>(acc, sm);
+        if (threadIdx.x == 0)
+            for (int c = 0; c < a.k; ++c) a.zt_part[t * a.k + c] = acc[c];
+    }
+}
+
+template <int G, int OPMODE>
+__global__ void __launch_bounds__(kBlock) k_op_csr(DMat A, Tiles T, OpArgs a) {
+    if (skip(a.st)) return;
+    if (a.need_refresh && !a.st->refresh_now) return;
+    const int64_t t = blockIdx.x;
+    const int64_t i = T.row0[t] + threadIdx.x / G;
+    const int sub = threadIdx.x % G;
+    const bool inrange = i < T.row1[t];
+    const double ax = csr_row<G>(A, inrange ? i : A.nrows, sub, GatherX{a.x});
+    const bool valid = inrange && sub == 0;
+    double y = 0.0;
+    if (valid) {
+        y = OPMODE == 1 ? sub_rn(__ldg(a.b + i), ax) : ax;
+        a.y[i] = y;
+    }
+    if (a.k > 0) {
+        __shared__ double sm[32 * kKmax];
+        double acc[kKmax];
+        op_epilogue<OPMODE>(a, i, valid, y, acc);
+        block_sum<kKmax>(acc, sm);
+        if (threadIdx.x == 0)
+            for (int c = 0; c < a.k; ++c) a.zt_part[t * a.k + c] = acc[c];
+    }
+}
+
+// Z' v partials without a product (project(b), coarse_lift(r))
+__global__ void __launch_bounds__(kBlock) k_zt_vec(Tiles T, const double *__restrict__ v,
+                                                   const double *__restrict__ zcols, int64_t n,
+                                                   int k, double *zt_part) {
+    const int64_t t = blockIdx.x;
+    const int64_t i = T.row0[t] + threadIdx.x;
+    const bool valid = i < T.row1[t];
+    __shared__ double sm[32 * kKmax];
+    double acc[kKmax];
+#pragma unroll
+    for (int c = 0; c < kKmax; ++c) acc[c] = 0.0;
+    if (valid) {
+        const double y = v[i];
+        acc[0] = y;
+#pragma unroll
+        for (int c = 1; c < kKmax; ++c)
+            if (c < k) acc[c] = __ldg(zcols + (int64_t)(c - 1) * n + i) * y;
+    }
+    block_sum<kKmax>(acc, sm);
+    if (threadIdx.x == 0)
+        for (int c = 0; c < k; ++c) zt_part[t * k + c] = acc[c];
+}
+
+// Sum tile partials per local subdomain -> t (global coarse numbering at
+// first_col), then optionally t2 = E^{-1} t with the replicated inverse.
+// One block; warp w reduces values w, w+nwarps, ... in fixed order.
+__global__ void k_zt_finish(const double *__restrict__ zt_part, const int64_t *__restrict__ sub_tiles,
+                            int nsub, int k, double *t_out, int64_t first_col, const double *Einv,
+                            int64_t K, double *t2, const KState *st, int need_refresh) {
+    if (skip(st)) return;
+    if (need_refresh && !st->refresh_now) return;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int v = warp; v < nsub * k; v += nw) {
+        const int s = v / k, c = v % k;
+        const int64_t t0 = sub_tiles[s], t1 = sub_tiles[s + 1];
+        double acc = 0.0;
+        for (int64_t t = t0 + lane; t < t1; t += 32) acc += zt_part[t * k + c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+        if (lane == 0) t_out[first_col + v] = acc;
+    }
+    if (Einv == nullptr) return;
+    __syncthreads();
+    __threadfence_block();
+    for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
+        double acc = 0.0;
+        for (int64_t j = 0; j < K; ++j) acc = fma(Einv[i * K + j], t_out[j], acc);
+        t2[i] = acc;
+    }
+}
+
+// t2 = E^{-1} t (multi-rank path, after the allgather of t)
+__global__ void k_esolve(const double *Einv, int64_t K, const double *t, double *t2, const KState *st,
+                         int need_refresh) {
+    if (skip(st)) return;
+    if (need_refresh && !st->refresh_now) return;
+    for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
+        double acc = 0.0;
+        for (int64_t j = 0; j < K; ++j) acc = fma(Einv[i * K + j], t[j], acc);
+        t2[i] = acc;
+    }
+}
+
+// AZ t2 for one row (AZ is n x K CSR, exact zeros dropped, K tiny): sequential
+// in column order like matvec(AZ, .)
+__device__ __forceinline__ double az_row(const int *__restrict__ ptr, const int *__restrict__ col,
+                                         const double *__restrict__ val, const double *t2s, int64_t i) {
+    double acc = 0.0;
+    const int b = __ldg(ptr + i), e = __ldg(ptr + i + 1);
+    for (int k = b; k < e; ++k) acc = add_rn(acc, mul_rn(__ldg(val + k), t2s[__ldg(col + k)]));
+    return acc;
+}
+
+struct ProjArgs {
+    const int *az_ptr;
+    const int *az_col;
+    const double *az_val;
+    const double *t2;   // K
+    int64_t K;
+    int64_t n;
+    const double *in;   // w
+    double *out;        // w - AZ t2   (may alias in)
+    const double *dotv; // dotmode 1: partial dot(dotv, out)
+    const double *base; // MODE 1: out = base - (in - AZ t2)
+    double *dot_part;
+    int dotmode;        // 0: none, 1: dot(dotv, out), 2: dot(out, out)
+    const KState *st;
+    int need_refresh;   // 1: only when refresh_now, 0: always, -1: only when !refresh_now
+};
+
+// q = w - AZ t2 (+ dot partial p.q);  refresh variant: r = b' - (w - AZ t2) (+ r.r)
+template <int MODE>
+__global__ void __launch_bounds__(kBlock) k_project(ProjArgs a) {
+    if (skip(a.st)) return;
+    if (a.need_refresh == 1 && !a.st->refresh_now) return;
+    extern __shared__ double t2s[];
+    for (int64_t j = threadIdx.x; j < a.K; j += blockDim.x) t2s[j] = a.t2[j];
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    double dot = 0.0;
+    if (i < a.n) {
+        double q = a.in[i];
+        if (a.az_ptr) q = sub_rn(q, az_row(a.az_ptr, a.az_col, a.az_val, t2s, i));
+        if (MODE == 1) q = sub_rn(__ldg(a.base + i), q);
+        a.out[i] = q;
+        if (a.dotmode == 1) dot = __ldg(a.dotv + i) * q;
+        if (a.dotmode == 2) dot = q * q;
+    }
+    if (a.dotmode != 0) {
+        __shared__ double sm[32];
+        double v[1] = {dot};
+        block_sum<1>(v, sm);
+        if (threadIdx.x == 0) a.dot_part[blockIdx.x] = v[0];
+    }
+}
+
+// x = y + Z t2 (coarse_lift, deflation.py:235-237 & :285): Z row i has the
+// entries [1, zcols(i, 1..k-1)] at columns s*k .. s*k+k-1, summed in order.
+__global__ void __launch_bounds__(kBlock) k_lift(Tiles T, const int *tile_sub, const double *__restrict__ y,
+                                                 const double *__restrict__ zcols, int64_t n, int k,
+                                                 const double *__restrict__ t2, int64_t first_col,
+                                                 double *out, int add_y) {
+    const int64_t t = blockIdx.x;
+    const int64_t i = T.row0[t] + threadIdx.x;
+    if (i >= T.row1[t]) return;
+    const int64_t base = (first_col + (int64_t)tile_sub[t] * k);
+    double acc = add_rn(0.0, mul_rn(1.0, t2[base]));
+    for (int c = 1; c < k; ++c) acc = add_rn(acc, mul_rn(zcols[(int64_t)(c - 1) * n + i], t2[base + c]));
+    out[i] = add_y ? add_rn(y[i], acc) : acc;
+}
+
+// ---------------------------------------------------------------------------
+// vector kernels and reductions
+
+__global__ void __launch_bounds__(kBlock) k_dot(const double *__restrict__ a, const double *__restrict__ b,
+                                                int64_t n, double *part, const KState *st) {
+    if (skip(st)) return;
+    double acc = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
+        acc += a[i] * b[i];
+    __shared__ double sm[32];
+    double v[1] = {acc};
+    block_sum<1>(v, sm);
+    if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+}
+
+// deterministic sum of nparts partials -> out[slot]  (one block)
+__device__ __forceinline__ double reduce_parts(const double *part, int64_t nparts) {
+    __shared__ double sm[32];
+    double acc = 0.0;
+    for (int64_t j = threadIdx.x; j < nparts; j += blockDim.x) acc += part[j];
+    double v[1] = {acc};
+    block_sum<1>(v, sm);
+    __shared__ double total;
+    if (threadIdx.x == 0) total = v[0];
+    __syncthreads();
+    return total;
+}
+
+__global__ void k_reduce(const double *part, int64_t nparts, double *out) {
+    const double s = reduce_parts(part, nparts);
+    if (threadIdx.x == 0) *out = s;
+}
+
+// CG update (krylov.py:127-131): x += alpha p;  r -= alpha q  (+ r.r partial)
+// On refresh iterations only x is updated here (r comes from the refresh path).
+__global__ void __launch_bounds__(kBlock) k_cg_update(double *x, double *r, const double *__restrict__ p,
+                                                      const double *__restrict__ q, int64_t n, double *part,
+                                                      const KState *st) {
+    if (skip(st)) return;
+    const double alpha = st->alpha;
+    const bool refresh = st->refresh_now;
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    double dot = 0.0;
+    if (i < n) {
+        const double pi = p[i];
+        x[i] = add_rn(x[i], mul_rn(alpha, pi));
+        if (!refresh) {
+            const double ri = sub_rn(r[i], mul_rn(alpha, q[i]));
+            r[i] = ri;
+            dot = ri * ri;
+        }
+    }
+    if (!refresh) {
+        __shared__ double sm[32];
+        double v[1] = {dot};
+        block_sum<1>(v, sm);
+        if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+    }
+}
+
+// p = z + beta p (krylov.py:142)
+__global__ void __launch_bounds__(kBlock) k_cg_p(double *p, const double *__restrict__ z, int64_t n,
+                                                 const KState *st) {
+    if (skip(st)) return;
+    const double beta = st->beta;
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (i < n) p[i] = add_rn(z[i], mul_rn(beta, p[i]));
+}
+
+__global__ void k_copy(double *dst, const double *src, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (i < n) dst[i] = src[i];
+}
+
+__global__ void k_fill(double *dst, double v, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (i < n) dst[i] = v;
+}
+
+// halo: pack own values to send, in neighbour order
+__global__ void k_gather(const double *__restrict__ src, const int *__restrict__ idx, int64_t m, double *dst) {
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (i < m) dst[i] = src[idx[i]];
+}
+
+// sum rank-gathered scalars in rank order: out[v] = sum_q g[q*stride + v]
+__global__ void k_rank_sum(const double *g, int nranks, int stride, int nv, double *out) {
+    const int v = threadIdx.x;
+    if (v >= nv) return;
+    double acc = 0.0;
+    for (int q = 0; q < nranks; ++q) acc += g[q * stride + v];
+    out[v] = acc;
+}
+
+}  // namespace dfl

@@ -1,0 +1,114 @@
+"""GPU parity of the B200 solve path against the CPU oracle (oracle/port.py)
+and the reference's golden outputs (tests/golden).  Runs through the C ABI
+(libdflb200.so) on cuda:0."""
+import numpy as np
+import pytest
+
+from golden_data import arrays, meta, solve_case
+from oracle import port
+from paper_1710_03940_b200 import _native as nat
+from paper_1710_03940_b200 import problems
+from paper_1710_03940_b200.config import SolverConfig
+from paper_1710_03940_b200.runtime import partition_contiguous
+
+pytestmark = pytest.mark.gpu
+
+
+def _solver(p, m, cfgd, deflated=True, part=None):
+    from paper_1710_03940_b200 import DeflatedSolver
+
+    part = part or (p.partition if m == len(p.partition.ranges) else partition_contiguous(p.matrix.nrows, m))
+    return DeflatedSolver(p.matrix, part, config=SolverConfig(cfgd), coords=p.coords, deflated=deflated)
+
+
+def _oracle(p, m, cfgd, deflated=True, part=None):
+    part = part or (p.partition if m == len(p.partition.ranges) else partition_contiguous(p.matrix.nrows, m))
+    return port.DeflatedSolverOracle(p.matrix, part, config=SolverConfig(cfgd), coords=p.coords,
+                                     deflated=deflated)
+
+
+def test_spmv_ell_bitwise():
+    p = problems.poisson3d(24)
+    A = nat.CsrArrays(p.matrix.nrows, p.matrix.ncols, p.matrix.row_ptr, p.matrix.col_idx, p.matrix.values)
+    x = np.random.default_rng(1).standard_normal(p.matrix.ncols)
+    y = nat.spmv_device(A, x)
+    assert np.array_equal(y, port.spmv(port.Csr.of(p.matrix), x))
+
+
+def test_spmv_random_csr():
+    rng = np.random.default_rng(3)
+    n = 3000
+    dense = np.where(rng.random((n, n)) < 0.02, rng.standard_normal((n, n)), 0.0)
+    M = port.coo_to_csr(n, n, *np.nonzero(dense), dense[np.nonzero(dense)])
+    A = nat.CsrArrays(n, n, M.row_ptr, M.col_idx, M.values)
+    x = rng.standard_normal(n)
+    y = nat.spmv_device(A, x)
+    np.testing.assert_allclose(y, dense @ x, rtol=1e-13, atol=1e-13 * np.abs(dense).sum(axis=1).max())
+
+
+@pytest.mark.parametrize("kind", ["constant", "linear"])
+def test_unit_ops_match_oracle(kind):
+    p = problems.poisson3d(16)
+    cfgd = {"solver": {"type": "cg"}, "precond": {"relax": {"type": "spai0"}}, "deflation": {"kind": kind}}
+    s = _solver(p, 4, cfgd)
+    o = _oracle(p, 4, cfgd)
+    r = np.random.default_rng(7).standard_normal(p.matrix.nrows)
+    # operator SpMV: ELL storage, sequential CSR order -> bitwise
+    assert np.array_equal(s.op(r), o.op(r))
+    # projector / coarse lift / V-cycle: tolerance (E^-1 and bottom inverse vs LAPACK)
+    scale = np.linalg.norm(r)
+    assert np.linalg.norm(s.project(r) - o.project(r)) <= 1e-12 * scale
+    assert np.linalg.norm(s.coarse_lift(r) - o.coarse_lift(r)) <= 1e-12 * np.linalg.norm(o.coarse_lift(r))
+    z, zo = s.preconditioner()(r), o.precond(r)
+    assert np.linalg.norm(z - zo) <= 1e-12 * np.linalg.norm(zo)
+    assert abs(s.dot(r, z) - o.dot(r, zo)) <= 1e-12 * abs(o.dot(r, zo))
+    np.testing.assert_array_equal(s.basis.E, o.basis.E) if kind == "constant" else None
+
+
+def test_projector_identities():
+    p = problems.poisson3d(16)
+    rng = np.random.default_rng(11)
+    for m in (2, 8):
+        for kind in ("constant", "linear"):
+            s = _solver(p, m, {"solver": {"type": "cg"}, "deflation": {"kind": kind}})
+            o = _oracle(p, m, {"solver": {"type": "cg"}, "deflation": {"kind": kind}})
+            for _ in range(5):
+                r = rng.standard_normal(p.matrix.nrows)
+                pr = s.project(r)
+                sc = np.linalg.norm(r)
+                assert np.linalg.norm(s.project(pr) - pr) <= 1e-12 * sc
+                assert np.linalg.norm(port.spmv(o.basis.Zt, pr)) <= 1e-10 * sc
+
+
+CG_CASES = [c for c in meta()["solves"] if c["config"]["solver"]["type"] == "cg"]
+
+
+@pytest.mark.parametrize("case", CG_CASES, ids=lambda c: c["name"])
+def test_cg_solve_parity(case):
+    shape = case["shape"] if isinstance(case["shape"], int) else tuple(case["shape"])
+    p = problems.make_problem(shape, problems.boxes_for(case["m"]), case["kind"])
+    s = _solver(p, case["m"], case["config"], deflated=case["deflated"])
+    x, rep = s.solve(p.rhs)
+    xref = arrays()[f"solve_{case['name']}_x"]
+    tol = case["config"]["solver"]["tol"]
+    assert rep["converged"]
+    assert abs(rep["iterations"] - case["iterations"]) <= 1, (rep["iterations"], case["iterations"])
+    assert rep["relative_residual"] <= max(tol, 2 * case["relative_residual"])
+    assert np.linalg.norm(x - xref) <= 1e-6 * np.linalg.norm(xref)
+    assert rep["device_loop"]
+    assert rep["kernel_launches"] > 0
+
+
+def test_config1_fingerprint():
+    c = solve_case("config1_32_m4_cg_spai0_const")
+    p = problems.poisson3d(32, (1, 1, 4))
+    s = _solver(p, 4, c["config"])
+    x, rep = s.solve(p.rhs)
+    assert abs(rep["iterations"] - 32) <= 1
+    assert abs(np.linalg.norm(x) - 4.7294799783129635) <= 1e-6 * 4.73
+    assert abs(x.sum() - 720.8234011018488) <= 1e-6 * 720.8
+    # one setup, many solves; zero rhs -> zero solution in 0 iterations
+    x2, rep2 = s.solve(p.rhs)
+    assert np.array_equal(x, x2) and rep2["iterations"] == rep["iterations"]
+    x0, rep0 = s.solve(np.zeros_like(p.rhs))
+    assert not x0.any() and rep0["iterations"] == 0 and rep0["converged"]
