@@ -1,0 +1,335 @@
+#!/usr/bin/env python
+"""Benchmark: deflated CG + local SA-AMG solve phase on B200 (BASELINE.json).
+
+Workload (configs[1]): 3-D 7-point Poisson, 150^3 unknowns per GPU, one
+subdomain per GPU in boxes_for(N) boxes (weak scaling), linear deflation,
+SA-AMG with SPAI-0 relaxation, CG to tol 1e-8.  A "step" is one full solve
+(DeflatedSolver.solve: projected rhs, Krylov loop, coarse lift) with b
+already resident in HBM; setup (host, native C++) and upload are outside the
+timed region and reported separately.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    python -m torch.distributed.run --nproc-per-node N bench.py --gpus N ...
+
+Rank 0 prints one JSON line.  ``--impl reference`` times the reference's CPU
+algorithm (the oracle port, oracle/port.py -- the reference itself is Python
+and cannot travel to the GPU box) on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+CFG = {
+    "solver": {"type": "cg", "tol": 1e-8, "maxiter": 1000},
+    "precond": {"relax": {"type": "spai0"}},
+    "deflation": {"kind": "linear"},
+}
+METRIC = "DCG+AMG solve sec & iters, 3D Poisson @1/2/4/8 B200; SpMV HBM GB/s vs peak"
+UNIT = "s/solve"
+
+
+def env_world():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def workload(N: int, edge: int):
+    from paper_1710_03940_b200 import problems
+
+    boxes = problems.boxes_for(N)
+    shape = tuple(edge * b for b in boxes)
+    return problems.BoxOrdering(shape, boxes), boxes, shape
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].strip() == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def max_over_ranks(v: float, ws: int) -> float:
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws: int):
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+def oracle_sample(A_rows, n, coords, partition, cores: int, iters_sample: int, full_iters: int | None):
+    """Time the CPU oracle (the reference's algorithm) on the same problem:
+    setup once, then a solve capped at `iters_sample` CG iterations; the
+    per-iteration time is scaled to the full iteration count."""
+    from oracle import port
+    from paper_1710_03940_b200.config import SolverConfig
+    from paper_1710_03940_b200.sparse import SparseMatrix
+
+    port.set_threads(cores)
+    A = SparseMatrix(n, n, *A_rows)
+    t0 = time.perf_counter()
+    o = port.DeflatedSolverOracle(A, partition, config=SolverConfig(CFG), coords=coords)
+    setup = time.perf_counter() - t0
+    h = 1.0 / (round(n ** (1 / 3)) + 1)
+    return o, setup
+
+
+def run_oracle_steps(o, n, h, steps, warmup, iters_sample, full_iters, cores):
+    b = np.full(n, h * h)
+    try:
+        from threadpoolctl import threadpool_limits
+        limiter = threadpool_limits(limits=cores)
+    except Exception:  # pragma: no cover
+        limiter = None
+    times = []
+    its = None
+    for i in range(warmup + steps):
+        x, rep = o.solve(b, maxiter=iters_sample)
+        its = rep["iterations"]
+        if i >= warmup:
+            times.append(rep["solve_seconds"])
+    if limiter is not None:
+        limiter.unregister() if hasattr(limiter, "unregister") else None
+    per_iter = statistics.mean(times) / max(1, its)
+    return per_iter * full_iters, per_iter, its
+
+
+def reference_arm(args, ws, rank):
+    """--impl reference: the reference's CPU algorithm (oracle port) on this
+    host, all cores, rank 0 only."""
+    if rank != 0:
+        return 0
+    from paper_1710_03940_b200 import problems
+
+    ordering, boxes, shape = workload(ws, args.edge)
+    n = ordering.n
+    ptr, col, val = problems.local_rows(ordering, 0, n, "poisson")
+    coords = problems.node_coords(ordering, 0, n)
+    cores = os.cpu_count() or 1
+    o, setup = oracle_sample((ptr, col, val), n, coords, ordering.partition(), cores, args.ref_iters, None)
+    h = 1.0 / (shape[0] + 1)
+    full = args.ref_full_iters or {1: 23, 2: 63, 4: 69, 8: 101}.get(ws, 23)
+    value, per_iter, its = run_oracle_steps(o, n, h, args.steps, args.warmup, args.ref_iters, full, cores)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": value * 1e3, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"poisson7 {shape[0]}x{shape[1]}x{shape[2]}, m={ws} boxes {list(boxes)}, linear "
+                               "deflation, SA-AMG+SPAI0, CG tol 1e-8 (configs[1])", "unknowns": n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"oracle/port.py (numpy + C restatement of deflamg) on the full problem, "
+                                   f"{its} CG iterations timed per step, scaled to {full} iterations "
+                                   f"(the reference's count); operator matvec threaded x{cores}, V-cycle serial "
+                                   f"as in the reference; oracle setup {setup:.1f}s untimed"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+def b200_arm(args, ws, rank, local):
+    import torch
+
+    from paper_1710_03940_b200 import problems
+    from paper_1710_03940_b200.config import SolverConfig
+    from paper_1710_03940_b200.deflation import DeflatedSolver, solve_device
+
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    ordering, boxes, shape = workload(ws, args.edge)
+    n = ordering.n
+    part = ordering.partition()
+    r0, r1 = part.ranges[rank]
+    t0 = time.perf_counter()
+    rows = problems.local_rows(ordering, r0, r1, "poisson")
+    coords = problems.node_coords(ordering, r0, r1)
+    gen_s = time.perf_counter() - t0
+    solver = DeflatedSolver.from_rows(rows, n, part, config=SolverConfig(CFG), coords_local=coords, device=local)
+    h = 1.0 / (shape[0] + 1)
+    nl = r1 - r0
+    b = torch.full((nl,), h * h, dtype=torch.float64, device="cuda")
+    x = torch.empty(nl, dtype=torch.float64, device="cuda")
+    dev_s, launches = [], 0
+    with ClockSampler(local) as clk:
+        time.sleep(0.5)
+        for _ in range(args.warmup):
+            rep = solve_device(solver, b.data_ptr(), x.data_ptr())
+        torch.cuda.synchronize()
+        barrier(ws)
+        torch.cuda.synchronize()
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            rep = solve_device(solver, b.data_ptr(), x.data_ptr())
+            dev_s.append(rep.solve_seconds)
+            launches += rep.kernel_launches
+        torch.cuda.synchronize()
+        barrier(ws)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - w0) / args.steps
+    iters = rep.iterations
+    step_s = max_over_ranks(statistics.mean(dev_s), ws)
+    # end to end through the public API: pinned host b -> x on the host
+    b_host = torch.full((nl,), h * h, dtype=torch.float64).pin_memory().numpy()
+    e2e = []
+    for i in range(args.warmup + args.steps):
+        barrier(ws)
+        t = time.perf_counter()
+        xh, report = solver.solve(b_host)
+        if i >= args.warmup:
+            e2e.append(time.perf_counter() - t)
+    e2e_s = max_over_ranks(statistics.mean(e2e), ws)
+    # roofline of the fine-level SpMV (the north-star kernel) and of the V-cycle
+    peak, peak_src = peaks()
+    spmv_ms, spmv_bytes = solver._ctx.time(0, 50)
+    vc_ms, vc_bytes = solver._ctx.time(1, 20)
+    spmv_gbs = spmv_bytes / (spmv_ms * 1e-3) / 1e9
+    vc_gbs = vc_bytes / (vc_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        with open(os.path.join(REPO, "profiles", "ncu_summary.json")) as fh:
+            traffic = json.load(fh).get("op_spmv_dram_bytes_per_launch")
+    except Exception:
+        pass
+    line = {
+        "metric": METRIC, "value": step_s, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"poisson7 {shape[0]}x{shape[1]}x{shape[2]}, m={ws} boxes {list(boxes)}, linear "
+                               "deflation, SA-AMG+SPAI0, CG tol 1e-8 (configs[1])",
+                   "unknowns": n, "unknowns_per_gpu": nl, "iterations": iters, "converged": bool(rep.converged),
+                   "l2": "inputs larger than L2 (matrices ~1.4 GB/GPU vs 126 MB L2); no flush",
+                   "parallelism": f"subdomain-dp{ws}"},
+        "iters": iters,
+        "relative_residual": report["relative_residual"],
+        "setup_seconds_host": solver.setup_seconds, "generate_seconds": gen_s,
+        "wall_ms_per_step": wall * 1e3,
+        "gpu_launches": int(launches),
+        "e2e": {"value": e2e_s, "unit": UNIT, "h2d_bytes_per_step": 8 * nl, "d2h_bytes_per_step": 8 * nl},
+        "roofline": {"bound": "hbm", "kernel": "operator SpMV (sliced-ELL fp64/int32, k_op_ell) fine level",
+                     "achieved": spmv_gbs, "peak": peak, "unit": "GB/s", "frac": spmv_gbs / peak,
+                     "traffic": traffic, "bytes_per_launch": spmv_bytes, "ms_per_launch": spmv_ms,
+                     "peak_source": peak_src},
+        "vcycle_roofline": {"achieved": vc_gbs, "frac": vc_gbs / peak, "bytes_per_cycle": vc_bytes,
+                            "ms_per_cycle": vc_ms},
+        "clocks": clk.summary(),
+    }
+    if ws == 1 and rank == 0 and not args.no_cpu:
+        cores = 1
+        from paper_1710_03940_b200.config import SolverConfig as _SC  # noqa: F401
+
+        A_rows = rows
+        o, setup = oracle_sample(A_rows, n, coords, part, cores, args.ref_iters, iters)
+        value, per_iter, its = run_oracle_steps(o, n, h, 1, 0, args.ref_iters, iters, cores)
+        line["cpu_baseline"] = {
+            "value": value, "unit": UNIT, "cores": cores, "kind": "port",
+            "sample": f"oracle/port.py on the same 150^3 problem, one solve capped at {its} CG iterations, "
+                      f"per-iteration time x {iters} iterations; 1 thread; oracle setup {setup:.1f}s untimed"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--edge", type=int, default=150, help="grid edge per subdomain (150 = configs[1])")
+    ap.add_argument("--ref-iters", type=int, default=3, help="CG iterations per CPU-oracle sample")
+    ap.add_argument("--ref-full-iters", type=int, default=0)
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline leg")
+    args = ap.parse_args()
+    ws, rank, local = env_world()
+    if args.gpus != ws and ws > 1:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {ws}", file=sys.stderr)
+    if args.impl == "reference":
+        return reference_arm(args, ws, rank)
+    return b200_arm(args, ws, rank, local)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -367,14 +367,44 @@ def split(A: Csr, ranges) -> list:
     return views
 
 
+_POOL = None
+
+
+def set_threads(t: int) -> None:
+    """Row-chunked threading of the distributed matvec, as the reference's
+    threads_per_subdomain (runtime.py:228-243); numerically inert."""
+    global _POOL
+    from concurrent.futures import ThreadPoolExecutor
+
+    _POOL = ThreadPoolExecutor(max_workers=t) if t > 1 else None
+    _POOL_T[0] = t
+
+
+_POOL_T = [1]
+
+
+def _local_matvec(A: Csr, x: np.ndarray) -> np.ndarray:
+    T = _POOL_T[0]
+    if _POOL is None or A.nrows < 2 * T:
+        return spmv(A, x)
+    out = np.empty(A.nrows)
+    lib = _clib()
+    bounds = [A.nrows * t // T for t in range(T + 1)]
+    futs = [_POOL.submit(lib.csr_spmv, _p(A.row_ptr), _p(A.col_idx), _p(A.values), _p(x), _p(out),
+                         bounds[t], bounds[t + 1]) for t in range(T) if bounds[t] < bounds[t + 1]]
+    for f in futs:
+        f.result()
+    return out
+
+
 def dist_spmv(views, x: np.ndarray) -> np.ndarray:
     """Halo gather + per-subdomain local product (reference: runtime.py:246-292).
     Ghost values are gathered by global index; the per-owner grouping of the
     reference is order-preserving, so this is the same vector."""
     y = np.empty(x.shape[0])
     for v in views:
-        xl = np.concatenate((x[v.begin:v.end], x[v.ghosts]))
-        y[v.begin:v.end] = spmv(v.local, xl)
+        xl = np.ascontiguousarray(np.concatenate((x[v.begin:v.end], x[v.ghosts])))
+        y[v.begin:v.end] = _local_matvec(v.local, xl)
     return y
 
 
@@ -662,7 +692,7 @@ class DeflatedSolverOracle:
             out[b:e] = h.apply(r[b:e])
         return out
 
-    def solve(self, b, *, max_seconds=None):
+    def solve(self, b, *, maxiter=None):
         import time
 
         b = np.asarray(b, dtype=np.float64)
@@ -672,7 +702,7 @@ class DeflatedSolverOracle:
         fn = cg if name == "cg" else bicgstab2
         tol = self.cfg.get("solver.tol")
         bnorm = math.sqrt(max(self.dot(b, b), 0.0))
-        maxiter = self.cfg.get("solver.maxiter")
+        maxiter = self.cfg.get("solver.maxiter") if maxiter is None else maxiter
         t0 = time.perf_counter()
         if bnorm == 0.0:
             x = np.zeros_like(b)

@@ -144,6 +144,7 @@ struct dfl_ctx {
     double *tvec = nullptr, *t2 = nullptr;
     double *zt_part = nullptr;
     double *tgather = nullptr;  // nranks * maxsub * k
+    unsigned int *ticket = nullptr;
     int max_nsub = 0;
     std::vector<int> rank_nsub;  // subdomains per rank (runtime.rank_subdomains)
     // work vectors (n, or n + n_ghost for operator inputs)
@@ -375,16 +376,17 @@ static int halo(dfl_ctx *ctx, double *v) {
 // Z' v partials -> t (global numbering) -> t2 = E^-1 t on every rank
 static int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh) {
     if (ctx->nranks == 1) {
-        k_zt_finish<<<1, 256, 0, ctx->st>>>(ctx->zt_part, ctx->sub_tiles, ctx->nsub, ctx->k, ctx->tvec, 0, ctx->Einv,
-                                            ctx->K, ctx->t2, st, need_refresh);
+        k_zt_finish<<<ctx->nsub * ctx->k, 512, 0, ctx->st>>>(ctx->zt_part, ctx->sub_tiles, ctx->nsub, ctx->k,
+                                                             ctx->tvec, 0, ctx->Einv, ctx->K, ctx->t2, st,
+                                                             need_refresh, ctx->ticket);
         ctx->launches++;
         return DFL_OK;
     }
     // local entries into a padded slot, allgather, unpack, solve
     const int64_t slot = (int64_t)ctx->max_nsub * ctx->k;
     double *mine = ctx->tgather + (int64_t)ctx->rank * slot;
-    k_zt_finish<<<1, 256, 0, ctx->st>>>(ctx->zt_part, ctx->sub_tiles, ctx->nsub, ctx->k, mine, 0, nullptr, ctx->K,
-                                        nullptr, st, need_refresh);
+    k_zt_finish<<<ctx->nsub * ctx->k, 512, 0, ctx->st>>>(ctx->zt_part, ctx->sub_tiles, ctx->nsub, ctx->k, mine, 0,
+                                                         nullptr, ctx->K, nullptr, st, need_refresh, ctx->ticket);
     RC(nccl_check(ctx, g_nccl.AllGather(mine, ctx->tgather, slot, ncclDouble_, ctx->comm, ctx->st), "ncclAllGather"));
     // unpack rank slots into t: rank q owns a contiguous subdomain range
     int64_t pos = 0;
@@ -534,8 +536,8 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
         {
             const double *rb = L == 0 ? rin : g.rb;
             double *xb = L == 0 ? zout : g.xb;
-            const int threads = std::min(512, std::max(32, (g.max_nb + 31) / 32 * 32));
-            k_bottom<<<g.nsub, threads, sizeof(double) * g.max_nb, ctx->st>>>(g.binvT, g.binv_off, g.b_off, rb, xb, st);
+            k_bottom<<<g.nsub, 256, sizeof(double) * (g.max_nb + 256), ctx->st>>>(g.binvT, g.binv_off, g.b_off, rb,
+                                                                                   xb, st);
             ctx->launches++;
         }
         for (int l = L - 1; l >= 0; --l) {
@@ -862,7 +864,7 @@ static int build_groups(dfl_ctx *ctx) {
             RC(dalloc(ctx, &g.rb, g.nb));
             RC(dalloc(ctx, &g.xb, g.nb));
         }
-        if (g.max_nb > 6000) {
+        if (g.max_nb > 5800) {
             ctx->err = "bottom level too large for shared-memory staging";
             return DFL_E_DIMENSION;
         }
@@ -1177,6 +1179,8 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
     RC(dalloc(ctx, &ctx->scal, 16));
     RC(dalloc(ctx, &ctx->sgather, (int64_t)8 * ctx->nranks));
     RC(dalloc(ctx, &ctx->state, 1));
+    RC(dalloc(ctx, &ctx->ticket, 4));
+    CK(cudaMemset(ctx->ticket, 0, 4 * sizeof(unsigned int)));
     CK(cudaMemset(ctx->x, 0, sizeof(double) * nx));
     CK(cudaMemset(ctx->xin, 0, sizeof(double) * nx));
     CK(cudaMemset(ctx->p, 0, sizeof(double) * nx));
@@ -1204,7 +1208,8 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     CK(cudaEventRecord(e_h0, ctx->st));
     RC(stage_in(ctx, ctx->b, b, ptr_kind));
     CK(cudaEventRecord(ctx->ev0, ctx->st));
-    const bool use_graph = ctx->nranks == 1;
+    const char *ng = getenv("DFL_NO_GRAPH");
+    const bool use_graph = ctx->nranks == 1 && !(ng && ng[0] == '1');
     RC(cg_solve_dev(ctx, p, use_graph));
     CK(cudaEventRecord(ctx->ev1, ctx->st));
     CK(cudaMemcpyAsync(x, ctx->xin, sizeof(double) * ctx->n,

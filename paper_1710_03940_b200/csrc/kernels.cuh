@@ -217,22 +217,44 @@ __global__ void __launch_bounds__(kBlock) k_csr(DMat A, RowArgs a) {
 }
 
 // bottom level: x = inv(A_bottom) r per subdomain, inverse stored transposed
-// (column j contiguous) so that thread i reads coalesced; r staged in smem.
-__global__ void k_bottom(const double *__restrict__ invT, const int64_t *__restrict__ inv_off,
-                         const int64_t *__restrict__ off, const double *__restrict__ r,
-                         double *__restrict__ x, const KState *st) {
+// (column j contiguous) so that lanes read coalesced; r staged in smem.  The
+// j range is split over the warps (fixed split, deterministic) and the warp
+// partials are added in warp order.
+__global__ void __launch_bounds__(256) k_bottom(const double *__restrict__ invT, const int64_t *__restrict__ inv_off,
+                                                const int64_t *__restrict__ off, const double *__restrict__ r,
+                                                double *__restrict__ x, const KState *st) {
     if (skip(st)) return;
-    extern __shared__ double rs[];
+    extern __shared__ double sh[];
     const int s = blockIdx.x;
     const int64_t o = off[s];
     const int n = (int)(off[s + 1] - o);
     const double *M = invT + inv_off[s];
+    double *rs = sh;            // n
+    double *part = sh + n;      // 8 warps x 32 lanes
     for (int j = threadIdx.x; j < n; j += blockDim.x) rs[j] = r[o + j];
     __syncthreads();
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        double acc = 0.0;
-        for (int j = 0; j < n; ++j) acc = fma(M[(int64_t)j * n + i], rs[j], acc);
-        x[o + i] = acc;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int jchunk = (n + nw - 1) / nw;
+    const int j0 = warp * jchunk, j1 = min(n, j0 + jchunk);
+    for (int ib = 0; ib < n; ib += 32) {
+        const int i = ib + lane;
+        double a0 = 0.0, a1 = 0.0;
+        if (i < n) {
+            int j = j0;
+            for (; j + 1 < j1; j += 2) {
+                a0 = fma(M[(int64_t)j * n + i], rs[j], a0);
+                a1 = fma(M[(int64_t)(j + 1) * n + i], rs[j + 1], a1);
+            }
+            if (j < j1) a0 = fma(M[(int64_t)j * n + i], rs[j], a0);
+        }
+        part[warp * 32 + lane] = a0 + a1;
+        __syncthreads();
+        if (warp == 0 && i < n) {
+            double acc = 0.0;
+            for (int w = 0; w < nw; ++w) acc += part[w * 32 + lane];
+            x[o + i] = acc;
+        }
+        __syncthreads();
     }
 }
 
@@ -344,31 +366,44 @@ __global__ void __launch_bounds__(kBlock) k_zt_vec(Tiles T, const double *__rest
 }
 
 // Sum tile partials per local subdomain -> t (global coarse numbering at
-// first_col), then optionally t2 = E^{-1} t with the replicated inverse.
-// One block; warp w reduces values w, w+nwarps, ... in fixed order.
-__global__ void k_zt_finish(const double *__restrict__ zt_part, const int64_t *__restrict__ sub_tiles,
-                            int nsub, int k, double *t_out, int64_t first_col, const double *Einv,
-                            int64_t K, double *t2, const KState *st, int need_refresh) {
+// first_col); one block per coarse value, fixed-order strided sums + tree.
+// The last block to finish (atomic ticket) then solves t2 = E^{-1} t with
+// the replicated inverse (Einv == nullptr: skip, multi-rank path).
+__global__ void __launch_bounds__(512) k_zt_finish(const double *__restrict__ zt_part,
+                                                   const int64_t *__restrict__ sub_tiles, int nsub, int k,
+                                                   double *t_out, int64_t first_col, const double *Einv,
+                                                   int64_t K, double *t2, const KState *st, int need_refresh,
+                                                   unsigned int *ticket) {
     if (skip(st)) return;
     if (need_refresh && !st->refresh_now) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int v = warp; v < nsub * k; v += nw) {
-        const int s = v / k, c = v % k;
-        const int64_t t0 = sub_tiles[s], t1 = sub_tiles[s + 1];
-        double acc = 0.0;
-        for (int64_t t = t0 + lane; t < t1; t += 32) acc += zt_part[t * k + c];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
-        if (lane == 0) t_out[first_col + v] = acc;
+    const int v = blockIdx.x;
+    const int s = v / k, c = v % k;
+    const int64_t t0 = sub_tiles[s], t1 = sub_tiles[s + 1];
+    double acc = 0.0;
+    for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) acc += zt_part[t * k + c];
+    __shared__ double sm[32];
+    double val[1] = {acc};
+    block_sum<1>(val, sm);
+    if (Einv == nullptr) {
+        if (threadIdx.x == 0) t_out[first_col + v] = val[0];
+        return;
     }
-    if (Einv == nullptr) return;
+    __shared__ bool last;
+    if (threadIdx.x == 0) {
+        t_out[first_col + v] = val[0];
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
     __syncthreads();
-    __threadfence_block();
+    if (!last) return;
+    __threadfence();
+    const volatile double *tv = t_out;
     for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
-        double acc = 0.0;
-        for (int64_t j = 0; j < K; ++j) acc = fma(Einv[i * K + j], t_out[j], acc);
-        t2[i] = acc;
+        double a = 0.0;
+        for (int64_t j = 0; j < K; ++j) a = fma(Einv[i * K + j], tv[j], a);
+        t2[i] = a;
     }
+    if (threadIdx.x == 0) *ticket = 0u;
 }
 
 // t2 = E^{-1} t (multi-rank path, after the allgather of t)

@@ -353,18 +353,14 @@ class DeflatedSolver:
         (deflation.py:284); the plain block-AMG path starts from zero too."""
         name = self.cfg.get("solver.type")
         b_local = self._local(b)
-        params = nat.SolveParams(
-            nat.DFL_SOLVER[name],
-            int(self.cfg.get("solver.maxiter")),
-            50,
-            1 if self.deflated else 0,
-            float(self.cfg.get("solver.tol")),
-        )
+        params = _params(self)
         x_local = np.empty(self.n_local)
         t0 = time.perf_counter()
         rep = self._ctx.solve(params, b_local, x_local)
         wall = time.perf_counter() - t0
-        x = self._global(x_local)
+        # x comes back in the layout of b: global in, global out; a rank's
+        # own rows in, its own rows out (no gather)
+        x = x_local if np.shape(b)[0] == self.n_local and self.n_local != self.n else self._global(x_local)
         brk = nat.breakdown_string(rep.breakdown) if rep.breakdown else None
         report = {
             "solver": name,
@@ -389,6 +385,23 @@ class DeflatedSolver:
             "level_sizes": [h.level_sizes for h in self.hierarchies],
         }
         return x, report
+
+
+def _params(solver: "DeflatedSolver", maxiter=None):
+    cfg = solver.cfg
+    return nat.SolveParams(
+        nat.DFL_SOLVER[cfg.get("solver.type")],
+        int(cfg.get("solver.maxiter") if maxiter is None else maxiter),
+        50,
+        1 if solver.deflated else 0,
+        float(cfg.get("solver.tol")),
+    )
+
+
+def solve_device(solver: "DeflatedSolver", b_ptr: int, x_ptr: int):
+    """Solve with this rank's b and x already in device memory (raw CUDA
+    pointers, e.g. ``torch.Tensor.data_ptr()``); returns the native report."""
+    return solver._ctx.solve(_params(solver), b_ptr, x_ptr, nat.PTR_DEVICE)
 
 
 def solve_deflated(A, b, partition=None, *, config=None, coords=None, deflated=True, threads_per_subdomain=1):
