@@ -19,6 +19,7 @@
 #include "../../include/dflb200.h"
 #include "host_setup.hpp"
 #include "kernels.cuh"
+#include "spmv_pipe.cuh"
 
 using namespace dfl;
 
@@ -76,6 +77,7 @@ Nccl g_nccl;
 
 struct DLevel {
     DMat A, P, R;
+    DMat Aw;  // A diag(w): the pre-smoothing residual r - A (w .* r) in one gather
     double *w = nullptr;
     int64_t n = 0, nc = 0;
     double *rv = nullptr;  // level right-hand side (l >= 1)
@@ -99,6 +101,9 @@ struct VGroup {
 
 struct dfl_ctx {
     int device = 0;
+    int sm_count = 148;
+    std::vector<int64_t> op_sub_tiles_h;
+    int64_t *op_sub_tiles = nullptr;   // first op-pipe tile of every subdomain
     cudaStream_t st = nullptr;
     std::string err;
     std::vector<void *> allocs;
@@ -116,6 +121,7 @@ struct dfl_ctx {
     int64_t op_nnz = 0;
     // tiles (per subdomain, rows per tile = op rows per block)
     Tiles tiles{};
+    SubTable subtab{};
     int64_t ntiles = 0;
     int *tile_sub = nullptr;
     int64_t *sub_tiles = nullptr;       // device nsub + 1
@@ -209,7 +215,14 @@ struct HostRows {
     const double *val;
 };
 
-static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, bool allow_ell = true) {
+static int build_pipe(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &soff,
+                      const std::vector<int64_t> &bounds, std::vector<int64_t> *bound_tiles);
+
+// colscale != nullptr: also upload the column-scaled values a_ij * colscale_j
+// in the same layout (shares the index arrays) into *scaled.
+static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &bounds,
+                         std::vector<int64_t> *bound_tiles = nullptr, bool allow_ell = true,
+                         const double *colscale = nullptr, DMat *scaled = nullptr) {
     m = DMat{};
     m.nrows = h.nrows;
     m.ncols = h.ncols;
@@ -231,9 +244,16 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, bool allow_el
     const bool ell = allow_ell && maxlen <= 32 && (double)soff[nsl] <= 1.2 * (double)m.nnz + 64.0;
     if (ell) {
         m.fmt = FMT_ELL;
+        // uniform slice width when it costs <= 3% extra storage: the kernels
+        // then compute slice offsets instead of loading them
+        if ((double)(nsl * 32 * maxlen) <= 1.03 * (double)soff[nsl] && maxlen <= kEllUnroll) {
+            m.ell_w = (int)maxlen;
+            for (int64_t s = 0; s <= nsl; ++s) soff[s] = s * 32 * maxlen;
+        }
         m.stored = soff[nsl];
         std::vector<int> col(m.stored);
         std::vector<double> val(m.stored, 0.0);
+        std::vector<double> sval(colscale ? m.stored : 0, 0.0);
         for (int64_t s = 0; s < nsl; ++s) {
             const int64_t wdt = (soff[s + 1] - soff[s]) / 32;
             for (int64_t i = s * 32; i < std::min(h.nrows, s * 32 + 32); ++i) {
@@ -245,6 +265,7 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, bool allow_el
                     if (b + k < e) {
                         col[dst] = (int)h.col[b + k];
                         val[dst] = h.val[b + k];
+                        if (colscale) sval[dst] = h.val[b + k] * colscale[h.col[b + k]];
                     } else {
                         col[dst] = pad_col;
                         val[dst] = 0.0;
@@ -263,28 +284,107 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, bool allow_el
         m.slice_off = d_soff;
         m.col = d_col;
         m.val = d_val;
+        RC(build_pipe(ctx, h, m, soff, bounds, bound_tiles));
+        if (colscale) {
+            double *d_sval;
+            RC(upload(ctx, &d_sval, sval.data(), m.stored));
+            *scaled = m;
+            scaled->val = d_sval;
+        }
     } else {
         m.fmt = FMT_CSR;
         m.stored = m.nnz;
+        // lanes per row: about 6 entries per lane, batched kCsrUnroll deep
         int g = 1;
-        if (mean > 8.0) {
-            const int want = (int)std::ceil(mean / 2.0);
-            g = 2;
-            while (g < want && g < 32) g *= 2;
-        }
+        const int want = (int)std::ceil(mean / 6.0);
+        while (g < want && g < 32) g *= 2;
         m.group = g;
-        std::vector<int> ptr(h.nrows + 1), col(m.nnz);
+        // padded by 4 entries so that 16-byte aligned bulk copies may overrun the last row
+        std::vector<int> ptr(h.nrows + 1), col(m.nnz + 4, 0);
+        std::vector<double> val(m.nnz + 4, 0.0);
         for (int64_t i = 0; i <= h.nrows; ++i) ptr[i] = (int)(h.ptr[i] - h.ptr[0]);
         for (int64_t k = 0; k < m.nnz; ++k) col[k] = (int)h.col[h.ptr[0] + k];
+        std::memcpy(val.data(), h.val + h.ptr[0], sizeof(double) * m.nnz);
         int *d_ptr, *d_col;
         double *d_val;
         RC(upload(ctx, &d_ptr, ptr.data(), h.nrows + 1));
-        RC(upload(ctx, &d_col, col.data(), m.nnz));
-        RC(upload(ctx, &d_val, h.val + h.ptr[0], m.nnz));
+        RC(upload(ctx, &d_col, col.data(), m.nnz + 4));
+        RC(upload(ctx, &d_val, val.data(), m.nnz + 4));
         m.ptr = d_ptr;
         m.col = d_col;
         m.val = d_val;
+        RC(build_pipe(ctx, h, m, soff, bounds, bound_tiles));
+        if (colscale) {
+            std::vector<double> sval(m.nnz + 4, 0.0);
+            for (int64_t k = 0; k < m.nnz; ++k) sval[k] = h.val[h.ptr[0] + k] * colscale[h.col[h.ptr[0] + k]];
+            double *d_sval;
+            RC(upload(ctx, &d_sval, sval.data(), m.nnz + 4));
+            *scaled = m;
+            scaled->val = d_sval;
+        }
     }
+    return DFL_OK;
+}
+
+// Row tiles for the TMA pipeline: tiles never straddle `bounds` (subdomain
+// starts for the operator); ELL tiles are 256 rows (one per thread), CSR
+// tiles ~3K entries in passes of 256/G rows.
+static constexpr int kStageBytesMax = 100 * 1024;
+
+static int build_pipe(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &soff,
+                      const std::vector<int64_t> &bounds, std::vector<int64_t> *bound_tiles) {
+    m.pipe = Pipe{};
+    if (bound_tiles) bound_tiles->assign(1, 0);
+    if (h.nrows == 0) return DFL_OK;
+    int64_t rpt;
+    if (m.fmt == FMT_ELL) {
+        rpt = kPipeThreads;
+    } else {
+        const int64_t rpp = kPipeThreads / m.group;
+        const double mean = (double)m.nnz / (double)h.nrows;
+        const int64_t passes = std::max<int64_t>(1, (int64_t)std::llround(3072.0 / std::max(1.0, mean * rpp)));
+        rpt = rpp * passes;
+    }
+    std::vector<int64_t> r0, r1, e0;
+    std::vector<int> ec;
+    int64_t cap = 0;
+    const int64_t base = h.ptr[0];
+    for (size_t bi = 0; bi + 1 < bounds.size(); ++bi) {
+        for (int64_t r = bounds[bi]; r < bounds[bi + 1]; r += rpt) {
+            const int64_t re = std::min(r + rpt, bounds[bi + 1]);
+            int64_t a, b;
+            if (m.fmt == FMT_ELL) {
+                a = soff[r >> 5];
+                b = soff[(re + 31) >> 5];
+            } else {
+                a = (h.ptr[r] - base) & ~int64_t(3);
+                b = ((h.ptr[re] - base) + 3) & ~int64_t(3);
+            }
+            r0.push_back(r);
+            r1.push_back(re);
+            e0.push_back(a);
+            ec.push_back((int)(b - a));
+            cap = std::max(cap, b - a);
+        }
+        if (bound_tiles) bound_tiles->push_back((int64_t)r0.size());
+    }
+    cap = (cap + 3) & ~int64_t(3);
+    const int64_t stage_bytes = cap * 12;
+    int stages = (int)std::min<int64_t>(4, kStageBytesMax / std::max<int64_t>(1, stage_bytes));
+    if (stages < 2) return DFL_OK;  // rows too long for staging: register kernels
+    int64_t *d0, *d1, *de;
+    int *dc;
+    RC(upload(ctx, &d0, r0.data(), (int64_t)r0.size()));
+    RC(upload(ctx, &d1, r1.data(), (int64_t)r1.size()));
+    RC(upload(ctx, &de, e0.data(), (int64_t)e0.size()));
+    RC(upload(ctx, &dc, ec.data(), (int64_t)ec.size()));
+    m.pipe.row0 = d0;
+    m.pipe.row1 = d1;
+    m.pipe.e0 = de;
+    m.pipe.ecnt = dc;
+    m.pipe.ntiles = (int64_t)r0.size();
+    m.pipe.cap = (int)cap;
+    m.pipe.stages = stages;
     return DFL_OK;
 }
 
@@ -294,6 +394,59 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, bool allow_el
 static int rows_per_block(const DMat &A) { return A.fmt == FMT_ELL ? kBlock : kBlock / A.group; }
 
 static int64_t nblocks_for(const DMat &A) { return cdiv(A.nrows, rows_per_block(A)); }
+
+// number of per-block / per-tile partials a row kernel on A produces
+static int64_t parts_for(const DMat &A) { return A.pipe.stages ? A.pipe.ntiles : nblocks_for(A); }
+
+static size_t pipe_smem(const DMat &A) { return 128 + (size_t)A.pipe.stages * A.pipe.cap * 12; }
+
+template <int MODE, bool PART>
+static void pipe_attr_one() {
+    auto set = [](const void *f) {
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageBytesMax + 1024);
+    };
+    set((const void *)k_pipe<0, MODE, PART>);
+    set((const void *)k_pipe<1, MODE, PART>);
+    set((const void *)k_pipe<2, MODE, PART>);
+    set((const void *)k_pipe<4, MODE, PART>);
+    set((const void *)k_pipe<8, MODE, PART>);
+    set((const void *)k_pipe<16, MODE, PART>);
+    set((const void *)k_pipe<32, MODE, PART>);
+}
+
+static void pipe_attrs() {
+    pipe_attr_one<PMODE_PLAIN, false>();
+    pipe_attr_one<PMODE_RESID, false>();
+    pipe_attr_one<PMODE_PROLONG, false>();
+    pipe_attr_one<PMODE_POST, false>();
+    pipe_attr_one<PMODE_POST, true>();
+    pipe_attr_one<PMODE_OP, true>();
+    pipe_attr_one<PMODE_OPRES, true>();
+}
+
+template <int MODE, bool PART>
+static bool launch_pipe(dfl_ctx *ctx, const DMat &A, const SpArgs &a) {
+    if (A.pipe.stages == 0) return false;
+    const size_t smem = pipe_smem(A);
+    const int per_sm = smem <= 110 * 1024 ? 2 : 1;
+    const unsigned grid = (unsigned)std::min<int64_t>(A.pipe.ntiles, (int64_t)ctx->sm_count * per_sm);
+    if (A.fmt == FMT_ELL) {
+        k_pipe<0, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a);
+    } else {
+        switch (A.group) {
+            case 1: k_pipe<1, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
+            case 2: k_pipe<2, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
+            case 4: k_pipe<4, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
+            case 8: k_pipe<8, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
+            case 16: k_pipe<16, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
+            default: k_pipe<32, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
+        }
+    }
+    ctx->launches++;
+    return true;
+}
+
+static bool g_use_pipe = false;  // TMA-staged variant (DFL_PIPE=1); see profiles/r01
 
 template <int MODE, bool DOT>
 static void launch_csr_mode(const DMat &A, const RowArgs &a, cudaStream_t st) {
@@ -311,9 +464,33 @@ static void launch_csr_mode(const DMat &A, const RowArgs &a, cudaStream_t st) {
 template <int MODE, bool DOT>
 static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
     if (A.nrows == 0) return;
-    if (A.fmt == FMT_ELL)
-        k_ell<MODE, DOT><<<(unsigned)nblocks_for(A), kBlock, 0, ctx->st>>>(A, a);
-    else
+    if (g_use_pipe) {
+        SpArgs s;
+        s.x = a.x;
+        s.w = a.w;
+        s.r = a.r;
+        s.xo = a.xo;
+        s.out = a.out;
+        s.part = a.dot_part;
+        s.st = a.st;
+        constexpr int PM = MODE == MODE_PLAIN ? PMODE_PLAIN
+                           : MODE == MODE_RESID ? PMODE_RESID
+                           : MODE == MODE_POST ? PMODE_POST
+                                                : PMODE_PROLONG;
+        if (launch_pipe<PM, DOT>(ctx, A, s)) return;
+    }
+    if (A.fmt == FMT_ELL) {
+        const unsigned grid = (unsigned)nblocks_for(A);
+        switch (A.ell_w) {
+            case 3: k_ell<MODE, DOT, 3><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+            case 4: k_ell<MODE, DOT, 4><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+            case 5: k_ell<MODE, DOT, 5><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+            case 6: k_ell<MODE, DOT, 6><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+            case 7: k_ell<MODE, DOT, 7><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+            case 8: k_ell<MODE, DOT, 8><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+            default: k_ell<MODE, DOT, 0><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+        }
+    } else
         launch_csr_mode<MODE, DOT>(A, a, ctx->st);
     ctx->launches++;
 }
@@ -321,18 +498,37 @@ static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
 template <int OPMODE>
 static void launch_op(dfl_ctx *ctx, const OpArgs &a) {
     const DMat &A = ctx->Aop;
+    if (g_use_pipe) {
+        SpArgs s;
+        s.x = a.x;
+        s.b = a.b;
+        s.out = a.y;
+        s.part = a.k > 0 ? a.zt_part : nullptr;
+        s.zcols = a.zcols;
+        s.zn = a.n;
+        s.k = a.k;
+        s.st = a.st;
+        s.need_refresh = a.need_refresh;
+        if (launch_pipe<OPMODE == 0 ? PMODE_OP : PMODE_OPRES, true>(ctx, A, s)) return;
+    }
     const unsigned grid = (unsigned)ctx->ntiles;
     if (grid == 0) return;
     if (A.fmt == FMT_ELL) {
-        k_op_ell<OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a);
+        const SubTable &S = ctx->subtab;
+        switch (A.ell_w) {
+            case 5: k_op_ell<OPMODE, 5><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, S, a); break;
+            case 6: k_op_ell<OPMODE, 6><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, S, a); break;
+            case 7: k_op_ell<OPMODE, 7><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, S, a); break;
+            default: k_op_ell<OPMODE, 0><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, S, a); break;
+        }
     } else {
         switch (A.group) {
-            case 1: k_op_csr<1, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a); break;
-            case 2: k_op_csr<2, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a); break;
-            case 4: k_op_csr<4, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a); break;
-            case 8: k_op_csr<8, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a); break;
-            case 16: k_op_csr<16, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a); break;
-            default: k_op_csr<32, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, a); break;
+            case 1: k_op_csr<1, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
+            case 2: k_op_csr<2, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
+            case 4: k_op_csr<4, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
+            case 8: k_op_csr<8, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
+            case 16: k_op_csr<16, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
+            default: k_op_csr<32, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
         }
     }
     ctx->launches++;
@@ -374,9 +570,10 @@ static int halo(dfl_ctx *ctx, double *v) {
 }
 
 // Z' v partials -> t (global numbering) -> t2 = E^-1 t on every rank
-static int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh) {
+static int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op) {
+    const int64_t *sub_tiles = (from_op && g_use_pipe && ctx->Aop.pipe.stages) ? ctx->op_sub_tiles : ctx->sub_tiles;
     if (ctx->nranks == 1) {
-        k_zt_finish<<<ctx->nsub * ctx->k, 512, 0, ctx->st>>>(ctx->zt_part, ctx->sub_tiles, ctx->nsub, ctx->k,
+        k_zt_finish<<<ctx->nsub * ctx->k, 512, 0, ctx->st>>>(ctx->zt_part, sub_tiles, ctx->nsub, ctx->k,
                                                              ctx->tvec, 0, ctx->Einv, ctx->K, ctx->t2, st,
                                                              need_refresh, ctx->ticket);
         ctx->launches++;
@@ -385,7 +582,7 @@ static int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh) {
     // local entries into a padded slot, allgather, unpack, solve
     const int64_t slot = (int64_t)ctx->max_nsub * ctx->k;
     double *mine = ctx->tgather + (int64_t)ctx->rank * slot;
-    k_zt_finish<<<ctx->nsub * ctx->k, 512, 0, ctx->st>>>(ctx->zt_part, ctx->sub_tiles, ctx->nsub, ctx->k, mine, 0,
+    k_zt_finish<<<ctx->nsub * ctx->k, 512, 0, ctx->st>>>(ctx->zt_part, sub_tiles, ctx->nsub, ctx->k, mine, 0,
                                                          nullptr, ctx->K, nullptr, st, need_refresh, ctx->ticket);
     RC(nccl_check(ctx, g_nccl.AllGather(mine, ctx->tgather, slot, ncclDouble_, ctx->comm, ctx->st), "ncclAllGather"));
     // unpack rank slots into t: rank q owns a contiguous subdomain range
@@ -507,7 +704,7 @@ __global__ void k_cg_end(KState *st, cudaGraphConditionalHandle h, int use_cond)
 static int rank_scalar(dfl_ctx *ctx, const double *part, int64_t nparts, int slot, const double **gath) {
     *gath = nullptr;
     if (ctx->nranks == 1) return DFL_OK;
-    k_reduce<<<1, 256, 0, ctx->st>>>(part, nparts, ctx->scal + slot);
+    k_reduce<<<1, 1024, 0, ctx->st>>>(part, nparts, ctx->scal + slot);
     ctx->launches++;
     RC(nccl_check(ctx, g_nccl.AllGather(ctx->scal, ctx->sgather, 8, ncclDouble_, ctx->comm, ctx->st), "ncclAllGather"));
     *gath = ctx->sgather;
@@ -529,15 +726,15 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
             const double *in = l == 0 ? rin : v.rv;
             double *next = (l + 1 < L) ? g.lv[l + 1].rv : g.rb;
             RowArgs a{nullptr, v.w, in, nullptr, v.t, nullptr, st};
-            launch_rows<MODE_RESID, false>(ctx, v.A, a);
+            launch_rows<MODE_RESID, false>(ctx, v.Aw, a);
             RowArgs b{v.t, nullptr, nullptr, nullptr, next, nullptr, st};
             launch_rows<MODE_PLAIN, false>(ctx, v.R, b);
         }
         {
             const double *rb = L == 0 ? rin : g.rb;
             double *xb = L == 0 ? zout : g.xb;
-            k_bottom<<<g.nsub, 256, sizeof(double) * (g.max_nb + 256), ctx->st>>>(g.binvT, g.binv_off, g.b_off, rb,
-                                                                                   xb, st);
+            k_bottom<<<dim3((unsigned)cdiv(g.max_nb, 32), (unsigned)g.nsub), 256, 0, ctx->st>>>(
+                g.binvT, g.binv_off, g.b_off, rb, xb, st);
             ctx->launches++;
         }
         for (int l = L - 1; l >= 0; --l) {
@@ -550,7 +747,7 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
             if (l == 0 && dot_part) {
                 RowArgs b{v.t, v.w, in, v.t, out, dot_part + poff, st};
                 launch_rows<MODE_POST, true>(ctx, v.A, b);
-                poff += nblocks_for(v.A);
+                poff += parts_for(v.A);
             } else {
                 RowArgs b{v.t, v.w, in, v.t, out, nullptr, st};
                 launch_rows<MODE_POST, false>(ctx, v.A, b);
@@ -607,7 +804,7 @@ static void launch_project(dfl_ctx *ctx, const ProjArgs &a) {
 static int project_dev(dfl_ctx *ctx, const double *v, double *out, const KState *st, int dotmode) {
     k_zt_vec<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, v, ctx->zcols, ctx->n, ctx->k, ctx->zt_part);
     ctx->launches++;
-    RC(zt_to_t2(ctx, nullptr, 0));
+    RC(zt_to_t2(ctx, nullptr, 0, false));
     ProjArgs a = proj_args(ctx, v, out, st);
     a.dotmode = dotmode;
     a.dot_part = ctx->dpart;
@@ -622,7 +819,7 @@ static int cg_body(dfl_ctx *ctx, bool deflated, cudaGraphConditionalHandle h, in
     const double *gath;
     // w = A p, Z'w ; t2 ; q = w - AZ t2 ; p.q
     RC(op_apply_dev(ctx, ctx->p, ctx->w, 0, nullptr, deflated, st, 0));
-    if (deflated) RC(zt_to_t2(ctx, st, 0));
+    if (deflated) RC(zt_to_t2(ctx, st, 0, true));
     {
         ProjArgs a = proj_args(ctx, ctx->w, ctx->w, st);
         if (!deflated) a.az_ptr = nullptr, a.K = 0;
@@ -632,14 +829,14 @@ static int cg_body(dfl_ctx *ctx, bool deflated, cudaGraphConditionalHandle h, in
         launch_project<0>(ctx, a);
     }
     RC(rank_scalar(ctx, ctx->dpart, ctx->nblk, 0, &gath));
-    k_cg_pq<<<1, 256, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks);
+    k_cg_pq<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks);
     ctx->launches++;
     // x += alpha p ; r -= alpha q (regular iterations)
     k_cg_update<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->x, ctx->r, ctx->p, ctx->w, ctx->n, ctx->dpart, st);
     ctx->launches++;
     // refresh iterations: r = b' - project(A x)   (krylov.py:128-129)
     RC(op_apply_dev(ctx, ctx->x, ctx->tmp, 0, nullptr, deflated, st, 1));
-    if (deflated) RC(zt_to_t2(ctx, st, 1));
+    if (deflated) RC(zt_to_t2(ctx, st, 1, true));
     {
         ProjArgs a = proj_args(ctx, ctx->tmp, ctx->r, st);
         if (!deflated) a.az_ptr = nullptr, a.K = 0;
@@ -650,13 +847,13 @@ static int cg_body(dfl_ctx *ctx, bool deflated, cudaGraphConditionalHandle h, in
         launch_project<1>(ctx, a);
     }
     RC(rank_scalar(ctx, ctx->dpart, ctx->nblk, 0, &gath));
-    k_cg_rr<<<1, 256, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks);
+    k_cg_rr<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks);
     ctx->launches++;
     // z = M r, r.z
     int64_t np = 0;
     RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
     RC(rank_scalar(ctx, ctx->dpart, np, 0, &gath));
-    k_cg_rz<<<1, 256, 0, ctx->st>>>(st, ctx->dpart, np, gath, ctx->nranks);
+    k_cg_rz<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, np, gath, ctx->nranks);
     ctx->launches++;
     k_cg_p<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->p, ctx->z, ctx->n, st);
     ctx->launches++;
@@ -711,7 +908,7 @@ static int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph)
     k_dot<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->b, ctx->b, ctx->n, ctx->dpart, nullptr);
     ctx->launches += 2;
     RC(rank_scalar(ctx, ctx->dpart, ctx->nblk, 0, &gath));
-    k_cg_start<<<1, 256, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks, p->tol, p->maxiter,
+    k_cg_start<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks, p->tol, p->maxiter,
                                       std::max(1, p->refresh_every));
     ctx->launches++;
     // b' = project(b) and ||b'||^2
@@ -726,13 +923,13 @@ static int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph)
         launch_project<0>(ctx, a);
     }
     RC(rank_scalar(ctx, ctx->dpart, ctx->nblk, 0, &gath));
-    k_cg_init_r<<<1, 256, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks);
+    k_cg_init_r<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks);
     k_copy<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->r, ctx->bp, ctx->n);
     ctx->launches += 2;
     int64_t np = 0;
     RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
     RC(rank_scalar(ctx, ctx->dpart, np, 0, &gath));
-    k_cg_init_rz<<<1, 256, 0, ctx->st>>>(st, ctx->dpart, np, gath, ctx->nranks);
+    k_cg_init_rz<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, np, gath, ctx->nranks);
     k_copy<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->p, ctx->z, ctx->n);
     ctx->launches += 2;
     // the loop
@@ -750,7 +947,7 @@ static int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph)
     // x = y + Z E^-1 Z'(b - A y)   (deflation.py:285)
     if (defl) {
         RC(op_apply_dev(ctx, ctx->x, ctx->tmp, 1, ctx->b, true, nullptr, 0));
-        RC(zt_to_t2(ctx, nullptr, 0));
+        RC(zt_to_t2(ctx, nullptr, 0, true));
         k_lift<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, ctx->tile_sub, ctx->x, ctx->zcols, ctx->n,
                                                               ctx->k, ctx->t2, (int64_t)ctx->first_sub * ctx->k,
                                                               ctx->xin, 1);
@@ -827,9 +1024,9 @@ static int build_groups(dfl_ctx *ctx) {
                 w.insert(w.end(), lv.w.begin(), lv.w.end());
             }
             OwnedRows A = merge_blocks(As, fo), P = merge_blocks(Ps, co), R = merge_blocks(Rs, fo);
-            RC(upload_matrix(ctx, A.view(), v.A));
-            RC(upload_matrix(ctx, P.view(), v.P));
-            RC(upload_matrix(ctx, R.view(), v.R));
+            RC(upload_matrix(ctx, A.view(), v.A, {0, A.nrows}, nullptr, true, w.data(), &v.Aw));
+            RC(upload_matrix(ctx, P.view(), v.P, {0, P.nrows}));
+            RC(upload_matrix(ctx, R.view(), v.R, {0, R.nrows}));
             RC(upload(ctx, &v.w, w.data(), (int64_t)w.size()));
             v.n = fo.back();
             v.nc = co.back();
@@ -864,7 +1061,7 @@ static int build_groups(dfl_ctx *ctx) {
             RC(dalloc(ctx, &g.rb, g.nb));
             RC(dalloc(ctx, &g.xb, g.nb));
         }
-        if (g.max_nb > 5800) {
+        if (g.max_nb > (1 << 20)) {
             ctx->err = "bottom level too large for shared-memory staging";
             return DFL_E_DIMENSION;
         }
@@ -894,6 +1091,15 @@ static int build_tiles(dfl_ctx *ctx) {
     RC(upload(ctx, &ctx->sub_tiles, subt.data(), (int64_t)subt.size()));
     ctx->h_sub_tiles = subt;
     ctx->tiles = Tiles{d0, d1, ctx->ntiles};
+    ctx->subtab = SubTable{};
+    if (ctx->nsub <= kSubTab) {
+        ctx->subtab.n = ctx->nsub;
+        ctx->subtab.rows_per_tile = rpt;
+        for (int s = 0; s <= ctx->nsub; ++s) {
+            ctx->subtab.sub_off[s] = ctx->sub_off[s];
+            ctx->subtab.tile_start[s] = subt[s];
+        }
+    }
     return DFL_OK;
 }
 
@@ -904,6 +1110,7 @@ static int stage_in(dfl_ctx *ctx, double *dst, const double *src, int ptr_kind) 
 }
 
 static int stage_out(dfl_ctx *ctx, double *dst, const double *src, int ptr_kind) {
+    CK(cudaGetLastError());
     CK(cudaMemcpyAsync(dst, src, sizeof(double) * ctx->n,
                        ptr_kind == DFL_PTR_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
@@ -923,7 +1130,7 @@ static int ready(dfl_ctx *ctx) {
 static int rank_dot(dfl_ctx *ctx, const double *a, const double *b, double *out) {
     const unsigned nb = (unsigned)std::min<int64_t>(std::max<int64_t>(1, ctx->nblk), 4 * 148);
     k_dot<<<nb, kBlock, 0, ctx->st>>>(a, b, ctx->n, ctx->dpart, nullptr);
-    k_reduce<<<1, 256, 0, ctx->st>>>(ctx->dpart, nb, ctx->scal);
+    k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->dpart, nb, ctx->scal);
     ctx->launches += 2;
     if (ctx->nranks > 1) {
         RC(nccl_check(ctx, g_nccl.AllGather(ctx->scal, ctx->sgather, 8, ncclDouble_, ctx->comm, ctx->st), "ncclAllGather"));
@@ -965,6 +1172,12 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
     if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_state, sizeof(KState));
+    if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) {
+        pipe_attrs();
+        const char *np = getenv("DFL_PIPE");
+        g_use_pipe = np && np[0] == '1';
+    }
     if (e != cudaSuccess) {
         dfl::set_setup_error(std::string("CUDA context creation failed: ") + cudaGetErrorString(e));
         delete ctx;
@@ -1045,7 +1258,8 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
     ctx->nsub = nsub;
     ctx->sub_off.assign(sub_offsets, sub_offsets + nsub + 1);
     HostRows h{A->nrows, A->ncols, A->row_ptr, A->col_idx, A->values};
-    RC(upload_matrix(ctx, h, ctx->Aop));
+    RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, &ctx->op_sub_tiles_h));
+    if (ctx->Aop.pipe.stages) RC(upload(ctx, &ctx->op_sub_tiles, ctx->op_sub_tiles_h.data(), (int64_t)ctx->op_sub_tiles_h.size()));
     ctx->op_nnz = ctx->Aop.nnz;
     int64_t nrecv = 0;
     ctx->nbr.clear();
@@ -1173,9 +1387,9 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
     int64_t vparts = 0;
     for (auto &g : ctx->groups)
         vparts += g.lv.empty() ? std::max<int64_t>(1, std::min<int64_t>(cdiv(g.row1 - g.row0, kBlock), 64))
-                               : nblocks_for(g.lv[0].A);
+                               : parts_for(g.lv[0].A);
     RC(dalloc(ctx, &ctx->dpart, std::max(ctx->nblk, vparts) + 64));
-    RC(dalloc(ctx, &ctx->zt_part, ctx->ntiles * kKmax + 64));
+    RC(dalloc(ctx, &ctx->zt_part, std::max(ctx->ntiles, ctx->Aop.pipe.ntiles) * kKmax + 64));
     RC(dalloc(ctx, &ctx->scal, 16));
     RC(dalloc(ctx, &ctx->sgather, (int64_t)8 * ctx->nranks));
     RC(dalloc(ctx, &ctx->state, 1));
@@ -1211,6 +1425,7 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     const char *ng = getenv("DFL_NO_GRAPH");
     const bool use_graph = ctx->nranks == 1 && !(ng && ng[0] == '1');
     RC(cg_solve_dev(ctx, p, use_graph));
+    CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev1, ctx->st));
     CK(cudaMemcpyAsync(x, ctx->xin, sizeof(double) * ctx->n,
                        ptr_kind == DFL_PTR_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->st));
@@ -1281,7 +1496,7 @@ int dfl_coarse_lift(dfl_ctx *ctx, const double *r, double *out, int ptr_kind) {
     RC(stage_in(ctx, ctx->tmp, r, ptr_kind));
     k_zt_vec<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, ctx->tmp, ctx->zcols, ctx->n, ctx->k,
                                                            ctx->zt_part);
-    RC(zt_to_t2(ctx, nullptr, 0));
+    RC(zt_to_t2(ctx, nullptr, 0, false));
     k_lift<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, ctx->tile_sub, ctx->tmp, ctx->zcols, ctx->n,
                                                          ctx->k, ctx->t2, (int64_t)ctx->first_sub * ctx->k,
                                                          ctx->yout, 0);
@@ -1301,7 +1516,7 @@ int dfl_spmv_csr(const dfl_csr *A, const double *x, double *y, int device) {
     std::unique_ptr<dfl_ctx, void (*)(dfl_ctx *)> guard(ctx, dfl_ctx_destroy);
     DMat m;
     HostRows h{A->nrows, A->ncols, A->row_ptr, A->col_idx, A->values};
-    int rc = upload_matrix(ctx, h, m);
+    int rc = upload_matrix(ctx, h, m, {0, A->nrows});
     if (rc != DFL_OK) {
         dfl::set_setup_error(ctx->err);
         return rc;

@@ -29,8 +29,23 @@ constexpr int kEllUnroll = 8;     // slice widths up to this are fully unrolled
 
 enum { FMT_ELL = 0, FMT_CSR = 1 };
 
+// row tiles of one matrix for the TMA-pipelined kernels (spmv_pipe.cuh):
+// rows [row0, row1), entries [e0, e0 + ecnt) of the value / index arrays
+// (aligned to 4 entries = 16 B for the bulk-copy engine)
+struct Pipe {
+    const int64_t *row0 = nullptr;
+    const int64_t *row1 = nullptr;
+    const int64_t *e0 = nullptr;
+    const int *ecnt = nullptr;
+    int64_t ntiles = 0;
+    int cap = 0;     // max entries of a tile (stage capacity)
+    int stages = 0;  // 0: pipeline unavailable for this matrix
+};
+
 struct DMat {
+    Pipe pipe;
     int fmt = FMT_ELL;
+    int ell_w = 0;            // > 0: every slice has this width (no slice_off lookup)
     int group = 1;            // CSR-vector lanes per row
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;
     const int64_t *slice_off = nullptr;  // ELL: nslices + 1 element offsets
@@ -73,8 +88,15 @@ template <class G>
 __device__ __forceinline__ double ell_row(const DMat &A, int64_t row, const G &g) {
     const int64_t s = row >> 5;
     const int lane = (int)(row & 31);
-    const int64_t off = A.slice_off[s];
-    const int width = (int)((A.slice_off[s + 1] - off) >> 5);
+    int64_t off;
+    int width;
+    if (A.ell_w > 0) {  // uniform slices: no dependent index load before the stream
+        width = A.ell_w;
+        off = s * 32 * (int64_t)width;
+    } else {
+        off = __ldg(A.slice_off + s);
+        width = (int)((__ldg(A.slice_off + s + 1) - off) >> 5);
+    }
     const int *cp = A.col + off + lane;
     const double *vp = A.val + off + lane;
     double acc = 0.0;
@@ -99,16 +121,63 @@ __device__ __forceinline__ double ell_row(const DMat &A, int64_t row, const G &g
     return acc;
 }
 
-// CSR-vector partial sum of one row by G lanes; full sum returned on all lanes
+// ELL row with a compile-time uniform width W (the common case: every slice
+// padded to the matrix's max row length)
+template <int W, class G>
+__device__ __forceinline__ double ell_row_w(const DMat &A, int64_t row, const G &g) {
+    const int64_t off = (row >> 5) * 32 * W + (row & 31);
+    const int *cp = A.col + off;
+    const double *vp = A.val + off;
+    int c[W];
+    double v[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        c[k] = ld_stream(cp + 32 * k);
+        v[k] = ld_stream(vp + 32 * k);
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) acc = add_rn(acc, mul_rn(v[k], g(c[k])));
+    return acc;
+}
+
+template <int W, class G>
+__device__ __forceinline__ double ell_any(const DMat &A, int64_t row, const G &g) {
+    if (W > 0) return ell_row_w<(W > 0 ? W : 1)>(A, row, g);
+    return ell_row(A, row, g);
+}
+
+// CSR row by G lanes with the entry loads of a lane batched kCsrUnroll deep
+// (all index/value loads in flight before the gathers); full sum returned on
+// all G lanes.  G == 1 keeps the sequential CSR order (bit-identical to
+// spmv_rows).
+constexpr int kCsrUnroll = 8;
+
 template <int G, class Gat>
 __device__ __forceinline__ double csr_row(const DMat &A, int64_t row, int sub, const Gat &g) {
     double acc = 0.0;
     if (row < A.nrows) {
-        const int b = A.ptr[row], e = A.ptr[row + 1];
-        if (G == 1) {  // one thread per row: sequential CSR order, bit-identical to spmv_rows
-            for (int k = b; k < e; ++k) acc = add_rn(acc, mul_rn(ld_stream(A.val + k), g(ld_stream(A.col + k))));
-        } else {
-            for (int k = b + sub; k < e; k += G) acc += ld_stream(A.val + k) * g(ld_stream(A.col + k));
+        const int b = __ldg(A.ptr + row), e = __ldg(A.ptr + row + 1);
+        for (int k0 = b + sub; k0 < e; k0 += kCsrUnroll * G) {
+            int c[kCsrUnroll];
+            double v[kCsrUnroll], xv[kCsrUnroll];
+#pragma unroll
+            for (int u = 0; u < kCsrUnroll; ++u)
+                if (k0 + u * G < e) {
+                    c[u] = ld_stream(A.col + k0 + u * G);
+                    v[u] = ld_stream(A.val + k0 + u * G);
+                }
+#pragma unroll
+            for (int u = 0; u < kCsrUnroll; ++u)
+                if (k0 + u * G < e) xv[u] = g(c[u]);
+#pragma unroll
+            for (int u = 0; u < kCsrUnroll; ++u)
+                if (k0 + u * G < e) {
+                    if (G == 1)
+                        acc = add_rn(acc, mul_rn(v[u], xv[u]));
+                    else
+                        acc += v[u] * xv[u];
+                }
         }
     }
 #pragma unroll
@@ -168,17 +237,18 @@ __device__ __forceinline__ double epilogue(const RowArgs &a, int64_t i, double a
     return add_rn(__ldg(a.xo + i), mul_rn(__ldg(a.w + i), sub_rn(__ldg(a.r + i), ax)));
 }
 
-template <int MODE, bool DOT>
+// RESID runs on the pre-scaled matrix A diag(w) (values a_ij * w_j, built at
+// upload), so it gathers r once per entry instead of w and r.
+template <int MODE, bool DOT, int W>
 __global__ void __launch_bounds__(kBlock) k_ell(DMat A, RowArgs a) {
-    if (skip(a.st)) return;
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     double dot = 0.0;
     if (i < A.nrows) {
         double ax;
         if (MODE == MODE_RESID)
-            ax = ell_row(A, i, GatherWR{a.w, a.r});
+            ax = ell_any<W>(A, i, GatherX{a.r});
         else
-            ax = ell_row(A, i, GatherX{a.x});
+            ax = ell_any<W>(A, i, GatherX{a.x});
         const double y = epilogue<MODE>(a, i, ax);
         a.out[i] = y;
         if (DOT) dot = __ldg(a.r + i) * y;
@@ -193,13 +263,12 @@ __global__ void __launch_bounds__(kBlock) k_ell(DMat A, RowArgs a) {
 
 template <int G, int MODE, bool DOT>
 __global__ void __launch_bounds__(kBlock) k_csr(DMat A, RowArgs a) {
-    if (skip(a.st)) return;
     constexpr int RPB = kBlock / G;
     const int64_t i = (int64_t)blockIdx.x * RPB + threadIdx.x / G;
     const int sub = threadIdx.x % G;
     double ax;
     if (MODE == MODE_RESID)
-        ax = csr_row<G>(A, i, sub, GatherWR{a.w, a.r});
+        ax = csr_row<G>(A, i, sub, GatherX{a.r});
     else
         ax = csr_row<G>(A, i, sub, GatherX{a.x});
     double dot = 0.0;
@@ -216,45 +285,42 @@ __global__ void __launch_bounds__(kBlock) k_csr(DMat A, RowArgs a) {
     }
 }
 
-// bottom level: x = inv(A_bottom) r per subdomain, inverse stored transposed
-// (column j contiguous) so that lanes read coalesced; r staged in smem.  The
-// j range is split over the warps (fixed split, deterministic) and the warp
-// partials are added in warp order.
+// bottom level: x = inv(A_bottom) r per subdomain.  Grid = (chunks of 32
+// rows, subdomains); inside a block the 8 warps split the j range (fixed
+// split, deterministic), lane = row, the inverse is stored transposed so the
+// lanes read it coalesced; warp partials are added in warp order.
 __global__ void __launch_bounds__(256) k_bottom(const double *__restrict__ invT, const int64_t *__restrict__ inv_off,
                                                 const int64_t *__restrict__ off, const double *__restrict__ r,
                                                 double *__restrict__ x, const KState *st) {
-    if (skip(st)) return;
-    extern __shared__ double sh[];
-    const int s = blockIdx.x;
+    __shared__ double part[8][33];
+    const int s = blockIdx.y;
     const int64_t o = off[s];
     const int n = (int)(off[s + 1] - o);
+    const int ib = blockIdx.x * 32;
+    if (ib >= n) return;
     const double *M = invT + inv_off[s];
-    double *rs = sh;            // n
-    double *part = sh + n;      // 8 warps x 32 lanes
-    for (int j = threadIdx.x; j < n; j += blockDim.x) rs[j] = r[o + j];
-    __syncthreads();
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const int jchunk = (n + nw - 1) / nw;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int jchunk = (n + 7) / 8;
     const int j0 = warp * jchunk, j1 = min(n, j0 + jchunk);
-    for (int ib = 0; ib < n; ib += 32) {
-        const int i = ib + lane;
-        double a0 = 0.0, a1 = 0.0;
-        if (i < n) {
-            int j = j0;
-            for (; j + 1 < j1; j += 2) {
-                a0 = fma(M[(int64_t)j * n + i], rs[j], a0);
-                a1 = fma(M[(int64_t)(j + 1) * n + i], rs[j + 1], a1);
-            }
-            if (j < j1) a0 = fma(M[(int64_t)j * n + i], rs[j], a0);
+    const int i = ib + lane;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (i < n) {
+        int j = j0;
+        for (; j + 3 < j1; j += 4) {
+            a0 = fma(__ldg(M + (int64_t)j * n + i), __ldg(r + o + j), a0);
+            a1 = fma(__ldg(M + (int64_t)(j + 1) * n + i), __ldg(r + o + j + 1), a1);
+            a2 = fma(__ldg(M + (int64_t)(j + 2) * n + i), __ldg(r + o + j + 2), a2);
+            a3 = fma(__ldg(M + (int64_t)(j + 3) * n + i), __ldg(r + o + j + 3), a3);
         }
-        part[warp * 32 + lane] = a0 + a1;
-        __syncthreads();
-        if (warp == 0 && i < n) {
-            double acc = 0.0;
-            for (int w = 0; w < nw; ++w) acc += part[w * 32 + lane];
-            x[o + i] = acc;
-        }
-        __syncthreads();
+        for (; j < j1; ++j) a0 = fma(__ldg(M + (int64_t)j * n + i), __ldg(r + o + j), a0);
+    }
+    part[warp][lane] = (a0 + a1) + (a2 + a3);
+    __syncthreads();
+    if (warp == 0 && i < n) {
+        double acc = 0.0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) acc += part[w][lane];
+        x[o + i] = acc;
     }
 }
 
@@ -268,6 +334,35 @@ struct Tiles {
     const int64_t *row1;
     int64_t ntiles;
 };
+
+// subdomain-aligned tiles without a global table lookup: tile t of
+// subdomain s covers rows sub_off[s] + (t - tile_start[s]) * rows_per_tile ...
+constexpr int kSubTab = 32;
+struct SubTable {
+    int n = 0;                 // 0: use the global Tiles arrays
+    int rows_per_tile = 0;
+    int64_t sub_off[kSubTab + 1];
+    int64_t tile_start[kSubTab + 1];
+};
+
+__device__ __forceinline__ void tile_rows(const SubTable &S, const Tiles &T, int64_t t, int64_t &r0, int64_t &r1) {
+    if (S.n > 0) {
+        // unrolled scan with static indices: the table stays in the constant bank
+        int64_t ts = S.tile_start[0], so = S.sub_off[0], se = S.sub_off[1];
+#pragma unroll
+        for (int s = 1; s < kSubTab; ++s)
+            if (s < S.n && S.tile_start[s] <= t) {
+                ts = S.tile_start[s];
+                so = S.sub_off[s];
+                se = S.sub_off[s + 1];
+            }
+        r0 = so + (t - ts) * S.rows_per_tile;
+        r1 = min(r0 + (int64_t)S.rows_per_tile, se);
+    } else {
+        r0 = T.row0[t];
+        r1 = T.row1[t];
+    }
+}
 
 struct OpArgs {
     const double *x;        // gathered input (n_local + n_ghost)
@@ -294,16 +389,17 @@ __device__ __forceinline__ void op_epilogue(const OpArgs &a, int64_t i, bool val
     }
 }
 
-template <int OPMODE>
-__global__ void __launch_bounds__(kBlock) k_op_ell(DMat A, Tiles T, OpArgs a) {
-    if (skip(a.st)) return;
+template <int OPMODE, int W>
+__global__ void __launch_bounds__(kBlock) k_op_ell(DMat A, Tiles T, SubTable S, OpArgs a) {
     if (a.need_refresh && !a.st->refresh_now) return;
     const int64_t t = blockIdx.x;
-    const int64_t i = T.row0[t] + threadIdx.x;
-    const bool valid = i < T.row1[t];
+    int64_t r0, r1;
+    tile_rows(S, T, t, r0, r1);
+    const int64_t i = r0 + threadIdx.x;
+    const bool valid = i < r1;
     double y = 0.0;
     if (valid) {
-        const double ax = ell_row(A, i, GatherX{a.x});
+        const double ax = ell_any<W>(A, i, GatherX{a.x});
         y = OPMODE == 1 ? sub_rn(__ldg(a.b + i), ax) : ax;
         a.y[i] = y;
     }
@@ -313,18 +409,21 @@ __global__ void __launch_bounds__(kBlock) k_op_ell(DMat A, Tiles T, OpArgs a) {
         op_epilogue<OPMODE>(a, i, valid, y, acc);
         block_sum<kKmax>(acc, sm);
         if (threadIdx.x == 0)
-            for (int c = 0; c < a.k; ++c) a.zt_part[t * a.k + c] = acc[c];
+            #pragma unroll
+            for (int c = 0; c < kKmax; ++c)
+                if (c < a.k) a.zt_part[t * a.k + c] = acc[c];
     }
 }
 
 template <int G, int OPMODE>
-__global__ void __launch_bounds__(kBlock) k_op_csr(DMat A, Tiles T, OpArgs a) {
-    if (skip(a.st)) return;
+__global__ void __launch_bounds__(kBlock) k_op_csr(DMat A, Tiles T, SubTable S, OpArgs a) {
     if (a.need_refresh && !a.st->refresh_now) return;
     const int64_t t = blockIdx.x;
-    const int64_t i = T.row0[t] + threadIdx.x / G;
+    int64_t r0, r1;
+    tile_rows(S, T, t, r0, r1);
+    const int64_t i = r0 + threadIdx.x / G;
     const int sub = threadIdx.x % G;
-    const bool inrange = i < T.row1[t];
+    const bool inrange = i < r1;
     const double ax = csr_row<G>(A, inrange ? i : A.nrows, sub, GatherX{a.x});
     const bool valid = inrange && sub == 0;
     double y = 0.0;
@@ -338,7 +437,9 @@ __global__ void __launch_bounds__(kBlock) k_op_csr(DMat A, Tiles T, OpArgs a) {
         op_epilogue<OPMODE>(a, i, valid, y, acc);
         block_sum<kKmax>(acc, sm);
         if (threadIdx.x == 0)
-            for (int c = 0; c < a.k; ++c) a.zt_part[t * a.k + c] = acc[c];
+            #pragma unroll
+            for (int c = 0; c < kKmax; ++c)
+                if (c < a.k) a.zt_part[t * a.k + c] = acc[c];
     }
 }
 
@@ -362,7 +463,9 @@ __global__ void __launch_bounds__(kBlock) k_zt_vec(Tiles T, const double *__rest
     }
     block_sum<kKmax>(acc, sm);
     if (threadIdx.x == 0)
-        for (int c = 0; c < k; ++c) zt_part[t * k + c] = acc[c];
+#pragma unroll
+        for (int c = 0; c < kKmax; ++c)
+            if (c < k) zt_part[t * k + c] = acc[c];
 }
 
 // Sum tile partials per local subdomain -> t (global coarse numbering at
@@ -504,9 +607,17 @@ __global__ void __launch_bounds__(kBlock) k_dot(const double *__restrict__ a, co
 // deterministic sum of nparts partials -> out[slot]  (one block)
 __device__ __forceinline__ double reduce_parts(const double *part, int64_t nparts) {
     __shared__ double sm[32];
-    double acc = 0.0;
-    for (int64_t j = threadIdx.x; j < nparts; j += blockDim.x) acc += part[j];
-    double v[1] = {acc};
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const int64_t step = blockDim.x;
+    int64_t j = threadIdx.x;
+    for (; j + 3 * step < nparts; j += 4 * step) {
+        a0 += part[j];
+        a1 += part[j + step];
+        a2 += part[j + 2 * step];
+        a3 += part[j + 3 * step];
+    }
+    for (; j < nparts; j += step) a0 += part[j];
+    double v[1] = {(a0 + a1) + (a2 + a3)};
     block_sum<1>(v, sm);
     __shared__ double total;
     if (threadIdx.x == 0) total = v[0];
