@@ -73,6 +73,14 @@ struct Nccl {
 Nccl g_nccl;
 }  // namespace
 
+static bool g_use_pipe = false;  // TMA-staged variant (DFL_PIPE=1); see profiles/r01
+// layout experiments (profiling knobs, read once per context creation)
+// (measured on 150^3, see profiles/r01/README.md: CSR-vector with ~12 entries
+// per lane beats SELL-32-1024 for the coarse operators and R / P)
+static bool g_allow_sell = false;    // DFL_SELL=1 enables SELL-C-sigma for irregular matrices
+static int g_csr_g = 0;              // DFL_CSR_G=n forces the CSR lanes per row
+static double g_csr_per_lane = 12.0; // DFL_CSR_PER_LANE: target entries per lane
+
 // ---------------------------------------------------------------------------
 
 struct DLevel {
@@ -220,9 +228,11 @@ static int build_pipe(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vecto
 
 // colscale != nullptr: also upload the column-scaled values a_ij * colscale_j
 // in the same layout (shares the index arrays) into *scaled.
+static constexpr int64_t kSigma = 1024;  // SELL-C-sigma sorting window
+
 static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &bounds,
                          std::vector<int64_t> *bound_tiles = nullptr, bool allow_ell = true,
-                         const double *colscale = nullptr, DMat *scaled = nullptr) {
+                         const double *colscale = nullptr, DMat *scaled = nullptr, bool allow_sell = true) {
     m = DMat{};
     m.nrows = h.nrows;
     m.ncols = h.ncols;
@@ -232,32 +242,63 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::ve
         return DFL_E_DIMENSION;
     }
     const int64_t nsl = cdiv(h.nrows, 32);
-    std::vector<int64_t> soff(nsl + 1, 0);
+    auto rlen = [&](int64_t i) { return h.ptr[i + 1] - h.ptr[i]; };
+    // slot -> row: identity, or (SELL-C-sigma) rows sorted by length,
+    // descending and stable, inside windows of kSigma rows
+    std::vector<int> perm;
+    auto slice_offsets = [&](const std::vector<int> &pm, int64_t &maxlen) {
+        std::vector<int64_t> so(nsl + 1, 0);
+        maxlen = 0;
+        for (int64_t s = 0; s < nsl; ++s) {
+            int64_t wmax = 0;
+            for (int64_t j = s * 32; j < std::min(h.nrows, s * 32 + 32); ++j)
+                wmax = std::max(wmax, rlen(pm.empty() ? j : pm[j]));
+            maxlen = std::max(maxlen, wmax);
+            so[s + 1] = so[s] + 32 * wmax;
+        }
+        return so;
+    };
     int64_t maxlen = 0;
-    for (int64_t s = 0; s < nsl; ++s) {
-        int64_t wmax = 0;
-        for (int64_t i = s * 32; i < std::min(h.nrows, s * 32 + 32); ++i) wmax = std::max(wmax, h.ptr[i + 1] - h.ptr[i]);
-        maxlen = std::max(maxlen, wmax);
-        soff[s + 1] = soff[s] + 32 * wmax;
-    }
+    std::vector<int64_t> soff = slice_offsets(perm, maxlen);
     const double mean = h.nrows ? (double)m.nnz / (double)h.nrows : 0.0;
-    const bool ell = allow_ell && maxlen <= 32 && (double)soff[nsl] <= 1.2 * (double)m.nnz + 64.0;
+    const double nnzd = (double)m.nnz + 64.0;
+    bool ell = false;
+    if (allow_ell && maxlen <= 8 && (double)(nsl * 32 * maxlen) <= 1.03 * nnzd) {
+        // uniform slice width: the kernels compute slice offsets instead of loading them
+        ell = true;
+        m.ell_w = (int)maxlen;
+        for (int64_t s = 0; s <= nsl; ++s) soff[s] = s * 32 * maxlen;
+    } else if (allow_ell && (double)soff[nsl] <= 1.03 * nnzd) {
+        ell = true;
+    } else if (allow_ell && allow_sell && g_allow_sell && maxlen <= 1024) {
+        perm.resize(h.nrows);
+        for (int64_t w0 = 0; w0 < h.nrows; w0 += kSigma) {
+            const int64_t w1 = std::min(h.nrows, w0 + kSigma);
+            for (int64_t j = w0; j < w1; ++j) perm[j] = (int)j;
+            std::stable_sort(perm.begin() + w0, perm.begin() + w1, [&](int a, int b) { return rlen(a) > rlen(b); });
+        }
+        int64_t ml = 0;
+        std::vector<int64_t> ss = slice_offsets(perm, ml);
+        if ((double)ss[nsl] <= 1.25 * nnzd) {
+            ell = true;
+            soff = ss;
+            maxlen = ml;
+        } else {
+            perm.clear();
+        }
+    }
+    if (!ell && allow_ell && maxlen <= 32 && (double)soff[nsl] <= 1.2 * nnzd) ell = true;
     if (ell) {
         m.fmt = FMT_ELL;
-        // uniform slice width when it costs <= 3% extra storage: the kernels
-        // then compute slice offsets instead of loading them
-        if ((double)(nsl * 32 * maxlen) <= 1.03 * (double)soff[nsl] && maxlen <= kEllUnroll) {
-            m.ell_w = (int)maxlen;
-            for (int64_t s = 0; s <= nsl; ++s) soff[s] = s * 32 * maxlen;
-        }
         m.stored = soff[nsl];
-        std::vector<int> col(m.stored);
+        std::vector<int> col(m.stored, 0);
         std::vector<double> val(m.stored, 0.0);
         std::vector<double> sval(colscale ? m.stored : 0, 0.0);
         for (int64_t s = 0; s < nsl; ++s) {
             const int64_t wdt = (soff[s + 1] - soff[s]) / 32;
-            for (int64_t i = s * 32; i < std::min(h.nrows, s * 32 + 32); ++i) {
-                const int lane = (int)(i - s * 32);
+            for (int64_t j = s * 32; j < std::min(h.nrows, s * 32 + 32); ++j) {
+                const int lane = (int)(j - s * 32);
+                const int64_t i = perm.empty() ? j : perm[j];
                 const int64_t b = h.ptr[i], e = h.ptr[i + 1];
                 const int pad_col = e > b ? (int)h.col[e - 1] : 0;
                 for (int64_t k = 0; k < wdt; ++k) {
@@ -268,12 +309,9 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::ve
                         if (colscale) sval[dst] = h.val[b + k] * colscale[h.col[b + k]];
                     } else {
                         col[dst] = pad_col;
-                        val[dst] = 0.0;
                     }
                 }
             }
-            for (int64_t i = std::min(h.nrows, s * 32 + 32); i < s * 32 + 32; ++i)  // rows past the end
-                for (int64_t k = 0; k < wdt; ++k) col[soff[s] + k * 32 + (i - s * 32)] = 0;
         }
         int64_t *d_soff;
         int *d_col;
@@ -284,7 +322,12 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::ve
         m.slice_off = d_soff;
         m.col = d_col;
         m.val = d_val;
-        RC(build_pipe(ctx, h, m, soff, bounds, bound_tiles));
+        if (!perm.empty()) {
+            int *d_perm;
+            RC(upload(ctx, &d_perm, perm.data(), h.nrows));
+            m.perm = d_perm;
+        }
+        if (perm.empty()) RC(build_pipe(ctx, h, m, soff, bounds, bound_tiles));
         if (colscale) {
             double *d_sval;
             RC(upload(ctx, &d_sval, sval.data(), m.stored));
@@ -296,8 +339,9 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::ve
         m.stored = m.nnz;
         // lanes per row: about 6 entries per lane, batched kCsrUnroll deep
         int g = 1;
-        const int want = (int)std::ceil(mean / 6.0);
+        const int want = (int)std::ceil(mean / g_csr_per_lane);
         while (g < want && g < 32) g *= 2;
+        if (g_csr_g > 0) g = g_csr_g;
         m.group = g;
         // padded by 4 entries so that 16-byte aligned bulk copies may overrun the last row
         std::vector<int> ptr(h.nrows + 1), col(m.nnz + 4, 0);
@@ -446,7 +490,6 @@ static bool launch_pipe(dfl_ctx *ctx, const DMat &A, const SpArgs &a) {
     return true;
 }
 
-static bool g_use_pipe = false;  // TMA-staged variant (DFL_PIPE=1); see profiles/r01
 
 template <int MODE, bool DOT>
 static void launch_csr_mode(const DMat &A, const RowArgs &a, cudaStream_t st) {
@@ -1177,6 +1220,12 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
         pipe_attrs();
         const char *np = getenv("DFL_PIPE");
         g_use_pipe = np && np[0] == '1';
+        const char *ns = getenv("DFL_SELL");
+        g_allow_sell = ns && ns[0] == '1';
+        const char *cg = getenv("DFL_CSR_G");
+        g_csr_g = cg ? atoi(cg) : 0;
+        const char *cl = getenv("DFL_CSR_PER_LANE");
+        g_csr_per_lane = cl ? atof(cl) : 12.0;
     }
     if (e != cudaSuccess) {
         dfl::set_setup_error(std::string("CUDA context creation failed: ") + cudaGetErrorString(e));
@@ -1258,7 +1307,7 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
     ctx->nsub = nsub;
     ctx->sub_off.assign(sub_offsets, sub_offsets + nsub + 1);
     HostRows h{A->nrows, A->ncols, A->row_ptr, A->col_idx, A->values};
-    RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, &ctx->op_sub_tiles_h));
+    RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, &ctx->op_sub_tiles_h, true, nullptr, nullptr, false));
     if (ctx->Aop.pipe.stages) RC(upload(ctx, &ctx->op_sub_tiles, ctx->op_sub_tiles_h.data(), (int64_t)ctx->op_sub_tiles_h.size()));
     ctx->op_nnz = ctx->Aop.nnz;
     int64_t nrecv = 0;

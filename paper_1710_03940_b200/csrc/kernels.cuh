@@ -52,6 +52,7 @@ struct DMat {
     const int *ptr = nullptr;            // CSR row pointer
     const int *col = nullptr;
     const double *val = nullptr;
+    const int *perm = nullptr;           // SELL-C-sigma: slot -> row (nullptr: identity)
 };
 
 // run-time state of one Krylov solve (device resident)
@@ -116,7 +117,22 @@ __device__ __forceinline__ double ell_row(const DMat &A, int64_t row, const G &g
         for (int k = 0; k < kEllUnroll; ++k)
             if (k < width) acc = add_rn(acc, mul_rn(v[k], xv[k]));
     } else {
-        for (int k = 0; k < width; ++k) acc = add_rn(acc, mul_rn(ld_stream(vp + 32 * k), g(ld_stream(cp + 32 * k))));
+        for (int k0 = 0; k0 < width; k0 += kEllUnroll) {
+            int c[kEllUnroll];
+            double v[kEllUnroll], xv[kEllUnroll];
+#pragma unroll
+            for (int k = 0; k < kEllUnroll; ++k)
+                if (k0 + k < width) {
+                    c[k] = ld_stream(cp + 32 * (k0 + k));
+                    v[k] = ld_stream(vp + 32 * (k0 + k));
+                }
+#pragma unroll
+            for (int k = 0; k < kEllUnroll; ++k)
+                if (k0 + k < width) xv[k] = g(c[k]);
+#pragma unroll
+            for (int k = 0; k < kEllUnroll; ++k)
+                if (k0 + k < width) acc = add_rn(acc, mul_rn(v[k], xv[k]));
+        }
     }
     return acc;
 }
@@ -241,14 +257,15 @@ __device__ __forceinline__ double epilogue(const RowArgs &a, int64_t i, double a
 // upload), so it gathers r once per entry instead of w and r.
 template <int MODE, bool DOT, int W>
 __global__ void __launch_bounds__(kBlock) k_ell(DMat A, RowArgs a) {
-    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    const int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x;  // storage slot
     double dot = 0.0;
-    if (i < A.nrows) {
+    if (j < A.nrows) {
+        const int64_t i = (W == 0 && A.perm) ? (int64_t)__ldg(A.perm + j) : j;  // matrix row
         double ax;
         if (MODE == MODE_RESID)
-            ax = ell_any<W>(A, i, GatherX{a.r});
+            ax = ell_any<W>(A, j, GatherX{a.r});
         else
-            ax = ell_any<W>(A, i, GatherX{a.x});
+            ax = ell_any<W>(A, j, GatherX{a.x});
         const double y = epilogue<MODE>(a, i, ax);
         a.out[i] = y;
         if (DOT) dot = __ldg(a.r + i) * y;
