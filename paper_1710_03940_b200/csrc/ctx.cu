@@ -166,6 +166,10 @@ struct dfl_ctx {
            *w = nullptr, *tmp = nullptr, *xin = nullptr, *yout = nullptr;
     double *dpart = nullptr;
     int64_t nblk = 0;
+    // BiCGStab(2) work vectors (allocated on first use)
+    double *br[3] = {nullptr, nullptr, nullptr}, *bd[3] = {nullptr, nullptr, nullptr};
+    double *bu = nullptr, *bshadow = nullptr, *zx = nullptr;
+    double *h_dots = nullptr;  // pinned
     double *scal = nullptr;     // [0..7] local reduced scalars
     double *sgather = nullptr;  // nranks * 8
     KState *state = nullptr;
@@ -941,6 +945,8 @@ static int build_loop_graph(dfl_ctx *ctx, bool deflated) {
 
 // ---------------------------------------------------------------------------
 // the whole solve on the device: b, x in ctx->b / ctx->xin
+static int lift_dev(dfl_ctx *ctx, const dfl_solve_params *p);
+
 static int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
     KState *st = ctx->state;
     const bool defl = p->deflated != 0;
@@ -987,8 +993,12 @@ static int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph)
             if (ctx->h_state->done) break;
         }
     }
-    // x = y + Z E^-1 Z'(b - A y)   (deflation.py:285)
-    if (defl) {
+    return lift_dev(ctx, p);
+}
+
+// x = y + Z E^-1 Z'(b - A y)   (deflation.py:285); y in ctx->x, x -> ctx->xin
+static int lift_dev(dfl_ctx *ctx, const dfl_solve_params *p) {
+    if (p->deflated) {
         RC(op_apply_dev(ctx, ctx->x, ctx->tmp, 1, ctx->b, true, nullptr, 0));
         RC(zt_to_t2(ctx, nullptr, 0, true));
         k_lift<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, ctx->tile_sub, ctx->x, ctx->zcols, ctx->n,
@@ -998,6 +1008,235 @@ static int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph)
         k_copy<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->xin, ctx->x, ctx->n);
     }
     ctx->launches++;
+    return DFL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// BiCGStab(2) (krylov.py:148-285), right preconditioned: op_hat = op o M with
+// op = project o A.  Host-driven: scalars are computed on the host in IEEE
+// double with the reference's expressions; every dot is a device reduction
+// read back at its branch point.
+
+static int fetch(dfl_ctx *ctx, const double *dev, int n, double *out) {
+    CK(cudaMemcpyAsync(ctx->h_dots, dev, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->st));
+    CK(cudaStreamSynchronize(ctx->st));
+    for (int q = 0; q < n; ++q) out[q] = ctx->h_dots[q];
+    return DFL_OK;
+}
+
+// global value of nq interleaved (stride 3) or plain (nq == 0 -> 1 stream) partials
+static int global_dots(dfl_ctx *ctx, const double *part, int64_t nparts, int nq, bool strided, double *out) {
+    if (strided)
+        k_reduce3<<<1, 1024, 0, ctx->st>>>(part, nparts, nq, ctx->scal);
+    else
+        k_reduce<<<1, 1024, 0, ctx->st>>>(part, nparts, ctx->scal);
+    ctx->launches++;
+    if (ctx->nranks > 1) {
+        RC(nccl_check(ctx, g_nccl.AllGather(ctx->scal, ctx->sgather, 8, ncclDouble_, ctx->comm, ctx->st),
+                      "ncclAllGather"));
+        k_rank_sum<<<1, 32, 0, ctx->st>>>(ctx->sgather, ctx->nranks, 8, nq, ctx->scal + 8);
+        ctx->launches++;
+        return fetch(ctx, ctx->scal + 8, nq, out);
+    }
+    return fetch(ctx, ctx->scal, nq, out);
+}
+
+static unsigned dot_grid(dfl_ctx *ctx) { return (unsigned)std::min<int64_t>(std::max<int64_t>(1, ctx->nblk), 4 * ctx->sm_count); }
+
+static int dots(dfl_ctx *ctx, int nq, const double *a0, const double *b0, const double *a1, const double *b1,
+                const double *a2, const double *b2, double *out) {
+    const unsigned g = dot_grid(ctx);
+    k_multidot<<<g, kBlock, 0, ctx->st>>>(a0, b0, a1, b1, a2, b2, nq, ctx->n, ctx->dpart);
+    ctx->launches++;
+    return global_dots(ctx, ctx->dpart, g, nq, true, out);
+}
+
+// out = op_hat(v) = project(A (M v)); with dotv: also returns dot(out, dotv)
+static int op_hat(dfl_ctx *ctx, bool defl, const double *v, double *out, const double *dotv, double *dot_out) {
+    RC(vcycle(ctx, v, ctx->zx, nullptr, nullptr, nullptr));
+    RC(op_apply_dev(ctx, ctx->zx, ctx->w, 0, nullptr, defl, nullptr, 0));
+    if (defl) RC(zt_to_t2(ctx, nullptr, 0, true));
+    ProjArgs a = proj_args(ctx, ctx->w, out, nullptr);
+    if (!defl) a.az_ptr = nullptr, a.K = 0;
+    if (dotv) {
+        a.dotmode = 1;
+        a.dotv = dotv;
+        a.dot_part = ctx->dpart;
+    }
+    launch_project<0>(ctx, a);
+    if (dotv) RC(global_dots(ctx, ctx->dpart, ctx->nblk, 1, false, dot_out));
+    return DFL_OK;
+}
+
+static int bicg_alloc(dfl_ctx *ctx) {
+    if (ctx->bu) return DFL_OK;
+    for (int j = 0; j < 3; ++j) {
+        RC(dalloc(ctx, &ctx->br[j], ctx->n));
+        RC(dalloc(ctx, &ctx->bd[j], ctx->n));
+    }
+    RC(dalloc(ctx, &ctx->bu, ctx->n));
+    RC(dalloc(ctx, &ctx->bshadow, ctx->n));
+    RC(dalloc(ctx, &ctx->zx, ctx->n + ctx->n_ghost));
+    CK(cudaMemset(ctx->zx, 0, sizeof(double) * (ctx->n + ctx->n_ghost)));
+    return DFL_OK;
+}
+
+static int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
+    RC(bicg_alloc(ctx));
+    const bool defl = p->deflated != 0;
+    const int64_t n = ctx->n;
+    const unsigned nb = (unsigned)ctx->nblk;
+    out = KState{};
+    double val[3];
+    // ||b|| (deflation.py:266), b' = project(b), ||b'||
+    RC(dots(ctx, 1, ctx->b, ctx->b, nullptr, nullptr, nullptr, nullptr, val));
+    out.bnorm = std::sqrt(std::max(val[0], 0.0));
+    const double target = std::max(0.0, p->tol * out.bnorm);  // max(tol*||b'||, atol) with tol = 0
+    out.target = target;
+    k_fill<<<nb, kBlock, 0, ctx->st>>>(ctx->bu, 0.0, n);
+    ctx->launches++;
+    if (out.bnorm == 0.0) {
+        out.converged = 1;
+        k_fill<<<nb, kBlock, 0, ctx->st>>>(ctx->x, 0.0, n);
+        ctx->launches++;
+        return DFL_OK;
+    }
+    if (defl) {
+        RC(project_dev(ctx, ctx->b, ctx->bp, nullptr, 0));
+    } else {
+        k_copy<<<nb, kBlock, 0, ctx->st>>>(ctx->bp, ctx->b, n);
+        ctx->launches++;
+    }
+    RC(dots(ctx, 1, ctx->bp, ctx->bp, nullptr, nullptr, nullptr, nullptr, val));
+    const double bpn = std::sqrt(std::max(val[0], 0.0));
+    if (bpn == 0.0) {  // bicgstab2 returns zeros (krylov.py:270-272)
+        out.converged = 1;
+        k_fill<<<nb, kBlock, 0, ctx->st>>>(ctx->x, 0.0, n);
+        ctx->launches++;
+        return DFL_OK;
+    }
+    double *r[3] = {ctx->br[0], ctx->br[1], ctx->br[2]};
+    double *d[3] = {ctx->bd[0], ctx->bd[1], ctx->bd[2]};
+    double *u = ctx->bu, *shadow = ctx->bshadow;
+    const double *r0init = ctx->bp;
+    k_copy<<<nb, kBlock, 0, ctx->st>>>(r[0], r0init, n);
+    k_fill<<<nb, kBlock, 0, ctx->st>>>(d[0], 0.0, n);
+    k_copy<<<nb, kBlock, 0, ctx->st>>>(shadow, r0init, n);
+    ctx->launches += 3;
+    double rho0 = 1.0, alpha = 0.0, omega = 1.0;
+    bool restarted = false;
+    int brk = DFL_BRK_NONE;
+    int iters = 0;
+    double resnorm = bpn;  // ||r[0]|| with r[0] = b'
+    auto fail = [&](int code) -> int {
+        if (restarted) return code;
+        restarted = true;
+        // r_shadow = r[0]; d = [0]; rho0, alpha, omega = 1, 0, 1  (krylov.py:165-175)
+        k_copy<<<nb, kBlock, 0, ctx->st>>>(shadow, r[0], n);
+        k_fill<<<nb, kBlock, 0, ctx->st>>>(d[0], 0.0, n);
+        ctx->launches += 2;
+        rho0 = 1.0;
+        alpha = 0.0;
+        omega = 1.0;
+        return DFL_BRK_NONE;
+    };
+    const int refresh = std::max(1, p->refresh_every);
+    while (iters < p->maxiter && resnorm > target) {
+        ++iters;
+        rho0 = -omega * rho0;
+        bool aborted = false, mid = false;
+        for (int j = 0; j < 2; ++j) {
+            RC(dots(ctx, 1, r[j], shadow, nullptr, nullptr, nullptr, nullptr, val));
+            const double rho1 = val[0];
+            if (rho0 == 0.0 || !std::isfinite(rho1)) {
+                brk = fail(DFL_BRK_RHO);
+                aborted = true;
+                break;
+            }
+            const double beta = alpha * rho1 / rho0;
+            rho0 = rho1;
+            k_bicg_d<<<nb, kBlock, 0, ctx->st>>>(r[0], d[0], r[1], d[1], j + 1, beta, n);
+            ctx->launches++;
+            double gd;
+            RC(op_hat(ctx, defl, d[j], d[j + 1], shadow, &gd));
+            if (gd == 0.0 || !std::isfinite(gd)) {
+                brk = fail(DFL_BRK_SHADOW);
+                aborted = true;
+                break;
+            }
+            alpha = rho0 / gd;
+            k_bicg_r<<<nb, kBlock, 0, ctx->st>>>(r[0], d[1], r[1], d[2], j + 1, u, d[0], alpha, n, ctx->dpart);
+            ctx->launches++;
+            RC(op_hat(ctx, defl, r[j], r[j + 1], nullptr, nullptr));
+            RC(global_dots(ctx, ctx->dpart, nb, 1, false, val));
+            resnorm = std::sqrt(std::max(val[0], 0.0));
+            if (resnorm <= target) {
+                mid = true;
+                break;
+            }
+        }
+        if (aborted) {
+            RC(dots(ctx, 1, r[0], r[0], nullptr, nullptr, nullptr, nullptr, val));
+            resnorm = std::sqrt(std::max(val[0], 0.0));
+            if (brk != DFL_BRK_NONE || resnorm <= target) break;
+            continue;
+        }
+        if (mid) break;
+        // minimal-residual step on r[1..2] (modified Gram-Schmidt, krylov.py:207-255)
+        RC(dots(ctx, 3, r[0], r[1], r[1], r[1], r[2], r[1], val));
+        const double sigma1 = val[1];
+        if (sigma1 == 0.0 || !std::isfinite(sigma1)) {
+            brk = fail(DFL_BRK_MR);
+            if (brk != DFL_BRK_NONE) break;
+            continue;
+        }
+        const double gp1 = val[0] / sigma1;
+        const double tau12 = val[2] / sigma1;
+        {
+            const unsigned g = dot_grid(ctx);
+            k_bicg_mr2<<<g, kBlock, 0, ctx->st>>>(r[2], r[1], r[0], tau12, n, ctx->dpart);
+            ctx->launches++;
+            RC(global_dots(ctx, ctx->dpart, g, 2, true, val));
+        }
+        const double sigma2 = val[0];
+        if (sigma2 == 0.0 || !std::isfinite(sigma2)) {
+            brk = fail(DFL_BRK_MR);
+            if (brk != DFL_BRK_NONE) break;
+            continue;
+        }
+        const double gp2 = val[1] / sigma2;
+        const double g2 = gp2;
+        omega = g2;
+        if (omega == 0.0 || !std::isfinite(omega)) {
+            brk = fail(DFL_BRK_OMEGA);
+            if (brk != DFL_BRK_NONE) break;
+            continue;
+        }
+        const double g1 = gp1 - tau12 * g2;
+        const double gpp1 = g2 + 0.0;
+        k_bicg_final<<<nb, kBlock, 0, ctx->st>>>(u, r[0], d[0], r[1], r[2], d[1], d[2], g1, gp2, g2, gpp1, gp1, n,
+                                                 ctx->dpart);
+        ctx->launches++;
+        if (iters % refresh == 0) {
+            // r[0] = r0 - op_hat(u)   (krylov.py:256-257)
+            RC(op_hat(ctx, defl, u, ctx->tmp, nullptr, nullptr));
+            ProjArgs a = proj_args(ctx, ctx->tmp, r[0], nullptr);
+            a.az_ptr = nullptr;
+            a.K = 0;
+            a.base = r0init;
+            a.dotmode = 2;
+            a.dot_part = ctx->dpart;
+            launch_project<1>(ctx, a);  // r[0] = r0 - tmp, partial r0.r0
+        }
+        RC(global_dots(ctx, ctx->dpart, nb, 1, false, val));
+        resnorm = std::sqrt(std::max(val[0], 0.0));
+    }
+    // x = x0 + M(u)  (krylov.py:284-285), into ctx->x (the y of the deflated system)
+    RC(vcycle(ctx, u, ctx->x, nullptr, nullptr, nullptr));
+    out.iters = iters;
+    out.resnorm = resnorm;
+    out.converged = resnorm <= target;
+    out.breakdown = out.converged ? DFL_BRK_NONE : brk;
     return DFL_OK;
 }
 
@@ -1243,6 +1482,7 @@ void dfl_ctx_destroy(dfl_ctx *ctx) {
     if (ctx->loop_exec) cudaGraphExecDestroy(ctx->loop_exec);
     for (void *p : ctx->allocs) cudaFree(p);
     if (ctx->h_state) cudaFreeHost(ctx->h_state);
+    if (ctx->h_dots) cudaFreeHost(ctx->h_dots);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
@@ -1442,6 +1682,7 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
     RC(dalloc(ctx, &ctx->scal, 16));
     RC(dalloc(ctx, &ctx->sgather, (int64_t)8 * ctx->nranks));
     RC(dalloc(ctx, &ctx->state, 1));
+    CK(cudaMallocHost(&ctx->h_dots, 16 * sizeof(double)));
     RC(dalloc(ctx, &ctx->ticket, 4));
     CK(cudaMemset(ctx->ticket, 0, 4 * sizeof(unsigned int)));
     CK(cudaMemset(ctx->x, 0, sizeof(double) * nx));
@@ -1455,8 +1696,8 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
 int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *x, int ptr_kind, dfl_report *rep) {
     RC(ready(ctx));
     if (!p || !rep) return DFL_E_STATE;
-    if (p->solver != DFL_SOLVER_CG) {
-        ctx->err = "only cg is implemented by this build of the device loop";
+    if (p->solver != DFL_SOLVER_CG && p->solver != DFL_SOLVER_BICGSTAB2) {
+        ctx->err = "solver must be cg or bicgstab2";
         return DFL_E_CONFIG;
     }
     if (p->deflated && !ctx->deflation) {
@@ -1472,8 +1713,15 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     RC(stage_in(ctx, ctx->b, b, ptr_kind));
     CK(cudaEventRecord(ctx->ev0, ctx->st));
     const char *ng = getenv("DFL_NO_GRAPH");
-    const bool use_graph = ctx->nranks == 1 && !(ng && ng[0] == '1');
-    RC(cg_solve_dev(ctx, p, use_graph));
+    const bool bicg = p->solver == DFL_SOLVER_BICGSTAB2;
+    const bool use_graph = !bicg && ctx->nranks == 1 && !(ng && ng[0] == '1');
+    KState bstate{};
+    if (bicg) {
+        RC(bicg_solve_dev(ctx, p, bstate));
+        RC(lift_dev(ctx, p));
+    } else {
+        RC(cg_solve_dev(ctx, p, use_graph));
+    }
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev1, ctx->st));
     CK(cudaMemcpyAsync(x, ctx->xin, sizeof(double) * ctx->n,
@@ -1487,7 +1735,7 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     CK(cudaEventElapsedTime(&ms_d2h, ctx->ev1, e_h1));
     cudaEventDestroy(e_h0);
     cudaEventDestroy(e_h1);
-    const KState s = *ctx->h_state;
+    const KState s = bicg ? bstate : *ctx->h_state;
     rep->iterations = s.iters;
     rep->converged = s.converged || (s.resnorm <= s.target);
     if (s.breakdown) rep->converged = 0;

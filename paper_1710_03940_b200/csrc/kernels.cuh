@@ -709,3 +709,116 @@ __global__ void k_rank_sum(const double *g, int nranks, int stride, int nv, doub
 }
 
 }  // namespace dfl
+
+namespace dfl {
+// ---------------------------------------------------------------------------
+// BiCGStab(2) vector kernels (krylov.py:148-262).  Coefficients are computed on
+// the host in IEEE double exactly as the reference's Python scalars and passed
+// by value; every update keeps the reference's operation order (no FMA).
+
+// up to three dot products sharing one pass: part[blk*3 + q] = sum a_q . b_q
+__global__ void __launch_bounds__(kBlock) k_multidot(const double *__restrict__ a0, const double *__restrict__ b0,
+                                                     const double *__restrict__ a1, const double *__restrict__ b1,
+                                                     const double *__restrict__ a2, const double *__restrict__ b2,
+                                                     int nq, int64_t n, double *part) {
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        acc[0] += a0[i] * b0[i];
+        if (nq > 1) acc[1] += a1[i] * b1[i];
+        if (nq > 2) acc[2] += a2[i] * b2[i];
+    }
+    __shared__ double sm[32 * 3];
+    block_sum<3>(acc, sm);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < 3; ++q) part[blockIdx.x * 3 + q] = acc[q];
+}
+
+// reduce nq interleaved partial streams (stride 3) -> out[0..nq)
+__global__ void k_reduce3(const double *part, int64_t nparts, int nq, double *out) {
+    __shared__ double sm[32 * 3];
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int64_t j = threadIdx.x; j < nparts; j += blockDim.x)
+        for (int q = 0; q < 3; ++q) acc[q] += part[j * 3 + q];
+    block_sum<3>(acc, sm);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < nq; ++q) out[q] = acc[q];
+}
+
+// d_i = r_i - beta d_i for i < cnt  (krylov.py:189-190)
+__global__ void __launch_bounds__(kBlock) k_bicg_d(const double *__restrict__ r0, double *d0,
+                                                   const double *__restrict__ r1, double *d1, int cnt, double beta,
+                                                   int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (i >= n) return;
+    d0[i] = sub_rn(r0[i], mul_rn(beta, d0[i]));
+    if (cnt > 1) d1[i] = sub_rn(r1[i], mul_rn(beta, d1[i]));
+}
+
+// r_i -= alpha d_{i+1} for i < cnt; u += alpha d_0; partial r_0.r_0
+// (krylov.py:199-203)
+__global__ void __launch_bounds__(kBlock) k_bicg_r(double *r0, const double *__restrict__ d1, double *r1,
+                                                   const double *__restrict__ d2, int cnt, double *u,
+                                                   const double *__restrict__ d0, double alpha, int64_t n,
+                                                   double *part) {
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    double dot = 0.0;
+    if (i < n) {
+        const double a = sub_rn(r0[i], mul_rn(alpha, d1[i]));
+        r0[i] = a;
+        dot = a * a;
+        if (cnt > 1) r1[i] = sub_rn(r1[i], mul_rn(alpha, d2[i]));
+        u[i] = add_rn(u[i], mul_rn(alpha, d0[i]));
+    }
+    __shared__ double sm[32];
+    double v[1] = {dot};
+    block_sum<1>(v, sm);
+    if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+}
+
+// r2 -= tau12 r1; partials (r2.r2, r0.r2)   (krylov.py:218-225)
+__global__ void __launch_bounds__(kBlock) k_bicg_mr2(double *r2, const double *__restrict__ r1,
+                                                     const double *__restrict__ r0, double tau12, int64_t n,
+                                                     double *part) {
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
+        const double v = sub_rn(r2[i], mul_rn(tau12, r1[i]));
+        r2[i] = v;
+        acc[0] += v * v;
+        acc[1] += r0[i] * v;
+    }
+    __shared__ double sm[32 * 3];
+    block_sum<3>(acc, sm);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < 3; ++q) part[blockIdx.x * 3 + q] = acc[q];
+}
+
+// the closing updates of one BiCGStab(2) group (krylov.py:247-253):
+//   u += g1 r0; r0 -= gp2 r2; d0 -= g2 d2; d0 -= g1 d1; u += gpp1 r1; r0 -= gp1 r1
+// + partial r0.r0 (unless the recurrence is refreshed afterwards)
+__global__ void __launch_bounds__(kBlock) k_bicg_final(double *u, double *r0, double *d0,
+                                                       const double *__restrict__ r1, const double *__restrict__ r2,
+                                                       const double *__restrict__ d1, const double *__restrict__ d2,
+                                                       double g1, double gp2, double g2, double gpp1, double gp1,
+                                                       int64_t n, double *part) {
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    double dot = 0.0;
+    if (i < n) {
+        const double r0i = r0[i], r1i = r1[i];
+        double ui = add_rn(u[i], mul_rn(g1, r0i));
+        double ri = sub_rn(r0i, mul_rn(gp2, r2[i]));
+        double di = sub_rn(d0[i], mul_rn(g2, d2[i]));
+        di = sub_rn(di, mul_rn(g1, d1[i]));
+        ui = add_rn(ui, mul_rn(gpp1, r1i));
+        ri = sub_rn(ri, mul_rn(gp1, r1i));
+        u[i] = ui;
+        r0[i] = ri;
+        d0[i] = di;
+        dot = ri * ri;
+    }
+    __shared__ double sm[32];
+    double v[1] = {dot};
+    block_sum<1>(v, sm);
+    if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+}
+
+}  // namespace dfl
