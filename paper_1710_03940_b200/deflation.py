@@ -22,7 +22,6 @@ or uses :meth:`DeflatedSolver.from_rows` with only its own rows.
 """
 from __future__ import annotations
 
-import math
 import os
 import time
 
@@ -31,8 +30,9 @@ import numpy as np
 from . import _native as nat
 from .config import SolverConfig, as_config
 from .dist import World, current_world
-from .errors import ConfigError, DimensionError, PartitionError, StructureError
-from .runtime import Partition, as_partition, rank_subdomains
+from .errors import ConfigError, DimensionError
+from .runtime import as_partition, rank_subdomains
+from .hostsetup import build_rank_setup
 from .sparse import as_csr_arrays
 
 __all__ = ["DeflatedSolver", "solve_deflated", "HierarchyInfo", "BasisInfo"]
@@ -81,17 +81,6 @@ def _check_config(cfg: SolverConfig, deflated: bool):
             raise ConfigError("deflation.inexact (inner GMRES on E) is not on the B200 solve path")
 
 
-def _amg_options(cfg: SolverConfig) -> nat.AmgOptions:
-    return nat.AmgOptions(
-        float(cfg.get("precond.coarsening.eps_strong")),
-        float(cfg.get("precond.coarsening.omega")),
-        float(cfg.get("precond.relax.damping")),
-        nat.DFL_RELAX[cfg.get("precond.relax.type")],
-        25,
-        int(cfg.get("precond.coarse_enough")),
-    )
-
-
 class DeflatedSolver:
     """One setup, many solves: subdomain split, per-block AMG, deflation
     basis -- with the solve phase on the GPU."""
@@ -135,166 +124,34 @@ class DeflatedSolver:
         self.world = world
         self.deflated = bool(deflated)
         self.inexact = False
-        subs = rank_subdomains(part.m, world.nranks, world.rank)
-        self.local_subdomains = subs
-        self.r0, self.r1 = part.ranges[subs.start][0], part.ranges[subs.stop - 1][1]
-        n = self.r1 - self.r0
-        lptr, lcol, lval = (np.ascontiguousarray(a) for a in rows)
-        lptr = lptr.astype(np.int64)
-        lcol = lcol.astype(np.int64)
-        lval = lval.astype(np.float64)
-        if lptr.shape[0] != n + 1:
-            raise PartitionError(f"rank rows have {lptr.shape[0] - 1} rows, expected {n}")
-        if global_coords is not None:
-            my_coords = global_coords[self.r0:self.r1]
-        else:
-            my_coords = None if coords is None else np.asarray(coords, dtype=np.float64).reshape(n, -1)
-        self.n_local = n
-
-        # --- column renumbering: own [0, n), ghosts [n, n+g) ascending global
-        own = (lcol >= self.r0) & (lcol < self.r1)
-        ghosts = np.unique(lcol[~own])
-        loc = np.empty_like(lcol)
-        loc[own] = lcol[own] - self.r0
-        loc[~own] = n + np.searchsorted(ghosts, lcol[~own])
-        self.ghosts = ghosts
-
-        # --- halo plan (runtime.py:246-271): owners by rank, send lists by exchange
-        sub_owner = part.owners(ghosts) if ghosts.size else np.zeros(0, dtype=np.int64)
-        rank_of_sub = np.empty(part.m, dtype=np.int64)
-        for q in range(world.nranks):
-            rank_of_sub[list(rank_subdomains(part.m, world.nranks, q))] = q
-        ghost_rank = rank_of_sub[sub_owner] if ghosts.size else np.zeros(0, dtype=np.int64)
-        if world.nranks == 1 and ghosts.size:
-            raise StructureError("single-rank operator has columns outside the matrix")
-        all_ghosts = world.allgather(ghosts)
-        nbr, recv_counts, send_counts, send_idx = [], [], [], []
-        for q in range(world.nranks):
-            if q == world.rank:
-                continue
-            rc = int(np.count_nonzero(ghost_rank == q))
-            gq = all_ghosts[q]
-            mine = gq[(gq >= self.r0) & (gq < self.r1)]
-            if rc or mine.size:
-                nbr.append(q)
-                recv_counts.append(rc)
-                send_counts.append(int(mine.size))
-                send_idx.append(mine - self.r0)
-        send_idx = np.concatenate(send_idx) if send_idx else np.zeros(0, dtype=np.int64)
-        self.halo_plan = {"neighbours": nbr, "recv": recv_counts, "send": send_counts}
-
-        op = nat.CsrArrays(n, n + ghosts.size, lptr, loc, lval)
-        sub_off = np.array([part.ranges[s][0] - self.r0 for s in subs] + [n], dtype=np.int64)
-
-        # --- per-subdomain AMG hierarchies on the diagonal blocks (deflation.py:208)
-        opts = _amg_options(self.cfg)
-        self._hier = []
-        self.hierarchies = []
-        for j, s in enumerate(subs):
-            b, e = int(sub_off[j]), int(sub_off[j + 1])
-            p0, p1 = lptr[b], lptr[e]
-            bc = loc[p0:p1]
-            keep = (bc >= b) & (bc < e)
-            rid = np.repeat(np.arange(e - b, dtype=np.int64), np.diff(lptr[b:e + 1]))
-            counts = np.bincount(rid[keep], minlength=e - b)
-            bptr = np.zeros(e - b + 1, dtype=np.int64)
-            np.cumsum(counts, out=bptr[1:])
-            block = nat.CsrArrays(e - b, e - b, bptr, bc[keep] - b, lval[p0:p1][keep])
-            h = nat.Hierarchy(block, opts)
-            self._hier.append(h)
-            self.hierarchies.append(HierarchyInfo(h.level_sizes, h.level_nnz()))
-
-        # --- deflation basis (deflation.py:83-163)
-        self.basis = None
-        k = 0
-        factorize_seconds = 0.0
-        if self.deflated:
-            kind = self.cfg.get("deflation.kind")
-            k, zext, owner, rowsub = self._basis_inputs(kind, my_coords, global_coords, ghosts, sub_owner, subs,
-                                                        sub_off)
-            K = part.m * k
-            AZ, E_rows = nat.basis_az(op, k, zext, owner, rowsub, K, subs.start, len(subs))
-            t_f = time.perf_counter()
-            E = np.concatenate(world.allgather(E_rows), axis=0)
-            Einv = nat.dense_inverse(E)
-            factorize_seconds = time.perf_counter() - t_f
-            self.basis = BasisInfo(kind, k, E, AZ[2][-1], factorize_seconds)
-            self._zcols = np.ascontiguousarray(zext[:n, 1:]) if k > 1 else None
-            self._AZ = nat.CsrArrays(*AZ)
-            self._Einv = Einv
-
+        hs = build_rank_setup(rows, part, self.cfg, coords, self.deflated, world, global_coords)
+        self.host = hs
+        self.local_subdomains = hs.subs
+        self.r0, self.r1, self.n_local = hs.r0, hs.r1, hs.n
+        self.ghosts = hs.ghosts
+        self.halo_plan = hs.halo_plan
+        self.hierarchies = [HierarchyInfo(h.level_sizes, h.level_nnz()) for h in hs.hier]
+        self.basis = (BasisInfo(hs.kind, hs.k, hs.E, int(hs.AZ.row_ptr[-1]), hs.factorize_seconds)
+                      if self.deflated else None)
         # --- device upload
         if device is None:
             device = int(os.environ.get("LOCAL_RANK", "0")) if world.nranks > 1 else 0
         self.device = device
         ctx = nat.DeviceContext(device)
-        if world.nranks > 1:
+        if world.nranks > 1 or os.environ.get("DFL_FORCE_COMM") == "1":
             nid = world.bcast(nat.nccl_unique_id() if world.rank == 0 else None)
             ctx.set_comm(world.nranks, world.rank, nid)
-        ctx.set_operator(op, sub_off, nbr, recv_counts, send_counts, send_idx)
-        for j, h in enumerate(self._hier):
+        plan = hs.halo_plan
+        ctx.set_operator(hs.op, hs.sub_off, plan["neighbours"], plan["recv"], plan["send"], hs.send_idx)
+        for j, h in enumerate(hs.hier):
             ctx.add_hierarchy(j, h)
         if self.deflated:
-            ctx.set_deflation(k, self._zcols, self._AZ, part.m * k, self._Einv, subs.start)
+            ctx.set_deflation(hs.k, hs.zcols, hs.AZ, part.m * hs.k, hs.Einv, hs.subs.start)
         ctx.finalize()
         self._ctx = ctx
-        self._hier = None  # host copies are no longer needed
+        hs.release()  # host copies of the hierarchies are no longer needed
         self.setup_seconds = time.perf_counter() - t_setup
-        self._factorize_seconds = factorize_seconds
-
-    def _basis_inputs(self, kind, my_coords, global_coords, ghosts, sub_owner, subs, sub_off):
-        """Z on own and ghost columns: [1, coords - centre_of_owner] with the
-        globally varying axes only (deflation.py:111-139)."""
-        world, part, n = self.world, self.partition, self.n_local
-        if kind == "linear":
-            if my_coords is None:
-                raise ConfigError("linear deflation needs node coordinates")
-            lo, hi = world.allreduce_minmax(my_coords.min(axis=0), my_coords.max(axis=0))
-            axes = [a for a in range(my_coords.shape[1]) if (hi[a] - lo[a]) > 0.0]
-        else:
-            axes = []
-        k = 1 + len(axes)
-        # centres of every subdomain (numpy mean exactly as the reference)
-        centres_local = []
-        for j, s in enumerate(subs):
-            if kind == "linear":
-                blk = my_coords[int(sub_off[j]):int(sub_off[j + 1])][:, axes]
-                centres_local.append(blk.mean(axis=0))
-            else:
-                centres_local.append(None)
-        centres = [c for part_list in world.allgather(centres_local) for c in part_list]
-        rowsub = np.repeat(np.arange(subs.start, subs.stop, dtype=np.int32), np.diff(sub_off))
-        ng = ghosts.size
-        zext = np.ones((n + ng, k))
-        owner = np.concatenate([rowsub, sub_owner.astype(np.int32)])
-        if kind == "linear":
-            for j, s in enumerate(subs):
-                b, e = int(sub_off[j]), int(sub_off[j + 1])
-                zext[b:e, 1:] = my_coords[b:e][:, axes] - centres[s]
-            if ng:
-                if global_coords is not None:
-                    gcoords = global_coords[ghosts][:, axes]
-                else:
-                    gcoords = self._exchange_ghost_coords(my_coords, ghosts)[:, axes]
-                for s in np.unique(sub_owner):
-                    sel = sub_owner == s
-                    zext[n:][sel, 1:] = gcoords[sel] - centres[int(s)]
-        return k, zext, owner, rowsub
-
-    def _exchange_ghost_coords(self, my_coords, ghosts):
-        world = self.world
-        requests = world.allgather(ghosts)
-        replies = {}
-        for q, gq in enumerate(requests):
-            sel = (gq >= self.r0) & (gq < self.r1)
-            replies[q] = (gq[sel], my_coords[gq[sel] - self.r0])
-        got = world.allgather(replies)
-        out = np.empty((ghosts.size, my_coords.shape[1]))
-        for q, rep in enumerate(got):
-            idx, vals = rep.get(world.rank, (np.zeros(0, np.int64), None))
-            if idx.size:
-                out[np.searchsorted(ghosts, idx)] = vals
-        return out
+        self._factorize_seconds = hs.factorize_seconds
 
     # -- properties mirrored from the reference ------------------------------
     @property

@@ -111,3 +111,19 @@ def test_config1_fingerprint():
     assert np.array_equal(x, x2) and rep2["iterations"] == rep["iterations"]
     x0, rep0 = s.solve(np.zeros_like(p.rhs))
     assert not x0.any() and rep0["iterations"] == 0 and rep0["converged"]
+
+
+@pytest.mark.parametrize("name", ["config1_32_m4_cg_spai0_const", "p16_m8_cg_spai0_lin", "p16_m4_bicg_spai0_lin"])
+def test_multirank_code_path_on_one_gpu(name, monkeypatch):
+    """DFL_FORCE_COMM=1 gives the context a 1-rank NCCL communicator, so the
+    multi-rank code path (host-driven loop, NCCL allgathers of the Z'w slots and
+    of the Krylov scalars, rank-ordered sums) runs on one GPU."""
+    monkeypatch.setenv("DFL_FORCE_COMM", "1")
+    case = solve_case(name)
+    p = problems.make_problem(case["shape"], problems.boxes_for(case["m"]), case["kind"])
+    s = _solver(p, case["m"], case["config"])
+    x, rep = s.solve(p.rhs)
+    xref = arrays()[f"solve_{name}_x"]
+    assert not rep["device_loop"]
+    assert abs(rep["iterations"] - case["iterations"]) <= 1
+    assert np.linalg.norm(x - xref) <= 1e-6 * np.linalg.norm(xref)
