@@ -222,6 +222,11 @@ int dfl_spmv_csr(const dfl_csr *A, const double *x, double *y, int device);
  *   what: 0 = operator SpMV (fine A), 1 = V-cycle, 2 = CG iteration */
 int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms_per_launch, double *bytes_per_launch);
 
+/* per-launch device times of one V-cycle, mean over reps; labels is a
+ * cap x 32 char buffer ("L<l> resid|restrict|prolong|post", "bottom");
+ * returns the number of launches (or a negative status) */
+int dfl_ctx_profile_vcycle(dfl_ctx *ctx, int reps, int cap, double *ms, char *labels);
+
 #ifdef __cplusplus
 }
 #endif

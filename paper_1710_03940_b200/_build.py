@@ -40,8 +40,8 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(s) <= t for s in _sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
+    if out is None and not force and up_to_date():
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     nvcc = _nvcc()
@@ -54,15 +54,20 @@ def build(force: bool = False, verbose: bool = False) -> str:
         objs.append(o)
     for f in CU_SOURCES:
         o = os.path.join(BUILD, f + ".o")
-        run([nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+        extra = os.environ.get("DFL_NVCC_FLAGS", "").split()
+        run([nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra,
              "-Xcompiler", "-ffp-contract=off", "-I", os.path.join(REPO, "include"),
              "-c", os.path.join(CSRC, f), "-o", o])
         objs.append(o)
-    tmp = LIB + ".tmp"
+    target = out or LIB
+    tmp = target + ".tmp"
     run([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-ldl", "-lpthread"])
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    o = None
+    if "--out" in sys.argv:
+        o = sys.argv[sys.argv.index("--out") + 1]
+    print(build(force="--force" in sys.argv, verbose=True, out=o))

@@ -14,7 +14,7 @@ import numpy as np
 from .errors import DeviceError, raise_for_status
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libdflb200.so")
+LIB_PATH = os.environ.get("DFL_LIB") or os.path.join(_PKG, "libdflb200.so")
 
 c_i64 = ctypes.c_int64
 c_i32 = ctypes.c_int32
@@ -100,6 +100,7 @@ def lib():
         "dfl_dot": ([c_vp, c_vp, c_vp, c_i32, P(c_dbl)], c_i32),
         "dfl_spmv_csr": ([P(Csr), c_vp, c_vp, c_i32], c_i32),
         "dfl_ctx_time": ([c_vp, c_i32, c_i32, P(c_dbl), P(c_dbl)], c_i32),
+        "dfl_ctx_profile_vcycle": ([c_vp, c_i32, c_i32, c_vp, c_vp], c_i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -307,6 +308,17 @@ class DeviceContext:
         out = c_dbl()
         self._c(lib().dfl_dot(self.h, _ptr(a), _ptr(b), PTR_HOST, ctypes.byref(out)))
         return out.value
+
+    def profile_vcycle(self, reps: int = 10):
+        """[(label, ms)] per launch of one V-cycle."""
+        cap = 256
+        ms = np.zeros(cap)
+        lab = ctypes.create_string_buffer(32 * cap)
+        cnt = lib().dfl_ctx_profile_vcycle(self.h, reps, cap, _ptr(ms), lab)
+        if cnt < 0:
+            self._c(cnt)
+        raw = lab.raw
+        return [(raw[32 * i:32 * i + 32].split(b"\0")[0].decode(), float(ms[i])) for i in range(cnt)]
 
     def time(self, what: int, reps: int):
         ms, by = c_dbl(), c_dbl()

@@ -77,7 +77,7 @@ static bool g_use_pipe = false;  // TMA-staged variant (DFL_PIPE=1); see profile
 // layout experiments (profiling knobs, read once per context creation)
 // (measured on 150^3, see profiles/r01/README.md: CSR-vector with ~12 entries
 // per lane beats SELL-32-1024 for the coarse operators and R / P)
-static bool g_allow_sell = false;    // DFL_SELL=1 enables SELL-C-sigma for irregular matrices
+static bool g_allow_sell = false;    // DFL_SELL=1: SELL-C-sigma for every irregular matrix
 static int g_csr_g = 0;              // DFL_CSR_G=n forces the CSR lanes per row
 static double g_csr_per_lane = 12.0; // DFL_CSR_PER_LANE: target entries per lane
 
@@ -180,7 +180,25 @@ struct dfl_ctx {
     int64_t body_kernels = 0;
     int64_t launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // per-launch profiling of the V-cycle (dfl_ctx_profile_vcycle)
+    bool prof_on = false;
+    std::vector<cudaEvent_t> prof_ev;
+    std::vector<std::string> prof_lab;
+    size_t prof_n = 0;
 };
+
+static void prof_mark(dfl_ctx *ctx, const std::string &label) {
+    if (!ctx->prof_on) return;
+    if (ctx->prof_n >= ctx->prof_ev.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ctx->prof_ev.push_back(e);
+        ctx->prof_lab.emplace_back();
+    }
+    cudaEventRecord(ctx->prof_ev[ctx->prof_n], ctx->st);
+    ctx->prof_lab[ctx->prof_n] = label;
+    ctx->prof_n++;
+}
 
 #define CK(call)                                                                             \
     do {                                                                                     \
@@ -233,6 +251,11 @@ static int build_pipe(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vecto
 // colscale != nullptr: also upload the column-scaled values a_ij * colscale_j
 // in the same layout (shares the index arrays) into *scaled.
 static constexpr int64_t kSigma = 1024;  // SELL-C-sigma sorting window
+// SELL-32-1024 for long-row matrices with enough rows to hide the per-warp
+// width imbalance (measured: L0 restriction and L1 operator, profiles/r01);
+// short-row (P) and small coarse matrices stay CSR-vector
+static constexpr int64_t kSellMinRows = 100000;
+static constexpr double kSellMinMean = 12.0;
 
 static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &bounds,
                          std::vector<int64_t> *bound_tiles = nullptr, bool allow_ell = true,
@@ -274,7 +297,8 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::ve
         for (int64_t s = 0; s <= nsl; ++s) soff[s] = s * 32 * maxlen;
     } else if (allow_ell && (double)soff[nsl] <= 1.03 * nnzd) {
         ell = true;
-    } else if (allow_ell && allow_sell && g_allow_sell && maxlen <= 1024) {
+    } else if (allow_ell && allow_sell && maxlen <= 1024 &&
+               (g_allow_sell || (h.nrows >= kSellMinRows && mean >= kSellMinMean))) {
         perm.resize(h.nrows);
         for (int64_t w0 = 0; w0 < h.nrows; w0 += kSigma) {
             const int64_t w1 = std::min(h.nrows, w0 + kSigma);
@@ -774,8 +798,10 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
             double *next = (l + 1 < L) ? g.lv[l + 1].rv : g.rb;
             RowArgs a{nullptr, v.w, in, nullptr, v.t, nullptr, st};
             launch_rows<MODE_RESID, false>(ctx, v.Aw, a);
+            prof_mark(ctx, "L" + std::to_string(l) + " resid");
             RowArgs b{v.t, nullptr, nullptr, nullptr, next, nullptr, st};
             launch_rows<MODE_PLAIN, false>(ctx, v.R, b);
+            prof_mark(ctx, "L" + std::to_string(l) + " restrict");
         }
         {
             const double *rb = L == 0 ? rin : g.rb;
@@ -783,6 +809,7 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
             k_bottom<<<dim3((unsigned)cdiv(g.max_nb, 32), (unsigned)g.nsub), 256, 0, ctx->st>>>(
                 g.binvT, g.binv_off, g.b_off, rb, xb, st);
             ctx->launches++;
+            prof_mark(ctx, "bottom");
         }
         for (int l = L - 1; l >= 0; --l) {
             DLevel &v = g.lv[l];
@@ -791,6 +818,7 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
             double *out = l == 0 ? zout : v.xv;
             RowArgs a{e, v.w, in, nullptr, v.t, nullptr, st};
             launch_rows<MODE_PROLONG, false>(ctx, v.P, a);
+            prof_mark(ctx, "L" + std::to_string(l) + " prolong");
             if (l == 0 && dot_part) {
                 RowArgs b{v.t, v.w, in, v.t, out, dot_part + poff, st};
                 launch_rows<MODE_POST, true>(ctx, v.A, b);
@@ -799,6 +827,7 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
                 RowArgs b{v.t, v.w, in, v.t, out, nullptr, st};
                 launch_rows<MODE_POST, false>(ctx, v.A, b);
             }
+            prof_mark(ctx, "L" + std::to_string(l) + " post");
         }
         if (L == 0 && dot_part) {
             // bottom-only group: explicit partial dot of this group's rows
@@ -1870,6 +1899,36 @@ int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
     CK(cudaEventElapsedTime(&t, ctx->ev0, ctx->ev1));
     *ms = t / reps;
     return DFL_OK;
+}
+
+// per-launch device times of one V-cycle (mean over reps), labels "L<l> <stage>"
+int dfl_ctx_profile_vcycle(dfl_ctx *ctx, int reps, int cap, double *ms, char *labels /* cap x 32 */) {
+    RC(ready(ctx));
+    if (reps < 1) reps = 1;
+    k_fill<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->r, 1.0, ctx->n);
+    RC(vcycle(ctx, ctx->r, ctx->z, nullptr, nullptr, nullptr));
+    std::vector<double> acc;
+    int count = 0;
+    for (int rep = 0; rep < reps; ++rep) {
+        ctx->prof_on = true;
+        ctx->prof_n = 0;
+        prof_mark(ctx, "start");
+        RC(vcycle(ctx, ctx->r, ctx->z, nullptr, nullptr, nullptr));
+        ctx->prof_on = false;
+        CK(cudaStreamSynchronize(ctx->st));
+        count = (int)ctx->prof_n - 1;
+        acc.resize(count, 0.0);
+        for (int i = 0; i < count; ++i) {
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, ctx->prof_ev[i], ctx->prof_ev[i + 1]));
+            acc[i] += t;
+        }
+    }
+    for (int i = 0; i < count && i < cap; ++i) {
+        ms[i] = acc[i] / reps;
+        std::snprintf(labels + 32 * i, 32, "%s", ctx->prof_lab[i + 1].c_str());
+    }
+    return std::min(count, cap);
 }
 
 }  // extern "C"

@@ -26,6 +26,9 @@ namespace dfl {
 constexpr int kBlock = 256;       // threads per block for row kernels
 constexpr int kKmax = 8;          // max deflation columns per subdomain
 constexpr int kEllUnroll = 8;     // slice widths up to this are fully unrolled
+#ifndef DFL_ELL_BATCH
+#define DFL_ELL_BATCH 8
+#endif
 
 enum { FMT_ELL = 0, FMT_CSR = 1 };
 
@@ -117,20 +120,21 @@ __device__ __forceinline__ double ell_row(const DMat &A, int64_t row, const G &g
         for (int k = 0; k < kEllUnroll; ++k)
             if (k < width) acc = add_rn(acc, mul_rn(v[k], xv[k]));
     } else {
-        for (int k0 = 0; k0 < width; k0 += kEllUnroll) {
-            int c[kEllUnroll];
-            double v[kEllUnroll], xv[kEllUnroll];
+        constexpr int B = DFL_ELL_BATCH;
+        for (int k0 = 0; k0 < width; k0 += B) {
+            int c[B];
+            double v[B], xv[B];
 #pragma unroll
-            for (int k = 0; k < kEllUnroll; ++k)
+            for (int k = 0; k < B; ++k)
                 if (k0 + k < width) {
                     c[k] = ld_stream(cp + 32 * (k0 + k));
                     v[k] = ld_stream(vp + 32 * (k0 + k));
                 }
 #pragma unroll
-            for (int k = 0; k < kEllUnroll; ++k)
+            for (int k = 0; k < B; ++k)
                 if (k0 + k < width) xv[k] = g(c[k]);
 #pragma unroll
-            for (int k = 0; k < kEllUnroll; ++k)
+            for (int k = 0; k < B; ++k)
                 if (k0 + k < width) acc = add_rn(acc, mul_rn(v[k], xv[k]));
         }
     }
@@ -167,7 +171,16 @@ __device__ __forceinline__ double ell_any(const DMat &A, int64_t row, const G &g
 // (all index/value loads in flight before the gathers); full sum returned on
 // all G lanes.  G == 1 keeps the sequential CSR order (bit-identical to
 // spmv_rows).
-constexpr int kCsrUnroll = 8;
+#ifndef DFL_ELL_BATCH
+#define DFL_ELL_BATCH 8
+#endif
+#ifndef DFL_CSR_UNROLL
+#define DFL_CSR_UNROLL 8
+#endif
+#ifndef DFL_CSR_MINB
+#define DFL_CSR_MINB 1
+#endif
+constexpr int kCsrUnroll = DFL_CSR_UNROLL;
 
 template <int G, class Gat>
 __device__ __forceinline__ double csr_row(const DMat &A, int64_t row, int sub, const Gat &g) {
@@ -255,8 +268,11 @@ __device__ __forceinline__ double epilogue(const RowArgs &a, int64_t i, double a
 
 // RESID runs on the pre-scaled matrix A diag(w) (values a_ij * w_j, built at
 // upload), so it gathers r once per entry instead of w and r.
+#ifndef DFL_ELL_MINB
+#define DFL_ELL_MINB 1
+#endif
 template <int MODE, bool DOT, int W>
-__global__ void __launch_bounds__(kBlock) k_ell(DMat A, RowArgs a) {
+__global__ void __launch_bounds__(kBlock, DFL_ELL_MINB) k_ell(DMat A, RowArgs a) {
     const int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x;  // storage slot
     double dot = 0.0;
     if (j < A.nrows) {
@@ -279,7 +295,7 @@ __global__ void __launch_bounds__(kBlock) k_ell(DMat A, RowArgs a) {
 }
 
 template <int G, int MODE, bool DOT>
-__global__ void __launch_bounds__(kBlock) k_csr(DMat A, RowArgs a) {
+__global__ void __launch_bounds__(kBlock, DFL_CSR_MINB) k_csr(DMat A, RowArgs a) {
     constexpr int RPB = kBlock / G;
     const int64_t i = (int64_t)blockIdx.x * RPB + threadIdx.x / G;
     const int sub = threadIdx.x % G;
