@@ -20,6 +20,7 @@
 #include "host_setup.hpp"
 #include "kernels.cuh"
 #include "spmv_pipe.cuh"
+#include "coarse.cuh"
 
 using namespace dfl;
 
@@ -74,6 +75,8 @@ Nccl g_nccl;
 }  // namespace
 
 static bool g_use_pipe = false;  // TMA-staged variant (DFL_PIPE=1); see profiles/r01
+static bool g_use_coarse = false;  // cooperative coarse-cycle kernel (DFL_COARSE=1; measured slower, profiles/r01)
+static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle
 // layout experiments (profiling knobs, read once per context creation)
 // (measured on 150^3, see profiles/r01/README.md: CSR-vector with ~12 entries
 // per lane beats SELL-32-1024 for the coarse operators and R / P)
@@ -103,6 +106,11 @@ struct VGroup {
     int64_t *binv_off = nullptr;     // per subdomain offset into binvT
     int64_t *b_off = nullptr;        // nsub + 1 row offsets in rb
     int max_nb = 0;
+    // levels [lc, L) and the bottom run in one cooperative kernel (coarse.cuh)
+    int lc = -1;                     // -1: no coarse kernel
+    CoarseArgs *cargs = nullptr;     // device copy
+    unsigned coarse_grid = 0;
+    double *binv = nullptr;          // row-major inverses for the cooperative kernel
     // host-side statistics
     std::vector<int64_t> nnzA, nnzP, rows;
 };
@@ -792,7 +800,8 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
         const double *rin = r + g.row0;
         double *zout = z + g.row0;
         const int L = (int)g.lv.size();
-        for (int l = 0; l < L; ++l) {
+        const int lc = (g.lc >= 0 && g_use_coarse) ? g.lc : L + 1;  // first level of the cooperative kernel
+        for (int l = 0; l < std::min(L, lc); ++l) {
             DLevel &v = g.lv[l];
             const double *in = l == 0 ? rin : v.rv;
             double *next = (l + 1 < L) ? g.lv[l + 1].rv : g.rb;
@@ -803,7 +812,18 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
             launch_rows<MODE_PLAIN, false>(ctx, v.R, b);
             prof_mark(ctx, "L" + std::to_string(l) + " restrict");
         }
-        {
+        if (lc <= L) {
+            const double *crin = lc == 0 ? rin : g.lv[lc < L ? lc : 0].rv;
+            double *cxout = lc == 0 ? zout : g.lv[lc < L ? lc : 0].xv;
+            if (lc == L && L > 0) {  // bottom only
+                crin = g.rb;
+                cxout = g.xb;
+            }
+            void *args[] = {(void *)&g.cargs, (void *)&crin, (void *)&cxout};
+            cudaLaunchCooperativeKernel((const void *)k_coarse_cycle, g.coarse_grid, 256, args, 0, ctx->st);
+            ctx->launches++;
+            prof_mark(ctx, "coarse L" + std::to_string(lc) + "+");
+        } else {
             const double *rb = L == 0 ? rin : g.rb;
             double *xb = L == 0 ? zout : g.xb;
             k_bottom<<<dim3((unsigned)cdiv(g.max_nb, 32), (unsigned)g.nsub), 256, 0, ctx->st>>>(
@@ -811,7 +831,7 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
             ctx->launches++;
             prof_mark(ctx, "bottom");
         }
-        for (int l = L - 1; l >= 0; --l) {
+        for (int l = std::min(L, lc) - 1; l >= 0; --l) {
             DLevel &v = g.lv[l];
             const double *in = l == 0 ? rin : v.rv;
             const double *e = (l + 1 < L) ? g.lv[l + 1].xv : g.xb;
@@ -829,8 +849,8 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
             }
             prof_mark(ctx, "L" + std::to_string(l) + " post");
         }
-        if (L == 0 && dot_part) {
-            // bottom-only group: explicit partial dot of this group's rows
+        if ((L == 0 || lc == 0) && dot_part) {
+            // the group's finest level ran without a fused dot: explicit partials
             const int64_t rows = g.row1 - g.row0;
             const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(rows, kBlock), 64));
             k_dot<<<nb, kBlock, 0, ctx->st>>>(rin, zout, rows, dot_part + poff, st);
@@ -1372,6 +1392,49 @@ static int build_groups(dfl_ctx *ctx) {
             RC(dalloc(ctx, &g.rb, g.nb));
             RC(dalloc(ctx, &g.xb, g.nb));
         }
+        {
+            // row-major inverses and the argument block of the cooperative kernel
+            std::vector<double> binv;
+            for (int j = s; j < e; ++j) {
+                const auto &bi = ctx->pending[j].levels.back().bottom_inv;
+                binv.insert(binv.end(), bi.begin(), bi.end());
+            }
+            RC(upload(ctx, &g.binv, binv.data(), (int64_t)binv.size()));
+            int lc = L;
+            for (int l = 0; l < L; ++l)
+                if (g.rows[l] <= kCoarseRows) {
+                    lc = l;
+                    break;
+                }
+            if (L - lc <= kMaxCoarse) {
+                CoarseArgs ca{};
+                ca.nlev = L - lc;
+                for (int l = lc; l < L; ++l) {
+                    const DLevel &v = g.lv[l];
+                    CLevel &cl = ca.lv[l - lc];
+                    cl.A = v.A;
+                    cl.Aw = v.Aw;
+                    cl.P = v.P;
+                    cl.R = v.R;
+                    cl.w = v.w;
+                    cl.rv = v.rv;
+                    cl.t = v.t;
+                    cl.xv = v.xv;
+                }
+                ca.binv = g.binv;
+                ca.binv_off = g.binv_off;
+                ca.b_off = g.b_off;
+                ca.nsub = g.nsub;
+                ca.nb = g.nb;
+                ca.rb = g.rb;
+                ca.xb = g.xb;
+                RC(upload(ctx, &g.cargs, &ca, 1));
+                int bps = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_coarse_cycle, 256, 0));
+                g.coarse_grid = (unsigned)(std::max(1, std::min(bps, 2)) * ctx->sm_count);
+                g.lc = bps > 0 ? lc : -1;
+            }
+        }
         if (g.max_nb > (1 << 20)) {
             ctx->err = "bottom level too large for shared-memory staging";
             return DFL_E_DIMENSION;
@@ -1488,6 +1551,8 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
         pipe_attrs();
         const char *np = getenv("DFL_PIPE");
         g_use_pipe = np && np[0] == '1';
+        const char *nc = getenv("DFL_COARSE");
+        g_use_coarse = nc && nc[0] == '1';
         const char *ns = getenv("DFL_SELL");
         g_allow_sell = ns && ns[0] == '1';
         const char *cg = getenv("DFL_CSR_G");
@@ -1708,7 +1773,10 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
     for (auto &g : ctx->groups)
         vparts += g.lv.empty() ? std::max<int64_t>(1, std::min<int64_t>(cdiv(g.row1 - g.row0, kBlock), 64))
                                : parts_for(g.lv[0].A);
-    RC(dalloc(ctx, &ctx->dpart, std::max(ctx->nblk, vparts) + 64));
+    // partial-sum scratch: one slot per block of the row kernels, or 3 per
+    // block of the multi-dot kernels (grid <= 4 * SMs)
+    const int64_t dslots = std::max({ctx->nblk, vparts, 3 * std::max<int64_t>(ctx->nblk, 4 * ctx->sm_count)});
+    RC(dalloc(ctx, &ctx->dpart, dslots + 64));
     RC(dalloc(ctx, &ctx->zt_part, std::max(ctx->ntiles, ctx->Aop.pipe.ntiles) * kKmax + 64));
     RC(dalloc(ctx, &ctx->scal, 16));
     RC(dalloc(ctx, &ctx->sgather, (int64_t)8 * ctx->nranks));
