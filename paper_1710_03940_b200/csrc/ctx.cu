@@ -264,6 +264,8 @@ static constexpr int64_t kSigma = 1024;  // SELL-C-sigma sorting window
 // short-row (P) and small coarse matrices stay CSR-vector
 static constexpr int64_t kSellMinRows = 100000;
 static constexpr double kSellMinMean = 12.0;
+static constexpr double kShortRowMean = 8.0;  // DFL_SHORT_PAD=x overrides the padding limit below
+static double kShortRowPad = 1.7;
 
 static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &bounds,
                          std::vector<int64_t> *bound_tiles = nullptr, bool allow_ell = true,
@@ -298,7 +300,8 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::ve
     const double mean = h.nrows ? (double)m.nnz / (double)h.nrows : 0.0;
     const double nnzd = (double)m.nnz + 64.0;
     bool ell = false;
-    if (allow_ell && maxlen <= 8 && (double)(nsl * 32 * maxlen) <= 1.03 * nnzd) {
+    const double upad = mean <= kShortRowMean ? kShortRowPad : 1.03;  // short rows: padding is cheaper than CSR
+    if (allow_ell && maxlen <= 8 && (double)(nsl * 32 * maxlen) <= upad * nnzd) {
         // uniform slice width: the kernels compute slice offsets instead of loading them
         ell = true;
         m.ell_w = (int)maxlen;
@@ -324,6 +327,13 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::ve
         }
     }
     if (!ell && allow_ell && maxlen <= 32 && (double)soff[nsl] <= 1.2 * nnzd) ell = true;
+    // short rows (prolongation, ~4 entries): coalesced sliced ELL beats 1-lane
+    // CSR even with ~40% padding (profiles/r01)
+    if (!ell && allow_ell && mean <= kShortRowMean && maxlen <= 16 && (double)soff[nsl] <= kShortRowPad * nnzd) {
+        ell = true;
+        perm.clear();
+        soff = slice_offsets(perm, maxlen);
+    }
     if (ell) {
         m.fmt = FMT_ELL;
         m.stored = soff[nsl];
@@ -1551,6 +1561,8 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
         pipe_attrs();
         const char *np = getenv("DFL_PIPE");
         g_use_pipe = np && np[0] == '1';
+        const char *sp = getenv("DFL_SHORT_PAD");
+        kShortRowPad = sp ? atof(sp) : 1.7;
         const char *nc = getenv("DFL_COARSE");
         g_use_coarse = nc && nc[0] == '1';
         const char *ns = getenv("DFL_SELL");

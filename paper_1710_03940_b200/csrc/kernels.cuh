@@ -161,10 +161,58 @@ __device__ __forceinline__ double ell_row_w(const DMat &A, int64_t row, const G 
     return acc;
 }
 
+// sliced ELL, width known per slice: dispatch to a compile-time width so the
+// register footprint is that of the widest case actually compiled (<= 8)
+template <int W, class G>
+__device__ __forceinline__ double ell_slice_w(const DMat &A, int64_t off, const G &g) {
+    const int *cp = A.col + off;
+    const double *vp = A.val + off;
+    int c[W];
+    double v[W];
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        c[k] = ld_stream(cp + 32 * k);
+        v[k] = ld_stream(vp + 32 * k);
+    }
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < W; ++k) acc = add_rn(acc, mul_rn(v[k], g(c[k])));
+    return acc;
+}
+
+// chunk of w <= 8 entries of a sliced row, accumulated into acc in order
+template <class G>
+__device__ __forceinline__ double ell_chunk(const DMat &A, int64_t o, int w, double acc, const G &g) {
+    // exact sequential order, fixed 8-wide predicated batch
+    int c[8];
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (k < w) {
+            c[k] = ld_stream(A.col + o + 32 * k);
+            v[k] = ld_stream(A.val + o + 32 * k);
+        }
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (k < w) acc = add_rn(acc, mul_rn(v[k], g(c[k])));
+    return acc;
+}
+
+template <class G>
+__device__ __forceinline__ double ell_row_sliced(const DMat &A, int64_t row, const G &g) {
+    const int64_t s = row >> 5;
+    const int64_t off = __ldg(A.slice_off + s);
+    const int width = (int)((__ldg(A.slice_off + s + 1) - off) >> 5);
+    const int64_t o = off + (row & 31);
+    double acc = 0.0;
+    for (int k0 = 0; k0 < width; k0 += 8) acc = ell_chunk(A, o + 32 * k0, min(8, width - k0), acc, g);
+    return acc;
+}
+
 template <int W, class G>
 __device__ __forceinline__ double ell_any(const DMat &A, int64_t row, const G &g) {
     if (W > 0) return ell_row_w<(W > 0 ? W : 1)>(A, row, g);
-    return ell_row(A, row, g);
+    return ell_row_sliced(A, row, g);  // slice_off is stored for uniform widths too
 }
 
 // CSR row by G lanes with the entry loads of a lane batched kCsrUnroll deep

@@ -1,5 +1,4 @@
 #!/bin/bash
-# full V-cycle breakdown: CSR-vector vs SELL-32-1024 for the irregular matrices
-for cfg in "" "DFL_SELL=1"; do
-  echo "== $cfg"; env $cfg timeout 200 python tools/prof_kernels.py --reps 20 2>&1 | tail -18
+for cfg in "DFL_SHORT_PAD=1.0" "DFL_SHORT_PAD=1.7" "DFL_SHORT_PAD=1.7 DFL_SELL=1"; do
+  echo "== $cfg"; env $cfg timeout 200 python tools/prof_kernels.py --reps 20 2>&1 | tail -18 | grep -E "vcycle|L0|L1"
 done
