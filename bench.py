@@ -264,7 +264,7 @@ def b200_arm(args, ws, rank, local):
     spmv_gbs = spmv_bytes / (spmv_ms * 1e-3) / 1e9
     vc_gbs = vc_bytes / (vc_ms * 1e-3) / 1e9
     traffic = None
-    try:
+    try:  # DRAM bytes per launch of the same kernel from the committed ncu --set full capture
         with open(os.path.join(REPO, "profiles", "ncu_summary.json")) as fh:
             traffic = json.load(fh).get("op_spmv_dram_bytes_per_launch")
     except Exception:

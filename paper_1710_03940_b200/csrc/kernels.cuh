@@ -319,8 +319,11 @@ __device__ __forceinline__ double epilogue(const RowArgs &a, int64_t i, double a
 #ifndef DFL_ELL_MINB
 #define DFL_ELL_MINB 1
 #endif
+#ifndef DFL_ELL_MINB0
+#define DFL_ELL_MINB0 1
+#endif
 template <int MODE, bool DOT, int W>
-__global__ void __launch_bounds__(kBlock, DFL_ELL_MINB) k_ell(DMat A, RowArgs a) {
+__global__ void __launch_bounds__(kBlock, W == 0 ? DFL_ELL_MINB0 : DFL_ELL_MINB) k_ell(DMat A, RowArgs a) {
     const int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x;  // storage slot
     double dot = 0.0;
     if (j < A.nrows) {

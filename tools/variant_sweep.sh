@@ -1,4 +1,4 @@
 #!/bin/bash
-for cfg in "DFL_SHORT_PAD=1.0" "DFL_SHORT_PAD=1.7" "DFL_SHORT_PAD=1.7 DFL_SELL=1"; do
-  echo "== $cfg"; env $cfg timeout 200 python tools/prof_kernels.py --reps 20 2>&1 | tail -18 | grep -E "vcycle|L0|L1"
+for lib in tools/variants/*.so; do
+  echo "== $lib"; DFL_LIB=$lib timeout 200 python tools/prof_kernels.py --reps 20 2>&1 | grep -E "vcycle|L0 restrict|L1 resid|L1 post"
 done
