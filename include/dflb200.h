@@ -219,7 +219,10 @@ int dfl_spmv_csr(const dfl_csr *A, const double *x, double *y, int device);
 /* timing of the unit operations for the roofline: runs `reps` back-to-back
  * launches of the named kernel family on the context's data and returns the
  * mean device milliseconds per launch and the algorithmic bytes per launch.
- *   what: 0 = operator SpMV (fine A), 1 = V-cycle, 2 = CG iteration */
+ *   what: 0 = operator SpMV (fine A; CSR fp64/int32 algorithmic bytes),
+ *         1 = V-cycle (bytes of SURVEY §8(d): CSR layouts),
+ *         2 = V-cycle (bytes the stored layouts actually need: ELL padding,
+ *             1-byte codes of FMT_CODE matrices, the w.*r pass) */
 int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms_per_launch, double *bytes_per_launch);
 
 /* per-launch device times of one V-cycle, mean over reps; labels is a

@@ -63,6 +63,15 @@ __device__ __forceinline__ void grid_rows(const DMat &A, const RowArgs &a, int64
 
 template <int MODE>
 __device__ __forceinline__ void grid_stage(const DMat &A, const RowArgs &a, int64_t gtid, int64_t gthreads) {
+    if (A.fmt == FMT_CODE) {  // code table read through L1; RESID gathers w_j * r_j on the fly
+        for (int64_t i = gtid; i < A.nrows; i += gthreads) {
+            const double ax = MODE == MODE_RESID
+                                  ? code_row_g(A, i, GatherWR{a.w, a.r}, A.ctab_delta, A.ctab_val)
+                                  : code_row_g(A, i, GatherX{a.x}, A.ctab_delta, A.ctab_val);
+            a.out[i] = epilogue<MODE>(a, i, ax);
+        }
+        return;
+    }
     if (A.fmt == FMT_ELL) {
         grid_rows<MODE, 0>(A, a, gtid, gthreads);
         return;

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <memory>
+#include <unordered_map>
 #include <string>
 #include <vector>
 
@@ -75,6 +76,7 @@ Nccl g_nccl;
 }  // namespace
 
 static bool g_use_pipe = false;  // TMA-staged variant (DFL_PIPE=1); see profiles/r01
+static bool g_use_code = true;    // stencil-coded ELL for few-(offset, value) matrices (DFL_NO_CODE=1 disables)
 static bool g_use_coarse = false;  // cooperative coarse-cycle kernel (DFL_COARSE=1; measured slower, profiles/r01)
 static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle
 // layout experiments (profiling knobs, read once per context creation)
@@ -89,6 +91,7 @@ static double g_csr_per_lane = 12.0; // DFL_CSR_PER_LANE: target entries per lan
 struct DLevel {
     DMat A, P, R;
     DMat Aw;  // A diag(w): the pre-smoothing residual r - A (w .* r) in one gather
+    double *wr = nullptr;  // coded A: w .* r gathered by the residual kernel
     double *w = nullptr;
     int64_t n = 0, nc = 0;
     double *rv = nullptr;  // level right-hand side (l >= 1)
@@ -258,6 +261,60 @@ static int build_pipe(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vecto
 
 // colscale != nullptr: also upload the column-scaled values a_ij * colscale_j
 // in the same layout (shares the index arrays) into *scaled.
+// FMT_CODE encoder: every row <= 8 entries and <= 255 distinct (column - row,
+// value-bits) pairs; returns false when the matrix does not qualify
+static int try_upload_code(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) {
+    ok = false;
+    struct Key {
+        int64_t d;
+        uint64_t v;
+        bool operator==(const Key &o) const { return d == o.d && v == o.v; }
+    };
+    struct KH {
+        size_t operator()(const Key &k) const { return std::hash<int64_t>()(k.d) * 1000003u ^ std::hash<uint64_t>()(k.v); }
+    };
+    std::unordered_map<Key, int, KH> dict;
+    std::vector<int> delta;
+    std::vector<double> val;
+    std::vector<uint8_t> codes((size_t)h.nrows * 8, (uint8_t)kCodePad);
+    for (int64_t i = 0; i < h.nrows; ++i) {
+        const int64_t b = h.ptr[i], e = h.ptr[i + 1];
+        if (e - b > 8) return DFL_OK;
+        for (int64_t k = b; k < e; ++k) {
+            uint64_t bits;
+            std::memcpy(&bits, &h.val[k], 8);
+            const int64_t d = h.col[k] - i;
+            if (d < INT32_MIN || d > INT32_MAX) return DFL_OK;
+            auto it = dict.find(Key{d, bits});
+            int code;
+            if (it == dict.end()) {
+                if (dict.size() >= kCodePad) return DFL_OK;
+                code = (int)dict.size();
+                dict.emplace(Key{d, bits}, code);
+                delta.push_back((int)d);
+                val.push_back(h.val[k]);
+            } else {
+                code = it->second;
+            }
+            codes[(size_t)i * 8 + (k - b)] = (uint8_t)code;
+        }
+    }
+    m.fmt = FMT_CODE;
+    m.stored = m.nnz;
+    m.ncodes = (int)delta.size();
+    uint8_t *d_codes;
+    int *d_delta;
+    double *d_val;
+    RC(upload(ctx, &d_codes, codes.data(), (int64_t)codes.size()));
+    RC(upload(ctx, &d_delta, delta.data(), (int64_t)std::max<size_t>(1, delta.size())));
+    RC(upload(ctx, &d_val, val.data(), (int64_t)std::max<size_t>(1, val.size())));
+    m.codes = reinterpret_cast<const uint2 *>(d_codes);
+    m.ctab_delta = d_delta;
+    m.ctab_val = d_val;
+    ok = true;
+    return DFL_OK;
+}
+
 static constexpr int64_t kSigma = 1024;  // SELL-C-sigma sorting window
 // SELL-32-1024 for long-row matrices with enough rows to hide the per-warp
 // width imbalance (measured: L0 restriction and L1 operator, profiles/r01);
@@ -269,7 +326,8 @@ static double kShortRowPad = 1.7;
 
 static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &bounds,
                          std::vector<int64_t> *bound_tiles = nullptr, bool allow_ell = true,
-                         const double *colscale = nullptr, DMat *scaled = nullptr, bool allow_sell = true) {
+                         const double *colscale = nullptr, DMat *scaled = nullptr, bool allow_sell = true,
+                         bool allow_code = true) {
     m = DMat{};
     m.nrows = h.nrows;
     m.ncols = h.ncols;
@@ -277,6 +335,14 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::ve
     if (h.ncols >= INT32_MAX || m.nnz >= INT32_MAX) {
         ctx->err = "matrix too large for int32 device indices";
         return DFL_E_DIMENSION;
+    }
+    if (g_use_code && allow_code && allow_ell && h.nrows > 0) {
+        bool ok = false;
+        RC(try_upload_code(ctx, h, m, ok));
+        if (ok) {
+            if (colscale) *scaled = m;  // RESID on a coded matrix gathers w .* r instead (k_wr)
+            return DFL_OK;
+        }
     }
     const int64_t nsl = cdiv(h.nrows, 32);
     auto rlen = [&](int64_t i) { return h.ptr[i + 1] - h.ptr[i]; };
@@ -481,12 +547,22 @@ static int build_pipe(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vecto
 // ---------------------------------------------------------------------------
 // kernel launch helpers
 
-static int rows_per_block(const DMat &A) { return A.fmt == FMT_ELL ? kBlock : kBlock / A.group; }
+static int rows_per_block(const DMat &A) { return A.fmt == FMT_CSR ? kBlock / A.group : kBlock; }
 
 static int64_t nblocks_for(const DMat &A) { return cdiv(A.nrows, rows_per_block(A)); }
 
+static int g_sm_count = 148;
+
+// grid of the grid-stride FMT_CODE kernels
+static int64_t code_grid(const dfl_ctx *, const DMat &A) {
+    return std::max<int64_t>(1, std::min<int64_t>(cdiv(A.nrows, kBlock), 8 * (int64_t)g_sm_count));
+}
+
 // number of per-block / per-tile partials a row kernel on A produces
-static int64_t parts_for(const DMat &A) { return A.pipe.stages ? A.pipe.ntiles : nblocks_for(A); }
+static int64_t parts_for(const DMat &A) {
+    if (A.fmt == FMT_CODE) return code_grid(nullptr, A);
+    return A.pipe.stages ? A.pipe.ntiles : nblocks_for(A);
+}
 
 static size_t pipe_smem(const DMat &A) { return 128 + (size_t)A.pipe.stages * A.pipe.cap * 12; }
 
@@ -553,6 +629,11 @@ static void launch_csr_mode(const DMat &A, const RowArgs &a, cudaStream_t st) {
 template <int MODE, bool DOT>
 static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
     if (A.nrows == 0) return;
+    if (A.fmt == FMT_CODE) {
+        k_code<MODE, DOT><<<(unsigned)code_grid(ctx, A), kBlock, 0, ctx->st>>>(A, a);
+        ctx->launches++;
+        return;
+    }
     if (g_use_pipe) {
         SpArgs s;
         s.x = a.x;
@@ -602,7 +683,9 @@ static void launch_op(dfl_ctx *ctx, const OpArgs &a) {
     }
     const unsigned grid = (unsigned)ctx->ntiles;
     if (grid == 0) return;
-    if (A.fmt == FMT_ELL) {
+    if (A.fmt == FMT_CODE) {
+        k_op_code<OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a);
+    } else if (A.fmt == FMT_ELL) {
         const SubTable &S = ctx->subtab;
         switch (A.ell_w) {
             case 5: k_op_ell<OPMODE, 5><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, S, a); break;
@@ -815,8 +898,15 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
             DLevel &v = g.lv[l];
             const double *in = l == 0 ? rin : v.rv;
             double *next = (l + 1 < L) ? g.lv[l + 1].rv : g.rb;
-            RowArgs a{nullptr, v.w, in, nullptr, v.t, nullptr, st};
-            launch_rows<MODE_RESID, false>(ctx, v.Aw, a);
+            if (v.A.fmt == FMT_CODE) {
+                k_wr<<<(unsigned)cdiv(v.n, kBlock), kBlock, 0, ctx->st>>>(v.w, in, v.wr, v.n);
+                ctx->launches++;
+                RowArgs a{v.wr, v.w, in, nullptr, v.t, nullptr, st};
+                launch_rows<MODE_RESID, false>(ctx, v.A, a);
+            } else {
+                RowArgs a{nullptr, v.w, in, nullptr, v.t, nullptr, st};
+                launch_rows<MODE_RESID, false>(ctx, v.Aw, a);
+            }
             prof_mark(ctx, "L" + std::to_string(l) + " resid");
             RowArgs b{v.t, nullptr, nullptr, nullptr, next, nullptr, st};
             launch_rows<MODE_PLAIN, false>(ctx, v.R, b);
@@ -1366,6 +1456,7 @@ static int build_groups(dfl_ctx *ctx) {
             }
             OwnedRows A = merge_blocks(As, fo), P = merge_blocks(Ps, co), R = merge_blocks(Rs, fo);
             RC(upload_matrix(ctx, A.view(), v.A, {0, A.nrows}, nullptr, true, w.data(), &v.Aw));
+            if (v.A.fmt == FMT_CODE) RC(dalloc(ctx, &v.wr, A.nrows));
             RC(upload_matrix(ctx, P.view(), v.P, {0, P.nrows}));
             RC(upload_matrix(ctx, R.view(), v.R, {0, R.nrows}));
             RC(upload(ctx, &v.w, w.data(), (int64_t)w.size()));
@@ -1557,10 +1648,13 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
     if (e == cudaSuccess) e = cudaEventCreate(&ctx->ev1);
     if (e == cudaSuccess) e = cudaMallocHost(&ctx->h_state, sizeof(KState));
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+    if (e == cudaSuccess) g_sm_count = ctx->sm_count;
     if (e == cudaSuccess) {
         pipe_attrs();
         const char *np = getenv("DFL_PIPE");
         g_use_pipe = np && np[0] == '1';
+        const char *ncd = getenv("DFL_NO_CODE");
+        g_use_code = !(ncd && ncd[0] == '1');
         const char *sp = getenv("DFL_SHORT_PAD");
         kShortRowPad = sp ? atof(sp) : 1.7;
         const char *nc = getenv("DFL_COARSE");
@@ -1655,7 +1749,9 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
     ctx->nsub = nsub;
     ctx->sub_off.assign(sub_offsets, sub_offsets + nsub + 1);
     HostRows h{A->nrows, A->ncols, A->row_ptr, A->col_idx, A->values};
-    RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, &ctx->op_sub_tiles_h, true, nullptr, nullptr, false));
+    // the operator stays uniform ELL (at the HBM roofline, 99.9%); FMT_CODE only
+    // pays off for the V-cycle kernels with longer epilogues (profiles/r01)
+    RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, &ctx->op_sub_tiles_h, true, nullptr, nullptr, false, false));
     if (ctx->Aop.pipe.stages) RC(upload(ctx, &ctx->op_sub_tiles, ctx->op_sub_tiles_h.data(), (int64_t)ctx->op_sub_tiles_h.size()));
     ctx->op_nnz = ctx->Aop.nnz;
     int64_t nrecv = 0;
@@ -1950,12 +2046,33 @@ int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
     if (reps < 1) reps = 1;
     auto run = [&]() -> int {
         if (what == 0) return op_apply_dev(ctx, ctx->p, ctx->w, 0, nullptr, false, nullptr, 0);
-        if (what == 1) return vcycle(ctx, ctx->r, ctx->z, nullptr, nullptr, nullptr);
+        if (what == 1 || what == 2) return vcycle(ctx, ctx->r, ctx->z, nullptr, nullptr, nullptr);
         ctx->err = "unknown timing target";
         return DFL_E_CONFIG;
     };
+    // bytes the stored format must move for one pass over M
+    auto mat = [](const DMat &M) -> double {
+        const double rows = (double)M.nrows;
+        if (M.fmt == FMT_CODE) return 8.0 * rows;
+        if (M.fmt == FMT_CSR) return 12.0 * (double)M.nnz + 4.0 * (rows + 1);
+        return 12.0 * (double)M.stored + (M.perm ? 4.0 * rows : 0.0) + (M.ell_w ? 0.0 : 8.0 * (rows / 32 + 1));
+    };
     if (what == 0) {
         *bytes = 12.0 * ctx->op_nnz + 4.0 * (ctx->n + 1) + 8.0 * (ctx->n + ctx->n_ghost) + 8.0 * ctx->n;
+    } else if (what == 2) {
+        double b = 0;
+        for (auto &g : ctx->groups) {
+            for (size_t l = 0; l < g.lv.size(); ++l) {
+                const DLevel &v = g.lv[l];
+                const double n = (double)g.rows[l], nc = (double)g.rows[l + 1];
+                b += v.A.fmt == FMT_CODE ? 24.0 * n + mat(v.A) + 24.0 * n : mat(v.Aw) + 24.0 * n;  // residual
+                b += mat(v.R) + 8.0 * n + 8.0 * nc;                                                // restriction
+                b += mat(v.P) + 8.0 * nc + 24.0 * n;                                               // prolongation
+                b += mat(v.A) + 40.0 * n;                                                          // post-smoothing
+            }
+            b += 8.0 * (double)g.nb * (double)g.nb / std::max(1, g.nsub) + 16.0 * (double)g.nb;
+        }
+        *bytes = b;
     } else {
         double b = 0;
         for (auto &g : ctx->groups) {

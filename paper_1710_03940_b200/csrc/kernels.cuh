@@ -30,7 +30,14 @@ constexpr int kEllUnroll = 8;     // slice widths up to this are fully unrolled
 #define DFL_ELL_BATCH 8
 #endif
 
-enum { FMT_ELL = 0, FMT_CSR = 1 };
+enum { FMT_ELL = 0, FMT_CSR = 1, FMT_CODE = 2 };
+
+// FMT_CODE ("stencil-coded ELL"): every row holds <= 8 one-byte codes; code c
+// stands for the pair (column - row, value) of a per-matrix table of <= 255
+// pairs (255 = padding).  Lossless for matrices with few distinct
+// (offset, value) pairs -- structured-grid operators: the 7-point Poisson
+// operator has 7 -- and 8 bytes per row instead of 12 per entry.
+constexpr unsigned kCodePad = 255u;
 
 // row tiles of one matrix for the TMA-pipelined kernels (spmv_pipe.cuh):
 // rows [row0, row1), entries [e0, e0 + ecnt) of the value / index arrays
@@ -56,6 +63,11 @@ struct DMat {
     const int *col = nullptr;
     const double *val = nullptr;
     const int *perm = nullptr;           // SELL-C-sigma: slot -> row (nullptr: identity)
+    // FMT_CODE
+    const uint2 *codes = nullptr;        // 8 codes per row, row-major
+    const int *ctab_delta = nullptr;     // column - row of each code
+    const double *ctab_val = nullptr;    // value of each code
+    int ncodes = 0;
 };
 
 // run-time state of one Krylov solve (device resident)
@@ -86,6 +98,46 @@ struct GatherWR {
     const double *__restrict__ r;
     __device__ __forceinline__ double operator()(int c) const { return mul_rn(__ldg(w + c), __ldg(r + c)); }
 };
+
+// code table into shared memory (called by all threads of the block)
+__device__ __forceinline__ void load_codes(const DMat &A, int *sd, double *sv) {
+    for (int t = threadIdx.x; t < A.ncodes; t += blockDim.x) {
+        sd[t] = A.ctab_delta[t];
+        sv[t] = A.ctab_val[t];
+    }
+    __syncthreads();
+}
+
+// sum_k val(c_k) * g(row + delta(c_k)) in storage (= CSR) order, no FMA:
+// bit-identical to spmv_rows
+template <class G>
+__device__ __forceinline__ double code_row_w(uint2 cw, int64_t row, const G &g, const int *sd, const double *sv) {
+    unsigned c[8];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        c[k] = (cw.x >> (8 * k)) & 0xffu;
+        c[k + 4] = (cw.y >> (8 * k)) & 0xffu;
+    }
+    double xv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (c[k] != kCodePad) xv[k] = g((int)(row + sd[c[k]]));
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (c[k] != kCodePad) acc = add_rn(acc, mul_rn(sv[c[k]], xv[k]));
+    return acc;
+}
+
+template <class G>
+__device__ __forceinline__ double code_row_g(const DMat &A, int64_t row, const G &g, const int *sd, const double *sv) {
+    return code_row_w(__ldcs(A.codes + row), row, g, sd, sv);
+}
+
+__device__ __forceinline__ double code_row(const DMat &A, int64_t row, const double *__restrict__ xg,
+                                           const int *sd, const double *sv) {
+    return code_row_g(A, row, GatherX{xg}, sd, sv);
+}
 
 // sequential, CSR-ordered row sum of an ELL row (bit-identical to spmv_rows)
 template <class G>
@@ -345,6 +397,43 @@ __global__ void __launch_bounds__(kBlock, W == 0 ? DFL_ELL_MINB0 : DFL_ELL_MINB)
     }
 }
 
+// FMT_CODE row kernel, grid-stride (the code table is staged once per block;
+// the next rows' codes are requested before the table load completes).
+// MODE_RESID: a.x holds w .* r (computed by k_wr), so t = r - A (w .* r)
+// keeps the reference's arithmetic exactly.  DOT: one partial per block.
+template <int MODE, bool DOT>
+__global__ void __launch_bounds__(kBlock) k_code(DMat A, RowArgs a) {
+    __shared__ int sd[256];
+    __shared__ double sv[256];
+    const int64_t stride = (int64_t)gridDim.x * kBlock;
+    int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    uint2 cw = i < A.nrows ? __ldcs(A.codes + i) : make_uint2(~0u, ~0u);
+    load_codes(A, sd, sv);
+    double dot = 0.0;
+    for (; i < A.nrows; i += stride) {
+        const int64_t inext = i + stride;
+        const uint2 cn = inext < A.nrows ? __ldcs(A.codes + inext) : make_uint2(~0u, ~0u);
+        const double ax = code_row_w(cw, i, GatherX{a.x}, sd, sv);
+        const double y = epilogue<MODE>(a, i, ax);
+        a.out[i] = y;
+        if (DOT) dot += __ldg(a.r + i) * y;
+        cw = cn;
+    }
+    if (DOT) {
+        __shared__ double sm[32];
+        double v[1] = {dot};
+        block_sum<1>(v, sm);
+        if (threadIdx.x == 0) a.dot_part[blockIdx.x] = v[0];
+    }
+}
+
+// wr = w .* r  (the relaxation x = w r of amg.py:193/195, rounded as there)
+__global__ void __launch_bounds__(kBlock) k_wr(const double *__restrict__ w, const double *__restrict__ r, double *wr,
+                                               int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (i < n) wr[i] = mul_rn(w[i], r[i]);
+}
+
 template <int G, int MODE, bool DOT>
 __global__ void __launch_bounds__(kBlock, DFL_CSR_MINB) k_csr(DMat A, RowArgs a) {
     constexpr int RPB = kBlock / G;
@@ -494,6 +583,36 @@ __global__ void __launch_bounds__(kBlock) k_op_ell(DMat A, Tiles T, SubTable S, 
         block_sum<kKmax>(acc, sm);
         if (threadIdx.x == 0)
             #pragma unroll
+            for (int c = 0; c < kKmax; ++c)
+                if (c < a.k) a.zt_part[t * a.k + c] = acc[c];
+    }
+}
+
+template <int OPMODE>
+__global__ void __launch_bounds__(kBlock) k_op_code(DMat A, Tiles T, SubTable S, OpArgs a) {
+    if (a.need_refresh && !a.st->refresh_now) return;
+    __shared__ int sd[256];
+    __shared__ double sv[256];
+    const int64_t t = blockIdx.x;
+    int64_t r0, r1;
+    tile_rows(S, T, t, r0, r1);
+    const int64_t i = r0 + threadIdx.x;
+    const bool valid = i < r1;
+    const uint2 cw = valid ? __ldcs(A.codes + i) : make_uint2(~0u, ~0u);  // in flight during the table load
+    load_codes(A, sd, sv);
+    double y = 0.0;
+    if (valid) {
+        const double ax = code_row_w(cw, i, GatherX{a.x}, sd, sv);
+        y = OPMODE == 1 ? sub_rn(__ldg(a.b + i), ax) : ax;
+        a.y[i] = y;
+    }
+    if (a.k > 0) {
+        __shared__ double sm[32 * kKmax];
+        double acc[kKmax];
+        op_epilogue<OPMODE>(a, i, valid, y, acc);
+        block_sum<kKmax>(acc, sm);
+        if (threadIdx.x == 0)
+#pragma unroll
             for (int c = 0; c < kKmax; ++c)
                 if (c < a.k) a.zt_part[t * a.k + c] = acc[c];
     }
