@@ -127,3 +127,22 @@ def test_multirank_code_path_on_one_gpu(name, monkeypatch):
     assert not rep["device_loop"]
     assert abs(rep["iterations"] - case["iterations"]) <= 1
     assert np.linalg.norm(x - xref) <= 1e-6 * np.linalg.norm(xref)
+
+
+@pytest.mark.slow
+def test_bench_workload_150_matches_oracle():
+    """configs[1] at N=1 (the bench workload): 150^3 Poisson, linear deflation,
+    SPAI-0, CG 1e-8.  The reference measured 23 iterations, true relative
+    residual 8.23e-9; the oracle reproduces the reference
+    bitwise, so x is compared against it."""
+    cfgd = {"solver": {"type": "cg", "tol": 1e-8}, "precond": {"relax": {"type": "spai0"}},
+            "deflation": {"kind": "linear"}}
+    p = problems.poisson3d(150)
+    s = _solver(p, 1, cfgd)
+    x, rep = s.solve(p.rhs)
+    assert rep["converged"] and abs(rep["iterations"] - 23) <= 1
+    assert rep["relative_residual"] <= 1e-8
+    o = _oracle(p, 1, cfgd)
+    xo, ro = o.solve(p.rhs)
+    assert ro["iterations"] == 23
+    assert np.linalg.norm(x - xo) <= 1e-6 * np.linalg.norm(xo)
