@@ -127,6 +127,7 @@ typedef struct {
 typedef struct dfl_matrix dfl_matrix; /* host CSR produced by setup */
 typedef struct dfl_hier dfl_hier;     /* host AMG hierarchy */
 typedef struct dfl_ctx dfl_ctx;       /* device solve context (one rank) */
+typedef struct dfl_fabric dfl_fabric; /* in-process communicator (tests) */
 
 /* ---- library ----------------------------------------------------------- */
 int dfl_abi_version(void);
@@ -176,6 +177,13 @@ const char *dfl_last_error(const dfl_ctx *ctx);
  * 128-byte ncclUniqueId produced on rank 0 by dfl_nccl_unique_id */
 int dfl_nccl_unique_id(void *nccl_id_128);
 int dfl_ctx_set_comm(dfl_ctx *ctx, int nranks, int rank, const void *nccl_id_128);
+/* in-process communicator: ranks are contexts driven by different host
+ * threads; collectives synchronise at a host barrier and copy from the peers'
+ * device buffers.  Exercises the multi-rank path (halo plan, allgathers,
+ * rank-ordered sums, host-driven loop) without NCCL, e.g. on one GPU. */
+int dfl_fabric_create(int nranks, dfl_fabric **out);
+void dfl_fabric_destroy(dfl_fabric *f);
+int dfl_ctx_set_fabric(dfl_ctx *ctx, dfl_fabric *f, int rank);
 
 /* Operator rows of this rank (all its subdomains), columns renumbered as in
  * dfl_basis_az, entries in the global CSR order.

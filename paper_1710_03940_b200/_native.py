@@ -87,6 +87,9 @@ def lib():
         "dfl_last_error": ([c_vp], ctypes.c_char_p),
         "dfl_nccl_unique_id": ([c_vp], c_i32),
         "dfl_ctx_set_comm": ([c_vp, c_i32, c_i32, c_vp], c_i32),
+        "dfl_fabric_create": ([c_i32, P(c_vp)], c_i32),
+        "dfl_fabric_destroy": ([c_vp], None),
+        "dfl_ctx_set_fabric": ([c_vp, c_vp, c_i32], c_i32),
         "dfl_ctx_set_operator": ([c_vp, P(Csr), c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp], c_i32),
         "dfl_ctx_add_hierarchy": ([c_vp, c_i32, c_vp], c_i32),
         "dfl_ctx_set_deflation": ([c_vp, c_i32, c_vp, P(Csr), c_i64, c_vp, c_i32], c_i32),
@@ -247,6 +250,10 @@ class DeviceContext:
     def _c(self, rc):
         check(rc, self.h)
 
+    def set_fabric(self, fabric: "Fabric", rank: int):
+        self._fabric = fabric  # keep alive
+        self._c(lib().dfl_ctx_set_fabric(self.h, fabric.h, rank))
+
     def set_comm(self, nranks: int, rank: int, nccl_id: bytes):
         buf = ctypes.create_string_buffer(nccl_id, 128)
         self._c(lib().dfl_ctx_set_comm(self.h, nranks, rank, buf))
@@ -324,6 +331,21 @@ class DeviceContext:
         ms, by = c_dbl(), c_dbl()
         self._c(lib().dfl_ctx_time(self.h, what, reps, ctypes.byref(ms), ctypes.byref(by)))
         return ms.value, by.value
+
+
+class Fabric:
+    """In-process communicator (dfl_fabric) for multi-rank tests on one device."""
+
+    def __init__(self, nranks: int):
+        h = c_vp()
+        check(lib().dfl_fabric_create(nranks, ctypes.byref(h)))
+        self.h = h
+        self.nranks = nranks
+
+    def __del__(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.dfl_fabric_destroy(self.h)
+            self.h = None
 
 
 def nccl_unique_id() -> bytes:

@@ -12,7 +12,9 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <condition_variable>
 #include <memory>
+#include <mutex>
 #include <unordered_map>
 #include <string>
 #include <vector>
@@ -118,8 +120,34 @@ struct VGroup {
     std::vector<int64_t> nnzA, nnzP, rows;
 };
 
+// In-process communicator for testing the multi-rank path without NCCL: the
+// ranks are contexts driven by different host threads (one device or
+// several); every collective synchronises its stream, meets the other ranks
+// at a host barrier and copies from the peers' published device buffers.
+struct dfl_fabric {
+    int nranks = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long generation = 0;
+    std::vector<dfl_ctx *> ctxs;
+    std::vector<const double *> pub;  // per-rank published buffer of the current collective
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const long gen = generation;
+        if (++arrived == nranks) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != gen; });
+        }
+    }
+};
+
 struct dfl_ctx {
     int device = 0;
+    dfl_fabric *fab = nullptr;
     int sm_count = 148;
     std::vector<int64_t> op_sub_tiles_h;
     int64_t *op_sub_tiles = nullptr;   // first op-pipe tile of every subdomain
@@ -717,13 +745,62 @@ static int nccl_check(dfl_ctx *ctx, int rc, const char *what) {
     return DFL_OK;
 }
 
+static bool multi(const dfl_ctx *ctx) { return ctx->comm != nullptr || ctx->fab != nullptr; }
+
+// allgather of `count` doubles per rank into recv[q * count] (send may alias
+// recv + rank * count)
+static int comm_allgather(dfl_ctx *ctx, const double *send, double *recv, size_t count) {
+    if (ctx->comm) return nccl_check(ctx, g_nccl.AllGather(send, recv, count, ncclDouble_, ctx->comm, ctx->st), "ncclAllGather");
+    dfl_fabric *f = ctx->fab;
+    CK(cudaStreamSynchronize(ctx->st));
+    f->pub[ctx->rank] = send;
+    f->barrier();
+    for (int q = 0; q < ctx->nranks; ++q) {
+        double *dst = recv + (size_t)q * count;
+        if (f->pub[q] != dst) CK(cudaMemcpyAsync(dst, f->pub[q], count * sizeof(double), cudaMemcpyDefault, ctx->st));
+    }
+    CK(cudaStreamSynchronize(ctx->st));
+    f->barrier();
+    return DFL_OK;
+}
+
 // fill the ghost part v[n .. n+n_ghost) from the neighbours (runtime.py:246-271)
 static int halo(dfl_ctx *ctx, double *v) {
-    if (ctx->nranks == 1 || ctx->nbr.empty()) return DFL_OK;
+    if (!multi(ctx) || (ctx->nbr.empty() && !ctx->fab)) return DFL_OK;
     if (ctx->nsend > 0) {
         k_gather<<<(unsigned)cdiv(ctx->nsend, kBlock), kBlock, 0, ctx->st>>>(v, ctx->send_idx, ctx->nsend,
                                                                               ctx->sendbuf);
         ctx->launches++;
+    }
+    if (ctx->fab) {  // every rank takes part in the barriers, neighbours or not
+        dfl_fabric *f = ctx->fab;
+        CK(cudaStreamSynchronize(ctx->st));
+        f->pub[ctx->rank] = ctx->sendbuf;
+        f->barrier();
+        int64_t ro = 0;
+        for (size_t qi = 0; qi < ctx->nbr.size(); ++qi) {
+            const dfl_ctx *peer = f->ctxs[ctx->nbr[qi]];
+            int64_t off = 0, cnt = -1;
+            for (size_t j = 0; j < peer->nbr.size(); ++j) {
+                if (peer->nbr[j] == ctx->rank) {
+                    cnt = peer->send_cnt[j];
+                    break;
+                }
+                off += peer->send_cnt[j];
+            }
+            if (cnt != ctx->recv_cnt[qi]) {
+                ctx->err = "halo plan mismatch between ranks";
+                f->barrier();
+                return DFL_E_COMM;
+            }
+            if (cnt > 0)
+                CK(cudaMemcpyAsync(v + ctx->n + ro, f->pub[ctx->nbr[qi]] + off, cnt * sizeof(double), cudaMemcpyDefault,
+                                   ctx->st));
+            ro += ctx->recv_cnt[qi];
+        }
+        CK(cudaStreamSynchronize(ctx->st));
+        f->barrier();
+        return DFL_OK;
     }
     RC(nccl_check(ctx, g_nccl.GroupStart(), "ncclGroupStart"));
     int64_t so = 0, ro = 0;
@@ -744,7 +821,7 @@ static int halo(dfl_ctx *ctx, double *v) {
 // Z' v partials -> t (global numbering) -> t2 = E^-1 t on every rank
 static int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op) {
     const int64_t *sub_tiles = (from_op && g_use_pipe && ctx->Aop.pipe.stages) ? ctx->op_sub_tiles : ctx->sub_tiles;
-    if (ctx->comm == nullptr) {
+    if (!multi(ctx)) {
         k_zt_finish<<<ctx->nsub * ctx->k, 512, 0, ctx->st>>>(ctx->zt_part, sub_tiles, ctx->nsub, ctx->k,
                                                              ctx->tvec, 0, ctx->Einv, ctx->K, ctx->t2, st,
                                                              need_refresh, ctx->ticket);
@@ -756,7 +833,7 @@ static int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_
     double *mine = ctx->tgather + (int64_t)ctx->rank * slot;
     k_zt_finish<<<ctx->nsub * ctx->k, 512, 0, ctx->st>>>(ctx->zt_part, sub_tiles, ctx->nsub, ctx->k, mine, 0,
                                                          nullptr, ctx->K, nullptr, st, need_refresh, ctx->ticket);
-    RC(nccl_check(ctx, g_nccl.AllGather(mine, ctx->tgather, slot, ncclDouble_, ctx->comm, ctx->st), "ncclAllGather"));
+    RC(comm_allgather(ctx, mine, ctx->tgather, slot));
     // unpack rank slots into t: rank q owns a contiguous subdomain range
     int64_t pos = 0;
     for (int q = 0; q < ctx->nranks; ++q) {
@@ -875,10 +952,10 @@ __global__ void k_cg_end(KState *st, cudaGraphConditionalHandle h, int use_cond)
 // reductions across ranks: returns the pointer the scalar kernel reads
 static int rank_scalar(dfl_ctx *ctx, const double *part, int64_t nparts, int slot, const double **gath) {
     *gath = nullptr;
-    if (ctx->comm == nullptr) return DFL_OK;
+    if (!multi(ctx)) return DFL_OK;
     k_reduce<<<1, 1024, 0, ctx->st>>>(part, nparts, ctx->scal + slot);
     ctx->launches++;
-    RC(nccl_check(ctx, g_nccl.AllGather(ctx->scal, ctx->sgather, 8, ncclDouble_, ctx->comm, ctx->st), "ncclAllGather"));
+    RC(comm_allgather(ctx, ctx->scal, ctx->sgather, 8));
     *gath = ctx->sgather;
     return DFL_OK;
 }
@@ -1180,9 +1257,8 @@ static int global_dots(dfl_ctx *ctx, const double *part, int64_t nparts, int nq,
     else
         k_reduce<<<1, 1024, 0, ctx->st>>>(part, nparts, ctx->scal);
     ctx->launches++;
-    if (ctx->comm != nullptr) {
-        RC(nccl_check(ctx, g_nccl.AllGather(ctx->scal, ctx->sgather, 8, ncclDouble_, ctx->comm, ctx->st),
-                      "ncclAllGather"));
+    if (multi(ctx)) {
+        RC(comm_allgather(ctx, ctx->scal, ctx->sgather, 8));
         k_rank_sum<<<1, 32, 0, ctx->st>>>(ctx->sgather, ctx->nranks, 8, nq, ctx->scal + 8);
         ctx->launches++;
         return fetch(ctx, ctx->scal + 8, nq, out);
@@ -1607,8 +1683,8 @@ static int rank_dot(dfl_ctx *ctx, const double *a, const double *b, double *out)
     k_dot<<<nb, kBlock, 0, ctx->st>>>(a, b, ctx->n, ctx->dpart, nullptr);
     k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->dpart, nb, ctx->scal);
     ctx->launches += 2;
-    if (ctx->comm != nullptr) {
-        RC(nccl_check(ctx, g_nccl.AllGather(ctx->scal, ctx->sgather, 8, ncclDouble_, ctx->comm, ctx->st), "ncclAllGather"));
+    if (multi(ctx)) {
+        RC(comm_allgather(ctx, ctx->scal, ctx->sgather, 8));
         k_rank_sum<<<1, 32, 0, ctx->st>>>(ctx->sgather, ctx->nranks, 8, 1, ctx->scal + 1);
         ctx->launches++;
         CK(cudaMemcpyAsync(out, ctx->scal + 1, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
@@ -1724,6 +1800,27 @@ int dfl_ctx_set_comm(dfl_ctx *ctx, int nranks, int rank, const void *id) {
     NcclId nid;
     std::memcpy(&nid, id, sizeof nid);
     return nccl_check(ctx, g_nccl.CommInitRank(&ctx->comm, nranks, nid, rank), "ncclCommInitRank");
+}
+
+int dfl_fabric_create(int nranks, dfl_fabric **out) {
+    if (!out || nranks < 1) return DFL_E_STATE;
+    auto *f = new dfl_fabric;
+    f->nranks = nranks;
+    f->ctxs.assign(nranks, nullptr);
+    f->pub.assign(nranks, nullptr);
+    *out = f;
+    return DFL_OK;
+}
+
+void dfl_fabric_destroy(dfl_fabric *f) { delete f; }
+
+int dfl_ctx_set_fabric(dfl_ctx *ctx, dfl_fabric *f, int rank) {
+    if (!ctx || !f || rank < 0 || rank >= f->nranks) return DFL_E_STATE;
+    ctx->fab = f;
+    ctx->nranks = f->nranks;
+    ctx->rank = rank;
+    f->ctxs[rank] = ctx;
+    return DFL_OK;
 }
 
 int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int64_t *sub_offsets, int32_t nnbr,
@@ -1921,7 +2018,7 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     CK(cudaEventRecord(ctx->ev0, ctx->st));
     const char *ng = getenv("DFL_NO_GRAPH");
     const bool bicg = p->solver == DFL_SOLVER_BICGSTAB2;
-    const bool use_graph = !bicg && ctx->comm == nullptr && !(ng && ng[0] == '1');
+    const bool use_graph = !bicg && !multi(ctx) && !(ng && ng[0] == '1');
     KState bstate{};
     if (bicg) {
         RC(bicg_solve_dev(ctx, p, bstate));

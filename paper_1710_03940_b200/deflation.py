@@ -86,7 +86,8 @@ class DeflatedSolver:
     basis -- with the solve phase on the GPU."""
 
     def __init__(self, A, partition=None, *, config=None, coords=None, deflated: bool = True,
-                 threads_per_subdomain: int = 1, device: int | None = None, world: World | None = None):
+                 threads_per_subdomain: int = 1, device: int | None = None, world: World | None = None,
+                 fabric=None):
         nrows, ncols, ptr, col, val = as_csr_arrays(A)
         if nrows != ncols:
             raise DimensionError(f"matrix must be square, got {nrows}x{ncols}")
@@ -101,7 +102,7 @@ class DeflatedSolver:
                 coords = coords[:, None]
             if coords.shape[0] != nrows:
                 raise ConfigError(f"got coordinates for {coords.shape[0]} nodes, expected {nrows}")
-        self._init(rows, nrows, part, config, coords, deflated, device, world, global_coords=coords)
+        self._init(rows, nrows, part, config, coords, deflated, device, world, global_coords=coords, fabric=fabric)
 
     # -- scale path: every rank passes only its own rows -----------------------
     @classmethod
@@ -116,7 +117,7 @@ class DeflatedSolver:
         return self
 
     # -------------------------------------------------------------------------
-    def _init(self, rows, nglobal, part, config, coords, deflated, device, world, global_coords):
+    def _init(self, rows, nglobal, part, config, coords, deflated, device, world, global_coords, fabric=None):
         t_setup = time.perf_counter()
         self.cfg = as_config(config)
         _check_config(self.cfg, deflated)
@@ -138,7 +139,9 @@ class DeflatedSolver:
             device = int(os.environ.get("LOCAL_RANK", "0")) if world.nranks > 1 else 0
         self.device = device
         ctx = nat.DeviceContext(device)
-        if world.nranks > 1 or os.environ.get("DFL_FORCE_COMM") == "1":
+        if fabric is not None:  # in-process communicator (tests)
+            ctx.set_fabric(fabric, world.rank)
+        elif world.nranks > 1 or os.environ.get("DFL_FORCE_COMM") == "1":
             nid = world.bcast(nat.nccl_unique_id() if world.rank == 0 else None)
             ctx.set_comm(world.nranks, world.rank, nid)
         plan = hs.halo_plan

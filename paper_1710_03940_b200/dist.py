@@ -47,3 +47,30 @@ def current_world() -> World:
     if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
         return World(dist.get_world_size(), dist.get_rank())
     return World()
+
+
+class ThreadWorld(World):
+    """Ranks as host threads of one process (tests of the multi-rank path with
+    the in-process communicator, ``_native.Fabric``)."""
+
+    class Shared:
+        def __init__(self, nranks: int):
+            import threading
+
+            self.nranks = nranks
+            self.slots = [None] * nranks
+            self.barrier = threading.Barrier(nranks)
+
+    def __init__(self, shared: "ThreadWorld.Shared", rank: int):
+        super().__init__(shared.nranks, rank, None)
+        self.shared = shared
+
+    def allgather(self, obj):
+        self.shared.slots[self.rank] = obj
+        self.shared.barrier.wait()
+        out = list(self.shared.slots)
+        self.shared.barrier.wait()
+        return out
+
+    def bcast(self, obj, root: int = 0):
+        return self.allgather(obj)[root]
