@@ -189,3 +189,61 @@ def test_multirank_in_process_fabric(name, nranks):
         assert abs(rep["iterations"] - case["iterations"]) <= 1, rep["iterations"]
         assert rep["relative_residual"] <= max(case["config"]["solver"]["tol"], 2 * case["relative_residual"])
         assert np.linalg.norm(x - xref) <= 1e-6 * np.linalg.norm(xref)
+
+
+MEDIUM = [
+    # config #4 shape: jump coefficients, damped Jacobi, linear deflation, CG
+    ("jump", 40, 8, {"solver": {"type": "cg", "tol": 1e-8}, "precond": {"relax": {"type": "damped_jacobi"}},
+                     "deflation": {"kind": "linear"}}),
+    # config #5 shape: nonsymmetric convection-diffusion, BiCGStab(2), SPAI-0, linear
+    ("convdiff", 40, 1, {"solver": {"type": "bicgstab2", "tol": 1e-8}, "precond": {"relax": {"type": "spai0"}},
+                         "deflation": {"kind": "linear"}}),
+    ("convdiff", 40, 8, {"solver": {"type": "bicgstab2", "tol": 1e-8}, "precond": {"relax": {"type": "spai0"}},
+                         "deflation": {"kind": "linear"}}),
+    # config #3 shape: constant deflation, strong-scaling boxes
+    ("poisson", 48, 8, {"solver": {"type": "cg", "tol": 1e-8}, "precond": {"relax": {"type": "spai0"}},
+                        "deflation": {"kind": "constant"}}),
+]
+
+
+@pytest.mark.parametrize("kind,n,m,cfgd", MEDIUM, ids=lambda v: str(v) if not isinstance(v, dict) else "")
+def test_medium_configs_vs_oracle(kind, n, m, cfgd):
+    p = problems.make_problem(n, problems.boxes_for(m), kind)
+    s = _solver(p, m, cfgd)
+    o = _oracle(p, m, cfgd)
+    x, rep = s.solve(p.rhs)
+    xo, ro = o.solve(p.rhs)
+    assert rep["converged"] == ro["converged"]
+    assert abs(rep["iterations"] - ro["iterations"]) <= 1, (rep["iterations"], ro["iterations"])
+    assert rep["relative_residual"] <= max(cfgd["solver"]["tol"], 2 * ro["relative_residual"])
+    assert np.linalg.norm(x - xo) <= 1e-6 * np.linalg.norm(xo)
+
+
+def test_maxiter_exhaustion_reports_not_converged():
+    cfgd = {"solver": {"type": "cg", "tol": 1e-12, "maxiter": 3}, "precond": {"relax": {"type": "spai0"}},
+            "deflation": {"kind": "linear"}}
+    p = problems.poisson3d(16, problems.boxes_for(8))
+    x, rep = _solver(p, 8, cfgd).solve(p.rhs)
+    xo, ro = _oracle(p, 8, cfgd).solve(p.rhs)
+    assert rep["iterations"] == ro["iterations"] == 3 and not rep["converged"] and not ro["converged"]
+    assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)
+    cfgd["solver"]["type"] = "bicgstab2"
+    x, rep = _solver(p, 8, cfgd).solve(p.rhs)
+    xo, ro = _oracle(p, 8, cfgd).solve(p.rhs)
+    assert rep["iterations"] == ro["iterations"] == 3 and not rep["converged"]
+    assert np.linalg.norm(x - xo) <= 1e-9 * np.linalg.norm(xo)
+
+
+def test_partition_contiguous_uneven_subdomains():
+    """partition_contiguous (not box aligned) with uneven hierarchy depths: the
+    subdomains are grouped by depth on the device."""
+    cfgd = {"solver": {"type": "cg", "tol": 1e-8}, "precond": {"relax": {"type": "spai0"}},
+            "deflation": {"kind": "linear"}}
+    p = problems.poisson3d((30, 20, 10))
+    part = partition_contiguous(p.matrix.nrows, 5)
+    s = _solver(p, 5, cfgd, part=part)
+    o = _oracle(p, 5, cfgd, part=part)
+    x, rep = s.solve(p.rhs)
+    xo, ro = o.solve(p.rhs)
+    assert abs(rep["iterations"] - ro["iterations"]) <= 1
+    assert np.linalg.norm(x - xo) <= 1e-6 * np.linalg.norm(xo)
