@@ -179,6 +179,14 @@ struct dfl_ctx {
     int *send_idx = nullptr;
     int64_t nsend = 0;
     double *sendbuf = nullptr;
+    // halo overlap: rows with ghost columns run after the exchange
+    bool split = false;
+    uint8_t *bflag = nullptr;
+    int *brows = nullptr, *bstart = nullptr, *bcnt = nullptr;
+    int64_t nbtiles = 0;
+    int64_t *sub_btiles = nullptr;
+    cudaStream_t st2 = nullptr;
+    cudaEvent_t ev_packed = nullptr, ev_halo = nullptr;
     // hierarchies
     std::vector<dfl::Hierarchy> pending;
     std::vector<int> pending_set;
@@ -696,7 +704,7 @@ static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
 template <int OPMODE>
 static void launch_op(dfl_ctx *ctx, const OpArgs &a) {
     const DMat &A = ctx->Aop;
-    if (g_use_pipe) {
+    if (g_use_pipe && !a.skip_rows && !ctx->split) {
         SpArgs s;
         s.x = a.x;
         s.b = a.b;
@@ -765,12 +773,19 @@ static int comm_allgather(dfl_ctx *ctx, const double *send, double *recv, size_t
 }
 
 // fill the ghost part v[n .. n+n_ghost) from the neighbours (runtime.py:246-271)
-static int halo(dfl_ctx *ctx, double *v) {
+// pack on ctx->st; the NCCL transfers run on `xs` (ctx->st, or the comm
+// stream when the operator overlaps them with its interior rows)
+static int halo(dfl_ctx *ctx, double *v, cudaStream_t xs = nullptr) {
     if (!multi(ctx) || (ctx->nbr.empty() && !ctx->fab)) return DFL_OK;
+    if (!xs) xs = ctx->st;
     if (ctx->nsend > 0) {
         k_gather<<<(unsigned)cdiv(ctx->nsend, kBlock), kBlock, 0, ctx->st>>>(v, ctx->send_idx, ctx->nsend,
                                                                               ctx->sendbuf);
         ctx->launches++;
+    }
+    if (xs != ctx->st && !ctx->fab) {
+        CK(cudaEventRecord(ctx->ev_packed, ctx->st));
+        CK(cudaStreamWaitEvent(xs, ctx->ev_packed, 0));
     }
     if (ctx->fab) {  // every rank takes part in the barriers, neighbours or not
         dfl_fabric *f = ctx->fab;
@@ -806,10 +821,10 @@ static int halo(dfl_ctx *ctx, double *v) {
     int64_t so = 0, ro = 0;
     for (size_t q = 0; q < ctx->nbr.size(); ++q) {
         if (ctx->send_cnt[q] > 0)
-            RC(nccl_check(ctx, g_nccl.Send(ctx->sendbuf + so, ctx->send_cnt[q], ncclDouble_, ctx->nbr[q], ctx->comm, ctx->st),
+            RC(nccl_check(ctx, g_nccl.Send(ctx->sendbuf + so, ctx->send_cnt[q], ncclDouble_, ctx->nbr[q], ctx->comm, xs),
                           "ncclSend"));
         if (ctx->recv_cnt[q] > 0)
-            RC(nccl_check(ctx, g_nccl.Recv(v + ctx->n + ro, ctx->recv_cnt[q], ncclDouble_, ctx->nbr[q], ctx->comm, ctx->st),
+            RC(nccl_check(ctx, g_nccl.Recv(v + ctx->n + ro, ctx->recv_cnt[q], ncclDouble_, ctx->nbr[q], ctx->comm, xs),
                           "ncclRecv"));
         so += ctx->send_cnt[q];
         ro += ctx->recv_cnt[q];
@@ -820,11 +835,14 @@ static int halo(dfl_ctx *ctx, double *v) {
 
 // Z' v partials -> t (global numbering) -> t2 = E^-1 t on every rank
 static int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op) {
-    const int64_t *sub_tiles = (from_op && g_use_pipe && ctx->Aop.pipe.stages) ? ctx->op_sub_tiles : ctx->sub_tiles;
+    const int64_t *sub_tiles =
+        (from_op && g_use_pipe && !ctx->split && ctx->Aop.pipe.stages) ? ctx->op_sub_tiles : ctx->sub_tiles;
     if (!multi(ctx)) {
         k_zt_finish<<<ctx->nsub * ctx->k, 512, 0, ctx->st>>>(ctx->zt_part, sub_tiles, ctx->nsub, ctx->k,
                                                              ctx->tvec, 0, ctx->Einv, ctx->K, ctx->t2, st,
-                                                             need_refresh, ctx->ticket);
+                                                             need_refresh, ctx->ticket,
+                                                             from_op && ctx->split ? ctx->sub_btiles : nullptr,
+                                                             ctx->ntiles);
         ctx->launches++;
         return DFL_OK;
     }
@@ -832,7 +850,9 @@ static int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_
     const int64_t slot = (int64_t)ctx->max_nsub * ctx->k;
     double *mine = ctx->tgather + (int64_t)ctx->rank * slot;
     k_zt_finish<<<ctx->nsub * ctx->k, 512, 0, ctx->st>>>(ctx->zt_part, sub_tiles, ctx->nsub, ctx->k, mine, 0,
-                                                         nullptr, ctx->K, nullptr, st, need_refresh, ctx->ticket);
+                                                         nullptr, ctx->K, nullptr, st, need_refresh, ctx->ticket,
+                                                         from_op && ctx->split ? ctx->sub_btiles : nullptr,
+                                                         ctx->ntiles);
     RC(comm_allgather(ctx, mine, ctx->tgather, slot));
     // unpack rank slots into t: rank q owns a contiguous subdomain range
     int64_t pos = 0;
@@ -1042,12 +1062,38 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
 // y = A x (opmode 0) or y = b - A x (opmode 1); with zt the Z'y tile partials
 static int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double *b, bool zt,
                         const KState *st, int need_refresh) {
-    RC(halo(ctx, xin));
     OpArgs a{xin, b, y, ctx->zcols, ctx->n, zt ? ctx->k : 0, ctx->zt_part, st, need_refresh};
+    if (!ctx->split) {
+        RC(halo(ctx, xin));
+        if (opmode == 0)
+            launch_op<0>(ctx, a);
+        else
+            launch_op<1>(ctx, a);
+        return DFL_OK;
+    }
+    // halo overlapped with the interior rows (runtime.py:283-292 split in two
+    // passes): pack -> exchange on the comm stream while the rows without ghost
+    // columns run, then the boundary rows
+    RC(halo(ctx, xin, ctx->st2));
+    a.skip_rows = ctx->bflag;
     if (opmode == 0)
         launch_op<0>(ctx, a);
     else
         launch_op<1>(ctx, a);
+    if (!ctx->fab) {
+        CK(cudaEventRecord(ctx->ev_halo, ctx->st2));
+        CK(cudaStreamWaitEvent(ctx->st, ctx->ev_halo, 0));
+    }
+    a.skip_rows = nullptr;
+    if (ctx->nbtiles > 0) {
+        if (opmode == 0)
+            k_op_bnd<0><<<(unsigned)ctx->nbtiles, kBlock, 0, ctx->st>>>(ctx->Aop, ctx->brows, ctx->bstart, ctx->bcnt,
+                                                                         ctx->ntiles, a);
+        else
+            k_op_bnd<1><<<(unsigned)ctx->nbtiles, kBlock, 0, ctx->st>>>(ctx->Aop, ctx->brows, ctx->bstart, ctx->bcnt,
+                                                                         ctx->ntiles, a);
+        ctx->launches++;
+    }
     return DFL_OK;
 }
 
@@ -1762,6 +1808,9 @@ void dfl_ctx_destroy(dfl_ctx *ctx) {
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
+    if (ctx->st2) cudaStreamDestroy(ctx->st2);
+    if (ctx->ev_packed) cudaEventDestroy(ctx->ev_packed);
+    if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
     if (ctx->st) cudaStreamDestroy(ctx->st);
     delete ctx;
 }
@@ -1878,6 +1927,40 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
         RC(upload(ctx, &ctx->send_idx, si.data(), ctx->nsend));
         RC(dalloc(ctx, &ctx->sendbuf, ctx->nsend));
     }
+    // rows with ghost columns (multi-rank only): second pass of the operator
+    ctx->split = false;
+    if (multi(ctx) && ctx->n_ghost > 0 && !(getenv("DFL_NO_OVERLAP") && getenv("DFL_NO_OVERLAP")[0] == '1')) {
+        std::vector<uint8_t> flag(ctx->n, 0);
+        std::vector<int> rows, bs, bc;
+        std::vector<int64_t> sbt{0};
+        for (int s = 0; s < nsub; ++s) {
+            const size_t first = rows.size();
+            for (int64_t i = sub_offsets[s]; i < sub_offsets[s + 1]; ++i)
+                for (int64_t e = A->row_ptr[i]; e < A->row_ptr[i + 1]; ++e)
+                    if (A->col_idx[e] >= ctx->n) {
+                        flag[i] = 1;
+                        rows.push_back((int)i);
+                        break;
+                    }
+            for (size_t j = first; j < rows.size(); j += kBlock) {
+                bs.push_back((int)j);
+                bc.push_back((int)std::min<size_t>(kBlock, rows.size() - j));
+            }
+            sbt.push_back((int64_t)bs.size());
+        }
+        ctx->nbtiles = (int64_t)bs.size();
+        RC(upload(ctx, &ctx->bflag, flag.data(), ctx->n));
+        RC(upload(ctx, &ctx->brows, rows.data(), (int64_t)rows.size()));
+        RC(upload(ctx, &ctx->bstart, bs.data(), (int64_t)bs.size()));
+        RC(upload(ctx, &ctx->bcnt, bc.data(), (int64_t)bc.size()));
+        RC(upload(ctx, &ctx->sub_btiles, sbt.data(), (int64_t)sbt.size()));
+        if (!ctx->st2) {
+            CK(cudaStreamCreateWithFlags(&ctx->st2, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&ctx->ev_packed, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
+        }
+        ctx->split = true;
+    }
     ctx->pending.assign(nsub, dfl::Hierarchy{});
     ctx->pending_set.assign(nsub, 0);
     ctx->have_op = true;
@@ -1982,7 +2065,7 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
     // block of the multi-dot kernels (grid <= 4 * SMs)
     const int64_t dslots = std::max({ctx->nblk, vparts, 3 * std::max<int64_t>(ctx->nblk, 4 * ctx->sm_count)});
     RC(dalloc(ctx, &ctx->dpart, dslots + 64));
-    RC(dalloc(ctx, &ctx->zt_part, std::max(ctx->ntiles, ctx->Aop.pipe.ntiles) * kKmax + 64));
+    RC(dalloc(ctx, &ctx->zt_part, (std::max(ctx->ntiles, ctx->Aop.pipe.ntiles) + ctx->nbtiles) * kKmax + 64));
     RC(dalloc(ctx, &ctx->scal, 16));
     RC(dalloc(ctx, &ctx->sgather, (int64_t)8 * ctx->nranks));
     RC(dalloc(ctx, &ctx->state, 1));

@@ -547,6 +547,7 @@ struct OpArgs {
     double *zt_part;        // ntiles * k
     const KState *st;
     int need_refresh;       // 1: skip unless st->refresh_now
+    const uint8_t *skip_rows = nullptr;  // halo overlap: rows with ghost columns are done later
 };
 
 template <int OPMODE, int NV>
@@ -569,7 +570,7 @@ __global__ void __launch_bounds__(kBlock) k_op_ell(DMat A, Tiles T, SubTable S, 
     int64_t r0, r1;
     tile_rows(S, T, t, r0, r1);
     const int64_t i = r0 + threadIdx.x;
-    const bool valid = i < r1;
+    const bool valid = i < r1 && !(a.skip_rows && a.skip_rows[i]);
     double y = 0.0;
     if (valid) {
         const double ax = ell_any<W>(A, i, GatherX{a.x});
@@ -597,7 +598,7 @@ __global__ void __launch_bounds__(kBlock) k_op_code(DMat A, Tiles T, SubTable S,
     int64_t r0, r1;
     tile_rows(S, T, t, r0, r1);
     const int64_t i = r0 + threadIdx.x;
-    const bool valid = i < r1;
+    const bool valid = i < r1 && !(a.skip_rows && a.skip_rows[i]);
     const uint2 cw = valid ? __ldcs(A.codes + i) : make_uint2(~0u, ~0u);  // in flight during the table load
     load_codes(A, sd, sv);
     double y = 0.0;
@@ -626,7 +627,7 @@ __global__ void __launch_bounds__(kBlock) k_op_csr(DMat A, Tiles T, SubTable S, 
     tile_rows(S, T, t, r0, r1);
     const int64_t i = r0 + threadIdx.x / G;
     const int sub = threadIdx.x % G;
-    const bool inrange = i < r1;
+    const bool inrange = i < r1 && !(a.skip_rows && a.skip_rows[i]);
     const double ax = csr_row<G>(A, inrange ? i : A.nrows, sub, GatherX{a.x});
     const bool valid = inrange && sub == 0;
     double y = 0.0;
@@ -643,6 +644,41 @@ __global__ void __launch_bounds__(kBlock) k_op_csr(DMat A, Tiles T, SubTable S, 
             #pragma unroll
             for (int c = 0; c < kKmax; ++c)
                 if (c < a.k) a.zt_part[t * a.k + c] = acc[c];
+    }
+}
+
+// Halo overlap, second pass: the rows with ghost columns (listed in brows,
+// grouped in subdomain-aligned tiles of <= 256) once the ghosts arrived.
+// Same per-row arithmetic as the first pass; Z'y partials of tile bt go to
+// zt_part[(toff + bt) * k ...].
+template <int OPMODE>
+__global__ void __launch_bounds__(kBlock) k_op_bnd(DMat A, const int *__restrict__ brows,
+                                                   const int *__restrict__ bstart, const int *__restrict__ bcnt,
+                                                   int64_t toff, OpArgs a) {
+    if (a.need_refresh && !a.st->refresh_now) return;
+    const int64_t bt = blockIdx.x;
+    const bool valid = (int)threadIdx.x < bcnt[bt];
+    const int64_t i = valid ? brows[bstart[bt] + threadIdx.x] : 0;
+    double y = 0.0;
+    if (valid) {
+        double ax = 0.0;
+        if (A.fmt == FMT_CSR) {
+            for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) ax = add_rn(ax, mul_rn(A.val[e], __ldg(a.x + A.col[e])));
+        } else {
+            ax = ell_row_sliced(A, i, GatherX{a.x});
+        }
+        y = OPMODE == 1 ? sub_rn(__ldg(a.b + i), ax) : ax;
+        a.y[i] = y;
+    }
+    if (a.k > 0) {
+        __shared__ double sm[32 * kKmax];
+        double acc[kKmax];
+        op_epilogue<OPMODE>(a, i, valid, y, acc);
+        block_sum<kKmax>(acc, sm);
+        if (threadIdx.x == 0)
+#pragma unroll
+            for (int c = 0; c < kKmax; ++c)
+                if (c < a.k) a.zt_part[(toff + bt) * a.k + c] = acc[c];
     }
 }
 
@@ -679,7 +715,8 @@ __global__ void __launch_bounds__(512) k_zt_finish(const double *__restrict__ zt
                                                    const int64_t *__restrict__ sub_tiles, int nsub, int k,
                                                    double *t_out, int64_t first_col, const double *Einv,
                                                    int64_t K, double *t2, const KState *st, int need_refresh,
-                                                   unsigned int *ticket) {
+                                                   unsigned int *ticket, const int64_t *sub_tiles2 = nullptr,
+                                                   int64_t toff2 = 0) {
     if (skip(st)) return;
     if (need_refresh && !st->refresh_now) return;
     const int v = blockIdx.x;
@@ -687,6 +724,9 @@ __global__ void __launch_bounds__(512) k_zt_finish(const double *__restrict__ zt
     const int64_t t0 = sub_tiles[s], t1 = sub_tiles[s + 1];
     double acc = 0.0;
     for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) acc += zt_part[t * k + c];
+    if (sub_tiles2)  // boundary-row tiles of the halo-overlapped operator
+        for (int64_t t = toff2 + sub_tiles2[s] + threadIdx.x; t < toff2 + sub_tiles2[s + 1]; t += blockDim.x)
+            acc += zt_part[t * k + c];
     __shared__ double sm[32];
     double val[1] = {acc};
     block_sum<1>(val, sm);
