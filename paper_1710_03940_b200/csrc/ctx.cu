@@ -962,6 +962,31 @@ __global__ void k_cg_rz(KState *st, const double *part, int64_t nparts, const do
     st->rz = rz;
 }
 
+// multi-rank: r.r and r.z arrive in one allgather (slots 0 and 1); the
+// convergence test uses r.r exactly as k_cg_rr, then beta as k_cg_rz
+__global__ void k_cg_rrz(KState *st, const double *gath, int nranks) {
+    if (st->done || threadIdx.x != 0) return;
+    double rr = 0.0, rz = 0.0;
+    for (int q = 0; q < nranks; ++q) {
+        rr += gath[q * 8 + 0];
+        rz += gath[q * 8 + 1];
+    }
+    st->rr = rr;
+    st->resnorm = sqrt(fmax(rr, 0.0));
+    if (st->resnorm <= st->target) {
+        st->converged = 1;
+        st->done = 1;
+        return;
+    }
+    if (rz == 0.0 || !isfinite(rz)) {
+        st->breakdown = DFL_BRK_RZ;
+        st->done = 1;
+        return;
+    }
+    st->beta = rz / st->rz;
+    st->rz = rz;
+}
+
 __global__ void k_cg_end(KState *st, cudaGraphConditionalHandle h, int use_cond) {
     if (threadIdx.x != 0) return;
     if (!st->done && st->iters >= st->maxiter) st->done = 1;
@@ -1165,15 +1190,24 @@ static int cg_body(dfl_ctx *ctx, bool deflated, cudaGraphConditionalHandle h, in
         a.need_refresh = 1;
         launch_project<1>(ctx, a);
     }
-    RC(rank_scalar(ctx, ctx->dpart, ctx->nblk, 0, &gath));
-    k_cg_rr<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks);
-    ctx->launches++;
-    // z = M r, r.z
     int64_t np = 0;
-    RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
-    RC(rank_scalar(ctx, ctx->dpart, np, 0, &gath));
-    k_cg_rz<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, np, gath, ctx->nranks);
-    ctx->launches++;
+    if (multi(ctx)) {
+        // one collective for r.r and r.z: the V-cycle runs before the
+        // convergence test (its result is discarded on the last iteration)
+        k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->dpart, ctx->nblk, ctx->scal + 0);
+        RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
+        k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->dpart, np, ctx->scal + 1);
+        RC(comm_allgather(ctx, ctx->scal, ctx->sgather, 8));
+        k_cg_rrz<<<1, 32, 0, ctx->st>>>(st, ctx->sgather, ctx->nranks);
+        ctx->launches += 3;
+    } else {
+        k_cg_rr<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, nullptr, 1);
+        ctx->launches++;
+        // z = M r, r.z
+        RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
+        k_cg_rz<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, np, nullptr, 1);
+        ctx->launches++;
+    }
     k_cg_p<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->p, ctx->z, ctx->n, st);
     ctx->launches++;
     k_cg_end<<<1, 32, 0, ctx->st>>>(st, h, use_cond);
