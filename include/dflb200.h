@@ -230,7 +230,9 @@ int dfl_spmv_csr(const dfl_csr *A, const double *x, double *y, int device);
  *   what: 0 = operator SpMV (fine A; CSR fp64/int32 algorithmic bytes),
  *         1 = V-cycle (bytes of SURVEY §8(d): CSR layouts),
  *         2 = V-cycle (bytes the stored layouts actually need: ELL padding,
- *             1-byte codes of FMT_CODE matrices, the w.*r pass) */
+ *             1-byte codes of FMT_CODE matrices, the w.*r pass),
+ *         3 = V-cycle captured once and replayed as a CUDA graph, as inside
+ *             the solve (bytes as 1) */
 int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms_per_launch, double *bytes_per_launch);
 
 /* per-launch device times of one V-cycle, mean over reps; labels is a

@@ -78,6 +78,8 @@ Nccl g_nccl;
 }  // namespace
 
 static bool g_use_pipe = false;  // TMA-staged variant (DFL_PIPE=1); see profiles/r01
+static bool g_use_vcode = false;  // value-coded ELL for V-cycle P/R with <= 255 values (DFL_VCODE=1; measured neutral)
+static double g_small_per_lane = 12.0;  // DFL_CSR_PER_LANE_SMALL: entries per lane for levels < 50K rows
 static bool g_use_code = true;    // stencil-coded ELL for few-(offset, value) matrices (DFL_NO_CODE=1 disables)
 static bool g_use_coarse = false;  // cooperative coarse-cycle kernel (DFL_COARSE=1; measured slower, profiles/r01)
 static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle
@@ -351,6 +353,32 @@ static int try_upload_code(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) {
     return DFL_OK;
 }
 
+// value codes for an ELL-layout matrix with <= 255 distinct values (bitwise)
+static int attach_value_codes(dfl_ctx *ctx, DMat &m, const std::vector<double> &val) {
+    std::unordered_map<uint64_t, int> dict;
+    std::vector<double> tab;
+    std::vector<uint8_t> code(val.size());
+    for (size_t e = 0; e < val.size(); ++e) {
+        uint64_t bits;
+        std::memcpy(&bits, &val[e], 8);
+        auto it = dict.find(bits);
+        if (it == dict.end()) {
+            if (dict.size() >= 255) return DFL_OK;  // not value-codable
+            it = dict.emplace(bits, (int)tab.size()).first;
+            tab.push_back(val[e]);
+        }
+        code[e] = (uint8_t)it->second;
+    }
+    uint8_t *d_code;
+    double *d_tab;
+    RC(upload(ctx, &d_code, code.data(), (int64_t)code.size()));
+    RC(upload(ctx, &d_tab, tab.data(), (int64_t)tab.size()));
+    m.vcode = d_code;
+    m.vtab = d_tab;
+    m.nvtab = (int)tab.size();
+    return DFL_OK;
+}
+
 static constexpr int64_t kSigma = 1024;  // SELL-C-sigma sorting window
 // SELL-32-1024 for long-row matrices with enough rows to hide the per-warp
 // width imbalance (measured: L0 restriction and L1 operator, profiles/r01);
@@ -363,7 +391,7 @@ static double kShortRowPad = 1.7;
 static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &bounds,
                          std::vector<int64_t> *bound_tiles = nullptr, bool allow_ell = true,
                          const double *colscale = nullptr, DMat *scaled = nullptr, bool allow_sell = true,
-                         bool allow_code = true) {
+                         bool allow_code = true, bool allow_vcode = false) {
     m = DMat{};
     m.nrows = h.nrows;
     m.ncols = h.ncols;
@@ -475,6 +503,7 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::ve
             RC(upload(ctx, &d_perm, perm.data(), h.nrows));
             m.perm = d_perm;
         }
+        if (g_use_vcode && allow_vcode) RC(attach_value_codes(ctx, m, val));
         if (perm.empty()) RC(build_pipe(ctx, h, m, soff, bounds, bound_tiles));
         if (colscale) {
             double *d_sval;
@@ -487,7 +516,7 @@ static int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::ve
         m.stored = m.nnz;
         // lanes per row: about 6 entries per lane, batched kCsrUnroll deep
         int g = 1;
-        const int want = (int)std::ceil(mean / g_csr_per_lane);
+        const int want = (int)std::ceil(mean / (h.nrows < 50000 ? g_small_per_lane : g_csr_per_lane));
         while (g < want && g < 32) g *= 2;
         if (g_csr_g > 0) g = g_csr_g;
         m.group = g;
@@ -596,7 +625,7 @@ static int64_t code_grid(const dfl_ctx *, const DMat &A) {
 
 // number of per-block / per-tile partials a row kernel on A produces
 static int64_t parts_for(const DMat &A) {
-    if (A.fmt == FMT_CODE) return code_grid(nullptr, A);
+    if (A.fmt == FMT_CODE || A.vcode) return code_grid(nullptr, A);
     return A.pipe.stages ? A.pipe.ntiles : nblocks_for(A);
 }
 
@@ -667,6 +696,11 @@ static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
     if (A.nrows == 0) return;
     if (A.fmt == FMT_CODE) {
         k_code<MODE, DOT><<<(unsigned)code_grid(ctx, A), kBlock, 0, ctx->st>>>(A, a);
+        ctx->launches++;
+        return;
+    }
+    if (A.vcode) {
+        k_vell<MODE, DOT><<<(unsigned)code_grid(ctx, A), kBlock, 0, ctx->st>>>(A, a);
         ctx->launches++;
         return;
     }
@@ -1613,8 +1647,8 @@ static int build_groups(dfl_ctx *ctx) {
             OwnedRows A = merge_blocks(As, fo), P = merge_blocks(Ps, co), R = merge_blocks(Rs, fo);
             RC(upload_matrix(ctx, A.view(), v.A, {0, A.nrows}, nullptr, true, w.data(), &v.Aw));
             if (v.A.fmt == FMT_CODE) RC(dalloc(ctx, &v.wr, A.nrows));
-            RC(upload_matrix(ctx, P.view(), v.P, {0, P.nrows}));
-            RC(upload_matrix(ctx, R.view(), v.R, {0, R.nrows}));
+            RC(upload_matrix(ctx, P.view(), v.P, {0, P.nrows}, nullptr, true, nullptr, nullptr, true, true, true));
+            RC(upload_matrix(ctx, R.view(), v.R, {0, R.nrows}, nullptr, true, nullptr, nullptr, true, true, true));
             RC(upload(ctx, &v.w, w.data(), (int64_t)w.size()));
             v.n = fo.back();
             v.nc = co.back();
@@ -1809,6 +1843,10 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
         pipe_attrs();
         const char *np = getenv("DFL_PIPE");
         g_use_pipe = np && np[0] == '1';
+        const char *nvc = getenv("DFL_VCODE");
+        g_use_vcode = nvc && nvc[0] == '1';
+        const char *spl = getenv("DFL_CSR_PER_LANE_SMALL");
+        g_small_per_lane = spl ? atof(spl) : 12.0;
         const char *ncd = getenv("DFL_NO_CODE");
         g_use_code = !(ncd && ncd[0] == '1');
         const char *sp = getenv("DFL_SHORT_PAD");
@@ -2269,7 +2307,8 @@ int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
         const double rows = (double)M.nrows;
         if (M.fmt == FMT_CODE) return 8.0 * rows;
         if (M.fmt == FMT_CSR) return 12.0 * (double)M.nnz + 4.0 * (rows + 1);
-        return 12.0 * (double)M.stored + (M.perm ? 4.0 * rows : 0.0) + (M.ell_w ? 0.0 : 8.0 * (rows / 32 + 1));
+        return (M.vcode ? 5.0 : 12.0) * (double)M.stored + (M.perm ? 4.0 * rows : 0.0) +
+               (M.ell_w ? 0.0 : 8.0 * (rows / 32 + 1));
     };
     if (what == 0) {
         *bytes = 12.0 * ctx->op_nnz + 4.0 * (ctx->n + 1) + 8.0 * (ctx->n + ctx->n_ghost) + 8.0 * ctx->n;
@@ -2301,6 +2340,32 @@ int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
     // fill the inputs with something finite
     k_fill<<<(unsigned)cdiv(ctx->n + ctx->n_ghost, kBlock), kBlock, 0, ctx->st>>>(ctx->p, 1.0, ctx->n + ctx->n_ghost);
     k_fill<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->r, 1.0, ctx->n);
+    if (what == 3) {  // the V-cycle as the solve runs it: captured once, replayed as a CUDA graph
+        double b = 0;
+        double tmp = 0;
+        RC(dfl_ctx_time(ctx, 1, 1, &tmp, &b));
+        *bytes = b;
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+        const int64_t before = ctx->launches;
+        int rc = vcycle(ctx, ctx->r, ctx->z, nullptr, nullptr, nullptr);
+        CK(cudaStreamEndCapture(ctx->st, &g));
+        ctx->launches = before;
+        if (rc != DFL_OK) return rc;
+        cudaGraphExec_t ge;
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        for (int i = 0; i < 3; ++i) CK(cudaGraphLaunch(ge, ctx->st));
+        CK(cudaEventRecord(ctx->ev0, ctx->st));
+        for (int i = 0; i < reps; ++i) CK(cudaGraphLaunch(ge, ctx->st));
+        CK(cudaEventRecord(ctx->ev1, ctx->st));
+        CK(cudaEventSynchronize(ctx->ev1));
+        float t = 0;
+        CK(cudaEventElapsedTime(&t, ctx->ev0, ctx->ev1));
+        *ms = t / reps;
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+        return DFL_OK;
+    }
     for (int i = 0; i < 3; ++i) RC(run());
     CK(cudaEventRecord(ctx->ev0, ctx->st));
     for (int i = 0; i < reps; ++i) RC(run());

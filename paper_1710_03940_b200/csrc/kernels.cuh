@@ -68,6 +68,11 @@ struct DMat {
     const int *ctab_delta = nullptr;     // column - row of each code
     const double *ctab_val = nullptr;    // value of each code
     int ncodes = 0;
+    // value-coded ELL ("VELL"): 1-byte value codes in the layout of val, the
+    // distinct values in vtab (<= 255); index arrays unchanged
+    const uint8_t *vcode = nullptr;
+    const double *vtab = nullptr;
+    int nvtab = 0;
 };
 
 // run-time state of one Krylov solve (device resident)
@@ -388,6 +393,63 @@ __global__ void __launch_bounds__(kBlock, W == 0 ? DFL_ELL_MINB0 : DFL_ELL_MINB)
         const double y = epilogue<MODE>(a, i, ax);
         a.out[i] = y;
         if (DOT) dot = __ldg(a.r + i) * y;
+    }
+    if (DOT) {
+        __shared__ double sm[32];
+        double v[1] = {dot};
+        block_sum<1>(v, sm);
+        if (threadIdx.x == 0) a.dot_part[blockIdx.x] = v[0];
+    }
+}
+
+// value-coded ELL row: value of entry e is vt[vcode[e]]
+template <class G>
+__device__ __forceinline__ double vell_row(const DMat &A, int64_t slot, int W, const G &g, const double *vt) {
+    const int64_t s = slot >> 5;
+    int64_t off;
+    int width;
+    if (A.ell_w > 0) {
+        width = A.ell_w;
+        off = s * 32 * (int64_t)width;
+    } else {
+        off = __ldg(A.slice_off + s);
+        width = (int)((__ldg(A.slice_off + s + 1) - off) >> 5);
+    }
+    off += slot & 31;
+    double acc = 0.0;
+    for (int k0 = 0; k0 < width; k0 += 8) {
+        int c[8];
+        unsigned v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k0 + k < width) {
+                c[k] = ld_stream(A.col + off + 32 * (k0 + k));
+                v[k] = ld_stream(A.vcode + off + 32 * (k0 + k));
+            }
+        double xv[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k0 + k < width) xv[k] = g(c[k]);
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+            if (k0 + k < width) acc = add_rn(acc, mul_rn(vt[v[k]], xv[k]));
+    }
+    return acc;
+}
+
+// value-coded ELL row kernel: grid-stride, value table staged once per block
+template <int MODE, bool DOT>
+__global__ void __launch_bounds__(kBlock) k_vell(DMat A, RowArgs a) {
+    __shared__ double vt[256];
+    for (int t = threadIdx.x; t < A.nvtab; t += blockDim.x) vt[t] = A.vtab[t];
+    __syncthreads();
+    double dot = 0.0;
+    for (int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x; j < A.nrows; j += (int64_t)gridDim.x * kBlock) {
+        const int64_t i = A.perm ? (int64_t)__ldg(A.perm + j) : j;
+        const double ax = vell_row(A, j, 0, GatherX{MODE == MODE_RESID ? a.r : a.x}, vt);
+        const double y = epilogue<MODE>(a, i, ax);
+        a.out[i] = y;
+        if (DOT) dot += __ldg(a.r + i) * y;
     }
     if (DOT) {
         __shared__ double sm[32];

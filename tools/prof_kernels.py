@@ -26,6 +26,7 @@ cfg = SolverConfig({"solver": {"type": "cg", "tol": 1e-8}, "precond": {"relax": 
 s = DeflatedSolver.from_rows(rows, o.n, o.partition(), config=cfg, coords_local=problems.node_coords(o, 0, o.n))
 print("spmv", s._ctx.time(0, a.reps))
 print("vcycle", s._ctx.time(1, a.reps))
+print("vcycle graph", s._ctx.time(3, a.reps))
 for lab, ms in s._ctx.profile_vcycle(10):
     print(f"  {lab:14s} {ms*1e3:8.1f} us")
 if a.solve:
