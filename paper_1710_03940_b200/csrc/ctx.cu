@@ -1367,7 +1367,7 @@ static int fetch(dfl_ctx *ctx, const double *dev, int n, double *out) {
 // global value of nq interleaved (stride 3) or plain (nq == 0 -> 1 stream) partials
 static int global_dots(dfl_ctx *ctx, const double *part, int64_t nparts, int nq, bool strided, double *out) {
     if (strided)
-        k_reduce3<<<1, 1024, 0, ctx->st>>>(part, nparts, nq, ctx->scal);
+        k_reduceq<<<1, 1024, 0, ctx->st>>>(part, nparts, nq, ctx->scal);
     else
         k_reduce<<<1, 1024, 0, ctx->st>>>(part, nparts, ctx->scal);
     ctx->launches++;
@@ -1383,9 +1383,10 @@ static int global_dots(dfl_ctx *ctx, const double *part, int64_t nparts, int nq,
 static unsigned dot_grid(dfl_ctx *ctx) { return (unsigned)std::min<int64_t>(std::max<int64_t>(1, ctx->nblk), 4 * ctx->sm_count); }
 
 static int dots(dfl_ctx *ctx, int nq, const double *a0, const double *b0, const double *a1, const double *b1,
-                const double *a2, const double *b2, double *out) {
+                const double *a2, const double *b2, double *out, const double *a3 = nullptr,
+                const double *b3 = nullptr) {
     const unsigned g = dot_grid(ctx);
-    k_multidot<<<g, kBlock, 0, ctx->st>>>(a0, b0, a1, b1, a2, b2, nq, ctx->n, ctx->dpart);
+    k_multidot<<<g, kBlock, 0, ctx->st>>>(a0, b0, a1, b1, a2, b2, a3, b3, nq, ctx->n, ctx->dpart);
     ctx->launches++;
     return global_dots(ctx, ctx->dpart, g, nq, true, out);
 }
@@ -1447,6 +1448,7 @@ static int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) 
         ctx->launches++;
     }
     RC(dots(ctx, 1, ctx->bp, ctx->bp, nullptr, nullptr, nullptr, nullptr, val));
+    const double bpbp = val[0];  // also r[0].shadow of the first step (both are b')
     const double bpn = std::sqrt(std::max(val[0], 0.0));
     if (bpn == 0.0) {  // bicgstab2 returns zeros (krylov.py:270-272)
         out.converged = 1;
@@ -1467,7 +1469,12 @@ static int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) 
     int brk = DFL_BRK_NONE;
     int iters = 0;
     double resnorm = bpn;  // ||r[0]|| with r[0] = b'
+    // r[j].shadow is fetched together with the residual norm that precedes it
+    // (one reduction, one host round trip); invalid after a restart
+    double rho_next = bpbp;
+    bool rho_valid = true;
     auto fail = [&](int code) -> int {
+        rho_valid = false;
         if (restarted) return code;
         restarted = true;
         // r_shadow = r[0]; d = [0]; rho0, alpha, omega = 1, 0, 1  (krylov.py:165-175)
@@ -1480,13 +1487,18 @@ static int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) 
         return DFL_BRK_NONE;
     };
     const int refresh = std::max(1, p->refresh_every);
+    double mr[3] = {0.0, 0.0, 0.0};  // r0.r1, r1.r1, r2.r1 after the BiCG part
     while (iters < p->maxiter && resnorm > target) {
         ++iters;
         rho0 = -omega * rho0;
         bool aborted = false, mid = false;
         for (int j = 0; j < 2; ++j) {
-            RC(dots(ctx, 1, r[j], shadow, nullptr, nullptr, nullptr, nullptr, val));
-            const double rho1 = val[0];
+            double rho1 = rho_next;
+            if (!rho_valid) {
+                RC(dots(ctx, 1, r[j], shadow, nullptr, nullptr, nullptr, nullptr, val));
+                rho1 = val[0];
+            }
+            rho_valid = false;
             if (rho0 == 0.0 || !std::isfinite(rho1)) {
                 brk = fail(DFL_BRK_RHO);
                 aborted = true;
@@ -1507,8 +1519,20 @@ static int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) 
             k_bicg_r<<<nb, kBlock, 0, ctx->st>>>(r[0], d[1], r[1], d[2], j + 1, u, d[0], alpha, n, ctx->dpart);
             ctx->launches++;
             RC(op_hat(ctx, defl, r[j], r[j + 1], nullptr, nullptr));
-            RC(global_dots(ctx, ctx->dpart, nb, 1, false, val));
-            resnorm = std::sqrt(std::max(val[0], 0.0));
+            if (j == 0) {  // ||r0|| and the next step's rho1 = r1.shadow
+                double v2[4];
+                RC(dots(ctx, 2, r[0], r[0], r[1], shadow, nullptr, nullptr, v2));
+                resnorm = std::sqrt(std::max(v2[0], 0.0));
+                rho_next = v2[1];
+                rho_valid = true;
+            } else {  // ||r0|| and the minimal-residual dots
+                double v4[4];
+                RC(dots(ctx, 4, r[0], r[0], r[0], r[1], r[1], r[1], v4, r[2], r[1]));
+                resnorm = std::sqrt(std::max(v4[0], 0.0));
+                mr[0] = v4[1];
+                mr[1] = v4[2];
+                mr[2] = v4[3];
+            }
             if (resnorm <= target) {
                 mid = true;
                 break;
@@ -1522,15 +1546,14 @@ static int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) 
         }
         if (mid) break;
         // minimal-residual step on r[1..2] (modified Gram-Schmidt, krylov.py:207-255)
-        RC(dots(ctx, 3, r[0], r[1], r[1], r[1], r[2], r[1], val));
-        const double sigma1 = val[1];
+        const double sigma1 = mr[1];
         if (sigma1 == 0.0 || !std::isfinite(sigma1)) {
             brk = fail(DFL_BRK_MR);
             if (brk != DFL_BRK_NONE) break;
             continue;
         }
-        const double gp1 = val[0] / sigma1;
-        const double tau12 = val[2] / sigma1;
+        const double gp1 = mr[0] / sigma1;
+        const double tau12 = mr[2] / sigma1;
         {
             const unsigned g = dot_grid(ctx);
             k_bicg_mr2<<<g, kBlock, 0, ctx->st>>>(r[2], r[1], r[0], tau12, n, ctx->dpart);
@@ -1563,12 +1586,13 @@ static int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) 
             a.az_ptr = nullptr;
             a.K = 0;
             a.base = r0init;
-            a.dotmode = 2;
-            a.dot_part = ctx->dpart;
-            launch_project<1>(ctx, a);  // r[0] = r0 - tmp, partial r0.r0
+            launch_project<1>(ctx, a);  // r[0] = r0 - tmp
         }
-        RC(global_dots(ctx, ctx->dpart, nb, 1, false, val));
-        resnorm = std::sqrt(std::max(val[0], 0.0));
+        double v2[4];  // ||r0|| and the next group's rho1 = r0.shadow
+        RC(dots(ctx, 2, r[0], r[0], r[0], shadow, nullptr, nullptr, v2));
+        resnorm = std::sqrt(std::max(v2[0], 0.0));
+        rho_next = v2[1];
+        rho_valid = true;
     }
     // x = x0 + M(u)  (krylov.py:284-285), into ctx->x (the y of the deflated system)
     RC(vcycle(ctx, u, ctx->x, nullptr, nullptr, nullptr));
@@ -2135,7 +2159,7 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
                                : parts_for(g.lv[0].A);
     // partial-sum scratch: one slot per block of the row kernels, or 3 per
     // block of the multi-dot kernels (grid <= 4 * SMs)
-    const int64_t dslots = std::max({ctx->nblk, vparts, 3 * std::max<int64_t>(ctx->nblk, 4 * ctx->sm_count)});
+    const int64_t dslots = std::max({ctx->nblk, vparts, kDotStride * std::max<int64_t>(ctx->nblk, 4 * ctx->sm_count)});
     RC(dalloc(ctx, &ctx->dpart, dslots + 64));
     RC(dalloc(ctx, &ctx->zt_part, (std::max(ctx->ntiles, ctx->Aop.pipe.ntiles) + ctx->nbtiles) * kKmax + 64));
     RC(dalloc(ctx, &ctx->scal, 16));

@@ -1004,30 +1004,33 @@ namespace dfl {
 // the host in IEEE double exactly as the reference's Python scalars and passed
 // by value; every update keeps the reference's operation order (no FMA).
 
-// up to three dot products sharing one pass: part[blk*3 + q] = sum a_q . b_q
+// up to four dot products sharing one pass: part[blk*4 + q] = sum a_q . b_q
+constexpr int kDotStride = 4;
 __global__ void __launch_bounds__(kBlock) k_multidot(const double *__restrict__ a0, const double *__restrict__ b0,
                                                      const double *__restrict__ a1, const double *__restrict__ b1,
                                                      const double *__restrict__ a2, const double *__restrict__ b2,
+                                                     const double *__restrict__ a3, const double *__restrict__ b3,
                                                      int nq, int64_t n, double *part) {
-    double acc[3] = {0.0, 0.0, 0.0};
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
         acc[0] += a0[i] * b0[i];
         if (nq > 1) acc[1] += a1[i] * b1[i];
         if (nq > 2) acc[2] += a2[i] * b2[i];
+        if (nq > 3) acc[3] += a3[i] * b3[i];
     }
-    __shared__ double sm[32 * 3];
-    block_sum<3>(acc, sm);
+    __shared__ double sm[32 * 4];
+    block_sum<4>(acc, sm);
     if (threadIdx.x == 0)
-        for (int q = 0; q < 3; ++q) part[blockIdx.x * 3 + q] = acc[q];
+        for (int q = 0; q < 4; ++q) part[blockIdx.x * kDotStride + q] = acc[q];
 }
 
-// reduce nq interleaved partial streams (stride 3) -> out[0..nq)
-__global__ void k_reduce3(const double *part, int64_t nparts, int nq, double *out) {
-    __shared__ double sm[32 * 3];
-    double acc[3] = {0.0, 0.0, 0.0};
+// reduce nq interleaved partial streams (stride kDotStride) -> out[0..nq)
+__global__ void k_reduceq(const double *part, int64_t nparts, int nq, double *out) {
+    __shared__ double sm[32 * 4];
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t j = threadIdx.x; j < nparts; j += blockDim.x)
-        for (int q = 0; q < 3; ++q) acc[q] += part[j * 3 + q];
-    block_sum<3>(acc, sm);
+        for (int q = 0; q < 4; ++q) acc[q] += part[j * kDotStride + q];
+    block_sum<4>(acc, sm);
     if (threadIdx.x == 0)
         for (int q = 0; q < nq; ++q) out[q] = acc[q];
 }
@@ -1077,7 +1080,7 @@ __global__ void __launch_bounds__(kBlock) k_bicg_mr2(double *r2, const double *_
     __shared__ double sm[32 * 3];
     block_sum<3>(acc, sm);
     if (threadIdx.x == 0)
-        for (int q = 0; q < 3; ++q) part[blockIdx.x * 3 + q] = acc[q];
+        for (int q = 0; q < 3; ++q) part[blockIdx.x * kDotStride + q] = acc[q];
 }
 
 // the closing updates of one BiCGStab(2) group (krylov.py:247-253):
