@@ -237,20 +237,25 @@ __device__ __forceinline__ double ell_slice_w(const DMat &A, int64_t off, const 
     return acc;
 }
 
-// chunk of w <= 8 entries of a sliced row, accumulated into acc in order
+#ifndef DFL_SLICE_CHUNK
+#define DFL_SLICE_CHUNK 8
+#endif
+constexpr int kChunk = DFL_SLICE_CHUNK;
+
+// chunk of w <= kChunk entries of a sliced row, accumulated into acc in order
 template <class G>
 __device__ __forceinline__ double ell_chunk(const DMat &A, int64_t o, int w, double acc, const G &g) {
-    // exact sequential order, fixed 8-wide predicated batch
-    int c[8];
-    double v[8];
+    // exact sequential order, fixed-width predicated batch
+    int c[kChunk];
+    double v[kChunk];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < kChunk; ++k)
         if (k < w) {
             c[k] = ld_stream(A.col + o + 32 * k);
             v[k] = ld_stream(A.val + o + 32 * k);
         }
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < kChunk; ++k)
         if (k < w) acc = add_rn(acc, mul_rn(v[k], g(c[k])));
     return acc;
 }
@@ -262,7 +267,7 @@ __device__ __forceinline__ double ell_row_sliced(const DMat &A, int64_t row, con
     const int width = (int)((__ldg(A.slice_off + s + 1) - off) >> 5);
     const int64_t o = off + (row & 31);
     double acc = 0.0;
-    for (int k0 = 0; k0 < width; k0 += 8) acc = ell_chunk(A, o + 32 * k0, min(8, width - k0), acc, g);
+    for (int k0 = 0; k0 < width; k0 += kChunk) acc = ell_chunk(A, o + 32 * k0, min(kChunk, width - k0), acc, g);
     return acc;
 }
 

@@ -1,4 +1,4 @@
 #!/bin/bash
-for cfg in "DFL_CSR_PER_LANE_SMALL=12" "DFL_CSR_PER_LANE_SMALL=4" "DFL_CSR_PER_LANE_SMALL=2" "DFL_CSR_PER_LANE_SMALL=1"; do
-  echo "== $cfg"; env $cfg timeout 200 python tools/prof_kernels.py --reps 20 2>&1 | grep -E "vcycle|L2|L3|bottom"
+for lib in tools/variants/*.so; do
+  echo "== $lib"; DFL_LIB=$lib timeout 200 python tools/prof_kernels.py --reps 20 2>&1 | grep -E "vcycle graph|L0 restrict|L1 resid|L1 post"
 done
