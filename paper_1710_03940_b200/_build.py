@@ -49,7 +49,7 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
     run = lambda cmd: subprocess.run(cmd, check=True, stdout=None if verbose else subprocess.DEVNULL)
     for f in CXX_SOURCES:
         o = os.path.join(BUILD, f + ".o")
-        run(["g++", "-O3", "-std=c++17", "-fPIC", "-ffp-contract=off", "-fno-fast-math",
+        run(["g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-ffp-contract=off", "-fno-fast-math",
              "-I", os.path.join(REPO, "include"), "-c", os.path.join(CSRC, f), "-o", o])
         objs.append(o)
     for f in CU_SOURCES:

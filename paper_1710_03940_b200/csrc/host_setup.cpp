@@ -11,7 +11,10 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
+#include <chrono>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -57,63 +60,93 @@ Csr transpose(const Csr &a) {
     return t;
 }
 
+// Host threads for the row-parallel setup kernels (every output row is
+// computed by exactly one thread with the sequential per-row arithmetic, so
+// the result does not depend on the thread count).  DFL_SETUP_THREADS
+// overrides the default (hardware concurrency).
+static int setup_threads() {
+    static int t = [] {
+        const char *e = std::getenv("DFL_SETUP_THREADS");
+        int v = e ? std::atoi(e) : (int)std::thread::hardware_concurrency();
+        return std::max(1, std::min(v, 64));
+    }();
+    return t;
+}
+
+template <class F>
+static void parallel_rows(int64_t n, int64_t min_chunk, F &&f) {
+    const int T = (int)std::min<int64_t>(setup_threads(), std::max<int64_t>(1, n / std::max<int64_t>(1, min_chunk)));
+    if (T <= 1) {
+        f(0, (int64_t)0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 0; t < T; ++t) th.emplace_back([&, t] { f(t, n * t / T, n * (t + 1) / T); });
+    for (auto &x : th) x.join();
+}
+
 // Gustavson product; per output row the values accumulate in (A entry,
 // B entry) order into a dense scratch row and the touched columns are
-// insertion-sorted (reference _kernels.pyx:55-115).
+// insertion-sorted (reference _kernels.pyx:55-115).  Row-parallel.
 Csr spgemm(const Csr &a, const Csr &b) {
     Csr c;
     c.nrows = a.nrows;
     c.ncols = b.ncols;
     c.ptr.assign(a.nrows + 1, 0);
-    std::vector<int64_t> mark(b.ncols, -1);
-    for (int64_t i = 0; i < a.nrows; ++i) {
-        int64_t cnt = 0;
-        for (int64_t ka = a.ptr[i]; ka < a.ptr[i + 1]; ++ka) {
-            const int64_t r = a.col[ka];
-            for (int64_t kb = b.ptr[r]; kb < b.ptr[r + 1]; ++kb) {
-                const int64_t j = b.col[kb];
-                if (mark[j] != i) {
-                    mark[j] = i;
-                    ++cnt;
+    parallel_rows(a.nrows, 4096, [&](int, int64_t r0, int64_t r1) {
+        std::vector<int64_t> mark(b.ncols, -1);
+        for (int64_t i = r0; i < r1; ++i) {
+            int64_t cnt = 0;
+            for (int64_t ka = a.ptr[i]; ka < a.ptr[i + 1]; ++ka) {
+                const int64_t r = a.col[ka];
+                for (int64_t kb = b.ptr[r]; kb < b.ptr[r + 1]; ++kb) {
+                    const int64_t j = b.col[kb];
+                    if (mark[j] != i) {
+                        mark[j] = i;
+                        ++cnt;
+                    }
                 }
             }
+            c.ptr[i + 1] = cnt;
         }
-        c.ptr[i + 1] = c.ptr[i] + cnt;
-    }
+    });
+    for (int64_t i = 0; i < a.nrows; ++i) c.ptr[i + 1] += c.ptr[i];
     c.col.resize(c.ptr.back());
     c.val.resize(c.ptr.back());
-    std::vector<double> acc(b.ncols, 0.0);
-    std::fill(mark.begin(), mark.end(), -1);
-    for (int64_t i = 0; i < a.nrows; ++i) {
-        int64_t *cols = c.col.data() + c.ptr[i];
-        int64_t len = 0;
-        for (int64_t ka = a.ptr[i]; ka < a.ptr[i + 1]; ++ka) {
-            const int64_t r = a.col[ka];
-            const double av = a.val[ka];
-            for (int64_t kb = b.ptr[r]; kb < b.ptr[r + 1]; ++kb) {
-                const int64_t j = b.col[kb];
-                acc[j] = acc[j] + av * b.val[kb];
-                if (mark[j] != i) {
-                    mark[j] = i;
-                    cols[len++] = j;
+    parallel_rows(a.nrows, 4096, [&](int, int64_t r0, int64_t r1) {
+        std::vector<double> acc(b.ncols, 0.0);
+        std::vector<int64_t> mark(b.ncols, -1);
+        for (int64_t i = r0; i < r1; ++i) {
+            int64_t *cols = c.col.data() + c.ptr[i];
+            int64_t len = 0;
+            for (int64_t ka = a.ptr[i]; ka < a.ptr[i + 1]; ++ka) {
+                const int64_t r = a.col[ka];
+                const double av = a.val[ka];
+                for (int64_t kb = b.ptr[r]; kb < b.ptr[r + 1]; ++kb) {
+                    const int64_t j = b.col[kb];
+                    acc[j] = acc[j] + av * b.val[kb];
+                    if (mark[j] != i) {
+                        mark[j] = i;
+                        cols[len++] = j;
+                    }
                 }
             }
-        }
-        for (int64_t p = 1; p < len; ++p) {
-            const int64_t key = cols[p];
-            int64_t q = p - 1;
-            while (q >= 0 && cols[q] > key) {
-                cols[q + 1] = cols[q];
-                --q;
+            for (int64_t p = 1; p < len; ++p) {
+                const int64_t key = cols[p];
+                int64_t q = p - 1;
+                while (q >= 0 && cols[q] > key) {
+                    cols[q + 1] = cols[q];
+                    --q;
+                }
+                cols[q + 1] = key;
             }
-            cols[q + 1] = key;
+            double *vals = c.val.data() + c.ptr[i];
+            for (int64_t p = 0; p < len; ++p) {
+                vals[p] = acc[cols[p]];
+                acc[cols[p]] = 0.0;
+            }
         }
-        double *vals = c.val.data() + c.ptr[i];
-        for (int64_t p = 0; p < len; ++p) {
-            vals[p] = acc[cols[p]];
-            acc[cols[p]] = 0.0;
-        }
-    }
+    });
     return c;
 }
 
@@ -343,12 +376,19 @@ int build_hierarchy(const Csr &a0, const dfl_amg_options &o, Hierarchy &h) {
     int li = 0;
     for (;;) {
         if (cur.nrows <= o.coarse_enough || li + 1 >= o.max_levels) return close_bottom(h, std::move(cur));
+        const bool verbose = std::getenv("DFL_SETUP_VERBOSE") != nullptr;
+        auto now = [] { return std::chrono::steady_clock::now(); };
+        auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+        auto t0 = now();
         std::vector<double> d;
         if (!diagonal(cur, d, "strength graph")) return DFL_E_STRUCTURE;
         const double eps = o.eps_strong * std::ldexp(1.0, -li);
         Csr s = strength(cur, d, eps);
+        auto t1 = now();
         std::vector<int64_t> label;
         const int64_t naggr = aggregate(s, label);
+        auto t2 = now();
+        if (verbose) fprintf(stderr, "L%d strength %.0f ms aggregate %.0f ms\n", li, ms(t0, t1), ms(t1, t2));
         if (naggr == cur.nrows) return close_bottom(h, std::move(cur));
         for (int64_t i = 0; i < cur.nrows; ++i)
             if (label[i] < 0) {
@@ -370,8 +410,11 @@ int build_hierarchy(const Csr &a0, const dfl_amg_options &o, Hierarchy &h) {
                 lv.w[i] = d[i] / sq;
             }
         }
+        auto t3 = now();
         Csr ap = spgemm(cur, lv.P);
         Csr next = spgemm(lv.R, ap);
+        if (verbose)
+            fprintf(stderr, "L%d P+R+w %.0f ms RAP %.0f ms\n", li, ms(t2, t3), ms(t3, now()));
         lv.A = std::move(cur);
         h.levels.push_back(std::move(lv));
         cur = std::move(next);
