@@ -14,6 +14,25 @@
 
 namespace dfl {
 
+// Vectors written earlier in the same (persistent / cluster) kernel are read
+// through L2 (ld.global.cg) -- never through the non-coherent L1/texture path.
+struct GatherCG {
+    const double *x;
+    __device__ __forceinline__ double operator()(int c) const { return __ldcg(x + c); }
+};
+struct GatherWRCG {
+    const double *w, *r;
+    __device__ __forceinline__ double operator()(int c) const { return mul_rn(__ldg(w + c), __ldcg(r + c)); }
+};
+
+template <int MODE>
+__device__ __forceinline__ double epilogue_cg(const RowArgs &a, int64_t i, double ax) {
+    if (MODE == MODE_PLAIN) return ax;
+    if (MODE == MODE_RESID) return sub_rn(__ldcg(a.r + i), ax);
+    if (MODE == MODE_PROLONG) return add_rn(mul_rn(__ldg(a.w + i), __ldcg(a.r + i)), ax);
+    return add_rn(__ldcg(a.xo + i), mul_rn(__ldg(a.w + i), sub_rn(__ldcg(a.r + i), ax)));
+}
+
 constexpr int kMaxCoarse = 16;
 
 struct CLevel {
@@ -44,8 +63,8 @@ __device__ __forceinline__ void grid_rows(const DMat &A, const RowArgs &a, int64
     if (G == 0) {
         for (int64_t j = gtid; j < A.nrows; j += gthreads) {
             const int64_t i = A.perm ? (int64_t)__ldg(A.perm + j) : j;
-            const double ax = ell_row(A, j, GatherX{MODE == MODE_RESID ? a.r : a.x});
-            a.out[i] = epilogue<MODE>(a, i, ax);
+            const double ax = ell_row(A, j, GatherCG{MODE == MODE_RESID ? a.r : a.x});
+            a.out[i] = epilogue_cg<MODE>(a, i, ax);
         }
     } else {
         constexpr int GG = G > 0 ? G : 1;
@@ -55,8 +74,8 @@ __device__ __forceinline__ void grid_rows(const DMat &A, const RowArgs &a, int64
         // the loop bound is uniform per warp (shuffles inside csr_row need all lanes)
         for (int64_t wr = warp * RPW; wr < A.nrows; wr += nwarps * RPW) {
             const int64_t row = wr + lane / GG;
-            const double ax = csr_row<GG>(A, row, lane % GG, GatherX{MODE == MODE_RESID ? a.r : a.x});
-            if (lane % GG == 0 && row < A.nrows) a.out[row] = epilogue<MODE>(a, row, ax);
+            const double ax = csr_row<GG>(A, row, lane % GG, GatherCG{MODE == MODE_RESID ? a.r : a.x});
+            if (lane % GG == 0 && row < A.nrows) a.out[row] = epilogue_cg<MODE>(a, row, ax);
         }
     }
 }
@@ -66,9 +85,9 @@ __device__ __forceinline__ void grid_stage(const DMat &A, const RowArgs &a, int6
     if (A.fmt == FMT_CODE) {  // code table read through L1; RESID gathers w_j * r_j on the fly
         for (int64_t i = gtid; i < A.nrows; i += gthreads) {
             const double ax = MODE == MODE_RESID
-                                  ? code_row_g(A, i, GatherWR{a.w, a.r}, A.ctab_delta, A.ctab_val)
-                                  : code_row_g(A, i, GatherX{a.x}, A.ctab_delta, A.ctab_val);
-            a.out[i] = epilogue<MODE>(a, i, ax);
+                                  ? code_row_g(A, i, GatherWRCG{a.w, a.r}, A.ctab_delta, A.ctab_val)
+                                  : code_row_g(A, i, GatherCG{a.x}, A.ctab_delta, A.ctab_val);
+            a.out[i] = epilogue_cg<MODE>(a, i, ax);
         }
         return;
     }
@@ -99,7 +118,7 @@ __device__ __forceinline__ void grid_bottom(const CoarseArgs &c, const double *r
         const int i = (int)(gr - o);
         const double *M = c.binv + c.binv_off[s] + (int64_t)i * n;
         double acc = 0.0;
-        for (int j = lane; j < n; j += 32) acc = fma(__ldg(M + j), rb[o + j], acc);
+        for (int j = lane; j < n; j += 32) acc = fma(__ldg(M + j), __ldcg(rb + o + j), acc);
 #pragma unroll
         for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
         if (lane == 0) xb[gr] = acc;
@@ -136,6 +155,76 @@ __global__ void __launch_bounds__(256) k_coarse_cycle(const CoarseArgs *__restri
         grid_stage<MODE_PROLONG>(v.P, RowArgs{e, v.w, in, nullptr, v.t, nullptr, nullptr}, gtid, gthreads);
         grid.sync();
         grid_stage<MODE_POST>(v.A, RowArgs{v.t, v.w, in, v.t, out, nullptr, nullptr}, gtid, gthreads);
+    }
+}
+
+}  // namespace dfl
+
+namespace dfl {
+// ---------------------------------------------------------------------------
+// The tiny end of the V-cycle (levels of <= kTinyRows rows and the bottom) in
+// ONE thread-block cluster: 8 CTAs x 1024 threads, stages separated by the
+// hardware cluster barrier.  Every tiny-level matrix is CSR; one warp per row
+// (lanes stride the row, shuffle reduction), the bottom one warp per row of
+// the row-major inverse.  Replaces 4 launches per tiny level + the bottom.
+constexpr int kTinyRows = 4096;
+constexpr int kTinyCtas = 8;
+constexpr int kTinyThreads = 1024;
+
+template <int MODE>
+__device__ __forceinline__ void tiny_stage(const DMat &A, const RowArgs &a, int gwarp, int nwarps, int lane) {
+    const double *xg = MODE == MODE_RESID ? a.r : a.x;
+    for (int64_t row = gwarp; row < A.nrows; row += nwarps) {
+        double acc = 0.0;
+        const int b = __ldg(A.ptr + row), e = __ldg(A.ptr + row + 1);
+        for (int k = b + lane; k < e; k += 32) acc += __ldg(A.val + k) * __ldcg(xg + __ldg(A.col + k));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) a.out[row] = epilogue_cg<MODE>(a, row, acc);
+    }
+}
+
+__global__ void __cluster_dims__(kTinyCtas, 1, 1) __launch_bounds__(kTinyThreads)
+    k_tiny_cycle(const CoarseArgs *__restrict__ cp, const double *rin, double *xout) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cluster = cg::this_cluster();
+    const CoarseArgs &c = *cp;
+    const int lane = threadIdx.x & 31;
+    const int gwarp = (int)(blockIdx.x * (kTinyThreads / 32) + (threadIdx.x >> 5));
+    const int nwarps = (int)(gridDim.x * (kTinyThreads / 32));
+    const double *rb = c.nlev ? c.rb : rin;
+    double *xb = c.nlev ? c.xb : xout;
+    for (int l = 0; l < c.nlev; ++l) {
+        const CLevel &v = c.lv[l];
+        const double *in = l == 0 ? rin : v.rv;
+        double *next = (l + 1 < c.nlev) ? c.lv[l + 1].rv : c.rb;
+        tiny_stage<MODE_RESID>(v.Aw, RowArgs{nullptr, v.w, in, nullptr, v.t, nullptr, nullptr}, gwarp, nwarps, lane);
+        cluster.sync();
+        tiny_stage<MODE_PLAIN>(v.R, RowArgs{v.t, nullptr, nullptr, nullptr, next, nullptr, nullptr}, gwarp, nwarps, lane);
+        cluster.sync();
+    }
+    // bottom: warp per row of the row-major inverse
+    for (int64_t gr = gwarp; gr < c.nb; gr += nwarps) {
+        int s = 0;
+        while (s + 1 < c.nsub && c.b_off[s + 1] <= gr) ++s;
+        const int64_t o = c.b_off[s];
+        const int n = (int)(c.b_off[s + 1] - o);
+        const double *M = c.binv + c.binv_off[s] + (gr - o) * n;
+        double acc = 0.0;
+        for (int j = lane; j < n; j += 32) acc = fma(__ldg(M + j), __ldcg(rb + o + j), acc);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (lane == 0) xb[gr] = acc;
+    }
+    for (int l = c.nlev - 1; l >= 0; --l) {
+        cluster.sync();
+        const CLevel &v = c.lv[l];
+        const double *in = l == 0 ? rin : v.rv;
+        const double *e = (l + 1 < c.nlev) ? c.lv[l + 1].xv : xb;
+        double *out = l == 0 ? xout : v.xv;
+        tiny_stage<MODE_PROLONG>(v.P, RowArgs{e, v.w, in, nullptr, v.t, nullptr, nullptr}, gwarp, nwarps, lane);
+        cluster.sync();
+        tiny_stage<MODE_POST>(v.A, RowArgs{v.t, v.w, in, v.t, out, nullptr, nullptr}, gwarp, nwarps, lane);
     }
 }
 

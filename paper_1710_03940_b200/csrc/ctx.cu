@@ -81,6 +81,7 @@ static bool g_use_pipe = false;  // TMA-staged variant (DFL_PIPE=1); see profile
 static bool g_use_vcode = false;  // value-coded ELL for V-cycle P/R with <= 255 values (DFL_VCODE=1; measured neutral)
 static double g_small_per_lane = 12.0;  // DFL_CSR_PER_LANE_SMALL: entries per lane for levels < 50K rows
 static bool g_use_code = true;    // stencil-coded ELL for few-(offset, value) matrices (DFL_NO_CODE=1 disables)
+static bool g_use_tiny = false;   // cluster kernel for the tiny levels (DFL_TINY=1; measured slower, profiles/r01)
 static bool g_use_coarse = false;  // cooperative coarse-cycle kernel (DFL_COARSE=1; measured slower, profiles/r01)
 static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle
 // layout experiments (profiling knobs, read once per context creation)
@@ -116,6 +117,8 @@ struct VGroup {
     // levels [lc, L) and the bottom run in one cooperative kernel (coarse.cuh)
     int lc = -1;                     // -1: no coarse kernel
     CoarseArgs *cargs = nullptr;     // device copy
+    int lt = -1;                     // levels [lt, L) + bottom run in k_tiny_cycle (-1: none)
+    CoarseArgs *targs = nullptr;
     unsigned coarse_grid = 0;
     double *binv = nullptr;          // row-major inverses for the cooperative kernel
     // host-side statistics
@@ -1049,7 +1052,9 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
         const double *rin = r + g.row0;
         double *zout = z + g.row0;
         const int L = (int)g.lv.size();
-        const int lc = (g.lc >= 0 && g_use_coarse) ? g.lc : L + 1;  // first level of the cooperative kernel
+        const bool use_coarse = g.lc >= 0 && g_use_coarse;
+        const bool use_tiny = !use_coarse && g.lt >= 0 && g_use_tiny;
+        const int lc = use_coarse ? g.lc : use_tiny ? g.lt : L + 1;  // first level of the fused tail kernel
         for (int l = 0; l < std::min(L, lc); ++l) {
             DLevel &v = g.lv[l];
             const double *in = l == 0 ? rin : v.rv;
@@ -1075,10 +1080,16 @@ static int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, do
                 crin = g.rb;
                 cxout = g.xb;
             }
-            void *args[] = {(void *)&g.cargs, (void *)&crin, (void *)&cxout};
-            cudaLaunchCooperativeKernel((const void *)k_coarse_cycle, g.coarse_grid, 256, args, 0, ctx->st);
-            ctx->launches++;
-            prof_mark(ctx, "coarse L" + std::to_string(lc) + "+");
+            if (use_tiny) {
+                k_tiny_cycle<<<kTinyCtas, kTinyThreads, 0, ctx->st>>>(g.targs, crin, cxout);
+                ctx->launches++;
+                prof_mark(ctx, "tiny L" + std::to_string(lc) + "+");
+            } else {
+                void *args[] = {(void *)&g.cargs, (void *)&crin, (void *)&cxout};
+                cudaLaunchCooperativeKernel((const void *)k_coarse_cycle, g.coarse_grid, 256, args, 0, ctx->st);
+                ctx->launches++;
+                prof_mark(ctx, "coarse L" + std::to_string(lc) + "+");
+            }
         } else {
             const double *rb = L == 0 ? rin : g.rb;
             double *xb = L == 0 ? zout : g.xb;
@@ -1669,10 +1680,12 @@ static int build_groups(dfl_ctx *ctx) {
                 w.insert(w.end(), lv.w.begin(), lv.w.end());
             }
             OwnedRows A = merge_blocks(As, fo), P = merge_blocks(Ps, co), R = merge_blocks(Rs, fo);
-            RC(upload_matrix(ctx, A.view(), v.A, {0, A.nrows}, nullptr, true, w.data(), &v.Aw));
+            // tiny levels stay CSR: they run inside the k_tiny_cycle cluster kernel
+            const bool tiny = g_use_tiny && fo.back() <= kTinyRows;
+            RC(upload_matrix(ctx, A.view(), v.A, {0, A.nrows}, nullptr, !tiny, w.data(), &v.Aw));
             if (v.A.fmt == FMT_CODE) RC(dalloc(ctx, &v.wr, A.nrows));
-            RC(upload_matrix(ctx, P.view(), v.P, {0, P.nrows}, nullptr, true, nullptr, nullptr, true, true, true));
-            RC(upload_matrix(ctx, R.view(), v.R, {0, R.nrows}, nullptr, true, nullptr, nullptr, true, true, true));
+            RC(upload_matrix(ctx, P.view(), v.P, {0, P.nrows}, nullptr, !tiny, nullptr, nullptr, true, true, true));
+            RC(upload_matrix(ctx, R.view(), v.R, {0, R.nrows}, nullptr, !tiny, nullptr, nullptr, true, true, true));
             RC(upload(ctx, &v.w, w.data(), (int64_t)w.size()));
             v.n = fo.back();
             v.nc = co.back();
@@ -1744,6 +1757,26 @@ static int build_groups(dfl_ctx *ctx) {
                 ca.rb = g.rb;
                 ca.xb = g.xb;
                 RC(upload(ctx, &g.cargs, &ca, 1));
+                // tiny tail: levels of <= kTinyRows rows + bottom (all CSR)
+                int lt = L;
+                for (int l = 0; l < L; ++l)
+                    if (g.rows[l] <= kTinyRows) {
+                        lt = l;
+                        break;
+                    }
+                if (g_use_tiny && g.nb <= kTinyRows && L - lt <= kMaxCoarse) {
+                    CoarseArgs ta = ca;
+                    ta.nlev = L - lt;
+                    for (int l = lt; l < L; ++l) ta.lv[l - lt] = ca.lv[l - lc];
+                    bool csr = true;
+                    for (int l = 0; l < ta.nlev; ++l)
+                        csr = csr && ta.lv[l].Aw.fmt == FMT_CSR && ta.lv[l].A.fmt == FMT_CSR &&
+                              ta.lv[l].P.fmt == FMT_CSR && ta.lv[l].R.fmt == FMT_CSR;
+                    if (csr && lt >= lc) {
+                        RC(upload(ctx, &g.targs, &ta, 1));
+                        g.lt = lt;
+                    }
+                }
                 int bps = 0;
                 CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_coarse_cycle, 256, 0));
                 g.coarse_grid = (unsigned)(std::max(1, std::min(bps, 2)) * ctx->sm_count);
@@ -1875,6 +1908,8 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
         g_use_code = !(ncd && ncd[0] == '1');
         const char *sp = getenv("DFL_SHORT_PAD");
         kShortRowPad = sp ? atof(sp) : 1.7;
+        const char *nt = getenv("DFL_TINY");
+        g_use_tiny = nt && nt[0] == '1';
         const char *nc = getenv("DFL_COARSE");
         g_use_coarse = nc && nc[0] == '1';
         const char *ns = getenv("DFL_SELL");
