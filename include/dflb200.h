@@ -25,7 +25,8 @@
  *     dfl_ctx_add_hierarchy <- deflation.py:208 (one AmgHierarchy per subdomain)
  *     dfl_ctx_set_deflation <- deflation.py:83-163 DeflationBasis (Z, AZ, E factor)
  *     dfl_solve             <- deflation.py:254-312 DeflatedSolver.solve, with
- *                              krylov.py:95-145 cg / krylov.py:148-285 bicgstab2
+ *                              krylov.py:95-145 cg / krylov.py:148-285 bicgstab2 /
+ *                              krylov.py:288-414 gmres, fgmres
  *     dfl_op_apply          <- runtime.py:283-292 DistributedOperator.apply
  *     dfl_precond_apply     <- deflation.py:239-250 preconditioner -> amg.py:201-212
  *     dfl_project           <- deflation.py:230-233 DeflatedSolver.project
@@ -63,6 +64,8 @@ extern "C" {
 /* solver kinds (solver.type) */
 #define DFL_SOLVER_CG 0
 #define DFL_SOLVER_BICGSTAB2 1
+#define DFL_SOLVER_GMRES 2     /* restarted, right preconditioned (krylov.py:401-406) */
+#define DFL_SOLVER_FGMRES 3    /* flexible (krylov.py:409-414) */
 
 /* which matrix of a hierarchy level */
 #define DFL_LEVEL_A 0
@@ -108,6 +111,8 @@ typedef struct {
     int32_t refresh_every;/* 50 (krylov.py:41) */
     int32_t deflated;     /* 0: plain block-AMG Krylov (deflation.py:287-290) */
     double tol;           /* solver.tol: atol = tol * ||b|| (deflation.py:266-270) */
+    int32_t restart;      /* solver.M: (F)GMRES restart length (deflation.py:275-276) */
+    int32_t reserved;
 } dfl_solve_params;
 
 typedef struct {

@@ -647,6 +647,82 @@ def bicgstab2(op, b, M, dot, atol, maxiter, refresh=REFRESH) -> tuple:
     return M(u), Report(it, res, ok, None if ok else brk, hist)
 
 
+def gmres_driver(op, b, M, dot, atol, maxiter, restart, flexible) -> tuple:
+    """Restarted (F)GMRES, right preconditioned, MGS Arnoldi with one
+    re-orthogonalisation pass (reference: krylov.py:288-414), x0 = 0."""
+    def norm(v):
+        return math.sqrt(max(dot(v, v), 0.0))
+
+    bnorm = norm(b)
+    if bnorm == 0.0:
+        return np.zeros_like(b), Report(0, 0.0, True)
+    target = max(0.0, atol)
+    op_hat = op if flexible else (lambda v: op(M(v)))
+    x = np.zeros_like(b)
+    r = b.copy()
+    res = norm(r)
+    total = 0
+    while total < maxiter and res > target:
+        steps = min(restart, maxiter - total)
+        V = [r / res]
+        Z = []
+        H = np.zeros((steps + 1, steps))
+        g = np.zeros(steps + 1)
+        g[0] = res
+        rot = []
+        j = 0
+        while j < steps:
+            if flexible:
+                z = M(V[j])
+                Z.append(z)
+                w = op_hat(z)
+            else:
+                w = op_hat(V[j])
+            for i in range(j + 1):
+                h = dot(w, V[i])
+                H[i, j] = h
+                w = w - h * V[i]
+            for i in range(j + 1):
+                e = dot(w, V[i])
+                H[i, j] += e
+                w = w - e * V[i]
+            hn = norm(w)
+            H[j + 1, j] = hn
+            exact = hn == 0.0
+            if not exact:
+                V.append(w / hn)
+            for i, (c, s) in enumerate(rot):
+                t = c * H[i, j] + s * H[i + 1, j]
+                H[i + 1, j] = -s * H[i, j] + c * H[i + 1, j]
+                H[i, j] = t
+            rad = math.hypot(H[j, j], H[j + 1, j])
+            c, s = (1.0, 0.0) if rad == 0.0 else (H[j, j] / rad, H[j + 1, j] / rad)
+            rot.append((c, s))
+            H[j, j] = c * H[j, j] + s * H[j + 1, j]
+            H[j + 1, j] = 0.0
+            g[j + 1] = -s * g[j]
+            g[j] = c * g[j]
+            inner = abs(g[j + 1])
+            j += 1
+            if exact or inner <= target:
+                break
+        y = np.zeros(j)
+        for i in range(j - 1, -1, -1):
+            y[i] = (g[i] - np.dot(H[i, i + 1:j], y[i + 1:j])) / H[i, i]
+        basis = Z if flexible else V
+        upd = basis[0] * y[0]
+        for i in range(1, j):
+            upd = upd + y[i] * basis[i]
+        if not flexible:
+            upd = M(upd)
+        x = x + upd
+        total += j
+        r = b - op(x)
+        res = norm(r)
+    ok = res <= target
+    return x, Report(total, res, ok)
+
+
 # ---------------------------------------------------------------------------
 # The deflated solver (reference: deflation.py:181-312)
 # ---------------------------------------------------------------------------
@@ -697,9 +773,14 @@ class DeflatedSolverOracle:
 
         b = np.asarray(b, dtype=np.float64)
         name = self.cfg.get("solver.type")
-        if name not in ("cg", "bicgstab2"):
+        if name not in ("cg", "bicgstab2", "gmres", "fgmres"):
             raise OracleError(f"solver {name} is not part of the B200 path")
-        fn = cg if name == "cg" else bicgstab2
+        if name in ("gmres", "fgmres"):
+            restart = self.cfg.get("solver.M")
+            flexible = name == "fgmres"
+            fn = lambda op, b, M, dot, atol, maxiter: gmres_driver(op, b, M, dot, atol, maxiter, restart, flexible)
+        else:
+            fn = cg if name == "cg" else bicgstab2
         tol = self.cfg.get("solver.tol")
         bnorm = math.sqrt(max(self.dot(b, b), 0.0))
         maxiter = self.cfg.get("solver.maxiter") if maxiter is None else maxiter

@@ -22,7 +22,7 @@ c_dbl = ctypes.c_double
 c_vp = ctypes.c_void_p
 
 DFL_RELAX = {"damped_jacobi": 0, "spai0": 1}
-DFL_SOLVER = {"cg": 0, "bicgstab2": 1}
+DFL_SOLVER = {"cg": 0, "bicgstab2": 1, "gmres": 2, "fgmres": 3}
 PTR_HOST, PTR_DEVICE = 0, 1
 LEVEL_A, LEVEL_P, LEVEL_R = 0, 1, 2
 
@@ -38,7 +38,7 @@ class AmgOptions(ctypes.Structure):
 
 class SolveParams(ctypes.Structure):
     _fields_ = [("solver", c_i32), ("maxiter", c_i32), ("refresh_every", c_i32), ("deflated", c_i32),
-                ("tol", c_dbl)]
+                ("tol", c_dbl), ("restart", c_i32), ("reserved", c_i32)]
 
 
 class Report(ctypes.Structure):

@@ -222,6 +222,12 @@ struct dfl_ctx {
     double *br[3] = {nullptr, nullptr, nullptr}, *bd[3] = {nullptr, nullptr, nullptr};
     double *bu = nullptr, *bshadow = nullptr, *zx = nullptr;
     double *h_dots = nullptr;  // pinned
+    // (F)GMRES (allocated on first use)
+    int gm_restart = 0;
+    std::vector<double *> gmV, gmZ;
+    const double **gmVp = nullptr, **gmZp = nullptr;  // device pointer arrays
+    double *gm_h = nullptr, *gm_e = nullptr, *gm_y = nullptr, *gm_part = nullptr, *gm_loc = nullptr,
+           *gm_gath = nullptr, *h_gm = nullptr;
     double *scal = nullptr;     // [0..7] local reduced scalars
     double *sgather = nullptr;  // nranks * 8
     KState *state = nullptr;
@@ -1615,6 +1621,205 @@ static int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) 
 }
 
 // ---------------------------------------------------------------------------
+// Restarted (F)GMRES (krylov.py:288-414), right preconditioned; host-driven:
+// the Hessenberg column, the Givens rotations and the back substitution run
+// on the host in IEEE double exactly as the reference's Python; one host
+// round trip per Arnoldi step.
+
+static constexpr int kGmLd = 128;  // max restart + 1
+
+static int gm_alloc(dfl_ctx *ctx, int restart, bool flexible) {
+    if (restart < 1 || restart + 1 > kGmLd) {
+        ctx->err = "solver.M (GMRES restart) must be in [1, " + std::to_string(kGmLd - 1) + "]";
+        return DFL_E_CONFIG;
+    }
+    RC(bicg_alloc(ctx));  // zx
+    const int64_t nx = ctx->n + ctx->n_ghost;
+    while ((int)ctx->gmV.size() < restart + 1) {
+        double *v;
+        RC(dalloc(ctx, &v, ctx->n));
+        ctx->gmV.push_back(v);
+    }
+    if (flexible)
+        while ((int)ctx->gmZ.size() < restart) {
+            double *z;
+            RC(dalloc(ctx, &z, nx));  // operator inputs: ghost tail
+            CK(cudaMemset(z, 0, sizeof(double) * nx));
+            ctx->gmZ.push_back(z);
+        }
+    if (!ctx->gmVp) {
+        RC(dalloc(ctx, (double **)&ctx->gmVp, kGmLd));
+        RC(dalloc(ctx, (double **)&ctx->gmZp, kGmLd));
+        RC(dalloc(ctx, &ctx->gm_h, kGmLd));
+        RC(dalloc(ctx, &ctx->gm_e, kGmLd));
+        RC(dalloc(ctx, &ctx->gm_y, kGmLd));
+        RC(dalloc(ctx, &ctx->gm_loc, kGmLd));
+        RC(dalloc(ctx, &ctx->gm_gath, (int64_t)kGmLd * ctx->nranks));
+        RC(dalloc(ctx, &ctx->gm_part, (int64_t)kGmLd * 4 * ctx->sm_count));
+        CK(cudaMallocHost(&ctx->h_gm, 4 * kGmLd * sizeof(double)));
+    }
+    CK(cudaMemcpy((void *)ctx->gmVp, ctx->gmV.data(), sizeof(double *) * ctx->gmV.size(), cudaMemcpyHostToDevice));
+    if (!ctx->gmZ.empty())
+        CK(cudaMemcpy((void *)ctx->gmZp, ctx->gmZ.data(), sizeof(double *) * ctx->gmZ.size(), cudaMemcpyHostToDevice));
+    ctx->gm_restart = restart;
+    return DFL_OK;
+}
+
+// dev_out[0..nvec) = sum over ranks of V[0..nvec) . w
+static int gm_vdots(dfl_ctx *ctx, int nvec, const double *w, double *dev_out) {
+    const unsigned gx = (unsigned)std::min<int64_t>(std::max<int64_t>(1, ctx->nblk), 4 * ctx->sm_count);
+    const dim3 grid(gx, (unsigned)cdiv(nvec, kVecGroup));
+    k_vdots<<<grid, kBlock, 0, ctx->st>>>(ctx->gmVp, nvec, w, ctx->n, ctx->gm_part, kGmLd);
+    ctx->launches++;
+    if (!multi(ctx)) {
+        k_vreduce<<<nvec, 1024, 0, ctx->st>>>(ctx->gm_part, gx, kGmLd, dev_out);
+        ctx->launches++;
+        return DFL_OK;
+    }
+    k_vreduce<<<nvec, 1024, 0, ctx->st>>>(ctx->gm_part, gx, kGmLd, ctx->gm_loc);
+    RC(comm_allgather(ctx, ctx->gm_loc, ctx->gm_gath, kGmLd));
+    k_rank_sum<<<1, kGmLd, 0, ctx->st>>>(ctx->gm_gath, ctx->nranks, kGmLd, nvec, dev_out);
+    ctx->launches += 2;
+    return DFL_OK;
+}
+
+// r = b' - project(A x), returns ||r||   (krylov.py:408)
+static int gm_residual(dfl_ctx *ctx, bool defl, double *resnorm) {
+    RC(op_apply_dev(ctx, ctx->x, ctx->w, 0, nullptr, defl, nullptr, 0));
+    if (defl) RC(zt_to_t2(ctx, nullptr, 0, true));
+    ProjArgs a = proj_args(ctx, ctx->w, ctx->r, nullptr);
+    if (!defl) a.az_ptr = nullptr, a.K = 0;
+    a.base = ctx->bp;
+    a.dotmode = 2;
+    a.dot_part = ctx->dpart;
+    launch_project<1>(ctx, a);
+    double v[4];
+    RC(global_dots(ctx, ctx->dpart, ctx->nblk, 1, false, v));
+    *resnorm = std::sqrt(std::max(v[0], 0.0));
+    return DFL_OK;
+}
+
+static int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KState &out) {
+    const bool defl = p->deflated != 0;
+    const int M = p->restart > 0 ? p->restart : 50;
+    RC(gm_alloc(ctx, M, flexible));
+    const int64_t n = ctx->n;
+    const unsigned nb = (unsigned)ctx->nblk;
+    const unsigned gx = (unsigned)std::min<int64_t>(std::max<int64_t>(1, ctx->nblk), 4 * ctx->sm_count);
+    out = KState{};
+    double val[4];
+    RC(dots(ctx, 1, ctx->b, ctx->b, nullptr, nullptr, nullptr, nullptr, val));
+    out.bnorm = std::sqrt(std::max(val[0], 0.0));
+    const double target = std::max(0.0, p->tol * out.bnorm);
+    out.target = target;
+    k_fill<<<nb, kBlock, 0, ctx->st>>>(ctx->x, 0.0, n);
+    ctx->launches++;
+    if (out.bnorm == 0.0) {
+        out.converged = 1;
+        return DFL_OK;
+    }
+    if (defl) {
+        RC(project_dev(ctx, ctx->b, ctx->bp, nullptr, 0));
+    } else {
+        k_copy<<<nb, kBlock, 0, ctx->st>>>(ctx->bp, ctx->b, n);
+        ctx->launches++;
+    }
+    RC(dots(ctx, 1, ctx->bp, ctx->bp, nullptr, nullptr, nullptr, nullptr, val));
+    double resnorm = std::sqrt(std::max(val[0], 0.0));
+    if (resnorm == 0.0) {
+        out.converged = 1;
+        return DFL_OK;
+    }
+    k_copy<<<nb, kBlock, 0, ctx->st>>>(ctx->r, ctx->bp, n);
+    ctx->launches++;
+    std::vector<double> H((size_t)(M + 1) * M), g(M + 1), cs(M), sn(M), y(M);
+    auto h = [&](int i, int j) -> double & { return H[(size_t)i * M + j]; };
+    int total = 0;
+    while (total < p->maxiter && resnorm > target) {
+        const int steps = std::min(M, p->maxiter - total);
+        std::fill(H.begin(), H.end(), 0.0);
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = resnorm;
+        k_vdiv<<<nb, kBlock, 0, ctx->st>>>(ctx->gmV[0], ctx->r, resnorm, n);  // V0 = r0 / ||r0||
+        ctx->launches++;
+        int j = 0;
+        while (j < steps) {
+            double *w = ctx->w;
+            if (flexible) {  // z_j = M(V_j), w = project(A z_j)
+                RC(vcycle(ctx, ctx->gmV[j], ctx->gmZ[j], nullptr, nullptr, nullptr));
+                RC(op_apply_dev(ctx, ctx->gmZ[j], w, 0, nullptr, defl, nullptr, 0));
+                if (defl) RC(zt_to_t2(ctx, nullptr, 0, true));
+                ProjArgs a = proj_args(ctx, w, w, nullptr);
+                if (!defl) a.az_ptr = nullptr, a.K = 0;
+                launch_project<0>(ctx, a);
+            } else {  // w = project(A (M V_j))
+                RC(op_hat(ctx, defl, ctx->gmV[j], ctx->tmp, nullptr, nullptr));
+                w = ctx->tmp;
+            }
+            // two Gram-Schmidt passes against V_0..V_j, then ||w||
+            RC(gm_vdots(ctx, j + 1, w, ctx->gm_h));
+            k_vsub<<<gx, kBlock, 0, ctx->st>>>(w, ctx->gmVp, ctx->gm_h, j + 1, n, nullptr);
+            RC(gm_vdots(ctx, j + 1, w, ctx->gm_e));
+            k_vsub<<<gx, kBlock, 0, ctx->st>>>(w, ctx->gmVp, ctx->gm_e, j + 1, n, ctx->dpart);
+            ctx->launches += 2;
+            RC(global_dots(ctx, ctx->dpart, gx, 1, false, val));
+            CK(cudaMemcpyAsync(ctx->h_gm, ctx->gm_h, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaMemcpyAsync(ctx->h_gm + kGmLd, ctx->gm_e, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost,
+                               ctx->st));
+            CK(cudaStreamSynchronize(ctx->st));
+            for (int i = 0; i <= j; ++i) {
+                h(i, j) = ctx->h_gm[i];
+                h(i, j) += ctx->h_gm[kGmLd + i];
+            }
+            const double hj1 = std::sqrt(std::max(val[0], 0.0));
+            h(j + 1, j) = hj1;
+            const bool exact = hj1 == 0.0;
+            if (!exact) {
+                k_vdiv<<<nb, kBlock, 0, ctx->st>>>(ctx->gmV[j + 1], w, hj1, n);
+                ctx->launches++;
+            }
+            for (int i = 0; i < j; ++i) {
+                const double t = cs[i] * h(i, j) + sn[i] * h(i + 1, j);
+                h(i + 1, j) = -sn[i] * h(i, j) + cs[i] * h(i + 1, j);
+                h(i, j) = t;
+            }
+            const double rad = std::hypot(h(j, j), h(j + 1, j));
+            cs[j] = rad == 0.0 ? 1.0 : h(j, j) / rad;
+            sn[j] = rad == 0.0 ? 0.0 : h(j + 1, j) / rad;
+            h(j, j) = cs[j] * h(j, j) + sn[j] * h(j + 1, j);
+            h(j + 1, j) = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            const double res = std::fabs(g[j + 1]);
+            ++j;
+            if (exact || res <= target) break;
+        }
+        for (int i = j - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int q = i + 1; q < j; ++q) s += h(i, q) * y[q];
+            y[i] = (g[i] - s) / h(i, i);
+        }
+        CK(cudaMemcpyAsync(ctx->gm_y, y.data(), sizeof(double) * j, cudaMemcpyHostToDevice, ctx->st));
+        if (flexible) {  // x = x + (Z_0 y_0 + y_1 Z_1 + ...)
+            k_vcombine<<<gx, kBlock, 0, ctx->st>>>(ctx->x, ctx->x, ctx->gmZp, ctx->gm_y, j, n);
+            ctx->launches++;
+        } else {  // x = x + M(V_0 y_0 + ...)
+            k_vcombine<<<gx, kBlock, 0, ctx->st>>>(ctx->tmp, nullptr, ctx->gmVp, ctx->gm_y, j, n);
+            RC(vcycle(ctx, ctx->tmp, ctx->zx, nullptr, nullptr, nullptr));
+            k_addv<<<nb, kBlock, 0, ctx->st>>>(ctx->x, ctx->zx, n);
+            ctx->launches += 2;
+        }
+        CK(cudaStreamSynchronize(ctx->st));  // y (host vector) was read by the async copy above
+        total += j;
+        RC(gm_residual(ctx, defl, &resnorm));
+    }
+    out.iters = total;
+    out.resnorm = resnorm;
+    out.converged = resnorm <= target;
+    return DFL_OK;
+}
+
+// ---------------------------------------------------------------------------
 // upload helpers for finalize
 
 struct OwnedRows {
@@ -1936,6 +2141,7 @@ void dfl_ctx_destroy(dfl_ctx *ctx) {
     for (void *p : ctx->allocs) cudaFree(p);
     if (ctx->h_state) cudaFreeHost(ctx->h_state);
     if (ctx->h_dots) cudaFreeHost(ctx->h_dots);
+    if (ctx->h_gm) cudaFreeHost(ctx->h_gm);
     if (ctx->ev0) cudaEventDestroy(ctx->ev0);
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
@@ -2214,8 +2420,8 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
 int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *x, int ptr_kind, dfl_report *rep) {
     RC(ready(ctx));
     if (!p || !rep) return DFL_E_STATE;
-    if (p->solver != DFL_SOLVER_CG && p->solver != DFL_SOLVER_BICGSTAB2) {
-        ctx->err = "solver must be cg or bicgstab2";
+    if (p->solver < DFL_SOLVER_CG || p->solver > DFL_SOLVER_FGMRES) {
+        ctx->err = "solver must be cg, bicgstab2, gmres or fgmres";
         return DFL_E_CONFIG;
     }
     if (p->deflated && !ctx->deflation) {
@@ -2231,11 +2437,14 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     RC(stage_in(ctx, ctx->b, b, ptr_kind));
     CK(cudaEventRecord(ctx->ev0, ctx->st));
     const char *ng = getenv("DFL_NO_GRAPH");
-    const bool bicg = p->solver == DFL_SOLVER_BICGSTAB2;
+    const bool bicg = p->solver != DFL_SOLVER_CG;  // host-driven solvers
     const bool use_graph = !bicg && !multi(ctx) && !(ng && ng[0] == '1');
     KState bstate{};
-    if (bicg) {
+    if (p->solver == DFL_SOLVER_BICGSTAB2) {
         RC(bicg_solve_dev(ctx, p, bstate));
+        RC(lift_dev(ctx, p));
+    } else if (p->solver == DFL_SOLVER_GMRES || p->solver == DFL_SOLVER_FGMRES) {
+        RC(gmres_solve_dev(ctx, p, p->solver == DFL_SOLVER_FGMRES, bstate));
         RC(lift_dev(ctx, p));
     } else {
         RC(cg_solve_dev(ctx, p, use_graph));

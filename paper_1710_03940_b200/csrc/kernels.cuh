@@ -935,6 +935,19 @@ __device__ __forceinline__ double reduce_parts(const double *part, int64_t npart
     return total;
 }
 
+// deterministic sum of part[0], part[ld], part[2 ld], ... (one block)
+__device__ __forceinline__ double reduce_parts_strided(const double *part, int64_t nparts, int ld) {
+    __shared__ double sm[32];
+    double acc = 0.0;
+    for (int64_t j = threadIdx.x; j < nparts; j += blockDim.x) acc += part[j * ld];
+    double v[1] = {acc};
+    block_sum<1>(v, sm);
+    __shared__ double total;
+    if (threadIdx.x == 0) total = v[0];
+    __syncthreads();
+    return total;
+}
+
 __global__ void k_reduce(const double *part, int64_t nparts, double *out) {
     const double s = reduce_parts(part, nparts);
     if (threadIdx.x == 0) *out = s;
@@ -1115,6 +1128,86 @@ __global__ void __launch_bounds__(kBlock) k_bicg_final(double *u, double *r0, do
     double v[1] = {dot};
     block_sum<1>(v, sm);
     if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+}
+
+}  // namespace dfl
+
+namespace dfl {
+// ---------------------------------------------------------------------------
+// (F)GMRES kernels (krylov.py:288-414): Arnoldi with two Gram-Schmidt passes
+// over the basis, done as classical Gram-Schmidt per pass (one multi-vector
+// reduction + one multi-vector update) instead of the reference's modified
+// Gram-Schmidt loop -- equal in exact arithmetic, both re-orthogonalised.
+
+constexpr int kVecGroup = 8;  // basis vectors per block of k_vdots
+
+// part[bx * ld + i] = sum over the block's rows of V_i . w, i in [8*by, 8*by+8)
+__global__ void __launch_bounds__(kBlock) k_vdots(const double *const *__restrict__ V, int nvec,
+                                                  const double *__restrict__ w, int64_t n, double *part, int ld) {
+    const int i0 = blockIdx.y * kVecGroup;
+    double acc[kVecGroup];
+#pragma unroll
+    for (int q = 0; q < kVecGroup; ++q) acc[q] = 0.0;
+    for (int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x; e < n; e += (int64_t)gridDim.x * kBlock) {
+        const double we = w[e];
+#pragma unroll
+        for (int q = 0; q < kVecGroup; ++q)
+            if (i0 + q < nvec) acc[q] += V[i0 + q][e] * we;
+    }
+    __shared__ double sm[32 * kVecGroup];
+    block_sum<kVecGroup>(acc, sm);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int q = 0; q < kVecGroup; ++q)
+            if (i0 + q < nvec) part[(int64_t)blockIdx.x * ld + i0 + q] = acc[q];
+}
+
+// out[i] = sum_bx part[bx * ld + i]   (one block per i)
+__global__ void k_vreduce(const double *part, int64_t nbx, int ld, double *out) {
+    const double s = reduce_parts_strided(part + blockIdx.x, nbx, ld);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+// w -= h_0 V_0; w -= h_1 V_1; ... (one rounding per step, as the MGS updates);
+// optional partial of w.w after the update
+__global__ void __launch_bounds__(kBlock) k_vsub(double *w, const double *const *__restrict__ V, const double *h,
+                                                 int nvec, int64_t n, double *part) {
+    double dot = 0.0;
+    for (int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x; e < n; e += (int64_t)gridDim.x * kBlock) {
+        double we = w[e];
+        for (int i = 0; i < nvec; ++i) we = sub_rn(we, mul_rn(h[i], V[i][e]));
+        w[e] = we;
+        dot += we * we;
+    }
+    if (part) {
+        __shared__ double sm[32];
+        double v[1] = {dot};
+        block_sum<1>(v, sm);
+        if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+    }
+}
+
+// out = (x +) (v_0 y_0 + y_1 v_1 + ...)  in the reference's order
+// (krylov.py:355-363, then x = x + update :407)
+__global__ void __launch_bounds__(kBlock) k_vcombine(double *out, const double *x, const double *const *__restrict__ V,
+                                                     const double *y, int nvec, int64_t n) {
+    for (int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x; e < n; e += (int64_t)gridDim.x * kBlock) {
+        double u = mul_rn(V[0][e], y[0]);
+        for (int i = 1; i < nvec; ++i) u = add_rn(u, mul_rn(y[i], V[i][e]));
+        out[e] = x ? add_rn(x[e], u) : u;
+    }
+}
+
+// x = x + u
+__global__ void __launch_bounds__(kBlock) k_addv(double *x, const double *__restrict__ u, int64_t n) {
+    const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (e < n) x[e] = add_rn(x[e], u[e]);
+}
+
+// out = in / s   (V_{j+1} = w / h_{j+1,j}, V_0 = r / ||r||)
+__global__ void __launch_bounds__(kBlock) k_vdiv(double *out, const double *in, double s, int64_t n) {
+    const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (e < n) out[e] = __ddiv_rn(in[e], s);
 }
 
 }  // namespace dfl

@@ -38,7 +38,7 @@ from .sparse import as_csr_arrays
 __all__ = ["DeflatedSolver", "solve_deflated", "HierarchyInfo", "BasisInfo"]
 
 DEFLATION_KINDS = ("constant", "linear")
-B200_SOLVERS = ("cg", "bicgstab2")
+B200_SOLVERS = ("cg", "bicgstab2", "gmres", "fgmres")
 
 
 class HierarchyInfo:
@@ -255,6 +255,8 @@ def _params(solver: "DeflatedSolver", maxiter=None):
         50,
         1 if solver.deflated else 0,
         float(cfg.get("solver.tol")),
+        int(cfg.get("solver.M")),
+        0,
     )
 
 

@@ -247,3 +247,28 @@ def test_partition_contiguous_uneven_subdomains():
     xo, ro = o.solve(p.rhs)
     assert abs(rep["iterations"] - ro["iterations"]) <= 1
     assert np.linalg.norm(x - xo) <= 1e-6 * np.linalg.norm(xo)
+
+
+def _gmres_golden():
+    import json
+    import os
+
+    from golden_data import HERE
+
+    with open(os.path.join(HERE, "golden_gmres.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("case", _gmres_golden(), ids=lambda c: c["name"])
+def test_gmres_fgmres_parity(case):
+    import os
+
+    from golden_data import HERE
+
+    p = problems.make_problem(case["shape"], problems.boxes_for(case["m"]), case["kind"])
+    x, rep = _solver(p, case["m"], case["config"]).solve(p.rhs)
+    xref = np.load(os.path.join(HERE, "golden_gmres.npz"))[case["name"]]
+    assert rep["converged"] and rep["solver"] == case["config"]["solver"]["type"]
+    assert abs(rep["iterations"] - case["iterations"]) <= 1, (rep["iterations"], case["iterations"])
+    assert rep["relative_residual"] <= max(1e-8, 2 * case["relative_residual"])
+    assert np.linalg.norm(x - xref) <= 1e-6 * np.linalg.norm(xref)

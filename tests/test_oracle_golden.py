@@ -103,3 +103,28 @@ def test_solves_match_reference(case):
     # same arithmetic in the same order: the oracle reproduces the reference bitwise
     assert rep["relative_residual"] == case["relative_residual"]
     assert np.array_equal(x, arrays()[f"solve_{case['name']}_x"])
+
+
+def _gmres_cases():
+    import json
+    import os
+
+    from golden_data import HERE
+
+    with open(os.path.join(HERE, "golden_gmres.json")) as fh:
+        return json.load(fh)
+
+
+@pytest.mark.parametrize("case", _gmres_cases(), ids=lambda c: c["name"])
+def test_gmres_solves_match_reference(case):
+    import os
+
+    from golden_data import HERE
+
+    p = problems.make_problem(case["shape"], problems.boxes_for(case["m"]), case["kind"])
+    s = port.DeflatedSolverOracle(p.matrix, p.partition, config=SolverConfig(case["config"]), coords=p.coords)
+    x, rep = s.solve(p.rhs)
+    assert rep["iterations"] == case["iterations"]
+    assert rep["relative_residual"] == case["relative_residual"]
+    xr = np.load(os.path.join(HERE, "golden_gmres.npz"))[case["name"]]
+    assert np.array_equal(x, xr)
