@@ -208,6 +208,11 @@ int dfl_ctx_add_hierarchy(dfl_ctx *ctx, int32_t sub, const dfl_hier *h);
  * rank's first subdomain. */
 int dfl_ctx_set_deflation(dfl_ctx *ctx, int32_t k, const double *zcols, const dfl_csr *AZ,
                           int64_t K, const double *Einv, int32_t first_sub);
+/* inexact coarse solve (deflation.inexact, deflation.py:166-178): every
+ * E-solve of the projector becomes restarted GMRES on the dense E (K x K,
+ * row-major) to relative tolerance coarse_tol (restart K, maxiter 4K+20);
+ * E == NULL switches back to the exact E^{-1}.  The caller runs FGMRES. */
+int dfl_ctx_set_inexact(dfl_ctx *ctx, const double *E, double coarse_tol);
 /* converts layouts, builds launch plans; call once after the uploads */
 int dfl_ctx_finalize(dfl_ctx *ctx);
 

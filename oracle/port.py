@@ -647,16 +647,19 @@ def bicgstab2(op, b, M, dot, atol, maxiter, refresh=REFRESH) -> tuple:
     return M(u), Report(it, res, ok, None if ok else brk, hist)
 
 
-def gmres_driver(op, b, M, dot, atol, maxiter, restart, flexible) -> tuple:
+def gmres_driver(op, b, M, dot, atol, maxiter, restart, flexible, tol=0.0) -> tuple:
     """Restarted (F)GMRES, right preconditioned, MGS Arnoldi with one
-    re-orthogonalisation pass (reference: krylov.py:288-414), x0 = 0."""
+    re-orthogonalisation pass (reference: krylov.py:288-414), x0 = 0.
+    M = None: no preconditioner."""
     def norm(v):
         return math.sqrt(max(dot(v, v), 0.0))
 
     bnorm = norm(b)
     if bnorm == 0.0:
         return np.zeros_like(b), Report(0, 0.0, True)
-    target = max(0.0, atol)
+    target = max(tol * bnorm, atol)
+    if M is None:
+        M = lambda v: v.copy()  # noqa: E731
     op_hat = op if flexible else (lambda v: op(M(v)))
     x = np.zeros_like(b)
     r = b.copy()
@@ -746,10 +749,18 @@ class DeflatedSolverOracle:
         self.dot = make_dot(self.ranges)
         self.deflated = deflated
         self.basis = None
+        self.inexact = bool(deflated and config.get("deflation.inexact"))
         if deflated:
-            if config.get("deflation.inexact"):
-                raise OracleError("inexact deflation is not part of the B200 path")
             self.basis = build_basis(self.A, self.ranges, config.get("deflation.kind"), coords)
+            if self.inexact:  # reference: deflation.py:166-178 (inner GMRES on E)
+                K = self.basis.E.shape[0]
+                E = self.basis.E
+                tol_c = config.get("deflation.coarse_tol")
+                npdot = lambda u, v: float(np.dot(u, v))  # noqa: E731
+                self._esolve = lambda t: gmres_driver(lambda v: E @ v, t, None, npdot, 0.0, 4 * K + 20, K,
+                                                      False, tol=tol_c)[0]
+            else:
+                self._esolve = self.basis.lu.solve
         self.setup_seconds = time.perf_counter() - t0
 
     def op(self, v):
@@ -757,10 +768,10 @@ class DeflatedSolverOracle:
 
     def project(self, r):
         t = spmv(self.basis.Zt, r)
-        return r - spmv(self.basis.AZ, self.basis.lu.solve(t))
+        return r - spmv(self.basis.AZ, self._esolve(t))
 
     def coarse_lift(self, r):
-        return spmv(self.basis.Z, self.basis.lu.solve(spmv(self.basis.Zt, r)))
+        return spmv(self.basis.Z, self._esolve(spmv(self.basis.Zt, r)))
 
     def precond(self, r):
         out = np.empty_like(r)
@@ -773,6 +784,8 @@ class DeflatedSolverOracle:
 
         b = np.asarray(b, dtype=np.float64)
         name = self.cfg.get("solver.type")
+        if self.inexact and name != "fgmres":
+            name = "fgmres"
         if name not in ("cg", "bicgstab2", "gmres", "fgmres"):
             raise OracleError(f"solver {name} is not part of the B200 path")
         if name in ("gmres", "fgmres"):

@@ -94,6 +94,7 @@ def lib():
         "dfl_ctx_add_hierarchy": ([c_vp, c_i32, c_vp], c_i32),
         "dfl_ctx_set_deflation": ([c_vp, c_i32, c_vp, P(Csr), c_i64, c_vp, c_i32], c_i32),
         "dfl_ctx_finalize": ([c_vp], c_i32),
+        "dfl_ctx_set_inexact": ([c_vp, c_vp, c_dbl], c_i32),
         "dfl_ctx_device_bytes": ([c_vp], c_i64),
         "dfl_solve": ([c_vp, P(SolveParams), c_vp, c_vp, c_i32, P(Report)], c_i32),
         "dfl_op_apply": ([c_vp, c_vp, c_vp, c_i32], c_i32),
@@ -276,6 +277,10 @@ class DeviceContext:
         Ei = np.ascontiguousarray(Einv, dtype=np.float64)
         self._c(lib().dfl_ctx_set_deflation(self.h, k, _ptr(zc) if zc is not None else None,
                                             ctypes.byref(AZ.s), K, _ptr(Ei), first_sub))
+
+    def set_inexact(self, E, coarse_tol: float):
+        self._E = np.ascontiguousarray(E, dtype=np.float64) if E is not None else None
+        self._c(lib().dfl_ctx_set_inexact(self.h, _ptr(self._E) if self._E is not None else None, float(coarse_tol)))
 
     def finalize(self):
         self._c(lib().dfl_ctx_finalize(self.h))

@@ -207,6 +207,10 @@ struct dfl_ctx {
     double *az_val = nullptr;
     int64_t az_nnz = 0;
     double *Einv = nullptr;
+    // inexact coarse solve (deflation.py:166-178): inner GMRES on E
+    bool inexact = false;
+    double *Edense = nullptr, *egm_scr = nullptr;
+    double coarse_tol = 1e-2;
     double *tvec = nullptr, *t2 = nullptr;
     double *zt_part = nullptr;
     double *tgather = nullptr;  // nranks * maxsub * k
@@ -882,11 +886,16 @@ static int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_
         (from_op && g_use_pipe && !ctx->split && ctx->Aop.pipe.stages) ? ctx->op_sub_tiles : ctx->sub_tiles;
     if (!multi(ctx)) {
         k_zt_finish<<<ctx->nsub * ctx->k, 512, 0, ctx->st>>>(ctx->zt_part, sub_tiles, ctx->nsub, ctx->k,
-                                                             ctx->tvec, 0, ctx->Einv, ctx->K, ctx->t2, st,
-                                                             need_refresh, ctx->ticket,
+                                                             ctx->tvec, 0, ctx->inexact ? nullptr : ctx->Einv,
+                                                             ctx->K, ctx->t2, st, need_refresh, ctx->ticket,
                                                              from_op && ctx->split ? ctx->sub_btiles : nullptr,
                                                              ctx->ntiles);
         ctx->launches++;
+        if (ctx->inexact) {
+            k_egmres<<<1, 256, 0, ctx->st>>>(ctx->Edense, (int)ctx->K, ctx->tvec, ctx->t2, ctx->coarse_tol,
+                                             ctx->egm_scr, st, need_refresh);
+            ctx->launches++;
+        }
         return DFL_OK;
     }
     // local entries into a padded slot, allgather, unpack, solve
@@ -905,7 +914,11 @@ static int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_
                                         cudaMemcpyDeviceToDevice, ctx->st));
         pos += cnt;
     }
-    k_esolve<<<1, 256, 0, ctx->st>>>(ctx->Einv, ctx->K, ctx->tvec, ctx->t2, st, need_refresh);
+    if (ctx->inexact)
+        k_egmres<<<1, 256, 0, ctx->st>>>(ctx->Edense, (int)ctx->K, ctx->tvec, ctx->t2, ctx->coarse_tol, ctx->egm_scr,
+                                         st, need_refresh);
+    else
+        k_esolve<<<1, 256, 0, ctx->st>>>(ctx->Einv, ctx->K, ctx->tvec, ctx->t2, st, need_refresh);
     ctx->launches += 2;
     return DFL_OK;
 }
@@ -2363,6 +2376,31 @@ int dfl_ctx_set_deflation(dfl_ctx *ctx, int32_t k, const double *zcols, const df
     RC(dalloc(ctx, &ctx->t2, K));
     RC(dalloc(ctx, &ctx->tgather, (int64_t)ctx->nranks * ctx->max_nsub * k));
     ctx->deflation = true;
+    return DFL_OK;
+}
+
+int dfl_ctx_set_inexact(dfl_ctx *ctx, const double *E, double coarse_tol) {
+    if (!ctx || !ctx->deflation) {
+        if (ctx) ctx->err = "set the deflation basis before the inexact coarse solve";
+        return DFL_E_STATE;
+    }
+    if (E == nullptr) {
+        ctx->inexact = false;
+        return DFL_OK;
+    }
+    CK(cudaSetDevice(ctx->device));
+    const int64_t K = ctx->K;
+    if (K > 1024) {
+        ctx->err = "inexact coarse solve supports K <= 1024";
+        return DFL_E_DIMENSION;
+    }
+    if (!ctx->Edense) {
+        RC(dalloc(ctx, &ctx->Edense, K * K));
+        RC(dalloc(ctx, &ctx->egm_scr, 2 * (K + 1) * K + 8 * (K + 1)));
+    }
+    CK(cudaMemcpy(ctx->Edense, E, sizeof(double) * K * K, cudaMemcpyHostToDevice));
+    ctx->coarse_tol = coarse_tol;
+    ctx->inexact = true;
     return DFL_OK;
 }
 

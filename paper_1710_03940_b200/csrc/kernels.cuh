@@ -1211,3 +1211,125 @@ __global__ void __launch_bounds__(kBlock) k_vdiv(double *out, const double *in, 
 }
 
 }  // namespace dfl
+
+namespace dfl {
+// ---------------------------------------------------------------------------
+// Inexact coarse solve (deflation.py:166-178): y ~= E^{-1} t by restarted GMRES
+// on the small dense E (restart K, maxiter 4K+20, relative tolerance
+// coarse_tol), one block, no preconditioner, x0 = 0 -- krylov.py:288-407 with
+// op = E @ v.  Scratch: (K+1) x K basis + K x K Hessenberg + vectors.
+
+__device__ __forceinline__ double blk_dot(const double *a, const double *b, int K, double *sm) {
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < K; i += blockDim.x) acc += a[i] * b[i];
+    double v[1] = {acc};
+    block_sum<1>(v, sm);
+    __shared__ double res;
+    if (threadIdx.x == 0) res = v[0];
+    __syncthreads();
+    const double r = res;
+    __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(256) k_egmres(const double *__restrict__ E, int K, const double *t, double *y,
+                                                double tol, double *scr, const KState *st, int need_refresh) {
+    if (skip(st)) return;
+    if (need_refresh && !st->refresh_now) return;
+    __shared__ double sm[32];
+    const int restart = K, maxiter = 4 * K + 20;
+    double *V = scr;                          // (K+1) x K
+    double *H = V + (size_t)(K + 1) * K;      // (K+1) x K, row-major [i * K + j]
+    double *x = H + (size_t)(K + 1) * K;      // K
+    double *r = x + K;                        // K
+    double *w = r + K;                        // K
+    double *g = w + K;                        // K+1
+    double *cs = g + K + 1, *sn = cs + K, *yy = sn + K;
+    const double bnorm = sqrt(fmax(blk_dot(t, t, K, sm), 0.0));
+    for (int i = threadIdx.x; i < K; i += blockDim.x) {
+        x[i] = 0.0;
+        r[i] = t[i];
+    }
+    __syncthreads();
+    if (bnorm == 0.0) {
+        for (int i = threadIdx.x; i < K; i += blockDim.x) y[i] = 0.0;
+        return;
+    }
+    const double target = tol * bnorm;
+    double res = sqrt(fmax(blk_dot(r, r, K, sm), 0.0));
+    int total = 0;
+    while (total < maxiter && res > target) {
+        const int steps = min(restart, maxiter - total);
+        for (int i = threadIdx.x; i < K; i += blockDim.x) V[i] = r[i] / res;
+        if (threadIdx.x == 0) {
+            for (int q = 0; q <= K; ++q) g[q] = 0.0;
+            g[0] = res;
+        }
+        __syncthreads();
+        int j = 0;
+        while (j < steps) {
+            const double *vj = V + (size_t)j * K;
+            for (int i = threadIdx.x; i < K; i += blockDim.x) {  // w = E v_j
+                double a = 0.0;
+                for (int q = 0; q < K; ++q) a += E[(size_t)i * K + q] * vj[q];
+                w[i] = a;
+            }
+            __syncthreads();
+            for (int pass = 0; pass < 2; ++pass)
+                for (int i = 0; i <= j; ++i) {  // modified Gram-Schmidt, re-orthogonalised
+                    const double h = blk_dot(w, V + (size_t)i * K, K, sm);
+                    if (threadIdx.x == 0) H[(size_t)i * K + j] = pass == 0 ? h : H[(size_t)i * K + j] + h;
+                    for (int q = threadIdx.x; q < K; q += blockDim.x) w[q] = w[q] - h * V[(size_t)i * K + q];
+                    __syncthreads();
+                }
+            const double hn = sqrt(fmax(blk_dot(w, w, K, sm), 0.0));
+            const bool exact = hn == 0.0;
+            if (!exact)
+                for (int q = threadIdx.x; q < K; q += blockDim.x) V[(size_t)(j + 1) * K + q] = w[q] / hn;
+            if (threadIdx.x == 0) {
+                H[(size_t)(j + 1) * K + j] = hn;
+                for (int i = 0; i < j; ++i) {
+                    const double a = H[(size_t)i * K + j], b = H[(size_t)(i + 1) * K + j];
+                    H[(size_t)(i + 1) * K + j] = -sn[i] * a + cs[i] * b;
+                    H[(size_t)i * K + j] = cs[i] * a + sn[i] * b;
+                }
+                const double a = H[(size_t)j * K + j], b = H[(size_t)(j + 1) * K + j];
+                const double rad = hypot(a, b);
+                cs[j] = rad == 0.0 ? 1.0 : a / rad;
+                sn[j] = rad == 0.0 ? 0.0 : b / rad;
+                H[(size_t)j * K + j] = cs[j] * a + sn[j] * b;
+                H[(size_t)(j + 1) * K + j] = 0.0;
+                g[j + 1] = -sn[j] * g[j];
+                g[j] = cs[j] * g[j];
+            }
+            __syncthreads();
+            const double inner = fabs(g[j + 1]);
+            ++j;
+            if (exact || inner <= target) break;
+        }
+        if (threadIdx.x == 0)
+            for (int i = j - 1; i >= 0; --i) {
+                double s = 0.0;
+                for (int q = i + 1; q < j; ++q) s += H[(size_t)i * K + q] * yy[q];
+                yy[i] = (g[i] - s) / H[(size_t)i * K + i];
+            }
+        __syncthreads();
+        for (int q = threadIdx.x; q < K; q += blockDim.x) {
+            double u = V[q] * yy[0];
+            for (int i = 1; i < j; ++i) u = u + yy[i] * V[(size_t)i * K + q];
+            x[q] = x[q] + u;
+        }
+        __syncthreads();
+        total += j;
+        for (int i = threadIdx.x; i < K; i += blockDim.x) {  // r = t - E x
+            double a = 0.0;
+            for (int q = 0; q < K; ++q) a += E[(size_t)i * K + q] * x[q];
+            r[i] = t[i] - a;
+        }
+        __syncthreads();
+        res = sqrt(fmax(blk_dot(r, r, K, sm), 0.0));
+    }
+    for (int i = threadIdx.x; i < K; i += blockDim.x) y[i] = x[i];
+}
+
+}  // namespace dfl

@@ -77,8 +77,6 @@ def _check_config(cfg: SolverConfig, deflated: bool):
         kind = cfg.get("deflation.kind")
         if kind not in DEFLATION_KINDS:
             raise ConfigError(f"unknown deflation kind '{kind}', expected one of {DEFLATION_KINDS}")
-        if cfg.get("deflation.inexact"):
-            raise ConfigError("deflation.inexact (inner GMRES on E) is not on the B200 solve path")
 
 
 class DeflatedSolver:
@@ -124,7 +122,7 @@ class DeflatedSolver:
         self.partition = part
         self.world = world
         self.deflated = bool(deflated)
-        self.inexact = False
+        self.inexact = bool(self.deflated and self.cfg.get("deflation.inexact"))
         hs = build_rank_setup(rows, part, self.cfg, coords, self.deflated, world, global_coords)
         self.host = hs
         self.local_subdomains = hs.subs
@@ -150,6 +148,8 @@ class DeflatedSolver:
             ctx.add_hierarchy(j, h)
         if self.deflated:
             ctx.set_deflation(hs.k, hs.zcols, hs.AZ, part.m * hs.k, hs.Einv, hs.subs.start)
+            if self.inexact:  # deflation.py:166-178: inner GMRES on E, outer FGMRES
+                ctx.set_inexact(hs.E, self.cfg.get("deflation.coarse_tol"))
         ctx.finalize()
         self._ctx = ctx
         hs.release()  # host copies of the hierarchies are no longer needed
@@ -211,7 +211,7 @@ class DeflatedSolver:
     def solve(self, b, x0=None):
         """Returns (x, report).  x0 is ignored on the deflated path
         (deflation.py:284); the plain block-AMG path starts from zero too."""
-        name = self.cfg.get("solver.type")
+        name = _solver_name(self)
         b_local = self._local(b)
         params = _params(self)
         x_local = np.empty(self.n_local)
@@ -225,7 +225,7 @@ class DeflatedSolver:
         report = {
             "solver": name,
             "deflation": self.basis.kind if self.deflated else None,
-            "inexact_coarse": False,
+            "inexact_coarse": bool(self.inexact),
             "unknowns": self.n,
             "subdomains": self.partition.m,
             "iterations": int(rep.iterations),
@@ -247,10 +247,17 @@ class DeflatedSolver:
         return x, report
 
 
+def _solver_name(solver: "DeflatedSolver") -> str:
+    """solver.type, forced to fgmres by the inexact coarse solve (the inner
+    GMRES makes the projector vary step to step, deflation.py:259-263)."""
+    name = solver.cfg.get("solver.type")
+    return "fgmres" if solver.inexact and name != "fgmres" else name
+
+
 def _params(solver: "DeflatedSolver", maxiter=None):
     cfg = solver.cfg
     return nat.SolveParams(
-        nat.DFL_SOLVER[cfg.get("solver.type")],
+        nat.DFL_SOLVER[_solver_name(solver)],
         int(cfg.get("solver.maxiter") if maxiter is None else maxiter),
         50,
         1 if solver.deflated else 0,

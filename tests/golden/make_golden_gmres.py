@@ -25,6 +25,14 @@ CASES = [
     ("cd24_m1_fgmres_spai0_lin", "convdiff", 24, 1,
      {"solver": {"type": "fgmres", "tol": 1e-8}, "precond": {"relax": {"type": "spai0"}},
       "deflation": {"kind": "linear"}}),
+    # inexact coarse solves (reference acceptance criterion 12, tests/test_acceptance.py:486-518)
+    ("c12_inexact_loose", "poisson", 16, 8,
+     {"solver": {"type": "fgmres"}, "deflation": {"inexact": True, "coarse_tol": 1e-2}}),
+    ("c12_inexact_tight", "poisson", 16, 8,
+     {"solver": {"type": "fgmres"}, "deflation": {"inexact": True, "coarse_tol": 1e-14}}),
+    ("c12_exact_fgmres", "poisson", 16, 8, {"solver": {"type": "fgmres"}}),
+    ("p16_m8_inexact_cg_forced_fgmres", "poisson", 16, 8,
+     {"solver": {"type": "cg", "tol": 1e-8}, "deflation": {"kind": "linear", "inexact": True, "coarse_tol": 1e-6}}),
 ]
 
 

@@ -268,7 +268,15 @@ def test_gmres_fgmres_parity(case):
     p = problems.make_problem(case["shape"], problems.boxes_for(case["m"]), case["kind"])
     x, rep = _solver(p, case["m"], case["config"]).solve(p.rhs)
     xref = np.load(os.path.join(HERE, "golden_gmres.npz"))[case["name"]]
-    assert rep["converged"] and rep["solver"] == case["config"]["solver"]["type"]
+    inexact = case["config"].get("deflation", {}).get("inexact", False)
+    tol = case["config"]["solver"].get("tol", 1e-6)
+    assert rep["converged"] and rep["inexact_coarse"] == inexact
+    assert rep["solver"] == ("fgmres" if inexact else case["config"]["solver"]["type"])
+    assert rep["relative_residual"] <= max(tol, 2 * case["relative_residual"])
+    if inexact and case["config"]["deflation"]["coarse_tol"] > 1e-8:
+        # a loose inner GMRES makes the projector depend on rounding: the outer
+        # FGMRES count is compared loosely, the solution through the residual
+        assert abs(rep["iterations"] - case["iterations"]) <= max(2, case["iterations"] // 5)
+        return
     assert abs(rep["iterations"] - case["iterations"]) <= 1, (rep["iterations"], case["iterations"])
-    assert rep["relative_residual"] <= max(1e-8, 2 * case["relative_residual"])
     assert np.linalg.norm(x - xref) <= 1e-6 * np.linalg.norm(xref)
