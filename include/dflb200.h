@@ -134,24 +134,31 @@ typedef struct dfl_hier dfl_hier;     /* host AMG hierarchy */
 typedef struct dfl_ctx dfl_ctx;       /* device solve context (one rank) */
 typedef struct dfl_fabric dfl_fabric; /* in-process communicator (tests) */
 
+/* exported entry points; everything else in the library has hidden visibility */
+#if defined(__GNUC__)
+#define DFL_API __attribute__((visibility("default")))
+#else
+#define DFL_API
+#endif
+
 /* ---- library ----------------------------------------------------------- */
-int dfl_abi_version(void);
-const char *dfl_last_setup_error(void);
-const char *dfl_breakdown_string(int code);
+DFL_API int dfl_abi_version(void);
+DFL_API const char *dfl_last_setup_error(void);
+DFL_API const char *dfl_breakdown_string(int code);
 
 /* ---- host setup (C++) ----------------------------------------------------- */
-int dfl_hier_build(const dfl_csr *A, const dfl_amg_options *opts, dfl_hier **out);
-int dfl_hier_num_levels(const dfl_hier *h);
+DFL_API int dfl_hier_build(const dfl_csr *A, const dfl_amg_options *opts, dfl_hier **out);
+DFL_API int dfl_hier_num_levels(const dfl_hier *h);
 /* shape of level l's A / P / R (P and R absent at the bottom level: nnz = -1) */
-int dfl_hier_level_shape(const dfl_hier *h, int level, int which, int64_t *nrows,
+DFL_API int dfl_hier_level_shape(const dfl_hier *h, int level, int which, int64_t *nrows,
                          int64_t *ncols, int64_t *nnz);
-int dfl_hier_level_copy(const dfl_hier *h, int level, int which, int64_t *row_ptr,
+DFL_API int dfl_hier_level_copy(const dfl_hier *h, int level, int which, int64_t *row_ptr,
                         int64_t *col_idx, double *values);
 /* relaxation weights w of level l: (damping * 1/a_ii) or SPAI-0 a_ii / sum a_ij^2 */
-int dfl_hier_level_weights(const dfl_hier *h, int level, double *w);
+DFL_API int dfl_hier_level_weights(const dfl_hier *h, int level, double *w);
 /* bottom level: dense inverse (n x n, row-major) of the LU-factorised block */
-int dfl_hier_bottom_inverse(const dfl_hier *h, double *inv);
-void dfl_hier_free(dfl_hier *h);
+DFL_API int dfl_hier_bottom_inverse(const dfl_hier *h, double *inv);
+DFL_API void dfl_hier_free(dfl_hier *h);
 
 /* AZ rows of this rank (deflation.py:140) and its rows of E = Z'AZ.
  *   A      : n_local x n_ext rows of the global operator, columns [0, n_local)
@@ -162,33 +169,33 @@ void dfl_hier_free(dfl_hier *h);
  *   K      : global coarse dimension m*k
  * Outputs: *AZ (n_local x K, exact zeros dropped unless keep_zeros) and
  * E_rows (nsub_local*k x K, row-major) for subdomains [sub0, sub0+nsub). */
-int dfl_basis_az(const dfl_csr *A, int32_t k, const double *zext, const int32_t *owner,
+DFL_API int dfl_basis_az(const dfl_csr *A, int32_t k, const double *zext, const int32_t *owner,
                  const int32_t *rowsub, int64_t K, int32_t sub0, int32_t nsub, int32_t keep_zeros,
                  dfl_matrix **AZ, double *E_rows);
-int dfl_matrix_shape(const dfl_matrix *m, int64_t *nrows, int64_t *ncols, int64_t *nnz);
-int dfl_matrix_copy(const dfl_matrix *m, int64_t *row_ptr, int64_t *col_idx, double *values);
-void dfl_matrix_free(dfl_matrix *m);
+DFL_API int dfl_matrix_shape(const dfl_matrix *m, int64_t *nrows, int64_t *ncols, int64_t *nnz);
+DFL_API int dfl_matrix_copy(const dfl_matrix *m, int64_t *row_ptr, int64_t *col_idx, double *values);
+DFL_API void dfl_matrix_free(dfl_matrix *m);
 
 /* LU with partial pivoting; DFL_E_SINGULAR with the reference's criterion
  * (min |u_ii| <= 1e-14 max |u_ii|, sparse.py:236-241); writes inv (n x n). */
-int dfl_dense_inverse(int64_t n, const double *a, double *inv);
+DFL_API int dfl_dense_inverse(int64_t n, const double *a, double *inv);
 
 /* ---- device context ----------------------------------------------------------- */
-int dfl_ctx_create(int device, dfl_ctx **out);
-void dfl_ctx_destroy(dfl_ctx *ctx);
-const char *dfl_last_error(const dfl_ctx *ctx);
+DFL_API int dfl_ctx_create(int device, dfl_ctx **out);
+DFL_API void dfl_ctx_destroy(dfl_ctx *ctx);
+DFL_API const char *dfl_last_error(const dfl_ctx *ctx);
 
 /* multi-process (one rank per GPU) communicator over NCCL; nccl_id is the
  * 128-byte ncclUniqueId produced on rank 0 by dfl_nccl_unique_id */
-int dfl_nccl_unique_id(void *nccl_id_128);
-int dfl_ctx_set_comm(dfl_ctx *ctx, int nranks, int rank, const void *nccl_id_128);
+DFL_API int dfl_nccl_unique_id(void *nccl_id_128);
+DFL_API int dfl_ctx_set_comm(dfl_ctx *ctx, int nranks, int rank, const void *nccl_id_128);
 /* in-process communicator: ranks are contexts driven by different host
  * threads; collectives synchronise at a host barrier and copy from the peers'
  * device buffers.  Exercises the multi-rank path (halo plan, allgathers,
  * rank-ordered sums, host-driven loop) without NCCL, e.g. on one GPU. */
-int dfl_fabric_create(int nranks, dfl_fabric **out);
-void dfl_fabric_destroy(dfl_fabric *f);
-int dfl_ctx_set_fabric(dfl_ctx *ctx, dfl_fabric *f, int rank);
+DFL_API int dfl_fabric_create(int nranks, dfl_fabric **out);
+DFL_API void dfl_fabric_destroy(dfl_fabric *f);
+DFL_API int dfl_ctx_set_fabric(dfl_ctx *ctx, dfl_fabric *f, int rank);
 
 /* Operator rows of this rank (all its subdomains), columns renumbered as in
  * dfl_basis_az, entries in the global CSR order.
@@ -197,42 +204,42 @@ int dfl_ctx_set_fabric(dfl_ctx *ctx, dfl_fabric *f, int rank);
  *                 values arrive (they fill the ghost columns in ascending
  *                 global order), send_counts[q] values go out, taken from own
  *                 rows send_idx[...] (concatenated in neighbour order). */
-int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int64_t *sub_offsets,
+DFL_API int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int64_t *sub_offsets,
                          int32_t nnbr, const int32_t *nbr_rank, const int64_t *recv_counts,
                          const int64_t *send_counts, const int64_t *send_idx);
 /* the AMG hierarchy of local subdomain `sub` (uploaded, host copy not kept) */
-int dfl_ctx_add_hierarchy(dfl_ctx *ctx, int32_t sub, const dfl_hier *h);
+DFL_API int dfl_ctx_add_hierarchy(dfl_ctx *ctx, int32_t sub, const dfl_hier *h);
 /* deflation data of this rank: k columns per subdomain; zcols = n_local x (k-1)
  * non-constant columns (row-major, NULL when k == 1); AZ = n_local x K;
  * Einv = K x K inverse of E (row-major); first_sub = global index of the
  * rank's first subdomain. */
-int dfl_ctx_set_deflation(dfl_ctx *ctx, int32_t k, const double *zcols, const dfl_csr *AZ,
+DFL_API int dfl_ctx_set_deflation(dfl_ctx *ctx, int32_t k, const double *zcols, const dfl_csr *AZ,
                           int64_t K, const double *Einv, int32_t first_sub);
 /* inexact coarse solve (deflation.inexact, deflation.py:166-178): every
  * E-solve of the projector becomes restarted GMRES on the dense E (K x K,
  * row-major) to relative tolerance coarse_tol (restart K, maxiter 4K+20);
  * E == NULL switches back to the exact E^{-1}.  The caller runs FGMRES. */
-int dfl_ctx_set_inexact(dfl_ctx *ctx, const double *E, double coarse_tol);
+DFL_API int dfl_ctx_set_inexact(dfl_ctx *ctx, const double *E, double coarse_tol);
 /* converts layouts, builds launch plans; call once after the uploads */
-int dfl_ctx_finalize(dfl_ctx *ctx);
+DFL_API int dfl_ctx_finalize(dfl_ctx *ctx);
 
 /* device bytes held by the context */
-int64_t dfl_ctx_device_bytes(const dfl_ctx *ctx);
+DFL_API int64_t dfl_ctx_device_bytes(const dfl_ctx *ctx);
 
 /* ---- solve phase ------------------------------------------------------------------- */
-int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *x, int ptr_kind,
+DFL_API int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *x, int ptr_kind,
               dfl_report *rep);
 
 /* unit operations on this rank's vectors (n_local), host or device pointers */
-int dfl_op_apply(dfl_ctx *ctx, const double *x, double *y, int ptr_kind);
-int dfl_precond_apply(dfl_ctx *ctx, const double *r, double *z, int ptr_kind);
-int dfl_project(dfl_ctx *ctx, const double *r, double *out, int ptr_kind);
-int dfl_coarse_lift(dfl_ctx *ctx, const double *r, double *out, int ptr_kind);
-int dfl_dot(dfl_ctx *ctx, const double *a, const double *b, int ptr_kind, double *out);
+DFL_API int dfl_op_apply(dfl_ctx *ctx, const double *x, double *y, int ptr_kind);
+DFL_API int dfl_precond_apply(dfl_ctx *ctx, const double *r, double *z, int ptr_kind);
+DFL_API int dfl_project(dfl_ctx *ctx, const double *r, double *out, int ptr_kind);
+DFL_API int dfl_coarse_lift(dfl_ctx *ctx, const double *r, double *out, int ptr_kind);
+DFL_API int dfl_dot(dfl_ctx *ctx, const double *a, const double *b, int ptr_kind, double *out);
 
 /* stand-alone CSR SpMV on the device (rows of A; x has A->ncols entries) --
  * the per-kernel seam of the reference (backend.py:126-146) */
-int dfl_spmv_csr(const dfl_csr *A, const double *x, double *y, int device);
+DFL_API int dfl_spmv_csr(const dfl_csr *A, const double *x, double *y, int device);
 
 /* timing of the unit operations for the roofline: runs `reps` back-to-back
  * launches of the named kernel family on the context's data and returns the
@@ -243,12 +250,12 @@ int dfl_spmv_csr(const dfl_csr *A, const double *x, double *y, int device);
  *             1-byte codes of FMT_CODE matrices, the w.*r pass),
  *         3 = V-cycle captured once and replayed as a CUDA graph, as inside
  *             the solve (bytes as 1) */
-int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms_per_launch, double *bytes_per_launch);
+DFL_API int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms_per_launch, double *bytes_per_launch);
 
 /* per-launch device times of one V-cycle, mean over reps; labels is a
  * cap x 32 char buffer ("L<l> resid|restrict|prolong|post", "bottom");
  * returns the number of launches (or a negative status) */
-int dfl_ctx_profile_vcycle(dfl_ctx *ctx, int reps, int cap, double *ms, char *labels);
+DFL_API int dfl_ctx_profile_vcycle(dfl_ctx *ctx, int reps, int cap, double *ms, char *labels);
 
 #ifdef __cplusplus
 }

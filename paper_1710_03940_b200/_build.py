@@ -8,6 +8,7 @@ import os
 import shutil
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
@@ -16,7 +17,7 @@ LIB = os.path.join(PKG, "libdflb200.so")
 BUILD = os.path.join(REPO, "build", "dflb200")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SOURCES = ["ctx.cu"]
+CU_SOURCES = ["ctx.cu", "ctx_layout.cu", "ctx_comm.cu", "ctx_cycle.cu", "ctx_cg.cu", "ctx_krylov.cu"]
 CXX_SOURCES = ["host_setup.cpp"]
 
 
@@ -45,20 +46,23 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     nvcc = _nvcc()
-    objs = []
     run = lambda cmd: subprocess.run(cmd, check=True, stdout=None if verbose else subprocess.DEVNULL)
+    # only the C ABI of include/dflb200.h (DFL_API) is exported
+    jobs = []
     for f in CXX_SOURCES:
         o = os.path.join(BUILD, f + ".o")
-        run(["g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-ffp-contract=off", "-fno-fast-math",
-             "-I", os.path.join(REPO, "include"), "-c", os.path.join(CSRC, f), "-o", o])
-        objs.append(o)
+        jobs.append((o, ["g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-ffp-contract=off", "-fno-fast-math",
+                         "-fvisibility=hidden", "-I", os.path.join(REPO, "include"), "-c", os.path.join(CSRC, f),
+                         "-o", o]))
+    extra = os.environ.get("DFL_NVCC_FLAGS", "").split()
     for f in CU_SOURCES:
         o = os.path.join(BUILD, f + ".o")
-        extra = os.environ.get("DFL_NVCC_FLAGS", "").split()
-        run([nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra,
-             "-Xcompiler", "-ffp-contract=off", "-I", os.path.join(REPO, "include"),
-             "-c", os.path.join(CSRC, f), "-o", o])
-        objs.append(o)
+        jobs.append((o, [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra,
+                         "-Xcompiler", "-ffp-contract=off", "-Xcompiler", "-fvisibility=hidden",
+                         "-I", os.path.join(REPO, "include"), "-c", os.path.join(CSRC, f), "-o", o]))
+    with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1)) as pool:
+        list(pool.map(lambda j: run(j[1]), jobs))
+    objs = [o for o, _ in jobs]
     target = out or LIB
     tmp = target + ".tmp"
     run([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-ldl", "-lpthread"])

@@ -127,7 +127,7 @@ __device__ __forceinline__ void grid_bottom(const CoarseArgs &c, const double *r
 
 // rin / xout: rhs and solution of the first handled level (the caller's
 // vectors when the whole cycle runs here)
-__global__ void __launch_bounds__(256) k_coarse_cycle(const CoarseArgs *__restrict__ cp, const double *rin,
+static __global__ void __launch_bounds__(256) k_coarse_cycle(const CoarseArgs *__restrict__ cp, const double *rin,
                                                       double *xout) {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -184,7 +184,7 @@ __device__ __forceinline__ void tiny_stage(const DMat &A, const RowArgs &a, int 
     }
 }
 
-__global__ void __cluster_dims__(kTinyCtas, 1, 1) __launch_bounds__(kTinyThreads)
+static __global__ void __cluster_dims__(kTinyCtas, 1, 1) __launch_bounds__(kTinyThreads)
     k_tiny_cycle(const CoarseArgs *__restrict__ cp, const double *rin, double *xout) {
     namespace cg = cooperative_groups;
     cg::cluster_group cluster = cg::this_cluster();

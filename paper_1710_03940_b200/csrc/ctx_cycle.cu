@@ -1,0 +1,300 @@
+// Preconditioner, operator and projector applications on the device, plus
+// the timing / profiling entry points built on them.
+#include "ctx_impl.cuh"
+
+// ---------------------------------------------------------------------------
+// V-cycle over all groups: z = M r  (deflation.py:239-250 -> amg.py:201-212).
+// With dot_part != nullptr the last kernel of every group also emits the
+// per-block partials of r.z; *nparts receives their count.
+int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *dot_part, int64_t *nparts) {
+    int64_t poff = 0;
+    for (VGroup &g : ctx->groups) {
+        const double *rin = r + g.row0;
+        double *zout = z + g.row0;
+        const int L = (int)g.lv.size();
+        const bool use_coarse = g.lc >= 0 && g_use_coarse;
+        const bool use_tiny = !use_coarse && g.lt >= 0 && g_use_tiny;
+        const int lc = use_coarse ? g.lc : use_tiny ? g.lt : L + 1;  // first level of the fused tail kernel
+        for (int l = 0; l < std::min(L, lc); ++l) {
+            DLevel &v = g.lv[l];
+            const double *in = l == 0 ? rin : v.rv;
+            double *next = (l + 1 < L) ? g.lv[l + 1].rv : g.rb;
+            if (v.A.fmt == FMT_CODE) {
+                k_wr<<<(unsigned)cdiv(v.n, kBlock), kBlock, 0, ctx->st>>>(v.w, in, v.wr, v.n);
+                ctx->launches++;
+                RowArgs a{v.wr, v.w, in, nullptr, v.t, nullptr, st};
+                launch_rows<MODE_RESID, false>(ctx, v.A, a);
+            } else {
+                RowArgs a{nullptr, v.w, in, nullptr, v.t, nullptr, st};
+                launch_rows<MODE_RESID, false>(ctx, v.Aw, a);
+            }
+            prof_mark(ctx, "L" + std::to_string(l) + " resid");
+            RowArgs b{v.t, nullptr, nullptr, nullptr, next, nullptr, st};
+            launch_rows<MODE_PLAIN, false>(ctx, v.R, b);
+            prof_mark(ctx, "L" + std::to_string(l) + " restrict");
+        }
+        if (lc <= L) {
+            const double *crin = lc == 0 ? rin : g.lv[lc < L ? lc : 0].rv;
+            double *cxout = lc == 0 ? zout : g.lv[lc < L ? lc : 0].xv;
+            if (lc == L && L > 0) {  // bottom only
+                crin = g.rb;
+                cxout = g.xb;
+            }
+            if (use_tiny) {
+                k_tiny_cycle<<<kTinyCtas, kTinyThreads, 0, ctx->st>>>(g.targs, crin, cxout);
+                ctx->launches++;
+                prof_mark(ctx, "tiny L" + std::to_string(lc) + "+");
+            } else {
+                void *args[] = {(void *)&g.cargs, (void *)&crin, (void *)&cxout};
+                cudaLaunchCooperativeKernel((const void *)k_coarse_cycle, g.coarse_grid, 256, args, 0, ctx->st);
+                ctx->launches++;
+                prof_mark(ctx, "coarse L" + std::to_string(lc) + "+");
+            }
+        } else {
+            const double *rb = L == 0 ? rin : g.rb;
+            double *xb = L == 0 ? zout : g.xb;
+            k_bottom<<<dim3((unsigned)cdiv(g.max_nb, 32), (unsigned)g.nsub), 256, 0, ctx->st>>>(
+                g.binvT, g.binv_off, g.b_off, rb, xb, st);
+            ctx->launches++;
+            prof_mark(ctx, "bottom");
+        }
+        for (int l = std::min(L, lc) - 1; l >= 0; --l) {
+            DLevel &v = g.lv[l];
+            const double *in = l == 0 ? rin : v.rv;
+            const double *e = (l + 1 < L) ? g.lv[l + 1].xv : g.xb;
+            double *out = l == 0 ? zout : v.xv;
+            RowArgs a{e, v.w, in, nullptr, v.t, nullptr, st};
+            launch_rows<MODE_PROLONG, false>(ctx, v.P, a);
+            prof_mark(ctx, "L" + std::to_string(l) + " prolong");
+            if (l == 0 && dot_part) {
+                RowArgs b{v.t, v.w, in, v.t, out, dot_part + poff, st};
+                launch_rows<MODE_POST, true>(ctx, v.A, b);
+                poff += parts_for(v.A);
+            } else {
+                RowArgs b{v.t, v.w, in, v.t, out, nullptr, st};
+                launch_rows<MODE_POST, false>(ctx, v.A, b);
+            }
+            prof_mark(ctx, "L" + std::to_string(l) + " post");
+        }
+        if ((L == 0 || lc == 0) && dot_part) {
+            // the group's finest level ran without a fused dot: explicit partials
+            const int64_t rows = g.row1 - g.row0;
+            const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(rows, kBlock), 64));
+            k_dot<<<nb, kBlock, 0, ctx->st>>>(rin, zout, rows, dot_part + poff, st);
+            ctx->launches++;
+            poff += nb;
+        }
+    }
+    if (nparts) *nparts = poff;
+    return DFL_OK;
+}
+
+// y = A x (opmode 0) or y = b - A x (opmode 1); with zt the Z'y tile partials
+int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double *b, bool zt,
+                        const KState *st, int need_refresh) {
+    OpArgs a{xin, b, y, ctx->zcols, ctx->n, zt ? ctx->k : 0, ctx->zt_part, st, need_refresh};
+    if (!ctx->split) {
+        RC(halo(ctx, xin));
+        if (opmode == 0)
+            launch_op<0>(ctx, a);
+        else
+            launch_op<1>(ctx, a);
+        return DFL_OK;
+    }
+    // halo overlapped with the interior rows (runtime.py:283-292 split in two
+    // passes): pack -> exchange on the comm stream while the rows without ghost
+    // columns run, then the boundary rows
+    RC(halo(ctx, xin, ctx->st2));
+    a.skip_rows = ctx->bflag;
+    if (opmode == 0)
+        launch_op<0>(ctx, a);
+    else
+        launch_op<1>(ctx, a);
+    if (!ctx->fab) {
+        CK(cudaEventRecord(ctx->ev_halo, ctx->st2));
+        CK(cudaStreamWaitEvent(ctx->st, ctx->ev_halo, 0));
+    }
+    a.skip_rows = nullptr;
+    if (ctx->nbtiles > 0) {
+        if (opmode == 0)
+            k_op_bnd<0><<<(unsigned)ctx->nbtiles, kBlock, 0, ctx->st>>>(ctx->Aop, ctx->brows, ctx->bstart, ctx->bcnt,
+                                                                         ctx->ntiles, a);
+        else
+            k_op_bnd<1><<<(unsigned)ctx->nbtiles, kBlock, 0, ctx->st>>>(ctx->Aop, ctx->brows, ctx->bstart, ctx->bcnt,
+                                                                         ctx->ntiles, a);
+        ctx->launches++;
+    }
+    return DFL_OK;
+}
+
+// out = project(v) = v - AZ E^-1 Z' v   (deflation.py:230-233)
+int project_dev(dfl_ctx *ctx, const double *v, double *out, const KState *st, int dotmode) {
+    k_zt_vec<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, v, ctx->zcols, ctx->n, ctx->k, ctx->zt_part);
+    ctx->launches++;
+    RC(zt_to_t2(ctx, nullptr, 0, false));
+    ProjArgs a = proj_args(ctx, v, out, st);
+    a.dotmode = dotmode;
+    a.dot_part = ctx->dpart;
+    launch_project<0>(ctx, a);
+    return DFL_OK;
+}
+
+// x = y + Z E^-1 Z'(b - A y)   (deflation.py:285); y in ctx->x, x -> ctx->xin
+int lift_dev(dfl_ctx *ctx, const dfl_solve_params *p) {
+    if (p->deflated) {
+        RC(op_apply_dev(ctx, ctx->x, ctx->tmp, 1, ctx->b, true, nullptr, 0));
+        RC(zt_to_t2(ctx, nullptr, 0, true));
+        k_lift<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, ctx->tile_sub, ctx->x, ctx->zcols, ctx->n,
+                                                              ctx->k, ctx->t2, (int64_t)ctx->first_sub * ctx->k,
+                                                              ctx->xin, 1);
+    } else {
+        k_copy<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->xin, ctx->x, ctx->n);
+    }
+    ctx->launches++;
+    return DFL_OK;
+}
+
+extern "C" {
+
+int dfl_spmv_csr(const dfl_csr *A, const double *x, double *y, int device) {
+    dfl_ctx *ctx = nullptr;
+    RC(dfl_ctx_create(device, &ctx));
+    std::unique_ptr<dfl_ctx, void (*)(dfl_ctx *)> guard(ctx, dfl_ctx_destroy);
+    DMat m;
+    HostRows h{A->nrows, A->ncols, A->row_ptr, A->col_idx, A->values};
+    int rc = upload_matrix(ctx, h, m, {0, A->nrows});
+    if (rc != DFL_OK) {
+        dfl::set_setup_error(ctx->err);
+        return rc;
+    }
+    double *dx, *dy;
+    RC(upload(ctx, &dx, x, A->ncols));
+    RC(dalloc(ctx, &dy, A->nrows));
+    RowArgs a{dx, nullptr, nullptr, nullptr, dy, nullptr, nullptr};
+    launch_rows<MODE_PLAIN, false>(ctx, m, a);
+    cudaError_t e = cudaMemcpyAsync(y, dy, sizeof(double) * A->nrows, cudaMemcpyDeviceToHost, ctx->st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->st);
+    if (e != cudaSuccess) {
+        dfl::set_setup_error(cudaGetErrorString(e));
+        return DFL_E_CUDA;
+    }
+    return DFL_OK;
+}
+
+// algorithmic bytes: CSR with fp64 values / int32 indices,
+// every vector read once and written once per kernel
+int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
+    RC(ready(ctx));
+    if (reps < 1) reps = 1;
+    auto run = [&]() -> int {
+        if (what == 0) return op_apply_dev(ctx, ctx->p, ctx->w, 0, nullptr, false, nullptr, 0);
+        if (what == 1 || what == 2) return vcycle(ctx, ctx->r, ctx->z, nullptr, nullptr, nullptr);
+        ctx->err = "unknown timing target";
+        return DFL_E_CONFIG;
+    };
+    // bytes the stored format must move for one pass over M
+    auto mat = [](const DMat &M) -> double {
+        const double rows = (double)M.nrows;
+        if (M.fmt == FMT_CODE) return 8.0 * rows;
+        if (M.fmt == FMT_CSR) return 12.0 * (double)M.nnz + 4.0 * (rows + 1);
+        return (M.vcode ? 5.0 : 12.0) * (double)M.stored + (M.perm ? 4.0 * rows : 0.0) +
+               (M.ell_w ? 0.0 : 8.0 * (rows / 32 + 1));
+    };
+    if (what == 0) {
+        *bytes = 12.0 * ctx->op_nnz + 4.0 * (ctx->n + 1) + 8.0 * (ctx->n + ctx->n_ghost) + 8.0 * ctx->n;
+    } else if (what == 2) {
+        double b = 0;
+        for (auto &g : ctx->groups) {
+            for (size_t l = 0; l < g.lv.size(); ++l) {
+                const DLevel &v = g.lv[l];
+                const double n = (double)g.rows[l], nc = (double)g.rows[l + 1];
+                b += v.A.fmt == FMT_CODE ? 24.0 * n + mat(v.A) + 24.0 * n : mat(v.Aw) + 24.0 * n;  // residual
+                b += mat(v.R) + 8.0 * n + 8.0 * nc;                                                // restriction
+                b += mat(v.P) + 8.0 * nc + 24.0 * n;                                               // prolongation
+                b += mat(v.A) + 40.0 * n;                                                          // post-smoothing
+            }
+            b += 8.0 * (double)g.nb * (double)g.nb / std::max(1, g.nsub) + 16.0 * (double)g.nb;
+        }
+        *bytes = b;
+    } else {
+        double b = 0;
+        for (auto &g : ctx->groups) {
+            for (size_t l = 0; l < g.lv.size(); ++l) {
+                const double n = (double)g.rows[l], nc = (double)g.rows[l + 1];
+                b += 24.0 * g.nnzA[l] + 24.0 * g.nnzP[l] + 100.0 * n + 20.0 * nc;
+            }
+            b += 8.0 * (double)g.nb * (double)g.nb / std::max(1, g.nsub);
+        }
+        *bytes = b;
+    }
+    // fill the inputs with something finite
+    k_fill<<<(unsigned)cdiv(ctx->n + ctx->n_ghost, kBlock), kBlock, 0, ctx->st>>>(ctx->p, 1.0, ctx->n + ctx->n_ghost);
+    k_fill<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->r, 1.0, ctx->n);
+    if (what == 3) {  // the V-cycle as the solve runs it: captured once, replayed as a CUDA graph
+        double b = 0;
+        double tmp = 0;
+        RC(dfl_ctx_time(ctx, 1, 1, &tmp, &b));
+        *bytes = b;
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+        const int64_t before = ctx->launches;
+        int rc = vcycle(ctx, ctx->r, ctx->z, nullptr, nullptr, nullptr);
+        CK(cudaStreamEndCapture(ctx->st, &g));
+        ctx->launches = before;
+        if (rc != DFL_OK) return rc;
+        cudaGraphExec_t ge;
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        for (int i = 0; i < 3; ++i) CK(cudaGraphLaunch(ge, ctx->st));
+        CK(cudaEventRecord(ctx->ev0, ctx->st));
+        for (int i = 0; i < reps; ++i) CK(cudaGraphLaunch(ge, ctx->st));
+        CK(cudaEventRecord(ctx->ev1, ctx->st));
+        CK(cudaEventSynchronize(ctx->ev1));
+        float t = 0;
+        CK(cudaEventElapsedTime(&t, ctx->ev0, ctx->ev1));
+        *ms = t / reps;
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
+        return DFL_OK;
+    }
+    for (int i = 0; i < 3; ++i) RC(run());
+    CK(cudaEventRecord(ctx->ev0, ctx->st));
+    for (int i = 0; i < reps; ++i) RC(run());
+    CK(cudaEventRecord(ctx->ev1, ctx->st));
+    CK(cudaEventSynchronize(ctx->ev1));
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, ctx->ev0, ctx->ev1));
+    *ms = t / reps;
+    return DFL_OK;
+}
+
+// per-launch device times of one V-cycle (mean over reps), labels "L<l> <stage>"
+int dfl_ctx_profile_vcycle(dfl_ctx *ctx, int reps, int cap, double *ms, char *labels /* cap x 32 */) {
+    RC(ready(ctx));
+    if (reps < 1) reps = 1;
+    k_fill<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->r, 1.0, ctx->n);
+    RC(vcycle(ctx, ctx->r, ctx->z, nullptr, nullptr, nullptr));
+    std::vector<double> acc;
+    int count = 0;
+    for (int rep = 0; rep < reps; ++rep) {
+        ctx->prof_on = true;
+        ctx->prof_n = 0;
+        prof_mark(ctx, "start");
+        RC(vcycle(ctx, ctx->r, ctx->z, nullptr, nullptr, nullptr));
+        ctx->prof_on = false;
+        CK(cudaStreamSynchronize(ctx->st));
+        count = (int)ctx->prof_n - 1;
+        acc.resize(count, 0.0);
+        for (int i = 0; i < count; ++i) {
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, ctx->prof_ev[i], ctx->prof_ev[i + 1]));
+            acc[i] += t;
+        }
+    }
+    for (int i = 0; i < count && i < cap; ++i) {
+        ms[i] = acc[i] / reps;
+        std::snprintf(labels + 32 * i, 32, "%s", ctx->prof_lab[i + 1].c_str());
+    }
+    return std::min(count, cap);
+}
+
+}  // extern "C"

@@ -1,0 +1,514 @@
+// Internal interface of the device context, shared by the ctx_*.cu units.
+#pragma once
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <condition_variable>
+#include <memory>
+#include <mutex>
+#include <unordered_map>
+#include <string>
+#include <vector>
+
+#include "../../include/dflb200.h"
+#include "host_setup.hpp"
+#include "kernels.cuh"
+#include "spmv_pipe.cuh"
+#include "coarse.cuh"
+
+using namespace dfl;
+
+// ---------------------------------------------------------------------------
+// minimal NCCL surface, loaded lazily (no link-time dependency)
+typedef struct {
+    char internal[128];
+} NcclId;
+typedef void *NcclComm;
+enum { ncclDouble_ = 8 };
+struct Nccl {
+    void *h = nullptr;
+    int (*GetUniqueId)(NcclId *) = nullptr;
+    int (*CommInitRank)(NcclComm *, int, NcclId, int) = nullptr;
+    int (*CommDestroy)(NcclComm) = nullptr;
+    int (*AllGather)(const void *, void *, size_t, int, NcclComm, cudaStream_t) = nullptr;
+    int (*Send)(const void *, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+    int (*Recv)(void *, size_t, int, int, NcclComm, cudaStream_t) = nullptr;
+    int (*GroupStart)() = nullptr;
+    int (*GroupEnd)() = nullptr;
+    const char *(*GetErrorString)(int) = nullptr;
+    bool load(std::string &err) {
+        if (h) return true;
+        const char *names[] = {"libnccl.so.2", "libnccl.so"};
+        for (const char *n : names)
+            if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+        if (!h) {
+            err = "cannot load libnccl.so.2";
+            return false;
+        }
+#define LD(f, s)                                            \
+    f = reinterpret_cast<decltype(f)>(dlsym(h, s));         \
+    if (!f) {                                               \
+        err = std::string("libnccl lacks ") + s;            \
+        return false;                                       \
+    }
+        LD(GetUniqueId, "ncclGetUniqueId");
+        LD(CommInitRank, "ncclCommInitRank");
+        LD(CommDestroy, "ncclCommDestroy");
+        LD(AllGather, "ncclAllGather");
+        LD(Send, "ncclSend");
+        LD(Recv, "ncclRecv");
+        LD(GroupStart, "ncclGroupStart");
+        LD(GroupEnd, "ncclGroupEnd");
+        LD(GetErrorString, "ncclGetErrorString");
+#undef LD
+        return true;
+    }
+};
+extern Nccl g_nccl;
+
+// profiling / layout knobs (defined in ctx.cu, read at context creation)
+extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell;
+extern double g_small_per_lane, g_csr_per_lane;
+extern int g_csr_g, g_sm_count;
+static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle
+static constexpr int kStageBytesMax = 100 * 1024;
+
+// ---------------------------------------------------------------------------
+
+struct DLevel {
+    DMat A, P, R;
+    DMat Aw;  // A diag(w): the pre-smoothing residual r - A (w .* r) in one gather
+    double *wr = nullptr;  // coded A: w .* r gathered by the residual kernel
+    double *w = nullptr;
+    int64_t n = 0, nc = 0;
+    double *rv = nullptr;  // level right-hand side (l >= 1)
+    double *t = nullptr;   // residual / prolongation scratch
+    double *xv = nullptr;  // level solution (l >= 1)
+};
+
+struct VGroup {
+    int sub0 = 0, nsub = 0;
+    int64_t row0 = 0, row1 = 0;
+    std::vector<DLevel> lv;          // smoothing levels
+    int64_t nb = 0;                  // bottom rows (all subdomains of the group)
+    double *rb = nullptr, *xb = nullptr;
+    double *binvT = nullptr;
+    int64_t *binv_off = nullptr;     // per subdomain offset into binvT
+    int64_t *b_off = nullptr;        // nsub + 1 row offsets in rb
+    int max_nb = 0;
+    // levels [lc, L) and the bottom run in one cooperative kernel (coarse.cuh)
+    int lc = -1;                     // -1: no coarse kernel
+    CoarseArgs *cargs = nullptr;     // device copy
+    int lt = -1;                     // levels [lt, L) + bottom run in k_tiny_cycle (-1: none)
+    CoarseArgs *targs = nullptr;
+    unsigned coarse_grid = 0;
+    double *binv = nullptr;          // row-major inverses for the cooperative kernel
+    // host-side statistics
+    std::vector<int64_t> nnzA, nnzP, rows;
+};
+
+// In-process communicator for testing the multi-rank path without NCCL: the
+// ranks are contexts driven by different host threads (one device or
+// several); every collective synchronises its stream, meets the other ranks
+// at a host barrier and copies from the peers' published device buffers.
+struct dfl_fabric {
+    int nranks = 0;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    long generation = 0;
+    std::vector<dfl_ctx *> ctxs;
+    std::vector<const double *> pub;  // per-rank published buffer of the current collective
+    void barrier() {
+        std::unique_lock<std::mutex> lk(mu);
+        const long gen = generation;
+        if (++arrived == nranks) {
+            arrived = 0;
+            ++generation;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return generation != gen; });
+        }
+    }
+};
+
+struct dfl_ctx {
+    int device = 0;
+    dfl_fabric *fab = nullptr;
+    int sm_count = 148;
+    std::vector<int64_t> op_sub_tiles_h;
+    int64_t *op_sub_tiles = nullptr;   // first op-pipe tile of every subdomain
+    cudaStream_t st = nullptr;
+    std::string err;
+    std::vector<void *> allocs;
+    int64_t bytes = 0;
+    // comm
+    int nranks = 1, rank = 0;
+    NcclComm comm = nullptr;
+    // operator
+    bool have_op = false, finalized = false;
+    int64_t n = 0, n_ghost = 0;
+    int nsub = 0;
+    std::vector<int64_t> sub_off;
+    DMat Aop;
+    std::vector<int64_t> op_nnz_rows;  // host stats
+    int64_t op_nnz = 0;
+    // tiles (per subdomain, rows per tile = op rows per block)
+    Tiles tiles{};
+    SubTable subtab{};
+    int64_t ntiles = 0;
+    int *tile_sub = nullptr;
+    int64_t *sub_tiles = nullptr;       // device nsub + 1
+    std::vector<int64_t> h_sub_tiles;
+    // halo
+    std::vector<int> nbr;
+    std::vector<int64_t> recv_cnt, send_cnt;
+    int *send_idx = nullptr;
+    int64_t nsend = 0;
+    double *sendbuf = nullptr;
+    // halo overlap: rows with ghost columns run after the exchange
+    bool split = false;
+    uint8_t *bflag = nullptr;
+    int *brows = nullptr, *bstart = nullptr, *bcnt = nullptr;
+    int64_t nbtiles = 0;
+    int64_t *sub_btiles = nullptr;
+    cudaStream_t st2 = nullptr;
+    cudaEvent_t ev_packed = nullptr, ev_halo = nullptr;
+    // hierarchies
+    std::vector<dfl::Hierarchy> pending;
+    std::vector<int> pending_set;
+    std::vector<VGroup> groups;
+    int relax = DFL_RELAX_DAMPED_JACOBI;
+    // deflation
+    bool deflation = false;
+    int k = 0;
+    int64_t K = 0;
+    int first_sub = 0;
+    double *zcols = nullptr;
+    int *az_ptr = nullptr, *az_col = nullptr;
+    double *az_val = nullptr;
+    int64_t az_nnz = 0;
+    double *Einv = nullptr;
+    // inexact coarse solve (deflation.py:166-178): inner GMRES on E
+    bool inexact = false;
+    double *Edense = nullptr, *egm_scr = nullptr;
+    double coarse_tol = 1e-2;
+    double *tvec = nullptr, *t2 = nullptr;
+    double *zt_part = nullptr;
+    double *tgather = nullptr;  // nranks * maxsub * k
+    unsigned int *ticket = nullptr;
+    int max_nsub = 0;
+    std::vector<int> rank_nsub;  // subdomains per rank (runtime.rank_subdomains)
+    // work vectors (n, or n + n_ghost for operator inputs)
+    double *b = nullptr, *bp = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr,
+           *w = nullptr, *tmp = nullptr, *xin = nullptr, *yout = nullptr;
+    double *dpart = nullptr;
+    int64_t nblk = 0;
+    // BiCGStab(2) work vectors (allocated on first use)
+    double *br[3] = {nullptr, nullptr, nullptr}, *bd[3] = {nullptr, nullptr, nullptr};
+    double *bu = nullptr, *bshadow = nullptr, *zx = nullptr;
+    double *h_dots = nullptr;  // pinned
+    // (F)GMRES (allocated on first use)
+    int gm_restart = 0;
+    std::vector<double *> gmV, gmZ;
+    const double **gmVp = nullptr, **gmZp = nullptr;  // device pointer arrays
+    double *gm_h = nullptr, *gm_e = nullptr, *gm_y = nullptr, *gm_part = nullptr, *gm_loc = nullptr,
+           *gm_gath = nullptr, *h_gm = nullptr;
+    double *scal = nullptr;     // [0..7] local reduced scalars
+    double *sgather = nullptr;  // nranks * 8
+    KState *state = nullptr;
+    KState *h_state = nullptr;  // pinned
+    // graph
+    cudaGraphExec_t loop_exec = nullptr;
+    int loop_key = -1;
+    int64_t body_kernels = 0;
+    int64_t launches = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // per-launch profiling of the V-cycle (dfl_ctx_profile_vcycle)
+    bool prof_on = false;
+    std::vector<cudaEvent_t> prof_ev;
+    std::vector<std::string> prof_lab;
+    size_t prof_n = 0;
+};
+
+inline void prof_mark(dfl_ctx *ctx, const std::string &label) {
+    if (!ctx->prof_on) return;
+    if (ctx->prof_n >= ctx->prof_ev.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ctx->prof_ev.push_back(e);
+        ctx->prof_lab.emplace_back();
+    }
+    cudaEventRecord(ctx->prof_ev[ctx->prof_n], ctx->st);
+    ctx->prof_lab[ctx->prof_n] = label;
+    ctx->prof_n++;
+}
+
+#define CK(call)                                                                             \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess) {                                                             \
+            ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);                  \
+            return DFL_E_CUDA;                                                               \
+        }                                                                                    \
+    } while (0)
+#define RC(call)                       \
+    do {                               \
+        int r_ = (call);               \
+        if (r_ != DFL_OK) return r_;   \
+    } while (0)
+
+static inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+template <class T>
+static int dalloc(dfl_ctx *ctx, T **p, int64_t count) {
+    *p = nullptr;
+    if (count <= 0) count = 1;
+    void *q = nullptr;
+    CK(cudaMalloc(&q, sizeof(T) * (size_t)count));
+    ctx->allocs.push_back(q);
+    ctx->bytes += sizeof(T) * count;
+    *p = static_cast<T *>(q);
+    return DFL_OK;
+}
+
+template <class T>
+static int upload(dfl_ctx *ctx, T **p, const T *h, int64_t count) {
+    RC(dalloc(ctx, p, count));
+    if (count > 0) CK(cudaMemcpy(*p, h, sizeof(T) * (size_t)count, cudaMemcpyHostToDevice));
+    return DFL_OK;
+}
+
+// ---------------------------------------------------------------------------
+// matrix upload with format selection
+
+struct HostRows {
+    int64_t nrows, ncols;
+    const int64_t *ptr;
+    const int64_t *col;
+    const double *val;
+};
+
+
+// ---------------------------------------------------------------------------
+// kernel launch helpers
+
+inline int rows_per_block(const DMat &A) { return A.fmt == FMT_CSR ? kBlock / A.group : kBlock; }
+
+inline int64_t nblocks_for(const DMat &A) { return cdiv(A.nrows, rows_per_block(A)); }
+
+// grid of the grid-stride FMT_CODE kernels
+inline int64_t code_grid(const dfl_ctx *, const DMat &A) {
+    return std::max<int64_t>(1, std::min<int64_t>(cdiv(A.nrows, kBlock), 8 * (int64_t)g_sm_count));
+}
+
+// number of per-block / per-tile partials a row kernel on A produces
+inline int64_t parts_for(const DMat &A) {
+    if (A.fmt == FMT_CODE || A.vcode) return code_grid(nullptr, A);
+    return A.pipe.stages ? A.pipe.ntiles : nblocks_for(A);
+}
+
+inline size_t pipe_smem(const DMat &A) { return 128 + (size_t)A.pipe.stages * A.pipe.cap * 12; }
+
+template <int MODE, bool PART>
+static void pipe_attr_one() {
+    auto set = [](const void *f) {
+        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageBytesMax + 1024);
+    };
+    set((const void *)k_pipe<0, MODE, PART>);
+    set((const void *)k_pipe<1, MODE, PART>);
+    set((const void *)k_pipe<2, MODE, PART>);
+    set((const void *)k_pipe<4, MODE, PART>);
+    set((const void *)k_pipe<8, MODE, PART>);
+    set((const void *)k_pipe<16, MODE, PART>);
+    set((const void *)k_pipe<32, MODE, PART>);
+}
+
+inline void pipe_attrs() {
+    pipe_attr_one<PMODE_PLAIN, false>();
+    pipe_attr_one<PMODE_RESID, false>();
+    pipe_attr_one<PMODE_PROLONG, false>();
+    pipe_attr_one<PMODE_POST, false>();
+    pipe_attr_one<PMODE_POST, true>();
+    pipe_attr_one<PMODE_OP, true>();
+    pipe_attr_one<PMODE_OPRES, true>();
+}
+
+template <int MODE, bool PART>
+static bool launch_pipe(dfl_ctx *ctx, const DMat &A, const SpArgs &a) {
+    if (A.pipe.stages == 0) return false;
+    const size_t smem = pipe_smem(A);
+    const int per_sm = smem <= 110 * 1024 ? 2 : 1;
+    const unsigned grid = (unsigned)std::min<int64_t>(A.pipe.ntiles, (int64_t)ctx->sm_count * per_sm);
+    if (A.fmt == FMT_ELL) {
+        k_pipe<0, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a);
+    } else {
+        switch (A.group) {
+            case 1: k_pipe<1, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
+            case 2: k_pipe<2, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
+            case 4: k_pipe<4, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
+            case 8: k_pipe<8, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
+            case 16: k_pipe<16, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
+            default: k_pipe<32, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
+        }
+    }
+    ctx->launches++;
+    return true;
+}
+
+
+template <int MODE, bool DOT>
+static void launch_csr_mode(const DMat &A, const RowArgs &a, cudaStream_t st) {
+    const dim3 grid((unsigned)nblocks_for(A));
+    switch (A.group) {
+        case 1: k_csr<1, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
+        case 2: k_csr<2, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
+        case 4: k_csr<4, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
+        case 8: k_csr<8, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
+        case 16: k_csr<16, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
+        default: k_csr<32, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
+    }
+}
+
+template <int MODE, bool DOT>
+static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
+    if (A.nrows == 0) return;
+    if (A.fmt == FMT_CODE) {
+        k_code<MODE, DOT><<<(unsigned)code_grid(ctx, A), kBlock, 0, ctx->st>>>(A, a);
+        ctx->launches++;
+        return;
+    }
+    if (A.vcode) {
+        k_vell<MODE, DOT><<<(unsigned)code_grid(ctx, A), kBlock, 0, ctx->st>>>(A, a);
+        ctx->launches++;
+        return;
+    }
+    if (g_use_pipe) {
+        SpArgs s;
+        s.x = a.x;
+        s.w = a.w;
+        s.r = a.r;
+        s.xo = a.xo;
+        s.out = a.out;
+        s.part = a.dot_part;
+        s.st = a.st;
+        constexpr int PM = MODE == MODE_PLAIN ? PMODE_PLAIN
+                           : MODE == MODE_RESID ? PMODE_RESID
+                           : MODE == MODE_POST ? PMODE_POST
+                                                : PMODE_PROLONG;
+        if (launch_pipe<PM, DOT>(ctx, A, s)) return;
+    }
+    if (A.fmt == FMT_ELL) {
+        const unsigned grid = (unsigned)nblocks_for(A);
+        switch (A.ell_w) {
+            case 3: k_ell<MODE, DOT, 3><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+            case 4: k_ell<MODE, DOT, 4><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+            case 5: k_ell<MODE, DOT, 5><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+            case 6: k_ell<MODE, DOT, 6><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+            case 7: k_ell<MODE, DOT, 7><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+            case 8: k_ell<MODE, DOT, 8><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+            default: k_ell<MODE, DOT, 0><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+        }
+    } else
+        launch_csr_mode<MODE, DOT>(A, a, ctx->st);
+    ctx->launches++;
+}
+
+template <int OPMODE>
+static void launch_op(dfl_ctx *ctx, const OpArgs &a) {
+    const DMat &A = ctx->Aop;
+    if (g_use_pipe && !a.skip_rows && !ctx->split) {
+        SpArgs s;
+        s.x = a.x;
+        s.b = a.b;
+        s.out = a.y;
+        s.part = a.k > 0 ? a.zt_part : nullptr;
+        s.zcols = a.zcols;
+        s.zn = a.n;
+        s.k = a.k;
+        s.st = a.st;
+        s.need_refresh = a.need_refresh;
+        if (launch_pipe<OPMODE == 0 ? PMODE_OP : PMODE_OPRES, true>(ctx, A, s)) return;
+    }
+    const unsigned grid = (unsigned)ctx->ntiles;
+    if (grid == 0) return;
+    if (A.fmt == FMT_CODE) {
+        k_op_code<OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a);
+    } else if (A.fmt == FMT_ELL) {
+        const SubTable &S = ctx->subtab;
+        switch (A.ell_w) {
+            case 5: k_op_ell<OPMODE, 5><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, S, a); break;
+            case 6: k_op_ell<OPMODE, 6><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, S, a); break;
+            case 7: k_op_ell<OPMODE, 7><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, S, a); break;
+            default: k_op_ell<OPMODE, 0><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, S, a); break;
+        }
+    } else {
+        switch (A.group) {
+            case 1: k_op_csr<1, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
+            case 2: k_op_csr<2, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
+            case 4: k_op_csr<4, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
+            case 8: k_op_csr<8, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
+            case 16: k_op_csr<16, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
+            default: k_op_csr<32, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
+        }
+    }
+    ctx->launches++;
+}
+
+// ---------------------------------------------------------------------------
+// cross-unit entry points (return DFL_OK or a DFL_E_* code, message in ctx->err)
+
+inline bool multi(const dfl_ctx *ctx) { return ctx->comm != nullptr || ctx->fab != nullptr; }
+
+inline ProjArgs proj_args(dfl_ctx *ctx, const double *in, double *out, const KState *st) {
+    ProjArgs a{};
+    if (ctx->deflation) {
+        a.az_ptr = ctx->az_ptr;
+        a.az_col = ctx->az_col;
+        a.az_val = ctx->az_val;
+    }
+    a.t2 = ctx->t2;
+    a.K = ctx->deflation ? ctx->K : 0;
+    a.n = ctx->n;
+    a.in = in;
+    a.out = out;
+    a.st = st;
+    return a;
+}
+
+template <int MODE>
+static void launch_project(dfl_ctx *ctx, const ProjArgs &a) {
+    k_project<MODE><<<(unsigned)ctx->nblk, kBlock, sizeof(double) * std::max<int64_t>(1, a.K), ctx->st>>>(a);
+    ctx->launches++;
+}
+
+// ctx_layout.cu
+extern double kShortRowPad;
+int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &bounds,
+                  std::vector<int64_t> *bound_tiles = nullptr, bool allow_ell = true,
+                  const double *colscale = nullptr, DMat *scaled = nullptr, bool allow_sell = true,
+                  bool allow_code = true, bool allow_vcode = false);
+int build_groups(dfl_ctx *ctx);
+int build_tiles(dfl_ctx *ctx);
+// ctx_comm.cu
+int comm_allgather(dfl_ctx *ctx, const double *send, double *recv, size_t count);
+int halo(dfl_ctx *ctx, double *v, cudaStream_t xs = nullptr);
+int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op);
+int rank_scalar(dfl_ctx *ctx, const double *part, int64_t nparts, int slot, const double **gath);
+// ctx_cycle.cu
+int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *dot_part, int64_t *nparts);
+int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double *b, bool zt, const KState *st,
+                 int need_refresh);
+int project_dev(dfl_ctx *ctx, const double *v, double *out, const KState *st, int dotmode);
+int lift_dev(dfl_ctx *ctx, const dfl_solve_params *p);
+// ctx_cg.cu / ctx_krylov.cu
+int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph);
+int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out);
+int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KState &out);
+// ctx.cu
+int ready(dfl_ctx *ctx);

@@ -1,0 +1,529 @@
+// Device layouts: format selection and upload of every matrix of the solve
+// phase, subdomain grouping of the V-cycle levels and row tiles of the operator.
+#include "ctx_impl.cuh"
+
+static int build_pipe(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &soff,
+                      const std::vector<int64_t> &bounds, std::vector<int64_t> *bound_tiles);
+
+// colscale != nullptr: also upload the column-scaled values a_ij * colscale_j
+// in the same layout (shares the index arrays) into *scaled.
+// FMT_CODE encoder: every row <= 8 entries and <= 255 distinct (column - row,
+// value-bits) pairs; returns false when the matrix does not qualify
+static int try_upload_code(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) {
+    ok = false;
+    struct Key {
+        int64_t d;
+        uint64_t v;
+        bool operator==(const Key &o) const { return d == o.d && v == o.v; }
+    };
+    struct KH {
+        size_t operator()(const Key &k) const { return std::hash<int64_t>()(k.d) * 1000003u ^ std::hash<uint64_t>()(k.v); }
+    };
+    std::unordered_map<Key, int, KH> dict;
+    std::vector<int> delta;
+    std::vector<double> val;
+    std::vector<uint8_t> codes((size_t)h.nrows * 8, (uint8_t)kCodePad);
+    for (int64_t i = 0; i < h.nrows; ++i) {
+        const int64_t b = h.ptr[i], e = h.ptr[i + 1];
+        if (e - b > 8) return DFL_OK;
+        for (int64_t k = b; k < e; ++k) {
+            uint64_t bits;
+            std::memcpy(&bits, &h.val[k], 8);
+            const int64_t d = h.col[k] - i;
+            if (d < INT32_MIN || d > INT32_MAX) return DFL_OK;
+            auto it = dict.find(Key{d, bits});
+            int code;
+            if (it == dict.end()) {
+                if (dict.size() >= kCodePad) return DFL_OK;
+                code = (int)dict.size();
+                dict.emplace(Key{d, bits}, code);
+                delta.push_back((int)d);
+                val.push_back(h.val[k]);
+            } else {
+                code = it->second;
+            }
+            codes[(size_t)i * 8 + (k - b)] = (uint8_t)code;
+        }
+    }
+    m.fmt = FMT_CODE;
+    m.stored = m.nnz;
+    m.ncodes = (int)delta.size();
+    uint8_t *d_codes;
+    int *d_delta;
+    double *d_val;
+    RC(upload(ctx, &d_codes, codes.data(), (int64_t)codes.size()));
+    RC(upload(ctx, &d_delta, delta.data(), (int64_t)std::max<size_t>(1, delta.size())));
+    RC(upload(ctx, &d_val, val.data(), (int64_t)std::max<size_t>(1, val.size())));
+    m.codes = reinterpret_cast<const uint2 *>(d_codes);
+    m.ctab_delta = d_delta;
+    m.ctab_val = d_val;
+    ok = true;
+    return DFL_OK;
+}
+
+// value codes for an ELL-layout matrix with <= 255 distinct values (bitwise)
+static int attach_value_codes(dfl_ctx *ctx, DMat &m, const std::vector<double> &val) {
+    std::unordered_map<uint64_t, int> dict;
+    std::vector<double> tab;
+    std::vector<uint8_t> code(val.size());
+    for (size_t e = 0; e < val.size(); ++e) {
+        uint64_t bits;
+        std::memcpy(&bits, &val[e], 8);
+        auto it = dict.find(bits);
+        if (it == dict.end()) {
+            if (dict.size() >= 255) return DFL_OK;  // not value-codable
+            it = dict.emplace(bits, (int)tab.size()).first;
+            tab.push_back(val[e]);
+        }
+        code[e] = (uint8_t)it->second;
+    }
+    uint8_t *d_code;
+    double *d_tab;
+    RC(upload(ctx, &d_code, code.data(), (int64_t)code.size()));
+    RC(upload(ctx, &d_tab, tab.data(), (int64_t)tab.size()));
+    m.vcode = d_code;
+    m.vtab = d_tab;
+    m.nvtab = (int)tab.size();
+    return DFL_OK;
+}
+
+static constexpr int64_t kSigma = 1024;  // SELL-C-sigma sorting window
+// SELL-32-1024 for long-row matrices with enough rows to hide the per-warp
+// width imbalance (measured: L0 restriction and L1 operator, profiles/r01);
+// short-row (P) and small coarse matrices stay CSR-vector
+static constexpr int64_t kSellMinRows = 100000;
+static constexpr double kSellMinMean = 12.0;
+static constexpr double kShortRowMean = 8.0;  // DFL_SHORT_PAD=x overrides the padding limit below
+double kShortRowPad = 1.7;
+
+int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &bounds,
+                  std::vector<int64_t> *bound_tiles, bool allow_ell, const double *colscale, DMat *scaled,
+                  bool allow_sell, bool allow_code, bool allow_vcode) {
+    m = DMat{};
+    m.nrows = h.nrows;
+    m.ncols = h.ncols;
+    m.nnz = h.ptr[h.nrows] - h.ptr[0];
+    if (h.ncols >= INT32_MAX || m.nnz >= INT32_MAX) {
+        ctx->err = "matrix too large for int32 device indices";
+        return DFL_E_DIMENSION;
+    }
+    if (g_use_code && allow_code && allow_ell && h.nrows > 0) {
+        bool ok = false;
+        RC(try_upload_code(ctx, h, m, ok));
+        if (ok) {
+            if (colscale) *scaled = m;  // RESID on a coded matrix gathers w .* r instead (k_wr)
+            return DFL_OK;
+        }
+    }
+    const int64_t nsl = cdiv(h.nrows, 32);
+    auto rlen = [&](int64_t i) { return h.ptr[i + 1] - h.ptr[i]; };
+    // slot -> row: identity, or (SELL-C-sigma) rows sorted by length,
+    // descending and stable, inside windows of kSigma rows
+    std::vector<int> perm;
+    auto slice_offsets = [&](const std::vector<int> &pm, int64_t &maxlen) {
+        std::vector<int64_t> so(nsl + 1, 0);
+        maxlen = 0;
+        for (int64_t s = 0; s < nsl; ++s) {
+            int64_t wmax = 0;
+            for (int64_t j = s * 32; j < std::min(h.nrows, s * 32 + 32); ++j)
+                wmax = std::max(wmax, rlen(pm.empty() ? j : pm[j]));
+            maxlen = std::max(maxlen, wmax);
+            so[s + 1] = so[s] + 32 * wmax;
+        }
+        return so;
+    };
+    int64_t maxlen = 0;
+    std::vector<int64_t> soff = slice_offsets(perm, maxlen);
+    const double mean = h.nrows ? (double)m.nnz / (double)h.nrows : 0.0;
+    const double nnzd = (double)m.nnz + 64.0;
+    bool ell = false;
+    const double upad = mean <= kShortRowMean ? kShortRowPad : 1.03;  // short rows: padding is cheaper than CSR
+    if (allow_ell && maxlen <= 8 && (double)(nsl * 32 * maxlen) <= upad * nnzd) {
+        // uniform slice width: the kernels compute slice offsets instead of loading them
+        ell = true;
+        m.ell_w = (int)maxlen;
+        for (int64_t s = 0; s <= nsl; ++s) soff[s] = s * 32 * maxlen;
+    } else if (allow_ell && (double)soff[nsl] <= 1.03 * nnzd) {
+        ell = true;
+    } else if (allow_ell && allow_sell && maxlen <= 1024 &&
+               (g_allow_sell || (h.nrows >= kSellMinRows && mean >= kSellMinMean))) {
+        perm.resize(h.nrows);
+        for (int64_t w0 = 0; w0 < h.nrows; w0 += kSigma) {
+            const int64_t w1 = std::min(h.nrows, w0 + kSigma);
+            for (int64_t j = w0; j < w1; ++j) perm[j] = (int)j;
+            std::stable_sort(perm.begin() + w0, perm.begin() + w1, [&](int a, int b) { return rlen(a) > rlen(b); });
+        }
+        int64_t ml = 0;
+        std::vector<int64_t> ss = slice_offsets(perm, ml);
+        if ((double)ss[nsl] <= 1.25 * nnzd) {
+            ell = true;
+            soff = ss;
+            maxlen = ml;
+        } else {
+            perm.clear();
+        }
+    }
+    if (!ell && allow_ell && maxlen <= 32 && (double)soff[nsl] <= 1.2 * nnzd) ell = true;
+    // short rows (prolongation, ~4 entries): coalesced sliced ELL beats 1-lane
+    // CSR even with ~40% padding (profiles/r01)
+    if (!ell && allow_ell && mean <= kShortRowMean && maxlen <= 16 && (double)soff[nsl] <= kShortRowPad * nnzd) {
+        ell = true;
+        perm.clear();
+        soff = slice_offsets(perm, maxlen);
+    }
+    if (ell) {
+        m.fmt = FMT_ELL;
+        m.stored = soff[nsl];
+        std::vector<int> col(m.stored, 0);
+        std::vector<double> val(m.stored, 0.0);
+        std::vector<double> sval(colscale ? m.stored : 0, 0.0);
+        for (int64_t s = 0; s < nsl; ++s) {
+            const int64_t wdt = (soff[s + 1] - soff[s]) / 32;
+            for (int64_t j = s * 32; j < std::min(h.nrows, s * 32 + 32); ++j) {
+                const int lane = (int)(j - s * 32);
+                const int64_t i = perm.empty() ? j : perm[j];
+                const int64_t b = h.ptr[i], e = h.ptr[i + 1];
+                const int pad_col = e > b ? (int)h.col[e - 1] : 0;
+                for (int64_t k = 0; k < wdt; ++k) {
+                    const int64_t dst = soff[s] + k * 32 + lane;
+                    if (b + k < e) {
+                        col[dst] = (int)h.col[b + k];
+                        val[dst] = h.val[b + k];
+                        if (colscale) sval[dst] = h.val[b + k] * colscale[h.col[b + k]];
+                    } else {
+                        col[dst] = pad_col;
+                    }
+                }
+            }
+        }
+        int64_t *d_soff;
+        int *d_col;
+        double *d_val;
+        RC(upload(ctx, &d_soff, soff.data(), nsl + 1));
+        RC(upload(ctx, &d_col, col.data(), m.stored));
+        RC(upload(ctx, &d_val, val.data(), m.stored));
+        m.slice_off = d_soff;
+        m.col = d_col;
+        m.val = d_val;
+        if (!perm.empty()) {
+            int *d_perm;
+            RC(upload(ctx, &d_perm, perm.data(), h.nrows));
+            m.perm = d_perm;
+        }
+        if (g_use_vcode && allow_vcode) RC(attach_value_codes(ctx, m, val));
+        if (perm.empty()) RC(build_pipe(ctx, h, m, soff, bounds, bound_tiles));
+        if (colscale) {
+            double *d_sval;
+            RC(upload(ctx, &d_sval, sval.data(), m.stored));
+            *scaled = m;
+            scaled->val = d_sval;
+        }
+    } else {
+        m.fmt = FMT_CSR;
+        m.stored = m.nnz;
+        // lanes per row: about 6 entries per lane, batched kCsrUnroll deep
+        int g = 1;
+        const int want = (int)std::ceil(mean / (h.nrows < 50000 ? g_small_per_lane : g_csr_per_lane));
+        while (g < want && g < 32) g *= 2;
+        if (g_csr_g > 0) g = g_csr_g;
+        m.group = g;
+        // padded by 4 entries so that 16-byte aligned bulk copies may overrun the last row
+        std::vector<int> ptr(h.nrows + 1), col(m.nnz + 4, 0);
+        std::vector<double> val(m.nnz + 4, 0.0);
+        for (int64_t i = 0; i <= h.nrows; ++i) ptr[i] = (int)(h.ptr[i] - h.ptr[0]);
+        for (int64_t k = 0; k < m.nnz; ++k) col[k] = (int)h.col[h.ptr[0] + k];
+        std::memcpy(val.data(), h.val + h.ptr[0], sizeof(double) * m.nnz);
+        int *d_ptr, *d_col;
+        double *d_val;
+        RC(upload(ctx, &d_ptr, ptr.data(), h.nrows + 1));
+        RC(upload(ctx, &d_col, col.data(), m.nnz + 4));
+        RC(upload(ctx, &d_val, val.data(), m.nnz + 4));
+        m.ptr = d_ptr;
+        m.col = d_col;
+        m.val = d_val;
+        RC(build_pipe(ctx, h, m, soff, bounds, bound_tiles));
+        if (colscale) {
+            std::vector<double> sval(m.nnz + 4, 0.0);
+            for (int64_t k = 0; k < m.nnz; ++k) sval[k] = h.val[h.ptr[0] + k] * colscale[h.col[h.ptr[0] + k]];
+            double *d_sval;
+            RC(upload(ctx, &d_sval, sval.data(), m.nnz + 4));
+            *scaled = m;
+            scaled->val = d_sval;
+        }
+    }
+    return DFL_OK;
+}
+
+// Row tiles for the TMA pipeline: tiles never straddle `bounds` (subdomain
+// starts for the operator); ELL tiles are 256 rows (one per thread), CSR
+// tiles ~3K entries in passes of 256/G rows.
+
+static int build_pipe(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &soff,
+                      const std::vector<int64_t> &bounds, std::vector<int64_t> *bound_tiles) {
+    m.pipe = Pipe{};
+    if (bound_tiles) bound_tiles->assign(1, 0);
+    if (h.nrows == 0) return DFL_OK;
+    int64_t rpt;
+    if (m.fmt == FMT_ELL) {
+        rpt = kPipeThreads;
+    } else {
+        const int64_t rpp = kPipeThreads / m.group;
+        const double mean = (double)m.nnz / (double)h.nrows;
+        const int64_t passes = std::max<int64_t>(1, (int64_t)std::llround(3072.0 / std::max(1.0, mean * rpp)));
+        rpt = rpp * passes;
+    }
+    std::vector<int64_t> r0, r1, e0;
+    std::vector<int> ec;
+    int64_t cap = 0;
+    const int64_t base = h.ptr[0];
+    for (size_t bi = 0; bi + 1 < bounds.size(); ++bi) {
+        for (int64_t r = bounds[bi]; r < bounds[bi + 1]; r += rpt) {
+            const int64_t re = std::min(r + rpt, bounds[bi + 1]);
+            int64_t a, b;
+            if (m.fmt == FMT_ELL) {
+                a = soff[r >> 5];
+                b = soff[(re + 31) >> 5];
+            } else {
+                a = (h.ptr[r] - base) & ~int64_t(3);
+                b = ((h.ptr[re] - base) + 3) & ~int64_t(3);
+            }
+            r0.push_back(r);
+            r1.push_back(re);
+            e0.push_back(a);
+            ec.push_back((int)(b - a));
+            cap = std::max(cap, b - a);
+        }
+        if (bound_tiles) bound_tiles->push_back((int64_t)r0.size());
+    }
+    cap = (cap + 3) & ~int64_t(3);
+    const int64_t stage_bytes = cap * 12;
+    int stages = (int)std::min<int64_t>(4, kStageBytesMax / std::max<int64_t>(1, stage_bytes));
+    if (stages < 2) return DFL_OK;  // rows too long for staging: register kernels
+    int64_t *d0, *d1, *de;
+    int *dc;
+    RC(upload(ctx, &d0, r0.data(), (int64_t)r0.size()));
+    RC(upload(ctx, &d1, r1.data(), (int64_t)r1.size()));
+    RC(upload(ctx, &de, e0.data(), (int64_t)e0.size()));
+    RC(upload(ctx, &dc, ec.data(), (int64_t)ec.size()));
+    m.pipe.row0 = d0;
+    m.pipe.row1 = d1;
+    m.pipe.e0 = de;
+    m.pipe.ecnt = dc;
+    m.pipe.ntiles = (int64_t)r0.size();
+    m.pipe.cap = (int)cap;
+    m.pipe.stages = stages;
+    return DFL_OK;
+}
+
+
+// ---------------------------------------------------------------------------
+// upload helpers for finalize
+
+struct OwnedRows {
+    int64_t nrows = 0, ncols = 0;
+    std::vector<int64_t> ptr{0}, col;
+    std::vector<double> val;
+    HostRows view() const { return HostRows{nrows, ncols, ptr.data(), col.data(), val.data()}; }
+};
+
+// block-diagonal concatenation: part j contributes rows at row offset, columns
+// shifted by col offset
+static OwnedRows merge_blocks(const std::vector<const dfl::Csr *> &parts, const std::vector<int64_t> &coff) {
+    OwnedRows m;
+    int64_t nnz = 0;
+    for (auto *p : parts) nnz += p->nnz(), m.nrows += p->nrows;
+    m.ncols = coff.back();
+    m.ptr.reserve(m.nrows + 1);
+    m.col.reserve(nnz);
+    m.val.reserve(nnz);
+    for (size_t j = 0; j < parts.size(); ++j) {
+        const dfl::Csr &p = *parts[j];
+        for (int64_t i = 0; i < p.nrows; ++i) {
+            for (int64_t k = p.ptr[i]; k < p.ptr[i + 1]; ++k) {
+                m.col.push_back(p.col[k] + coff[j]);
+                m.val.push_back(p.val[k]);
+            }
+            m.ptr.push_back((int64_t)m.col.size());
+        }
+    }
+    return m;
+}
+
+int build_groups(dfl_ctx *ctx) {
+    ctx->groups.clear();
+    int s = 0;
+    while (s < ctx->nsub) {
+        const size_t depth = ctx->pending[s].levels.size();
+        int e = s + 1;
+        while (e < ctx->nsub && ctx->pending[e].levels.size() == depth) ++e;
+        VGroup g;
+        g.sub0 = s;
+        g.nsub = e - s;
+        g.row0 = ctx->sub_off[s];
+        g.row1 = ctx->sub_off[e];
+        const int L = (int)depth - 1;
+        for (int j = s; j < e; ++j)
+            if (ctx->pending[j].levels[0].A.nrows != ctx->sub_off[j + 1] - ctx->sub_off[j]) {
+                ctx->err = "hierarchy of subdomain " + std::to_string(j) + " does not match its row range";
+                return DFL_E_DIMENSION;
+            }
+        for (int l = 0; l < L; ++l) {
+            DLevel v;
+            std::vector<const dfl::Csr *> As, Ps, Rs;
+            std::vector<int64_t> fo{0}, co{0};
+            std::vector<double> w;
+            for (int j = s; j < e; ++j) {
+                const dfl::Level &lv = ctx->pending[j].levels[l];
+                As.push_back(&lv.A);
+                Ps.push_back(&lv.P);
+                Rs.push_back(&lv.R);
+                fo.push_back(fo.back() + lv.A.nrows);
+                co.push_back(co.back() + lv.P.ncols);
+                w.insert(w.end(), lv.w.begin(), lv.w.end());
+            }
+            OwnedRows A = merge_blocks(As, fo), P = merge_blocks(Ps, co), R = merge_blocks(Rs, fo);
+            // tiny levels stay CSR: they run inside the k_tiny_cycle cluster kernel
+            const bool tiny = g_use_tiny && fo.back() <= kTinyRows;
+            RC(upload_matrix(ctx, A.view(), v.A, {0, A.nrows}, nullptr, !tiny, w.data(), &v.Aw));
+            if (v.A.fmt == FMT_CODE) RC(dalloc(ctx, &v.wr, A.nrows));
+            RC(upload_matrix(ctx, P.view(), v.P, {0, P.nrows}, nullptr, !tiny, nullptr, nullptr, true, true, true));
+            RC(upload_matrix(ctx, R.view(), v.R, {0, R.nrows}, nullptr, !tiny, nullptr, nullptr, true, true, true));
+            RC(upload(ctx, &v.w, w.data(), (int64_t)w.size()));
+            v.n = fo.back();
+            v.nc = co.back();
+            RC(dalloc(ctx, &v.t, v.n));
+            if (l > 0) {
+                RC(dalloc(ctx, &v.rv, v.n));
+                RC(dalloc(ctx, &v.xv, v.n));
+            }
+            g.nnzA.push_back(A.ptr.back());
+            g.nnzP.push_back(P.ptr.back());
+            g.rows.push_back(v.n);
+            g.lv.push_back(v);
+        }
+        // bottom level
+        std::vector<int64_t> boff{0}, ioff{0};
+        std::vector<double> invT;
+        for (int j = s; j < e; ++j) {
+            const dfl::Level &bl = ctx->pending[j].levels.back();
+            const int64_t nb = bl.A.nrows;
+            boff.push_back(boff.back() + nb);
+            ioff.push_back(ioff.back() + nb * nb);
+            g.max_nb = std::max<int>(g.max_nb, (int)nb);
+            for (int64_t c = 0; c < nb; ++c)
+                for (int64_t i = 0; i < nb; ++i) invT.push_back(bl.bottom_inv[i * nb + c]);
+        }
+        g.nb = boff.back();
+        g.rows.push_back(g.nb);
+        RC(upload(ctx, &g.binvT, invT.data(), (int64_t)invT.size()));
+        RC(upload(ctx, &g.binv_off, ioff.data(), (int64_t)ioff.size()));
+        RC(upload(ctx, &g.b_off, boff.data(), (int64_t)boff.size()));
+        if (L > 0) {
+            RC(dalloc(ctx, &g.rb, g.nb));
+            RC(dalloc(ctx, &g.xb, g.nb));
+        }
+        {
+            // row-major inverses and the argument block of the cooperative kernel
+            std::vector<double> binv;
+            for (int j = s; j < e; ++j) {
+                const auto &bi = ctx->pending[j].levels.back().bottom_inv;
+                binv.insert(binv.end(), bi.begin(), bi.end());
+            }
+            RC(upload(ctx, &g.binv, binv.data(), (int64_t)binv.size()));
+            int lc = L;
+            for (int l = 0; l < L; ++l)
+                if (g.rows[l] <= kCoarseRows) {
+                    lc = l;
+                    break;
+                }
+            if (L - lc <= kMaxCoarse) {
+                CoarseArgs ca{};
+                ca.nlev = L - lc;
+                for (int l = lc; l < L; ++l) {
+                    const DLevel &v = g.lv[l];
+                    CLevel &cl = ca.lv[l - lc];
+                    cl.A = v.A;
+                    cl.Aw = v.Aw;
+                    cl.P = v.P;
+                    cl.R = v.R;
+                    cl.w = v.w;
+                    cl.rv = v.rv;
+                    cl.t = v.t;
+                    cl.xv = v.xv;
+                }
+                ca.binv = g.binv;
+                ca.binv_off = g.binv_off;
+                ca.b_off = g.b_off;
+                ca.nsub = g.nsub;
+                ca.nb = g.nb;
+                ca.rb = g.rb;
+                ca.xb = g.xb;
+                RC(upload(ctx, &g.cargs, &ca, 1));
+                // tiny tail: levels of <= kTinyRows rows + bottom (all CSR)
+                int lt = L;
+                for (int l = 0; l < L; ++l)
+                    if (g.rows[l] <= kTinyRows) {
+                        lt = l;
+                        break;
+                    }
+                if (g_use_tiny && g.nb <= kTinyRows && L - lt <= kMaxCoarse) {
+                    CoarseArgs ta = ca;
+                    ta.nlev = L - lt;
+                    for (int l = lt; l < L; ++l) ta.lv[l - lt] = ca.lv[l - lc];
+                    bool csr = true;
+                    for (int l = 0; l < ta.nlev; ++l)
+                        csr = csr && ta.lv[l].Aw.fmt == FMT_CSR && ta.lv[l].A.fmt == FMT_CSR &&
+                              ta.lv[l].P.fmt == FMT_CSR && ta.lv[l].R.fmt == FMT_CSR;
+                    if (csr && lt >= lc) {
+                        RC(upload(ctx, &g.targs, &ta, 1));
+                        g.lt = lt;
+                    }
+                }
+                int bps = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_coarse_cycle, 256, 0));
+                g.coarse_grid = (unsigned)(std::max(1, std::min(bps, 2)) * ctx->sm_count);
+                g.lc = bps > 0 ? lc : -1;
+            }
+        }
+        if (g.max_nb > (1 << 20)) {
+            ctx->err = "bottom level too large for shared-memory staging";
+            return DFL_E_DIMENSION;
+        }
+        ctx->groups.push_back(std::move(g));
+        s = e;
+    }
+    return DFL_OK;
+}
+
+int build_tiles(dfl_ctx *ctx) {
+    const int rpt = rows_per_block(ctx->Aop);
+    std::vector<int64_t> r0, r1, subt{0};
+    std::vector<int> ts;
+    for (int s = 0; s < ctx->nsub; ++s) {
+        for (int64_t i = ctx->sub_off[s]; i < ctx->sub_off[s + 1]; i += rpt) {
+            r0.push_back(i);
+            r1.push_back(std::min(i + rpt, ctx->sub_off[s + 1]));
+            ts.push_back(s);
+        }
+        subt.push_back((int64_t)r0.size());
+    }
+    ctx->ntiles = (int64_t)r0.size();
+    int64_t *d0, *d1;
+    RC(upload(ctx, &d0, r0.data(), ctx->ntiles));
+    RC(upload(ctx, &d1, r1.data(), ctx->ntiles));
+    RC(upload(ctx, &ctx->tile_sub, ts.data(), ctx->ntiles));
+    RC(upload(ctx, &ctx->sub_tiles, subt.data(), (int64_t)subt.size()));
+    ctx->h_sub_tiles = subt;
+    ctx->tiles = Tiles{d0, d1, ctx->ntiles};
+    ctx->subtab = SubTable{};
+    if (ctx->nsub <= kSubTab) {
+        ctx->subtab.n = ctx->nsub;
+        ctx->subtab.rows_per_tile = rpt;
+        for (int s = 0; s <= ctx->nsub; ++s) {
+            ctx->subtab.sub_off[s] = ctx->sub_off[s];
+            ctx->subtab.tile_start[s] = subt[s];
+        }
+    }
+    return DFL_OK;
+}
+

@@ -495,7 +495,7 @@ __global__ void __launch_bounds__(kBlock) k_code(DMat A, RowArgs a) {
 }
 
 // wr = w .* r  (the relaxation x = w r of amg.py:193/195, rounded as there)
-__global__ void __launch_bounds__(kBlock) k_wr(const double *__restrict__ w, const double *__restrict__ r, double *wr,
+static __global__ void __launch_bounds__(kBlock) k_wr(const double *__restrict__ w, const double *__restrict__ r, double *wr,
                                                int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (i < n) wr[i] = mul_rn(w[i], r[i]);
@@ -529,7 +529,7 @@ __global__ void __launch_bounds__(kBlock, DFL_CSR_MINB) k_csr(DMat A, RowArgs a)
 // rows, subdomains); inside a block the 8 warps split the j range (fixed
 // split, deterministic), lane = row, the inverse is stored transposed so the
 // lanes read it coalesced; warp partials are added in warp order.
-__global__ void __launch_bounds__(256) k_bottom(const double *__restrict__ invT, const int64_t *__restrict__ inv_off,
+static __global__ void __launch_bounds__(256) k_bottom(const double *__restrict__ invT, const int64_t *__restrict__ inv_off,
                                                 const int64_t *__restrict__ off, const double *__restrict__ r,
                                                 double *__restrict__ x, const KState *st) {
     __shared__ double part[8][33];
@@ -750,7 +750,7 @@ __global__ void __launch_bounds__(kBlock) k_op_bnd(DMat A, const int *__restrict
 }
 
 // Z' v partials without a product (project(b), coarse_lift(r))
-__global__ void __launch_bounds__(kBlock) k_zt_vec(Tiles T, const double *__restrict__ v,
+static __global__ void __launch_bounds__(kBlock) k_zt_vec(Tiles T, const double *__restrict__ v,
                                                    const double *__restrict__ zcols, int64_t n,
                                                    int k, double *zt_part) {
     const int64_t t = blockIdx.x;
@@ -778,7 +778,7 @@ __global__ void __launch_bounds__(kBlock) k_zt_vec(Tiles T, const double *__rest
 // first_col); one block per coarse value, fixed-order strided sums + tree.
 // The last block to finish (atomic ticket) then solves t2 = E^{-1} t with
 // the replicated inverse (Einv == nullptr: skip, multi-rank path).
-__global__ void __launch_bounds__(512) k_zt_finish(const double *__restrict__ zt_part,
+static __global__ void __launch_bounds__(512) k_zt_finish(const double *__restrict__ zt_part,
                                                    const int64_t *__restrict__ sub_tiles, int nsub, int k,
                                                    double *t_out, int64_t first_col, const double *Einv,
                                                    int64_t K, double *t2, const KState *st, int need_refresh,
@@ -820,7 +820,7 @@ __global__ void __launch_bounds__(512) k_zt_finish(const double *__restrict__ zt
 }
 
 // t2 = E^{-1} t (multi-rank path, after the allgather of t)
-__global__ void k_esolve(const double *Einv, int64_t K, const double *t, double *t2, const KState *st,
+static __global__ void k_esolve(const double *Einv, int64_t K, const double *t, double *t2, const KState *st,
                          int need_refresh) {
     if (skip(st)) return;
     if (need_refresh && !st->refresh_now) return;
@@ -886,7 +886,7 @@ __global__ void __launch_bounds__(kBlock) k_project(ProjArgs a) {
 
 // x = y + Z t2 (coarse_lift, deflation.py:235-237 & :285): Z row i has the
 // entries [1, zcols(i, 1..k-1)] at columns s*k .. s*k+k-1, summed in order.
-__global__ void __launch_bounds__(kBlock) k_lift(Tiles T, const int *tile_sub, const double *__restrict__ y,
+static __global__ void __launch_bounds__(kBlock) k_lift(Tiles T, const int *tile_sub, const double *__restrict__ y,
                                                  const double *__restrict__ zcols, int64_t n, int k,
                                                  const double *__restrict__ t2, int64_t first_col,
                                                  double *out, int add_y) {
@@ -902,7 +902,7 @@ __global__ void __launch_bounds__(kBlock) k_lift(Tiles T, const int *tile_sub, c
 // ---------------------------------------------------------------------------
 // vector kernels and reductions
 
-__global__ void __launch_bounds__(kBlock) k_dot(const double *__restrict__ a, const double *__restrict__ b,
+static __global__ void __launch_bounds__(kBlock) k_dot(const double *__restrict__ a, const double *__restrict__ b,
                                                 int64_t n, double *part, const KState *st) {
     if (skip(st)) return;
     double acc = 0.0;
@@ -948,14 +948,14 @@ __device__ __forceinline__ double reduce_parts_strided(const double *part, int64
     return total;
 }
 
-__global__ void k_reduce(const double *part, int64_t nparts, double *out) {
+static __global__ void k_reduce(const double *part, int64_t nparts, double *out) {
     const double s = reduce_parts(part, nparts);
     if (threadIdx.x == 0) *out = s;
 }
 
 // CG update (krylov.py:127-131): x += alpha p;  r -= alpha q  (+ r.r partial)
 // On refresh iterations only x is updated here (r comes from the refresh path).
-__global__ void __launch_bounds__(kBlock) k_cg_update(double *x, double *r, const double *__restrict__ p,
+static __global__ void __launch_bounds__(kBlock) k_cg_update(double *x, double *r, const double *__restrict__ p,
                                                       const double *__restrict__ q, int64_t n, double *part,
                                                       const KState *st) {
     if (skip(st)) return;
@@ -981,7 +981,7 @@ __global__ void __launch_bounds__(kBlock) k_cg_update(double *x, double *r, cons
 }
 
 // p = z + beta p (krylov.py:142)
-__global__ void __launch_bounds__(kBlock) k_cg_p(double *p, const double *__restrict__ z, int64_t n,
+static __global__ void __launch_bounds__(kBlock) k_cg_p(double *p, const double *__restrict__ z, int64_t n,
                                                  const KState *st) {
     if (skip(st)) return;
     const double beta = st->beta;
@@ -989,24 +989,24 @@ __global__ void __launch_bounds__(kBlock) k_cg_p(double *p, const double *__rest
     if (i < n) p[i] = add_rn(z[i], mul_rn(beta, p[i]));
 }
 
-__global__ void k_copy(double *dst, const double *src, int64_t n) {
+static __global__ void k_copy(double *dst, const double *src, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (i < n) dst[i] = src[i];
 }
 
-__global__ void k_fill(double *dst, double v, int64_t n) {
+static __global__ void k_fill(double *dst, double v, int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (i < n) dst[i] = v;
 }
 
 // halo: pack own values to send, in neighbour order
-__global__ void k_gather(const double *__restrict__ src, const int *__restrict__ idx, int64_t m, double *dst) {
+static __global__ void k_gather(const double *__restrict__ src, const int *__restrict__ idx, int64_t m, double *dst) {
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (i < m) dst[i] = src[idx[i]];
 }
 
 // sum rank-gathered scalars in rank order: out[v] = sum_q g[q*stride + v]
-__global__ void k_rank_sum(const double *g, int nranks, int stride, int nv, double *out) {
+static __global__ void k_rank_sum(const double *g, int nranks, int stride, int nv, double *out) {
     const int v = threadIdx.x;
     if (v >= nv) return;
     double acc = 0.0;
@@ -1024,7 +1024,7 @@ namespace dfl {
 
 // up to four dot products sharing one pass: part[blk*4 + q] = sum a_q . b_q
 constexpr int kDotStride = 4;
-__global__ void __launch_bounds__(kBlock) k_multidot(const double *__restrict__ a0, const double *__restrict__ b0,
+static __global__ void __launch_bounds__(kBlock) k_multidot(const double *__restrict__ a0, const double *__restrict__ b0,
                                                      const double *__restrict__ a1, const double *__restrict__ b1,
                                                      const double *__restrict__ a2, const double *__restrict__ b2,
                                                      const double *__restrict__ a3, const double *__restrict__ b3,
@@ -1043,7 +1043,7 @@ __global__ void __launch_bounds__(kBlock) k_multidot(const double *__restrict__ 
 }
 
 // reduce nq interleaved partial streams (stride kDotStride) -> out[0..nq)
-__global__ void k_reduceq(const double *part, int64_t nparts, int nq, double *out) {
+static __global__ void k_reduceq(const double *part, int64_t nparts, int nq, double *out) {
     __shared__ double sm[32 * 4];
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t j = threadIdx.x; j < nparts; j += blockDim.x)
@@ -1054,7 +1054,7 @@ __global__ void k_reduceq(const double *part, int64_t nparts, int nq, double *ou
 }
 
 // d_i = r_i - beta d_i for i < cnt  (krylov.py:189-190)
-__global__ void __launch_bounds__(kBlock) k_bicg_d(const double *__restrict__ r0, double *d0,
+static __global__ void __launch_bounds__(kBlock) k_bicg_d(const double *__restrict__ r0, double *d0,
                                                    const double *__restrict__ r1, double *d1, int cnt, double beta,
                                                    int64_t n) {
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
@@ -1065,7 +1065,7 @@ __global__ void __launch_bounds__(kBlock) k_bicg_d(const double *__restrict__ r0
 
 // r_i -= alpha d_{i+1} for i < cnt; u += alpha d_0; partial r_0.r_0
 // (krylov.py:199-203)
-__global__ void __launch_bounds__(kBlock) k_bicg_r(double *r0, const double *__restrict__ d1, double *r1,
+static __global__ void __launch_bounds__(kBlock) k_bicg_r(double *r0, const double *__restrict__ d1, double *r1,
                                                    const double *__restrict__ d2, int cnt, double *u,
                                                    const double *__restrict__ d0, double alpha, int64_t n,
                                                    double *part) {
@@ -1085,7 +1085,7 @@ __global__ void __launch_bounds__(kBlock) k_bicg_r(double *r0, const double *__r
 }
 
 // r2 -= tau12 r1; partials (r2.r2, r0.r2)   (krylov.py:218-225)
-__global__ void __launch_bounds__(kBlock) k_bicg_mr2(double *r2, const double *__restrict__ r1,
+static __global__ void __launch_bounds__(kBlock) k_bicg_mr2(double *r2, const double *__restrict__ r1,
                                                      const double *__restrict__ r0, double tau12, int64_t n,
                                                      double *part) {
     double acc[3] = {0.0, 0.0, 0.0};
@@ -1104,7 +1104,7 @@ __global__ void __launch_bounds__(kBlock) k_bicg_mr2(double *r2, const double *_
 // the closing updates of one BiCGStab(2) group (krylov.py:247-253):
 //   u += g1 r0; r0 -= gp2 r2; d0 -= g2 d2; d0 -= g1 d1; u += gpp1 r1; r0 -= gp1 r1
 // + partial r0.r0 (unless the recurrence is refreshed afterwards)
-__global__ void __launch_bounds__(kBlock) k_bicg_final(double *u, double *r0, double *d0,
+static __global__ void __launch_bounds__(kBlock) k_bicg_final(double *u, double *r0, double *d0,
                                                        const double *__restrict__ r1, const double *__restrict__ r2,
                                                        const double *__restrict__ d1, const double *__restrict__ d2,
                                                        double g1, double gp2, double g2, double gpp1, double gp1,
@@ -1142,7 +1142,7 @@ namespace dfl {
 constexpr int kVecGroup = 8;  // basis vectors per block of k_vdots
 
 // part[bx * ld + i] = sum over the block's rows of V_i . w, i in [8*by, 8*by+8)
-__global__ void __launch_bounds__(kBlock) k_vdots(const double *const *__restrict__ V, int nvec,
+static __global__ void __launch_bounds__(kBlock) k_vdots(const double *const *__restrict__ V, int nvec,
                                                   const double *__restrict__ w, int64_t n, double *part, int ld) {
     const int i0 = blockIdx.y * kVecGroup;
     double acc[kVecGroup];
@@ -1163,14 +1163,14 @@ __global__ void __launch_bounds__(kBlock) k_vdots(const double *const *__restric
 }
 
 // out[i] = sum_bx part[bx * ld + i]   (one block per i)
-__global__ void k_vreduce(const double *part, int64_t nbx, int ld, double *out) {
+static __global__ void k_vreduce(const double *part, int64_t nbx, int ld, double *out) {
     const double s = reduce_parts_strided(part + blockIdx.x, nbx, ld);
     if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
 // w -= h_0 V_0; w -= h_1 V_1; ... (one rounding per step, as the MGS updates);
 // optional partial of w.w after the update
-__global__ void __launch_bounds__(kBlock) k_vsub(double *w, const double *const *__restrict__ V, const double *h,
+static __global__ void __launch_bounds__(kBlock) k_vsub(double *w, const double *const *__restrict__ V, const double *h,
                                                  int nvec, int64_t n, double *part) {
     double dot = 0.0;
     for (int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x; e < n; e += (int64_t)gridDim.x * kBlock) {
@@ -1189,7 +1189,7 @@ __global__ void __launch_bounds__(kBlock) k_vsub(double *w, const double *const 
 
 // out = (x +) (v_0 y_0 + y_1 v_1 + ...)  in the reference's order
 // (krylov.py:355-363, then x = x + update :407)
-__global__ void __launch_bounds__(kBlock) k_vcombine(double *out, const double *x, const double *const *__restrict__ V,
+static __global__ void __launch_bounds__(kBlock) k_vcombine(double *out, const double *x, const double *const *__restrict__ V,
                                                      const double *y, int nvec, int64_t n) {
     for (int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x; e < n; e += (int64_t)gridDim.x * kBlock) {
         double u = mul_rn(V[0][e], y[0]);
@@ -1199,13 +1199,13 @@ __global__ void __launch_bounds__(kBlock) k_vcombine(double *out, const double *
 }
 
 // x = x + u
-__global__ void __launch_bounds__(kBlock) k_addv(double *x, const double *__restrict__ u, int64_t n) {
+static __global__ void __launch_bounds__(kBlock) k_addv(double *x, const double *__restrict__ u, int64_t n) {
     const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (e < n) x[e] = add_rn(x[e], u[e]);
 }
 
 // out = in / s   (V_{j+1} = w / h_{j+1,j}, V_0 = r / ||r||)
-__global__ void __launch_bounds__(kBlock) k_vdiv(double *out, const double *in, double s, int64_t n) {
+static __global__ void __launch_bounds__(kBlock) k_vdiv(double *out, const double *in, double s, int64_t n) {
     const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (e < n) out[e] = __ddiv_rn(in[e], s);
 }
@@ -1232,7 +1232,7 @@ __device__ __forceinline__ double blk_dot(const double *a, const double *b, int 
     return r;
 }
 
-__global__ void __launch_bounds__(256) k_egmres(const double *__restrict__ E, int K, const double *t, double *y,
+static __global__ void __launch_bounds__(256) k_egmres(const double *__restrict__ E, int K, const double *t, double *y,
                                                 double tol, double *scr, const KState *st, int need_refresh) {
     if (skip(st)) return;
     if (need_refresh && !st->refresh_now) return;
