@@ -257,6 +257,67 @@ DFL_API int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms_per_launch
  * returns the number of launches (or a negative status) */
 DFL_API int dfl_ctx_profile_vcycle(dfl_ctx *ctx, int reps, int cap, double *ms, char *labels);
 
+/* ---- pressure-Schur block solver (schur.py, paper §4.2) -------------------------------
+ * Saddle-point systems split by a pressure mask into [K G; D S] (schur.py:84-120,
+ * split on the host).  Outer FGMRES on the monolithic matrix, right
+ * preconditioned by the pressure-correction sweep (schur.py:235-251):
+ * GMRES on K (SPAI-0), FGMRES on the matrix-free S - D diag(K)^-1 G with the
+ * deflated block AMG of S as preconditioner, GMRES on K again. */
+typedef struct dfl_block dfl_block;
+
+typedef struct {
+    int64_t n;                     /* unknowns of the monolithic system */
+    int64_t n_u;                   /* velocity unknowns (mask false); n_p = n - n_u */
+    const dfl_csr *A;              /* monolithic matrix (outer operator) */
+    const dfl_csr *K, *G, *D, *S;  /* blocks, fields in their original relative order */
+    const int32_t *u_idx;          /* n_u positions of the velocity unknowns, ascending */
+    const int32_t *p_idx;          /* n_p positions of the pressure unknowns, ascending */
+    const double *wK;              /* SPAI-0 weights of K (amg.py:160-166) */
+    const double *invKdiag;        /* 1 / diag(K) */
+} dfl_block_desc;
+
+typedef struct {
+    double tol;        /* solver.tol: outer target tol ||b|| (schur.py:337-345) */
+    int32_t maxiter;   /* solver.maxiter */
+    int32_t restart;   /* solver.M */
+    int32_t usolver;   /* precond.usolver.solver.type: DFL_SOLVER_GMRES or _FGMRES */
+    int32_t umaxiter;
+    double utol;
+    int32_t psolver;   /* precond.psolver.isolver.type: DFL_SOLVER_GMRES or _FGMRES */
+    int32_t pmaxiter;
+    double ptol;
+} dfl_block_params;
+
+typedef struct {
+    int32_t iterations;           /* outer FGMRES steps */
+    int32_t converged;
+    double relative_residual;     /* ||b - A x|| / ||b|| */
+    double solve_seconds;         /* device time of the outer solve */
+    int64_t velocity_iterations;  /* cumulative inner counts (schur.py:188-190) */
+    int64_t pressure_iterations;
+    int64_t kernel_launches;
+} dfl_block_report;
+
+/* pctx: finalized single-rank context holding the deflated AMG solver of S
+ * (schur.py:210-217), shared with the block (same stream); NULL when n_p == 0
+ * or when only the operators are needed -- the block then creates its own
+ * context on `device`.  The block must be freed before pctx is destroyed. */
+DFL_API int dfl_block_create(dfl_ctx *pctx, int device, const dfl_block_desc *desc, dfl_block **out);
+DFL_API void dfl_block_free(dfl_block *b);
+DFL_API const char *dfl_block_last_error(const dfl_block *b);
+DFL_API int64_t dfl_block_device_bytes(const dfl_block *b);
+/* schur.py:254-360 SchurSolver.solve */
+DFL_API int dfl_block_solve(dfl_block *b, const dfl_block_params *p, const double *rhs, double *x, int ptr_kind,
+                            dfl_block_report *rep);
+/* schur.py:235-251 one sweep (u, p) = M(b_u, b_p); cumulative inner counts of this call */
+DFL_API int dfl_block_precond(dfl_block *b, const dfl_block_params *p, const double *b_u, const double *b_p,
+                              double *u, double *pp, int ptr_kind, int64_t *velocity_iterations,
+                              int64_t *pressure_iterations);
+/* schur.py:145-152 out = S p - D diag(K)^-1 G p */
+DFL_API int dfl_block_schur_apply(dfl_block *b, const double *p, double *out, int ptr_kind);
+/* y = A x on the monolithic matrix */
+DFL_API int dfl_block_apply(dfl_block *b, const double *x, double *y, int ptr_kind);
+
 #ifdef __cplusplus
 }
 #endif

@@ -41,6 +41,22 @@ class SolveParams(ctypes.Structure):
                 ("tol", c_dbl), ("restart", c_i32), ("reserved", c_i32)]
 
 
+class BlockDesc(ctypes.Structure):
+    _fields_ = [("n", c_i64), ("n_u", c_i64), ("A", c_vp), ("K", c_vp), ("G", c_vp), ("D", c_vp), ("S", c_vp),
+                ("u_idx", c_vp), ("p_idx", c_vp), ("wK", c_vp), ("invKdiag", c_vp)]
+
+
+class BlockParams(ctypes.Structure):
+    _fields_ = [("tol", c_dbl), ("maxiter", c_i32), ("restart", c_i32), ("usolver", c_i32), ("umaxiter", c_i32),
+                ("utol", c_dbl), ("psolver", c_i32), ("pmaxiter", c_i32), ("ptol", c_dbl)]
+
+
+class BlockReport(ctypes.Structure):
+    _fields_ = [("iterations", c_i32), ("converged", c_i32), ("relative_residual", c_dbl),
+                ("solve_seconds", c_dbl), ("velocity_iterations", c_i64), ("pressure_iterations", c_i64),
+                ("kernel_launches", c_i64)]
+
+
 class Report(ctypes.Structure):
     _fields_ = [("iterations", c_i32), ("converged", c_i32), ("breakdown", c_i32), ("device_loop", c_i32),
                 ("bnorm", c_dbl), ("resnorm", c_dbl), ("relative_residual", c_dbl),
@@ -105,6 +121,14 @@ def lib():
         "dfl_spmv_csr": ([P(Csr), c_vp, c_vp, c_i32], c_i32),
         "dfl_ctx_time": ([c_vp, c_i32, c_i32, P(c_dbl), P(c_dbl)], c_i32),
         "dfl_ctx_profile_vcycle": ([c_vp, c_i32, c_i32, c_vp, c_vp], c_i32),
+        "dfl_block_create": ([c_vp, c_i32, P(BlockDesc), P(c_vp)], c_i32),
+        "dfl_block_free": ([c_vp], None),
+        "dfl_block_last_error": ([c_vp], ctypes.c_char_p),
+        "dfl_block_device_bytes": ([c_vp], c_i64),
+        "dfl_block_solve": ([c_vp, P(BlockParams), c_vp, c_vp, c_i32, P(BlockReport)], c_i32),
+        "dfl_block_precond": ([c_vp, P(BlockParams), c_vp, c_vp, c_vp, c_vp, c_i32, P(c_i64), P(c_i64)], c_i32),
+        "dfl_block_schur_apply": ([c_vp, c_vp, c_vp, c_i32], c_i32),
+        "dfl_block_apply": ([c_vp, c_vp, c_vp, c_i32], c_i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -368,3 +392,69 @@ def spmv_device(A: CsrArrays, x: np.ndarray, device: int = 0) -> np.ndarray:
 
 def breakdown_string(code: int) -> str:
     return (lib().dfl_breakdown_string(code) or b"").decode()
+
+
+class DeviceBlock:
+    """A saddle-point block system on the device (dfl_block).  ``pressure`` is
+    the DeviceContext of the deflated pressure solver (shares its stream) or
+    None (operators only, or no pressure unknowns)."""
+
+    def __init__(self, n, n_u, A: CsrArrays, K, G, D, S, u_idx, p_idx, wK, invKdiag, pressure=None,
+                 device: int = 0):
+        self._keep = [A, K, G, D, S]
+        self._u = np.ascontiguousarray(u_idx, dtype=np.int32)
+        self._p = np.ascontiguousarray(p_idx, dtype=np.int32)
+        self._w = np.ascontiguousarray(wK, dtype=np.float64)
+        self._k = np.ascontiguousarray(invKdiag, dtype=np.float64)
+        ref = lambda m: ctypes.cast(ctypes.pointer(m.s), c_vp) if m is not None else None  # noqa: E731
+        d = BlockDesc(int(n), int(n_u), ref(A), ref(K), ref(G), ref(D), ref(S), _ptr(self._u), _ptr(self._p),
+                      _ptr(self._w), _ptr(self._k))
+        self.pressure = pressure  # keep the context alive for the block's lifetime
+        h = c_vp()
+        check(lib().dfl_block_create(pressure.h if pressure is not None else None, int(device), ctypes.byref(d),
+                                     ctypes.byref(h)))
+        self.h = h
+        self.n, self.n_u, self.n_p = int(n), int(n_u), int(n) - int(n_u)
+
+    def close(self):
+        if getattr(self, "h", None) and _lib is not None:
+            _lib.dfl_block_free(self.h)
+            self.h = None
+
+    __del__ = close
+
+    def _c(self, rc):
+        if rc != 0:
+            raise_for_status(rc, (lib().dfl_block_last_error(self.h) or b"").decode())
+
+    @property
+    def device_bytes(self) -> int:
+        return lib().dfl_block_device_bytes(self.h)
+
+    def solve(self, params: BlockParams, b, x, ptr_kind: int = PTR_HOST) -> BlockReport:
+        rep = BlockReport()
+        bp = _ptr(b) if ptr_kind == PTR_HOST else c_vp(b)
+        xp = _ptr(x) if ptr_kind == PTR_HOST else c_vp(x)
+        self._c(lib().dfl_block_solve(self.h, ctypes.byref(params), bp, xp, ptr_kind, ctypes.byref(rep)))
+        return rep
+
+    def precond(self, params: BlockParams, b_u, b_p):
+        b_u = np.ascontiguousarray(b_u, dtype=np.float64)
+        b_p = np.ascontiguousarray(b_p, dtype=np.float64)
+        u, p = np.empty(self.n_u), np.empty(self.n_p)
+        vi, pi = c_i64(), c_i64()
+        self._c(lib().dfl_block_precond(self.h, ctypes.byref(params), _ptr(b_u), _ptr(b_p), _ptr(u), _ptr(p),
+                                        PTR_HOST, ctypes.byref(vi), ctypes.byref(pi)))
+        return u, p, vi.value, pi.value
+
+    def schur_apply(self, p):
+        p = np.ascontiguousarray(p, dtype=np.float64)
+        out = np.empty(self.n_p)
+        self._c(lib().dfl_block_schur_apply(self.h, _ptr(p), _ptr(out), PTR_HOST))
+        return out
+
+    def apply(self, x):
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        out = np.empty(self.n)
+        self._c(lib().dfl_block_apply(self.h, _ptr(x), _ptr(out), PTR_HOST))
+        return out

@@ -31,7 +31,12 @@ __all__ = [
     "convdiff3d",
     "make_problem",
     "local_rows",
+    "SaddlePointProblem",
+    "saddle_point",
+    "STABILIZATION_EPS",
 ]
+
+STABILIZATION_EPS = 1e-2  # pressure-pressure block eps * h^2 (reference problems.py:28)
 
 KINDS = ("poisson", "jump", "convdiff")
 
@@ -224,3 +229,84 @@ def convdiff3d(n, boxes=(1, 1, 1), c=(0.3, 0.2, 0.1)) -> Problem:
     """Nonsymmetric convection-diffusion: 6 on the diagonal, forward
     neighbour -1 + c_a, backward -1 - c_a (BASELINE.md §4, config #5)."""
     return make_problem(n, boxes, "convdiff", c=c)
+
+
+@dataclass(frozen=True)
+class SaddlePointProblem:
+    """Stokes-like system, unknowns interleaved per node as (u_x, u_y, u_z, p);
+    ``mask`` is True on pressure unknowns, ``rhs`` = A ``solution``
+    (reference problems.py:174-187)."""
+
+    ordering: BoxOrdering
+    matrix: SparseMatrix
+    rhs: np.ndarray
+    mask: np.ndarray
+    solution: np.ndarray
+    node_coords: np.ndarray
+    node_partition: Partition
+    unknown_partition: Partition
+
+
+def csr_matvec(A: SparseMatrix, x: np.ndarray) -> np.ndarray:
+    """A x with every row summed left to right in column order (the order of
+    the reference's CSR kernel), so generated right-hand sides match it bit
+    for bit."""
+    nnz_row = np.diff(A.row_ptr)
+    nr = A.nrows
+    out = np.zeros(nr)
+    if nr == 0 or A.nnz == 0:
+        return out
+    start = A.row_ptr[:-1]
+    for k in range(int(nnz_row.max())):
+        live = np.flatnonzero(nnz_row > k)
+        e = start[live] + k
+        out[live] = out[live] + A.values[e] * x[A.col_idx[e]]
+    return out
+
+
+def saddle_point(n, boxes=(1, 1, 1)) -> SaddlePointProblem:
+    """Four-field block system (reference problems.py:190-254): per velocity
+    component the 7-point Laplacian with h^2 added to the diagonal; centred
+    pressure gradient +-h/2 (one-sided terms dropped at the boundary) and its
+    exact transpose as divergence; eps h^2 on the pressure diagonal."""
+    ordering = BoxOrdering(n, boxes)
+    nx, ny, nz = ordering.shape
+    N = ordering.n
+    h = 1.0 / (nx + 1)
+    k = np.arange(N, dtype=np.int64)
+    ix, iy, iz = k % nx, (k // nx) % ny, k // (nx * ny)  # natural (x-fastest) node k
+    pn = ordering.index_of(ix, iy, iz)                    # its box-ordered index
+    rows, cols, vals = [], [], []
+    coord, extent, step = (ix, iy, iz), (nx, ny, nz), (1, nx, nx * ny)
+    for c in range(3):
+        rows.append(4 * pn + c)
+        cols.append(4 * pn + c)
+        vals.append(np.full(N, 6.0 + h * h))
+        for a in range(3):  # Laplacian couplings, both directions
+            i = k[coord[a] < extent[a] - 1]
+            j = i + step[a]
+            rows += [4 * pn[i] + c, 4 * pn[j] + c]
+            cols += [4 * pn[j] + c, 4 * pn[i] + c]
+            vals += [np.full(i.size, -1.0), np.full(i.size, -1.0)]
+    for c in range(3):  # gradient (velocity row, pressure column) and divergence
+        for sign, sel in ((1.0, coord[c] < extent[c] - 1), (-1.0, coord[c] > 0)):
+            i = k[sel]
+            j = i + int(sign) * step[c]
+            g = np.full(i.size, sign * h / 2.0)
+            rows += [4 * pn[i] + c, 4 * pn[j] + 3]
+            cols += [4 * pn[j] + 3, 4 * pn[i] + c]
+            vals += [g, g]
+    rows.append(4 * pn + 3)
+    cols.append(4 * pn + 3)
+    vals.append(np.full(N, STABILIZATION_EPS * h * h))
+    nuk = 4 * N
+    A = SparseMatrix.from_coo(nuk, nuk, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals))
+    mask = np.tile(np.array([False, False, False, True]), N)
+    solution = np.sin(0.37 * (np.arange(nuk) + 1.0)) + 1.5
+    coords = np.empty((N, 3))
+    hx, hy, hz = ordering.spacing()
+    coords[pn, 0], coords[pn, 1], coords[pn, 2] = (ix + 1) * hx, (iy + 1) * hy, (iz + 1) * hz
+    node_part = ordering.partition()
+    unknown_part = Partition(nuk, tuple((4 * b, 4 * e) for (b, e) in node_part.ranges))
+    return SaddlePointProblem(ordering, A, csr_matvec(A, solution), mask, solution, coords, node_part,
+                              unknown_part)
