@@ -249,7 +249,9 @@ DFL_API int dfl_spmv_csr(const dfl_csr *A, const double *x, double *y, int devic
  *         2 = V-cycle (bytes the stored layouts actually need: ELL padding,
  *             1-byte codes of FMT_CODE matrices, the w.*r pass),
  *         3 = V-cycle captured once and replayed as a CUDA graph, as inside
- *             the solve (bytes as 1) */
+ *             the solve (bytes as 1),
+ *         4 = operator SpMV with the fused Z'y tile partials (as in CG),
+ *         5 = projection q = w - AZ t2 with the fused p.q partials */
 DFL_API int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms_per_launch, double *bytes_per_launch);
 
 /* per-launch device times of one V-cycle, mean over reps; labels is a

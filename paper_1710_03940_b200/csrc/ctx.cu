@@ -16,6 +16,9 @@ bool g_use_coarse = false;  // cooperative coarse-cycle kernel (DFL_COARSE=1; me
 // (measured on 150^3, see profiles/r01/README.md: CSR-vector with ~12 entries
 // per lane beats SELL-32-1024 for the coarse operators and R / P)
 bool g_allow_sell = false;    // DFL_SELL=1: SELL-C-sigma for every irregular matrix
+bool g_wr_split = false;      // DFL_WR_SPLIT=1: coded residual reads w .* r from a k_wr pass
+bool g_no_fin = true;         // DFL_FIN=1: CG scalars finished in the producing kernels (measured slower)
+bool g_pdl = true;            // DFL_NO_PDL=1: plain launches instead of programmatic dependent launch
 int g_csr_g = 0;              // DFL_CSR_G=n forces the CSR lanes per row
 double g_csr_per_lane = 12.0; // DFL_CSR_PER_LANE: target entries per lane
 int g_sm_count = 148;
@@ -46,12 +49,12 @@ int ready(dfl_ctx *ctx) {
 
 static int rank_dot(dfl_ctx *ctx, const double *a, const double *b, double *out) {
     const unsigned nb = (unsigned)std::min<int64_t>(std::max<int64_t>(1, ctx->nblk), 4 * 148);
-    k_dot<<<nb, kBlock, 0, ctx->st>>>(a, b, ctx->n, ctx->dpart, nullptr);
-    k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->dpart, nb, ctx->scal);
+    launch_k(ctx->st, k_dot, nb, kBlock, 0, a, b, ctx->n, ctx->dpart, nullptr);
+    launch_k(ctx->st, k_reduce, 1, 1024, 0, ctx->dpart, nb, ctx->scal);
     ctx->launches += 2;
     if (multi(ctx)) {
         RC(comm_allgather(ctx, ctx->scal, ctx->sgather, 8));
-        k_rank_sum<<<1, 32, 0, ctx->st>>>(ctx->sgather, ctx->nranks, 8, 1, ctx->scal + 1);
+        launch_k(ctx->st, k_rank_sum, 1, 32, 0, ctx->sgather, ctx->nranks, 8, 1, ctx->scal + 1);
         ctx->launches++;
         CK(cudaMemcpyAsync(out, ctx->scal + 1, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
     } else {
@@ -110,6 +113,12 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
         g_use_coarse = nc && nc[0] == '1';
         const char *ns = getenv("DFL_SELL");
         g_allow_sell = ns && ns[0] == '1';
+        const char *ws = getenv("DFL_WR_SPLIT");
+        g_wr_split = ws && ws[0] == '1';
+        const char *nf = getenv("DFL_FIN");
+        g_no_fin = !(nf && nf[0] == '1');
+        const char *np2 = getenv("DFL_NO_PDL");
+        g_pdl = !(np2 && np2[0] == '1');
         const char *cg = getenv("DFL_CSR_G");
         g_csr_g = cg ? atoi(cg) : 0;
         const char *cl = getenv("DFL_CSR_PER_LANE");
@@ -137,6 +146,7 @@ void dfl_ctx_destroy(dfl_ctx *ctx) {
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
     if (ctx->st2) cudaStreamDestroy(ctx->st2);
+    if (ctx->st_if) cudaStreamDestroy(ctx->st_if);
     if (ctx->ev_packed) cudaEventDestroy(ctx->ev_packed);
     if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
     if (ctx->st) cudaStreamDestroy(ctx->st);
@@ -289,13 +299,36 @@ int dfl_ctx_set_deflation(dfl_ctx *ctx, int32_t k, const double *zcols, const df
     for (int c = 1; c < k; ++c)
         for (int64_t i = 0; i < ctx->n; ++i) zc[(size_t)(c - 1) * ctx->n + i] = zcols[i * (k - 1) + (c - 1)];
     RC(upload(ctx, &ctx->zcols, zc.data(), (int64_t)zc.size()));
-    std::vector<int> ptr(ctx->n + 1), col(AZ->row_ptr[ctx->n]);
-    for (int64_t i = 0; i <= ctx->n; ++i) ptr[i] = (int)AZ->row_ptr[i];
-    for (size_t j = 0; j < col.size(); ++j) col[j] = (int)AZ->col_idx[j];
-    ctx->az_nnz = (int64_t)col.size();
-    RC(upload(ctx, &ctx->az_ptr, ptr.data(), (int64_t)ptr.size()));
-    RC(upload(ctx, &ctx->az_col, col.data(), ctx->az_nnz));
-    RC(upload(ctx, &ctx->az_val, AZ->values, ctx->az_nnz));
+    // AZ: own-subdomain block dense (k x n), the other entries as an extras CSR
+    // (kernels.cuh, ProjArgs); column order inside a row is preserved
+    const int64_t n = ctx->n;
+    std::vector<double> azd((size_t)k * n, 0.0);
+    std::vector<int> xptr(n + 1, 0), xcol;
+    std::vector<double> xval;
+    for (int s = 0; s < ctx->nsub; ++s) {
+        const int64_t own0 = (int64_t)(first_sub + s) * k;
+        for (int64_t i = ctx->sub_off[s]; i < ctx->sub_off[s + 1]; ++i) {
+            for (int64_t e = AZ->row_ptr[i]; e < AZ->row_ptr[i + 1]; ++e) {
+                const int64_t c = AZ->col_idx[e];
+                if (c >= own0 && c < own0 + k) {
+                    azd[(size_t)(c - own0) * n + i] = AZ->values[e];
+                } else {
+                    xcol.push_back((int)c);
+                    xval.push_back(AZ->values[e]);
+                }
+            }
+            xptr[i + 1] = (int)xcol.size();
+        }
+    }
+    ctx->az_nnz = AZ->row_ptr[n];
+    ctx->ax_nnz = (int64_t)xcol.size();
+    RC(upload(ctx, &ctx->azd, azd.data(), (int64_t)azd.size()));
+    if (ctx->ax_nnz > 0) {
+        RC(upload(ctx, &ctx->ax_ptr, xptr.data(), n + 1));
+        RC(upload(ctx, &ctx->ax_col, xcol.data(), ctx->ax_nnz));
+        RC(upload(ctx, &ctx->ax_val, xval.data(), ctx->ax_nnz));
+    }
+    if (!ctx->sub_off_d) RC(upload(ctx, &ctx->sub_off_d, ctx->sub_off.data(), (int64_t)ctx->sub_off.size()));
     RC(upload(ctx, &ctx->Einv, Einv, K * K));
     RC(dalloc(ctx, &ctx->tvec, K));
     RC(dalloc(ctx, &ctx->t2, K));
@@ -357,6 +390,12 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
     RC(dalloc(ctx, &ctx->tmp, ctx->n));
     RC(dalloc(ctx, &ctx->yout, ctx->n));
     ctx->nblk = cdiv(ctx->n, kBlock);
+    {
+        // one full wave of the grid-stride vector kernels (the smallest residency among them)
+        const int occ = std::min({occupancy(k_project<0, 4>), occupancy(k_project<1, 4>),
+                                  occupancy(k_cg_update), occupancy(k_cg_p), occupancy(k_dot)});
+        ctx->vgrid = std::max<int64_t>(1, std::min<int64_t>(ctx->nblk, (int64_t)occ * ctx->sm_count));
+    }
     int64_t vparts = 0;
     for (auto &g : ctx->groups)
         vparts += g.lv.empty() ? std::max<int64_t>(1, std::min<int64_t>(cdiv(g.row1 - g.row0, kBlock), 64))
@@ -372,6 +411,12 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
     CK(cudaMallocHost(&ctx->h_dots, 16 * sizeof(double)));
     RC(dalloc(ctx, &ctx->ticket, 4));
     CK(cudaMemset(ctx->ticket, 0, 4 * sizeof(unsigned int)));
+    // grid-finish groups: the largest grid of a finishing kernel is the
+    // operator / vector grid (ntiles, nblk) or the V-cycle's dot kernel
+    ctx->fin_groups = cdiv(std::max({ctx->nblk, ctx->ntiles, vparts}), kFinGroup) + ctx->nsub + 2;
+    RC(dalloc(ctx, &ctx->fin_tick, ctx->fin_groups + 1));
+    CK(cudaMemset(ctx->fin_tick, 0, sizeof(unsigned int) * (ctx->fin_groups + 1)));
+    RC(dalloc(ctx, &ctx->fin_gpart, ctx->fin_groups * kKmax));
     CK(cudaMemset(ctx->x, 0, sizeof(double) * nx));
     CK(cudaMemset(ctx->xin, 0, sizeof(double) * nx));
     CK(cudaMemset(ctx->p, 0, sizeof(double) * nx));
@@ -436,7 +481,9 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     rep->solve_seconds = ms_solve * 1e-3;
     rep->h2d_seconds = ms_h2d * 1e-3;
     rep->d2h_seconds = ms_d2h * 1e-3;
-    rep->kernel_launches = ctx->launches + (use_graph ? ctx->body_kernels * std::max(1, s.iters) : 0);
+    rep->kernel_launches = ctx->launches + (use_graph ? ctx->body_kernels * std::max(1, s.iters) +
+                                                            ctx->if_kernels * (s.iters / std::max(1, p->refresh_every))
+                                                      : 0);
     // true residual ||b - A x|| / ||b|| (deflation.py:293-297; outside the timed span)
     if (s.bnorm == 0.0) {
         rep->relative_residual = 0.0;
@@ -481,10 +528,10 @@ int dfl_coarse_lift(dfl_ctx *ctx, const double *r, double *out, int ptr_kind) {
         return DFL_E_STATE;
     }
     RC(stage_in(ctx, ctx->tmp, r, ptr_kind));
-    k_zt_vec<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, ctx->tmp, ctx->zcols, ctx->n, ctx->k,
+    launch_k(ctx->st, k_zt_vec, (unsigned)ctx->ntiles, kBlock, 0, ctx->tiles, ctx->tmp, ctx->zcols, ctx->n, ctx->k,
                                                            ctx->zt_part);
     RC(zt_to_t2(ctx, nullptr, 0, false));
-    k_lift<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, ctx->tile_sub, ctx->tmp, ctx->zcols, ctx->n,
+    launch_k(ctx->st, k_lift, (unsigned)ctx->ntiles, kBlock, 0, ctx->tiles, ctx->tile_sub, ctx->tmp, ctx->zcols, ctx->n,
                                                          ctx->k, ctx->t2, (int64_t)ctx->first_sub * ctx->k,
                                                          ctx->yout, 0);
     return stage_out(ctx, out, ctx->yout, ptr_kind);

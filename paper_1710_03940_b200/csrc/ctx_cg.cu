@@ -18,6 +18,7 @@ __device__ __forceinline__ double scalar_in(const double *part, int64_t nparts, 
 // bnorm = ||b|| (deflation.py:266), atol = tol * bnorm
 __global__ void k_cg_start(KState *st, const double *part, int64_t nparts, const double *gath, int nranks,
                            double tol, int maxiter, int refresh) {
+    DFL_PDL_ENTRY;
     const double bb = scalar_in(part, nparts, gath, nranks, 0);
     if (threadIdx.x != 0) return;
     KState s{};
@@ -35,6 +36,7 @@ __global__ void k_cg_start(KState *st, const double *part, int64_t nparts, const
 // ||b'|| of the projected rhs: zero -> zero solution; r = b' meets the target
 // -> converged at 0 iterations (krylov.py:101-113)
 __global__ void k_cg_init_r(KState *st, const double *part, int64_t nparts, const double *gath, int nranks) {
+    DFL_PDL_ENTRY;
     if (st->done) return;
     const double bb = scalar_in(part, nparts, gath, nranks, 0);
     if (threadIdx.x != 0) return;
@@ -49,57 +51,45 @@ __global__ void k_cg_init_r(KState *st, const double *part, int64_t nparts, cons
 }
 
 __global__ void k_cg_init_rz(KState *st, const double *part, int64_t nparts, const double *gath, int nranks) {
+    DFL_PDL_ENTRY;
     if (st->done) return;
     const double rz = scalar_in(part, nparts, gath, nranks, 0);
     if (threadIdx.x == 0) st->rz = rz;
 }
 
-// iters += 1; pAp (krylov.py:119-126)
-__global__ void k_cg_pq(KState *st, const double *part, int64_t nparts, const double *gath, int nranks) {
+// iters += 1; pAp (krylov.py:119-126); with use_if also the refresh IF condition
+__global__ void k_cg_pq(KState *st, const double *part, int64_t nparts, const double *gath, int nranks,
+                        int use_if, cudaGraphConditionalHandle hif) {
+    DFL_PDL_ENTRY;
     if (st->done) return;
     const double pq = scalar_in(part, nparts, gath, nranks, 0);
     if (threadIdx.x != 0) return;
-    st->iters += 1;
-    st->pq = pq;
-    if (pq <= 0.0 || !isfinite(pq)) {
-        st->breakdown = DFL_BRK_CURVATURE;
-        st->done = 1;
-        return;
-    }
-    st->alpha = st->rz / pq;
-    st->refresh_now = (st->iters % st->refresh_every) == 0;
+    cg_step_pq(st, pq);
+    if (use_if) cudaGraphSetConditional(hif, (!st->done && st->refresh_now) ? 1u : 0u);
 }
 
 // resnorm test (krylov.py:132-136)
 __global__ void k_cg_rr(KState *st, const double *part, int64_t nparts, const double *gath, int nranks) {
+    DFL_PDL_ENTRY;
     if (st->done) return;
     const double rr = scalar_in(part, nparts, gath, nranks, 0);
     if (threadIdx.x != 0) return;
-    st->rr = rr;
-    st->resnorm = sqrt(fmax(rr, 0.0));
-    if (st->resnorm <= st->target) {
-        st->converged = 1;
-        st->done = 1;
-    }
+    cg_step_rr(st, rr);
 }
 
 // beta (krylov.py:138-143)
 __global__ void k_cg_rz(KState *st, const double *part, int64_t nparts, const double *gath, int nranks) {
+    DFL_PDL_ENTRY;
     if (st->done) return;
     const double rz = scalar_in(part, nparts, gath, nranks, 0);
     if (threadIdx.x != 0) return;
-    if (rz == 0.0 || !isfinite(rz)) {
-        st->breakdown = DFL_BRK_RZ;
-        st->done = 1;
-        return;
-    }
-    st->beta = rz / st->rz;
-    st->rz = rz;
+    cg_step_rz(st, rz);
 }
 
 // multi-rank: r.r and r.z arrive in one allgather (slots 0 and 1); the
 // convergence test uses r.r exactly as k_cg_rr, then beta as k_cg_rz
 __global__ void k_cg_rrz(KState *st, const double *gath, int nranks) {
+    DFL_PDL_ENTRY;
     if (st->done || threadIdx.x != 0) return;
     double rr = 0.0, rz = 0.0;
     for (int q = 0; q < nranks; ++q) {
@@ -123,67 +113,142 @@ __global__ void k_cg_rrz(KState *st, const double *gath, int nranks) {
 }
 
 __global__ void k_cg_end(KState *st, cudaGraphConditionalHandle h, int use_cond) {
+    DFL_PDL_ENTRY;
     if (threadIdx.x != 0) return;
     if (!st->done && st->iters >= st->maxiter) st->done = 1;
     if (use_cond) cudaGraphSetConditional(h, st->done ? 0u : 1u);
 }
 
 // ---------------------------------------------------------------------------
-// one CG iteration (krylov.py:119-143) on the projected operator
-static int cg_body(dfl_ctx *ctx, bool deflated, cudaGraphConditionalHandle h, int use_cond) {
+// one CG iteration (krylov.py:119-143) on the projected operator.
+//
+// Single rank: the scalar steps run in the last block of the kernel that
+// produces their reduction (grid finish, kernels.cuh Fin), the operator
+// kernel finishes Z'w -> t -> t2 itself, and with a graph the refresh of
+// krylov.py:128-129 is a conditional IF node (no launches on the other 49 of
+// 50 iterations).  Body: op, project(+alpha), update(+r.r test), [refresh],
+// V-cycle (+beta), p update (+loop condition).  Several ranks: partials are
+// reduced, allgathered and consumed by single-block scalar kernels.
+struct CgGraph {
+    int use_cond = 0;
+    cudaGraphConditionalHandle h = 0;
+    int use_if = 0;  // refresh as an IF node
+    cudaGraphConditionalHandle hif = 0;
+};
+
+// r = b' - project(A x)  (krylov.py:128-129); need_refresh: predicated on st->refresh_now
+static int cg_refresh(dfl_ctx *ctx, bool deflated, int need_refresh) {
+    KState *st = ctx->state;
+    bool tz = false;
+    RC(op_apply_dev(ctx, ctx->x, ctx->tmp, 0, nullptr, deflated, st, need_refresh, &tz));
+    if (deflated) RC(zt_to_t2(ctx, st, need_refresh, true, tz));
+    ProjArgs a = proj_args(ctx, ctx->tmp, ctx->r, st);
+    if (!deflated) a.azd = nullptr, a.K = 0;
+    a.base = ctx->bp;
+    a.dotmode = 2;
+    a.dot_part = ctx->dpart;
+    a.need_refresh = need_refresh;
+    a.fin = make_fin(ctx, ACT_RR);
+    launch_project<1>(ctx, a);
+    return DFL_OK;
+}
+
+static int capture_refresh_if(dfl_ctx *ctx, bool deflated, cudaGraphConditionalHandle hif) {
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t capg = nullptr;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    CK(cudaStreamGetCaptureInfo(ctx->st, &cs, nullptr, &capg, &deps, &nd));
+    cudaGraphNodeParams ip = {};
+    ip.type = cudaGraphNodeTypeConditional;
+    ip.conditional.handle = hif;
+    ip.conditional.type = cudaGraphCondTypeIf;
+    ip.conditional.size = 1;
+    cudaGraphNode_t ifnode;
+    CK(cudaGraphAddNode(&ifnode, capg, deps, nd, &ip));
+    CK(cudaStreamUpdateCaptureDependencies(ctx->st, &ifnode, 1, cudaStreamSetCaptureDependencies));
+    if (!ctx->st_if) CK(cudaStreamCreateWithFlags(&ctx->st_if, cudaStreamNonBlocking));
+    cudaStream_t main = ctx->st;
+    CK(cudaStreamBeginCaptureToGraph(ctx->st_if, ip.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                     cudaStreamCaptureModeThreadLocal));
+    ctx->st = ctx->st_if;
+    const int64_t before = ctx->launches;
+    const int rc = cg_refresh(ctx, deflated, 0);
+    ctx->if_kernels = ctx->launches - before;  // run on refresh iterations only
+    ctx->launches = before;
+    ctx->st = main;
+    cudaGraph_t g2 = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(ctx->st_if, &g2);
+    RC(rc);
+    CK(ce);
+    return DFL_OK;
+}
+
+static int cg_body(dfl_ctx *ctx, bool deflated, const CgGraph &G) {
     KState *st = ctx->state;
     const double *gath;
-    // w = A p, Z'w ; t2 ; q = w - AZ t2 ; p.q
-    RC(op_apply_dev(ctx, ctx->p, ctx->w, 0, nullptr, deflated, st, 0));
-    if (deflated) RC(zt_to_t2(ctx, st, 0, true));
+    const bool single = !multi(ctx);
+    // w = A p, Z'w -> t2 ; q = w - AZ t2 ; p.q
+    bool tz = false;
+    RC(op_apply_dev(ctx, ctx->p, ctx->w, 0, nullptr, deflated, st, 0, &tz));
+    if (deflated) RC(zt_to_t2(ctx, st, 0, true, tz));
     {
         ProjArgs a = proj_args(ctx, ctx->w, ctx->w, st);
-        if (!deflated) a.az_ptr = nullptr, a.K = 0;
+        if (!deflated) a.azd = nullptr, a.K = 0;
         a.dotmode = 1;
         a.dotv = ctx->p;
         a.dot_part = ctx->dpart;
+        a.fin = make_fin(ctx, ACT_PQ);
+        a.fin.use_if = G.use_if;
+        a.fin.hif = G.hif;
         launch_project<0>(ctx, a);
+        if (!a.fin.tick) {
+            RC(rank_scalar(ctx, ctx->dpart, ctx->vgrid, 0, &gath));
+            launch_k(ctx->st, k_cg_pq, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, gath, ctx->nranks, G.use_if, G.hif);
+            ctx->launches++;
+        }
     }
-    RC(rank_scalar(ctx, ctx->dpart, ctx->nblk, 0, &gath));
-    k_cg_pq<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks);
-    ctx->launches++;
-    // x += alpha p ; r -= alpha q (regular iterations)
-    k_cg_update<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->x, ctx->r, ctx->p, ctx->w, ctx->n, ctx->dpart, st);
+    // x += alpha p ; r -= alpha q (regular iterations; + r.r test when finished in-kernel)
+    const Fin frr = make_fin(ctx, ACT_RR);
+    launch_k(ctx->st, k_cg_update, (unsigned)ctx->vgrid, kBlock, 0, ctx->x, ctx->r, ctx->p, ctx->w, ctx->n, ctx->dpart, st,
+                                                            frr);
     ctx->launches++;
     // refresh iterations: r = b' - project(A x)   (krylov.py:128-129)
-    RC(op_apply_dev(ctx, ctx->x, ctx->tmp, 0, nullptr, deflated, st, 1));
-    if (deflated) RC(zt_to_t2(ctx, st, 1, true));
-    {
-        ProjArgs a = proj_args(ctx, ctx->tmp, ctx->r, st);
-        if (!deflated) a.az_ptr = nullptr, a.K = 0;
-        a.base = ctx->bp;
-        a.dotmode = 2;
-        a.dot_part = ctx->dpart;
-        a.need_refresh = 1;
-        launch_project<1>(ctx, a);
-    }
+    if (G.use_if)
+        RC(capture_refresh_if(ctx, deflated, G.hif));
+    else
+        RC(cg_refresh(ctx, deflated, 1));
     int64_t np = 0;
-    if (multi(ctx)) {
+    if (!single) {
         // one collective for r.r and r.z: the V-cycle runs before the
         // convergence test (its result is discarded on the last iteration)
-        k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->dpart, ctx->nblk, ctx->scal + 0);
+        launch_k(ctx->st, k_reduce, 1, 1024, 0, ctx->dpart, ctx->vgrid, ctx->scal + 0);
         RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
-        k_reduce<<<1, 1024, 0, ctx->st>>>(ctx->dpart, np, ctx->scal + 1);
+        launch_k(ctx->st, k_reduce, 1, 1024, 0, ctx->dpart, np, ctx->scal + 1);
         RC(comm_allgather(ctx, ctx->scal, ctx->sgather, 8));
-        k_cg_rrz<<<1, 32, 0, ctx->st>>>(st, ctx->sgather, ctx->nranks);
+        launch_k(ctx->st, k_cg_rrz, 1, 32, 0, st, ctx->sgather, ctx->nranks);
         ctx->launches += 3;
     } else {
-        k_cg_rr<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, nullptr, 1);
-        ctx->launches++;
-        // z = M r, r.z
-        RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
-        k_cg_rz<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, np, nullptr, 1);
+        if (!frr.tick) {
+            launch_k(ctx->st, k_cg_rr, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, nullptr, 1);
+            ctx->launches++;
+        }
+        // z = M r, r.z -> beta
+        const Fin frz = make_fin(ctx, ACT_RZ);
+        bool used = false;
+        RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np, &frz, &used));
+        if (!used) {
+            launch_k(ctx->st, k_cg_rz, 1, 1024, 0, st, ctx->dpart, np, nullptr, 1);
+            ctx->launches++;
+        }
+    }
+    launch_k(ctx->st, k_cg_p, (unsigned)ctx->vgrid, kBlock, 0, ctx->p, ctx->z, ctx->n, st, G.use_cond, G.h, G.use_if,
+                                                       G.hif);
+    ctx->launches++;
+    if (!G.use_cond) {
+        launch_k(ctx->st, k_cg_end, 1, 32, 0, st, 0, 0);
         ctx->launches++;
     }
-    k_cg_p<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->p, ctx->z, ctx->n, st);
-    ctx->launches++;
-    k_cg_end<<<1, 32, 0, ctx->st>>>(st, h, use_cond);
-    ctx->launches++;
     return DFL_OK;
 }
 
@@ -206,9 +271,15 @@ static int build_loop_graph(dfl_ctx *ctx, bool deflated) {
     cudaGraphNode_t node;
     CK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
     cudaGraph_t body = cp.conditional.phGraph_out[0];
+    CgGraph G;
+    G.use_cond = 1;
+    G.h = h;
+    const char *ni = getenv("DFL_NO_IF");
+    G.use_if = !(ni && ni[0] == '1');
+    if (G.use_if) CK(cudaGraphConditionalHandleCreate(&G.hif, body, 0, 0));
     CK(cudaStreamBeginCaptureToGraph(ctx->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     const int64_t before = ctx->launches;
-    int rc = cg_body(ctx, deflated, h, 1);
+    int rc = cg_body(ctx, deflated, G);
     cudaGraph_t captured = nullptr;
     cudaError_t ce = cudaStreamEndCapture(ctx->st, &captured);
     if (rc != DFL_OK) return rc;
@@ -227,13 +298,15 @@ int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
     KState *st = ctx->state;
     const bool defl = p->deflated != 0;
     const double *gath;
+    // grid-finish counters start at zero (a failed launch could leave them dirty)
+    if (ctx->fin_tick) CK(cudaMemsetAsync(ctx->fin_tick, 0, sizeof(unsigned) * (ctx->fin_groups + 1), ctx->st));
     // x = 0 (y of the deflated system)
-    k_fill<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->x, 0.0, ctx->n);
+    launch_k(ctx->st, k_fill, (unsigned)ctx->nblk, kBlock, 0, ctx->x, 0.0, ctx->n);
     // ||b||
-    k_dot<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->b, ctx->b, ctx->n, ctx->dpart, nullptr);
+    launch_k(ctx->st, k_dot, (unsigned)ctx->vgrid, kBlock, 0, ctx->b, ctx->b, ctx->n, ctx->dpart, nullptr);
     ctx->launches += 2;
-    RC(rank_scalar(ctx, ctx->dpart, ctx->nblk, 0, &gath));
-    k_cg_start<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks, p->tol, p->maxiter,
+    RC(rank_scalar(ctx, ctx->dpart, ctx->vgrid, 0, &gath));
+    launch_k(ctx->st, k_cg_start, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, gath, ctx->nranks, p->tol, p->maxiter,
                                       std::max(1, p->refresh_every));
     ctx->launches++;
     // b' = project(b) and ||b'||^2
@@ -241,21 +314,21 @@ int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
         RC(project_dev(ctx, ctx->b, ctx->bp, nullptr, 2));
     } else {
         ProjArgs a = proj_args(ctx, ctx->b, ctx->bp, nullptr);
-        a.az_ptr = nullptr;
+        a.azd = nullptr;
         a.K = 0;
         a.dotmode = 2;
         a.dot_part = ctx->dpart;
         launch_project<0>(ctx, a);
     }
-    RC(rank_scalar(ctx, ctx->dpart, ctx->nblk, 0, &gath));
-    k_cg_init_r<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, ctx->nblk, gath, ctx->nranks);
-    k_copy<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->r, ctx->bp, ctx->n);
+    RC(rank_scalar(ctx, ctx->dpart, ctx->vgrid, 0, &gath));
+    launch_k(ctx->st, k_cg_init_r, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, gath, ctx->nranks);
+    launch_k(ctx->st, k_copy, (unsigned)ctx->nblk, kBlock, 0, ctx->r, ctx->bp, ctx->n);
     ctx->launches += 2;
     int64_t np = 0;
     RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
     RC(rank_scalar(ctx, ctx->dpart, np, 0, &gath));
-    k_cg_init_rz<<<1, 1024, 0, ctx->st>>>(st, ctx->dpart, np, gath, ctx->nranks);
-    k_copy<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->p, ctx->z, ctx->n);
+    launch_k(ctx->st, k_cg_init_rz, 1, 1024, 0, st, ctx->dpart, np, gath, ctx->nranks);
+    launch_k(ctx->st, k_copy, (unsigned)ctx->nblk, kBlock, 0, ctx->p, ctx->z, ctx->n);
     ctx->launches += 2;
     // the loop
     if (use_graph) {
@@ -263,7 +336,7 @@ int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
         CK(cudaGraphLaunch(ctx->loop_exec, ctx->st));
     } else {
         for (;;) {
-            RC(cg_body(ctx, defl, 0, 0));
+            RC(cg_body(ctx, defl, CgGraph{}));
             CK(cudaMemcpyAsync(ctx->h_state, st, sizeof(KState), cudaMemcpyDeviceToHost, ctx->st));
             CK(cudaStreamSynchronize(ctx->st));
             if (ctx->h_state->done) break;

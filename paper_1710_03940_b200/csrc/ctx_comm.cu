@@ -39,7 +39,7 @@ int halo(dfl_ctx *ctx, double *v, cudaStream_t xs) {
     if (!multi(ctx) || (ctx->nbr.empty() && !ctx->fab)) return DFL_OK;
     if (!xs) xs = ctx->st;
     if (ctx->nsend > 0) {
-        k_gather<<<(unsigned)cdiv(ctx->nsend, kBlock), kBlock, 0, ctx->st>>>(v, ctx->send_idx, ctx->nsend,
+        launch_k(ctx->st, k_gather, (unsigned)cdiv(ctx->nsend, kBlock), kBlock, 0, v, ctx->send_idx, ctx->nsend,
                                                                               ctx->sendbuf);
         ctx->launches++;
     }
@@ -94,18 +94,27 @@ int halo(dfl_ctx *ctx, double *v, cudaStream_t xs) {
 }
 
 // Z' v partials -> t (global numbering) -> t2 = E^-1 t on every rank
-int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op) {
+// (t_ready: the operator kernel already wrote t, and t2 unless inexact)
+int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op, bool t_ready) {
     const int64_t *sub_tiles =
         (from_op && g_use_pipe && !ctx->split && ctx->Aop.pipe.stages) ? ctx->op_sub_tiles : ctx->sub_tiles;
+    if (t_ready) {
+        if (ctx->inexact) {
+            launch_k(ctx->st, k_egmres, 1, 256, 0, ctx->Edense, (int)ctx->K, ctx->tvec, ctx->t2, ctx->coarse_tol,
+                                             ctx->egm_scr, st, need_refresh);
+            ctx->launches++;
+        }
+        return DFL_OK;
+    }
     if (!multi(ctx)) {
-        k_zt_finish<<<ctx->nsub * ctx->k, 512, 0, ctx->st>>>(ctx->zt_part, sub_tiles, ctx->nsub, ctx->k,
+        launch_k(ctx->st, k_zt_finish, ctx->nsub * ctx->k, 512, 0, ctx->zt_part, sub_tiles, ctx->nsub, ctx->k,
                                                              ctx->tvec, 0, ctx->inexact ? nullptr : ctx->Einv,
                                                              ctx->K, ctx->t2, st, need_refresh, ctx->ticket,
                                                              from_op && ctx->split ? ctx->sub_btiles : nullptr,
                                                              ctx->ntiles);
         ctx->launches++;
         if (ctx->inexact) {
-            k_egmres<<<1, 256, 0, ctx->st>>>(ctx->Edense, (int)ctx->K, ctx->tvec, ctx->t2, ctx->coarse_tol,
+            launch_k(ctx->st, k_egmres, 1, 256, 0, ctx->Edense, (int)ctx->K, ctx->tvec, ctx->t2, ctx->coarse_tol,
                                              ctx->egm_scr, st, need_refresh);
             ctx->launches++;
         }
@@ -114,7 +123,7 @@ int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op) {
     // local entries into a padded slot, allgather, unpack, solve
     const int64_t slot = (int64_t)ctx->max_nsub * ctx->k;
     double *mine = ctx->tgather + (int64_t)ctx->rank * slot;
-    k_zt_finish<<<ctx->nsub * ctx->k, 512, 0, ctx->st>>>(ctx->zt_part, sub_tiles, ctx->nsub, ctx->k, mine, 0,
+    launch_k(ctx->st, k_zt_finish, ctx->nsub * ctx->k, 512, 0, ctx->zt_part, sub_tiles, ctx->nsub, ctx->k, mine, 0,
                                                          nullptr, ctx->K, nullptr, st, need_refresh, ctx->ticket,
                                                          from_op && ctx->split ? ctx->sub_btiles : nullptr,
                                                          ctx->ntiles);
@@ -128,10 +137,10 @@ int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op) {
         pos += cnt;
     }
     if (ctx->inexact)
-        k_egmres<<<1, 256, 0, ctx->st>>>(ctx->Edense, (int)ctx->K, ctx->tvec, ctx->t2, ctx->coarse_tol, ctx->egm_scr,
+        launch_k(ctx->st, k_egmres, 1, 256, 0, ctx->Edense, (int)ctx->K, ctx->tvec, ctx->t2, ctx->coarse_tol, ctx->egm_scr,
                                          st, need_refresh);
     else
-        k_esolve<<<1, 256, 0, ctx->st>>>(ctx->Einv, ctx->K, ctx->tvec, ctx->t2, st, need_refresh);
+        launch_k(ctx->st, k_esolve, 1, 256, 0, ctx->Einv, ctx->K, ctx->tvec, ctx->t2, st, need_refresh);
     ctx->launches += 2;
     return DFL_OK;
 }
@@ -141,7 +150,7 @@ int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op) {
 int rank_scalar(dfl_ctx *ctx, const double *part, int64_t nparts, int slot, const double **gath) {
     *gath = nullptr;
     if (!multi(ctx)) return DFL_OK;
-    k_reduce<<<1, 1024, 0, ctx->st>>>(part, nparts, ctx->scal + slot);
+    launch_k(ctx->st, k_reduce, 1, 1024, 0, part, nparts, ctx->scal + slot);
     ctx->launches++;
     RC(comm_allgather(ctx, ctx->scal, ctx->sgather, 8));
     *gath = ctx->sgather;

@@ -6,8 +6,12 @@
 // V-cycle over all groups: z = M r  (deflation.py:239-250 -> amg.py:201-212).
 // With dot_part != nullptr the last kernel of every group also emits the
 // per-block partials of r.z; *nparts receives their count.
-int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *dot_part, int64_t *nparts) {
+// With fin (single group only) the dot kernel also finishes the reduction
+// and runs fin->act (*fin_used = true).
+int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *dot_part, int64_t *nparts,
+           const Fin *fin, bool *fin_used) {
     int64_t poff = 0;
+    if (fin_used) *fin_used = false;
     for (VGroup &g : ctx->groups) {
         const double *rin = r + g.row0;
         double *zout = z + g.row0;
@@ -20,9 +24,13 @@ int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *d
             const double *in = l == 0 ? rin : v.rv;
             double *next = (l + 1 < L) ? g.lv[l + 1].rv : g.rb;
             if (v.A.fmt == FMT_CODE) {
-                k_wr<<<(unsigned)cdiv(v.n, kBlock), kBlock, 0, ctx->st>>>(v.w, in, v.wr, v.n);
-                ctx->launches++;
-                RowArgs a{v.wr, v.w, in, nullptr, v.t, nullptr, st};
+                const double *wr = nullptr;  // w .* r formed at the gather
+                if (g_wr_split) {
+                    launch_k(ctx->st, k_wr, (unsigned)cdiv(v.n, kBlock), kBlock, 0, v.w, in, v.wr, v.n);
+                    ctx->launches++;
+                    wr = v.wr;
+                }
+                RowArgs a{wr, v.w, in, nullptr, v.t, nullptr, st};
                 launch_rows<MODE_RESID, false>(ctx, v.A, a);
             } else {
                 RowArgs a{nullptr, v.w, in, nullptr, v.t, nullptr, st};
@@ -53,7 +61,7 @@ int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *d
         } else {
             const double *rb = L == 0 ? rin : g.rb;
             double *xb = L == 0 ? zout : g.xb;
-            k_bottom<<<dim3((unsigned)cdiv(g.max_nb, 32), (unsigned)g.nsub), 256, 0, ctx->st>>>(
+            launch_k(ctx->st, k_bottom, dim3((unsigned)cdiv(g.max_nb, 32), (unsigned)g.nsub), 256, 0, 
                 g.binvT, g.binv_off, g.b_off, rb, xb, st);
             ctx->launches++;
             prof_mark(ctx, "bottom");
@@ -68,6 +76,10 @@ int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *d
             prof_mark(ctx, "L" + std::to_string(l) + " prolong");
             if (l == 0 && dot_part) {
                 RowArgs b{v.t, v.w, in, v.t, out, dot_part + poff, st};
+                if (fin && fin->tick && ctx->groups.size() == 1 && !g_use_pipe) {
+                    b.fin = *fin;
+                    if (fin_used) *fin_used = true;
+                }
                 launch_rows<MODE_POST, true>(ctx, v.A, b);
                 poff += parts_for(v.A);
             } else {
@@ -80,7 +92,7 @@ int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *d
             // the group's finest level ran without a fused dot: explicit partials
             const int64_t rows = g.row1 - g.row0;
             const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(rows, kBlock), 64));
-            k_dot<<<nb, kBlock, 0, ctx->st>>>(rin, zout, rows, dot_part + poff, st);
+            launch_k(ctx->st, k_dot, nb, kBlock, 0, rin, zout, rows, dot_part + poff, st);
             ctx->launches++;
             poff += nb;
         }
@@ -91,8 +103,19 @@ int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *d
 
 // y = A x (opmode 0) or y = b - A x (opmode 1); with zt the Z'y tile partials
 int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double *b, bool zt,
-                        const KState *st, int need_refresh) {
+                        const KState *st, int need_refresh, bool *fin_zt) {
     OpArgs a{xin, b, y, ctx->zcols, ctx->n, zt ? ctx->k : 0, ctx->zt_part, st, need_refresh};
+    if (fin_zt) *fin_zt = false;
+    if (fin_zt && zt && ctx->k > 0 && op_fusable(ctx)) {
+        a.tick = ctx->fin_tick;
+        a.gpart = ctx->fin_gpart;
+        a.t = ctx->tvec;
+        a.Einv = ctx->inexact ? nullptr : ctx->Einv;
+        a.t2 = ctx->t2;
+        a.K = ctx->K;
+        a.first_col = (int64_t)ctx->first_sub * ctx->k;
+        *fin_zt = true;
+    }
     if (!ctx->split) {
         RC(halo(ctx, xin));
         if (opmode == 0)
@@ -117,10 +140,10 @@ int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double 
     a.skip_rows = nullptr;
     if (ctx->nbtiles > 0) {
         if (opmode == 0)
-            k_op_bnd<0><<<(unsigned)ctx->nbtiles, kBlock, 0, ctx->st>>>(ctx->Aop, ctx->brows, ctx->bstart, ctx->bcnt,
+            launch_k(ctx->st, k_op_bnd<0>, (unsigned)ctx->nbtiles, kBlock, 0, ctx->Aop, ctx->brows, ctx->bstart, ctx->bcnt,
                                                                          ctx->ntiles, a);
         else
-            k_op_bnd<1><<<(unsigned)ctx->nbtiles, kBlock, 0, ctx->st>>>(ctx->Aop, ctx->brows, ctx->bstart, ctx->bcnt,
+            launch_k(ctx->st, k_op_bnd<1>, (unsigned)ctx->nbtiles, kBlock, 0, ctx->Aop, ctx->brows, ctx->bstart, ctx->bcnt,
                                                                          ctx->ntiles, a);
         ctx->launches++;
     }
@@ -129,7 +152,7 @@ int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double 
 
 // out = project(v) = v - AZ E^-1 Z' v   (deflation.py:230-233)
 int project_dev(dfl_ctx *ctx, const double *v, double *out, const KState *st, int dotmode) {
-    k_zt_vec<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, v, ctx->zcols, ctx->n, ctx->k, ctx->zt_part);
+    launch_k(ctx->st, k_zt_vec, (unsigned)ctx->ntiles, kBlock, 0, ctx->tiles, v, ctx->zcols, ctx->n, ctx->k, ctx->zt_part);
     ctx->launches++;
     RC(zt_to_t2(ctx, nullptr, 0, false));
     ProjArgs a = proj_args(ctx, v, out, st);
@@ -144,11 +167,11 @@ int lift_dev(dfl_ctx *ctx, const dfl_solve_params *p) {
     if (p->deflated) {
         RC(op_apply_dev(ctx, ctx->x, ctx->tmp, 1, ctx->b, true, nullptr, 0));
         RC(zt_to_t2(ctx, nullptr, 0, true));
-        k_lift<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, ctx->tile_sub, ctx->x, ctx->zcols, ctx->n,
+        launch_k(ctx->st, k_lift, (unsigned)ctx->ntiles, kBlock, 0, ctx->tiles, ctx->tile_sub, ctx->x, ctx->zcols, ctx->n,
                                                               ctx->k, ctx->t2, (int64_t)ctx->first_sub * ctx->k,
                                                               ctx->xin, 1);
     } else {
-        k_copy<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->xin, ctx->x, ctx->n);
+        launch_k(ctx->st, k_copy, (unsigned)ctx->nblk, kBlock, 0, ctx->xin, ctx->x, ctx->n);
     }
     ctx->launches++;
     return DFL_OK;
@@ -189,6 +212,15 @@ int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
     auto run = [&]() -> int {
         if (what == 0) return op_apply_dev(ctx, ctx->p, ctx->w, 0, nullptr, false, nullptr, 0);
         if (what == 1 || what == 2) return vcycle(ctx, ctx->r, ctx->z, nullptr, nullptr, nullptr);
+        if (what == 4) return op_apply_dev(ctx, ctx->p, ctx->w, 0, nullptr, ctx->deflation, nullptr, 0);
+        if (what == 5) {  // q = w - AZ t2 with the fused p.q partials (the CG projection)
+            ProjArgs a = proj_args(ctx, ctx->w, ctx->tmp, nullptr);
+            a.dotmode = 1;
+            a.dotv = ctx->p;
+            a.dot_part = ctx->dpart;
+            launch_project<0>(ctx, a);
+            return DFL_OK;
+        }
         ctx->err = "unknown timing target";
         return DFL_E_CONFIG;
     };
@@ -200,8 +232,12 @@ int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
         return (M.vcode ? 5.0 : 12.0) * (double)M.stored + (M.perm ? 4.0 * rows : 0.0) +
                (M.ell_w ? 0.0 : 8.0 * (rows / 32 + 1));
     };
-    if (what == 0) {
+    if (what == 0 || what == 4) {
         *bytes = 12.0 * ctx->op_nnz + 4.0 * (ctx->n + 1) + 8.0 * (ctx->n + ctx->n_ghost) + 8.0 * ctx->n;
+        if (what == 4 && ctx->deflation) *bytes += 8.0 * (ctx->k - 1) * ctx->n;  // Z columns 1..k-1
+    } else if (what == 5) {
+        // w, p read, q written + AZ (CSR fp64/int32, as uploaded)
+        *bytes = 24.0 * ctx->n + (ctx->deflation ? 12.0 * ctx->az_nnz + 4.0 * (ctx->n + 1) : 0.0);
     } else if (what == 2) {
         double b = 0;
         for (auto &g : ctx->groups) {
@@ -228,8 +264,9 @@ int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
         *bytes = b;
     }
     // fill the inputs with something finite
-    k_fill<<<(unsigned)cdiv(ctx->n + ctx->n_ghost, kBlock), kBlock, 0, ctx->st>>>(ctx->p, 1.0, ctx->n + ctx->n_ghost);
-    k_fill<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->r, 1.0, ctx->n);
+    launch_k(ctx->st, k_fill, (unsigned)cdiv(ctx->n + ctx->n_ghost, kBlock), kBlock, 0, ctx->p, 1.0, ctx->n + ctx->n_ghost);
+    launch_k(ctx->st, k_fill, (unsigned)ctx->nblk, kBlock, 0, ctx->r, 1.0, ctx->n);
+    launch_k(ctx->st, k_fill, (unsigned)ctx->nblk, kBlock, 0, ctx->w, 1.0, ctx->n);
     if (what == 3) {  // the V-cycle as the solve runs it: captured once, replayed as a CUDA graph
         double b = 0;
         double tmp = 0;
@@ -271,7 +308,7 @@ int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
 int dfl_ctx_profile_vcycle(dfl_ctx *ctx, int reps, int cap, double *ms, char *labels /* cap x 32 */) {
     RC(ready(ctx));
     if (reps < 1) reps = 1;
-    k_fill<<<(unsigned)ctx->nblk, kBlock, 0, ctx->st>>>(ctx->r, 1.0, ctx->n);
+    launch_k(ctx->st, k_fill, (unsigned)ctx->nblk, kBlock, 0, ctx->r, 1.0, ctx->n);
     RC(vcycle(ctx, ctx->r, ctx->z, nullptr, nullptr, nullptr));
     std::vector<double> acc;
     int count = 0;

@@ -72,7 +72,7 @@ struct Nccl {
 extern Nccl g_nccl;
 
 // profiling / layout knobs (defined in ctx.cu, read at context creation)
-extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell;
+extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl;
 extern double g_small_per_lane, g_csr_per_lane;
 extern int g_csr_g, g_sm_count;
 static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle
@@ -190,9 +190,11 @@ struct dfl_ctx {
     int64_t K = 0;
     int first_sub = 0;
     double *zcols = nullptr;
-    int *az_ptr = nullptr, *az_col = nullptr;
-    double *az_val = nullptr;
-    int64_t az_nnz = 0;
+    double *azd = nullptr;                  // own-block AZ values, k x n column-major
+    int *ax_ptr = nullptr, *ax_col = nullptr;  // AZ entries outside the own block (nullptr: none)
+    double *ax_val = nullptr;
+    int64_t az_nnz = 0, ax_nnz = 0;
+    int64_t *sub_off_d = nullptr;           // nsub + 1 local row offsets
     double *Einv = nullptr;
     // inexact coarse solve (deflation.py:166-178): inner GMRES on E
     bool inexact = false;
@@ -202,6 +204,11 @@ struct dfl_ctx {
     double *zt_part = nullptr;
     double *tgather = nullptr;  // nranks * maxsub * k
     unsigned int *ticket = nullptr;
+    // grid finish (kernels.cuh Fin): counters (zero between launches) and group sums
+    unsigned int *fin_tick = nullptr;
+    double *fin_gpart = nullptr;
+    int64_t fin_groups = 0;
+    cudaStream_t st_if = nullptr;  // capture stream of the refresh IF body
     int max_nsub = 0;
     std::vector<int> rank_nsub;  // subdomains per rank (runtime.rank_subdomains)
     // work vectors (n, or n + n_ghost for operator inputs)
@@ -209,6 +216,7 @@ struct dfl_ctx {
            *w = nullptr, *tmp = nullptr, *xin = nullptr, *yout = nullptr;
     double *dpart = nullptr;
     int64_t nblk = 0;
+    int64_t vgrid = 0;  // grid of the grid-stride vector kernels (projection, CG updates, dots)
     // BiCGStab(2) work vectors (allocated on first use)
     double *br[3] = {nullptr, nullptr, nullptr}, *bd[3] = {nullptr, nullptr, nullptr};
     double *bu = nullptr, *bshadow = nullptr, *zx = nullptr;
@@ -227,6 +235,7 @@ struct dfl_ctx {
     cudaGraphExec_t loop_exec = nullptr;
     int loop_key = -1;
     int64_t body_kernels = 0;
+    int64_t if_kernels = 0;  // refresh IF body (graph)
     int64_t launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // per-launch profiling of the V-cycle (dfl_ctx_profile_vcycle)
@@ -298,18 +307,52 @@ struct HostRows {
 // ---------------------------------------------------------------------------
 // kernel launch helpers
 
+// Every solve-path kernel is launched with programmatic stream serialization
+// (PDL; kernels.cuh DFL_PDL_ENTRY): inside the captured CUDA graphs this
+// becomes a programmatic edge, so a kernel's launch overlaps the tail of the
+// one before it.  DFL_NO_PDL=1 launches them plainly.
+template <typename... KArgs, typename... Args>
+inline void launch_k(cudaStream_t st, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    if (g_pdl) {
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 inline int rows_per_block(const DMat &A) { return A.fmt == FMT_CSR ? kBlock / A.group : kBlock; }
 
 inline int64_t nblocks_for(const DMat &A) { return cdiv(A.nrows, rows_per_block(A)); }
 
-// grid of the grid-stride FMT_CODE kernels
-inline int64_t code_grid(const dfl_ctx *, const DMat &A) {
-    return std::max<int64_t>(1, std::min<int64_t>(cdiv(A.nrows, kBlock), 8 * (int64_t)g_sm_count));
+// resident blocks per SM of a kBlock-thread kernel (grid-stride grids are
+// sized to one full wave: a second partial wave would double the tail)
+template <class K>
+inline int occupancy(K kernel) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kBlock, 0) != cudaSuccess) b = 1;
+    return std::max(1, b);
 }
 
-// number of per-block / per-tile partials a row kernel on A produces
+// grid of the grid-stride FMT_CODE / VELL kernels: one wave of the instance
+template <int MODE, bool DOT>
+inline int64_t code_grid(const DMat &A) {
+    static const int occ_code = occupancy(k_code<MODE, DOT>);
+    static const int occ_vell = occupancy(k_vell<MODE, DOT>);
+    const int occ = A.vcode ? occ_vell : occ_code;
+    return std::max<int64_t>(1, std::min<int64_t>(cdiv(A.nrows, kBlock), (int64_t)occ * g_sm_count));
+}
+
+// number of per-block / per-tile partials the POST-with-dot kernel on A produces
 inline int64_t parts_for(const DMat &A) {
-    if (A.fmt == FMT_CODE || A.vcode) return code_grid(nullptr, A);
+    if (A.fmt == FMT_CODE || A.vcode) return code_grid<MODE_POST, true>(A);
     return A.pipe.stages ? A.pipe.ntiles : nblocks_for(A);
 }
 
@@ -366,12 +409,12 @@ template <int MODE, bool DOT>
 static void launch_csr_mode(const DMat &A, const RowArgs &a, cudaStream_t st) {
     const dim3 grid((unsigned)nblocks_for(A));
     switch (A.group) {
-        case 1: k_csr<1, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
-        case 2: k_csr<2, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
-        case 4: k_csr<4, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
-        case 8: k_csr<8, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
-        case 16: k_csr<16, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
-        default: k_csr<32, MODE, DOT><<<grid, kBlock, 0, st>>>(A, a); break;
+        case 1: launch_k(st, k_csr<1, MODE, DOT>, grid, kBlock, 0, A, a); break;
+        case 2: launch_k(st, k_csr<2, MODE, DOT>, grid, kBlock, 0, A, a); break;
+        case 4: launch_k(st, k_csr<4, MODE, DOT>, grid, kBlock, 0, A, a); break;
+        case 8: launch_k(st, k_csr<8, MODE, DOT>, grid, kBlock, 0, A, a); break;
+        case 16: launch_k(st, k_csr<16, MODE, DOT>, grid, kBlock, 0, A, a); break;
+        default: launch_k(st, k_csr<32, MODE, DOT>, grid, kBlock, 0, A, a); break;
     }
 }
 
@@ -379,12 +422,12 @@ template <int MODE, bool DOT>
 static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
     if (A.nrows == 0) return;
     if (A.fmt == FMT_CODE) {
-        k_code<MODE, DOT><<<(unsigned)code_grid(ctx, A), kBlock, 0, ctx->st>>>(A, a);
+        launch_k(ctx->st, k_code<MODE, DOT>, (unsigned)code_grid<MODE, DOT>(A), kBlock, 0, A, a);
         ctx->launches++;
         return;
     }
     if (A.vcode) {
-        k_vell<MODE, DOT><<<(unsigned)code_grid(ctx, A), kBlock, 0, ctx->st>>>(A, a);
+        launch_k(ctx->st, k_vell<MODE, DOT>, (unsigned)code_grid<MODE, DOT>(A), kBlock, 0, A, a);
         ctx->launches++;
         return;
     }
@@ -406,17 +449,33 @@ static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
     if (A.fmt == FMT_ELL) {
         const unsigned grid = (unsigned)nblocks_for(A);
         switch (A.ell_w) {
-            case 3: k_ell<MODE, DOT, 3><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
-            case 4: k_ell<MODE, DOT, 4><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
-            case 5: k_ell<MODE, DOT, 5><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
-            case 6: k_ell<MODE, DOT, 6><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
-            case 7: k_ell<MODE, DOT, 7><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
-            case 8: k_ell<MODE, DOT, 8><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
-            default: k_ell<MODE, DOT, 0><<<grid, kBlock, 0, ctx->st>>>(A, a); break;
+            case 3: launch_k(ctx->st, k_ell<MODE, DOT, 3>, grid, kBlock, 0, A, a); break;
+            case 4: launch_k(ctx->st, k_ell<MODE, DOT, 4>, grid, kBlock, 0, A, a); break;
+            case 5: launch_k(ctx->st, k_ell<MODE, DOT, 5>, grid, kBlock, 0, A, a); break;
+            case 6: launch_k(ctx->st, k_ell<MODE, DOT, 6>, grid, kBlock, 0, A, a); break;
+            case 7: launch_k(ctx->st, k_ell<MODE, DOT, 7>, grid, kBlock, 0, A, a); break;
+            case 8: launch_k(ctx->st, k_ell<MODE, DOT, 8>, grid, kBlock, 0, A, a); break;
+            default: launch_k(ctx->st, k_ell<MODE, DOT, 0>, grid, kBlock, 0, A, a); break;
         }
     } else
         launch_csr_mode<MODE, DOT>(A, a, ctx->st);
     ctx->launches++;
+}
+
+template <int OPMODE, int NV>
+static void launch_op_nv(dfl_ctx *ctx, const OpArgs &a, unsigned grid) {
+    const DMat &A = ctx->Aop;
+    const SubTable &S = ctx->subtab;
+    if (A.fmt == FMT_CODE) {
+        launch_k(ctx->st, k_op_code<OPMODE, NV>, grid, kBlock, 0, A, ctx->tiles, S, a);
+        return;
+    }
+    switch (A.ell_w) {
+        case 5: launch_k(ctx->st, k_op_ell<OPMODE, 5, NV>, grid, kBlock, 0, A, ctx->tiles, S, a); break;
+        case 6: launch_k(ctx->st, k_op_ell<OPMODE, 6, NV>, grid, kBlock, 0, A, ctx->tiles, S, a); break;
+        case 7: launch_k(ctx->st, k_op_ell<OPMODE, 7, NV>, grid, kBlock, 0, A, ctx->tiles, S, a); break;
+        default: launch_k(ctx->st, k_op_ell<OPMODE, 0, NV>, grid, kBlock, 0, A, ctx->tiles, S, a); break;
+    }
 }
 
 template <int OPMODE>
@@ -437,24 +496,24 @@ static void launch_op(dfl_ctx *ctx, const OpArgs &a) {
     }
     const unsigned grid = (unsigned)ctx->ntiles;
     if (grid == 0) return;
-    if (A.fmt == FMT_CODE) {
-        k_op_code<OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a);
-    } else if (A.fmt == FMT_ELL) {
-        const SubTable &S = ctx->subtab;
-        switch (A.ell_w) {
-            case 5: k_op_ell<OPMODE, 5><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, S, a); break;
-            case 6: k_op_ell<OPMODE, 6><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, S, a); break;
-            case 7: k_op_ell<OPMODE, 7><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, S, a); break;
-            default: k_op_ell<OPMODE, 0><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, S, a); break;
-        }
+    if (A.fmt == FMT_CODE || A.fmt == FMT_ELL) {
+        // Z'y epilogue width: the smallest power of two >= k
+        if (a.k <= 1)
+            launch_op_nv<OPMODE, 1>(ctx, a, grid);
+        else if (a.k <= 2)
+            launch_op_nv<OPMODE, 2>(ctx, a, grid);
+        else if (a.k <= 4)
+            launch_op_nv<OPMODE, 4>(ctx, a, grid);
+        else
+            launch_op_nv<OPMODE, 8>(ctx, a, grid);
     } else {
         switch (A.group) {
-            case 1: k_op_csr<1, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
-            case 2: k_op_csr<2, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
-            case 4: k_op_csr<4, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
-            case 8: k_op_csr<8, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
-            case 16: k_op_csr<16, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
-            default: k_op_csr<32, OPMODE><<<grid, kBlock, 0, ctx->st>>>(A, ctx->tiles, ctx->subtab, a); break;
+            case 1: launch_k(ctx->st, k_op_csr<1, OPMODE>, grid, kBlock, 0, A, ctx->tiles, ctx->subtab, a); break;
+            case 2: launch_k(ctx->st, k_op_csr<2, OPMODE>, grid, kBlock, 0, A, ctx->tiles, ctx->subtab, a); break;
+            case 4: launch_k(ctx->st, k_op_csr<4, OPMODE>, grid, kBlock, 0, A, ctx->tiles, ctx->subtab, a); break;
+            case 8: launch_k(ctx->st, k_op_csr<8, OPMODE>, grid, kBlock, 0, A, ctx->tiles, ctx->subtab, a); break;
+            case 16: launch_k(ctx->st, k_op_csr<16, OPMODE>, grid, kBlock, 0, A, ctx->tiles, ctx->subtab, a); break;
+            default: launch_k(ctx->st, k_op_csr<32, OPMODE>, grid, kBlock, 0, A, ctx->tiles, ctx->subtab, a); break;
         }
     }
     ctx->launches++;
@@ -468,9 +527,14 @@ inline bool multi(const dfl_ctx *ctx) { return ctx->comm != nullptr || ctx->fab 
 inline ProjArgs proj_args(dfl_ctx *ctx, const double *in, double *out, const KState *st) {
     ProjArgs a{};
     if (ctx->deflation) {
-        a.az_ptr = ctx->az_ptr;
-        a.az_col = ctx->az_col;
-        a.az_val = ctx->az_val;
+        a.azd = ctx->azd;
+        a.ax_ptr = ctx->ax_ptr;
+        a.ax_col = ctx->ax_col;
+        a.ax_val = ctx->ax_val;
+        a.sub_off = ctx->sub_off_d;
+        a.nsub = ctx->nsub;
+        a.k = ctx->k;
+        a.own_base = (int64_t)ctx->first_sub * ctx->k;
     }
     a.t2 = ctx->t2;
     a.K = ctx->deflation ? ctx->K : 0;
@@ -481,11 +545,21 @@ inline ProjArgs proj_args(dfl_ctx *ctx, const double *in, double *out, const KSt
     return a;
 }
 
+// deflation columns per subdomain -> the k_project instance (KZ >= k)
 template <int MODE>
 static void launch_project(dfl_ctx *ctx, const ProjArgs &a) {
-    k_project<MODE><<<(unsigned)ctx->nblk, kBlock, sizeof(double) * std::max<int64_t>(1, a.K), ctx->st>>>(a);
+    const unsigned g = (unsigned)ctx->vgrid;
+    if (!a.azd || a.k <= 1)
+        launch_k(ctx->st, k_project<MODE, 1>, g, kBlock, 0, a);
+    else if (a.k <= 2)
+        launch_k(ctx->st, k_project<MODE, 2>, g, kBlock, 0, a);
+    else if (a.k <= 4)
+        launch_k(ctx->st, k_project<MODE, 4>, g, kBlock, 0, a);
+    else
+        launch_k(ctx->st, k_project<MODE, 8>, g, kBlock, 0, a);
     ctx->launches++;
 }
+
 
 // ctx_layout.cu
 extern double kShortRowPad;
@@ -495,15 +569,34 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
                   bool allow_code = true, bool allow_vcode = false);
 int build_groups(dfl_ctx *ctx);
 int build_tiles(dfl_ctx *ctx);
+// single-rank grid finish of the CG scalars (Fin); nullptr-tick Fin when off
+inline Fin make_fin(dfl_ctx *ctx, int act) {
+    Fin f{};
+    if (multi(ctx) || !ctx->fin_tick || g_no_fin) return f;
+    f.tick = ctx->fin_tick;
+    f.gpart = ctx->fin_gpart;
+    f.st = ctx->state;
+    f.act = act;
+    return f;
+}
+// the operator kernel can finish Z'y -> t (-> t2) itself
+inline bool op_fusable(const dfl_ctx *ctx) {
+    return !multi(ctx) && !ctx->split && !g_use_pipe && ctx->subtab.n > 0 && ctx->fin_tick && !g_no_fin &&
+           (ctx->Aop.fmt == FMT_ELL || ctx->Aop.fmt == FMT_CODE);
+}
+
 // ctx_comm.cu
 int comm_allgather(dfl_ctx *ctx, const double *send, double *recv, size_t count);
 int halo(dfl_ctx *ctx, double *v, cudaStream_t xs = nullptr);
-int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op);
+int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op, bool t_ready = false);
 int rank_scalar(dfl_ctx *ctx, const double *part, int64_t nparts, int slot, const double **gath);
 // ctx_cycle.cu
-int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *dot_part, int64_t *nparts);
+int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *dot_part, int64_t *nparts,
+           const Fin *fin = nullptr, bool *fin_used = nullptr);
+// fin_zt != nullptr: finish Z'y -> t (-> t2) inside the operator kernel when
+// op_fusable(); *fin_zt tells whether it did (then zt_to_t2 is not needed)
 int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double *b, bool zt, const KState *st,
-                 int need_refresh);
+                 int need_refresh, bool *fin_zt = nullptr);
 int project_dev(dfl_ctx *ctx, const double *v, double *out, const KState *st, int dotmode);
 int lift_dev(dfl_ctx *ctx, const dfl_solve_params *p);
 // ctx_cg.cu / ctx_krylov.cu

@@ -17,13 +17,13 @@ static int fetch(dfl_ctx *ctx, const double *dev, int n, double *out) {
 // global value of nq interleaved (stride 3) or plain (nq == 0 -> 1 stream) partials
 static int global_dots(dfl_ctx *ctx, const double *part, int64_t nparts, int nq, bool strided, double *out) {
     if (strided)
-        k_reduceq<<<1, 1024, 0, ctx->st>>>(part, nparts, nq, ctx->scal);
+        launch_k(ctx->st, k_reduceq, 1, 1024, 0, part, nparts, nq, ctx->scal);
     else
-        k_reduce<<<1, 1024, 0, ctx->st>>>(part, nparts, ctx->scal);
+        launch_k(ctx->st, k_reduce, 1, 1024, 0, part, nparts, ctx->scal);
     ctx->launches++;
     if (multi(ctx)) {
         RC(comm_allgather(ctx, ctx->scal, ctx->sgather, 8));
-        k_rank_sum<<<1, 32, 0, ctx->st>>>(ctx->sgather, ctx->nranks, 8, nq, ctx->scal + 8);
+        launch_k(ctx->st, k_rank_sum, 1, 32, 0, ctx->sgather, ctx->nranks, 8, nq, ctx->scal + 8);
         ctx->launches++;
         return fetch(ctx, ctx->scal + 8, nq, out);
     }
@@ -36,7 +36,7 @@ static int dots(dfl_ctx *ctx, int nq, const double *a0, const double *b0, const 
                 const double *a2, const double *b2, double *out, const double *a3 = nullptr,
                 const double *b3 = nullptr) {
     const unsigned g = dot_grid(ctx);
-    k_multidot<<<g, kBlock, 0, ctx->st>>>(a0, b0, a1, b1, a2, b2, a3, b3, nq, ctx->n, ctx->dpart);
+    launch_k(ctx->st, k_multidot, g, kBlock, 0, a0, b0, a1, b1, a2, b2, a3, b3, nq, ctx->n, ctx->dpart);
     ctx->launches++;
     return global_dots(ctx, ctx->dpart, g, nq, true, out);
 }
@@ -47,14 +47,14 @@ static int op_hat(dfl_ctx *ctx, bool defl, const double *v, double *out, const d
     RC(op_apply_dev(ctx, ctx->zx, ctx->w, 0, nullptr, defl, nullptr, 0));
     if (defl) RC(zt_to_t2(ctx, nullptr, 0, true));
     ProjArgs a = proj_args(ctx, ctx->w, out, nullptr);
-    if (!defl) a.az_ptr = nullptr, a.K = 0;
+    if (!defl) a.azd = nullptr, a.K = 0;
     if (dotv) {
         a.dotmode = 1;
         a.dotv = dotv;
         a.dot_part = ctx->dpart;
     }
     launch_project<0>(ctx, a);
-    if (dotv) RC(global_dots(ctx, ctx->dpart, ctx->nblk, 1, false, dot_out));
+    if (dotv) RC(global_dots(ctx, ctx->dpart, ctx->vgrid, 1, false, dot_out));
     return DFL_OK;
 }
 
@@ -83,18 +83,18 @@ int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
     out.bnorm = std::sqrt(std::max(val[0], 0.0));
     const double target = std::max(0.0, p->tol * out.bnorm);  // max(tol*||b'||, atol) with tol = 0
     out.target = target;
-    k_fill<<<nb, kBlock, 0, ctx->st>>>(ctx->bu, 0.0, n);
+    launch_k(ctx->st, k_fill, nb, kBlock, 0, ctx->bu, 0.0, n);
     ctx->launches++;
     if (out.bnorm == 0.0) {
         out.converged = 1;
-        k_fill<<<nb, kBlock, 0, ctx->st>>>(ctx->x, 0.0, n);
+        launch_k(ctx->st, k_fill, nb, kBlock, 0, ctx->x, 0.0, n);
         ctx->launches++;
         return DFL_OK;
     }
     if (defl) {
         RC(project_dev(ctx, ctx->b, ctx->bp, nullptr, 0));
     } else {
-        k_copy<<<nb, kBlock, 0, ctx->st>>>(ctx->bp, ctx->b, n);
+        launch_k(ctx->st, k_copy, nb, kBlock, 0, ctx->bp, ctx->b, n);
         ctx->launches++;
     }
     RC(dots(ctx, 1, ctx->bp, ctx->bp, nullptr, nullptr, nullptr, nullptr, val));
@@ -102,7 +102,7 @@ int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
     const double bpn = std::sqrt(std::max(val[0], 0.0));
     if (bpn == 0.0) {  // bicgstab2 returns zeros (krylov.py:270-272)
         out.converged = 1;
-        k_fill<<<nb, kBlock, 0, ctx->st>>>(ctx->x, 0.0, n);
+        launch_k(ctx->st, k_fill, nb, kBlock, 0, ctx->x, 0.0, n);
         ctx->launches++;
         return DFL_OK;
     }
@@ -110,9 +110,9 @@ int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
     double *d[3] = {ctx->bd[0], ctx->bd[1], ctx->bd[2]};
     double *u = ctx->bu, *shadow = ctx->bshadow;
     const double *r0init = ctx->bp;
-    k_copy<<<nb, kBlock, 0, ctx->st>>>(r[0], r0init, n);
-    k_fill<<<nb, kBlock, 0, ctx->st>>>(d[0], 0.0, n);
-    k_copy<<<nb, kBlock, 0, ctx->st>>>(shadow, r0init, n);
+    launch_k(ctx->st, k_copy, nb, kBlock, 0, r[0], r0init, n);
+    launch_k(ctx->st, k_fill, nb, kBlock, 0, d[0], 0.0, n);
+    launch_k(ctx->st, k_copy, nb, kBlock, 0, shadow, r0init, n);
     ctx->launches += 3;
     double rho0 = 1.0, alpha = 0.0, omega = 1.0;
     bool restarted = false;
@@ -128,8 +128,8 @@ int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
         if (restarted) return code;
         restarted = true;
         // r_shadow = r[0]; d = [0]; rho0, alpha, omega = 1, 0, 1  (krylov.py:165-175)
-        k_copy<<<nb, kBlock, 0, ctx->st>>>(shadow, r[0], n);
-        k_fill<<<nb, kBlock, 0, ctx->st>>>(d[0], 0.0, n);
+        launch_k(ctx->st, k_copy, nb, kBlock, 0, shadow, r[0], n);
+        launch_k(ctx->st, k_fill, nb, kBlock, 0, d[0], 0.0, n);
         ctx->launches += 2;
         rho0 = 1.0;
         alpha = 0.0;
@@ -156,7 +156,7 @@ int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
             }
             const double beta = alpha * rho1 / rho0;
             rho0 = rho1;
-            k_bicg_d<<<nb, kBlock, 0, ctx->st>>>(r[0], d[0], r[1], d[1], j + 1, beta, n);
+            launch_k(ctx->st, k_bicg_d, nb, kBlock, 0, r[0], d[0], r[1], d[1], j + 1, beta, n);
             ctx->launches++;
             double gd;
             RC(op_hat(ctx, defl, d[j], d[j + 1], shadow, &gd));
@@ -166,7 +166,7 @@ int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
                 break;
             }
             alpha = rho0 / gd;
-            k_bicg_r<<<nb, kBlock, 0, ctx->st>>>(r[0], d[1], r[1], d[2], j + 1, u, d[0], alpha, n, ctx->dpart);
+            launch_k(ctx->st, k_bicg_r, nb, kBlock, 0, r[0], d[1], r[1], d[2], j + 1, u, d[0], alpha, n, ctx->dpart);
             ctx->launches++;
             RC(op_hat(ctx, defl, r[j], r[j + 1], nullptr, nullptr));
             if (j == 0) {  // ||r0|| and the next step's rho1 = r1.shadow
@@ -206,7 +206,7 @@ int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
         const double tau12 = mr[2] / sigma1;
         {
             const unsigned g = dot_grid(ctx);
-            k_bicg_mr2<<<g, kBlock, 0, ctx->st>>>(r[2], r[1], r[0], tau12, n, ctx->dpart);
+            launch_k(ctx->st, k_bicg_mr2, g, kBlock, 0, r[2], r[1], r[0], tau12, n, ctx->dpart);
             ctx->launches++;
             RC(global_dots(ctx, ctx->dpart, g, 2, true, val));
         }
@@ -226,14 +226,14 @@ int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
         }
         const double g1 = gp1 - tau12 * g2;
         const double gpp1 = g2 + 0.0;
-        k_bicg_final<<<nb, kBlock, 0, ctx->st>>>(u, r[0], d[0], r[1], r[2], d[1], d[2], g1, gp2, g2, gpp1, gp1, n,
+        launch_k(ctx->st, k_bicg_final, nb, kBlock, 0, u, r[0], d[0], r[1], r[2], d[1], d[2], g1, gp2, g2, gpp1, gp1, n,
                                                  ctx->dpart);
         ctx->launches++;
         if (iters % refresh == 0) {
             // r[0] = r0 - op_hat(u)   (krylov.py:256-257)
             RC(op_hat(ctx, defl, u, ctx->tmp, nullptr, nullptr));
             ProjArgs a = proj_args(ctx, ctx->tmp, r[0], nullptr);
-            a.az_ptr = nullptr;
+            a.azd = nullptr;
             a.K = 0;
             a.base = r0init;
             launch_project<1>(ctx, a);  // r[0] = r0 - tmp
@@ -302,16 +302,16 @@ static int gm_alloc(dfl_ctx *ctx, int restart, bool flexible) {
 static int gm_vdots(dfl_ctx *ctx, int nvec, const double *w, double *dev_out) {
     const unsigned gx = (unsigned)std::min<int64_t>(std::max<int64_t>(1, ctx->nblk), 4 * ctx->sm_count);
     const dim3 grid(gx, (unsigned)cdiv(nvec, kVecGroup));
-    k_vdots<<<grid, kBlock, 0, ctx->st>>>(ctx->gmVp, nvec, w, ctx->n, ctx->gm_part, kGmLd);
+    launch_k(ctx->st, k_vdots, grid, kBlock, 0, ctx->gmVp, nvec, w, ctx->n, ctx->gm_part, kGmLd);
     ctx->launches++;
     if (!multi(ctx)) {
-        k_vreduce<<<nvec, 1024, 0, ctx->st>>>(ctx->gm_part, gx, kGmLd, dev_out);
+        launch_k(ctx->st, k_vreduce, nvec, 1024, 0, ctx->gm_part, gx, kGmLd, dev_out);
         ctx->launches++;
         return DFL_OK;
     }
-    k_vreduce<<<nvec, 1024, 0, ctx->st>>>(ctx->gm_part, gx, kGmLd, ctx->gm_loc);
+    launch_k(ctx->st, k_vreduce, nvec, 1024, 0, ctx->gm_part, gx, kGmLd, ctx->gm_loc);
     RC(comm_allgather(ctx, ctx->gm_loc, ctx->gm_gath, kGmLd));
-    k_rank_sum<<<1, kGmLd, 0, ctx->st>>>(ctx->gm_gath, ctx->nranks, kGmLd, nvec, dev_out);
+    launch_k(ctx->st, k_rank_sum, 1, kGmLd, 0, ctx->gm_gath, ctx->nranks, kGmLd, nvec, dev_out);
     ctx->launches += 2;
     return DFL_OK;
 }
@@ -321,13 +321,13 @@ static int gm_residual(dfl_ctx *ctx, bool defl, double *resnorm) {
     RC(op_apply_dev(ctx, ctx->x, ctx->w, 0, nullptr, defl, nullptr, 0));
     if (defl) RC(zt_to_t2(ctx, nullptr, 0, true));
     ProjArgs a = proj_args(ctx, ctx->w, ctx->r, nullptr);
-    if (!defl) a.az_ptr = nullptr, a.K = 0;
+    if (!defl) a.azd = nullptr, a.K = 0;
     a.base = ctx->bp;
     a.dotmode = 2;
     a.dot_part = ctx->dpart;
     launch_project<1>(ctx, a);
     double v[4];
-    RC(global_dots(ctx, ctx->dpart, ctx->nblk, 1, false, v));
+    RC(global_dots(ctx, ctx->dpart, ctx->vgrid, 1, false, v));
     *resnorm = std::sqrt(std::max(v[0], 0.0));
     return DFL_OK;
 }
@@ -345,7 +345,7 @@ int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KSta
     out.bnorm = std::sqrt(std::max(val[0], 0.0));
     const double target = std::max(0.0, p->tol * out.bnorm);
     out.target = target;
-    k_fill<<<nb, kBlock, 0, ctx->st>>>(ctx->x, 0.0, n);
+    launch_k(ctx->st, k_fill, nb, kBlock, 0, ctx->x, 0.0, n);
     ctx->launches++;
     if (out.bnorm == 0.0) {
         out.converged = 1;
@@ -354,7 +354,7 @@ int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KSta
     if (defl) {
         RC(project_dev(ctx, ctx->b, ctx->bp, nullptr, 0));
     } else {
-        k_copy<<<nb, kBlock, 0, ctx->st>>>(ctx->bp, ctx->b, n);
+        launch_k(ctx->st, k_copy, nb, kBlock, 0, ctx->bp, ctx->b, n);
         ctx->launches++;
     }
     RC(dots(ctx, 1, ctx->bp, ctx->bp, nullptr, nullptr, nullptr, nullptr, val));
@@ -363,7 +363,7 @@ int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KSta
         out.converged = 1;
         return DFL_OK;
     }
-    k_copy<<<nb, kBlock, 0, ctx->st>>>(ctx->r, ctx->bp, n);
+    launch_k(ctx->st, k_copy, nb, kBlock, 0, ctx->r, ctx->bp, n);
     ctx->launches++;
     std::vector<double> H((size_t)(M + 1) * M), g(M + 1), cs(M), sn(M), y(M);
     auto h = [&](int i, int j) -> double & { return H[(size_t)i * M + j]; };
@@ -373,7 +373,7 @@ int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KSta
         std::fill(H.begin(), H.end(), 0.0);
         std::fill(g.begin(), g.end(), 0.0);
         g[0] = resnorm;
-        k_vdiv<<<nb, kBlock, 0, ctx->st>>>(ctx->gmV[0], ctx->r, resnorm, n);  // V0 = r0 / ||r0||
+        launch_k(ctx->st, k_vdiv, nb, kBlock, 0, ctx->gmV[0], ctx->r, resnorm, n);  // V0 = r0 / ||r0||
         ctx->launches++;
         int j = 0;
         while (j < steps) {
@@ -383,7 +383,7 @@ int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KSta
                 RC(op_apply_dev(ctx, ctx->gmZ[j], w, 0, nullptr, defl, nullptr, 0));
                 if (defl) RC(zt_to_t2(ctx, nullptr, 0, true));
                 ProjArgs a = proj_args(ctx, w, w, nullptr);
-                if (!defl) a.az_ptr = nullptr, a.K = 0;
+                if (!defl) a.azd = nullptr, a.K = 0;
                 launch_project<0>(ctx, a);
             } else {  // w = project(A (M V_j))
                 RC(op_hat(ctx, defl, ctx->gmV[j], ctx->tmp, nullptr, nullptr));
@@ -391,9 +391,9 @@ int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KSta
             }
             // two Gram-Schmidt passes against V_0..V_j, then ||w||
             RC(gm_vdots(ctx, j + 1, w, ctx->gm_h));
-            k_vsub<<<gx, kBlock, 0, ctx->st>>>(w, ctx->gmVp, ctx->gm_h, j + 1, n, nullptr);
+            launch_k(ctx->st, k_vsub, gx, kBlock, 0, w, ctx->gmVp, ctx->gm_h, j + 1, n, nullptr);
             RC(gm_vdots(ctx, j + 1, w, ctx->gm_e));
-            k_vsub<<<gx, kBlock, 0, ctx->st>>>(w, ctx->gmVp, ctx->gm_e, j + 1, n, ctx->dpart);
+            launch_k(ctx->st, k_vsub, gx, kBlock, 0, w, ctx->gmVp, ctx->gm_e, j + 1, n, ctx->dpart);
             ctx->launches += 2;
             RC(global_dots(ctx, ctx->dpart, gx, 1, false, val));
             CK(cudaMemcpyAsync(ctx->h_gm, ctx->gm_h, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, ctx->st));
@@ -408,7 +408,7 @@ int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KSta
             h(j + 1, j) = hj1;
             const bool exact = hj1 == 0.0;
             if (!exact) {
-                k_vdiv<<<nb, kBlock, 0, ctx->st>>>(ctx->gmV[j + 1], w, hj1, n);
+                launch_k(ctx->st, k_vdiv, nb, kBlock, 0, ctx->gmV[j + 1], w, hj1, n);
                 ctx->launches++;
             }
             for (int i = 0; i < j; ++i) {
@@ -434,12 +434,12 @@ int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KSta
         }
         CK(cudaMemcpyAsync(ctx->gm_y, y.data(), sizeof(double) * j, cudaMemcpyHostToDevice, ctx->st));
         if (flexible) {  // x = x + (Z_0 y_0 + y_1 Z_1 + ...)
-            k_vcombine<<<gx, kBlock, 0, ctx->st>>>(ctx->x, ctx->x, ctx->gmZp, ctx->gm_y, j, n);
+            launch_k(ctx->st, k_vcombine, gx, kBlock, 0, ctx->x, ctx->x, ctx->gmZp, ctx->gm_y, j, n);
             ctx->launches++;
         } else {  // x = x + M(V_0 y_0 + ...)
-            k_vcombine<<<gx, kBlock, 0, ctx->st>>>(ctx->tmp, nullptr, ctx->gmVp, ctx->gm_y, j, n);
+            launch_k(ctx->st, k_vcombine, gx, kBlock, 0, ctx->tmp, nullptr, ctx->gmVp, ctx->gm_y, j, n);
             RC(vcycle(ctx, ctx->tmp, ctx->zx, nullptr, nullptr, nullptr));
-            k_addv<<<nb, kBlock, 0, ctx->st>>>(ctx->x, ctx->zx, n);
+            launch_k(ctx->st, k_addv, nb, kBlock, 0, ctx->x, ctx->zx, n);
             ctx->launches += 2;
         }
         CK(cudaStreamSynchronize(ctx->st));  // y (host vector) was read by the async copy above

@@ -385,7 +385,7 @@ int build_groups(dfl_ctx *ctx) {
             // tiny levels stay CSR: they run inside the k_tiny_cycle cluster kernel
             const bool tiny = g_use_tiny && fo.back() <= kTinyRows;
             RC(upload_matrix(ctx, A.view(), v.A, {0, A.nrows}, nullptr, !tiny, w.data(), &v.Aw));
-            if (v.A.fmt == FMT_CODE) RC(dalloc(ctx, &v.wr, A.nrows));
+            if (v.A.fmt == FMT_CODE && g_wr_split) RC(dalloc(ctx, &v.wr, A.nrows));
             RC(upload_matrix(ctx, P.view(), v.P, {0, P.nrows}, nullptr, !tiny, nullptr, nullptr, true, true, true));
             RC(upload_matrix(ctx, R.view(), v.R, {0, R.nrows}, nullptr, !tiny, nullptr, nullptr, true, true, true));
             RC(upload(ctx, &v.w, w.data(), (int64_t)w.size()));
@@ -519,9 +519,12 @@ int build_tiles(dfl_ctx *ctx) {
     if (ctx->nsub <= kSubTab) {
         ctx->subtab.n = ctx->nsub;
         ctx->subtab.rows_per_tile = rpt;
+        int64_t gacc = 0;
         for (int s = 0; s <= ctx->nsub; ++s) {
             ctx->subtab.sub_off[s] = ctx->sub_off[s];
             ctx->subtab.tile_start[s] = subt[s];
+            ctx->subtab.group_start[s] = gacc;
+            if (s < ctx->nsub) gacc += cdiv(subt[s + 1] - subt[s], kFinGroup);
         }
     }
     return DFL_OK;

@@ -84,6 +84,22 @@ struct KState {
     double rho0, rho1, omega, gamma_div;
 };
 
+// Programmatic dependent launch: every kernel first waits for the grid it
+// depends on (griddepcontrol.wait: full completion and memory flush of the
+// previous kernel in the stream; a no-op when launched without the PDL
+// attribute), so the launch of a kernel overlaps the drain of the one before
+// it.  With DFL_PDL_TRIGGER=1 kernels also signal launch_dependents at entry
+// (the next grid becomes resident during this one's last wave) -- measured
+// slower for the V-cycle (profiles/r01/README.md), so off by default.
+#ifndef DFL_PDL_TRIGGER
+#define DFL_PDL_TRIGGER 0  // early trigger measured: V-cycle graph 345 vs 324 us
+#endif
+#if DFL_PDL_TRIGGER
+#define DFL_PDL_ENTRY asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
+#else
+#define DFL_PDL_ENTRY asm volatile("griddepcontrol.wait;" ::: "memory")
+#endif
+
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
@@ -347,7 +363,185 @@ __device__ __forceinline__ void block_sum(double (&v)[NV], double *smem /* 32*NV
     }
 }
 
+// Block sum of NV values per thread (NV a power of two <= 32) with a
+// transposing warp butterfly: every halving step exchanges half of the
+// values (NV/2 + NV/4 + ... shuffles instead of 5 NV), then the remaining
+// xor steps reduce one value.  Fixed pattern, hence deterministic.  Returns
+// the block total of value j in thread j (j < NV); other threads get 0.
+template <int NV>
+__device__ __forceinline__ double block_sum_t(double (&v)[NV], double *smem /* 32*NV */) {
+    static_assert(NV >= 1 && NV <= 32 && (NV & (NV - 1)) == 0, "NV must be a power of two");
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int col = 0;
+#pragma unroll
+    for (int st = 0; (NV >> st) > 1; ++st) {
+        const int h = NV >> (st + 1), o = 16 >> st;
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int j = 0; j < h; ++j) {
+            const double send = up ? v[j] : v[j + h];
+            const double keep = up ? v[j + h] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+        if (up) col += h;
+    }
+    constexpr int kRest = 32 / NV;  // lanes that still hold the same column
+#pragma unroll
+    for (int o = kRest / 2; o > 0; o >>= 1) v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+    if ((lane & (kRest - 1)) == 0) smem[warp * NV + col] = v[0];
+    __syncthreads();
+    double tot = 0.0;
+    if ((int)threadIdx.x < NV) {
+        const int nw = blockDim.x >> 5;
+        for (int q = 0; q < nw; ++q) tot += smem[q * NV + threadIdx.x];
+    }
+    return tot;
+}
+
 __device__ __forceinline__ bool skip(const KState *st) { return st != nullptr && st->done; }
+
+// ---------------------------------------------------------------------------
+// Grid finish (single rank): the scalar step that consumes a reduction runs in
+// the last block of the kernel that produced the partials, instead of in a
+// separate single-block launch.  Blocks are grouped in runs of kFinGroup; the
+// last block of a group (atomic ticket) sums the group's partials in index
+// order, the last group sums the group sums in index order -- the result does
+// not depend on which block finishes last (deterministic).
+// tick[0] counts finished groups, tick[1 + g] the blocks of group g; every
+// counter is reset by the block that completes it, so they are zero between
+// launches.
+constexpr int kFinGroup = 64;
+enum { ACT_NONE = 0, ACT_PQ = 1, ACT_RR = 2, ACT_RZ = 3 };
+
+struct Fin {
+    unsigned *tick = nullptr;  // nullptr: plain partials, no finish
+    double *gpart = nullptr;   // one sum per group (x NV)
+    KState *st = nullptr;
+    int act = ACT_NONE;
+    int use_if = 0;            // ACT_PQ: set the refresh IF condition
+    cudaGraphConditionalHandle hif = 0;
+};
+
+// Release / acquire at GPU scope.  The block's partial stores are ordered
+// before thread 0's release by the barrier in front of it (cumulativity), so
+// one thread fences per block, with acq_rel rather than the sequentially
+// consistent fence of __threadfence().
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+// Block b of group g (blocks [gb0, gb0 + gs)) hands in its NV values (thread
+// j < NV holds value j).  Returns true, in every thread of the one block that
+// completes the last group; the group sums are then in gpart[0 .. ng*NV).
+template <int NV>
+__device__ __forceinline__ bool fin_arrive(unsigned *tick, double *part, double *gpart, int64_t b, double v,
+                                           unsigned g, int64_t gb0, unsigned gs, unsigned ng) {
+    __shared__ int s_last;
+    if ((int)threadIdx.x < NV) part[b * NV + threadIdx.x] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        fence_acq_rel_gpu();
+        const bool last = atomicAdd(tick + 1 + g, 1u) == gs - 1;
+        if (last) fence_acq_rel_gpu();
+        s_last = last;
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            double a = lane < (int)gs ? __ldcg(part + (gb0 + lane) * NV + j) : 0.0;
+            if (lane + 32 < (int)gs) a += __ldcg(part + (gb0 + lane + 32) * NV + j);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+            if (lane == 0) gpart[(int64_t)g * NV + j] = a;
+        }
+        if (lane == 0) {
+            tick[1 + g] = 0u;
+            fence_acq_rel_gpu();
+            const bool last = atomicAdd(tick, 1u) == ng - 1;
+            if (last) {
+                tick[0] = 0u;
+                fence_acq_rel_gpu();
+            }
+            s_last = last;
+        }
+    }
+    __syncthreads();
+    return s_last != 0;
+}
+
+// sum of group sums [g0, g1) of value j, fixed order; valid in lane 0 of warp 0
+template <int NV>
+__device__ __forceinline__ double fin_total(const double *gpart, int64_t g0, int64_t g1, int j) {
+    const int lane = threadIdx.x & 31;
+    double a = 0.0;
+    for (int64_t q = g0 + lane; q < g1; q += 32) a += __ldcg(gpart + q * NV + j);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
+    return a;
+}
+
+// the CG scalar steps of krylov.py:119-143 (also used by the single-block
+// kernels of ctx_cg.cu, which call them with the reduced value)
+__device__ __forceinline__ void cg_step_pq(KState *st, double pq) {  // iters += 1; alpha
+    st->iters += 1;
+    st->pq = pq;
+    if (pq <= 0.0 || !isfinite(pq)) {
+        st->breakdown = DFL_BRK_CURVATURE;
+        st->done = 1;
+        return;
+    }
+    st->alpha = st->rz / pq;
+    st->refresh_now = (st->iters % st->refresh_every) == 0;
+}
+__device__ __forceinline__ void cg_step_rr(KState *st, double rr) {  // convergence test
+    st->rr = rr;
+    st->resnorm = sqrt(fmax(rr, 0.0));
+    if (st->resnorm <= st->target) {
+        st->converged = 1;
+        st->done = 1;
+    }
+}
+__device__ __forceinline__ void cg_step_rz(KState *st, double rz) {  // beta
+    if (rz == 0.0 || !isfinite(rz)) {
+        st->breakdown = DFL_BRK_RZ;
+        st->done = 1;
+        return;
+    }
+    st->beta = rz / st->rz;
+    st->rz = rz;
+}
+
+__device__ __forceinline__ void fin_action(const Fin &f, double tot) {
+    KState *st = f.st;
+    if (st->done) return;  // as the single-block kernels: nothing after the loop ended
+    if (f.act == ACT_PQ) {
+        cg_step_pq(st, tot);
+        if (f.use_if) cudaGraphSetConditional(f.hif, (!st->done && st->refresh_now) ? 1u : 0u);
+    } else if (f.act == ACT_RR) {
+        cg_step_rr(st, tot);
+    } else if (f.act == ACT_RZ) {
+        cg_step_rz(st, tot);
+    }
+}
+
+// end of a row / vector kernel with one dot partial per block (block_sum<1>
+// result in thread 0's v): plain partial, or partial + grid finish
+__device__ __forceinline__ void dot_out(const Fin &f, double *part, double v) {
+    if (!f.tick) {
+        if (threadIdx.x == 0) part[blockIdx.x] = v;
+        return;
+    }
+    const unsigned g = blockIdx.x / kFinGroup;
+    const unsigned ng = (gridDim.x + kFinGroup - 1) / kFinGroup;
+    const unsigned gs = min((unsigned)kFinGroup, gridDim.x - g * kFinGroup);
+    if (fin_arrive<1>(f.tick, part, f.gpart, blockIdx.x, v, g, (int64_t)g * kFinGroup, gs, ng)) {
+        if (threadIdx.x < 32) {
+            const double tot = fin_total<1>(f.gpart, 0, ng, 0);
+            if (threadIdx.x == 0) fin_action(f, tot);
+        }
+    }
+}
 
 // ---------------------------------------------------------------------------
 // V-cycle kernels (amg.py:201-212), one per fused stage.
@@ -365,6 +559,7 @@ struct RowArgs {
     double *out;
     double *dot_part;  // POST: per-block r.out partials (nullptr: none)
     const KState *st;
+    Fin fin{};         // POST with dot: grid finish (single rank)
 };
 
 template <int MODE>
@@ -386,6 +581,7 @@ __device__ __forceinline__ double epilogue(const RowArgs &a, int64_t i, double a
 #endif
 template <int MODE, bool DOT, int W>
 __global__ void __launch_bounds__(kBlock, W == 0 ? DFL_ELL_MINB0 : DFL_ELL_MINB) k_ell(DMat A, RowArgs a) {
+    DFL_PDL_ENTRY;
     const int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x;  // storage slot
     double dot = 0.0;
     if (j < A.nrows) {
@@ -403,7 +599,7 @@ __global__ void __launch_bounds__(kBlock, W == 0 ? DFL_ELL_MINB0 : DFL_ELL_MINB)
         __shared__ double sm[32];
         double v[1] = {dot};
         block_sum<1>(v, sm);
-        if (threadIdx.x == 0) a.dot_part[blockIdx.x] = v[0];
+        dot_out(a.fin, a.dot_part, v[0]);
     }
 }
 
@@ -445,6 +641,7 @@ __device__ __forceinline__ double vell_row(const DMat &A, int64_t slot, int W, c
 // value-coded ELL row kernel: grid-stride, value table staged once per block
 template <int MODE, bool DOT>
 __global__ void __launch_bounds__(kBlock) k_vell(DMat A, RowArgs a) {
+    DFL_PDL_ENTRY;
     __shared__ double vt[256];
     for (int t = threadIdx.x; t < A.nvtab; t += blockDim.x) vt[t] = A.vtab[t];
     __syncthreads();
@@ -460,16 +657,18 @@ __global__ void __launch_bounds__(kBlock) k_vell(DMat A, RowArgs a) {
         __shared__ double sm[32];
         double v[1] = {dot};
         block_sum<1>(v, sm);
-        if (threadIdx.x == 0) a.dot_part[blockIdx.x] = v[0];
+        dot_out(a.fin, a.dot_part, v[0]);
     }
 }
 
 // FMT_CODE row kernel, grid-stride (the code table is staged once per block;
 // the next rows' codes are requested before the table load completes).
-// MODE_RESID: a.x holds w .* r (computed by k_wr), so t = r - A (w .* r)
-// keeps the reference's arithmetic exactly.  DOT: one partial per block.
+// MODE_RESID: t = r - A (w .* r) with the products w_j * r_j rounded at the
+// gather (a.x == nullptr) or read from a.x = w .* r (k_wr, DFL_WR_SPLIT=1);
+// either way the reference's arithmetic exactly.  DOT: one partial per block.
 template <int MODE, bool DOT>
 __global__ void __launch_bounds__(kBlock) k_code(DMat A, RowArgs a) {
+    DFL_PDL_ENTRY;
     __shared__ int sd[256];
     __shared__ double sv[256];
     const int64_t stride = (int64_t)gridDim.x * kBlock;
@@ -480,7 +679,8 @@ __global__ void __launch_bounds__(kBlock) k_code(DMat A, RowArgs a) {
     for (; i < A.nrows; i += stride) {
         const int64_t inext = i + stride;
         const uint2 cn = inext < A.nrows ? __ldcs(A.codes + inext) : make_uint2(~0u, ~0u);
-        const double ax = code_row_w(cw, i, GatherX{a.x}, sd, sv);
+        const double ax = (MODE == MODE_RESID && a.x == nullptr) ? code_row_w(cw, i, GatherWR{a.w, a.r}, sd, sv)
+                                                                 : code_row_w(cw, i, GatherX{a.x}, sd, sv);
         const double y = epilogue<MODE>(a, i, ax);
         a.out[i] = y;
         if (DOT) dot += __ldg(a.r + i) * y;
@@ -490,19 +690,21 @@ __global__ void __launch_bounds__(kBlock) k_code(DMat A, RowArgs a) {
         __shared__ double sm[32];
         double v[1] = {dot};
         block_sum<1>(v, sm);
-        if (threadIdx.x == 0) a.dot_part[blockIdx.x] = v[0];
+        dot_out(a.fin, a.dot_part, v[0]);
     }
 }
 
 // wr = w .* r  (the relaxation x = w r of amg.py:193/195, rounded as there)
 static __global__ void __launch_bounds__(kBlock) k_wr(const double *__restrict__ w, const double *__restrict__ r, double *wr,
                                                int64_t n) {
+    DFL_PDL_ENTRY;
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (i < n) wr[i] = mul_rn(w[i], r[i]);
 }
 
 template <int G, int MODE, bool DOT>
 __global__ void __launch_bounds__(kBlock, DFL_CSR_MINB) k_csr(DMat A, RowArgs a) {
+    DFL_PDL_ENTRY;
     constexpr int RPB = kBlock / G;
     const int64_t i = (int64_t)blockIdx.x * RPB + threadIdx.x / G;
     const int sub = threadIdx.x % G;
@@ -521,7 +723,7 @@ __global__ void __launch_bounds__(kBlock, DFL_CSR_MINB) k_csr(DMat A, RowArgs a)
         __shared__ double sm[32];
         double v[1] = {dot};
         block_sum<1>(v, sm);
-        if (threadIdx.x == 0) a.dot_part[blockIdx.x] = v[0];
+        dot_out(a.fin, a.dot_part, v[0]);
     }
 }
 
@@ -532,6 +734,7 @@ __global__ void __launch_bounds__(kBlock, DFL_CSR_MINB) k_csr(DMat A, RowArgs a)
 static __global__ void __launch_bounds__(256) k_bottom(const double *__restrict__ invT, const int64_t *__restrict__ inv_off,
                                                 const int64_t *__restrict__ off, const double *__restrict__ r,
                                                 double *__restrict__ x, const KState *st) {
+    DFL_PDL_ENTRY;
     __shared__ double part[8][33];
     const int s = blockIdx.y;
     const int64_t o = off[s];
@@ -583,25 +786,25 @@ struct SubTable {
     int rows_per_tile = 0;
     int64_t sub_off[kSubTab + 1];
     int64_t tile_start[kSubTab + 1];
+    int64_t group_start[kSubTab + 1];  // grid-finish groups of kFinGroup tiles, per subdomain
 };
 
-__device__ __forceinline__ void tile_rows(const SubTable &S, const Tiles &T, int64_t t, int64_t &r0, int64_t &r1) {
+
+// rows [r0, r1) of tile t; returns its subdomain (S.n > 0) or -1.  The table
+// is a __grid_constant__ kernel parameter, so the (block-uniform) scan reads
+// the constant bank directly; one subdomain -- the common case -- is a
+// straight-line path.
+__device__ __forceinline__ int tile_rows(const SubTable &S, const Tiles &T, int64_t t, int64_t &r0, int64_t &r1) {
     if (S.n > 0) {
-        // unrolled scan with static indices: the table stays in the constant bank
-        int64_t ts = S.tile_start[0], so = S.sub_off[0], se = S.sub_off[1];
-#pragma unroll
-        for (int s = 1; s < kSubTab; ++s)
-            if (s < S.n && S.tile_start[s] <= t) {
-                ts = S.tile_start[s];
-                so = S.sub_off[s];
-                se = S.sub_off[s + 1];
-            }
-        r0 = so + (t - ts) * S.rows_per_tile;
-        r1 = min(r0 + (int64_t)S.rows_per_tile, se);
-    } else {
-        r0 = T.row0[t];
-        r1 = T.row1[t];
+        int s = 0;
+        while (s + 1 < S.n && S.tile_start[s + 1] <= t) ++s;
+        r0 = S.sub_off[s] + (t - S.tile_start[s]) * S.rows_per_tile;
+        r1 = min(r0 + (int64_t)S.rows_per_tile, S.sub_off[s + 1]);
+        return s;
     }
+    r0 = T.row0[t];
+    r1 = T.row1[t];
+    return -1;
 }
 
 struct OpArgs {
@@ -615,11 +818,22 @@ struct OpArgs {
     const KState *st;
     int need_refresh;       // 1: skip unless st->refresh_now
     const uint8_t *skip_rows = nullptr;  // halo overlap: rows with ghost columns are done later
+    // grid finish of Z'y (single rank, SubTable tiles): the last block sums the
+    // tile partials per subdomain into t and, with Einv, solves t2 = E^-1 t
+    unsigned *tick = nullptr;
+    double *gpart = nullptr;
+    double *t = nullptr;
+    const double *Einv = nullptr;
+    double *t2 = nullptr;
+    int64_t K = 0;
+    int64_t first_col = 0;
 };
 
-template <int OPMODE, int NV>
-__device__ __forceinline__ void op_epilogue(const OpArgs &a, int64_t i, bool valid, double y,
-                                            double (&acc)[NV]) {
+// Z'y partials of one tile: thread c < k writes column c (NV >= k, power of two)
+template <int NV>
+__device__ __forceinline__ void op_zt(const OpArgs &a, int64_t i, bool valid, double y, int64_t slot) {
+    __shared__ double sm[32 * NV];
+    double acc[NV];
 #pragma unroll
     for (int c = 0; c < NV; ++c) acc[c] = 0.0;
     if (valid) {
@@ -628,14 +842,56 @@ __device__ __forceinline__ void op_epilogue(const OpArgs &a, int64_t i, bool val
         for (int c = 1; c < NV; ++c)
             if (c < a.k) acc[c] = __ldg(a.zcols + (int64_t)(c - 1) * a.n + i) * y;
     }
+    const double tot = block_sum_t<NV>(acc, sm);
+    if ((int)threadIdx.x < a.k) a.zt_part[slot * a.k + threadIdx.x] = tot;
 }
 
-template <int OPMODE, int W>
-__global__ void __launch_bounds__(kBlock) k_op_ell(DMat A, Tiles T, SubTable S, OpArgs a) {
+// Z'y partials of tile t with the grid finish (OpArgs::tick set): partials
+// at stride NV; the last block writes t and t2 = E^-1 t (deflation.py:230-233)
+template <int NV>
+__device__ __forceinline__ void op_zt_fin(const OpArgs &a, const SubTable &S, int64_t i, bool valid, double y,
+                                          int64_t t, int s) {
+    __shared__ double sm[32 * NV];
+    double acc[NV];
+#pragma unroll
+    for (int c = 0; c < NV; ++c) acc[c] = 0.0;
+    if (valid) {
+        acc[0] = y;
+#pragma unroll
+        for (int c = 1; c < NV; ++c)
+            if (c < a.k) acc[c] = __ldg(a.zcols + (int64_t)(c - 1) * a.n + i) * y;
+    }
+    const double tot = block_sum_t<NV>(acc, sm);
+    const int64_t lt = t - S.tile_start[s];
+    const int64_t ntl = S.tile_start[s + 1] - S.tile_start[s];
+    const unsigned g = (unsigned)(S.group_start[s] + lt / kFinGroup);
+    const int64_t gb0 = S.tile_start[s] + (lt / kFinGroup) * kFinGroup;
+    const unsigned gs = (unsigned)min((int64_t)kFinGroup, ntl - (lt / kFinGroup) * kFinGroup);
+    const unsigned ng = (unsigned)S.group_start[S.n];
+    if (!fin_arrive<NV>(a.tick, a.zt_part, a.gpart, t, tot, g, gb0, gs, ng)) return;
+    if (threadIdx.x < 32) {
+        for (int q = 0; q < S.n * a.k; ++q) {
+            const int sq = q / a.k, c = q % a.k;
+            const double v = fin_total<NV>(a.gpart, S.group_start[sq], S.group_start[sq + 1], c);
+            if (threadIdx.x == 0) a.t[a.first_col + q] = v;
+        }
+    }
+    __syncthreads();
+    if (a.Einv == nullptr) return;
+    for (int64_t r = threadIdx.x; r < a.K; r += blockDim.x) {
+        double acc2 = 0.0;
+        for (int64_t j = 0; j < a.K; ++j) acc2 = fma(a.Einv[r * a.K + j], __ldcg(a.t + j), acc2);
+        a.t2[r] = acc2;
+    }
+}
+
+template <int OPMODE, int W, int NV>
+__global__ void __launch_bounds__(kBlock) k_op_ell(DMat A, Tiles T, const __grid_constant__ SubTable S, OpArgs a) {
+    DFL_PDL_ENTRY;
     if (a.need_refresh && !a.st->refresh_now) return;
     const int64_t t = blockIdx.x;
     int64_t r0, r1;
-    tile_rows(S, T, t, r0, r1);
+    const int sub = tile_rows(S, T, t, r0, r1);
     const int64_t i = r0 + threadIdx.x;
     const bool valid = i < r1 && !(a.skip_rows && a.skip_rows[i]);
     double y = 0.0;
@@ -645,25 +901,22 @@ __global__ void __launch_bounds__(kBlock) k_op_ell(DMat A, Tiles T, SubTable S, 
         a.y[i] = y;
     }
     if (a.k > 0) {
-        __shared__ double sm[32 * kKmax];
-        double acc[kKmax];
-        op_epilogue<OPMODE>(a, i, valid, y, acc);
-        block_sum<kKmax>(acc, sm);
-        if (threadIdx.x == 0)
-            #pragma unroll
-            for (int c = 0; c < kKmax; ++c)
-                if (c < a.k) a.zt_part[t * a.k + c] = acc[c];
+        if (a.tick)
+            op_zt_fin<NV>(a, S, i, valid, y, t, sub);
+        else
+            op_zt<NV>(a, i, valid, y, t);
     }
 }
 
-template <int OPMODE>
-__global__ void __launch_bounds__(kBlock) k_op_code(DMat A, Tiles T, SubTable S, OpArgs a) {
+template <int OPMODE, int NV>
+__global__ void __launch_bounds__(kBlock) k_op_code(DMat A, Tiles T, const __grid_constant__ SubTable S, OpArgs a) {
+    DFL_PDL_ENTRY;
     if (a.need_refresh && !a.st->refresh_now) return;
     __shared__ int sd[256];
     __shared__ double sv[256];
     const int64_t t = blockIdx.x;
     int64_t r0, r1;
-    tile_rows(S, T, t, r0, r1);
+    const int sub = tile_rows(S, T, t, r0, r1);
     const int64_t i = r0 + threadIdx.x;
     const bool valid = i < r1 && !(a.skip_rows && a.skip_rows[i]);
     const uint2 cw = valid ? __ldcs(A.codes + i) : make_uint2(~0u, ~0u);  // in flight during the table load
@@ -675,19 +928,16 @@ __global__ void __launch_bounds__(kBlock) k_op_code(DMat A, Tiles T, SubTable S,
         a.y[i] = y;
     }
     if (a.k > 0) {
-        __shared__ double sm[32 * kKmax];
-        double acc[kKmax];
-        op_epilogue<OPMODE>(a, i, valid, y, acc);
-        block_sum<kKmax>(acc, sm);
-        if (threadIdx.x == 0)
-#pragma unroll
-            for (int c = 0; c < kKmax; ++c)
-                if (c < a.k) a.zt_part[t * a.k + c] = acc[c];
+        if (a.tick)
+            op_zt_fin<NV>(a, S, i, valid, y, t, sub);
+        else
+            op_zt<NV>(a, i, valid, y, t);
     }
 }
 
-template <int G, int OPMODE>
-__global__ void __launch_bounds__(kBlock) k_op_csr(DMat A, Tiles T, SubTable S, OpArgs a) {
+template <int G, int OPMODE, int NV = kKmax>
+__global__ void __launch_bounds__(kBlock) k_op_csr(DMat A, Tiles T, const __grid_constant__ SubTable S, OpArgs a) {
+    DFL_PDL_ENTRY;
     if (a.need_refresh && !a.st->refresh_now) return;
     const int64_t t = blockIdx.x;
     int64_t r0, r1;
@@ -702,16 +952,7 @@ __global__ void __launch_bounds__(kBlock) k_op_csr(DMat A, Tiles T, SubTable S, 
         y = OPMODE == 1 ? sub_rn(__ldg(a.b + i), ax) : ax;
         a.y[i] = y;
     }
-    if (a.k > 0) {
-        __shared__ double sm[32 * kKmax];
-        double acc[kKmax];
-        op_epilogue<OPMODE>(a, i, valid, y, acc);
-        block_sum<kKmax>(acc, sm);
-        if (threadIdx.x == 0)
-            #pragma unroll
-            for (int c = 0; c < kKmax; ++c)
-                if (c < a.k) a.zt_part[t * a.k + c] = acc[c];
-    }
+    if (a.k > 0) op_zt<NV>(a, i, valid, y, t);
 }
 
 // Halo overlap, second pass: the rows with ghost columns (listed in brows,
@@ -722,6 +963,7 @@ template <int OPMODE>
 __global__ void __launch_bounds__(kBlock) k_op_bnd(DMat A, const int *__restrict__ brows,
                                                    const int *__restrict__ bstart, const int *__restrict__ bcnt,
                                                    int64_t toff, OpArgs a) {
+    DFL_PDL_ENTRY;
     if (a.need_refresh && !a.st->refresh_now) return;
     const int64_t bt = blockIdx.x;
     const bool valid = (int)threadIdx.x < bcnt[bt];
@@ -737,22 +979,14 @@ __global__ void __launch_bounds__(kBlock) k_op_bnd(DMat A, const int *__restrict
         y = OPMODE == 1 ? sub_rn(__ldg(a.b + i), ax) : ax;
         a.y[i] = y;
     }
-    if (a.k > 0) {
-        __shared__ double sm[32 * kKmax];
-        double acc[kKmax];
-        op_epilogue<OPMODE>(a, i, valid, y, acc);
-        block_sum<kKmax>(acc, sm);
-        if (threadIdx.x == 0)
-#pragma unroll
-            for (int c = 0; c < kKmax; ++c)
-                if (c < a.k) a.zt_part[(toff + bt) * a.k + c] = acc[c];
-    }
+    if (a.k > 0) op_zt<kKmax>(a, i, valid, y, toff + bt);
 }
 
 // Z' v partials without a product (project(b), coarse_lift(r))
 static __global__ void __launch_bounds__(kBlock) k_zt_vec(Tiles T, const double *__restrict__ v,
                                                    const double *__restrict__ zcols, int64_t n,
                                                    int k, double *zt_part) {
+    DFL_PDL_ENTRY;
     const int64_t t = blockIdx.x;
     const int64_t i = T.row0[t] + threadIdx.x;
     const bool valid = i < T.row1[t];
@@ -784,6 +1018,7 @@ static __global__ void __launch_bounds__(512) k_zt_finish(const double *__restri
                                                    int64_t K, double *t2, const KState *st, int need_refresh,
                                                    unsigned int *ticket, const int64_t *sub_tiles2 = nullptr,
                                                    int64_t toff2 = 0) {
+    DFL_PDL_ENTRY;
     if (skip(st)) return;
     if (need_refresh && !st->refresh_now) return;
     const int v = blockIdx.x;
@@ -822,6 +1057,7 @@ static __global__ void __launch_bounds__(512) k_zt_finish(const double *__restri
 // t2 = E^{-1} t (multi-rank path, after the allgather of t)
 static __global__ void k_esolve(const double *Einv, int64_t K, const double *t, double *t2, const KState *st,
                          int need_refresh) {
+    DFL_PDL_ENTRY;
     if (skip(st)) return;
     if (need_refresh && !st->refresh_now) return;
     for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
@@ -831,20 +1067,23 @@ static __global__ void k_esolve(const double *Einv, int64_t K, const double *t, 
     }
 }
 
-// AZ t2 for one row (AZ is n x K CSR, exact zeros dropped, K tiny): sequential
-// in column order like matvec(AZ, .)
-__device__ __forceinline__ double az_row(const int *__restrict__ ptr, const int *__restrict__ col,
-                                         const double *__restrict__ val, const double *t2s, int64_t i) {
-    double acc = 0.0;
-    const int b = __ldg(ptr + i), e = __ldg(ptr + i + 1);
-    for (int k = b; k < e; ++k) acc = add_rn(acc, mul_rn(__ldg(val + k), t2s[__ldg(col + k)]));
-    return acc;
-}
-
+// AZ storage (deflation.py:140-149): row i of AZ has its entries in the k
+// columns of its own subdomain (always present: a_ii z_i) plus, on rows next
+// to another subdomain, a few in that subdomain's columns.  The own block is
+// stored dense (k x n, column-major, absent entries as 0.0) and the rest as a
+// CSR of "extra" entries (nullptr if there are none).  AZ t2 is summed in
+// column order like matvec(AZ, .): extras left of the own block, the block,
+// extras right of it.  An explicit 0.0 adds +-0 to the running sum, which
+// leaves it unchanged, so the result equals the CSR sum bit for bit.
 struct ProjArgs {
-    const int *az_ptr;
-    const int *az_col;
-    const double *az_val;
+    const double *azd;     // k x n own-block values (nullptr: no deflation term)
+    const int *ax_ptr;     // extras (n + 1 row pointer), nullptr: none
+    const int *ax_col;
+    const double *ax_val;
+    const int64_t *sub_off;  // nsub + 1 local row offsets (device)
+    int nsub;
+    int k;
+    int64_t own_base;      // global coarse column of the rank's first subdomain
     const double *t2;   // K
     int64_t K;
     int64_t n;
@@ -856,31 +1095,64 @@ struct ProjArgs {
     int dotmode;        // 0: none, 1: dot(dotv, out), 2: dot(out, out)
     const KState *st;
     int need_refresh;   // 1: only when refresh_now, 0: always, -1: only when !refresh_now
+    Fin fin;            // dotmode != 0: grid finish (single rank)
 };
 
+// t2 is read through the read-only path (every thread of a subdomain reads the
+// same k values: L1 broadcast), so no shared-memory staging and no barrier
+// stands in front of the streaming loads
+template <int KZ>
+__device__ __forceinline__ double az_row(const ProjArgs &a, int64_t i) {
+    double v[KZ];
+#pragma unroll
+    for (int c = 0; c < KZ; ++c)
+        if (c < a.k) v[c] = __ldcs(a.azd + (int64_t)c * a.n + i);
+    int s = 0;
+    if (a.nsub > 1) {  // subdomain of row i: last s with sub_off[s] <= i
+        int lo = 0, hi = a.nsub - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(a.sub_off + mid) <= i) lo = mid; else hi = mid - 1;
+        }
+        s = lo;
+    }
+    const double *t2o = a.t2 + a.own_base + (int64_t)s * a.k;
+    const int64_t own0 = a.own_base + (int64_t)s * a.k;
+    double acc = 0.0;
+    int e = 0, e1 = 0;
+    if (a.ax_ptr) {
+        e = __ldg(a.ax_ptr + i);
+        e1 = __ldg(a.ax_ptr + i + 1);
+        for (; e < e1 && __ldg(a.ax_col + e) < own0; ++e)
+            acc = add_rn(acc, mul_rn(__ldg(a.ax_val + e), __ldg(a.t2 + __ldg(a.ax_col + e))));
+    }
+#pragma unroll
+    for (int c = 0; c < KZ; ++c)
+        if (c < a.k) acc = add_rn(acc, mul_rn(v[c], __ldg(t2o + c)));
+    for (; e < e1; ++e) acc = add_rn(acc, mul_rn(__ldg(a.ax_val + e), __ldg(a.t2 + __ldg(a.ax_col + e))));
+    return acc;
+}
+
 // q = w - AZ t2 (+ dot partial p.q);  refresh variant: r = b' - (w - AZ t2) (+ r.r)
-template <int MODE>
+template <int MODE, int KZ>
 __global__ void __launch_bounds__(kBlock) k_project(ProjArgs a) {
+    DFL_PDL_ENTRY;
     if (skip(a.st)) return;
     if (a.need_refresh == 1 && !a.st->refresh_now) return;
-    extern __shared__ double t2s[];
-    for (int64_t j = threadIdx.x; j < a.K; j += blockDim.x) t2s[j] = a.t2[j];
-    __syncthreads();
-    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    double dot = 0.0;
-    if (i < a.n) {
+    double dot = 0.0;  // grid-stride (grid = ctx->vgrid): one partial per block
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * kBlock) {
         double q = a.in[i];
-        if (a.az_ptr) q = sub_rn(q, az_row(a.az_ptr, a.az_col, a.az_val, t2s, i));
+        if (a.azd) q = sub_rn(q, az_row<KZ>(a, i));
         if (MODE == 1) q = sub_rn(__ldg(a.base + i), q);
         a.out[i] = q;
-        if (a.dotmode == 1) dot = __ldg(a.dotv + i) * q;
-        if (a.dotmode == 2) dot = q * q;
+        if (a.dotmode == 1) dot += __ldg(a.dotv + i) * q;
+        if (a.dotmode == 2) dot += q * q;
     }
     if (a.dotmode != 0) {
         __shared__ double sm[32];
         double v[1] = {dot};
         block_sum<1>(v, sm);
-        if (threadIdx.x == 0) a.dot_part[blockIdx.x] = v[0];
+        dot_out(a.fin, a.dot_part, v[0]);
     }
 }
 
@@ -890,6 +1162,7 @@ static __global__ void __launch_bounds__(kBlock) k_lift(Tiles T, const int *tile
                                                  const double *__restrict__ zcols, int64_t n, int k,
                                                  const double *__restrict__ t2, int64_t first_col,
                                                  double *out, int add_y) {
+    DFL_PDL_ENTRY;
     const int64_t t = blockIdx.x;
     const int64_t i = T.row0[t] + threadIdx.x;
     if (i >= T.row1[t]) return;
@@ -904,6 +1177,7 @@ static __global__ void __launch_bounds__(kBlock) k_lift(Tiles T, const int *tile
 
 static __global__ void __launch_bounds__(kBlock) k_dot(const double *__restrict__ a, const double *__restrict__ b,
                                                 int64_t n, double *part, const KState *st) {
+    DFL_PDL_ENTRY;
     if (skip(st)) return;
     double acc = 0.0;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
@@ -949,6 +1223,7 @@ __device__ __forceinline__ double reduce_parts_strided(const double *part, int64
 }
 
 static __global__ void k_reduce(const double *part, int64_t nparts, double *out) {
+    DFL_PDL_ENTRY;
     const double s = reduce_parts(part, nparts);
     if (threadIdx.x == 0) *out = s;
 }
@@ -957,56 +1232,70 @@ static __global__ void k_reduce(const double *part, int64_t nparts, double *out)
 // On refresh iterations only x is updated here (r comes from the refresh path).
 static __global__ void __launch_bounds__(kBlock) k_cg_update(double *x, double *r, const double *__restrict__ p,
                                                       const double *__restrict__ q, int64_t n, double *part,
-                                                      const KState *st) {
+                                                      const KState *st, Fin fin) {
+    DFL_PDL_ENTRY;
     if (skip(st)) return;
     const double alpha = st->alpha;
     const bool refresh = st->refresh_now;
-    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    double dot = 0.0;
-    if (i < n) {
+    double dot = 0.0;  // grid-stride (grid = ctx->vgrid)
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
         const double pi = p[i];
         x[i] = add_rn(x[i], mul_rn(alpha, pi));
         if (!refresh) {
             const double ri = sub_rn(r[i], mul_rn(alpha, q[i]));
             r[i] = ri;
-            dot = ri * ri;
+            dot += ri * ri;
         }
     }
     if (!refresh) {
         __shared__ double sm[32];
         double v[1] = {dot};
         block_sum<1>(v, sm);
-        if (threadIdx.x == 0) part[blockIdx.x] = v[0];
+        dot_out(fin, part, v[0]);
     }
 }
 
-// p = z + beta p (krylov.py:142)
+// p = z + beta p (krylov.py:142).  With a graph handle, block 0 also ends the
+// iteration (maxiter test, while condition) and clears the refresh IF
+// condition for the next iteration.
 static __global__ void __launch_bounds__(kBlock) k_cg_p(double *p, const double *__restrict__ z, int64_t n,
-                                                 const KState *st) {
+                                                 KState *st, int use_cond, cudaGraphConditionalHandle h,
+                                                 int use_if, cudaGraphConditionalHandle hif) {
+    DFL_PDL_ENTRY;
+    if (use_cond && blockIdx.x == 0 && threadIdx.x == 0) {
+        const bool done = st->done || st->iters >= st->maxiter;
+        if (done && !st->done) st->done = 1;  // maxiter: the loop ends, p is not needed
+        cudaGraphSetConditional(h, done ? 0u : 1u);
+        if (use_if) cudaGraphSetConditional(hif, 0u);
+    }
     if (skip(st)) return;
     const double beta = st->beta;
-    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    if (i < n) p[i] = add_rn(z[i], mul_rn(beta, p[i]));
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock)
+        p[i] = add_rn(z[i], mul_rn(beta, p[i]));
 }
 
 static __global__ void k_copy(double *dst, const double *src, int64_t n) {
+    DFL_PDL_ENTRY;
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (i < n) dst[i] = src[i];
 }
 
 static __global__ void k_fill(double *dst, double v, int64_t n) {
+    DFL_PDL_ENTRY;
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (i < n) dst[i] = v;
 }
 
 // halo: pack own values to send, in neighbour order
 static __global__ void k_gather(const double *__restrict__ src, const int *__restrict__ idx, int64_t m, double *dst) {
+    DFL_PDL_ENTRY;
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (i < m) dst[i] = src[idx[i]];
 }
 
 // sum rank-gathered scalars in rank order: out[v] = sum_q g[q*stride + v]
 static __global__ void k_rank_sum(const double *g, int nranks, int stride, int nv, double *out) {
+    DFL_PDL_ENTRY;
     const int v = threadIdx.x;
     if (v >= nv) return;
     double acc = 0.0;
@@ -1029,6 +1318,7 @@ static __global__ void __launch_bounds__(kBlock) k_multidot(const double *__rest
                                                      const double *__restrict__ a2, const double *__restrict__ b2,
                                                      const double *__restrict__ a3, const double *__restrict__ b3,
                                                      int nq, int64_t n, double *part) {
+    DFL_PDL_ENTRY;
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
         acc[0] += a0[i] * b0[i];
@@ -1044,6 +1334,7 @@ static __global__ void __launch_bounds__(kBlock) k_multidot(const double *__rest
 
 // reduce nq interleaved partial streams (stride kDotStride) -> out[0..nq)
 static __global__ void k_reduceq(const double *part, int64_t nparts, int nq, double *out) {
+    DFL_PDL_ENTRY;
     __shared__ double sm[32 * 4];
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
     for (int64_t j = threadIdx.x; j < nparts; j += blockDim.x)
@@ -1057,6 +1348,7 @@ static __global__ void k_reduceq(const double *part, int64_t nparts, int nq, dou
 static __global__ void __launch_bounds__(kBlock) k_bicg_d(const double *__restrict__ r0, double *d0,
                                                    const double *__restrict__ r1, double *d1, int cnt, double beta,
                                                    int64_t n) {
+    DFL_PDL_ENTRY;
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (i >= n) return;
     d0[i] = sub_rn(r0[i], mul_rn(beta, d0[i]));
@@ -1069,6 +1361,7 @@ static __global__ void __launch_bounds__(kBlock) k_bicg_r(double *r0, const doub
                                                    const double *__restrict__ d2, int cnt, double *u,
                                                    const double *__restrict__ d0, double alpha, int64_t n,
                                                    double *part) {
+    DFL_PDL_ENTRY;
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     double dot = 0.0;
     if (i < n) {
@@ -1088,6 +1381,7 @@ static __global__ void __launch_bounds__(kBlock) k_bicg_r(double *r0, const doub
 static __global__ void __launch_bounds__(kBlock) k_bicg_mr2(double *r2, const double *__restrict__ r1,
                                                      const double *__restrict__ r0, double tau12, int64_t n,
                                                      double *part) {
+    DFL_PDL_ENTRY;
     double acc[3] = {0.0, 0.0, 0.0};
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kBlock) {
         const double v = sub_rn(r2[i], mul_rn(tau12, r1[i]));
@@ -1109,6 +1403,7 @@ static __global__ void __launch_bounds__(kBlock) k_bicg_final(double *u, double 
                                                        const double *__restrict__ d1, const double *__restrict__ d2,
                                                        double g1, double gp2, double g2, double gpp1, double gp1,
                                                        int64_t n, double *part) {
+    DFL_PDL_ENTRY;
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     double dot = 0.0;
     if (i < n) {
@@ -1144,6 +1439,7 @@ constexpr int kVecGroup = 8;  // basis vectors per block of k_vdots
 // part[bx * ld + i] = sum over the block's rows of V_i . w, i in [8*by, 8*by+8)
 static __global__ void __launch_bounds__(kBlock) k_vdots(const double *const *__restrict__ V, int nvec,
                                                   const double *__restrict__ w, int64_t n, double *part, int ld) {
+    DFL_PDL_ENTRY;
     const int i0 = blockIdx.y * kVecGroup;
     double acc[kVecGroup];
 #pragma unroll
@@ -1164,6 +1460,7 @@ static __global__ void __launch_bounds__(kBlock) k_vdots(const double *const *__
 
 // out[i] = sum_bx part[bx * ld + i]   (one block per i)
 static __global__ void k_vreduce(const double *part, int64_t nbx, int ld, double *out) {
+    DFL_PDL_ENTRY;
     const double s = reduce_parts_strided(part + blockIdx.x, nbx, ld);
     if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
@@ -1172,6 +1469,7 @@ static __global__ void k_vreduce(const double *part, int64_t nbx, int ld, double
 // optional partial of w.w after the update
 static __global__ void __launch_bounds__(kBlock) k_vsub(double *w, const double *const *__restrict__ V, const double *h,
                                                  int nvec, int64_t n, double *part) {
+    DFL_PDL_ENTRY;
     double dot = 0.0;
     for (int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x; e < n; e += (int64_t)gridDim.x * kBlock) {
         double we = w[e];
@@ -1191,6 +1489,7 @@ static __global__ void __launch_bounds__(kBlock) k_vsub(double *w, const double 
 // (krylov.py:355-363, then x = x + update :407)
 static __global__ void __launch_bounds__(kBlock) k_vcombine(double *out, const double *x, const double *const *__restrict__ V,
                                                      const double *y, int nvec, int64_t n) {
+    DFL_PDL_ENTRY;
     for (int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x; e < n; e += (int64_t)gridDim.x * kBlock) {
         double u = mul_rn(V[0][e], y[0]);
         for (int i = 1; i < nvec; ++i) u = add_rn(u, mul_rn(y[i], V[i][e]));
@@ -1200,12 +1499,14 @@ static __global__ void __launch_bounds__(kBlock) k_vcombine(double *out, const d
 
 // x = x + u
 static __global__ void __launch_bounds__(kBlock) k_addv(double *x, const double *__restrict__ u, int64_t n) {
+    DFL_PDL_ENTRY;
     const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (e < n) x[e] = add_rn(x[e], u[e]);
 }
 
 // out = in / s   (V_{j+1} = w / h_{j+1,j}, V_0 = r / ||r||)
 static __global__ void __launch_bounds__(kBlock) k_vdiv(double *out, const double *in, double s, int64_t n) {
+    DFL_PDL_ENTRY;
     const int64_t e = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (e < n) out[e] = __ddiv_rn(in[e], s);
 }
@@ -1234,6 +1535,7 @@ __device__ __forceinline__ double blk_dot(const double *a, const double *b, int 
 
 static __global__ void __launch_bounds__(256) k_egmres(const double *__restrict__ E, int K, const double *t, double *y,
                                                 double tol, double *scr, const KState *st, int need_refresh) {
+    DFL_PDL_ENTRY;
     if (skip(st)) return;
     if (need_refresh && !st->refresh_now) return;
     __shared__ double sm[32];
