@@ -18,6 +18,8 @@ bool g_use_coarse = false;  // cooperative coarse-cycle kernel (DFL_COARSE=1; me
 bool g_allow_sell = false;    // DFL_SELL=1: SELL-C-sigma for every irregular matrix
 bool g_wr_split = false;      // DFL_WR_SPLIT=1: coded residual reads w .* r from a k_wr pass
 bool g_no_fin = true;         // DFL_FIN=1: CG scalars finished in the producing kernels (measured slower)
+bool g_use_class = true;      // DFL_NO_CLASS=1: no row-class coded matrices
+bool g_code_pipe = true;      // DFL_CODE_PIPE=0: coded rows without the software pipeline
 bool g_pdl = true;            // DFL_NO_PDL=1: plain launches instead of programmatic dependent launch
 int g_csr_g = 0;              // DFL_CSR_G=n forces the CSR lanes per row
 double g_csr_per_lane = 12.0; // DFL_CSR_PER_LANE: target entries per lane
@@ -117,6 +119,10 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
         g_wr_split = ws && ws[0] == '1';
         const char *nf = getenv("DFL_FIN");
         g_no_fin = !(nf && nf[0] == '1');
+        const char *ncl = getenv("DFL_NO_CLASS");
+        g_use_class = !(ncl && ncl[0] == '1');
+        const char *cp = getenv("DFL_CODE_PIPE");
+        g_code_pipe = !(cp && cp[0] == '0');
         const char *np2 = getenv("DFL_NO_PDL");
         g_pdl = !(np2 && np2[0] == '1');
         const char *cg = getenv("DFL_CSR_G");
@@ -180,9 +186,15 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
     ctx->nsub = nsub;
     ctx->sub_off.assign(sub_offsets, sub_offsets + nsub + 1);
     HostRows h{A->nrows, A->ncols, A->row_ptr, A->col_idx, A->values};
-    // the operator stays uniform ELL (at the HBM roofline, 99.9%); FMT_CODE only
-    // pays off for the V-cycle kernels with longer epilogues (profiles/r01)
-    RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, &ctx->op_sub_tiles_h, true, nullptr, nullptr, false, false));
+    // the operator: row-class coded when it has few distinct rows (structured
+    // grids; 1 byte per row instead of 12 per entry), else uniform ELL (at the
+    // HBM roofline); FMT_CODE only pays off for the V-cycle kernels with longer
+    // epilogues (profiles/r01).  The halo-overlapped boundary pass (k_op_bnd)
+    // reads ELL / CSR, so a rank with ghost columns keeps those.
+    const char *no_ov = getenv("DFL_NO_OVERLAP");
+    const bool will_split = multi(ctx) && A->ncols > A->nrows && !(no_ov && no_ov[0] == '1');
+    RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, &ctx->op_sub_tiles_h, true, nullptr, nullptr, false, false,
+                     false, !will_split));
     if (ctx->Aop.pipe.stages) RC(upload(ctx, &ctx->op_sub_tiles, ctx->op_sub_tiles_h.data(), (int64_t)ctx->op_sub_tiles_h.size()));
     ctx->op_nnz = ctx->Aop.nnz;
     int64_t nrecv = 0;

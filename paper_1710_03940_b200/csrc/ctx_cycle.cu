@@ -23,9 +23,9 @@ int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *d
             DLevel &v = g.lv[l];
             const double *in = l == 0 ? rin : v.rv;
             double *next = (l + 1 < L) ? g.lv[l + 1].rv : g.rb;
-            if (v.A.fmt == FMT_CODE) {
+            if (v.A.fmt == FMT_CODE || v.A.fmt == FMT_CLASS) {
                 const double *wr = nullptr;  // w .* r formed at the gather
-                if (g_wr_split) {
+                if (g_wr_split && v.A.fmt == FMT_CODE) {
                     launch_k(ctx->st, k_wr, (unsigned)cdiv(v.n, kBlock), kBlock, 0, v.w, in, v.wr, v.n);
                     ctx->launches++;
                     wr = v.wr;
@@ -228,6 +228,7 @@ int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
     auto mat = [](const DMat &M) -> double {
         const double rows = (double)M.nrows;
         if (M.fmt == FMT_CODE) return 8.0 * rows;
+        if (M.fmt == FMT_CLASS) return 1.0 * rows;
         if (M.fmt == FMT_CSR) return 12.0 * (double)M.nnz + 4.0 * (rows + 1);
         return (M.vcode ? 5.0 : 12.0) * (double)M.stored + (M.perm ? 4.0 * rows : 0.0) +
                (M.ell_w ? 0.0 : 8.0 * (rows / 32 + 1));
@@ -244,7 +245,7 @@ int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
             for (size_t l = 0; l < g.lv.size(); ++l) {
                 const DLevel &v = g.lv[l];
                 const double n = (double)g.rows[l], nc = (double)g.rows[l + 1];
-                b += v.A.fmt == FMT_CODE ? 24.0 * n + mat(v.A) + 24.0 * n : mat(v.Aw) + 24.0 * n;  // residual
+                b += (v.A.fmt == FMT_CODE || v.A.fmt == FMT_CLASS) ? 24.0 * n + mat(v.A) + 24.0 * n : mat(v.Aw) + 24.0 * n;  // residual
                 b += mat(v.R) + 8.0 * n + 8.0 * nc;                                                // restriction
                 b += mat(v.P) + 8.0 * nc + 24.0 * n;                                               // prolongation
                 b += mat(v.A) + 40.0 * n;                                                          // post-smoothing

@@ -72,7 +72,7 @@ struct Nccl {
 extern Nccl g_nccl;
 
 // profiling / layout knobs (defined in ctx.cu, read at context creation)
-extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl;
+extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl, g_code_pipe, g_use_class;
 extern double g_small_per_lane, g_csr_per_lane;
 extern int g_csr_g, g_sm_count;
 static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle
@@ -195,6 +195,7 @@ struct dfl_ctx {
     double *ax_val = nullptr;
     int64_t az_nnz = 0, ax_nnz = 0;
     int64_t *sub_off_d = nullptr;           // nsub + 1 local row offsets
+    std::vector<std::unique_ptr<ClassTab>> class_tabs;  // FMT_CLASS tables (DMat::class_id)
     double *Einv = nullptr;
     // inexact coarse solve (deflation.py:166-178): inner GMRES on E
     bool inexact = false;
@@ -344,14 +345,21 @@ inline int occupancy(K kernel) {
 // grid of the grid-stride FMT_CODE / VELL kernels: one wave of the instance
 template <int MODE, bool DOT>
 inline int64_t code_grid(const DMat &A) {
-    static const int occ_code = occupancy(k_code<MODE, DOT>);
+    static const int occ_code = g_code_pipe ? occupancy(k_codep<MODE, DOT>) : occupancy(k_code<MODE, DOT>);
     static const int occ_vell = occupancy(k_vell<MODE, DOT>);
     const int occ = A.vcode ? occ_vell : occ_code;
     return std::max<int64_t>(1, std::min<int64_t>(cdiv(A.nrows, kBlock), (int64_t)occ * g_sm_count));
 }
 
+template <int MODE, bool DOT>
+inline int64_t class_grid(const DMat &A) {
+    static const int occ = occupancy(k_class<MODE, DOT>);
+    return std::max<int64_t>(1, std::min<int64_t>(cdiv(A.nrows, kBlock), (int64_t)occ * g_sm_count));
+}
+
 // number of per-block / per-tile partials the POST-with-dot kernel on A produces
 inline int64_t parts_for(const DMat &A) {
+    if (A.fmt == FMT_CLASS) return class_grid<MODE_POST, true>(A);
     if (A.fmt == FMT_CODE || A.vcode) return code_grid<MODE_POST, true>(A);
     return A.pipe.stages ? A.pipe.ntiles : nblocks_for(A);
 }
@@ -421,8 +429,17 @@ static void launch_csr_mode(const DMat &A, const RowArgs &a, cudaStream_t st) {
 template <int MODE, bool DOT>
 static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
     if (A.nrows == 0) return;
+    if (A.fmt == FMT_CLASS) {
+        launch_k(ctx->st, k_class<MODE, DOT>, (unsigned)class_grid<MODE, DOT>(A), kBlock, 0, A, a,
+                 *ctx->class_tabs[A.class_id]);
+        ctx->launches++;
+        return;
+    }
     if (A.fmt == FMT_CODE) {
-        launch_k(ctx->st, k_code<MODE, DOT>, (unsigned)code_grid<MODE, DOT>(A), kBlock, 0, A, a);
+        if (g_code_pipe)
+            launch_k(ctx->st, k_codep<MODE, DOT>, (unsigned)code_grid<MODE, DOT>(A), kBlock, 0, A, a);
+        else
+            launch_k(ctx->st, k_code<MODE, DOT>, (unsigned)code_grid<MODE, DOT>(A), kBlock, 0, A, a);
         ctx->launches++;
         return;
     }
@@ -466,6 +483,10 @@ template <int OPMODE, int NV>
 static void launch_op_nv(dfl_ctx *ctx, const OpArgs &a, unsigned grid) {
     const DMat &A = ctx->Aop;
     const SubTable &S = ctx->subtab;
+    if (A.fmt == FMT_CLASS) {
+        launch_k(ctx->st, k_op_class<OPMODE, NV>, grid, kBlock, 0, A, ctx->tiles, S, a, *ctx->class_tabs[A.class_id]);
+        return;
+    }
     if (A.fmt == FMT_CODE) {
         launch_k(ctx->st, k_op_code<OPMODE, NV>, grid, kBlock, 0, A, ctx->tiles, S, a);
         return;
@@ -496,7 +517,7 @@ static void launch_op(dfl_ctx *ctx, const OpArgs &a) {
     }
     const unsigned grid = (unsigned)ctx->ntiles;
     if (grid == 0) return;
-    if (A.fmt == FMT_CODE || A.fmt == FMT_ELL) {
+    if (A.fmt == FMT_CODE || A.fmt == FMT_ELL || A.fmt == FMT_CLASS) {
         // Z'y epilogue width: the smallest power of two >= k
         if (a.k <= 1)
             launch_op_nv<OPMODE, 1>(ctx, a, grid);
@@ -566,7 +587,7 @@ extern double kShortRowPad;
 int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &bounds,
                   std::vector<int64_t> *bound_tiles = nullptr, bool allow_ell = true,
                   const double *colscale = nullptr, DMat *scaled = nullptr, bool allow_sell = true,
-                  bool allow_code = true, bool allow_vcode = false);
+                  bool allow_code = true, bool allow_vcode = false, bool allow_class = true);
 int build_groups(dfl_ctx *ctx);
 int build_tiles(dfl_ctx *ctx);
 // single-rank grid finish of the CG scalars (Fin); nullptr-tick Fin when off
@@ -582,7 +603,7 @@ inline Fin make_fin(dfl_ctx *ctx, int act) {
 // the operator kernel can finish Z'y -> t (-> t2) itself
 inline bool op_fusable(const dfl_ctx *ctx) {
     return !multi(ctx) && !ctx->split && !g_use_pipe && ctx->subtab.n > 0 && ctx->fin_tick && !g_no_fin &&
-           (ctx->Aop.fmt == FMT_ELL || ctx->Aop.fmt == FMT_CODE);
+           (ctx->Aop.fmt == FMT_ELL || ctx->Aop.fmt == FMT_CODE || ctx->Aop.fmt == FMT_CLASS);
 }
 
 // ctx_comm.cu

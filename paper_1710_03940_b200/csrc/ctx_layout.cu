@@ -48,6 +48,8 @@ static int try_upload_code(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) {
     m.fmt = FMT_CODE;
     m.stored = m.nnz;
     m.ncodes = (int)delta.size();
+    m.code_lead = 0;
+    for (int d : delta) m.code_lead = std::max(m.code_lead, d);
     uint8_t *d_codes;
     int *d_delta;
     double *d_val;
@@ -57,6 +59,74 @@ static int try_upload_code(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) {
     m.codes = reinterpret_cast<const uint2 *>(d_codes);
     m.ctab_delta = d_delta;
     m.ctab_val = d_val;
+    ok = true;
+    return DFL_OK;
+}
+
+// FMT_CLASS encoder (kernels.cuh ClassTab): rows of <= 8 entries, <= kMaxClass
+// distinct rows (ordered (column - row, value bits) lists).  ok = false leaves
+// m untouched for the next format.
+static int try_upload_class(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) {
+    ok = false;
+    struct Row {
+        int len = 0;
+        int d[8];
+        uint64_t v[8];
+        bool operator==(const Row &o) const {
+            if (len != o.len) return false;
+            for (int k = 0; k < len; ++k)
+                if (d[k] != o.d[k] || v[k] != o.v[k]) return false;
+            return true;
+        }
+    };
+    struct RH {
+        size_t operator()(const Row &r) const {
+            uint64_t x = (uint64_t)r.len * 0x9e3779b97f4a7c15ull;
+            for (int k = 0; k < r.len; ++k) x = (x ^ ((uint64_t)(uint32_t)r.d[k] * 0x100000001b3ull) ^ r.v[k]) * 0xff51afd7ed558ccdull;
+            return (size_t)x;
+        }
+    };
+    std::unordered_map<Row, int, RH> dict;
+    std::vector<Row> rows;
+    std::vector<uint8_t> cls((size_t)h.nrows);
+    for (int64_t i = 0; i < h.nrows; ++i) {
+        const int64_t b = h.ptr[i], e = h.ptr[i + 1];
+        if (e - b > 8) return DFL_OK;
+        Row r;
+        r.len = (int)(e - b);
+        for (int64_t k = b; k < e; ++k) {
+            const int64_t d = h.col[k] - i;
+            if (d < INT32_MIN || d > INT32_MAX) return DFL_OK;
+            r.d[k - b] = (int)d;
+            std::memcpy(&r.v[k - b], &h.val[k], 8);
+        }
+        auto it = dict.find(r);
+        if (it == dict.end()) {
+            if ((int)rows.size() >= kMaxClass) return DFL_OK;
+            it = dict.emplace(r, (int)rows.size()).first;
+            rows.push_back(r);
+        }
+        cls[(size_t)i] = (uint8_t)it->second;
+    }
+    auto tab = std::make_unique<ClassTab>();
+    std::memset(tab.get(), 0, sizeof(ClassTab));
+    tab->n = (int)rows.size();
+    tab->lead = 0;
+    for (int c = 0; c < tab->n; ++c) {
+        tab->len[c] = rows[c].len;
+        for (int k = 0; k < rows[c].len; ++k) {
+            tab->delta[c][k] = rows[c].d[k];
+            std::memcpy(&tab->val[c][k], &rows[c].v[k], 8);
+            tab->lead = std::max(tab->lead, rows[c].d[k]);
+        }
+    }
+    uint8_t *d_cls;
+    RC(upload(ctx, &d_cls, cls.data(), std::max<int64_t>(1, h.nrows)));
+    m.fmt = FMT_CLASS;
+    m.stored = m.nnz;
+    m.cls = d_cls;
+    m.class_id = (int)ctx->class_tabs.size();
+    ctx->class_tabs.push_back(std::move(tab));
     ok = true;
     return DFL_OK;
 }
@@ -98,7 +168,7 @@ double kShortRowPad = 1.7;
 
 int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &bounds,
                   std::vector<int64_t> *bound_tiles, bool allow_ell, const double *colscale, DMat *scaled,
-                  bool allow_sell, bool allow_code, bool allow_vcode) {
+                  bool allow_sell, bool allow_code, bool allow_vcode, bool allow_class) {
     m = DMat{};
     m.nrows = h.nrows;
     m.ncols = h.ncols;
@@ -106,6 +176,14 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
     if (h.ncols >= INT32_MAX || m.nnz >= INT32_MAX) {
         ctx->err = "matrix too large for int32 device indices";
         return DFL_E_DIMENSION;
+    }
+    if (g_use_class && allow_class && allow_ell && h.nrows > 0) {
+        bool ok = false;
+        RC(try_upload_class(ctx, h, m, ok));
+        if (ok) {
+            if (colscale) *scaled = m;  // RESID on a class-coded matrix gathers w .* r
+            return DFL_OK;
+        }
     }
     if (g_use_code && allow_code && allow_ell && h.nrows > 0) {
         bool ok = false;
@@ -384,7 +462,8 @@ int build_groups(dfl_ctx *ctx) {
             OwnedRows A = merge_blocks(As, fo), P = merge_blocks(Ps, co), R = merge_blocks(Rs, fo);
             // tiny levels stay CSR: they run inside the k_tiny_cycle cluster kernel
             const bool tiny = g_use_tiny && fo.back() <= kTinyRows;
-            RC(upload_matrix(ctx, A.view(), v.A, {0, A.nrows}, nullptr, !tiny, w.data(), &v.Aw));
+            RC(upload_matrix(ctx, A.view(), v.A, {0, A.nrows}, nullptr, !tiny, w.data(), &v.Aw, true, true, false,
+                             !g_use_coarse));
             if (v.A.fmt == FMT_CODE && g_wr_split) RC(dalloc(ctx, &v.wr, A.nrows));
             RC(upload_matrix(ctx, P.view(), v.P, {0, P.nrows}, nullptr, !tiny, nullptr, nullptr, true, true, true));
             RC(upload_matrix(ctx, R.view(), v.R, {0, R.nrows}, nullptr, !tiny, nullptr, nullptr, true, true, true));

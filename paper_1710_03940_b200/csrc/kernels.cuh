@@ -30,7 +30,24 @@ constexpr int kEllUnroll = 8;     // slice widths up to this are fully unrolled
 #define DFL_ELL_BATCH 8
 #endif
 
-enum { FMT_ELL = 0, FMT_CSR = 1, FMT_CODE = 2 };
+enum { FMT_ELL = 0, FMT_CSR = 1, FMT_CODE = 2, FMT_CLASS = 3 };
+
+// FMT_CLASS ("row-class coded"): every row is one of <= kMaxClass distinct
+// rows, a row being the ordered list of its (column - row, value) entries
+// (<= 8).  The matrix is one byte per row (the class); the class table
+// travels as a __grid_constant__ kernel parameter, so a warp whose rows share
+// a class reads its offsets and values as constant-bank broadcasts.  Lossless:
+// a row is summed in its CSR order without FMA, bit-identical to spmv_rows.
+// Structured-grid operators fit (7-point Poisson: 27 classes: interior, 6
+// faces, 12 edges, 8 corners); the upload falls back to CODE / ELL otherwise.
+constexpr int kMaxClass = 64;
+struct ClassTab {
+    int n;
+    int lead;                  // largest column - row (leading gather edge)
+    int len[kMaxClass];
+    int delta[kMaxClass][8];
+    double val[kMaxClass][8];
+};
 
 // FMT_CODE ("stencil-coded ELL"): every row holds <= 8 one-byte codes; code c
 // stands for the pair (column - row, value) of a per-matrix table of <= 255
@@ -65,6 +82,10 @@ struct DMat {
     const int *perm = nullptr;           // SELL-C-sigma: slot -> row (nullptr: identity)
     // FMT_CODE
     const uint2 *codes = nullptr;        // 8 codes per row, row-major
+    int code_lead = 0;                   // largest column - row of the table (leading gather edge)
+    // FMT_CLASS
+    const uint8_t *cls = nullptr;        // class of every row
+    int class_id = -1;                   // index of the ClassTab in the context
     const int *ctab_delta = nullptr;     // column - row of each code
     const double *ctab_val = nullptr;    // value of each code
     int ncodes = 0;
@@ -694,6 +715,154 @@ __global__ void __launch_bounds__(kBlock) k_code(DMat A, RowArgs a) {
     }
 }
 
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+// FMT_CODE row kernel, software-pipelined: the codes and the own-row operands
+// of the next row are loaded one iteration ahead, and the leading edge of its
+// gathers (row + code_lead: data no earlier row has touched, hence a DRAM
+// miss in the gather chain) is prefetched into L2, so a row's critical path
+// is one L2 gather instead of DRAM (codes) + DRAM (first-touch gather).
+template <int MODE, bool DOT>
+__global__ void __launch_bounds__(kBlock) k_codep(DMat A, RowArgs a) {
+    DFL_PDL_ENTRY;
+    __shared__ int sd[256];
+    __shared__ double sv[256];
+    constexpr bool kR = MODE != MODE_PLAIN || DOT;  // needs r_i
+    constexpr bool kPost = MODE == MODE_POST;       // needs w_i, x_i
+    const bool wr = MODE == MODE_RESID && a.x == nullptr;
+    const double *gx = wr ? a.r : a.x;
+    const int64_t n = A.nrows, ncols = A.ncols;
+    const int64_t stride = (int64_t)gridDim.x * kBlock;
+    int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    uint2 cw = make_uint2(~0u, ~0u);
+    double ri = 0.0, wi = 0.0, xi = 0.0;
+    if (i < n) {
+        cw = __ldcs(A.codes + i);
+        if (kR) ri = __ldg(a.r + i);
+        if (kPost) {
+            wi = __ldg(a.w + i);
+            xi = __ldg(a.xo + i);
+        }
+        const int64_t pe = min(i + (int64_t)A.code_lead, ncols - 1);
+        prefetch_l2(gx + pe);
+        if (wr) prefetch_l2(a.w + pe);
+    }
+    load_codes(A, sd, sv);
+    double dot = 0.0;
+    for (; i < n; i += stride) {
+        const int64_t in = i + stride;
+        uint2 cn = make_uint2(~0u, ~0u);
+        double rn = 0.0, wn = 0.0, xn = 0.0;
+        if (in < n) {
+            cn = __ldcs(A.codes + in);
+            if (kR) rn = __ldg(a.r + in);
+            if (kPost) {
+                wn = __ldg(a.w + in);
+                xn = __ldg(a.xo + in);
+            }
+            const int64_t pe = min(in + (int64_t)A.code_lead, ncols - 1);
+            prefetch_l2(gx + pe);
+            if (wr) prefetch_l2(a.w + pe);
+        }
+        const double ax = wr ? code_row_w(cw, i, GatherWR{a.w, a.r}, sd, sv) : code_row_w(cw, i, GatherX{a.x}, sd, sv);
+        double y;
+        if (MODE == MODE_PLAIN) y = ax;
+        else if (MODE == MODE_RESID) y = sub_rn(ri, ax);
+        else if (MODE == MODE_POST) y = add_rn(xi, mul_rn(wi, sub_rn(ri, ax)));
+        else y = epilogue<MODE>(a, i, ax);
+        a.out[i] = y;
+        if (DOT) dot += ri * y;
+        cw = cn;
+        ri = rn;
+        wi = wn;
+        xi = xn;
+    }
+    if (DOT) {
+        __shared__ double sm[32];
+        double v[1] = {dot};
+        block_sum<1>(v, sm);
+        dot_out(a.fin, a.dot_part, v[0]);
+    }
+}
+
+// one row of a FMT_CLASS matrix, CSR order, no FMA
+template <class G>
+__device__ __forceinline__ double class_row(const ClassTab &T, int c, int64_t row, const G &g) {
+    const int len = T.len[c];
+    double xv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (k < len) xv[k] = g((int)(row + T.delta[c][k]));
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+        if (k < len) acc = add_rn(acc, mul_rn(T.val[c][k], xv[k]));
+    return acc;
+}
+
+// FMT_CLASS row kernel (V-cycle stages), grid-stride over one wave, software
+// pipelined like k_codep: the next row's class byte and own-row operands are
+// loaded one iteration ahead and its leading gather edge is prefetched to L2
+template <int MODE, bool DOT>
+__global__ void __launch_bounds__(kBlock) k_class(DMat A, RowArgs a, const __grid_constant__ ClassTab T) {
+    DFL_PDL_ENTRY;
+    constexpr bool kR = MODE != MODE_PLAIN || DOT;
+    constexpr bool kPost = MODE == MODE_POST;
+    const bool wr = MODE == MODE_RESID && a.x == nullptr;
+    const double *gx = wr ? a.r : a.x;
+    const int64_t n = A.nrows, ncols = A.ncols;
+    const int64_t stride = (int64_t)gridDim.x * kBlock;
+    int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    int c = 0;
+    double ri = 0.0, wi = 0.0, xi = 0.0;
+    if (i < n) {
+        c = __ldcs(A.cls + i);
+        if (kR) ri = __ldg(a.r + i);
+        if (kPost) {
+            wi = __ldg(a.w + i);
+            xi = __ldg(a.xo + i);
+        }
+        const int64_t pe = min(i + (int64_t)T.lead, ncols - 1);
+        prefetch_l2(gx + pe);
+        if (wr) prefetch_l2(a.w + pe);
+    }
+    double dot = 0.0;
+    for (; i < n; i += stride) {
+        const int64_t in = i + stride;
+        int cn = 0;
+        double rn = 0.0, wn = 0.0, xn = 0.0;
+        if (in < n) {
+            cn = __ldcs(A.cls + in);
+            if (kR) rn = __ldg(a.r + in);
+            if (kPost) {
+                wn = __ldg(a.w + in);
+                xn = __ldg(a.xo + in);
+            }
+            const int64_t pe = min(in + (int64_t)T.lead, ncols - 1);
+            prefetch_l2(gx + pe);
+            if (wr) prefetch_l2(a.w + pe);
+        }
+        const double ax = wr ? class_row(T, c, i, GatherWR{a.w, a.r}) : class_row(T, c, i, GatherX{a.x});
+        double y;
+        if (MODE == MODE_PLAIN) y = ax;
+        else if (MODE == MODE_RESID) y = sub_rn(ri, ax);
+        else if (MODE == MODE_POST) y = add_rn(xi, mul_rn(wi, sub_rn(ri, ax)));
+        else y = epilogue<MODE>(a, i, ax);
+        a.out[i] = y;
+        if (DOT) dot += ri * y;
+        c = cn;
+        ri = rn;
+        wi = wn;
+        xi = xn;
+    }
+    if (DOT) {
+        __shared__ double sm[32];
+        double v[1] = {dot};
+        block_sum<1>(v, sm);
+        dot_out(a.fin, a.dot_part, v[0]);
+    }
+}
+
 // wr = w .* r  (the relaxation x = w r of amg.py:193/195, rounded as there)
 static __global__ void __launch_bounds__(kBlock) k_wr(const double *__restrict__ w, const double *__restrict__ r, double *wr,
                                                int64_t n) {
@@ -924,6 +1093,30 @@ __global__ void __launch_bounds__(kBlock) k_op_code(DMat A, Tiles T, const __gri
     double y = 0.0;
     if (valid) {
         const double ax = code_row_w(cw, i, GatherX{a.x}, sd, sv);
+        y = OPMODE == 1 ? sub_rn(__ldg(a.b + i), ax) : ax;
+        a.y[i] = y;
+    }
+    if (a.k > 0) {
+        if (a.tick)
+            op_zt_fin<NV>(a, S, i, valid, y, t, sub);
+        else
+            op_zt<NV>(a, i, valid, y, t);
+    }
+}
+
+template <int OPMODE, int NV>
+__global__ void __launch_bounds__(kBlock) k_op_class(DMat A, Tiles T, const __grid_constant__ SubTable S, OpArgs a,
+                                                     const __grid_constant__ ClassTab C) {
+    DFL_PDL_ENTRY;
+    if (a.need_refresh && !a.st->refresh_now) return;
+    const int64_t t = blockIdx.x;
+    int64_t r0, r1;
+    const int sub = tile_rows(S, T, t, r0, r1);
+    const int64_t i = r0 + threadIdx.x;
+    const bool valid = i < r1 && !(a.skip_rows && a.skip_rows[i]);
+    double y = 0.0;
+    if (valid) {
+        const double ax = class_row(C, __ldcs(A.cls + i), i, GatherX{a.x});
         y = OPMODE == 1 ? sub_rn(__ldg(a.b + i), ax) : ax;
         a.y[i] = y;
     }

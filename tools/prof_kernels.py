@@ -25,6 +25,8 @@ cfg = SolverConfig({"solver": {"type": "cg", "tol": 1e-8}, "precond": {"relax": 
                     "deflation": {"kind": "linear"}})
 s = DeflatedSolver.from_rows(rows, o.n, o.partition(), config=cfg, coords_local=problems.node_coords(o, 0, o.n))
 print("spmv", s._ctx.time(0, a.reps))
+print("spmv_zt", s._ctx.time(4, a.reps))
+print("project", s._ctx.time(5, a.reps))
 print("vcycle", s._ctx.time(1, a.reps))
 print("vcycle graph", s._ctx.time(3, a.reps))
 for lab, ms in s._ctx.profile_vcycle(10):
