@@ -72,7 +72,7 @@ struct Nccl {
 extern Nccl g_nccl;
 
 // profiling / layout knobs (defined in ctx.cu, read at context creation)
-extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl, g_code_pipe, g_use_class;
+extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl, g_code_pipe, g_use_class, g_op_pf;
 extern double g_small_per_lane, g_csr_per_lane;
 extern int g_csr_g, g_sm_count;
 static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle
@@ -484,7 +484,10 @@ static void launch_op_nv(dfl_ctx *ctx, const OpArgs &a, unsigned grid) {
     const DMat &A = ctx->Aop;
     const SubTable &S = ctx->subtab;
     if (A.fmt == FMT_CLASS) {
-        launch_k(ctx->st, k_op_class<OPMODE, NV>, grid, kBlock, 0, A, ctx->tiles, S, a, *ctx->class_tabs[A.class_id]);
+        static const int occ = occupancy(k_op_class<OPMODE, NV>);
+        OpArgs b = a;
+        b.pf = g_op_pf ? (int64_t)occ * g_sm_count * kBlock : 0;
+        launch_k(ctx->st, k_op_class<OPMODE, NV>, grid, kBlock, 0, A, ctx->tiles, S, b, *ctx->class_tabs[A.class_id]);
         return;
     }
     if (A.fmt == FMT_CODE) {

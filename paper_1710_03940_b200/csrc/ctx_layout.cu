@@ -63,9 +63,10 @@ static int try_upload_code(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) {
     return DFL_OK;
 }
 
-// FMT_CLASS encoder (kernels.cuh ClassTab): rows of <= 8 entries, <= kMaxClass
-// distinct rows (ordered (column - row, value bits) lists).  ok = false leaves
-// m untouched for the next format.
+// FMT_CLASS encoder (kernels.cuh ClassTab): the dominant row (most frequent,
+// <= 7 entries) and its subsets as presence masks, <= kMaxClass generic
+// classes for the rest, every row <= 8 entries.  ok = false leaves m
+// untouched for the next format.
 static int try_upload_class(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) {
     ok = false;
     struct Row {
@@ -82,23 +83,60 @@ static int try_upload_class(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) 
     struct RH {
         size_t operator()(const Row &r) const {
             uint64_t x = (uint64_t)r.len * 0x9e3779b97f4a7c15ull;
-            for (int k = 0; k < r.len; ++k) x = (x ^ ((uint64_t)(uint32_t)r.d[k] * 0x100000001b3ull) ^ r.v[k]) * 0xff51afd7ed558ccdull;
+            for (int k = 0; k < r.len; ++k)
+                x = (x ^ ((uint64_t)(uint32_t)r.d[k] * 0x100000001b3ull) ^ r.v[k]) * 0xff51afd7ed558ccdull;
             return (size_t)x;
         }
     };
+    auto row_of = [&](int64_t i, Row &r) -> bool {
+        const int64_t b = h.ptr[i], e = h.ptr[i + 1];
+        if (e - b > 8) return false;
+        r.len = (int)(e - b);
+        for (int64_t k = b; k < e; ++k) {
+            const int64_t d = h.col[k] - i;
+            if (d < INT32_MIN || d > INT32_MAX) return false;
+            r.d[k - b] = (int)d;
+            std::memcpy(&r.v[k - b], &h.val[k], 8);
+        }
+        return true;
+    };
+    // pass 1: the dominant row (count distinct rows, give up beyond a bound)
+    std::unordered_map<Row, int64_t, RH> count;
+    Row r;
+    for (int64_t i = 0; i < h.nrows; ++i) {
+        if (!row_of(i, r)) return DFL_OK;
+        auto it = count.find(r);
+        if (it == count.end()) {
+            if (count.size() >= 4096) return DFL_OK;
+            count.emplace(r, 1);
+        } else {
+            it->second++;
+        }
+    }
+    Row dom;
+    int64_t best = -1;
+    for (auto &kv : count)
+        if (kv.second > best) best = kv.second, dom = kv.first;
+    const bool have_dom = dom.len <= 7;
+    // pass 2: masks for subsets of the dominant row, generic classes for the rest
     std::unordered_map<Row, int, RH> dict;
     std::vector<Row> rows;
     std::vector<uint8_t> cls((size_t)h.nrows);
     for (int64_t i = 0; i < h.nrows; ++i) {
-        const int64_t b = h.ptr[i], e = h.ptr[i + 1];
-        if (e - b > 8) return DFL_OK;
-        Row r;
-        r.len = (int)(e - b);
-        for (int64_t k = b; k < e; ++k) {
-            const int64_t d = h.col[k] - i;
-            if (d < INT32_MIN || d > INT32_MAX) return DFL_OK;
-            r.d[k - b] = (int)d;
-            std::memcpy(&r.v[k - b], &h.val[k], 8);
+        row_of(i, r);
+        if (have_dom) {
+            unsigned mask = 0;
+            int k = 0;
+            bool sub = true;
+            for (int e = 0; e < r.len && sub; ++e) {
+                while (k < dom.len && dom.d[k] != r.d[e]) ++k;
+                if (k == dom.len || dom.v[k] != r.v[e]) sub = false;
+                else mask |= 1u << k++;
+            }
+            if (sub) {
+                cls[(size_t)i] = (uint8_t)(0x80u | mask);
+                continue;
+            }
         }
         auto it = dict.find(r);
         if (it == dict.end()) {
@@ -111,7 +149,16 @@ static int try_upload_class(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) 
     auto tab = std::make_unique<ClassTab>();
     std::memset(tab.get(), 0, sizeof(ClassTab));
     tab->n = (int)rows.size();
+    tab->dom = -1;
     tab->lead = 0;
+    if (have_dom) {
+        tab->dlen = dom.len;
+        for (int k = 0; k < dom.len; ++k) {
+            tab->ddelta[k] = dom.d[k];
+            std::memcpy(&tab->dval[k], &dom.v[k], 8);
+            tab->lead = std::max(tab->lead, dom.d[k]);
+        }
+    }
     for (int c = 0; c < tab->n; ++c) {
         tab->len[c] = rows[c].len;
         for (int k = 0; k < rows[c].len; ++k) {

@@ -32,18 +32,22 @@ constexpr int kEllUnroll = 8;     // slice widths up to this are fully unrolled
 
 enum { FMT_ELL = 0, FMT_CSR = 1, FMT_CODE = 2, FMT_CLASS = 3 };
 
-// FMT_CLASS ("row-class coded"): every row is one of <= kMaxClass distinct
-// rows, a row being the ordered list of its (column - row, value) entries
-// (<= 8).  The matrix is one byte per row (the class); the class table
-// travels as a __grid_constant__ kernel parameter, so a warp whose rows share
-// a class reads its offsets and values as constant-bank broadcasts.  Lossless:
-// a row is summed in its CSR order without FMA, bit-identical to spmv_rows.
-// Structured-grid operators fit (7-point Poisson: 27 classes: interior, 6
-// faces, 12 edges, 8 corners); the upload falls back to CODE / ELL otherwise.
+// FMT_CLASS ("row-class coded"): one byte per row.  The most frequent row
+// (the interior stencil: ordered (column - row, value) entries, <= 7) is the
+// dominant row; a row whose entries are a subset of it (face / edge / corner
+// rows of a structured-grid operator) is coded as 0x80 | presence mask, any
+// other row as one of <= kMaxClass generic classes.  The table travels as a
+// __grid_constant__ kernel parameter.  Lossless: a row is summed in its CSR
+// order without FMA, bit-identical to spmv_rows.  The upload falls back to
+// CODE / ELL when the rows do not fit.
 constexpr int kMaxClass = 64;
 struct ClassTab {
     int n;
     int lead;                  // largest column - row (leading gather edge)
+    int dom;                   // unused (kept for the table layout)
+    int dlen;                  // dominant row: <= 7 entries (offset, value), the rows
+    int ddelta[8];             // that are subsets of it carry a presence mask
+    double dval[8];
     int len[kMaxClass];
     int delta[kMaxClass][8];
     double val[kMaxClass][8];
@@ -597,6 +601,12 @@ __device__ __forceinline__ double epilogue(const RowArgs &a, int64_t i, double a
 #ifndef DFL_ELL_MINB
 #define DFL_ELL_MINB 1
 #endif
+#ifndef DFL_OPCLASS_MINB
+#define DFL_OPCLASS_MINB 8
+#endif
+#ifndef DFL_CLASS_MINB
+#define DFL_CLASS_MINB 5
+#endif
 #ifndef DFL_ELL_MINB0
 #define DFL_ELL_MINB0 1
 #endif
@@ -785,26 +795,43 @@ __global__ void __launch_bounds__(kBlock) k_codep(DMat A, RowArgs a) {
     }
 }
 
-// one row of a FMT_CLASS matrix, CSR order, no FMA
+// one row of a FMT_CLASS matrix, CSR order, no FMA.  Row byte c:
+//   c >= 0x80: the row is a subset of the dominant row (the interior stencil)
+//              -- bit k of c says whether its entry k is present; offsets and
+//              values are compile-time offsets into the grid-constant table
+//              (constant-bank operands), so the warp runs one predicated
+//              stream whatever mix of interior / face / edge rows it holds;
+//   c <  0x80: generic class id (rows that are not such subsets), summed by a
+//              separate out-of-line loop.
+template <class G>
+__device__ __forceinline__ double class_row_slow(const ClassTab &T, int c, int64_t row, const G &g) {
+    double acc = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < T.len[c]; ++k) acc = add_rn(acc, mul_rn(T.val[c][k], g((int)(row + T.delta[c][k]))));
+    return acc;
+}
+
 template <class G>
 __device__ __forceinline__ double class_row(const ClassTab &T, int c, int64_t row, const G &g) {
-    const int len = T.len[c];
-    double xv[8];
+    if (c & 0x80) {
+        double xv[7];
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-        if (k < len) xv[k] = g((int)(row + T.delta[c][k]));
-    double acc = 0.0;
+        for (int k = 0; k < 7; ++k)
+            if ((c >> k) & 1) xv[k] = g((int)(row + T.ddelta[k]));
+        double acc = 0.0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k)
-        if (k < len) acc = add_rn(acc, mul_rn(T.val[c][k], xv[k]));
-    return acc;
+        for (int k = 0; k < 7; ++k)
+            if ((c >> k) & 1) acc = add_rn(acc, mul_rn(T.dval[k], xv[k]));
+        return acc;
+    }
+    return class_row_slow(T, c, row, g);
 }
 
 // FMT_CLASS row kernel (V-cycle stages), grid-stride over one wave, software
 // pipelined like k_codep: the next row's class byte and own-row operands are
 // loaded one iteration ahead and its leading gather edge is prefetched to L2
 template <int MODE, bool DOT>
-__global__ void __launch_bounds__(kBlock) k_class(DMat A, RowArgs a, const __grid_constant__ ClassTab T) {
+__global__ void __launch_bounds__(kBlock, MODE == MODE_RESID ? 4 : DFL_CLASS_MINB) k_class(DMat A, RowArgs a, const __grid_constant__ ClassTab T) {
     DFL_PDL_ENTRY;
     constexpr bool kR = MODE != MODE_PLAIN || DOT;
     constexpr bool kPost = MODE == MODE_POST;
@@ -996,6 +1023,7 @@ struct OpArgs {
     double *t2 = nullptr;
     int64_t K = 0;
     int64_t first_col = 0;
+    int64_t pf = 0;  // FMT_CLASS: L2 prefetch distance in rows (0: none)
 };
 
 // Z'y partials of one tile: thread c < k writes column c (NV >= k, power of two)
@@ -1104,15 +1132,27 @@ __global__ void __launch_bounds__(kBlock) k_op_code(DMat A, Tiles T, const __gri
     }
 }
 
+// One row per thread, one tile per block.  The chain of a row is class byte
+// -> table -> gathers; both DRAM first touches in it (the class byte and the
+// leading gather edge x[i + lead]) are prefetched into L2 one wave ahead
+// (a.pf rows: the resident rows of the whole GPU), so the blocks of the next
+// wave find them there.
 template <int OPMODE, int NV>
-__global__ void __launch_bounds__(kBlock) k_op_class(DMat A, Tiles T, const __grid_constant__ SubTable S, OpArgs a,
-                                                     const __grid_constant__ ClassTab C) {
+__global__ void __launch_bounds__(kBlock, DFL_OPCLASS_MINB) k_op_class(DMat A, Tiles T, const __grid_constant__ SubTable S,
+                                                                      OpArgs a, const __grid_constant__ ClassTab C) {
     DFL_PDL_ENTRY;
     if (a.need_refresh && !a.st->refresh_now) return;
     const int64_t t = blockIdx.x;
     int64_t r0, r1;
     const int sub = tile_rows(S, T, t, r0, r1);
     const int64_t i = r0 + threadIdx.x;
+    if (a.pf > 0) {
+        const int64_t ip = i + a.pf;
+        if (ip < A.nrows) {
+            prefetch_l2(A.cls + ip);
+            prefetch_l2(a.x + min(ip + (int64_t)C.lead, A.ncols - 1));
+        }
+    }
     const bool valid = i < r1 && !(a.skip_rows && a.skip_rows[i]);
     double y = 0.0;
     if (valid) {
