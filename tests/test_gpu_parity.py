@@ -35,6 +35,32 @@ def test_spmv_ell_bitwise():
     assert np.array_equal(y, port.spmv(port.Csr.of(p.matrix), x))
 
 
+@pytest.mark.parametrize("variant", ["poisson", "generic_rows", "too_many_classes", "jump", "convdiff"])
+def test_spmv_class_coded_bitwise(variant):
+    """Row-class coded upload (FMT_CLASS: dominant-stencil subsets as masks,
+    generic classes, fallback beyond 64 classes) sums every row in CSR order:
+    bit-identical to the reference's spmv_rows restated in the oracle."""
+    rng = np.random.default_rng(7)
+    if variant == "jump":
+        M = problems.jump3d(20).matrix
+    elif variant == "convdiff":
+        M = problems.convdiff3d(20).matrix
+    else:
+        M = problems.poisson3d(22).matrix
+    vals = M.values.copy()
+    if variant in ("generic_rows", "too_many_classes"):
+        rows = rng.choice(M.nrows, 40 if variant == "generic_rows" else 300, replace=False)
+        for j, i in enumerate(rows):  # distinct diagonal values: rows outside the dominant stencil
+            b, e = M.row_ptr[i], M.row_ptr[i + 1]
+            d = b + int(np.nonzero(M.col_idx[b:e] == i)[0][0])
+            vals[d] = 6.0 + 0.25 * (1 + j % (20 if variant == "generic_rows" else 300))
+    A = nat.CsrArrays(M.nrows, M.ncols, M.row_ptr, M.col_idx, vals)
+    x = rng.standard_normal(M.ncols)
+    y = nat.spmv_device(A, x)
+    ref = port.spmv(port.Csr(M.nrows, M.ncols, M.row_ptr, M.col_idx, vals), x)
+    assert np.array_equal(y, ref)
+
+
 def test_spmv_random_csr():
     rng = np.random.default_rng(3)
     n = 3000
