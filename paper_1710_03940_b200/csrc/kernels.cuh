@@ -131,6 +131,10 @@ __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(
 
 template <class T>
 __device__ __forceinline__ T ld_stream(const T *p) { return __ldcs(p); }
+__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+#ifndef DFL_SLICE_PREFETCH
+#define DFL_SLICE_PREFETCH 0  // measured slower (L0 restriction 43.4 -> 46.0 us)
+#endif
 
 // ---------------------------------------------------------------------------
 // gather functors: the value an entry multiplies
@@ -279,7 +283,7 @@ __device__ __forceinline__ double ell_slice_w(const DMat &A, int64_t off, const 
 }
 
 #ifndef DFL_SLICE_CHUNK
-#define DFL_SLICE_CHUNK 8
+#define DFL_SLICE_CHUNK 4
 #endif
 constexpr int kChunk = DFL_SLICE_CHUNK;
 
@@ -308,7 +312,22 @@ __device__ __forceinline__ double ell_row_sliced(const DMat &A, int64_t row, con
     const int width = (int)((__ldg(A.slice_off + s + 1) - off) >> 5);
     const int64_t o = off + (row & 31);
     double acc = 0.0;
-    for (int k0 = 0; k0 < width; k0 += kChunk) acc = ell_chunk(A, o + 32 * k0, min(kChunk, width - k0), acc, g);
+    for (int k0 = 0; k0 < width; k0 += kChunk) {
+#if DFL_SLICE_PREFETCH
+        // long rows: pull the next chunk of the matrix stream into L2 while this
+        // one's gathers run, so the next chunk's loads are L2 hits
+        if (k0 + kChunk < width) {
+            const int nk = min(kChunk, width - k0 - kChunk);
+#pragma unroll
+            for (int k = 0; k < kChunk; ++k)
+                if (k < nk) {
+                    prefetch_l2(A.col + o + 32 * (k0 + kChunk + k));
+                    prefetch_l2(A.val + o + 32 * (k0 + kChunk + k));
+                }
+        }
+#endif
+        acc = ell_chunk(A, o + 32 * k0, min(kChunk, width - k0), acc, g);
+    }
     return acc;
 }
 
@@ -608,7 +627,7 @@ __device__ __forceinline__ double epilogue(const RowArgs &a, int64_t i, double a
 #define DFL_CLASS_MINB 5
 #endif
 #ifndef DFL_ELL_MINB0
-#define DFL_ELL_MINB0 1
+#define DFL_ELL_MINB0 6
 #endif
 template <int MODE, bool DOT, int W>
 __global__ void __launch_bounds__(kBlock, W == 0 ? DFL_ELL_MINB0 : DFL_ELL_MINB) k_ell(DMat A, RowArgs a) {
@@ -725,7 +744,6 @@ __global__ void __launch_bounds__(kBlock) k_code(DMat A, RowArgs a) {
     }
 }
 
-__device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 
 // FMT_CODE row kernel, software-pipelined: the codes and the own-row operands
 // of the next row are loaded one iteration ahead, and the leading edge of its
