@@ -147,6 +147,8 @@ void dfl_ctx_destroy(dfl_ctx *ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->st) cudaStreamSynchronize(ctx->st);
     if (ctx->loop_exec) cudaGraphExecDestroy(ctx->loop_exec);
+    if (ctx->bg_exec) cudaGraphExecDestroy(ctx->bg_exec);
+    if (ctx->h_bstate) cudaFreeHost(ctx->h_bstate);
     for (void *p : ctx->allocs) cudaFree(p);
     if (ctx->h_state) cudaFreeHost(ctx->h_state);
     if (ctx->h_dots) cudaFreeHost(ctx->h_dots);
@@ -463,8 +465,12 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     const bool bicg = p->solver != DFL_SOLVER_CG;  // host-driven solvers
     const bool use_graph = !bicg && !multi(ctx) && !(ng && ng[0] == '1');
     KState bstate{};
+    const bool dev_loop = !multi(ctx) && !(ng && ng[0] == '1');  // device-side Krylov loops (single rank)
     if (p->solver == DFL_SOLVER_BICGSTAB2) {
-        RC(bicg_solve_dev(ctx, p, bstate));
+        if (dev_loop)
+            RC(bicg_solve_graph(ctx, p, bstate));
+        else
+            RC(bicg_solve_dev(ctx, p, bstate));
         RC(lift_dev(ctx, p));
     } else if (p->solver == DFL_SOLVER_GMRES || p->solver == DFL_SOLVER_FGMRES) {
         RC(gmres_solve_dev(ctx, p, p->solver == DFL_SOLVER_FGMRES, bstate));
@@ -490,7 +496,7 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     rep->converged = s.converged || (s.resnorm <= s.target);
     if (s.breakdown) rep->converged = 0;
     rep->breakdown = rep->converged ? DFL_BRK_NONE : s.breakdown;
-    rep->device_loop = use_graph ? 1 : 0;
+    rep->device_loop = (use_graph || (p->solver == DFL_SOLVER_BICGSTAB2 && dev_loop)) ? 1 : 0;
     rep->bnorm = s.bnorm;
     rep->resnorm = s.resnorm;
     rep->solve_seconds = ms_solve * 1e-3;

@@ -236,6 +236,11 @@ struct dfl_ctx {
     cudaGraphExec_t loop_exec = nullptr;
     int loop_key = -1;
     int64_t body_kernels = 0;
+    // BiCGStab(2) device loop (ctx_bicg.cu)
+    void *bstate = nullptr, *h_bstate = nullptr;
+    cudaGraphExec_t bg_exec = nullptr;
+    int bg_key = -1;
+    int64_t bg_body_kernels = 0;
     int64_t if_kernels = 0;  // refresh IF body (graph)
     int64_t launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -626,6 +631,8 @@ int lift_dev(dfl_ctx *ctx, const dfl_solve_params *p);
 // ctx_cg.cu / ctx_krylov.cu
 int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph);
 int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out);
+int bicg_prologue(dfl_ctx *ctx, const dfl_solve_params *p, KState &out);
+int bicg_solve_graph(dfl_ctx *ctx, const dfl_solve_params *p, KState &out);  // ctx_bicg.cu
 int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KState &out);
 // ctx.cu
 int ready(dfl_ctx *ctx);

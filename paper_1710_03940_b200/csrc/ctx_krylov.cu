@@ -71,14 +71,16 @@ static int bicg_alloc(dfl_ctx *ctx) {
     return DFL_OK;
 }
 
-int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
+// ||b|| (deflation.py:266), b' = project(b), ||b'||; r0 = shadow = b', d0 = 0,
+// u = 0.  out.converged = 1 (and x = 0) when b or b' vanishes
+// (krylov.py:270-272); otherwise out.resnorm = ||b'|| and out.rho1 = b'.b'.
+int bicg_prologue(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
     RC(bicg_alloc(ctx));
     const bool defl = p->deflated != 0;
     const int64_t n = ctx->n;
     const unsigned nb = (unsigned)ctx->nblk;
     out = KState{};
     double val[3];
-    // ||b|| (deflation.py:266), b' = project(b), ||b'||
     RC(dots(ctx, 1, ctx->b, ctx->b, nullptr, nullptr, nullptr, nullptr, val));
     out.bnorm = std::sqrt(std::max(val[0], 0.0));
     const double target = std::max(0.0, p->tol * out.bnorm);  // max(tol*||b'||, atol) with tol = 0
@@ -98,22 +100,34 @@ int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
         ctx->launches++;
     }
     RC(dots(ctx, 1, ctx->bp, ctx->bp, nullptr, nullptr, nullptr, nullptr, val));
-    const double bpbp = val[0];  // also r[0].shadow of the first step (both are b')
-    const double bpn = std::sqrt(std::max(val[0], 0.0));
-    if (bpn == 0.0) {  // bicgstab2 returns zeros (krylov.py:270-272)
+    out.rho1 = val[0];  // also r[0].shadow of the first step (both are b')
+    out.resnorm = std::sqrt(std::max(val[0], 0.0));
+    if (out.resnorm == 0.0) {  // bicgstab2 returns zeros (krylov.py:270-272)
         out.converged = 1;
         launch_k(ctx->st, k_fill, nb, kBlock, 0, ctx->x, 0.0, n);
         ctx->launches++;
         return DFL_OK;
     }
+    launch_k(ctx->st, k_copy, nb, kBlock, 0, ctx->br[0], (const double *)ctx->bp, n);
+    launch_k(ctx->st, k_fill, nb, kBlock, 0, ctx->bd[0], 0.0, n);
+    launch_k(ctx->st, k_copy, nb, kBlock, 0, ctx->bshadow, (const double *)ctx->bp, n);
+    ctx->launches += 3;
+    return DFL_OK;
+}
+
+int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
+    RC(bicg_prologue(ctx, p, out));
+    if (out.converged) return DFL_OK;
+    const bool defl = p->deflated != 0;
+    const int64_t n = ctx->n;
+    const unsigned nb = (unsigned)ctx->nblk;
+    const double target = out.target;
+    const double bpbp = out.rho1, bpn = out.resnorm;
+    double val[3];
     double *r[3] = {ctx->br[0], ctx->br[1], ctx->br[2]};
     double *d[3] = {ctx->bd[0], ctx->bd[1], ctx->bd[2]};
     double *u = ctx->bu, *shadow = ctx->bshadow;
     const double *r0init = ctx->bp;
-    launch_k(ctx->st, k_copy, nb, kBlock, 0, r[0], r0init, n);
-    launch_k(ctx->st, k_fill, nb, kBlock, 0, d[0], 0.0, n);
-    launch_k(ctx->st, k_copy, nb, kBlock, 0, shadow, r0init, n);
-    ctx->launches += 3;
     double rho0 = 1.0, alpha = 0.0, omega = 1.0;
     bool restarted = false;
     int brk = DFL_BRK_NONE;

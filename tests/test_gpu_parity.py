@@ -120,8 +120,26 @@ def test_solve_parity(case):
     assert abs(rep["iterations"] - case["iterations"]) <= 1, (rep["iterations"], case["iterations"])
     assert rep["relative_residual"] <= max(tol, 2 * case["relative_residual"])
     assert np.linalg.norm(x - xref) <= 1e-6 * np.linalg.norm(xref)
-    assert rep["device_loop"] == (case["config"]["solver"]["type"] == "cg")
+    assert rep["device_loop"] == (case["config"]["solver"]["type"] in ("cg", "bicgstab2"))
     assert rep["kernel_launches"] > 0
+
+
+@pytest.mark.parametrize("case", [c for c in meta()["solves"] if c["config"]["solver"]["type"] == "bicgstab2"],
+                         ids=lambda c: c["name"])
+def test_bicgstab2_device_loop_matches_host_loop(case, monkeypatch):
+    """The graph-resident BiCGStab(2) (ctx_bicg.cu) and the host-driven one
+    (ctx_krylov.cu, DFL_NO_GRAPH=1) run the same recurrence: same group count,
+    same breakdown report, solutions equal to rounding."""
+    shape = case["shape"] if isinstance(case["shape"], int) else tuple(case["shape"])
+    p = problems.make_problem(shape, problems.boxes_for(case["m"]), case["kind"])
+    s = _solver(p, case["m"], case["config"], deflated=case["deflated"])
+    x_dev, rep_dev = s.solve(p.rhs)
+    monkeypatch.setenv("DFL_NO_GRAPH", "1")
+    x_host, rep_host = s.solve(p.rhs)
+    assert rep_dev["device_loop"] and not rep_host["device_loop"]
+    assert rep_dev["iterations"] == rep_host["iterations"]
+    assert rep_dev["converged"] == rep_host["converged"]
+    assert np.linalg.norm(x_dev - x_host) <= 1e-12 * np.linalg.norm(x_host)
 
 
 def test_config1_fingerprint():
