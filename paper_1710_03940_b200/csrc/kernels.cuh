@@ -348,7 +348,7 @@ __device__ __forceinline__ double ell_any(const DMat &A, int64_t row, const G &g
 #define DFL_CSR_UNROLL 8
 #endif
 #ifndef DFL_CSR_MINB
-#define DFL_CSR_MINB 1
+#define DFL_CSR_MINB 4
 #endif
 constexpr int kCsrUnroll = DFL_CSR_UNROLL;
 
