@@ -305,6 +305,10 @@ __device__ __forceinline__ double ell_chunk(const DMat &A, int64_t o, int w, dou
     return acc;
 }
 
+#ifndef DFL_SLICE_PIPE
+#define DFL_SLICE_PIPE 0  // register double buffer: measured neutral (profiles/r01/README.md)
+#endif
+
 template <class G>
 __device__ __forceinline__ double ell_row_sliced(const DMat &A, int64_t row, const G &g) {
     const int64_t s = row >> 5;
@@ -312,6 +316,43 @@ __device__ __forceinline__ double ell_row_sliced(const DMat &A, int64_t row, con
     const int width = (int)((__ldg(A.slice_off + s + 1) - off) >> 5);
     const int64_t o = off + (row & 31);
     double acc = 0.0;
+#if DFL_SLICE_PIPE
+    // register double buffer: chunk k+1's column / value loads are in flight
+    // while chunk k's gathers run, so DRAM sees this row's stream continuously
+    // (same sequential summation order as below: bit-identical)
+    int c[kChunk];
+    double v[kChunk];
+#pragma unroll
+    for (int k = 0; k < kChunk; ++k)
+        if (k < width) {
+            c[k] = ld_stream(A.col + o + 32 * k);
+            v[k] = ld_stream(A.val + o + 32 * k);
+        }
+    for (int k0 = 0; k0 < width; k0 += kChunk) {
+        const int k1 = k0 + kChunk;
+        int cn[kChunk];
+        double vn[kChunk];
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k)
+            if (k1 + k < width) {
+                cn[k] = ld_stream(A.col + o + 32 * (k1 + k));
+                vn[k] = ld_stream(A.val + o + 32 * (k1 + k));
+            }
+        double xv[kChunk];
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k)
+            if (k0 + k < width) xv[k] = g(c[k]);
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k)
+            if (k0 + k < width) acc = add_rn(acc, mul_rn(v[k], xv[k]));
+#pragma unroll
+        for (int k = 0; k < kChunk; ++k) {
+            c[k] = cn[k];
+            v[k] = vn[k];
+        }
+    }
+    return acc;
+#else
     for (int k0 = 0; k0 < width; k0 += kChunk) {
 #if DFL_SLICE_PREFETCH
         // long rows: pull the next chunk of the matrix stream into L2 while this
@@ -329,6 +370,7 @@ __device__ __forceinline__ double ell_row_sliced(const DMat &A, int64_t row, con
         acc = ell_chunk(A, o + 32 * k0, min(kChunk, width - k0), acc, g);
     }
     return acc;
+#endif
 }
 
 template <int W, class G>
