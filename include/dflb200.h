@@ -112,7 +112,9 @@ typedef struct {
     int32_t deflated;     /* 0: plain block-AMG Krylov (deflation.py:287-290) */
     double tol;           /* solver.tol: atol = tol * ||b|| (deflation.py:266-270) */
     int32_t restart;      /* solver.M: (F)GMRES restart length (deflation.py:275-276) */
-    int32_t reserved;
+    int32_t x0_given;     /* 1: x holds the initial guess on entry (plain block-AMG Krylov only:
+                             krylov.py:108/275/383 r = b - A x0; the deflated path ignores x0,
+                             deflation.py:284) */
 } dfl_solve_params;
 
 typedef struct {

@@ -38,7 +38,7 @@ class AmgOptions(ctypes.Structure):
 
 class SolveParams(ctypes.Structure):
     _fields_ = [("solver", c_i32), ("maxiter", c_i32), ("refresh_every", c_i32), ("deflated", c_i32),
-                ("tol", c_dbl), ("restart", c_i32), ("reserved", c_i32)]
+                ("tol", c_dbl), ("restart", c_i32), ("x0_given", c_i32)]
 
 
 class BlockDesc(ctypes.Structure):

@@ -460,6 +460,10 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     CK(cudaEventCreate(&e_h1));
     CK(cudaEventRecord(e_h0, ctx->st));
     RC(stage_in(ctx, ctx->b, b, ptr_kind));
+    if (p->x0_given && !p->deflated) {
+        if (!ctx->x0) RC(dalloc(ctx, &ctx->x0, ctx->n));
+        RC(stage_in(ctx, ctx->x0, x, ptr_kind));
+    }
     CK(cudaEventRecord(ctx->ev0, ctx->st));
     const char *ng = getenv("DFL_NO_GRAPH");
     const bool bicg = p->solver != DFL_SOLVER_CG;  // host-driven solvers

@@ -488,6 +488,10 @@ int bicg_solve_graph(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
     ctx->launches += ctx->bg_body_kernels * std::max(1, s.iters);
     // x = x0 + M(u)  (krylov.py:284-285), into ctx->x (the y of the deflated system)
     RC(vcycle(ctx, ctx->bu, ctx->x, nullptr, nullptr, nullptr));
+    if (use_x0(ctx, p)) {
+        launch_k(ctx->st, k_addv, (unsigned)ctx->nblk, kBlock, 0, ctx->x, (const double *)ctx->x0, ctx->n);
+        ctx->launches++;
+    }
     out.iters = s.iters;
     out.resnorm = s.resnorm;
     out.converged = s.resnorm <= out.target;

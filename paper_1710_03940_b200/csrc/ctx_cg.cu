@@ -320,10 +320,22 @@ int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
         a.dot_part = ctx->dpart;
         launch_project<0>(ctx, a);
     }
+    const bool x0 = use_x0(ctx, p);
+    if (x0) {  // x = x0 (unless b = 0), r = b - A x0 and ||r|| (krylov.py:108-109)
+        launch_k(ctx->st, k_copy_live, (unsigned)ctx->nblk, kBlock, 0, ctx->x, (const double *)ctx->x0, ctx->n,
+                 (const KState *)st);
+        RC(op_apply_dev(ctx, ctx->x, ctx->r, 1, ctx->b, false, nullptr, 0));
+        launch_k(ctx->st, k_dot, (unsigned)ctx->vgrid, kBlock, 0, (const double *)ctx->r, (const double *)ctx->r,
+                 ctx->n, ctx->dpart, (const KState *)nullptr);
+        ctx->launches += 2;
+    }
     RC(rank_scalar(ctx, ctx->dpart, ctx->vgrid, 0, &gath));
     launch_k(ctx->st, k_cg_init_r, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, gath, ctx->nranks);
-    launch_k(ctx->st, k_copy, (unsigned)ctx->nblk, kBlock, 0, ctx->r, ctx->bp, ctx->n);
-    ctx->launches += 2;
+    ctx->launches++;
+    if (!x0) {
+        launch_k(ctx->st, k_copy, (unsigned)ctx->nblk, kBlock, 0, ctx->r, ctx->bp, ctx->n);
+        ctx->launches++;
+    }
     int64_t np = 0;
     RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
     RC(rank_scalar(ctx, ctx->dpart, np, 0, &gath));

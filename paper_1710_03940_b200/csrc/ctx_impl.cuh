@@ -216,6 +216,7 @@ struct dfl_ctx {
     double *b = nullptr, *bp = nullptr, *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr,
            *w = nullptr, *tmp = nullptr, *xin = nullptr, *yout = nullptr;
     double *dpart = nullptr;
+    double *x0 = nullptr;  // initial guess of a plain (non-deflated) solve, dfl_solve_params.x0_given
     int64_t nblk = 0;
     int64_t vgrid = 0;  // grid of the grid-stride vector kernels (projection, CG updates, dots)
     // BiCGStab(2) work vectors (allocated on first use)
@@ -552,6 +553,8 @@ static void launch_op(dfl_ctx *ctx, const OpArgs &a) {
 // cross-unit entry points (return DFL_OK or a DFL_E_* code, message in ctx->err)
 
 inline bool multi(const dfl_ctx *ctx) { return ctx->comm != nullptr || ctx->fab != nullptr; }
+// the plain block-AMG Krylov path starts from x0 (krylov.py:108/275/383)
+inline bool use_x0(const dfl_ctx *ctx, const dfl_solve_params *p) { return p->x0_given && !p->deflated && ctx->x0; }
 
 inline ProjArgs proj_args(dfl_ctx *ctx, const double *in, double *out, const KState *st) {
     ProjArgs a{};

@@ -93,8 +93,13 @@ int bicg_prologue(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
         ctx->launches++;
         return DFL_OK;
     }
+    const bool x0 = use_x0(ctx, p);
     if (defl) {
         RC(project_dev(ctx, ctx->b, ctx->bp, nullptr, 0));
+    } else if (x0) {  // r0 = b - A x0 (krylov.py:275)
+        launch_k(ctx->st, k_copy, nb, kBlock, 0, ctx->x, (const double *)ctx->x0, n);
+        ctx->launches++;
+        RC(op_apply_dev(ctx, ctx->x, ctx->bp, 1, ctx->b, false, nullptr, 0));
     } else {
         launch_k(ctx->st, k_copy, nb, kBlock, 0, ctx->bp, ctx->b, n);
         ctx->launches++;
@@ -102,9 +107,12 @@ int bicg_prologue(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
     RC(dots(ctx, 1, ctx->bp, ctx->bp, nullptr, nullptr, nullptr, nullptr, val));
     out.rho1 = val[0];  // also r[0].shadow of the first step (both are b')
     out.resnorm = std::sqrt(std::max(val[0], 0.0));
-    if (out.resnorm == 0.0) {  // bicgstab2 returns zeros (krylov.py:270-272)
+    if (out.resnorm == 0.0) {  // the recurrence returns u = 0: x = x0 + M(0)
         out.converged = 1;
-        launch_k(ctx->st, k_fill, nb, kBlock, 0, ctx->x, 0.0, n);
+        if (x0)
+            launch_k(ctx->st, k_copy, nb, kBlock, 0, ctx->x, (const double *)ctx->x0, n);
+        else
+            launch_k(ctx->st, k_fill, nb, kBlock, 0, ctx->x, 0.0, n);
         ctx->launches++;
         return DFL_OK;
     }
@@ -260,6 +268,10 @@ int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
     }
     // x = x0 + M(u)  (krylov.py:284-285), into ctx->x (the y of the deflated system)
     RC(vcycle(ctx, u, ctx->x, nullptr, nullptr, nullptr));
+    if (use_x0(ctx, p)) {
+        launch_k(ctx->st, k_addv, nb, kBlock, 0, ctx->x, (const double *)ctx->x0, n);
+        ctx->launches++;
+    }
     out.iters = iters;
     out.resnorm = resnorm;
     out.converged = resnorm <= target;
@@ -371,13 +383,20 @@ int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KSta
         launch_k(ctx->st, k_copy, nb, kBlock, 0, ctx->bp, ctx->b, n);
         ctx->launches++;
     }
-    RC(dots(ctx, 1, ctx->bp, ctx->bp, nullptr, nullptr, nullptr, nullptr, val));
-    double resnorm = std::sqrt(std::max(val[0], 0.0));
+    double resnorm;
+    if (use_x0(ctx, p)) {  // x = x0, r = b - A x0 (krylov.py:383)
+        launch_k(ctx->st, k_copy, nb, kBlock, 0, ctx->x, (const double *)ctx->x0, n);
+        ctx->launches++;
+        RC(gm_residual(ctx, defl, &resnorm));
+    } else {
+        RC(dots(ctx, 1, ctx->bp, ctx->bp, nullptr, nullptr, nullptr, nullptr, val));
+        resnorm = std::sqrt(std::max(val[0], 0.0));
+        launch_k(ctx->st, k_copy, nb, kBlock, 0, ctx->r, ctx->bp, n);
+    }
     if (resnorm == 0.0) {
         out.converged = 1;
         return DFL_OK;
     }
-    launch_k(ctx->st, k_copy, nb, kBlock, 0, ctx->r, ctx->bp, n);
     ctx->launches++;
     std::vector<double> H((size_t)(M + 1) * M), g(M + 1), cs(M), sn(M), y(M);
     auto h = [&](int i, int j) -> double & { return H[(size_t)i * M + j]; };

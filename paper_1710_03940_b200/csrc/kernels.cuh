@@ -1567,6 +1567,14 @@ static __global__ void __launch_bounds__(kBlock) k_cg_p(double *p, const double 
         p[i] = add_rn(z[i], mul_rn(beta, p[i]));
 }
 
+// dst = src unless the solve already ended (b = 0 keeps the zero solution)
+static __global__ void k_copy_live(double *dst, const double *src, int64_t n, const KState *st) {
+    DFL_PDL_ENTRY;
+    if (skip(st)) return;
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (i < n) dst[i] = src[i];
+}
+
 static __global__ void k_copy(double *dst, const double *src, int64_t n) {
     DFL_PDL_ENTRY;
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;

@@ -210,11 +210,18 @@ class DeflatedSolver:
     # -- the solve ----------------------------------------------------------------
     def solve(self, b, x0=None):
         """Returns (x, report).  x0 is ignored on the deflated path
-        (deflation.py:284); the plain block-AMG path starts from zero too."""
+        (deflation.py:284); the plain block-AMG path starts from it
+        (deflation.py:287-290, krylov.py:108: r = b - A x0)."""
         name = _solver_name(self)
         b_local = self._local(b)
         params = _params(self)
-        x_local = np.empty(self.n_local)
+        if x0 is not None and not self.deflated:
+            if np.shape(x0) != np.shape(b):
+                raise DimensionError(f"x0 has shape {np.shape(x0)}, b has {np.shape(b)}")
+            x_local = np.array(self._local(x0), dtype=np.float64, copy=True)
+            params.x0_given = 1
+        else:
+            x_local = np.empty(self.n_local)
         t0 = time.perf_counter()
         rep = self._ctx.solve(params, b_local, x_local)
         wall = time.perf_counter() - t0

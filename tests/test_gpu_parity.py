@@ -324,3 +324,51 @@ def test_gmres_fgmres_parity(case):
         return
     assert abs(rep["iterations"] - case["iterations"]) <= 1, (rep["iterations"], case["iterations"])
     assert np.linalg.norm(x - xref) <= 1e-6 * np.linalg.norm(xref)
+
+
+def _x0_cases():
+    import json
+    import os
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    with open(os.path.join(here, "golden_x0.json")) as fh:
+        return json.load(fh)["cases"]
+
+
+@pytest.mark.parametrize("case", _x0_cases(), ids=lambda c: c["name"])
+def test_initial_guess_plain_path_matches_reference(case):
+    """deflated=False passes x0 through (deflation.py:287-290): r = b - A x0
+    (krylov.py:108/275/383).  Golden: the reference itself
+    (tests/golden/make_golden_x0.py)."""
+    import os
+
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    xref = dict(np.load(os.path.join(here, "golden_x0.npz")))[case["name"] + "/x"]
+    p = problems.poisson3d(case["shape"], problems.boxes_for(case["m"]))
+    s = _solver(p, case["m"], case["config"], deflated=False)
+    i = np.arange(p.matrix.nrows, dtype=np.float64)
+    x0 = 1e-3 * np.sin(0.37 * i) + 5e-4 * np.cos(0.011 * i)
+    x, rep = s.solve(p.rhs, x0=x0)
+    tol = case["config"]["solver"]["tol"]
+    assert rep["converged"]
+    assert abs(rep["iterations"] - case["iterations"]) <= 1, (rep["iterations"], case["iterations"])
+    assert rep["relative_residual"] <= max(tol, 2 * case["relative_residual"])
+    assert np.linalg.norm(x - xref) <= 1e-6 * np.linalg.norm(xref)
+
+
+def test_initial_guess_edge_cases():
+    """x0 = the exact solution: 0 iterations and x returned as given; the
+    deflated path ignores x0 (deflation.py:284): bitwise the zero-guess solve."""
+    p = problems.poisson3d(12, problems.boxes_for(2))
+    xs = np.random.default_rng(5).standard_normal(p.matrix.nrows)
+    b = port.spmv(port.Csr.of(p.matrix), xs)
+    for solver in ("cg", "bicgstab2", "gmres"):
+        s = _solver(p, 2, {"solver": {"type": solver, "tol": 1e-8}}, deflated=False)
+        x, rep = s.solve(b, x0=xs)
+        assert rep["iterations"] == 0 and rep["converged"], (solver, rep["iterations"])
+        assert np.array_equal(x, xs), solver
+    cfg = {"solver": {"type": "cg", "tol": 1e-8}, "deflation": {"kind": "linear"}}
+    s = _solver(p, 2, cfg)
+    x_a, rep_a = s.solve(b)
+    x_b, rep_b = s.solve(b, x0=xs)
+    assert np.array_equal(x_a, x_b) and rep_a["iterations"] == rep_b["iterations"]
