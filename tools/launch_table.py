@@ -15,7 +15,7 @@ def main(path, top=30):
         if len(r) <= vi:
             continue
         v = float(r[vi].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "ns": 1e-3, "us": 1.0, "ms": 1e3}.get(r[ui], 1.0)
         name = r[ki][:80]
         agg[name][0] += 1
         agg[name][1] += v
