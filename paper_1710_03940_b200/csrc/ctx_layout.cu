@@ -178,6 +178,56 @@ static int try_upload_class(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) 
     return DFL_OK;
 }
 
+// FMT_PCODE encoder (kernels.cuh): ok = false leaves m untouched
+static int try_upload_pcode(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) {
+    ok = false;
+    const int64_t n = h.nrows;
+    std::unordered_map<uint64_t, int> dict;
+    std::vector<double> tab;
+    std::vector<int> c0(n, 0);
+    std::vector<uint32_t> d((size_t)3 * n, 0u), v(n, 0u);
+    for (int64_t i = 0; i < n; ++i) {
+        const int64_t b = h.ptr[i], e = h.ptr[i + 1];
+        if (e - b > kPcMaxLen) return DFL_OK;
+        uint32_t w = (uint32_t)(e - b);
+        if (e > b) c0[i] = (int)h.col[b];
+        for (int64_t k = b; k < e; ++k) {
+            const int64_t j = k - b;
+            if (j > 0) {
+                const int64_t dl = h.col[k] - h.col[b];
+                if (dl <= 0 || dl > 65535) return DFL_OK;  // unsorted or too spread
+                d[(size_t)((j - 1) >> 1) * n + i] |= (uint32_t)dl << (16 * ((j - 1) & 1));
+            }
+            uint64_t bits;
+            std::memcpy(&bits, &h.val[k], 8);
+            auto it = dict.find(bits);
+            if (it == dict.end()) {
+                if (dict.size() >= 16) return DFL_OK;
+                it = dict.emplace(bits, (int)tab.size()).first;
+                tab.push_back(h.val[k]);
+            }
+            w |= (uint32_t)it->second << (3 + 4 * j);
+        }
+        v[i] = w;
+    }
+    tab.resize(16, 0.0);
+    int *d_c0;
+    uint32_t *d_d, *d_v;
+    double *d_tab;
+    RC(upload(ctx, &d_c0, c0.data(), std::max<int64_t>(1, n)));
+    RC(upload(ctx, &d_d, d.data(), std::max<int64_t>(1, 3 * n)));
+    RC(upload(ctx, &d_v, v.data(), std::max<int64_t>(1, n)));
+    RC(upload(ctx, &d_tab, tab.data(), 16));
+    m.fmt = FMT_PCODE;
+    m.stored = m.nnz;
+    m.pc_c0 = d_c0;
+    m.pc_d = d_d;
+    m.pc_v = d_v;
+    m.pc_tab = d_tab;
+    ok = true;
+    return DFL_OK;
+}
+
 // value codes for an ELL-layout matrix with <= 255 distinct values (bitwise)
 static int attach_value_codes(dfl_ctx *ctx, DMat &m, const std::vector<double> &val) {
     std::unordered_map<uint64_t, int> dict;
@@ -239,6 +289,12 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
             if (colscale) *scaled = m;  // RESID on a coded matrix gathers w .* r instead (k_wr)
             return DFL_OK;
         }
+    }
+    // delta/value-coded rows: only where no pre-scaled copy is needed (P, R)
+    if (g_use_pcode && !g_use_coarse && !g_use_tiny && allow_code && allow_ell && !colscale && h.nrows > 0) {
+        bool ok = false;
+        RC(try_upload_pcode(ctx, h, m, ok));
+        if (ok) return DFL_OK;
     }
     const int64_t nsl = cdiv(h.nrows, 32);
     auto rlen = [&](int64_t i) { return h.ptr[i + 1] - h.ptr[i]; };

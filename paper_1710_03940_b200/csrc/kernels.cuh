@@ -30,7 +30,17 @@ constexpr int kEllUnroll = 8;     // slice widths up to this are fully unrolled
 #define DFL_ELL_BATCH 8
 #endif
 
-enum { FMT_ELL = 0, FMT_CSR = 1, FMT_CODE = 2, FMT_CLASS = 3 };
+enum { FMT_ELL = 0, FMT_CSR = 1, FMT_CODE = 2, FMT_CLASS = 3, FMT_PCODE = 4 };
+
+// FMT_PCODE ("delta/value-coded rows"): matrices with <= 7 entries per row,
+// column-sorted rows whose columns lie within 65535 of the row's first one and
+// <= 15 distinct values -- the smoothed prolongation of a structured problem
+// (150^3: 9 values, deltas <= 12597).  Per row, structure-of-arrays: the first
+// column (int32), six 16-bit column deltas (3 x uint32) and one uint32 holding
+// the length (3 bits) and seven 4-bit value codes; the value table (16
+// doubles) is staged in shared memory.  20 bytes per row instead of 12 per
+// ELL slot (72 at width 6); lossless, CSR order, no FMA: bit-identical.
+constexpr int kPcMaxLen = 7;
 
 // FMT_CLASS ("row-class coded"): one byte per row.  The most frequent row
 // (the interior stencil: ordered (column - row, value) entries, <= 7) is the
@@ -90,6 +100,11 @@ struct DMat {
     // FMT_CLASS
     const uint8_t *cls = nullptr;        // class of every row
     int class_id = -1;                   // index of the ClassTab in the context
+    // FMT_PCODE
+    const int *pc_c0 = nullptr;          // first column of every row
+    const uint32_t *pc_d = nullptr;      // 3 x nrows: 16-bit deltas of entries 1..6 (SoA)
+    const uint32_t *pc_v = nullptr;      // length | 4-bit value codes << (3 + 4k)
+    const double *pc_tab = nullptr;      // 16 values
     const int *ctab_delta = nullptr;     // column - row of each code
     const double *ctab_val = nullptr;    // value of each code
     int ncodes = 0;
@@ -941,6 +956,52 @@ __global__ void __launch_bounds__(kBlock, MODE == MODE_RESID ? 4 : DFL_CLASS_MIN
         ri = rn;
         wi = wn;
         xi = xn;
+    }
+    if (DOT) {
+        __shared__ double sm[32];
+        double v[1] = {dot};
+        block_sum<1>(v, sm);
+        dot_out(a.fin, a.dot_part, v[0]);
+    }
+}
+
+// FMT_PCODE row kernel: one row per thread
+template <int MODE, bool DOT>
+__global__ void __launch_bounds__(kBlock) k_pcode(DMat A, RowArgs a) {
+    DFL_PDL_ENTRY;
+    __shared__ double tab[16];
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    const bool valid = i < A.nrows;
+    int c0 = 0;
+    uint32_t d0 = 0, d1 = 0, d2 = 0, vw = 0;
+    if (valid) {
+        c0 = __ldcs(A.pc_c0 + i);
+        vw = __ldcs(A.pc_v + i);
+        d0 = __ldcs(A.pc_d + i);
+        d1 = __ldcs(A.pc_d + A.nrows + i);
+        d2 = __ldcs(A.pc_d + 2 * A.nrows + i);
+    }
+    if (threadIdx.x < 16) tab[threadIdx.x] = A.pc_tab[threadIdx.x];
+    __syncthreads();
+    double dot = 0.0;
+    if (valid) {
+        const int len = (int)(vw & 7u);
+        const uint32_t dl[3] = {d0, d1, d2};
+        const double *x = MODE == MODE_RESID ? a.r : a.x;
+        double xv[kPcMaxLen];
+#pragma unroll
+        for (int k = 0; k < kPcMaxLen; ++k)
+            if (k < len) {
+                const int col = k == 0 ? c0 : c0 + (int)((dl[(k - 1) >> 1] >> (16 * ((k - 1) & 1))) & 0xffffu);
+                xv[k] = __ldg(x + col);
+            }
+        double acc = 0.0;
+#pragma unroll
+        for (int k = 0; k < kPcMaxLen; ++k)
+            if (k < len) acc = add_rn(acc, mul_rn(tab[(vw >> (3 + 4 * k)) & 0xfu], xv[k]));
+        const double y = epilogue<MODE>(a, i, acc);
+        a.out[i] = y;
+        if (DOT) dot = __ldg(a.r + i) * y;
     }
     if (DOT) {
         __shared__ double sm[32];

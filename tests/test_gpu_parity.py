@@ -61,6 +61,21 @@ def test_spmv_class_coded_bitwise(variant):
     assert np.array_equal(y, ref)
 
 
+@pytest.mark.parametrize("level", [0, 1])
+def test_spmv_prolongation_pcode_bitwise(level):
+    """The smoothed prolongation P of a structured problem (<= 7 entries, <= 15
+    distinct values: FMT_PCODE delta/value-coded rows at level 0; the generic
+    fallback at level 1) is bit-identical to spmv_rows."""
+    p = problems.poisson3d(20)
+    A = nat.CsrArrays(p.matrix.nrows, p.matrix.ncols, p.matrix.row_ptr, p.matrix.col_idx, p.matrix.values)
+    h = nat.Hierarchy(A, nat.AmgOptions(0.08, 2 / 3, 0.8, nat.DFL_RELAX["spai0"], 25, 500))
+    nr, nc, ptr, col, val = h.matrix(level, nat.LEVEL_P)
+    P = nat.CsrArrays(nr, nc, ptr, col, val)
+    x = np.random.default_rng(11).standard_normal(nc)
+    y = nat.spmv_device(P, x)
+    assert np.array_equal(y, port.spmv(port.Csr(nr, nc, ptr, col, val), x))
+
+
 def test_spmv_random_csr():
     rng = np.random.default_rng(3)
     n = 3000
