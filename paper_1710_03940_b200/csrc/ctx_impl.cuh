@@ -72,7 +72,7 @@ struct Nccl {
 extern Nccl g_nccl;
 
 // profiling / layout knobs (defined in ctx.cu, read at context creation)
-extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl, g_code_pipe, g_use_class, g_op_pf, g_use_pcode;
+extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl, g_code_pipe, g_use_class, g_op_pf, g_use_pcode, g_use_scode;
 extern double g_small_per_lane, g_csr_per_lane;
 extern int g_csr_g, g_sm_count;
 static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle
@@ -365,7 +365,7 @@ inline int64_t class_grid(const DMat &A) {
 
 // number of per-block / per-tile partials the POST-with-dot kernel on A produces
 inline int64_t parts_for(const DMat &A) {
-    if (A.fmt == FMT_PCODE) return cdiv(A.nrows, kBlock);
+    if (A.fmt == FMT_PCODE || A.fmt == FMT_SCODE) return cdiv(A.nrows, kBlock);
     if (A.fmt == FMT_CLASS) return class_grid<MODE_POST, true>(A);
     if (A.fmt == FMT_CODE || A.vcode) return code_grid<MODE_POST, true>(A);
     return A.pipe.stages ? A.pipe.ntiles : nblocks_for(A);
@@ -438,6 +438,11 @@ static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
     if (A.nrows == 0) return;
     if (A.fmt == FMT_PCODE) {
         launch_k(ctx->st, k_pcode<MODE, DOT>, (unsigned)cdiv(A.nrows, kBlock), kBlock, 0, A, a);
+        ctx->launches++;
+        return;
+    }
+    if (A.fmt == FMT_SCODE) {
+        launch_k(ctx->st, k_scode<MODE, DOT>, (unsigned)cdiv(A.nrows, kBlock), kBlock, 0, A, a);
         ctx->launches++;
         return;
     }

@@ -228,6 +228,81 @@ static int try_upload_pcode(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) 
     return DFL_OK;
 }
 
+// FMT_SCODE encoder (kernels.cuh): SELL-32 slots sorted by row length inside
+// windows of kSigmaS rows; ok = false leaves m untouched
+static constexpr int64_t kSigmaS = 1024;
+static int try_upload_scode(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) {
+    ok = false;
+    const int64_t n = h.nrows;
+    std::unordered_map<uint64_t, int> dict;
+    std::vector<double> tab;
+    auto rlen = [&](int64_t i) { return h.ptr[i + 1] - h.ptr[i]; };
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = h.ptr[i]; k < h.ptr[i + 1]; ++k) {
+            if (k > h.ptr[i]) {
+                const int64_t gap = h.col[k] - h.col[k - 1];
+                if (gap < 0 || gap > 65535) return DFL_OK;
+            }
+            uint64_t bits;
+            std::memcpy(&bits, &h.val[k], 8);
+            if (dict.find(bits) == dict.end()) {
+                if (dict.size() >= 255) return DFL_OK;
+                dict.emplace(bits, (int)tab.size());
+                tab.push_back(h.val[k]);
+            }
+        }
+    std::vector<int> perm(n);
+    for (int64_t w0 = 0; w0 < n; w0 += kSigmaS) {
+        const int64_t w1 = std::min(n, w0 + kSigmaS);
+        for (int64_t j = w0; j < w1; ++j) perm[j] = (int)j;
+        std::stable_sort(perm.begin() + w0, perm.begin() + w1, [&](int a, int b) { return rlen(a) > rlen(b); });
+    }
+    const int64_t nsl = cdiv(n, 32);
+    std::vector<int64_t> soff(nsl + 1, 0);
+    for (int64_t sl = 0; sl < nsl; ++sl) {
+        int64_t wmax = 0;
+        for (int64_t j = sl * 32; j < std::min(n, sl * 32 + 32); ++j) wmax = std::max(wmax, rlen(perm[j]));
+        soff[sl + 1] = soff[sl] + 32 * wmax;
+    }
+    std::vector<uint16_t> gap(soff[nsl], 0);
+    std::vector<uint8_t> code(soff[nsl], (uint8_t)kScPad);  // padding: skipped by the kernel
+    std::vector<int> c0(n, 0);
+    for (int64_t sl = 0; sl < nsl; ++sl)
+        for (int64_t j = sl * 32; j < std::min(n, sl * 32 + 32); ++j) {
+            const int64_t i = perm[j], b = h.ptr[i], e = h.ptr[i + 1];
+            if (e > b) c0[j] = (int)h.col[b];
+            for (int64_t k = b; k < e; ++k) {
+                const int64_t dst = soff[sl] + (k - b) * 32 + (j - sl * 32);
+                gap[dst] = (uint16_t)(k == b ? 0 : h.col[k] - h.col[k - 1]);
+                uint64_t bits;
+                std::memcpy(&bits, &h.val[k], 8);
+                code[dst] = (uint8_t)dict[bits];
+            }
+        }
+    int64_t *d_soff;
+    int *d_perm, *d_c0;
+    uint16_t *d_gap;
+    uint8_t *d_code;
+    double *d_tab;
+    RC(upload(ctx, &d_soff, soff.data(), nsl + 1));
+    RC(upload(ctx, &d_perm, perm.data(), std::max<int64_t>(1, n)));
+    RC(upload(ctx, &d_c0, c0.data(), std::max<int64_t>(1, n)));
+    RC(upload(ctx, &d_gap, gap.data(), std::max<int64_t>(1, soff[nsl])));
+    RC(upload(ctx, &d_code, code.data(), std::max<int64_t>(1, soff[nsl])));
+    RC(upload(ctx, &d_tab, tab.data(), std::max<int64_t>(1, (int64_t)tab.size())));
+    m.fmt = FMT_SCODE;
+    m.stored = soff[nsl];
+    m.slice_off = d_soff;
+    m.perm = d_perm;
+    m.pc_c0 = d_c0;
+    m.sc_gap = d_gap;
+    m.sc_code = d_code;
+    m.pc_tab = d_tab;
+    m.sc_ntab = (int)tab.size();
+    ok = true;
+    return DFL_OK;
+}
+
 // value codes for an ELL-layout matrix with <= 255 distinct values (bitwise)
 static int attach_value_codes(dfl_ctx *ctx, DMat &m, const std::vector<double> &val) {
     std::unordered_map<uint64_t, int> dict;
@@ -295,6 +370,12 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
         bool ok = false;
         RC(try_upload_pcode(ctx, h, m, ok));
         if (ok) return DFL_OK;
+        // long rows (the restriction): gap/value-coded SELL
+        const double meanr = h.nrows ? (double)m.nnz / (double)h.nrows : 0.0;
+        if (g_use_scode && h.nrows >= kSellMinRows && meanr >= kSellMinMean) {
+            RC(try_upload_scode(ctx, h, m, ok));
+            if (ok) return DFL_OK;
+        }
     }
     const int64_t nsl = cdiv(h.nrows, 32);
     auto rlen = [&](int64_t i) { return h.ptr[i + 1] - h.ptr[i]; };

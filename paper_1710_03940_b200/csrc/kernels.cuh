@@ -30,7 +30,16 @@ constexpr int kEllUnroll = 8;     // slice widths up to this are fully unrolled
 #define DFL_ELL_BATCH 8
 #endif
 
-enum { FMT_ELL = 0, FMT_CSR = 1, FMT_CODE = 2, FMT_CLASS = 3, FMT_PCODE = 4 };
+enum { FMT_ELL = 0, FMT_CSR = 1, FMT_CODE = 2, FMT_CLASS = 3, FMT_PCODE = 4, FMT_SCODE = 5 };
+
+// FMT_SCODE ("gap/value-coded SELL"): long-row matrices with <= 255 distinct
+// values whose consecutive columns in a row differ by < 65536 -- the
+// restriction R = P^T of a structured problem (150^3: 9 values, 28 entries
+// per row, gaps <= 22.5K).  SELL-32 slices (rows sorted by length inside 1024-row
+// windows, slot -> row permutation); per slot the first column (int32); per
+// entry a 16-bit column gap and an 8-bit value code, column-major inside the
+// slice.  3 bytes per entry instead of 12; the running column is summed
+// along the row; CSR order, no FMA: bit-identical.
 
 // FMT_PCODE ("delta/value-coded rows"): matrices with <= 7 entries per row,
 // column-sorted rows whose columns lie within 65535 of the row's first one and
@@ -100,6 +109,10 @@ struct DMat {
     // FMT_CLASS
     const uint8_t *cls = nullptr;        // class of every row
     int class_id = -1;                   // index of the ClassTab in the context
+    // FMT_SCODE (with slice_off, perm, pc_c0 per slot, pc_tab[<=256])
+    const uint16_t *sc_gap = nullptr;
+    const uint8_t *sc_code = nullptr;
+    int sc_ntab = 0;
     // FMT_PCODE
     const int *pc_c0 = nullptr;          // first column of every row
     const uint32_t *pc_d = nullptr;      // 3 x nrows: 16-bit deltas of entries 1..6 (SoA)
@@ -999,6 +1012,68 @@ __global__ void __launch_bounds__(kBlock) k_pcode(DMat A, RowArgs a) {
 #pragma unroll
         for (int k = 0; k < kPcMaxLen; ++k)
             if (k < len) acc = add_rn(acc, mul_rn(tab[(vw >> (3 + 4 * k)) & 0xfu], xv[k]));
+        const double y = epilogue<MODE>(a, i, acc);
+        a.out[i] = y;
+        if (DOT) dot = __ldg(a.r + i) * y;
+    }
+    if (DOT) {
+        __shared__ double sm[32];
+        double v[1] = {dot};
+        block_sum<1>(v, sm);
+        dot_out(a.fin, a.dot_part, v[0]);
+    }
+}
+
+constexpr unsigned kScPad = 255u;  // value code of the slice padding (skipped)
+#ifndef DFL_SC_CHUNK
+#define DFL_SC_CHUNK 8
+#endif
+#ifndef DFL_SC_MINB
+#define DFL_SC_MINB 6
+#endif
+
+// FMT_SCODE row kernel: one thread per slot
+template <int MODE, bool DOT>
+__global__ void __launch_bounds__(kBlock, DFL_SC_MINB) k_scode(DMat A, RowArgs a) {
+    DFL_PDL_ENTRY;
+    __shared__ double tab[256];
+    const int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x;  // storage slot
+    const bool valid = j < A.nrows;
+    int64_t off = 0;
+    int width = 0, col = 0;
+    if (valid) {
+        const int64_t s = j >> 5;
+        off = __ldg(A.slice_off + s);
+        width = (int)((__ldg(A.slice_off + s + 1) - off) >> 5);
+        off += j & 31;
+        col = __ldcs(A.pc_c0 + j);
+    }
+    for (int t = threadIdx.x; t < A.sc_ntab; t += kBlock) tab[t] = A.pc_tab[t];
+    __syncthreads();
+    double dot = 0.0;
+    if (valid) {
+        const int64_t i = A.perm ? (int64_t)__ldg(A.perm + j) : j;  // matrix row
+        const double *x = MODE == MODE_RESID ? a.r : a.x;
+        double acc = 0.0;
+        for (int k0 = 0; k0 < width; k0 += DFL_SC_CHUNK) {
+            unsigned g[DFL_SC_CHUNK], c[DFL_SC_CHUNK];
+#pragma unroll
+            for (int k = 0; k < DFL_SC_CHUNK; ++k)
+                if (k0 + k < width) {
+                    g[k] = __ldcs(A.sc_gap + off + 32 * (k0 + k));
+                    c[k] = __ldcs(A.sc_code + off + 32 * (k0 + k));
+                }
+            double xv[DFL_SC_CHUNK];
+#pragma unroll
+            for (int k = 0; k < DFL_SC_CHUNK; ++k)
+                if (k0 + k < width && c[k] != kScPad) {
+                    col += (int)g[k];
+                    xv[k] = __ldg(x + col);
+                }
+#pragma unroll
+            for (int k = 0; k < DFL_SC_CHUNK; ++k)
+                if (k0 + k < width && c[k] != kScPad) acc = add_rn(acc, mul_rn(tab[c[k]], xv[k]));
+        }
         const double y = epilogue<MODE>(a, i, acc);
         a.out[i] = y;
         if (DOT) dot = __ldg(a.r + i) * y;

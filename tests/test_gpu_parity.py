@@ -62,18 +62,26 @@ def test_spmv_class_coded_bitwise(variant):
 
 
 @pytest.mark.parametrize("level", [0, 1])
-def test_spmv_prolongation_pcode_bitwise(level):
+@pytest.mark.parametrize("which", ["P", "R"])
+def test_spmv_transfer_operators_coded_bitwise(level, which, monkeypatch):
     """The smoothed prolongation P of a structured problem (<= 7 entries, <= 15
-    distinct values: FMT_PCODE delta/value-coded rows at level 0; the generic
-    fallback at level 1) is bit-identical to spmv_rows."""
-    p = problems.poisson3d(20)
+    distinct values: FMT_PCODE delta/value-coded rows at level 0) and the
+    restriction R = P^T (long rows, 9 values: FMT_SCODE gap/value-coded SELL,
+    100^3 so that it has >= 100K rows) are bit-identical to spmv_rows; the
+    generic fallbacks at level 1 (multi-lane CSR for R) agree to rounding."""
+    monkeypatch.setenv("DFL_SCODE", "1")  # opt-in format, read at context creation
+    p = problems.poisson3d(100 if which == "R" and level == 0 else 20)
     A = nat.CsrArrays(p.matrix.nrows, p.matrix.ncols, p.matrix.row_ptr, p.matrix.col_idx, p.matrix.values)
     h = nat.Hierarchy(A, nat.AmgOptions(0.08, 2 / 3, 0.8, nat.DFL_RELAX["spai0"], 25, 500))
-    nr, nc, ptr, col, val = h.matrix(level, nat.LEVEL_P)
+    nr, nc, ptr, col, val = h.matrix(level, nat.LEVEL_P if which == "P" else nat.LEVEL_R)
     P = nat.CsrArrays(nr, nc, ptr, col, val)
     x = np.random.default_rng(11).standard_normal(nc)
     y = nat.spmv_device(P, x)
-    assert np.array_equal(y, port.spmv(port.Csr(nr, nc, ptr, col, val), x))
+    ref = port.spmv(port.Csr(nr, nc, ptr, col, val), x)
+    if level == 0:
+        assert np.array_equal(y, ref)
+    else:
+        np.testing.assert_allclose(y, ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
 
 
 def test_spmv_random_csr():
