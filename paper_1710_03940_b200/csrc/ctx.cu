@@ -18,6 +18,7 @@ bool g_use_coarse = false;  // cooperative coarse-cycle kernel (DFL_COARSE=1; me
 bool g_allow_sell = false;    // DFL_SELL=1: SELL-C-sigma for every irregular matrix
 bool g_wr_split = false;      // DFL_WR_SPLIT=1: coded residual reads w .* r from a k_wr pass
 bool g_no_fin = true;         // DFL_FIN=1: CG scalars finished in the producing kernels (measured slower)
+bool g_sell_wave = false;     // DFL_SELL_WAVE=1: sliced ELL grid-stride over one resident wave
 bool g_use_scode = false;     // DFL_SCODE=1: gap/value-coded SELL for R (measured slower: 71 vs 41 us)
 bool g_use_pcode = true;      // DFL_NO_PCODE=1: no delta/value-coded rows (P)
 bool g_op_pf = true;          // DFL_OP_PF=0: no next-wave L2 prefetch in the class-coded operator
@@ -122,6 +123,8 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
         g_wr_split = ws && ws[0] == '1';
         const char *nf = getenv("DFL_FIN");
         g_no_fin = !(nf && nf[0] == '1');
+        const char *swv = getenv("DFL_SELL_WAVE");
+        g_sell_wave = swv && swv[0] == '1';
         const char *nsc = getenv("DFL_SCODE");
         g_use_scode = nsc && nsc[0] == '1';
         const char *npc = getenv("DFL_NO_PCODE");

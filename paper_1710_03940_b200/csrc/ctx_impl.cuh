@@ -72,7 +72,7 @@ struct Nccl {
 extern Nccl g_nccl;
 
 // profiling / layout knobs (defined in ctx.cu, read at context creation)
-extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl, g_code_pipe, g_use_class, g_op_pf, g_use_pcode, g_use_scode;
+extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl, g_code_pipe, g_use_class, g_op_pf, g_use_pcode, g_use_scode, g_sell_wave;
 extern double g_small_per_lane, g_csr_per_lane;
 extern int g_csr_g, g_sm_count;
 static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle
@@ -363,12 +363,24 @@ inline int64_t class_grid(const DMat &A) {
     return std::max<int64_t>(1, std::min<int64_t>(cdiv(A.nrows, kBlock), (int64_t)occ * g_sm_count));
 }
 
+// grid of the sliced-ELL kernels: every slot (default) or one resident wave
+// run grid-stride (DFL_SELL_WAVE=1)
+template <int MODE, bool DOT>
+inline int64_t sell_grid(const DMat &A) {
+    const int64_t nb = cdiv(A.nrows, kBlock);
+    if (!g_sell_wave) return nb;
+    static const int occ = occupancy(k_ell<MODE, DOT, 0>);
+    return std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)occ * g_sm_count));
+}
+
 // number of per-block / per-tile partials the POST-with-dot kernel on A produces
 inline int64_t parts_for(const DMat &A) {
     if (A.fmt == FMT_PCODE || A.fmt == FMT_SCODE) return cdiv(A.nrows, kBlock);
     if (A.fmt == FMT_CLASS) return class_grid<MODE_POST, true>(A);
     if (A.fmt == FMT_CODE || A.vcode) return code_grid<MODE_POST, true>(A);
-    return A.pipe.stages ? A.pipe.ntiles : nblocks_for(A);
+    if (g_use_pipe && A.pipe.stages) return A.pipe.ntiles;
+    if (A.fmt == FMT_ELL && A.ell_w == 0) return sell_grid<MODE_POST, true>(A);
+    return nblocks_for(A);
 }
 
 inline size_t pipe_smem(const DMat &A) { return 128 + (size_t)A.pipe.stages * A.pipe.cap * 12; }
@@ -489,7 +501,7 @@ static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
             case 6: launch_k(ctx->st, k_ell<MODE, DOT, 6>, grid, kBlock, 0, A, a); break;
             case 7: launch_k(ctx->st, k_ell<MODE, DOT, 7>, grid, kBlock, 0, A, a); break;
             case 8: launch_k(ctx->st, k_ell<MODE, DOT, 8>, grid, kBlock, 0, A, a); break;
-            default: launch_k(ctx->st, k_ell<MODE, DOT, 0>, grid, kBlock, 0, A, a); break;
+            default: launch_k(ctx->st, k_ell<MODE, DOT, 0>, (unsigned)sell_grid<MODE, DOT>(A), kBlock, 0, A, a); break;
         }
     } else
         launch_csr_mode<MODE, DOT>(A, a, ctx->st);

@@ -702,9 +702,10 @@ __device__ __forceinline__ double epilogue(const RowArgs &a, int64_t i, double a
 template <int MODE, bool DOT, int W>
 __global__ void __launch_bounds__(kBlock, W == 0 ? DFL_ELL_MINB0 : DFL_ELL_MINB) k_ell(DMat A, RowArgs a) {
     DFL_PDL_ENTRY;
-    const int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x;  // storage slot
     double dot = 0.0;
-    if (j < A.nrows) {
+    // one slot per thread; sliced matrices (W == 0) may run grid-stride over
+    // one resident wave (launch_rows, DFL_SELL_WAVE)
+    for (int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x; j < A.nrows; j += (int64_t)gridDim.x * kBlock) {
         const int64_t i = (W == 0 && A.perm) ? (int64_t)__ldg(A.perm + j) : j;  // matrix row
         double ax;
         if (MODE == MODE_RESID)
@@ -713,7 +714,7 @@ __global__ void __launch_bounds__(kBlock, W == 0 ? DFL_ELL_MINB0 : DFL_ELL_MINB)
             ax = ell_any<W>(A, j, GatherX{a.x});
         const double y = epilogue<MODE>(a, i, ax);
         a.out[i] = y;
-        if (DOT) dot = __ldg(a.r + i) * y;
+        if (DOT) dot += __ldg(a.r + i) * y;
     }
     if (DOT) {
         __shared__ double sm[32];
