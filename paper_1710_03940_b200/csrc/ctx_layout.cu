@@ -408,7 +408,7 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
     } else if (allow_ell && (double)soff[nsl] <= 1.03 * nnzd) {
         ell = true;
     } else if (allow_ell && allow_sell && maxlen <= 1024 &&
-               (g_allow_sell || (h.nrows >= kSellMinRows && mean >= kSellMinMean))) {
+               (g_allow_sell || (!g_no_sell && h.nrows >= kSellMinRows && mean >= kSellMinMean))) {
         perm.resize(h.nrows);
         for (int64_t w0 = 0; w0 < h.nrows; w0 += kSigma) {
             const int64_t w1 = std::min(h.nrows, w0 + kSigma);
