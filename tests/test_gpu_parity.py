@@ -395,3 +395,24 @@ def test_initial_guess_edge_cases():
     x_a, rep_a = s.solve(b)
     x_b, rep_b = s.solve(b, x0=xs)
     assert np.array_equal(x_a, x_b) and rep_a["iterations"] == rep_b["iterations"]
+
+
+@pytest.mark.parametrize("loop", ["graph", "host"])
+def test_true_residual_refresh_past_50_iterations(loop, monkeypatch):
+    """A solve that crosses the every-50-iterations true-residual refresh
+    (krylov.py:128-129): with the device graph it is an IF-conditional node,
+    with the host-driven loop a predicated kernel sequence.  1e6 coefficient
+    jumps, weak damped Jacobi, no deflation: ~95 CG iterations."""
+    if loop == "host":
+        monkeypatch.setenv("DFL_NO_GRAPH", "1")
+    cfgd = {"solver": {"type": "cg", "tol": 1e-12, "maxiter": 200},
+            "precond": {"relax": {"type": "damped_jacobi", "damping": 0.2}}}
+    p = problems.make_problem(32, problems.boxes_for(2), "jump", contrast=1e6)
+    x, rep = _solver(p, 2, cfgd, deflated=False).solve(p.rhs)
+    xo, ro = _oracle(p, 2, cfgd, deflated=False).solve(p.rhs)
+    assert ro["iterations"] > 50
+    assert rep["device_loop"] == (loop == "graph")
+    assert rep["converged"] == ro["converged"]
+    assert abs(rep["iterations"] - ro["iterations"]) <= 1, (rep["iterations"], ro["iterations"])
+    assert rep["relative_residual"] <= 2 * ro["relative_residual"]
+    assert np.linalg.norm(x - xo) <= 1e-6 * np.linalg.norm(xo)
