@@ -107,7 +107,7 @@ int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op, boo
         return DFL_OK;
     }
     if (!multi(ctx)) {
-        launch_k(ctx->st, k_zt_finish, ctx->nsub * ctx->k, 512, 0, ctx->zt_part, sub_tiles, ctx->nsub, ctx->k,
+        launch_k(ctx->st, k_zt_finish, ctx->nsub * ctx->k, 1024, 0, ctx->zt_part, sub_tiles, ctx->nsub, ctx->k,
                                                              ctx->tvec, 0, ctx->inexact ? nullptr : ctx->Einv,
                                                              ctx->K, ctx->t2, st, need_refresh, ctx->ticket,
                                                              from_op && ctx->split ? ctx->sub_btiles : nullptr,
@@ -123,7 +123,7 @@ int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op, boo
     // local entries into a padded slot, allgather, unpack, solve
     const int64_t slot = (int64_t)ctx->max_nsub * ctx->k;
     double *mine = ctx->tgather + (int64_t)ctx->rank * slot;
-    launch_k(ctx->st, k_zt_finish, ctx->nsub * ctx->k, 512, 0, ctx->zt_part, sub_tiles, ctx->nsub, ctx->k, mine, 0,
+    launch_k(ctx->st, k_zt_finish, ctx->nsub * ctx->k, 1024, 0, ctx->zt_part, sub_tiles, ctx->nsub, ctx->k, mine, 0,
                                                          nullptr, ctx->K, nullptr, st, need_refresh, ctx->ticket,
                                                          from_op && ctx->split ? ctx->sub_btiles : nullptr,
                                                          ctx->ntiles);

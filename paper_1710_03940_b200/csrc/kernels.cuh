@@ -1442,7 +1442,7 @@ static __global__ void __launch_bounds__(kBlock) k_zt_vec(Tiles T, const double 
 // first_col); one block per coarse value, fixed-order strided sums + tree.
 // The last block to finish (atomic ticket) then solves t2 = E^{-1} t with
 // the replicated inverse (Einv == nullptr: skip, multi-rank path).
-static __global__ void __launch_bounds__(512) k_zt_finish(const double *__restrict__ zt_part,
+static __global__ void __launch_bounds__(1024) k_zt_finish(const double *__restrict__ zt_part,
                                                    const int64_t *__restrict__ sub_tiles, int nsub, int k,
                                                    double *t_out, int64_t first_col, const double *Einv,
                                                    int64_t K, double *t2, const KState *st, int need_refresh,
@@ -1454,11 +1454,23 @@ static __global__ void __launch_bounds__(512) k_zt_finish(const double *__restri
     const int v = blockIdx.x;
     const int s = v / k, c = v % k;
     const int64_t t0 = sub_tiles[s], t1 = sub_tiles[s + 1];
-    double acc = 0.0;
-    for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) acc += zt_part[t * k + c];
+    // four independent accumulators: the strided loads of a thread are in
+    // flight together instead of one L2 round trip per tile (fixed order:
+    // deterministic)
+    const int64_t bs = blockDim.x;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    int64_t t = t0 + threadIdx.x;
+    for (; t + 3 * bs < t1; t += 4 * bs) {
+        a0 += zt_part[t * k + c];
+        a1 += zt_part[(t + bs) * k + c];
+        a2 += zt_part[(t + 2 * bs) * k + c];
+        a3 += zt_part[(t + 3 * bs) * k + c];
+    }
+    for (; t < t1; t += bs) a0 += zt_part[t * k + c];
+    double acc = (a0 + a1) + (a2 + a3);
     if (sub_tiles2)  // boundary-row tiles of the halo-overlapped operator
-        for (int64_t t = toff2 + sub_tiles2[s] + threadIdx.x; t < toff2 + sub_tiles2[s + 1]; t += blockDim.x)
-            acc += zt_part[t * k + c];
+        for (int64_t t2i = toff2 + sub_tiles2[s] + threadIdx.x; t2i < toff2 + sub_tiles2[s + 1]; t2i += bs)
+            acc += zt_part[t2i * k + c];
     __shared__ double sm[32];
     double val[1] = {acc};
     block_sum<1>(val, sm);
