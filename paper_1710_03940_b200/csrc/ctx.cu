@@ -18,6 +18,7 @@ bool g_use_coarse = false;  // cooperative coarse-cycle kernel (DFL_COARSE=1; me
 bool g_allow_sell = false;    // DFL_SELL=1: SELL-C-sigma for every irregular matrix
 bool g_wr_split = false;      // DFL_WR_SPLIT=1: coded residual reads w .* r from a k_wr pass
 bool g_no_fin = true;         // DFL_FIN=1: CG scalars finished in the producing kernels (measured slower)
+bool g_nccl_graph = false;    // DFL_NCCL_GRAPH=1: several NCCL ranks replay the captured CG body (measured neutral on 1 rank)
 bool g_no_sell = false;       // DFL_NO_SELL=1: long-row matrices as CSR-vector instead of SELL
 bool g_sell_wave = false;     // DFL_SELL_WAVE=1: sliced ELL grid-stride over one resident wave
 bool g_use_scode = false;     // DFL_SCODE=1: gap/value-coded SELL for R (measured slower: 71 vs 41 us)
@@ -124,6 +125,8 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
         g_wr_split = ws && ws[0] == '1';
         const char *nf = getenv("DFL_FIN");
         g_no_fin = !(nf && nf[0] == '1');
+        const char *ngr = getenv("DFL_NCCL_GRAPH");
+        g_nccl_graph = ngr && ngr[0] == '1';
         const char *nse = getenv("DFL_NO_SELL");
         g_no_sell = nse && nse[0] == '1';
         const char *swv = getenv("DFL_SELL_WAVE");
@@ -160,6 +163,10 @@ void dfl_ctx_destroy(dfl_ctx *ctx) {
     if (ctx->st) cudaStreamSynchronize(ctx->st);
     if (ctx->loop_exec) cudaGraphExecDestroy(ctx->loop_exec);
     if (ctx->bg_exec) cudaGraphExecDestroy(ctx->bg_exec);
+    if (ctx->body_exec) cudaGraphExecDestroy(ctx->body_exec);
+    if (ctx->h_state2) cudaFreeHost(ctx->h_state2);
+    for (cudaEvent_t e : ctx->ev_it)
+        if (e) cudaEventDestroy(e);
     if (ctx->h_bstate) cudaFreeHost(ctx->h_bstate);
     for (void *p : ctx->allocs) cudaFree(p);
     if (ctx->h_state) cudaFreeHost(ctx->h_state);

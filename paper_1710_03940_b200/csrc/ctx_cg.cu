@@ -292,6 +292,32 @@ static int build_loop_graph(dfl_ctx *ctx, bool deflated) {
     return DFL_OK;
 }
 
+// the CG body as a plain graph (several NCCL ranks: no conditional nodes)
+static int build_body_graph(dfl_ctx *ctx, bool deflated) {
+    const int key = deflated ? 1 : 0;
+    if (ctx->body_exec && ctx->body_key == key) return DFL_OK;
+    if (ctx->body_exec) {
+        cudaGraphExecDestroy(ctx->body_exec);
+        ctx->body_exec = nullptr;
+    }
+    if (!ctx->h_state2) CK(cudaMallocHost(&ctx->h_state2, 2 * sizeof(KState)));
+    for (int q = 0; q < 2; ++q)
+        if (!ctx->ev_it[q]) CK(cudaEventCreateWithFlags(&ctx->ev_it[q], cudaEventDisableTiming));
+    CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+    const int64_t before = ctx->launches;
+    int rc = cg_body(ctx, deflated, CgGraph{});
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(ctx->st, &g);
+    if (rc != DFL_OK) return rc;
+    CK(ce);
+    ctx->body_graph_kernels = ctx->launches - before;
+    ctx->launches = before;
+    CK(cudaGraphInstantiate(&ctx->body_exec, g, 0));
+    cudaGraphDestroy(g);
+    ctx->body_key = key;
+    return DFL_OK;
+}
+
 // ---------------------------------------------------------------------------
 // the whole solve on the device: b, x in ctx->b / ctx->xin
 int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
@@ -346,6 +372,24 @@ int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
     if (use_graph) {
         RC(build_loop_graph(ctx, defl));
         CK(cudaGraphLaunch(ctx->loop_exec, ctx->st));
+    } else if (ctx->comm && g_nccl_graph) {
+        // NCCL ranks: the body (collectives included) captured once and replayed
+        // per iteration; the host reads `done` one iteration late, so the GPU
+        // always has the next iteration queued.  The extra iteration after the
+        // last one skips its updates (KState.done) on every rank alike.
+        RC(build_body_graph(ctx, defl));
+        int64_t replays = 0;
+        for (int it = 0;; ++it) {
+            CK(cudaGraphLaunch(ctx->body_exec, ctx->st));
+            ++replays;
+            CK(cudaMemcpyAsync(ctx->h_state2 + (it & 1), st, sizeof(KState), cudaMemcpyDeviceToHost, ctx->st));
+            CK(cudaEventRecord(ctx->ev_it[it & 1], ctx->st));
+            if (it > 0) {
+                CK(cudaEventSynchronize(ctx->ev_it[(it - 1) & 1]));
+                if (ctx->h_state2[(it - 1) & 1].done) break;
+            }
+        }
+        ctx->launches += ctx->body_graph_kernels * replays;
     } else {
         for (;;) {
             RC(cg_body(ctx, defl, CgGraph{}));

@@ -72,7 +72,7 @@ struct Nccl {
 extern Nccl g_nccl;
 
 // profiling / layout knobs (defined in ctx.cu, read at context creation)
-extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl, g_code_pipe, g_use_class, g_op_pf, g_use_pcode, g_use_scode, g_sell_wave, g_no_sell;
+extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl, g_code_pipe, g_use_class, g_op_pf, g_use_pcode, g_use_scode, g_sell_wave, g_no_sell, g_nccl_graph;
 extern double g_small_per_lane, g_csr_per_lane;
 extern int g_csr_g, g_sm_count;
 static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle
@@ -237,6 +237,12 @@ struct dfl_ctx {
     cudaGraphExec_t loop_exec = nullptr;
     int loop_key = -1;
     int64_t body_kernels = 0;
+    // several NCCL ranks: the CG body replayed as a graph, done read one iteration late
+    cudaGraphExec_t body_exec = nullptr;
+    int body_key = -1;
+    int64_t body_graph_kernels = 0;
+    KState *h_state2 = nullptr;  // pinned, 2
+    cudaEvent_t ev_it[2] = {nullptr, nullptr};
     // BiCGStab(2) device loop (ctx_bicg.cu)
     void *bstate = nullptr, *h_bstate = nullptr;
     cudaGraphExec_t bg_exec = nullptr;

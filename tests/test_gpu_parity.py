@@ -180,12 +180,15 @@ def test_config1_fingerprint():
     assert not x0.any() and rep0["iterations"] == 0 and rep0["converged"]
 
 
+@pytest.mark.parametrize("replay", ["0", "1"])
 @pytest.mark.parametrize("name", ["config1_32_m4_cg_spai0_const", "p16_m8_cg_spai0_lin", "p16_m4_bicg_spai0_lin"])
-def test_multirank_code_path_on_one_gpu(name, monkeypatch):
+def test_multirank_code_path_on_one_gpu(name, replay, monkeypatch):
     """DFL_FORCE_COMM=1 gives the context a 1-rank NCCL communicator, so the
     multi-rank code path (host-driven loop, NCCL allgathers of the Z'w slots and
-    of the Krylov scalars, rank-ordered sums) runs on one GPU."""
+    of the Krylov scalars, rank-ordered sums) runs on one GPU; DFL_NCCL_GRAPH=1
+    replays the captured CG body (collectives inside) with the late done check."""
     monkeypatch.setenv("DFL_FORCE_COMM", "1")
+    monkeypatch.setenv("DFL_NCCL_GRAPH", replay)
     case = solve_case(name)
     p = problems.make_problem(case["shape"], problems.boxes_for(case["m"]), case["kind"])
     s = _solver(p, case["m"], case["config"])
