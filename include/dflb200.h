@@ -232,6 +232,12 @@ DFL_API int64_t dfl_ctx_device_bytes(const dfl_ctx *ctx);
 DFL_API int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *x, int ptr_kind,
               dfl_report *rep);
 
+/* page-locked host buffers for solve results (cached: a freed block is reused by the next
+ * allocation of the same size, so x can be read back at full copy speed without pinning
+ * memory on every solve).  NULL when the driver refuses the allocation. */
+DFL_API void *dfl_host_alloc(int64_t bytes);
+DFL_API void dfl_host_free(void *ptr);
+
 /* unit operations on this rank's vectors (n_local), host or device pointers */
 DFL_API int dfl_op_apply(dfl_ctx *ctx, const double *x, double *y, int ptr_kind);
 DFL_API int dfl_precond_apply(dfl_ctx *ctx, const double *r, double *z, int ptr_kind);

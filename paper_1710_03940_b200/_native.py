@@ -113,6 +113,8 @@ def lib():
         "dfl_ctx_set_inexact": ([c_vp, c_vp, c_dbl], c_i32),
         "dfl_ctx_device_bytes": ([c_vp], c_i64),
         "dfl_solve": ([c_vp, P(SolveParams), c_vp, c_vp, c_i32, P(Report)], c_i32),
+        "dfl_host_alloc": ([c_i64], c_vp),
+        "dfl_host_free": ([c_vp], None),
         "dfl_op_apply": ([c_vp, c_vp, c_vp, c_i32], c_i32),
         "dfl_precond_apply": ([c_vp, c_vp, c_vp, c_i32], c_i32),
         "dfl_project": ([c_vp, c_vp, c_vp, c_i32], c_i32),
@@ -149,6 +151,20 @@ def exported_symbols():
     with open(hdr) as fh:
         text = fh.read()
     return sorted(set(re.findall(r"\b(dfl_[a-z0-9_]+)\s*\(", text)))
+
+
+def pinned_empty(n: int) -> np.ndarray:
+    """float64[n] in page-locked host memory from the library's block cache
+    (dfl_host_alloc); the block goes back to the cache when the array (and
+    every view of it) is gone.  Pageable memory if the driver refuses."""
+    import weakref
+
+    p = lib().dfl_host_alloc(8 * n) if n > 0 else None
+    if not p:
+        return np.empty(n)
+    buf = (ctypes.c_double * n).from_address(p)
+    weakref.finalize(buf, lib().dfl_host_free, c_vp(p))
+    return np.frombuffer(buf, dtype=np.float64)
 
 
 def _ptr(a: np.ndarray):

@@ -4,6 +4,8 @@
 // while-conditional, so a whole CG solve is a handful of launches and no
 // host round trip per iteration (single rank); with several ranks the loop is
 // host-driven with NCCL collectives between kernels.
+#include <map>
+#include <mutex>
 #include "ctx_impl.cuh"
 
 bool g_use_pipe = false;  // TMA-staged variant (DFL_PIPE=1); see profiles/r01
@@ -176,6 +178,7 @@ void dfl_ctx_destroy(dfl_ctx *ctx) {
     if (ctx->ev1) cudaEventDestroy(ctx->ev1);
     if (ctx->comm) g_nccl.CommDestroy(ctx->comm);
     if (ctx->st2) cudaStreamDestroy(ctx->st2);
+    if (ctx->st_copy) cudaStreamDestroy(ctx->st_copy);
     if (ctx->st_if) cudaStreamDestroy(ctx->st_if);
     if (ctx->ev_packed) cudaEventDestroy(ctx->ev_packed);
     if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
@@ -503,18 +506,30 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev1, ctx->st));
+    // x goes back on its own stream while the true-residual kernels run on
+    // the solve stream (both only read xin)
+    if (!ctx->st_copy) CK(cudaStreamCreateWithFlags(&ctx->st_copy, cudaStreamNonBlocking));
+    CK(cudaStreamWaitEvent(ctx->st_copy, ctx->ev1, 0));
     CK(cudaMemcpyAsync(x, ctx->xin, sizeof(double) * ctx->n,
-                       ptr_kind == DFL_PTR_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->st));
-    CK(cudaEventRecord(e_h1, ctx->st));
+                       ptr_kind == DFL_PTR_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->st_copy));
+    CK(cudaEventRecord(e_h1, ctx->st_copy));
     CK(cudaMemcpyAsync(ctx->h_state, ctx->state, sizeof(KState), cudaMemcpyDeviceToHost, ctx->st));
     CK(cudaStreamSynchronize(ctx->st));
+    const KState s = bicg ? bstate : *ctx->h_state;
+    // true residual ||b - A x|| / ||b|| (deflation.py:293-297; outside the timed span)
+    const int64_t solve_launches = ctx->launches;
+    double rr = 0.0;
+    if (s.bnorm != 0.0) {
+        RC(op_apply_dev(ctx, ctx->xin, ctx->tmp, 1, ctx->b, false, nullptr, 0));
+        RC(rank_dot(ctx, ctx->tmp, ctx->tmp, &rr));
+    }
+    CK(cudaStreamSynchronize(ctx->st_copy));
     float ms_h2d = 0, ms_solve = 0, ms_d2h = 0;
     CK(cudaEventElapsedTime(&ms_h2d, e_h0, ctx->ev0));
     CK(cudaEventElapsedTime(&ms_solve, ctx->ev0, ctx->ev1));
     CK(cudaEventElapsedTime(&ms_d2h, ctx->ev1, e_h1));
     cudaEventDestroy(e_h0);
     cudaEventDestroy(e_h1);
-    const KState s = bicg ? bstate : *ctx->h_state;
     rep->iterations = s.iters;
     rep->converged = s.converged || (s.resnorm <= s.target);
     if (s.breakdown) rep->converged = 0;
@@ -525,19 +540,45 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     rep->solve_seconds = ms_solve * 1e-3;
     rep->h2d_seconds = ms_h2d * 1e-3;
     rep->d2h_seconds = ms_d2h * 1e-3;
-    rep->kernel_launches = ctx->launches + (use_graph ? ctx->body_kernels * std::max(1, s.iters) +
+    rep->kernel_launches = solve_launches + (use_graph ? ctx->body_kernels * std::max(1, s.iters) +
                                                             ctx->if_kernels * (s.iters / std::max(1, p->refresh_every))
                                                       : 0);
-    // true residual ||b - A x|| / ||b|| (deflation.py:293-297; outside the timed span)
-    if (s.bnorm == 0.0) {
-        rep->relative_residual = 0.0;
-    } else {
-        RC(op_apply_dev(ctx, ctx->xin, ctx->tmp, 1, ctx->b, false, nullptr, 0));
-        double rr = 0.0;
-        RC(rank_dot(ctx, ctx->tmp, ctx->tmp, &rr));
-        rep->relative_residual = std::sqrt(std::max(rr, 0.0)) / s.bnorm;
-    }
+    rep->relative_residual = s.bnorm == 0.0 ? 0.0 : std::sqrt(std::max(rr, 0.0)) / s.bnorm;
     return DFL_OK;
+}
+
+// pinned host block cache (bytes -> free blocks; live block -> bytes)
+static std::mutex g_host_mu;
+static std::multimap<int64_t, void *> g_host_free;
+static std::map<void *, int64_t> g_host_live;
+
+void *dfl_host_alloc(int64_t bytes) {
+    if (bytes <= 0) return nullptr;
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    void *p = nullptr;
+    auto it = g_host_free.find(bytes);
+    if (it != g_host_free.end()) {
+        p = it->second;
+        g_host_free.erase(it);
+    } else if (cudaHostAlloc(&p, (size_t)bytes, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    g_host_live[p] = bytes;
+    return p;
+}
+
+void dfl_host_free(void *ptr) {
+    if (!ptr) return;
+    std::lock_guard<std::mutex> lk(g_host_mu);
+    auto it = g_host_live.find(ptr);
+    if (it == g_host_live.end()) return;
+    // keep at most four cached blocks per size
+    if (g_host_free.count(it->second) < 4)
+        g_host_free.emplace(it->second, ptr);
+    else
+        cudaFreeHost(ptr);
+    g_host_live.erase(it);
 }
 
 int dfl_op_apply(dfl_ctx *ctx, const double *x, double *y, int ptr_kind) {

@@ -144,6 +144,7 @@ struct dfl_ctx {
     std::vector<int64_t> op_sub_tiles_h;
     int64_t *op_sub_tiles = nullptr;   // first op-pipe tile of every subdomain
     cudaStream_t st = nullptr;
+    cudaStream_t st_copy = nullptr;  // x read-back, overlapped with the true-residual kernels
     std::string err;
     std::vector<void *> allocs;
     int64_t bytes = 0;

@@ -221,7 +221,8 @@ class DeflatedSolver:
             x_local = np.array(self._local(x0), dtype=np.float64, copy=True)
             params.x0_given = 1
         else:
-            x_local = np.empty(self.n_local)
+            # page-locked, so the read-back of x runs at full copy speed
+            x_local = nat.pinned_empty(self.n_local)
         t0 = time.perf_counter()
         rep = self._ctx.solve(params, b_local, x_local)
         wall = time.perf_counter() - t0
