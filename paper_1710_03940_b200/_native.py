@@ -87,6 +87,7 @@ def lib():
         "dfl_last_setup_error": ([], ctypes.c_char_p),
         "dfl_breakdown_string": ([c_i32], ctypes.c_char_p),
         "dfl_hier_build": ([P(Csr), P(AmgOptions), P(c_vp)], c_i32),
+        "dfl_setup_device": ([c_i32], c_i32),
         "dfl_hier_num_levels": ([c_vp], c_i32),
         "dfl_hier_level_shape": ([c_vp, c_i32, c_i32, P(c_i64), P(c_i64), P(c_i64)], c_i32),
         "dfl_hier_level_copy": ([c_vp, c_i32, c_i32, c_vp, c_vp, c_vp], c_i32),
@@ -194,9 +195,17 @@ class CsrArrays:
 class Hierarchy:
     """Host AMG hierarchy built by the native setup (dfl_hier_build)."""
 
-    def __init__(self, A: CsrArrays, opts: AmgOptions):
+    def __init__(self, A: CsrArrays, opts: AmgOptions, device: int | None = None):
+        """device: build the products on that GPU (dfl_setup_device), else on the host."""
         h = c_vp()
-        check(lib().dfl_hier_build(ctypes.byref(A.s), ctypes.byref(opts), ctypes.byref(h)))
+        L = lib()
+        if device is not None:
+            check(L.dfl_setup_device(int(device)))
+        try:
+            check(L.dfl_hier_build(ctypes.byref(A.s), ctypes.byref(opts), ctypes.byref(h)))
+        finally:
+            if device is not None:
+                L.dfl_setup_device(-1)
         self.h = h
 
     def __del__(self):

@@ -145,6 +145,7 @@ struct dfl_ctx {
     int64_t *op_sub_tiles = nullptr;   // first op-pipe tile of every subdomain
     cudaStream_t st = nullptr;
     cudaStream_t st_copy = nullptr;  // x read-back, overlapped with the true-residual kernels
+    std::mutex setup_mu;             // allocation list / class tables while levels convert in parallel
     std::string err;
     std::vector<void *> allocs;
     int64_t bytes = 0;
@@ -294,6 +295,7 @@ static int dalloc(dfl_ctx *ctx, T **p, int64_t count) {
     if (count <= 0) count = 1;
     void *q = nullptr;
     CK(cudaMalloc(&q, sizeof(T) * (size_t)count));
+    std::lock_guard<std::mutex> lk(ctx->setup_mu);
     ctx->allocs.push_back(q);
     ctx->bytes += sizeof(T) * count;
     *p = static_cast<T *>(q);

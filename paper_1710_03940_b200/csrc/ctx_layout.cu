@@ -1,3 +1,4 @@
+#include <thread>
 // Device layouts: format selection and upload of every matrix of the solve
 // phase, subdomain grouping of the V-cycle levels and row tiles of the operator.
 #include "ctx_impl.cuh"
@@ -172,8 +173,11 @@ static int try_upload_class(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) 
     m.fmt = FMT_CLASS;
     m.stored = m.nnz;
     m.cls = d_cls;
-    m.class_id = (int)ctx->class_tabs.size();
-    ctx->class_tabs.push_back(std::move(tab));
+    {
+        std::lock_guard<std::mutex> lk(ctx->setup_mu);
+        m.class_id = (int)ctx->class_tabs.size();
+        ctx->class_tabs.push_back(std::move(tab));
+    }
     ok = true;
     return DFL_OK;
 }
@@ -629,38 +633,66 @@ int build_groups(dfl_ctx *ctx) {
                 ctx->err = "hierarchy of subdomain " + std::to_string(j) + " does not match its row range";
                 return DFL_E_DIMENSION;
             }
+        // the levels' A / P / R layouts are converted and uploaded concurrently
+        // (independent host work; allocations are serialised by setup_mu)
+        std::vector<DLevel> vs(L);
+        std::vector<OwnedRows> Am(L), Pm(L), Rm(L);
+        std::vector<std::vector<double>> wl(L);
+        std::vector<std::vector<int64_t>> fol(L), col(L);
+        std::vector<std::vector<const dfl::Csr *>> As(L), Ps(L), Rs(L);
         for (int l = 0; l < L; ++l) {
-            DLevel v;
-            std::vector<const dfl::Csr *> As, Ps, Rs;
-            std::vector<int64_t> fo{0}, co{0};
-            std::vector<double> w;
+            fol[l] = {0};
+            col[l] = {0};
             for (int j = s; j < e; ++j) {
                 const dfl::Level &lv = ctx->pending[j].levels[l];
-                As.push_back(&lv.A);
-                Ps.push_back(&lv.P);
-                Rs.push_back(&lv.R);
-                fo.push_back(fo.back() + lv.A.nrows);
-                co.push_back(co.back() + lv.P.ncols);
-                w.insert(w.end(), lv.w.begin(), lv.w.end());
+                As[l].push_back(&lv.A);
+                Ps[l].push_back(&lv.P);
+                Rs[l].push_back(&lv.R);
+                fol[l].push_back(fol[l].back() + lv.A.nrows);
+                col[l].push_back(col[l].back() + lv.P.ncols);
+                wl[l].insert(wl[l].end(), lv.w.begin(), lv.w.end());
             }
-            OwnedRows A = merge_blocks(As, fo), P = merge_blocks(Ps, co), R = merge_blocks(Rs, fo);
-            // tiny levels stay CSR: they run inside the k_tiny_cycle cluster kernel
-            const bool tiny = g_use_tiny && fo.back() <= kTinyRows;
-            RC(upload_matrix(ctx, A.view(), v.A, {0, A.nrows}, nullptr, !tiny, w.data(), &v.Aw, true, true, false,
-                             !g_use_coarse));
-            if (v.A.fmt == FMT_CODE && g_wr_split) RC(dalloc(ctx, &v.wr, A.nrows));
-            RC(upload_matrix(ctx, P.view(), v.P, {0, P.nrows}, nullptr, !tiny, nullptr, nullptr, true, true, true));
-            RC(upload_matrix(ctx, R.view(), v.R, {0, R.nrows}, nullptr, !tiny, nullptr, nullptr, true, true, true));
-            RC(upload(ctx, &v.w, w.data(), (int64_t)w.size()));
-            v.n = fo.back();
-            v.nc = co.back();
+        }
+        std::vector<int> rcs(3 * L, DFL_OK);
+        {
+            std::vector<std::thread> th;
+            for (int l = 0; l < L; ++l)
+                for (int which = 0; which < 3; ++which)
+                    th.emplace_back([&, l, which] {
+                        cudaSetDevice(ctx->device);
+                        DLevel &v = vs[l];
+                        // tiny levels stay CSR: they run inside the k_tiny_cycle cluster kernel
+                        const bool tiny = g_use_tiny && fol[l].back() <= kTinyRows;
+                        int &rc = rcs[3 * l + which];
+                        if (which == 0) Am[l] = merge_blocks(As[l], fol[l]);
+                        else if (which == 1) Pm[l] = merge_blocks(Ps[l], col[l]);
+                        else Rm[l] = merge_blocks(Rs[l], fol[l]);
+                        if (which == 0)
+                            rc = upload_matrix(ctx, Am[l].view(), v.A, {0, Am[l].nrows}, nullptr, !tiny, wl[l].data(),
+                                               &v.Aw, true, true, false, !g_use_coarse);
+                        else if (which == 1)
+                            rc = upload_matrix(ctx, Pm[l].view(), v.P, {0, Pm[l].nrows}, nullptr, !tiny, nullptr,
+                                               nullptr, true, true, true);
+                        else
+                            rc = upload_matrix(ctx, Rm[l].view(), v.R, {0, Rm[l].nrows}, nullptr, !tiny, nullptr,
+                                               nullptr, true, true, true);
+                    });
+            for (auto &t : th) t.join();
+        }
+        for (int rc : rcs) RC(rc);
+        for (int l = 0; l < L; ++l) {
+            DLevel &v = vs[l];
+            if (v.A.fmt == FMT_CODE && g_wr_split) RC(dalloc(ctx, &v.wr, Am[l].nrows));
+            RC(upload(ctx, &v.w, wl[l].data(), (int64_t)wl[l].size()));
+            v.n = fol[l].back();
+            v.nc = col[l].back();
             RC(dalloc(ctx, &v.t, v.n));
             if (l > 0) {
                 RC(dalloc(ctx, &v.rv, v.n));
                 RC(dalloc(ctx, &v.xv, v.n));
             }
-            g.nnzA.push_back(A.ptr.back());
-            g.nnzP.push_back(P.ptr.back());
+            g.nnzA.push_back(Am[l].ptr.back());
+            g.nnzP.push_back(Pm[l].ptr.back());
             g.rows.push_back(v.n);
             g.lv.push_back(v);
         }

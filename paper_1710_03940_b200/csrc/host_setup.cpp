@@ -193,7 +193,7 @@ static Csr strength(const Csr &a, const std::vector<double> &d, double eps) {
 }
 
 // greedy distance-2 aggregation, ascending node order (amg.py:87-125)
-static int64_t aggregate(const Csr &s, std::vector<int64_t> &label) {
+int64_t aggregate(const Csr &s, std::vector<int64_t> &label) {
     const int64_t n = s.nrows;
     label.assign(n, -1);
     int64_t naggr = 0;
@@ -352,7 +352,7 @@ static std::vector<double> to_dense(const Csr &a) {
     return d;
 }
 
-static int close_bottom(Hierarchy &h, Csr &&a) {
+int close_bottom(Hierarchy &h, Csr &&a) {
     Level lv;
     lv.A = std::move(a);
     lv.bottom = true;
@@ -370,6 +370,7 @@ int build_hierarchy(const Csr &a0, const dfl_amg_options &o, Hierarchy &h) {
         set_setup_error("relaxation must be damped_jacobi or spai0 on the B200 path");
         return DFL_E_CONFIG;
     }
+    if (setup_device() >= 0) return build_hierarchy_dev(a0, o, h);
     h.levels.clear();
     h.relax = o.relax;
     Csr cur = a0;

@@ -39,6 +39,12 @@ Csr spgemm(const Csr &a, const Csr &b);
 bool diagonal(const Csr &a, std::vector<double> &d, const char *what);
 int lu_inverse(int64_t n, const double *a, double *inv);
 int build_hierarchy(const Csr &a0, const dfl_amg_options &o, Hierarchy &h);
+int64_t aggregate(const Csr &s, std::vector<int64_t> &label);
+int close_bottom(Hierarchy &h, Csr &&a);
+// device-side products (setup_dev.cu)
+void set_setup_device(int device);
+int setup_device();
+int build_hierarchy_dev(const Csr &a0, const dfl_amg_options &o, Hierarchy &h);
 int basis_az(const dfl_csr *A, int k, const double *zext, const int32_t *owner,
              const int32_t *rowsub, int64_t K, int sub0, int nsub, int keep_zeros, Csr &az,
              double *E_rows);

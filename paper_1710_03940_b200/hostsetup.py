@@ -83,10 +83,12 @@ class RankSetup:
 
 
 def build_rank_setup(rows, part, cfg, coords, deflated: bool, world: World, global_coords=None,
-                     build_hierarchies: bool = True) -> RankSetup:
+                     build_hierarchies: bool = True, setup_device: int | None = None) -> RankSetup:
     """rows = (row_ptr, col_idx, values) of this rank's rows, global columns.
     coords: the rank's rows' coordinates (or None); global_coords: all of them
-    when every rank holds the global problem (drop-in API)."""
+    when every rank holds the global problem (drop-in API).  setup_device: a
+    GPU for the strength filter / prolongation / Galerkin products of the
+    hierarchies (setup_dev.cu, bit-identical), None for the host."""
     subs = rank_subdomains(part.m, world.nranks, world.rank)
     r0, r1 = part.ranges[subs.start][0], part.ranges[subs.stop - 1][1]
     n = r1 - r0
@@ -138,7 +140,7 @@ def build_rank_setup(rows, part, cfg, coords, deflated: bool, world: World, glob
     if build_hierarchies:
         t0 = time.perf_counter()
         opts = amg_options(cfg)
-        hs.hier = [nat.Hierarchy(hs.local_block(j), opts) for j in range(len(subs))]
+        hs.hier = [nat.Hierarchy(hs.local_block(j), opts, device=setup_device) for j in range(len(subs))]
         hs.hierarchy_seconds = time.perf_counter() - t0
 
     if deflated:
