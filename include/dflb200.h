@@ -150,7 +150,7 @@ DFL_API const char *dfl_breakdown_string(int code);
 
 /* ---- host setup (C++) ----------------------------------------------------- */
 DFL_API int dfl_hier_build(const dfl_csr *A, const dfl_amg_options *opts, dfl_hier **out);
-/* device >= 0: later dfl_hier_build calls of this thread's process run the strength filter,
+/* device >= 0: later dfl_hier_build calls on the calling thread run the strength filter,
  * smoothed prolongation, transpose and Galerkin products on that GPU (setup_dev.cu; the
  * hierarchy is bit-identical to the host build; greedy aggregation and the bottom LU stay
  * on the host).  -1 (default): all on the host. */

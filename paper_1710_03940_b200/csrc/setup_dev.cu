@@ -383,7 +383,7 @@ int64_t max_row(const Csr &a) {
 
 }  // namespace
 
-static int g_setup_device = -1;
+static thread_local int g_setup_device = -1;  // per calling thread (ranks may build concurrently)
 
 void set_setup_device(int device) { g_setup_device = device; }
 int setup_device() { return g_setup_device; }
