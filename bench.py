@@ -220,8 +220,11 @@ def b200_arm(args, ws, rank, local):
     part = ordering.partition()
     r0, r1 = part.ranges[rank]
     t0 = time.perf_counter()
-    rows = problems.local_rows(ordering, r0, r1, "poisson")
-    coords = problems.node_coords(ordering, r0, r1)
+    # the rank's rows and coordinates generated on its GPU (gen_dev.cu, bit-identical to the host generator)
+    from paper_1710_03940_b200 import _native as nat
+
+    ptr, col, val, coords = nat.gen_rows(local, ordering.shape, ordering.boxes, "poisson", r0, r1)
+    rows = (ptr, col, val)
     gen_s = time.perf_counter() - t0
     solver = DeflatedSolver.from_rows(rows, n, part, config=SolverConfig(CFG), coords_local=coords, device=local)
     h = 1.0 / (shape[0] + 1)

@@ -131,6 +131,20 @@ typedef struct {
     int64_t kernel_launches;    /* kernels of this library launched by the solve */
 } dfl_report;
 
+/* structured test problems (problems.py make_problem; reference problems.py:143-171 for the
+ * Poisson kind, BASELINE.md §4 for the other two) */
+#define DFL_GEN_POISSON 0
+#define DFL_GEN_JUMP 1
+#define DFL_GEN_CONVDIFF 2
+typedef struct {
+    int64_t shape[3]; /* grid nodes per axis */
+    int64_t boxes[3]; /* subdomain boxes per axis (box-contiguous unknown ordering) */
+    int32_t kind;     /* DFL_GEN_* */
+    int32_t cells;    /* jump: checkerboard blocks per axis */
+    double contrast;  /* jump: kappa on odd blocks */
+    double conv[3];   /* convdiff: c per axis */
+} dfl_gen_params;
+
 typedef struct dfl_matrix dfl_matrix; /* host CSR produced by setup */
 typedef struct dfl_hier dfl_hier;     /* host AMG hierarchy */
 typedef struct dfl_ctx dfl_ctx;       /* device solve context (one rank) */
@@ -155,6 +169,15 @@ DFL_API int dfl_hier_build(const dfl_csr *A, const dfl_amg_options *opts, dfl_hi
  * hierarchy is bit-identical to the host build; greedy aggregation and the bottom LU stay
  * on the host).  -1 (default): all on the host. */
 DFL_API int dfl_setup_device(int device);
+
+/* ---- problem generation on the GPU (gen_dev.cu; problems.py local_rows / node_coords /
+ *      make_problem's unknown_of_node, bit-identical) ---------------------------------- */
+/* CSR rows [r0, r1) with global columns into host arrays: row_ptr[r1-r0+1], col_idx and values
+ * with room for 7 (r1-r0) entries; *nnz = entries written; coords[(r1-r0)*3] or NULL */
+DFL_API int dfl_gen_rows(int device, const dfl_gen_params *p, int64_t r0, int64_t r1, int64_t *row_ptr,
+                         int64_t *col_idx, double *values, int64_t *nnz, double *coords);
+/* natural (x-fastest) node k -> unknown index, for every node of the grid */
+DFL_API int dfl_gen_unknown_of_node(int device, const dfl_gen_params *p, int64_t *uon);
 DFL_API int dfl_hier_num_levels(const dfl_hier *h);
 /* shape of level l's A / P / R (P and R absent at the bottom level: nnz = -1) */
 DFL_API int dfl_hier_level_shape(const dfl_hier *h, int level, int which, int64_t *nrows,

@@ -67,6 +67,38 @@ class Report(ctypes.Structure):
 _lib = None
 
 
+class GenParams(ctypes.Structure):
+    _fields_ = [("shape", c_i64 * 3), ("boxes", c_i64 * 3), ("kind", c_i32), ("cells", c_i32),
+                ("contrast", c_dbl), ("conv", c_dbl * 3)]
+
+
+GEN_KIND = {"poisson": 0, "jump": 1, "convdiff": 2}
+
+
+def gen_rows(device: int, shape, boxes, kind: str, r0: int, r1: int, contrast=1e4, cells=4, c=(0.3, 0.2, 0.1),
+             coords: bool = True):
+    """CSR rows [r0, r1) of a structured problem built on the GPU
+    (dfl_gen_rows); returns (row_ptr, col_idx, values, coords or None)."""
+    p = GenParams((c_i64 * 3)(*shape), (c_i64 * 3)(*boxes), GEN_KIND[kind], int(cells), float(contrast),
+                  (c_dbl * 3)(*[float(v) for v in c]))
+    nr = r1 - r0
+    ptr = np.empty(nr + 1, dtype=np.int64)
+    col = np.empty(7 * nr, dtype=np.int64)
+    val = np.empty(7 * nr)
+    xyz = np.empty((nr, 3)) if coords else None
+    nnz = c_i64()
+    check(lib().dfl_gen_rows(int(device), ctypes.byref(p), int(r0), int(r1), _ptr(ptr), _ptr(col), _ptr(val),
+                             ctypes.byref(nnz), _ptr(xyz) if coords else None))
+    return ptr, col[: nnz.value], val[: nnz.value], xyz
+
+
+def gen_unknown_of_node(device: int, shape, boxes, n: int) -> np.ndarray:
+    p = GenParams((c_i64 * 3)(*shape), (c_i64 * 3)(*boxes), 0, 4, 1e4, (c_dbl * 3)(0.0, 0.0, 0.0))
+    uon = np.empty(n, dtype=np.int64)
+    check(lib().dfl_gen_unknown_of_node(int(device), ctypes.byref(p), _ptr(uon)))
+    return uon
+
+
 def lib():
     """Load libdflb200.so (built in-tree by ``paper_1710_03940_b200._build``)."""
     global _lib
@@ -88,6 +120,8 @@ def lib():
         "dfl_breakdown_string": ([c_i32], ctypes.c_char_p),
         "dfl_hier_build": ([P(Csr), P(AmgOptions), P(c_vp)], c_i32),
         "dfl_setup_device": ([c_i32], c_i32),
+        "dfl_gen_rows": ([c_i32, P(GenParams), c_i64, c_i64, c_vp, c_vp, c_vp, P(c_i64), c_vp], c_i32),
+        "dfl_gen_unknown_of_node": ([c_i32, P(GenParams), c_vp], c_i32),
         "dfl_hier_num_levels": ([c_vp], c_i32),
         "dfl_hier_level_shape": ([c_vp, c_i32, c_i32, P(c_i64), P(c_i64), P(c_i64)], c_i32),
         "dfl_hier_level_copy": ([c_vp, c_i32, c_i32, c_vp, c_vp, c_vp], c_i32),

@@ -132,11 +132,18 @@ def _kappa(ordering: BoxOrdering, ix, iy, iz, contrast: float, cells: int):
 
 
 def local_rows(ordering: BoxOrdering, r0: int, r1: int, kind: str = "poisson",
-               contrast: float = 1e4, cells: int = 4, c=(0.3, 0.2, 0.1)):
+               contrast: float = 1e4, cells: int = 4, c=(0.3, 0.2, 0.1), device: int | None = None):
     """CSR rows [r0, r1) of the global operator (global column indices),
-    columns ascending within each row."""
+    columns ascending within each row.  device: build them on that GPU
+    (csrc/gen_dev.cu, the same bits; 150^3 in ~0.1 s instead of seconds)."""
     if kind not in KINDS:
         raise ValueError(f"unknown problem kind {kind!r}")
+    if device is not None:
+        from . import _native as nat
+
+        ptr, col, val, _ = nat.gen_rows(device, ordering.shape, ordering.boxes, kind, r0, r1, contrast, cells, c,
+                                        coords=False)
+        return ptr, col, val
     rows = np.arange(r0, r1, dtype=np.int64)
     ix, iy, iz = ordering.nodes_of(rows)
     nx, ny, nz = ordering.shape
@@ -200,22 +207,32 @@ def node_coords(ordering: BoxOrdering, r0: int, r1: int) -> np.ndarray:
     return np.stack([(ix + 1) * hx, (iy + 1) * hy, (iz + 1) * hz], axis=1)
 
 
-def make_problem(shape, boxes=(1, 1, 1), kind: str = "poisson", **kw) -> Problem:
+def make_problem(shape, boxes=(1, 1, 1), kind: str = "poisson", device: int | None = None, **kw) -> Problem:
+    """device: generate rows, coordinates and the node map on that GPU
+    (csrc/gen_dev.cu, bit-identical to the host generator)."""
     ordering = BoxOrdering(shape, boxes)
     n = ordering.n
-    ptr, col, val = local_rows(ordering, 0, n, kind, **kw)
-    A = SparseMatrix(n, n, ptr, col, val)
     h = 1.0 / (ordering.shape[0] + 1)
     rhs = np.full(n, h * h)
+    if kind not in KINDS:
+        raise ValueError(f"unknown problem kind {kind!r}")
+    if device is not None:
+        from . import _native as nat
+
+        ptr, col, val, coords = nat.gen_rows(device, ordering.shape, ordering.boxes, kind, 0, n, **kw)
+        uon = nat.gen_unknown_of_node(device, ordering.shape, ordering.boxes, n)
+        return Problem(ordering, SparseMatrix(n, n, ptr, col, val), rhs, coords, ordering.partition(), uon, kind)
+    ptr, col, val = local_rows(ordering, 0, n, kind, **kw)
+    A = SparseMatrix(n, n, ptr, col, val)
     nx, ny, nz = ordering.shape
     k = np.arange(n, dtype=np.int64)
     uon = ordering.index_of(k % nx, (k // nx) % ny, k // (nx * ny))
     return Problem(ordering, A, rhs, node_coords(ordering, 0, n), ordering.partition(), uon, kind)
 
 
-def poisson3d(n, boxes=(1, 1, 1)) -> Problem:
+def poisson3d(n, boxes=(1, 1, 1), device: int | None = None) -> Problem:
     """7-point Poisson on the unit cube (reference problems.py:143-171)."""
-    return make_problem(n, boxes, "poisson")
+    return make_problem(n, boxes, "poisson", device=device)
 
 
 def jump3d(n, boxes=(1, 1, 1), contrast: float = 1e4, cells: int = 4) -> Problem:
