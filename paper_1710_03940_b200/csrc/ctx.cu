@@ -285,7 +285,7 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
         }
         ctx->split = true;
     }
-    ctx->pending.assign(nsub, dfl::Hierarchy{});
+    ctx->pending.assign(nsub, nullptr);
     ctx->pending_set.assign(nsub, 0);
     ctx->have_op = true;
     ctx->finalized = false;
@@ -298,13 +298,13 @@ int dfl_ctx_add_hierarchy(dfl_ctx *ctx, int32_t sub, const dfl_hier *h) {
         ctx->err = "hierarchy for an unknown subdomain (set the operator first)";
         return DFL_E_STATE;
     }
-    const dfl::Hierarchy &src = h->h;
+    const dfl::Hierarchy &src = *h->sp;
     if (sub > 0 && src.relax != ctx->relax) {
         ctx->err = "all subdomains must use the same relaxation";
         return DFL_E_CONFIG;
     }
     ctx->relax = src.relax;
-    ctx->pending[sub] = src;
+    ctx->pending[sub] = h->sp;
     ctx->pending_set[sub] = 1;
     return DFL_OK;
 }

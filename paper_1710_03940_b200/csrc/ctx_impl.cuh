@@ -182,7 +182,7 @@ struct dfl_ctx {
     cudaStream_t st2 = nullptr;
     cudaEvent_t ev_packed = nullptr, ev_halo = nullptr;
     // hierarchies
-    std::vector<dfl::Hierarchy> pending;
+    std::vector<std::shared_ptr<const dfl::Hierarchy>> pending;  // added hierarchies until finalize
     std::vector<int> pending_set;
     std::vector<VGroup> groups;
     int relax = DFL_RELAX_DAMPED_JACOBI;

@@ -619,9 +619,9 @@ int build_groups(dfl_ctx *ctx) {
     ctx->groups.clear();
     int s = 0;
     while (s < ctx->nsub) {
-        const size_t depth = ctx->pending[s].levels.size();
+        const size_t depth = ctx->pending[s]->levels.size();
         int e = s + 1;
-        while (e < ctx->nsub && ctx->pending[e].levels.size() == depth) ++e;
+        while (e < ctx->nsub && ctx->pending[e]->levels.size() == depth) ++e;
         VGroup g;
         g.sub0 = s;
         g.nsub = e - s;
@@ -629,7 +629,7 @@ int build_groups(dfl_ctx *ctx) {
         g.row1 = ctx->sub_off[e];
         const int L = (int)depth - 1;
         for (int j = s; j < e; ++j)
-            if (ctx->pending[j].levels[0].A.nrows != ctx->sub_off[j + 1] - ctx->sub_off[j]) {
+            if (ctx->pending[j]->levels[0].A.nrows != ctx->sub_off[j + 1] - ctx->sub_off[j]) {
                 ctx->err = "hierarchy of subdomain " + std::to_string(j) + " does not match its row range";
                 return DFL_E_DIMENSION;
             }
@@ -644,7 +644,7 @@ int build_groups(dfl_ctx *ctx) {
             fol[l] = {0};
             col[l] = {0};
             for (int j = s; j < e; ++j) {
-                const dfl::Level &lv = ctx->pending[j].levels[l];
+                const dfl::Level &lv = ctx->pending[j]->levels[l];
                 As[l].push_back(&lv.A);
                 Ps[l].push_back(&lv.P);
                 Rs[l].push_back(&lv.R);
@@ -700,7 +700,7 @@ int build_groups(dfl_ctx *ctx) {
         std::vector<int64_t> boff{0}, ioff{0};
         std::vector<double> invT;
         for (int j = s; j < e; ++j) {
-            const dfl::Level &bl = ctx->pending[j].levels.back();
+            const dfl::Level &bl = ctx->pending[j]->levels.back();
             const int64_t nb = bl.A.nrows;
             boff.push_back(boff.back() + nb);
             ioff.push_back(ioff.back() + nb * nb);
@@ -721,7 +721,7 @@ int build_groups(dfl_ctx *ctx) {
             // row-major inverses and the argument block of the cooperative kernel
             std::vector<double> binv;
             for (int j = s; j < e; ++j) {
-                const auto &bi = ctx->pending[j].levels.back().bottom_inv;
+                const auto &bi = ctx->pending[j]->levels.back().bottom_inv;
                 binv.insert(binv.end(), bi.begin(), bi.end());
             }
             RC(upload(ctx, &g.binv, binv.data(), (int64_t)binv.size()));

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -53,5 +54,7 @@ int basis_az(const dfl_csr *A, int k, const double *zext, const int32_t *owner,
 
 // opaque handle of the C ABI
 struct dfl_hier {
-    dfl::Hierarchy h;
+    // shared with the device contexts it is added to (no deep copy on dfl_ctx_add_hierarchy)
+    std::shared_ptr<dfl::Hierarchy> sp = std::make_shared<dfl::Hierarchy>();
+    dfl::Hierarchy &h = *sp;
 };

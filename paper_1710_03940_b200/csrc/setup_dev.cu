@@ -40,6 +40,8 @@ struct DCsr {
 
 struct Dev {
     cudaStream_t st = nullptr;
+    cudaMemPool_t pool = nullptr;  // trimmed when the build ends (the pages stay mapped during it)
+    uint64_t old_threshold = 0;
     std::vector<void *> live;
     std::string err;
     bool ok = true;
@@ -76,6 +78,10 @@ struct Dev {
         if (st) {
             cudaStreamSynchronize(st);
             cudaStreamDestroy(st);
+        }
+        if (pool) {
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &old_threshold);
+            cudaMemPoolTrimTo(pool, 0);
         }
     }
 };
@@ -395,10 +401,10 @@ int build_hierarchy_dev(const Csr &a0, const dfl_amg_options &o, Hierarchy &h) {
     DCK(cudaStreamCreateWithFlags(&dv.st, cudaStreamNonBlocking));
     {
         // keep the stream-ordered pool's pages mapped across the per-level syncs
-        cudaMemPool_t pool;
-        DCK(cudaDeviceGetDefaultMemPool(&pool, g_setup_device));
+        DCK(cudaDeviceGetDefaultMemPool(&dv.pool, g_setup_device));
+        DCK(cudaMemPoolGetAttribute(dv.pool, cudaMemPoolAttrReleaseThreshold, &dv.old_threshold));
         uint64_t keep = UINT64_MAX;
-        DCK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        DCK(cudaMemPoolSetAttribute(dv.pool, cudaMemPoolAttrReleaseThreshold, &keep));
     }
     h.levels.clear();
     h.relax = o.relax;
