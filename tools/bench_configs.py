@@ -45,8 +45,10 @@ def run(name, steps):
     ordering = problems.BoxOrdering(shape, problems.boxes_for(m))
     n = ordering.n
     t0 = time.perf_counter()
-    rows = problems.local_rows(ordering, 0, n, kind)
-    coords = problems.node_coords(ordering, 0, n)
+    from paper_1710_03940_b200 import _native as nat
+
+    ptr, col, val, coords = nat.gen_rows(0, ordering.shape, ordering.boxes, kind, 0, n)  # on the GPU
+    rows = (ptr, col, val)
     gen = time.perf_counter() - t0
     s = DeflatedSolver.from_rows(rows, n, ordering.partition(), config=SolverConfig(cfgd), coords_local=coords)
     h = 1.0 / (ordering.shape[0] + 1)
