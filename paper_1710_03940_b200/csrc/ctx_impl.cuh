@@ -73,6 +73,7 @@ extern Nccl g_nccl;
 
 // profiling / layout knobs (defined in ctx.cu, read at context creation)
 extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl, g_code_pipe, g_use_class, g_op_pf, g_use_pcode, g_use_scode, g_sell_wave, g_no_sell, g_nccl_graph;
+extern unsigned g_fin_mask;
 extern double g_small_per_lane, g_csr_per_lane;
 extern int g_csr_g, g_sm_count;
 static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle
@@ -636,7 +637,7 @@ int build_tiles(dfl_ctx *ctx);
 // single-rank grid finish of the CG scalars (Fin); nullptr-tick Fin when off
 inline Fin make_fin(dfl_ctx *ctx, int act) {
     Fin f{};
-    if (multi(ctx) || !ctx->fin_tick || g_no_fin) return f;
+    if (multi(ctx) || !ctx->fin_tick || g_no_fin || !((g_fin_mask >> act) & 1u)) return f;
     f.tick = ctx->fin_tick;
     f.gpart = ctx->fin_gpart;
     f.st = ctx->state;
@@ -646,6 +647,7 @@ inline Fin make_fin(dfl_ctx *ctx, int act) {
 // the operator kernel can finish Z'y -> t (-> t2) itself
 inline bool op_fusable(const dfl_ctx *ctx) {
     return !multi(ctx) && !ctx->split && !g_use_pipe && ctx->subtab.n > 0 && ctx->fin_tick && !g_no_fin &&
+           (g_fin_mask & 16u) &&
            (ctx->Aop.fmt == FMT_ELL || ctx->Aop.fmt == FMT_CODE || ctx->Aop.fmt == FMT_CLASS);
 }
 
