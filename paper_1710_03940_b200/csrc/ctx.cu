@@ -20,6 +20,7 @@ bool g_use_coarse = false;  // cooperative coarse-cycle kernel (DFL_COARSE=1; me
 bool g_allow_sell = false;    // DFL_SELL=1: SELL-C-sigma for every irregular matrix
 bool g_wr_split = false;      // DFL_WR_SPLIT=1: coded residual reads w .* r from a k_wr pass
 bool g_no_fin = true;                // DFL_FIN=1: CG scalars finished in the producing kernels (measured slower)
+int g_keep_mb = 0;                   // DFL_KEEP_MB: L2 evict-last loads for CSR matrices up to this size
 unsigned g_fin_mask = 0xffffffffu;   // with !g_no_fin: which finishes run in-kernel (DFL_FIN_MASK)
 bool g_nccl_graph = false;    // DFL_NCCL_GRAPH=1: several NCCL ranks replay the captured CG body (measured neutral on 1 rank)
 bool g_no_sell = false;       // DFL_NO_SELL=1: long-row matrices as CSR-vector instead of SELL
@@ -130,6 +131,8 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
         g_no_fin = !(nf && nf[0] == '1');
         // DFL_FIN_MASK: bit 1 << ACT_* enables the grid finish per CG scalar (PQ 2, RR 4, RZ 8),
         // bit 16 the operator's in-kernel Z'y finish; DFL_FIN=1 enables all of them
+        const char *km = getenv("DFL_KEEP_MB");
+        if (km) g_keep_mb = atoi(km);
         const char *fm = getenv("DFL_FIN_MASK");
         if (fm) {
             g_fin_mask = (unsigned)atoi(fm);

@@ -74,6 +74,7 @@ extern Nccl g_nccl;
 // profiling / layout knobs (defined in ctx.cu, read at context creation)
 extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl, g_code_pipe, g_use_class, g_op_pf, g_use_pcode, g_use_scode, g_sell_wave, g_no_sell, g_nccl_graph;
 extern unsigned g_fin_mask;
+extern int g_keep_mb;
 extern double g_small_per_lane, g_csr_per_lane;
 extern int g_csr_g, g_sm_count;
 static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle

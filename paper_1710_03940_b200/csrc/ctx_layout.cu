@@ -487,6 +487,8 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
     } else {
         m.fmt = FMT_CSR;
         m.stored = m.nnz;
+        // DFL_KEEP_MB: CSR matrices up to this size load with an L2 evict-last policy (0: off)
+        m.keep = (double)m.nnz * 12.0 <= (double)g_keep_mb * 1048576.0 ? 1 : 0;
         // lanes per row: about 6 entries per lane, batched kCsrUnroll deep
         int g = 1;
         const int want = (int)std::ceil(mean / (h.nrows < 50000 ? g_small_per_lane : g_csr_per_lane));

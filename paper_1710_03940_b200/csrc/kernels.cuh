@@ -97,6 +97,7 @@ struct DMat {
     int fmt = FMT_ELL;
     int ell_w = 0;            // > 0: every slice has this width (no slice_off lookup)
     int group = 1;            // CSR-vector lanes per row
+    int keep = 0;             // CSR small enough to stay L2-resident across cycles: loads with an evict-last policy
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;
     const int64_t *slice_off = nullptr;  // ELL: nslices + 1 element offsets
     const int *ptr = nullptr;            // CSR row pointer
@@ -159,6 +160,23 @@ __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(
 
 template <class T>
 __device__ __forceinline__ T ld_stream(const T *p) { return __ldcs(p); }
+// evict-last loads for the coarse-level matrices (they fit in L2 next to the
+// gathered vectors while the fine-level streams pass through evict-first)
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ int ld_keep(const int *p, uint64_t pol) {
+    int v;
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld_keep(const double *p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
 __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 #ifndef DFL_SLICE_PREFETCH
 #define DFL_SLICE_PREFETCH 0  // measured slower (L0 restriction 43.4 -> 46.0 us)
@@ -427,14 +445,20 @@ __device__ __forceinline__ double csr_row(const DMat &A, int64_t row, int sub, c
     double acc = 0.0;
     if (row < A.nrows) {
         const int b = __ldg(A.ptr + row), e = __ldg(A.ptr + row + 1);
+        const uint64_t pol = A.keep ? l2_keep_policy() : 0;
         for (int k0 = b + sub; k0 < e; k0 += kCsrUnroll * G) {
             int c[kCsrUnroll];
             double v[kCsrUnroll], xv[kCsrUnroll];
 #pragma unroll
             for (int u = 0; u < kCsrUnroll; ++u)
                 if (k0 + u * G < e) {
-                    c[u] = ld_stream(A.col + k0 + u * G);
-                    v[u] = ld_stream(A.val + k0 + u * G);
+                    if (A.keep) {
+                        c[u] = ld_keep(A.col + k0 + u * G, pol);
+                        v[u] = ld_keep(A.val + k0 + u * G, pol);
+                    } else {
+                        c[u] = ld_stream(A.col + k0 + u * G);
+                        v[u] = ld_stream(A.val + k0 + u * G);
+                    }
                 }
 #pragma unroll
             for (int u = 0; u < kCsrUnroll; ++u)

@@ -419,3 +419,33 @@ def test_true_residual_refresh_past_50_iterations(loop, monkeypatch):
     assert abs(rep["iterations"] - ro["iterations"]) <= 1, (rep["iterations"], ro["iterations"])
     assert rep["relative_residual"] <= 2 * ro["relative_residual"]
     assert np.linalg.norm(x - xo) <= 1e-6 * np.linalg.norm(xo)
+
+
+def test_results_in_pinned_blocks_stay_valid():
+    """x comes back in a page-locked block from the library's cache; a block
+    is reused only after its array is gone, so earlier results survive later
+    solves and views keep their block alive."""
+    import gc
+
+    p = problems.poisson3d(20, problems.boxes_for(2))
+    cfgd = {"solver": {"type": "cg", "tol": 1e-8}, "precond": {"relax": {"type": "spai0"}},
+            "deflation": {"kind": "linear"}}
+    s = _solver(p, 2, cfgd)
+    x1, _ = s.solve(p.rhs)
+    keep = x1.copy()
+    view = x1[5:50]
+    del x1
+    gc.collect()
+    for scale in (2.0, -3.0, 0.5):
+        x, _ = s.solve(scale * p.rhs)
+        assert np.allclose(x, scale * keep, rtol=1e-6, atol=1e-9 * abs(scale) * np.abs(keep).max())
+    assert np.array_equal(view, keep[5:50])
+    xs = [s.solve(p.rhs)[0] for _ in range(6)]  # more live results than cached blocks per size
+    for x in xs:
+        assert np.array_equal(x, xs[0])
+    a = nat.pinned_empty(1000)
+    a[:] = 1.0
+    del a
+    gc.collect()
+    b = nat.pinned_empty(1000)
+    assert b.shape == (1000,)
