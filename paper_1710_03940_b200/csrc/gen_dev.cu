@@ -108,7 +108,7 @@ __global__ void k_gen_rows(Geo g, Stencil s, int64_t r0, int64_t nr, int64_t *__
             ++slot;
         }
     v[0] = s.kind == DFL_GEN_JUMP ? diag : s.diag;
-    if (!FILL) {
+    if constexpr (!FILL) {
         int cnt = 0;
         for (int k = 0; k < 7; ++k) cnt += c[k] >= 0;
         ptr[i] = cnt;
@@ -118,28 +118,29 @@ __global__ void k_gen_rows(Geo g, Stencil s, int64_t r0, int64_t nr, int64_t *__
             coords[3 * i + 2] = __dmul_rn((double)(iz + 1), g.hz);
         }
         return;
-    }
-    // stable insertion sort by column, invalid (-1) last
-    for (int k = 1; k < 7; ++k) {
-        const int64_t kc = c[k] >= 0 ? c[k] : INT64_MAX;
-        const int64_t cc = c[k];
-        const double vv = v[k];
-        int q = k - 1;
-        while (q >= 0 && (c[q] >= 0 ? c[q] : INT64_MAX) > kc) {
-            c[q + 1] = c[q];
-            v[q + 1] = v[q];
-            --q;
+    } else {
+        // stable insertion sort by column, invalid (-1) last
+        for (int k = 1; k < 7; ++k) {
+            const int64_t kc = c[k] >= 0 ? c[k] : INT64_MAX;
+            const int64_t cc = c[k];
+            const double vv = v[k];
+            int q = k - 1;
+            while (q >= 0 && (c[q] >= 0 ? c[q] : INT64_MAX) > kc) {
+                c[q + 1] = c[q];
+                v[q + 1] = v[q];
+                --q;
+            }
+            c[q + 1] = cc;
+            v[q + 1] = vv;
         }
-        c[q + 1] = cc;
-        v[q + 1] = vv;
+        int64_t o = ptr[i];
+        for (int k = 0; k < 7; ++k)
+            if (c[k] >= 0) {
+                col[o] = c[k];
+                val[o] = v[k];
+                ++o;
+            }
     }
-    int64_t o = ptr[i];
-    for (int k = 0; k < 7; ++k)
-        if (c[k] >= 0) {
-            col[o] = c[k];
-            val[o] = v[k];
-            ++o;
-        }
 }
 
 __global__ void k_gen_uon(Geo g, int64_t n, int64_t *__restrict__ uon) {
