@@ -454,6 +454,7 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
     // block of the multi-dot kernels (grid <= 4 * SMs)
     const int64_t dslots = std::max({ctx->nblk, vparts, kDotStride * std::max<int64_t>(ctx->nblk, 4 * ctx->sm_count)});
     RC(dalloc(ctx, &ctx->dpart, dslots + 64));
+    RC(dalloc(ctx, &ctx->dpart_pq, ctx->vgrid + 64));
     RC(dalloc(ctx, &ctx->zt_part, (std::max(ctx->ntiles, ctx->Aop.pipe.ntiles) + ctx->nbtiles) * kKmax + 64));
     RC(dalloc(ctx, &ctx->scal, 16));
     RC(dalloc(ctx, &ctx->sgather, (int64_t)8 * ctx->nranks));

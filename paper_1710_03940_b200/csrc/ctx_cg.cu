@@ -184,10 +184,55 @@ static int capture_refresh_if(dfl_ctx *ctx, bool deflated, cudaGraphConditionalH
     return DFL_OK;
 }
 
+// DFL_FUSE_PU=1: the cooperative k_proj_update fits when the one-wave vector
+// grid is co-resident for it
+static bool fuse_pu_ok(dfl_ctx *ctx, int k) {
+    static const bool on = [] {
+        const char *e = getenv("DFL_FUSE_PU");
+        return e && e[0] == '1';
+    }();
+    if (!on || !ctx->dpart_pq) return false;
+    const int kz = k <= 1 ? 1 : k <= 2 ? 2 : k <= 4 ? 4 : 8;
+    const int occ = kz == 1 ? occupancy(k_proj_update<1>) : kz == 2 ? occupancy(k_proj_update<2>)
+                  : kz == 4 ? occupancy(k_proj_update<4>) : occupancy(k_proj_update<8>);
+    return ctx->vgrid <= (int64_t)occ * ctx->sm_count;
+}
+
+template <int KZ>
+static int launch_pu(dfl_ctx *ctx, const ProjArgs &a, int use_if, cudaGraphConditionalHandle hif) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ctx->vgrid);
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = ctx->st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    int na = 1;
+    if (g_pdl) {
+        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[1].val.programmaticStreamSerializationAllowed = 1;
+        na = 2;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    CK(cudaLaunchKernelEx(&cfg, k_proj_update<KZ>, a, ctx->x, ctx->r, ctx->dpart_pq, ctx->state, use_if, hif));
+    ctx->launches++;
+    return DFL_OK;
+}
+
+static int launch_proj_update(dfl_ctx *ctx, const ProjArgs &a, int use_if, cudaGraphConditionalHandle hif) {
+    const int k = a.azd ? a.k : 1;
+    if (k <= 1) return launch_pu<1>(ctx, a, use_if, hif);
+    if (k <= 2) return launch_pu<2>(ctx, a, use_if, hif);
+    if (k <= 4) return launch_pu<4>(ctx, a, use_if, hif);
+    return launch_pu<8>(ctx, a, use_if, hif);
+}
+
 static int cg_body(dfl_ctx *ctx, bool deflated, const CgGraph &G) {
     KState *st = ctx->state;
     const double *gath;
     const bool single = !multi(ctx);
+    bool fused = false;
     // w = A p, Z'w -> t2 ; q = w - AZ t2 ; p.q
     bool tz = false;
     RC(op_apply_dev(ctx, ctx->p, ctx->w, 0, nullptr, deflated, st, 0, &tz));
@@ -201,18 +246,26 @@ static int cg_body(dfl_ctx *ctx, bool deflated, const CgGraph &G) {
         a.fin = make_fin(ctx, ACT_PQ);
         a.fin.use_if = G.use_if;
         a.fin.hif = G.hif;
-        launch_project<0>(ctx, a);
-        if (!a.fin.tick) {
-            RC(rank_scalar(ctx, ctx->dpart, ctx->vgrid, 0, &gath));
-            launch_k(ctx->st, k_cg_pq, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, gath, ctx->nranks, G.use_if, G.hif);
-            ctx->launches++;
+        if (single && !a.fin.tick && fuse_pu_ok(ctx, a.azd ? a.k : 1)) {
+            // projection + scalar step + update in one cooperative kernel (DFL_FUSE_PU=1)
+            RC(launch_proj_update(ctx, a, G.use_if, G.hif));
+            fused = true;
+        } else {
+            launch_project<0>(ctx, a);
+            if (!a.fin.tick) {
+                RC(rank_scalar(ctx, ctx->dpart, ctx->vgrid, 0, &gath));
+                launch_k(ctx->st, k_cg_pq, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, gath, ctx->nranks, G.use_if, G.hif);
+                ctx->launches++;
+            }
         }
     }
     // x += alpha p ; r -= alpha q (regular iterations; + r.r test when finished in-kernel)
-    const Fin frr = make_fin(ctx, ACT_RR);
-    launch_k(ctx->st, k_cg_update, (unsigned)ctx->vgrid, kBlock, 0, ctx->x, ctx->r, ctx->p, ctx->w, ctx->n, ctx->dpart, st,
-                                                            frr);
-    ctx->launches++;
+    const Fin frr = fused ? Fin{} : make_fin(ctx, ACT_RR);
+    if (!fused) {
+        launch_k(ctx->st, k_cg_update, (unsigned)ctx->vgrid, kBlock, 0, ctx->x, ctx->r, ctx->p, ctx->w, ctx->n,
+                 ctx->dpart, st, frr);
+        ctx->launches++;
+    }
     // refresh iterations: r = b' - project(A x)   (krylov.py:128-129)
     if (G.use_if)
         RC(capture_refresh_if(ctx, deflated, G.hif));

@@ -147,7 +147,8 @@ struct dfl_ctx {
     int64_t *op_sub_tiles = nullptr;   // first op-pipe tile of every subdomain
     cudaStream_t st = nullptr;
     cudaStream_t st_copy = nullptr;  // x read-back, overlapped with the true-residual kernels
-    std::mutex setup_mu;             // allocation list / class tables while levels convert in parallel
+    std::mutex setup_mu;
+    double *dpart_pq = nullptr;      // p.q partials of the fused projection + update (DFL_FUSE_PU)             // allocation list / class tables while levels convert in parallel
     std::string err;
     std::vector<void *> allocs;
     int64_t bytes = 0;

@@ -18,6 +18,7 @@
 // projector of deflation.py:230-233 and the CG recurrences of krylov.py:95-145.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -1692,6 +1693,68 @@ static __global__ void k_reduce(const double *part, int64_t nparts, double *out)
     DFL_PDL_ENTRY;
     const double s = reduce_parts(part, nparts);
     if (threadIdx.x == 0) *out = s;
+}
+
+// Projection + CG update in one cooperative kernel (single rank, DFL_FUSE_PU=1):
+// q = w - AZ t2 with p.q partials (as k_project<0>), a grid barrier, then every
+// block reduces the partials itself, block 0 records the scalar step of
+// krylov.py:119-126 (cg_step_pq, refresh IF condition), and all blocks apply
+// x += alpha p, r -= alpha q (+ r.r partials) while p and q are still in L2
+// (as k_cg_update).  The KState fields are read before the barrier, so no
+// block sees block 0's update.  pq_part: the p.q partials (a buffer of their
+// own: the r.r partials reuse a.dot_part while slower blocks still reduce).
+template <int KZ>
+__global__ void __launch_bounds__(kBlock, 6) k_proj_update(ProjArgs a, double *x, double *r, double *pq_part,
+                                                        KState *st, int use_if, cudaGraphConditionalHandle hif) {
+    DFL_PDL_ENTRY;
+    __shared__ int s_done, s_iters, s_every;
+    __shared__ double s_rz;
+    if (threadIdx.x == 0) {
+        s_done = st->done;
+        s_iters = st->iters;
+        s_every = st->refresh_every;
+        s_rz = st->rz;
+    }
+    __syncthreads();
+    if (s_done) return;  // uniform across the grid: no block reaches the barrier
+    double dot = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * kBlock) {
+        double q = a.in[i];
+        if (a.azd) q = sub_rn(q, az_row<KZ>(a, i));
+        a.out[i] = q;
+        dot += __ldg(a.dotv + i) * q;
+    }
+    {
+        __shared__ double sm[32];
+        double v[1] = {dot};
+        block_sum<1>(v, sm);
+        if (threadIdx.x == 0) pq_part[blockIdx.x] = v[0];
+    }
+    cooperative_groups::this_grid().sync();
+    const double pq = reduce_parts(pq_part, gridDim.x);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        cg_step_pq(st, pq);
+        if (use_if) cudaGraphSetConditional(hif, (!st->done && st->refresh_now) ? 1u : 0u);
+    }
+    if (pq <= 0.0 || !isfinite(pq)) return;  // curvature breakdown: no update (cg_step_pq)
+    const double alpha = s_rz / pq;
+    const bool refresh = ((s_iters + 1) % s_every) == 0;
+    double rr = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * kBlock) {
+        const double pi = a.dotv[i];
+        x[i] = add_rn(x[i], mul_rn(alpha, pi));
+        if (!refresh) {
+            const double ri = sub_rn(r[i], mul_rn(alpha, a.out[i]));
+            r[i] = ri;
+            rr += ri * ri;
+        }
+    }
+    if (!refresh) {
+        __shared__ double sm2[32];
+        double v[1] = {rr};
+        block_sum<1>(v, sm2);
+        if (threadIdx.x == 0) a.dot_part[blockIdx.x] = v[0];
+    }
 }
 
 // CG update (krylov.py:127-131): x += alpha p;  r -= alpha q  (+ r.r partial)
