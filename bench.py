@@ -47,6 +47,18 @@ def env_world():
     return ws, rank, local
 
 
+def cpu_model() -> str:
+    """Host CPU model and logical core count (state them beside the CPU number)."""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return f"{ln.split(':', 1)[1].strip()}, {os.cpu_count()} logical cores"
+    except OSError:
+        pass
+    return f"unknown, {os.cpu_count()} logical cores"
+
+
 def peaks():
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
@@ -191,7 +203,7 @@ def reference_arm(args, ws, rank):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"poisson7 {shape[0]}x{shape[1]}x{shape[2]}, m={ws} boxes {list(boxes)}, linear "
                                "deflation, SA-AMG+SPAI0, CG tol 1e-8 (configs[1])", "unknowns": n},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port", "cpu": cpu_model(),
                          "sample": f"oracle/port.py (numpy + C restatement of deflamg) on the full problem, "
                                    f"{its} CG iterations timed per step, scaled to {full} iterations "
                                    f"(the reference's count); operator matvec threaded x{cores}, V-cycle serial "
@@ -330,7 +342,7 @@ def b200_arm(args, ws, rank, local):
         o, setup = oracle_sample(A_rows, n, coords, part, cores, args.ref_iters, iters)
         value, per_iter, its = run_oracle_steps(o, n, h, 1, 0, args.ref_iters, iters, cores)
         line["cpu_baseline"] = {
-            "value": value, "unit": UNIT, "cores": cores, "kind": "port",
+            "value": value, "unit": UNIT, "cores": cores, "kind": "port", "cpu": cpu_model(),
             "sample": f"oracle/port.py on the same 150^3 problem, one solve capped at {its} CG iterations, "
                       f"per-iteration time x {iters} iterations; 1 thread; oracle setup {setup:.1f}s untimed"}
     if rank == 0:
