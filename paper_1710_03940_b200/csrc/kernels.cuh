@@ -721,6 +721,9 @@ __device__ __forceinline__ double epilogue(const RowArgs &a, int64_t i, double a
 #ifndef DFL_CLASS_MINB
 #define DFL_CLASS_MINB 5
 #endif
+#ifndef DFL_CLASS_RESID_MINB
+#define DFL_CLASS_RESID_MINB 4  // the w .* r gathers of the pre-smoothing residual
+#endif
 #ifndef DFL_ELL_MINB0
 #define DFL_ELL_MINB0 6
 #endif
@@ -945,7 +948,7 @@ __device__ __forceinline__ double class_row(const ClassTab &T, int c, int64_t ro
 // pipelined like k_codep: the next row's class byte and own-row operands are
 // loaded one iteration ahead and its leading gather edge is prefetched to L2
 template <int MODE, bool DOT>
-__global__ void __launch_bounds__(kBlock, MODE == MODE_RESID ? 4 : DFL_CLASS_MINB) k_class(DMat A, RowArgs a, const __grid_constant__ ClassTab T) {
+__global__ void __launch_bounds__(kBlock, MODE == MODE_RESID ? DFL_CLASS_RESID_MINB : DFL_CLASS_MINB) k_class(DMat A, RowArgs a, const __grid_constant__ ClassTab T) {
     DFL_PDL_ENTRY;
     constexpr bool kR = MODE != MODE_PLAIN || DOT;
     constexpr bool kPost = MODE == MODE_POST;
