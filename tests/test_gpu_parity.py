@@ -449,3 +449,30 @@ def test_results_in_pinned_blocks_stay_valid():
     gc.collect()
     b = nat.pinned_empty(1000)
     assert b.shape == (1000,)
+
+
+@pytest.mark.parametrize("diag", [[1.0, -1.0], [2.0, -1.0, 3.0, -4.0, 1.0, -2.0] * 20])
+def test_cg_curvature_breakdown_on_indefinite_matrix(diag):
+    """reference tests/test_krylov.py:150-156 through the solver API: an
+    indefinite operator stops CG with converged=False and the 'curvature'
+    breakdown (krylov.py:121-123), never an exception; same report and x as
+    the oracle."""
+    from paper_1710_03940_b200 import DeflatedSolver
+    from paper_1710_03940_b200.runtime import Partition
+    from paper_1710_03940_b200.sparse import SparseMatrix
+
+    n = len(diag)
+    A = SparseMatrix.from_dense(np.diag(diag))
+    b = np.zeros(n)
+    b[1::2] = 1.0
+    part = Partition(n, ((0, n),))
+    cfgd = {"solver": {"type": "cg", "tol": 1e-10, "maxiter": 10}, "precond": {"relax": {"type": "spai0"}}}
+    s = DeflatedSolver(A, part, config=SolverConfig(cfgd), deflated=False)
+    x, rep = s.solve(b)
+    o = port.DeflatedSolverOracle(A, part, config=SolverConfig(cfgd), deflated=False)
+    xo, ro = o.solve(b)
+    assert not rep["converged"] and not ro["converged"]
+    assert rep["breakdown"] and "curvature" in rep["breakdown"]
+    assert ro["breakdown"] and "curvature" in ro["breakdown"]
+    assert rep["iterations"] == ro["iterations"]
+    assert np.allclose(x, xo, rtol=1e-12, atol=1e-14)
