@@ -34,32 +34,12 @@ from .errors import ConfigError, DimensionError
 from .runtime import as_partition, rank_subdomains
 from .hostsetup import build_rank_setup
 from .sparse import as_csr_arrays
+from .surface import DeflationBasis, DeviceOperator, SubdomainHierarchy, subdomain_views
 
-__all__ = ["DeflatedSolver", "solve_deflated", "HierarchyInfo", "BasisInfo"]
+__all__ = ["DeflatedSolver", "solve_deflated", "build_basis", "make_coarse_solve", "DeflationBasis"]
 
 DEFLATION_KINDS = ("constant", "linear")
 B200_SOLVERS = ("cg", "bicgstab2", "gmres", "fgmres")
-
-
-class HierarchyInfo:
-    """What the report and tests need from a subdomain hierarchy."""
-
-    def __init__(self, level_sizes, level_nnz):
-        self.level_sizes = list(level_sizes)
-        self.level_nnz = list(level_nnz)
-
-
-class BasisInfo:
-    def __init__(self, kind, k, E, AZ_nnz, factorize_seconds):
-        self.kind = kind
-        self.columns_per_subdomain = k
-        self.E = E
-        self.AZ_nnz = AZ_nnz
-        self.factorize_seconds = factorize_seconds
-
-    @property
-    def n_coarse(self) -> int:
-        return int(self.E.shape[0])
 
 
 def _check_config(cfg: SolverConfig, deflated: bool):
@@ -91,6 +71,7 @@ class DeflatedSolver:
             raise DimensionError(f"matrix must be square, got {nrows}x{ncols}")
         part = as_partition(partition, nrows)
         world = world or current_world()
+        self.A = A
         subs = rank_subdomains(part.m, world.nranks, world.rank)
         r0, r1 = part.ranges[subs.start][0], part.ranges[subs.stop - 1][1]
         rows = (ptr[r0:r1 + 1] - ptr[r0], col[ptr[r0]:ptr[r1]], val[ptr[r0]:ptr[r1]])
@@ -109,6 +90,7 @@ class DeflatedSolver:
         """``rows`` = (row_ptr, col_idx, values) of this rank's rows (global
         column indices); ``coords_local`` their coordinates."""
         self = cls.__new__(cls)
+        self.A = None
         part = as_partition(partition, nglobal)
         world = world or current_world()
         self._init(rows, nglobal, part, config, coords_local, deflated, device, world, global_coords=None)
@@ -136,8 +118,12 @@ class DeflatedSolver:
         self.r0, self.r1, self.n_local = hs.r0, hs.r1, hs.n
         self.ghosts = hs.ghosts
         self.halo_plan = hs.halo_plan
-        self.hierarchies = [HierarchyInfo(h.level_sizes, h.level_nnz()) for h in hs.hier]
-        self.basis = (BasisInfo(hs.kind, hs.k, hs.E, int(hs.AZ.row_ptr[-1]), hs.factorize_seconds)
+        self._coords_local = None if coords is None else (
+            np.asarray(coords)[hs.r0:hs.r1] if global_coords is not None else np.asarray(coords))
+        self._views = None
+        self.hierarchies = [SubdomainHierarchy(self, j, h.level_sizes, h.level_nnz()) for j, h in enumerate(hs.hier)]
+        self.basis = (DeflationBasis(hs.kind, hs.k, hs.E, hs.centres, hs.factorize_seconds, int(hs.AZ.row_ptr[-1]),
+                                     _hs=hs, _nglobal=part.nglobal)
                       if self.deflated else None)
         # --- device upload
         self.device = device
@@ -188,10 +174,20 @@ class DeflatedSolver:
             return v_local
         return np.concatenate(self.world.allgather(v_local))
 
+    # -- attribute surface (deflation.py:205-221) -------------------------------
+    @property
+    def views(self) -> list:
+        """SubdomainView per (local) subdomain (runtime.py:80-152)."""
+        if self._views is None:
+            self._views = subdomain_views(self.host, self.partition, self._coords_local)
+        return self._views
+
+    @property
+    def op(self) -> DeviceOperator:
+        """Distributed A v (runtime.py:279-292) on the GPU: ``op.apply(v)`` or ``op(v)``."""
+        return DeviceOperator(self)
+
     # -- building blocks (device) ---------------------------------------------
-    def op(self, v):
-        """Distributed A v (runtime.py:283-292) on the GPU."""
-        return self._global(self._ctx.op_apply(self._local(v)))
 
     def project(self, r):
         """r - AZ E^{-1} Z' r (deflation.py:230-233) on the GPU."""
@@ -284,6 +280,76 @@ def solve_device(solver: "DeflatedSolver", b_ptr: int, x_ptr: int):
     """Solve with this rank's b and x already in device memory (raw CUDA
     pointers, e.g. ``torch.Tensor.data_ptr()``); returns the native report."""
     return solver._ctx.solve(_params(solver), b_ptr, x_ptr, nat.PTR_DEVICE)
+
+
+def build_basis(A, partition, kind: str = "constant", coords=None) -> DeflationBasis:
+    """Z, A Z and E = Z'AZ with its LU (deflation.py:83-163), from the
+    native host setup (bit-identical values; the solver uploads the same
+    products).  Single process: the whole matrix."""
+    if kind not in DEFLATION_KINDS:
+        raise ConfigError(f"unknown deflation kind '{kind}', expected one of {DEFLATION_KINDS}")
+    nrows, ncols, ptr, col, val = as_csr_arrays(A)
+    if nrows != ncols:
+        raise DimensionError(f"matrix must be square, got {nrows}x{ncols}")
+    part = as_partition(partition, nrows)
+    if kind == "linear":
+        if coords is None:
+            raise ConfigError("linear deflation needs node coordinates")
+        coords = np.asarray(coords, dtype=np.float64)
+        if coords.ndim == 1:
+            coords = coords[:, None]
+        if coords.shape[0] != nrows:
+            raise ConfigError(f"got coordinates for {coords.shape[0]} nodes, expected {nrows}")
+    cfg = SolverConfig({"deflation": {"kind": kind}})
+    hs = build_rank_setup((ptr, col, val), part, cfg, coords, True, World(), coords, build_hierarchies=False)
+    basis = DeflationBasis(hs.kind, hs.k, hs.E, hs.centres, hs.factorize_seconds, int(hs.AZ.row_ptr[-1]),
+                           _hs=hs, _nglobal=part.nglobal)
+    basis.coarse_lu  # noqa: B018  (the reference factorises here; singular E raises now)
+    return basis
+
+
+def make_coarse_solve(basis: DeflationBasis, inexact: bool = False, coarse_tol: float = 1e-2):
+    """The E-solve of the projector (deflation.py:166-178) as a host
+    callable; the device solve uses the replicated E^-1 (exact) or its
+    own inner GMRES (``deflation.inexact``)."""
+    if not inexact:
+        return basis.coarse_lu.solve
+    E = basis.E
+    K = basis.n_coarse
+
+    def solve(t):
+        # restarted GMRES on the dense E, restart K, maxiter 4K+20, relative tol (krylov.py:288-414)
+        t = np.asarray(t, dtype=np.float64)
+        y = np.zeros(K)
+        bn = float(np.linalg.norm(t))
+        if bn == 0.0:
+            return y
+        for _ in range(4 * K + 20):
+            r = t - E @ y
+            beta = float(np.linalg.norm(r))
+            if beta <= coarse_tol * bn:
+                break
+            V = np.zeros((K, K + 1))
+            H = np.zeros((K + 1, K))
+            V[:, 0] = r / beta
+            j_end = K
+            for j in range(K):
+                w = E @ V[:, j]
+                for i in range(j + 1):
+                    H[i, j] = float(np.dot(V[:, i], w))
+                    w = w - H[i, j] * V[:, i]
+                H[j + 1, j] = float(np.linalg.norm(w))
+                if H[j + 1, j] == 0.0:
+                    j_end = j + 1
+                    break
+                V[:, j + 1] = w / H[j + 1, j]
+            e1 = np.zeros(j_end + 1)
+            e1[0] = beta
+            c = np.linalg.lstsq(H[:j_end + 1, :j_end], e1, rcond=None)[0]
+            y = y + V[:, :j_end] @ c
+        return y
+
+    return solve
 
 
 def solve_deflated(A, b, partition=None, *, config=None, coords=None, deflated=True, threads_per_subdomain=1):

@@ -59,6 +59,9 @@ class RankSetup:
     k: int = 0
     zext: np.ndarray | None = None    # (n + n_ghost) x k values of Z
     zcols: np.ndarray | None = None   # n x (k-1) non-constant columns
+    zowner: np.ndarray | None = None  # owning subdomain of every own + ghost column of Z
+    rowsub: np.ndarray | None = None  # owning subdomain of every own row
+    centres: list | None = None       # DeflationBasis.centers (deflation.py:117-129)
     AZ: nat.CsrArrays | None = None
     E: np.ndarray | None = None
     Einv: np.ndarray | None = None
@@ -145,7 +148,7 @@ def build_rank_setup(rows, part, cfg, coords, deflated: bool, world: World, glob
 
     if deflated:
         kind = cfg.get("deflation.kind")
-        k, zext, owner, rowsub = _basis_inputs(hs, part, world, kind, my_coords, global_coords)
+        k, zext, owner, rowsub, centres = _basis_inputs(hs, part, world, kind, my_coords, global_coords)
         K = part.m * k
         az, E_rows = nat.basis_az(hs.op, k, zext, owner, rowsub, K, subs.start, len(subs))
         t_f = time.perf_counter()
@@ -153,6 +156,7 @@ def build_rank_setup(rows, part, cfg, coords, deflated: bool, world: World, glob
         Einv = nat.dense_inverse(E)
         hs.factorize_seconds = time.perf_counter() - t_f
         hs.kind, hs.k, hs.zext, hs.E, hs.Einv = kind, k, zext, E, Einv
+        hs.zowner, hs.rowsub, hs.centres = owner, rowsub, centres
         hs.zcols = np.ascontiguousarray(zext[:n, 1:]) if k > 1 else None
         hs.AZ = nat.CsrArrays(*az)
     return hs
@@ -194,7 +198,7 @@ def _basis_inputs(hs: RankSetup, part, world: World, kind, my_coords, global_coo
             for s in np.unique(hs.ghost_owner):
                 sel = hs.ghost_owner == s
                 zext[n:][sel, 1:] = gcoords[sel] - centres[int(s)]
-    return k, zext, owner, rowsub
+    return k, zext, owner, rowsub, centres
 
 
 def _exchange_ghost_coords(hs: RankSetup, world: World, my_coords):
