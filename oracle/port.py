@@ -135,6 +135,8 @@ def spmv(A: Csr, x: np.ndarray) -> np.ndarray:
     x = np.ascontiguousarray(x, dtype=np.float64)
     if x.shape != (A.ncols,):
         raise OracleError(f"spmv operand {x.shape} vs ncols {A.ncols}")
+    if _POOL is not None and A.nrows >= 65536:
+        return _local_matvec(A, x)  # row-chunked over the pool: every row summed as above
     out = np.empty(A.nrows)
     _clib().csr_spmv(_p(A.row_ptr), _p(A.col_idx), _p(A.values), _p(x), _p(out), 0, A.nrows)
     return out
@@ -372,15 +374,19 @@ _POOL = None
 
 def set_threads(t: int) -> None:
     """Row-chunked threading of the distributed matvec, as the reference's
-    threads_per_subdomain (runtime.py:228-243); numerically inert."""
+    threads_per_subdomain (runtime.py:228-243), and of the V-cycle's
+    products on levels of >= 64K rows; numerically inert (each row is
+    summed by one thread in CSR order)."""
     global _POOL
     from concurrent.futures import ThreadPoolExecutor
 
     _POOL = ThreadPoolExecutor(max_workers=t) if t > 1 else None
     _POOL_T[0] = t
+    _SUBPOOL[0] = ThreadPoolExecutor(max_workers=t) if t > 1 else None
 
 
 _POOL_T = [1]
+_SUBPOOL = [None]  # subdomain-level pool of the preconditioner (a separate pool: no nested waits)
 
 
 def _local_matvec(A: Csr, x: np.ndarray) -> np.ndarray:
@@ -775,6 +781,13 @@ class DeflatedSolverOracle:
 
     def precond(self, r):
         out = np.empty_like(r)
+        if _SUBPOOL[0] is not None and len(self.ranges) > 1:
+            # one V-cycle per subdomain, the subdomains concurrently (numerically inert)
+            def one(j):
+                b, e = self.ranges[j]
+                out[b:e] = self.hierarchies[j].apply(r[b:e])
+            list(_SUBPOOL[0].map(one, range(len(self.ranges))))
+            return out
         for h, (b, e) in zip(self.hierarchies, self.ranges):
             out[b:e] = h.apply(r[b:e])
         return out

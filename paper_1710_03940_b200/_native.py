@@ -25,6 +25,7 @@ DFL_RELAX = {"damped_jacobi": 0, "spai0": 1}
 DFL_SOLVER = {"cg": 0, "bicgstab2": 1, "gmres": 2, "fgmres": 3}
 PTR_HOST, PTR_DEVICE = 0, 1
 LEVEL_A, LEVEL_P, LEVEL_R = 0, 1, 2
+DFL_TIME_FLUSH_L2, DFL_TIME_FORMAT_BYTES = 0x100, 0x200  # dfl_ctx_time flags (include/dflb200.h)
 
 
 class Csr(ctypes.Structure):

@@ -206,9 +206,12 @@ int dfl_spmv_csr(const dfl_csr *A, const double *x, double *y, int device) {
 
 // algorithmic bytes: CSR with fp64 values / int32 indices,
 // every vector read once and written once per kernel
-int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
+int dfl_ctx_time(dfl_ctx *ctx, int what_flags, int reps, double *ms, double *bytes) {
     RC(ready(ctx));
     if (reps < 1) reps = 1;
+    const bool flush = (what_flags & DFL_TIME_FLUSH_L2) != 0;
+    const bool fmt_bytes = (what_flags & DFL_TIME_FORMAT_BYTES) != 0;
+    const int what = what_flags & 0xff;
     auto run = [&]() -> int {
         if (what == 0) return op_apply_dev(ctx, ctx->p, ctx->w, 0, nullptr, false, nullptr, 0);
         if (what == 1 || what == 2) return vcycle(ctx, ctx->r, ctx->z, nullptr, nullptr, nullptr);
@@ -235,7 +238,11 @@ int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
         return (M.vcode ? 5.0 : 12.0) * (double)M.stored + (M.perm ? 4.0 * rows : 0.0) +
                (M.ell_w ? 0.0 : 8.0 * (rows / 32 + 1));
     };
-    if (what == 0 || what == 4) {
+    if ((what == 0 || what == 4) && fmt_bytes) {
+        // the stored layout's bytes: each stored matrix byte once, x read once, y written once
+        *bytes = mat(ctx->Aop) + 8.0 * (ctx->n + ctx->n_ghost) + 8.0 * ctx->n;
+        if (what == 4 && ctx->deflation) *bytes += 8.0 * (ctx->k - 1) * ctx->n;  // Z columns 1..k-1
+    } else if (what == 0 || what == 4) {
         *bytes = 12.0 * ctx->op_nnz + 4.0 * (ctx->n + 1) + 8.0 * (ctx->n + ctx->n_ghost) + 8.0 * ctx->n;
         if (what == 4 && ctx->deflation) *bytes += 8.0 * (ctx->k - 1) * ctx->n;  // Z columns 1..k-1
     } else if (what == 5) {
@@ -297,6 +304,32 @@ int dfl_ctx_time(dfl_ctx *ctx, int what, int reps, double *ms, double *bytes) {
         return DFL_OK;
     }
     for (int i = 0; i < 3; ++i) RC(run());
+    if (flush) {
+        // cold L2 before every launch: write a buffer twice the L2 size, then
+        // time the launch alone between its own pair of events
+        const size_t fb = (size_t)256 << 20;
+        void *buf = nullptr;
+        CK(cudaMalloc(&buf, fb));
+        double tot = 0.0;
+        for (int i = 0; i < reps; ++i) {
+            CK(cudaMemsetAsync(buf, i & 0xff, fb, ctx->st));
+            CK(cudaEventRecord(ctx->ev0, ctx->st));
+            const int rc = run();
+            CK(cudaEventRecord(ctx->ev1, ctx->st));
+            if (rc != DFL_OK) {
+                cudaStreamSynchronize(ctx->st);
+                cudaFree(buf);
+                return rc;
+            }
+            CK(cudaEventSynchronize(ctx->ev1));
+            float t = 0;
+            CK(cudaEventElapsedTime(&t, ctx->ev0, ctx->ev1));
+            tot += t;
+        }
+        CK(cudaFree(buf));
+        *ms = tot / reps;
+        return DFL_OK;
+    }
     CK(cudaEventRecord(ctx->ev0, ctx->st));
     for (int i = 0; i < reps; ++i) RC(run());
     CK(cudaEventRecord(ctx->ev1, ctx->st));
