@@ -437,7 +437,15 @@ int basis_az(const dfl_csr *A, int k, const double *zext, const int32_t *owner,
     az.ptr.assign(n + 1, 0);
     az.col.clear();
     az.val.clear();
-    std::fill(E_rows, E_rows + (int64_t)nsub * k * K, 0.0);
+    // E = Z'AZ sums ~10^6 products per entry whose linear-column parts
+    // cancel almost completely (A applied to a linear function vanishes in
+    // the interior); a naive double sum leaves errors of ~1e-6 relative in
+    // the small entries, which makes the projector inconsistent with the
+    // device's Z' sums and stalls CG (200^3 jump problem, m=8: 130 vs 65
+    // iterations).  Accumulate in extended precision and round once: E is
+    // then Z'AZ of the stored AZ values to within an ulp, at least as
+    // accurate as the reference's blocked dgemm (deflation.py:144-149).
+    std::vector<long double> Eacc((size_t)nsub * k * K, 0.0L);
     for (int64_t i = 0; i < n; ++i) {
         cols.clear();
         for (int64_t e = A->row_ptr[i]; e < A->row_ptr[i + 1]; ++e) {
@@ -458,7 +466,8 @@ int basis_az(const dfl_csr *A, int k, const double *zext, const int32_t *owner,
         const int ls = rowsub[i] - sub0;
         for (int64_t cc : cols) {
             const double v = acc[cc];
-            for (int a = 0; a < k; ++a) E_rows[((int64_t)ls * k + a) * K + cc] += zext[i * k + a] * v;
+            for (int a = 0; a < k; ++a)
+                Eacc[((int64_t)ls * k + a) * K + cc] += (long double)zext[i * k + a] * (long double)v;
             if (keep_zeros || v != 0.0) {
                 az.col.push_back(cc);
                 az.val.push_back(v);
@@ -467,6 +476,7 @@ int basis_az(const dfl_csr *A, int k, const double *zext, const int32_t *owner,
         }
         az.ptr[i + 1] = (int64_t)az.col.size();
     }
+    for (size_t q = 0; q < Eacc.size(); ++q) E_rows[q] = (double)Eacc[q];
     return DFL_OK;
 }
 
