@@ -56,6 +56,7 @@ extern "C" {
 #define DFL_E_CONFIG (-6)      /* ConfigError */
 #define DFL_E_CUDA (-7)        /* CUDA runtime failure */
 #define DFL_E_STATE (-8)       /* call out of order (e.g. solve before finalize) */
+#define DFL_E_PARSE (-9)       /* ParseError (input files) */
 
 /* relaxation kinds (precond.relax.type) */
 #define DFL_RELAX_DAMPED_JACOBI 0
@@ -205,6 +206,17 @@ DFL_API int dfl_basis_az(const dfl_csr *A, int32_t k, const double *zext, const 
 DFL_API int dfl_matrix_shape(const dfl_matrix *m, int64_t *nrows, int64_t *ncols, int64_t *nnz);
 DFL_API int dfl_matrix_copy(const dfl_matrix *m, int64_t *row_ptr, int64_t *col_idx, double *values);
 DFL_API void dfl_matrix_free(dfl_matrix *m);
+
+/* ---- input files (mmio.py:29-157; native readers, csrc/mmio.cpp) -----------------------
+ * dfl_mm_read: MatrixMarket coordinate real|integer, general|symmetric ->
+ *   CSR (1-based indices converted, symmetric entries mirrored, entries in
+ *   (row, col) order with duplicates summed in file order) -- replaces
+ *   mmio.read_matrix_market (mmio.py:29-101).
+ * dfl_vec_read: one float per line (mask = 0, mmio.read_vector :115-131) or
+ *   one 0/1 per line (mask != 0, mmio.read_mask :140-157) -> n x 1 matrix.
+ * Failures: DFL_E_PARSE, "<path>:<line>: <reason>" in dfl_last_setup_error(). */
+DFL_API int dfl_mm_read(const char *path, dfl_matrix **out);
+DFL_API int dfl_vec_read(const char *path, int32_t mask, dfl_matrix **out);
 
 /* LU with partial pivoting; DFL_E_SINGULAR with the reference's criterion
  * (min |u_ii| <= 1e-14 max |u_ii|, sparse.py:236-241); writes inv (n x n). */

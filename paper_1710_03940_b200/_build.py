@@ -18,7 +18,7 @@ BUILD = os.path.join(REPO, "build", "dflb200")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SOURCES = ["ctx.cu", "ctx_layout.cu", "ctx_comm.cu", "ctx_cycle.cu", "ctx_cg.cu", "ctx_krylov.cu", "ctx_bicg.cu", "ctx_block.cu", "setup_dev.cu", "gen_dev.cu"]
-CXX_SOURCES = ["host_setup.cpp"]
+CXX_SOURCES = ["host_setup.cpp", "mmio.cpp"]
 
 
 def _nvcc() -> str:

@@ -133,6 +133,8 @@ def lib():
         "dfl_matrix_shape": ([c_vp, P(c_i64), P(c_i64), P(c_i64)], c_i32),
         "dfl_matrix_copy": ([c_vp, c_vp, c_vp, c_vp], c_i32),
         "dfl_matrix_free": ([c_vp], None),
+        "dfl_mm_read": ([ctypes.c_char_p, P(c_vp)], c_i32),
+        "dfl_vec_read": ([ctypes.c_char_p, c_i32, P(c_vp)], c_i32),
         "dfl_dense_inverse": ([c_i64, c_vp, c_vp], c_i32),
         "dfl_ctx_create": ([c_i32, P(c_vp)], c_i32),
         "dfl_ctx_destroy": ([c_vp], None),

@@ -8,31 +8,15 @@
 #include <mutex>
 #include "ctx_impl.cuh"
 
-bool g_use_pipe = false;  // TMA-staged variant (DFL_PIPE=1); see profiles/r01
-bool g_use_vcode = false;  // value-coded ELL for V-cycle P/R with <= 255 values (DFL_VCODE=1; measured neutral)
-double g_small_per_lane = 12.0;  // DFL_CSR_PER_LANE_SMALL: entries per lane for levels < 50K rows
-bool g_use_code = true;    // stencil-coded ELL for few-(offset, value) matrices (DFL_NO_CODE=1 disables)
-bool g_use_tiny = false;   // cluster kernel for the tiny levels (DFL_TINY=1; measured slower, profiles/r01)
-bool g_use_coarse = false;  // cooperative coarse-cycle kernel (DFL_COARSE=1; measured slower, profiles/r01)
-// layout experiments (profiling knobs, read once per context creation)
-// (measured on 150^3, see profiles/r01/README.md: CSR-vector with ~12 entries
-// per lane beats SELL-32-1024 for the coarse operators and R / P)
-bool g_allow_sell = false;    // DFL_SELL=1: SELL-C-sigma for every irregular matrix
-bool g_wr_split = false;      // DFL_WR_SPLIT=1: coded residual reads w .* r from a k_wr pass
-bool g_no_fin = true;                // DFL_FIN=1: CG scalars finished in the producing kernels (measured slower)
-int g_keep_mb = 0;                   // DFL_KEEP_MB: L2 evict-last loads for CSR matrices up to this size
-unsigned g_fin_mask = 0xffffffffu;   // with !g_no_fin: which finishes run in-kernel (DFL_FIN_MASK)
-bool g_nccl_graph = false;    // DFL_NCCL_GRAPH=1: several NCCL ranks replay the captured CG body (measured neutral on 1 rank)
-bool g_no_sell = false;       // DFL_NO_SELL=1: long-row matrices as CSR-vector instead of SELL
-bool g_sell_wave = false;     // DFL_SELL_WAVE=1: sliced ELL grid-stride over one resident wave
-bool g_use_scode = false;     // DFL_SCODE=1: gap/value-coded SELL for R (measured slower: 71 vs 41 us)
-bool g_use_pcode = true;      // DFL_NO_PCODE=1: no delta/value-coded rows (P)
-bool g_op_pf = true;          // DFL_OP_PF=0: no next-wave L2 prefetch in the class-coded operator
+// format / launch switches (read once per context creation; the A/B record
+// of every layout and launch variant that was measured and dropped is in
+// profiles/r01/README.md and profiles/r02/README.md)
+bool g_use_code = true;       // DFL_NO_CODE=1: no stencil-coded ELL
 bool g_use_class = true;      // DFL_NO_CLASS=1: no row-class coded matrices
-bool g_code_pipe = true;      // DFL_CODE_PIPE=0: coded rows without the software pipeline
+bool g_use_pcode = true;      // DFL_NO_PCODE=1: no delta/value-coded rows (P)
+bool g_no_sell = false;       // DFL_NO_SELL=1: long-row matrices as CSR-vector instead of SELL
 bool g_pdl = true;            // DFL_NO_PDL=1: plain launches instead of programmatic dependent launch
-int g_csr_g = 0;              // DFL_CSR_G=n forces the CSR lanes per row
-double g_csr_per_lane = 12.0; // DFL_CSR_PER_LANE: target entries per lane
+bool g_nccl_graph = false;    // DFL_NCCL_GRAPH=1: several NCCL ranks replay the captured CG body
 int g_sm_count = 148;
 
 static int stage_in(dfl_ctx *ctx, double *dst, const double *src, int ptr_kind) {
@@ -108,58 +92,16 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
     if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
     if (e == cudaSuccess) g_sm_count = ctx->sm_count;
     if (e == cudaSuccess) {
-        pipe_attrs();
-        const char *np = getenv("DFL_PIPE");
-        g_use_pipe = np && np[0] == '1';
-        const char *nvc = getenv("DFL_VCODE");
-        g_use_vcode = nvc && nvc[0] == '1';
-        const char *spl = getenv("DFL_CSR_PER_LANE_SMALL");
-        g_small_per_lane = spl ? atof(spl) : 12.0;
-        const char *ncd = getenv("DFL_NO_CODE");
-        g_use_code = !(ncd && ncd[0] == '1');
-        const char *sp = getenv("DFL_SHORT_PAD");
-        kShortRowPad = sp ? atof(sp) : 1.7;
-        const char *nt = getenv("DFL_TINY");
-        g_use_tiny = nt && nt[0] == '1';
-        const char *nc = getenv("DFL_COARSE");
-        g_use_coarse = nc && nc[0] == '1';
-        const char *ns = getenv("DFL_SELL");
-        g_allow_sell = ns && ns[0] == '1';
-        const char *ws = getenv("DFL_WR_SPLIT");
-        g_wr_split = ws && ws[0] == '1';
-        const char *nf = getenv("DFL_FIN");
-        g_no_fin = !(nf && nf[0] == '1');
-        // DFL_FIN_MASK: bit 1 << ACT_* enables the grid finish per CG scalar (PQ 2, RR 4, RZ 8),
-        // bit 16 the operator's in-kernel Z'y finish; DFL_FIN=1 enables all of them
-        const char *km = getenv("DFL_KEEP_MB");
-        if (km) g_keep_mb = atoi(km);
-        const char *fm = getenv("DFL_FIN_MASK");
-        if (fm) {
-            g_fin_mask = (unsigned)atoi(fm);
-            g_no_fin = g_fin_mask == 0;
-        }
-        const char *ngr = getenv("DFL_NCCL_GRAPH");
-        g_nccl_graph = ngr && ngr[0] == '1';
-        const char *nse = getenv("DFL_NO_SELL");
-        g_no_sell = nse && nse[0] == '1';
-        const char *swv = getenv("DFL_SELL_WAVE");
-        g_sell_wave = swv && swv[0] == '1';
-        const char *nsc = getenv("DFL_SCODE");
-        g_use_scode = nsc && nsc[0] == '1';
-        const char *npc = getenv("DFL_NO_PCODE");
-        g_use_pcode = !(npc && npc[0] == '1');
-        const char *opf = getenv("DFL_OP_PF");
-        g_op_pf = !(opf && opf[0] == '0');
-        const char *ncl = getenv("DFL_NO_CLASS");
-        g_use_class = !(ncl && ncl[0] == '1');
-        const char *cp = getenv("DFL_CODE_PIPE");
-        g_code_pipe = !(cp && cp[0] == '0');
-        const char *np2 = getenv("DFL_NO_PDL");
-        g_pdl = !(np2 && np2[0] == '1');
-        const char *cg = getenv("DFL_CSR_G");
-        g_csr_g = cg ? atoi(cg) : 0;
-        const char *cl = getenv("DFL_CSR_PER_LANE");
-        g_csr_per_lane = cl ? atof(cl) : 12.0;
+        auto on = [](const char *name) {
+            const char *v = getenv(name);
+            return v && v[0] == '1';
+        };
+        g_use_code = !on("DFL_NO_CODE");
+        g_use_class = !on("DFL_NO_CLASS");
+        g_use_pcode = !on("DFL_NO_PCODE");
+        g_no_sell = on("DFL_NO_SELL");
+        g_pdl = !on("DFL_NO_PDL");
+        g_nccl_graph = on("DFL_NCCL_GRAPH");
     }
     if (e != cudaSuccess) {
         dfl::set_setup_error(std::string("CUDA context creation failed: ") + cudaGetErrorString(e));
@@ -231,9 +173,7 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
     // reads ELL / CSR, so a rank with ghost columns keeps those.
     const char *no_ov = getenv("DFL_NO_OVERLAP");
     const bool will_split = multi(ctx) && A->ncols > A->nrows && !(no_ov && no_ov[0] == '1');
-    RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, &ctx->op_sub_tiles_h, true, nullptr, nullptr, false, false,
-                     false, !will_split));
-    if (ctx->Aop.pipe.stages) RC(upload(ctx, &ctx->op_sub_tiles, ctx->op_sub_tiles_h.data(), (int64_t)ctx->op_sub_tiles_h.size()));
+    RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, nullptr, true, nullptr, nullptr, false, false, !will_split));
     ctx->op_nnz = ctx->Aop.nnz;
     int64_t nrecv = 0;
     ctx->nbr.clear();
@@ -454,20 +394,13 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
     // block of the multi-dot kernels (grid <= 4 * SMs)
     const int64_t dslots = std::max({ctx->nblk, vparts, kDotStride * std::max<int64_t>(ctx->nblk, 4 * ctx->sm_count)});
     RC(dalloc(ctx, &ctx->dpart, dslots + 64));
-    RC(dalloc(ctx, &ctx->dpart_pq, ctx->vgrid + 64));
-    RC(dalloc(ctx, &ctx->zt_part, (std::max(ctx->ntiles, ctx->Aop.pipe.ntiles) + ctx->nbtiles) * kKmax + 64));
+    RC(dalloc(ctx, &ctx->zt_part, (ctx->ntiles + ctx->nbtiles) * kKmax + 64));
     RC(dalloc(ctx, &ctx->scal, 16));
     RC(dalloc(ctx, &ctx->sgather, (int64_t)8 * ctx->nranks));
     RC(dalloc(ctx, &ctx->state, 1));
     CK(cudaMallocHost(&ctx->h_dots, 16 * sizeof(double)));
     RC(dalloc(ctx, &ctx->ticket, 4));
     CK(cudaMemset(ctx->ticket, 0, 4 * sizeof(unsigned int)));
-    // grid-finish groups: the largest grid of a finishing kernel is the
-    // operator / vector grid (ntiles, nblk) or the V-cycle's dot kernel
-    ctx->fin_groups = cdiv(std::max({ctx->nblk, ctx->ntiles, vparts}), kFinGroup) + ctx->nsub + 2;
-    RC(dalloc(ctx, &ctx->fin_tick, ctx->fin_groups + 1));
-    CK(cudaMemset(ctx->fin_tick, 0, sizeof(unsigned int) * (ctx->fin_groups + 1)));
-    RC(dalloc(ctx, &ctx->fin_gpart, ctx->fin_groups * kKmax));
     CK(cudaMemset(ctx->x, 0, sizeof(double) * nx));
     CK(cudaMemset(ctx->xin, 0, sizeof(double) * nx));
     CK(cudaMemset(ctx->p, 0, sizeof(double) * nx));

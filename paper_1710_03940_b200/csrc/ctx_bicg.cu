@@ -323,9 +323,8 @@ static unsigned bg_dot_grid(dfl_ctx *ctx) {
 // out = op_hat(v) = project(A (M v)); with dotv: per-block partials of out.dotv in dpart (vgrid)
 static int bg_op_hat(dfl_ctx *ctx, bool defl, KState *ks, const double *v, double *out, const double *dotv) {
     RC(vcycle(ctx, v, ctx->zx, ks, nullptr, nullptr));
-    bool tz = false;
-    RC(op_apply_dev(ctx, ctx->zx, ctx->w, 0, nullptr, defl, ks, 0, &tz));
-    if (defl) RC(zt_to_t2(ctx, ks, 0, true, tz));
+    RC(op_apply_dev(ctx, ctx->zx, ctx->w, 0, nullptr, defl, ks, 0));
+    if (defl) RC(zt_to_t2(ctx, ks, 0, true));
     ProjArgs a = proj_args(ctx, ctx->w, out, ks);
     if (!defl) a.azd = nullptr, a.K = 0;
     if (dotv) {

@@ -122,13 +122,12 @@ __global__ void k_cg_end(KState *st, cudaGraphConditionalHandle h, int use_cond)
 // ---------------------------------------------------------------------------
 // one CG iteration (krylov.py:119-143) on the projected operator.
 //
-// Single rank: the scalar steps run in the last block of the kernel that
-// produces their reduction (grid finish, kernels.cuh Fin), the operator
-// kernel finishes Z'w -> t -> t2 itself, and with a graph the refresh of
+// Body: op (+Z'w partials), Z'w finish + E^-1, project (+p.q), alpha step,
+// update (+r.r), convergence step, [refresh], V-cycle (+r.z), beta step,
+// p update (+loop condition).  Single rank: with a graph the refresh of
 // krylov.py:128-129 is a conditional IF node (no launches on the other 49 of
-// 50 iterations).  Body: op, project(+alpha), update(+r.r test), [refresh],
-// V-cycle (+beta), p update (+loop condition).  Several ranks: partials are
-// reduced, allgathered and consumed by single-block scalar kernels.
+// 50 iterations).  Several ranks: partials are reduced, allgathered and
+// consumed by single-block scalar kernels.
 struct CgGraph {
     int use_cond = 0;
     cudaGraphConditionalHandle h = 0;
@@ -139,16 +138,14 @@ struct CgGraph {
 // r = b' - project(A x)  (krylov.py:128-129); need_refresh: predicated on st->refresh_now
 static int cg_refresh(dfl_ctx *ctx, bool deflated, int need_refresh) {
     KState *st = ctx->state;
-    bool tz = false;
-    RC(op_apply_dev(ctx, ctx->x, ctx->tmp, 0, nullptr, deflated, st, need_refresh, &tz));
-    if (deflated) RC(zt_to_t2(ctx, st, need_refresh, true, tz));
+    RC(op_apply_dev(ctx, ctx->x, ctx->tmp, 0, nullptr, deflated, st, need_refresh));
+    if (deflated) RC(zt_to_t2(ctx, st, need_refresh, true));
     ProjArgs a = proj_args(ctx, ctx->tmp, ctx->r, st);
     if (!deflated) a.azd = nullptr, a.K = 0;
     a.base = ctx->bp;
     a.dotmode = 2;
     a.dot_part = ctx->dpart;
     a.need_refresh = need_refresh;
-    a.fin = make_fin(ctx, ACT_RR);
     launch_project<1>(ctx, a);
     return DFL_OK;
 }
@@ -184,88 +181,28 @@ static int capture_refresh_if(dfl_ctx *ctx, bool deflated, cudaGraphConditionalH
     return DFL_OK;
 }
 
-// DFL_FUSE_PU=1: the cooperative k_proj_update fits when the one-wave vector
-// grid is co-resident for it
-static bool fuse_pu_ok(dfl_ctx *ctx, int k) {
-    static const bool on = [] {
-        const char *e = getenv("DFL_FUSE_PU");
-        return e && e[0] == '1';
-    }();
-    if (!on || !ctx->dpart_pq) return false;
-    const int kz = k <= 1 ? 1 : k <= 2 ? 2 : k <= 4 ? 4 : 8;
-    const int occ = kz == 1 ? occupancy(k_proj_update<1>) : kz == 2 ? occupancy(k_proj_update<2>)
-                  : kz == 4 ? occupancy(k_proj_update<4>) : occupancy(k_proj_update<8>);
-    return ctx->vgrid <= (int64_t)occ * ctx->sm_count;
-}
-
-template <int KZ>
-static int launch_pu(dfl_ctx *ctx, const ProjArgs &a, int use_if, cudaGraphConditionalHandle hif) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)ctx->vgrid);
-    cfg.blockDim = dim3(kBlock);
-    cfg.stream = ctx->st;
-    cudaLaunchAttribute at[2];
-    at[0].id = cudaLaunchAttributeCooperative;
-    at[0].val.cooperative = 1;
-    int na = 1;
-    if (g_pdl) {
-        at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[1].val.programmaticStreamSerializationAllowed = 1;
-        na = 2;
-    }
-    cfg.attrs = at;
-    cfg.numAttrs = na;
-    CK(cudaLaunchKernelEx(&cfg, k_proj_update<KZ>, a, ctx->x, ctx->r, ctx->dpart_pq, ctx->state, use_if, hif));
-    ctx->launches++;
-    return DFL_OK;
-}
-
-static int launch_proj_update(dfl_ctx *ctx, const ProjArgs &a, int use_if, cudaGraphConditionalHandle hif) {
-    const int k = a.azd ? a.k : 1;
-    if (k <= 1) return launch_pu<1>(ctx, a, use_if, hif);
-    if (k <= 2) return launch_pu<2>(ctx, a, use_if, hif);
-    if (k <= 4) return launch_pu<4>(ctx, a, use_if, hif);
-    return launch_pu<8>(ctx, a, use_if, hif);
-}
-
 static int cg_body(dfl_ctx *ctx, bool deflated, const CgGraph &G) {
     KState *st = ctx->state;
     const double *gath;
     const bool single = !multi(ctx);
-    bool fused = false;
     // w = A p, Z'w -> t2 ; q = w - AZ t2 ; p.q
-    bool tz = false;
-    RC(op_apply_dev(ctx, ctx->p, ctx->w, 0, nullptr, deflated, st, 0, &tz));
-    if (deflated) RC(zt_to_t2(ctx, st, 0, true, tz));
+    RC(op_apply_dev(ctx, ctx->p, ctx->w, 0, nullptr, deflated, st, 0));
+    if (deflated) RC(zt_to_t2(ctx, st, 0, true));
     {
         ProjArgs a = proj_args(ctx, ctx->w, ctx->w, st);
         if (!deflated) a.azd = nullptr, a.K = 0;
         a.dotmode = 1;
         a.dotv = ctx->p;
         a.dot_part = ctx->dpart;
-        a.fin = make_fin(ctx, ACT_PQ);
-        a.fin.use_if = G.use_if;
-        a.fin.hif = G.hif;
-        if (single && !a.fin.tick && fuse_pu_ok(ctx, a.azd ? a.k : 1)) {
-            // projection + scalar step + update in one cooperative kernel (DFL_FUSE_PU=1)
-            RC(launch_proj_update(ctx, a, G.use_if, G.hif));
-            fused = true;
-        } else {
-            launch_project<0>(ctx, a);
-            if (!a.fin.tick) {
-                RC(rank_scalar(ctx, ctx->dpart, ctx->vgrid, 0, &gath));
-                launch_k(ctx->st, k_cg_pq, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, gath, ctx->nranks, G.use_if, G.hif);
-                ctx->launches++;
-            }
-        }
-    }
-    // x += alpha p ; r -= alpha q (regular iterations; + r.r test when finished in-kernel)
-    const Fin frr = fused ? Fin{} : make_fin(ctx, ACT_RR);
-    if (!fused) {
-        launch_k(ctx->st, k_cg_update, (unsigned)ctx->vgrid, kBlock, 0, ctx->x, ctx->r, ctx->p, ctx->w, ctx->n,
-                 ctx->dpart, st, frr);
+        launch_project<0>(ctx, a);
+        RC(rank_scalar(ctx, ctx->dpart, ctx->vgrid, 0, &gath));
+        launch_k(ctx->st, k_cg_pq, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, gath, ctx->nranks, G.use_if, G.hif);
         ctx->launches++;
     }
+    // x += alpha p ; r -= alpha q (regular iterations)
+    launch_k(ctx->st, k_cg_update, (unsigned)ctx->vgrid, kBlock, 0, ctx->x, ctx->r, ctx->p, ctx->w, ctx->n,
+             ctx->dpart, st);
+    ctx->launches++;
     // refresh iterations: r = b' - project(A x)   (krylov.py:128-129)
     if (G.use_if)
         RC(capture_refresh_if(ctx, deflated, G.hif));
@@ -282,18 +219,12 @@ static int cg_body(dfl_ctx *ctx, bool deflated, const CgGraph &G) {
         launch_k(ctx->st, k_cg_rrz, 1, 32, 0, st, ctx->sgather, ctx->nranks);
         ctx->launches += 3;
     } else {
-        if (!frr.tick) {
-            launch_k(ctx->st, k_cg_rr, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, nullptr, 1);
-            ctx->launches++;
-        }
+        launch_k(ctx->st, k_cg_rr, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, nullptr, 1);
+        ctx->launches++;
         // z = M r, r.z -> beta
-        const Fin frz = make_fin(ctx, ACT_RZ);
-        bool used = false;
-        RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np, &frz, &used));
-        if (!used) {
-            launch_k(ctx->st, k_cg_rz, 1, 1024, 0, st, ctx->dpart, np, nullptr, 1);
-            ctx->launches++;
-        }
+        RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
+        launch_k(ctx->st, k_cg_rz, 1, 1024, 0, st, ctx->dpart, np, nullptr, 1);
+        ctx->launches++;
     }
     launch_k(ctx->st, k_cg_p, (unsigned)ctx->vgrid, kBlock, 0, ctx->p, ctx->z, ctx->n, st, G.use_cond, G.h, G.use_if,
                                                        G.hif);
@@ -377,8 +308,6 @@ int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
     KState *st = ctx->state;
     const bool defl = p->deflated != 0;
     const double *gath;
-    // grid-finish counters start at zero (a failed launch could leave them dirty)
-    if (ctx->fin_tick) CK(cudaMemsetAsync(ctx->fin_tick, 0, sizeof(unsigned) * (ctx->fin_groups + 1), ctx->st));
     // x = 0 (y of the deflated system)
     launch_k(ctx->st, k_fill, (unsigned)ctx->nblk, kBlock, 0, ctx->x, 0.0, ctx->n);
     // ||b||

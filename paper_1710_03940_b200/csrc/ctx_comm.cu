@@ -94,18 +94,8 @@ int halo(dfl_ctx *ctx, double *v, cudaStream_t xs) {
 }
 
 // Z' v partials -> t (global numbering) -> t2 = E^-1 t on every rank
-// (t_ready: the operator kernel already wrote t, and t2 unless inexact)
-int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op, bool t_ready) {
-    const int64_t *sub_tiles =
-        (from_op && g_use_pipe && !ctx->split && ctx->Aop.pipe.stages) ? ctx->op_sub_tiles : ctx->sub_tiles;
-    if (t_ready) {
-        if (ctx->inexact) {
-            launch_k(ctx->st, k_egmres, 1, 256, 0, ctx->Edense, (int)ctx->K, ctx->tvec, ctx->t2, ctx->coarse_tol,
-                                             ctx->egm_scr, st, need_refresh);
-            ctx->launches++;
-        }
-        return DFL_OK;
-    }
+int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op) {
+    const int64_t *sub_tiles = ctx->sub_tiles;
     if (!multi(ctx)) {
         launch_k(ctx->st, k_zt_finish, ctx->nsub * ctx->k, 1024, 0, ctx->zt_part, sub_tiles, ctx->nsub, ctx->k,
                                                              ctx->tvec, 0, ctx->inexact ? nullptr : ctx->Einv,

@@ -6,31 +6,19 @@
 // V-cycle over all groups: z = M r  (deflation.py:239-250 -> amg.py:201-212).
 // With dot_part != nullptr the last kernel of every group also emits the
 // per-block partials of r.z; *nparts receives their count.
-// With fin (single group only) the dot kernel also finishes the reduction
-// and runs fin->act (*fin_used = true).
-int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *dot_part, int64_t *nparts,
-           const Fin *fin, bool *fin_used) {
+int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *dot_part, int64_t *nparts) {
     int64_t poff = 0;
-    if (fin_used) *fin_used = false;
     for (VGroup &g : ctx->groups) {
         const double *rin = r + g.row0;
         double *zout = z + g.row0;
         const int L = (int)g.lv.size();
-        const bool use_coarse = g.lc >= 0 && g_use_coarse;
-        const bool use_tiny = !use_coarse && g.lt >= 0 && g_use_tiny;
-        const int lc = use_coarse ? g.lc : use_tiny ? g.lt : L + 1;  // first level of the fused tail kernel
-        for (int l = 0; l < std::min(L, lc); ++l) {
+        for (int l = 0; l < L; ++l) {
             DLevel &v = g.lv[l];
             const double *in = l == 0 ? rin : v.rv;
             double *next = (l + 1 < L) ? g.lv[l + 1].rv : g.rb;
             if (v.A.fmt == FMT_CODE || v.A.fmt == FMT_CLASS) {
-                const double *wr = nullptr;  // w .* r formed at the gather
-                if (g_wr_split && v.A.fmt == FMT_CODE) {
-                    launch_k(ctx->st, k_wr, (unsigned)cdiv(v.n, kBlock), kBlock, 0, v.w, in, v.wr, v.n);
-                    ctx->launches++;
-                    wr = v.wr;
-                }
-                RowArgs a{wr, v.w, in, nullptr, v.t, nullptr, st};
+                // w .* r formed at the gather
+                RowArgs a{nullptr, v.w, in, nullptr, v.t, nullptr, st};
                 launch_rows<MODE_RESID, false>(ctx, v.A, a);
             } else {
                 RowArgs a{nullptr, v.w, in, nullptr, v.t, nullptr, st};
@@ -41,24 +29,7 @@ int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *d
             launch_rows<MODE_PLAIN, false>(ctx, v.R, b);
             prof_mark(ctx, "L" + std::to_string(l) + " restrict");
         }
-        if (lc <= L) {
-            const double *crin = lc == 0 ? rin : g.lv[lc < L ? lc : 0].rv;
-            double *cxout = lc == 0 ? zout : g.lv[lc < L ? lc : 0].xv;
-            if (lc == L && L > 0) {  // bottom only
-                crin = g.rb;
-                cxout = g.xb;
-            }
-            if (use_tiny) {
-                k_tiny_cycle<<<kTinyCtas, kTinyThreads, 0, ctx->st>>>(g.targs, crin, cxout);
-                ctx->launches++;
-                prof_mark(ctx, "tiny L" + std::to_string(lc) + "+");
-            } else {
-                void *args[] = {(void *)&g.cargs, (void *)&crin, (void *)&cxout};
-                cudaLaunchCooperativeKernel((const void *)k_coarse_cycle, g.coarse_grid, 256, args, 0, ctx->st);
-                ctx->launches++;
-                prof_mark(ctx, "coarse L" + std::to_string(lc) + "+");
-            }
-        } else {
+        {
             const double *rb = L == 0 ? rin : g.rb;
             double *xb = L == 0 ? zout : g.xb;
             launch_k(ctx->st, k_bottom, dim3((unsigned)cdiv(g.max_nb, 32), (unsigned)g.nsub), 256, 0, 
@@ -66,7 +37,7 @@ int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *d
             ctx->launches++;
             prof_mark(ctx, "bottom");
         }
-        for (int l = std::min(L, lc) - 1; l >= 0; --l) {
+        for (int l = L - 1; l >= 0; --l) {
             DLevel &v = g.lv[l];
             const double *in = l == 0 ? rin : v.rv;
             const double *e = (l + 1 < L) ? g.lv[l + 1].xv : g.xb;
@@ -76,10 +47,6 @@ int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *d
             prof_mark(ctx, "L" + std::to_string(l) + " prolong");
             if (l == 0 && dot_part) {
                 RowArgs b{v.t, v.w, in, v.t, out, dot_part + poff, st};
-                if (fin && fin->tick && ctx->groups.size() == 1 && !g_use_pipe) {
-                    b.fin = *fin;
-                    if (fin_used) *fin_used = true;
-                }
                 launch_rows<MODE_POST, true>(ctx, v.A, b);
                 poff += parts_for(v.A);
             } else {
@@ -88,7 +55,7 @@ int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *d
             }
             prof_mark(ctx, "L" + std::to_string(l) + " post");
         }
-        if ((L == 0 || lc == 0) && dot_part) {
+        if (L == 0 && dot_part) {
             // the group's finest level ran without a fused dot: explicit partials
             const int64_t rows = g.row1 - g.row0;
             const unsigned nb = (unsigned)std::max<int64_t>(1, std::min<int64_t>(cdiv(rows, kBlock), 64));
@@ -103,19 +70,8 @@ int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *d
 
 // y = A x (opmode 0) or y = b - A x (opmode 1); with zt the Z'y tile partials
 int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double *b, bool zt,
-                        const KState *st, int need_refresh, bool *fin_zt) {
+                        const KState *st, int need_refresh) {
     OpArgs a{xin, b, y, ctx->zcols, ctx->n, zt ? ctx->k : 0, ctx->zt_part, st, need_refresh};
-    if (fin_zt) *fin_zt = false;
-    if (fin_zt && zt && ctx->k > 0 && op_fusable(ctx)) {
-        a.tick = ctx->fin_tick;
-        a.gpart = ctx->fin_gpart;
-        a.t = ctx->tvec;
-        a.Einv = ctx->inexact ? nullptr : ctx->Einv;
-        a.t2 = ctx->t2;
-        a.K = ctx->K;
-        a.first_col = (int64_t)ctx->first_sub * ctx->k;
-        *fin_zt = true;
-    }
     if (!ctx->split) {
         RC(halo(ctx, xin));
         if (opmode == 0)
@@ -233,9 +189,8 @@ int dfl_ctx_time(dfl_ctx *ctx, int what_flags, int reps, double *ms, double *byt
         if (M.fmt == FMT_CODE) return 8.0 * rows;
         if (M.fmt == FMT_CLASS) return 1.0 * rows;
         if (M.fmt == FMT_PCODE) return 20.0 * rows;
-        if (M.fmt == FMT_SCODE) return 3.0 * (double)M.stored + 8.0 * rows + 8.0 * (rows / 32 + 1);
         if (M.fmt == FMT_CSR) return 12.0 * (double)M.nnz + 4.0 * (rows + 1);
-        return (M.vcode ? 5.0 : 12.0) * (double)M.stored + (M.perm ? 4.0 * rows : 0.0) +
+        return 12.0 * (double)M.stored + (M.perm ? 4.0 * rows : 0.0) +
                (M.ell_w ? 0.0 : 8.0 * (rows / 32 + 1));
     };
     if ((what == 0 || what == 4) && fmt_bytes) {

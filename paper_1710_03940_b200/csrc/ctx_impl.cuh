@@ -18,8 +18,6 @@
 #include "../../include/dflb200.h"
 #include "host_setup.hpp"
 #include "kernels.cuh"
-#include "spmv_pipe.cuh"
-#include "coarse.cuh"
 
 using namespace dfl;
 
@@ -72,13 +70,8 @@ struct Nccl {
 extern Nccl g_nccl;
 
 // profiling / layout knobs (defined in ctx.cu, read at context creation)
-extern bool g_use_pipe, g_use_vcode, g_use_code, g_use_tiny, g_use_coarse, g_allow_sell, g_wr_split, g_no_fin, g_pdl, g_code_pipe, g_use_class, g_op_pf, g_use_pcode, g_use_scode, g_sell_wave, g_no_sell, g_nccl_graph;
-extern unsigned g_fin_mask;
-extern int g_keep_mb;
-extern double g_small_per_lane, g_csr_per_lane;
-extern int g_csr_g, g_sm_count;
-static constexpr int64_t kCoarseRows = 65536;  // levels at or below this size run in k_coarse_cycle
-static constexpr int kStageBytesMax = 100 * 1024;
+extern bool g_use_code, g_use_class, g_use_pcode, g_no_sell, g_pdl, g_nccl_graph;
+extern int g_sm_count;
 
 // ---------------------------------------------------------------------------
 
@@ -103,13 +96,6 @@ struct VGroup {
     int64_t *binv_off = nullptr;     // per subdomain offset into binvT
     int64_t *b_off = nullptr;        // nsub + 1 row offsets in rb
     int max_nb = 0;
-    // levels [lc, L) and the bottom run in one cooperative kernel (coarse.cuh)
-    int lc = -1;                     // -1: no coarse kernel
-    CoarseArgs *cargs = nullptr;     // device copy
-    int lt = -1;                     // levels [lt, L) + bottom run in k_tiny_cycle (-1: none)
-    CoarseArgs *targs = nullptr;
-    unsigned coarse_grid = 0;
-    double *binv = nullptr;          // row-major inverses for the cooperative kernel
     // host-side statistics
     std::vector<int64_t> nnzA, nnzP, rows;
 };
@@ -143,12 +129,9 @@ struct dfl_ctx {
     int device = 0;
     dfl_fabric *fab = nullptr;
     int sm_count = 148;
-    std::vector<int64_t> op_sub_tiles_h;
-    int64_t *op_sub_tiles = nullptr;   // first op-pipe tile of every subdomain
     cudaStream_t st = nullptr;
     cudaStream_t st_copy = nullptr;  // x read-back, overlapped with the true-residual kernels
     std::mutex setup_mu;
-    double *dpart_pq = nullptr;      // p.q partials of the fused projection + update (DFL_FUSE_PU)             // allocation list / class tables while levels convert in parallel
     std::string err;
     std::vector<void *> allocs;
     int64_t bytes = 0;
@@ -210,10 +193,6 @@ struct dfl_ctx {
     double *zt_part = nullptr;
     double *tgather = nullptr;  // nranks * maxsub * k
     unsigned int *ticket = nullptr;
-    // grid finish (kernels.cuh Fin): counters (zero between launches) and group sums
-    unsigned int *fin_tick = nullptr;
-    double *fin_gpart = nullptr;
-    int64_t fin_groups = 0;
     cudaStream_t st_if = nullptr;  // capture stream of the refresh IF body
     int max_nsub = 0;
     std::vector<int> rank_nsub;  // subdomains per rank (runtime.rank_subdomains)
@@ -360,12 +339,10 @@ inline int occupancy(K kernel) {
     return std::max(1, b);
 }
 
-// grid of the grid-stride FMT_CODE / VELL kernels: one wave of the instance
+// grid of the grid-stride FMT_CODE kernels: one wave of the instance
 template <int MODE, bool DOT>
 inline int64_t code_grid(const DMat &A) {
-    static const int occ_code = g_code_pipe ? occupancy(k_codep<MODE, DOT>) : occupancy(k_code<MODE, DOT>);
-    static const int occ_vell = occupancy(k_vell<MODE, DOT>);
-    const int occ = A.vcode ? occ_vell : occ_code;
+    static const int occ = occupancy(k_codep<MODE, DOT>);
     return std::max<int64_t>(1, std::min<int64_t>(cdiv(A.nrows, kBlock), (int64_t)occ * g_sm_count));
 }
 
@@ -375,74 +352,13 @@ inline int64_t class_grid(const DMat &A) {
     return std::max<int64_t>(1, std::min<int64_t>(cdiv(A.nrows, kBlock), (int64_t)occ * g_sm_count));
 }
 
-// grid of the sliced-ELL kernels: every slot (default) or one resident wave
-// run grid-stride (DFL_SELL_WAVE=1)
-template <int MODE, bool DOT>
-inline int64_t sell_grid(const DMat &A) {
-    const int64_t nb = cdiv(A.nrows, kBlock);
-    if (!g_sell_wave) return nb;
-    static const int occ = occupancy(k_ell<MODE, DOT, 0>);
-    return std::max<int64_t>(1, std::min<int64_t>(nb, (int64_t)occ * g_sm_count));
-}
-
 // number of per-block / per-tile partials the POST-with-dot kernel on A produces
 inline int64_t parts_for(const DMat &A) {
-    if (A.fmt == FMT_PCODE || A.fmt == FMT_SCODE) return cdiv(A.nrows, kBlock);
+    if (A.fmt == FMT_PCODE) return cdiv(A.nrows, kBlock);
     if (A.fmt == FMT_CLASS) return class_grid<MODE_POST, true>(A);
-    if (A.fmt == FMT_CODE || A.vcode) return code_grid<MODE_POST, true>(A);
-    if (g_use_pipe && A.pipe.stages) return A.pipe.ntiles;
-    if (A.fmt == FMT_ELL && A.ell_w == 0) return sell_grid<MODE_POST, true>(A);
+    if (A.fmt == FMT_CODE) return code_grid<MODE_POST, true>(A);
     return nblocks_for(A);
 }
-
-inline size_t pipe_smem(const DMat &A) { return 128 + (size_t)A.pipe.stages * A.pipe.cap * 12; }
-
-template <int MODE, bool PART>
-static void pipe_attr_one() {
-    auto set = [](const void *f) {
-        cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kStageBytesMax + 1024);
-    };
-    set((const void *)k_pipe<0, MODE, PART>);
-    set((const void *)k_pipe<1, MODE, PART>);
-    set((const void *)k_pipe<2, MODE, PART>);
-    set((const void *)k_pipe<4, MODE, PART>);
-    set((const void *)k_pipe<8, MODE, PART>);
-    set((const void *)k_pipe<16, MODE, PART>);
-    set((const void *)k_pipe<32, MODE, PART>);
-}
-
-inline void pipe_attrs() {
-    pipe_attr_one<PMODE_PLAIN, false>();
-    pipe_attr_one<PMODE_RESID, false>();
-    pipe_attr_one<PMODE_PROLONG, false>();
-    pipe_attr_one<PMODE_POST, false>();
-    pipe_attr_one<PMODE_POST, true>();
-    pipe_attr_one<PMODE_OP, true>();
-    pipe_attr_one<PMODE_OPRES, true>();
-}
-
-template <int MODE, bool PART>
-static bool launch_pipe(dfl_ctx *ctx, const DMat &A, const SpArgs &a) {
-    if (A.pipe.stages == 0) return false;
-    const size_t smem = pipe_smem(A);
-    const int per_sm = smem <= 110 * 1024 ? 2 : 1;
-    const unsigned grid = (unsigned)std::min<int64_t>(A.pipe.ntiles, (int64_t)ctx->sm_count * per_sm);
-    if (A.fmt == FMT_ELL) {
-        k_pipe<0, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a);
-    } else {
-        switch (A.group) {
-            case 1: k_pipe<1, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
-            case 2: k_pipe<2, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
-            case 4: k_pipe<4, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
-            case 8: k_pipe<8, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
-            case 16: k_pipe<16, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
-            default: k_pipe<32, MODE, PART><<<grid, kPipeThreads, smem, ctx->st>>>(A, a); break;
-        }
-    }
-    ctx->launches++;
-    return true;
-}
-
 
 template <int MODE, bool DOT>
 static void launch_csr_mode(const DMat &A, const RowArgs &a, cudaStream_t st) {
@@ -465,11 +381,6 @@ static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
         ctx->launches++;
         return;
     }
-    if (A.fmt == FMT_SCODE) {
-        launch_k(ctx->st, k_scode<MODE, DOT>, (unsigned)cdiv(A.nrows, kBlock), kBlock, 0, A, a);
-        ctx->launches++;
-        return;
-    }
     if (A.fmt == FMT_CLASS) {
         launch_k(ctx->st, k_class<MODE, DOT>, (unsigned)class_grid<MODE, DOT>(A), kBlock, 0, A, a,
                  *ctx->class_tabs[A.class_id]);
@@ -477,32 +388,9 @@ static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
         return;
     }
     if (A.fmt == FMT_CODE) {
-        if (g_code_pipe)
-            launch_k(ctx->st, k_codep<MODE, DOT>, (unsigned)code_grid<MODE, DOT>(A), kBlock, 0, A, a);
-        else
-            launch_k(ctx->st, k_code<MODE, DOT>, (unsigned)code_grid<MODE, DOT>(A), kBlock, 0, A, a);
+        launch_k(ctx->st, k_codep<MODE, DOT>, (unsigned)code_grid<MODE, DOT>(A), kBlock, 0, A, a);
         ctx->launches++;
         return;
-    }
-    if (A.vcode) {
-        launch_k(ctx->st, k_vell<MODE, DOT>, (unsigned)code_grid<MODE, DOT>(A), kBlock, 0, A, a);
-        ctx->launches++;
-        return;
-    }
-    if (g_use_pipe) {
-        SpArgs s;
-        s.x = a.x;
-        s.w = a.w;
-        s.r = a.r;
-        s.xo = a.xo;
-        s.out = a.out;
-        s.part = a.dot_part;
-        s.st = a.st;
-        constexpr int PM = MODE == MODE_PLAIN ? PMODE_PLAIN
-                           : MODE == MODE_RESID ? PMODE_RESID
-                           : MODE == MODE_POST ? PMODE_POST
-                                                : PMODE_PROLONG;
-        if (launch_pipe<PM, DOT>(ctx, A, s)) return;
     }
     if (A.fmt == FMT_ELL) {
         const unsigned grid = (unsigned)nblocks_for(A);
@@ -513,7 +401,7 @@ static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
             case 6: launch_k(ctx->st, k_ell<MODE, DOT, 6>, grid, kBlock, 0, A, a); break;
             case 7: launch_k(ctx->st, k_ell<MODE, DOT, 7>, grid, kBlock, 0, A, a); break;
             case 8: launch_k(ctx->st, k_ell<MODE, DOT, 8>, grid, kBlock, 0, A, a); break;
-            default: launch_k(ctx->st, k_ell<MODE, DOT, 0>, (unsigned)sell_grid<MODE, DOT>(A), kBlock, 0, A, a); break;
+            default: launch_k(ctx->st, k_ell<MODE, DOT, 0>, grid, kBlock, 0, A, a); break;
         }
     } else
         launch_csr_mode<MODE, DOT>(A, a, ctx->st);
@@ -527,7 +415,7 @@ static void launch_op_nv(dfl_ctx *ctx, const OpArgs &a, unsigned grid) {
     if (A.fmt == FMT_CLASS) {
         static const int occ = occupancy(k_op_class<OPMODE, NV>);
         OpArgs b = a;
-        b.pf = g_op_pf ? (int64_t)occ * g_sm_count * kBlock : 0;
+        b.pf = (int64_t)occ * g_sm_count * kBlock;  // next-wave L2 prefetch distance
         launch_k(ctx->st, k_op_class<OPMODE, NV>, grid, kBlock, 0, A, ctx->tiles, S, b, *ctx->class_tabs[A.class_id]);
         return;
     }
@@ -546,19 +434,6 @@ static void launch_op_nv(dfl_ctx *ctx, const OpArgs &a, unsigned grid) {
 template <int OPMODE>
 static void launch_op(dfl_ctx *ctx, const OpArgs &a) {
     const DMat &A = ctx->Aop;
-    if (g_use_pipe && !a.skip_rows && !ctx->split) {
-        SpArgs s;
-        s.x = a.x;
-        s.b = a.b;
-        s.out = a.y;
-        s.part = a.k > 0 ? a.zt_part : nullptr;
-        s.zcols = a.zcols;
-        s.zn = a.n;
-        s.k = a.k;
-        s.st = a.st;
-        s.need_refresh = a.need_refresh;
-        if (launch_pipe<OPMODE == 0 ? PMODE_OP : PMODE_OPRES, true>(ctx, A, s)) return;
-    }
     const unsigned grid = (unsigned)ctx->ntiles;
     if (grid == 0) return;
     if (A.fmt == FMT_CODE || A.fmt == FMT_ELL || A.fmt == FMT_CLASS) {
@@ -629,42 +504,22 @@ static void launch_project(dfl_ctx *ctx, const ProjArgs &a) {
 
 
 // ctx_layout.cu
-extern double kShortRowPad;
 int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &bounds,
                   std::vector<int64_t> *bound_tiles = nullptr, bool allow_ell = true,
                   const double *colscale = nullptr, DMat *scaled = nullptr, bool allow_sell = true,
-                  bool allow_code = true, bool allow_vcode = false, bool allow_class = true);
+                  bool allow_code = true, bool allow_class = true);
 int build_groups(dfl_ctx *ctx);
 int build_tiles(dfl_ctx *ctx);
-// single-rank grid finish of the CG scalars (Fin); nullptr-tick Fin when off
-inline Fin make_fin(dfl_ctx *ctx, int act) {
-    Fin f{};
-    if (multi(ctx) || !ctx->fin_tick || g_no_fin || !((g_fin_mask >> act) & 1u)) return f;
-    f.tick = ctx->fin_tick;
-    f.gpart = ctx->fin_gpart;
-    f.st = ctx->state;
-    f.act = act;
-    return f;
-}
-// the operator kernel can finish Z'y -> t (-> t2) itself
-inline bool op_fusable(const dfl_ctx *ctx) {
-    return !multi(ctx) && !ctx->split && !g_use_pipe && ctx->subtab.n > 0 && ctx->fin_tick && !g_no_fin &&
-           (g_fin_mask & 16u) &&
-           (ctx->Aop.fmt == FMT_ELL || ctx->Aop.fmt == FMT_CODE || ctx->Aop.fmt == FMT_CLASS);
-}
 
 // ctx_comm.cu
 int comm_allgather(dfl_ctx *ctx, const double *send, double *recv, size_t count);
 int halo(dfl_ctx *ctx, double *v, cudaStream_t xs = nullptr);
-int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op, bool t_ready = false);
+int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op);
 int rank_scalar(dfl_ctx *ctx, const double *part, int64_t nparts, int slot, const double **gath);
 // ctx_cycle.cu
-int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *dot_part, int64_t *nparts,
-           const Fin *fin = nullptr, bool *fin_used = nullptr);
-// fin_zt != nullptr: finish Z'y -> t (-> t2) inside the operator kernel when
-// op_fusable(); *fin_zt tells whether it did (then zt_to_t2 is not needed)
+int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *dot_part, int64_t *nparts);
 int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double *b, bool zt, const KState *st,
-                 int need_refresh, bool *fin_zt = nullptr);
+                 int need_refresh);
 int project_dev(dfl_ctx *ctx, const double *v, double *out, const KState *st, int dotmode);
 int lift_dev(dfl_ctx *ctx, const dfl_solve_params *p);
 // ctx_cg.cu / ctx_krylov.cu

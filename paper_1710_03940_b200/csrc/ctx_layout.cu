@@ -3,9 +3,6 @@
 // phase, subdomain grouping of the V-cycle levels and row tiles of the operator.
 #include "ctx_impl.cuh"
 
-static int build_pipe(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &soff,
-                      const std::vector<int64_t> &bounds, std::vector<int64_t> *bound_tiles);
-
 // colscale != nullptr: also upload the column-scaled values a_ij * colscale_j
 // in the same layout (shares the index arrays) into *scaled.
 // FMT_CODE encoder: every row <= 8 entries and <= 255 distinct (column - row,
@@ -232,106 +229,6 @@ static int try_upload_pcode(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) 
     return DFL_OK;
 }
 
-// FMT_SCODE encoder (kernels.cuh): SELL-32 slots sorted by row length inside
-// windows of kSigmaS rows; ok = false leaves m untouched
-static constexpr int64_t kSigmaS = 1024;
-static int try_upload_scode(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) {
-    ok = false;
-    const int64_t n = h.nrows;
-    std::unordered_map<uint64_t, int> dict;
-    std::vector<double> tab;
-    auto rlen = [&](int64_t i) { return h.ptr[i + 1] - h.ptr[i]; };
-    for (int64_t i = 0; i < n; ++i)
-        for (int64_t k = h.ptr[i]; k < h.ptr[i + 1]; ++k) {
-            if (k > h.ptr[i]) {
-                const int64_t gap = h.col[k] - h.col[k - 1];
-                if (gap < 0 || gap > 65535) return DFL_OK;
-            }
-            uint64_t bits;
-            std::memcpy(&bits, &h.val[k], 8);
-            if (dict.find(bits) == dict.end()) {
-                if (dict.size() >= 255) return DFL_OK;
-                dict.emplace(bits, (int)tab.size());
-                tab.push_back(h.val[k]);
-            }
-        }
-    std::vector<int> perm(n);
-    for (int64_t w0 = 0; w0 < n; w0 += kSigmaS) {
-        const int64_t w1 = std::min(n, w0 + kSigmaS);
-        for (int64_t j = w0; j < w1; ++j) perm[j] = (int)j;
-        std::stable_sort(perm.begin() + w0, perm.begin() + w1, [&](int a, int b) { return rlen(a) > rlen(b); });
-    }
-    const int64_t nsl = cdiv(n, 32);
-    std::vector<int64_t> soff(nsl + 1, 0);
-    for (int64_t sl = 0; sl < nsl; ++sl) {
-        int64_t wmax = 0;
-        for (int64_t j = sl * 32; j < std::min(n, sl * 32 + 32); ++j) wmax = std::max(wmax, rlen(perm[j]));
-        soff[sl + 1] = soff[sl] + 32 * wmax;
-    }
-    std::vector<uint16_t> gap(soff[nsl], 0);
-    std::vector<uint8_t> code(soff[nsl], (uint8_t)kScPad);  // padding: skipped by the kernel
-    std::vector<int> c0(n, 0);
-    for (int64_t sl = 0; sl < nsl; ++sl)
-        for (int64_t j = sl * 32; j < std::min(n, sl * 32 + 32); ++j) {
-            const int64_t i = perm[j], b = h.ptr[i], e = h.ptr[i + 1];
-            if (e > b) c0[j] = (int)h.col[b];
-            for (int64_t k = b; k < e; ++k) {
-                const int64_t dst = soff[sl] + (k - b) * 32 + (j - sl * 32);
-                gap[dst] = (uint16_t)(k == b ? 0 : h.col[k] - h.col[k - 1]);
-                uint64_t bits;
-                std::memcpy(&bits, &h.val[k], 8);
-                code[dst] = (uint8_t)dict[bits];
-            }
-        }
-    int64_t *d_soff;
-    int *d_perm, *d_c0;
-    uint16_t *d_gap;
-    uint8_t *d_code;
-    double *d_tab;
-    RC(upload(ctx, &d_soff, soff.data(), nsl + 1));
-    RC(upload(ctx, &d_perm, perm.data(), std::max<int64_t>(1, n)));
-    RC(upload(ctx, &d_c0, c0.data(), std::max<int64_t>(1, n)));
-    RC(upload(ctx, &d_gap, gap.data(), std::max<int64_t>(1, soff[nsl])));
-    RC(upload(ctx, &d_code, code.data(), std::max<int64_t>(1, soff[nsl])));
-    RC(upload(ctx, &d_tab, tab.data(), std::max<int64_t>(1, (int64_t)tab.size())));
-    m.fmt = FMT_SCODE;
-    m.stored = soff[nsl];
-    m.slice_off = d_soff;
-    m.perm = d_perm;
-    m.pc_c0 = d_c0;
-    m.sc_gap = d_gap;
-    m.sc_code = d_code;
-    m.pc_tab = d_tab;
-    m.sc_ntab = (int)tab.size();
-    ok = true;
-    return DFL_OK;
-}
-
-// value codes for an ELL-layout matrix with <= 255 distinct values (bitwise)
-static int attach_value_codes(dfl_ctx *ctx, DMat &m, const std::vector<double> &val) {
-    std::unordered_map<uint64_t, int> dict;
-    std::vector<double> tab;
-    std::vector<uint8_t> code(val.size());
-    for (size_t e = 0; e < val.size(); ++e) {
-        uint64_t bits;
-        std::memcpy(&bits, &val[e], 8);
-        auto it = dict.find(bits);
-        if (it == dict.end()) {
-            if (dict.size() >= 255) return DFL_OK;  // not value-codable
-            it = dict.emplace(bits, (int)tab.size()).first;
-            tab.push_back(val[e]);
-        }
-        code[e] = (uint8_t)it->second;
-    }
-    uint8_t *d_code;
-    double *d_tab;
-    RC(upload(ctx, &d_code, code.data(), (int64_t)code.size()));
-    RC(upload(ctx, &d_tab, tab.data(), (int64_t)tab.size()));
-    m.vcode = d_code;
-    m.vtab = d_tab;
-    m.nvtab = (int)tab.size();
-    return DFL_OK;
-}
 
 static constexpr int64_t kSigma = 1024;  // SELL-C-sigma sorting window
 // SELL-32-1024 for long-row matrices with enough rows to hide the per-warp
@@ -339,12 +236,13 @@ static constexpr int64_t kSigma = 1024;  // SELL-C-sigma sorting window
 // short-row (P) and small coarse matrices stay CSR-vector
 static constexpr int64_t kSellMinRows = 100000;
 static constexpr double kSellMinMean = 12.0;
-static constexpr double kShortRowMean = 8.0;  // DFL_SHORT_PAD=x overrides the padding limit below
-double kShortRowPad = 1.7;
+static constexpr double kShortRowMean = 8.0;
+static constexpr double kShortRowPad = 1.7;     // short rows: padding is cheaper than CSR up to this
+static constexpr double kCsrPerLane = 12.0;     // CSR-vector: target entries per lane
 
 int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &bounds,
                   std::vector<int64_t> *bound_tiles, bool allow_ell, const double *colscale, DMat *scaled,
-                  bool allow_sell, bool allow_code, bool allow_vcode, bool allow_class) {
+                  bool allow_sell, bool allow_code, bool allow_class) {
     m = DMat{};
     m.nrows = h.nrows;
     m.ncols = h.ncols;
@@ -365,21 +263,15 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
         bool ok = false;
         RC(try_upload_code(ctx, h, m, ok));
         if (ok) {
-            if (colscale) *scaled = m;  // RESID on a coded matrix gathers w .* r instead (k_wr)
+            if (colscale) *scaled = m;  // RESID on a coded matrix gathers w .* r
             return DFL_OK;
         }
     }
     // delta/value-coded rows: only where no pre-scaled copy is needed (P, R)
-    if (g_use_pcode && !g_use_coarse && !g_use_tiny && allow_code && allow_ell && !colscale && h.nrows > 0) {
+    if (g_use_pcode && allow_code && allow_ell && !colscale && h.nrows > 0) {
         bool ok = false;
         RC(try_upload_pcode(ctx, h, m, ok));
         if (ok) return DFL_OK;
-        // long rows (the restriction): gap/value-coded SELL
-        const double meanr = h.nrows ? (double)m.nnz / (double)h.nrows : 0.0;
-        if (g_use_scode && h.nrows >= kSellMinRows && meanr >= kSellMinMean) {
-            RC(try_upload_scode(ctx, h, m, ok));
-            if (ok) return DFL_OK;
-        }
     }
     const int64_t nsl = cdiv(h.nrows, 32);
     auto rlen = [&](int64_t i) { return h.ptr[i + 1] - h.ptr[i]; };
@@ -403,7 +295,7 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
     const double mean = h.nrows ? (double)m.nnz / (double)h.nrows : 0.0;
     const double nnzd = (double)m.nnz + 64.0;
     bool ell = false;
-    const double upad = mean <= kShortRowMean ? kShortRowPad : 1.03;  // short rows: padding is cheaper than CSR
+    const double upad = mean <= kShortRowMean ? kShortRowPad : 1.03;
     if (allow_ell && maxlen <= 8 && (double)(nsl * 32 * maxlen) <= upad * nnzd) {
         // uniform slice width: the kernels compute slice offsets instead of loading them
         ell = true;
@@ -412,7 +304,7 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
     } else if (allow_ell && (double)soff[nsl] <= 1.03 * nnzd) {
         ell = true;
     } else if (allow_ell && allow_sell && maxlen <= 1024 &&
-               (g_allow_sell || (!g_no_sell && h.nrows >= kSellMinRows && mean >= kSellMinMean))) {
+               !g_no_sell && h.nrows >= kSellMinRows && mean >= kSellMinMean) {
         perm.resize(h.nrows);
         for (int64_t w0 = 0; w0 < h.nrows; w0 += kSigma) {
             const int64_t w1 = std::min(h.nrows, w0 + kSigma);
@@ -476,8 +368,6 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
             RC(upload(ctx, &d_perm, perm.data(), h.nrows));
             m.perm = d_perm;
         }
-        if (g_use_vcode && allow_vcode) RC(attach_value_codes(ctx, m, val));
-        if (perm.empty()) RC(build_pipe(ctx, h, m, soff, bounds, bound_tiles));
         if (colscale) {
             double *d_sval;
             RC(upload(ctx, &d_sval, sval.data(), m.stored));
@@ -487,15 +377,12 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
     } else {
         m.fmt = FMT_CSR;
         m.stored = m.nnz;
-        // DFL_KEEP_MB: CSR matrices up to this size load with an L2 evict-last policy (0: off)
-        m.keep = (double)m.nnz * 12.0 <= (double)g_keep_mb * 1048576.0 ? 1 : 0;
-        // lanes per row: about 6 entries per lane, batched kCsrUnroll deep
+        // lanes per row: about kCsrPerLane entries per lane, batched kCsrUnroll deep
         int g = 1;
-        const int want = (int)std::ceil(mean / (h.nrows < 50000 ? g_small_per_lane : g_csr_per_lane));
+        const int want = (int)std::ceil(mean / kCsrPerLane);
         while (g < want && g < 32) g *= 2;
-        if (g_csr_g > 0) g = g_csr_g;
         m.group = g;
-        // padded by 4 entries so that 16-byte aligned bulk copies may overrun the last row
+        // padded by 4 entries (aligned vector loads may overrun the last row)
         std::vector<int> ptr(h.nrows + 1), col(m.nnz + 4, 0);
         std::vector<double> val(m.nnz + 4, 0.0);
         for (int64_t i = 0; i <= h.nrows; ++i) ptr[i] = (int)(h.ptr[i] - h.ptr[0]);
@@ -509,7 +396,6 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
         m.ptr = d_ptr;
         m.col = d_col;
         m.val = d_val;
-        RC(build_pipe(ctx, h, m, soff, bounds, bound_tiles));
         if (colscale) {
             std::vector<double> sval(m.nnz + 4, 0.0);
             for (int64_t k = 0; k < m.nnz; ++k) sval[k] = h.val[h.ptr[0] + k] * colscale[h.col[h.ptr[0] + k]];
@@ -521,68 +407,6 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
     }
     return DFL_OK;
 }
-
-// Row tiles for the TMA pipeline: tiles never straddle `bounds` (subdomain
-// starts for the operator); ELL tiles are 256 rows (one per thread), CSR
-// tiles ~3K entries in passes of 256/G rows.
-
-static int build_pipe(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &soff,
-                      const std::vector<int64_t> &bounds, std::vector<int64_t> *bound_tiles) {
-    m.pipe = Pipe{};
-    if (bound_tiles) bound_tiles->assign(1, 0);
-    if (h.nrows == 0) return DFL_OK;
-    int64_t rpt;
-    if (m.fmt == FMT_ELL) {
-        rpt = kPipeThreads;
-    } else {
-        const int64_t rpp = kPipeThreads / m.group;
-        const double mean = (double)m.nnz / (double)h.nrows;
-        const int64_t passes = std::max<int64_t>(1, (int64_t)std::llround(3072.0 / std::max(1.0, mean * rpp)));
-        rpt = rpp * passes;
-    }
-    std::vector<int64_t> r0, r1, e0;
-    std::vector<int> ec;
-    int64_t cap = 0;
-    const int64_t base = h.ptr[0];
-    for (size_t bi = 0; bi + 1 < bounds.size(); ++bi) {
-        for (int64_t r = bounds[bi]; r < bounds[bi + 1]; r += rpt) {
-            const int64_t re = std::min(r + rpt, bounds[bi + 1]);
-            int64_t a, b;
-            if (m.fmt == FMT_ELL) {
-                a = soff[r >> 5];
-                b = soff[(re + 31) >> 5];
-            } else {
-                a = (h.ptr[r] - base) & ~int64_t(3);
-                b = ((h.ptr[re] - base) + 3) & ~int64_t(3);
-            }
-            r0.push_back(r);
-            r1.push_back(re);
-            e0.push_back(a);
-            ec.push_back((int)(b - a));
-            cap = std::max(cap, b - a);
-        }
-        if (bound_tiles) bound_tiles->push_back((int64_t)r0.size());
-    }
-    cap = (cap + 3) & ~int64_t(3);
-    const int64_t stage_bytes = cap * 12;
-    int stages = (int)std::min<int64_t>(4, kStageBytesMax / std::max<int64_t>(1, stage_bytes));
-    if (stages < 2) return DFL_OK;  // rows too long for staging: register kernels
-    int64_t *d0, *d1, *de;
-    int *dc;
-    RC(upload(ctx, &d0, r0.data(), (int64_t)r0.size()));
-    RC(upload(ctx, &d1, r1.data(), (int64_t)r1.size()));
-    RC(upload(ctx, &de, e0.data(), (int64_t)e0.size()));
-    RC(upload(ctx, &dc, ec.data(), (int64_t)ec.size()));
-    m.pipe.row0 = d0;
-    m.pipe.row1 = d1;
-    m.pipe.e0 = de;
-    m.pipe.ecnt = dc;
-    m.pipe.ntiles = (int64_t)r0.size();
-    m.pipe.cap = (int)cap;
-    m.pipe.stages = stages;
-    return DFL_OK;
-}
-
 
 // ---------------------------------------------------------------------------
 // upload helpers for finalize
@@ -663,20 +487,18 @@ int build_groups(dfl_ctx *ctx) {
                     th.emplace_back([&, l, which] {
                         cudaSetDevice(ctx->device);
                         DLevel &v = vs[l];
-                        // tiny levels stay CSR: they run inside the k_tiny_cycle cluster kernel
-                        const bool tiny = g_use_tiny && fol[l].back() <= kTinyRows;
                         int &rc = rcs[3 * l + which];
                         if (which == 0) Am[l] = merge_blocks(As[l], fol[l]);
                         else if (which == 1) Pm[l] = merge_blocks(Ps[l], col[l]);
                         else Rm[l] = merge_blocks(Rs[l], fol[l]);
                         if (which == 0)
-                            rc = upload_matrix(ctx, Am[l].view(), v.A, {0, Am[l].nrows}, nullptr, !tiny, wl[l].data(),
-                                               &v.Aw, true, true, false, !g_use_coarse);
+                            rc = upload_matrix(ctx, Am[l].view(), v.A, {0, Am[l].nrows}, nullptr, true, wl[l].data(),
+                                               &v.Aw, true, true, true);
                         else if (which == 1)
-                            rc = upload_matrix(ctx, Pm[l].view(), v.P, {0, Pm[l].nrows}, nullptr, !tiny, nullptr,
+                            rc = upload_matrix(ctx, Pm[l].view(), v.P, {0, Pm[l].nrows}, nullptr, true, nullptr,
                                                nullptr, true, true, true);
                         else
-                            rc = upload_matrix(ctx, Rm[l].view(), v.R, {0, Rm[l].nrows}, nullptr, !tiny, nullptr,
+                            rc = upload_matrix(ctx, Rm[l].view(), v.R, {0, Rm[l].nrows}, nullptr, true, nullptr,
                                                nullptr, true, true, true);
                     });
             for (auto &t : th) t.join();
@@ -684,7 +506,6 @@ int build_groups(dfl_ctx *ctx) {
         for (int rc : rcs) RC(rc);
         for (int l = 0; l < L; ++l) {
             DLevel &v = vs[l];
-            if (v.A.fmt == FMT_CODE && g_wr_split) RC(dalloc(ctx, &v.wr, Am[l].nrows));
             RC(upload(ctx, &v.w, wl[l].data(), (int64_t)wl[l].size()));
             v.n = fol[l].back();
             v.nc = col[l].back();
@@ -718,69 +539,6 @@ int build_groups(dfl_ctx *ctx) {
         if (L > 0) {
             RC(dalloc(ctx, &g.rb, g.nb));
             RC(dalloc(ctx, &g.xb, g.nb));
-        }
-        {
-            // row-major inverses and the argument block of the cooperative kernel
-            std::vector<double> binv;
-            for (int j = s; j < e; ++j) {
-                const auto &bi = ctx->pending[j]->levels.back().bottom_inv;
-                binv.insert(binv.end(), bi.begin(), bi.end());
-            }
-            RC(upload(ctx, &g.binv, binv.data(), (int64_t)binv.size()));
-            int lc = L;
-            for (int l = 0; l < L; ++l)
-                if (g.rows[l] <= kCoarseRows) {
-                    lc = l;
-                    break;
-                }
-            if (L - lc <= kMaxCoarse) {
-                CoarseArgs ca{};
-                ca.nlev = L - lc;
-                for (int l = lc; l < L; ++l) {
-                    const DLevel &v = g.lv[l];
-                    CLevel &cl = ca.lv[l - lc];
-                    cl.A = v.A;
-                    cl.Aw = v.Aw;
-                    cl.P = v.P;
-                    cl.R = v.R;
-                    cl.w = v.w;
-                    cl.rv = v.rv;
-                    cl.t = v.t;
-                    cl.xv = v.xv;
-                }
-                ca.binv = g.binv;
-                ca.binv_off = g.binv_off;
-                ca.b_off = g.b_off;
-                ca.nsub = g.nsub;
-                ca.nb = g.nb;
-                ca.rb = g.rb;
-                ca.xb = g.xb;
-                RC(upload(ctx, &g.cargs, &ca, 1));
-                // tiny tail: levels of <= kTinyRows rows + bottom (all CSR)
-                int lt = L;
-                for (int l = 0; l < L; ++l)
-                    if (g.rows[l] <= kTinyRows) {
-                        lt = l;
-                        break;
-                    }
-                if (g_use_tiny && g.nb <= kTinyRows && L - lt <= kMaxCoarse) {
-                    CoarseArgs ta = ca;
-                    ta.nlev = L - lt;
-                    for (int l = lt; l < L; ++l) ta.lv[l - lt] = ca.lv[l - lc];
-                    bool csr = true;
-                    for (int l = 0; l < ta.nlev; ++l)
-                        csr = csr && ta.lv[l].Aw.fmt == FMT_CSR && ta.lv[l].A.fmt == FMT_CSR &&
-                              ta.lv[l].P.fmt == FMT_CSR && ta.lv[l].R.fmt == FMT_CSR;
-                    if (csr && lt >= lc) {
-                        RC(upload(ctx, &g.targs, &ta, 1));
-                        g.lt = lt;
-                    }
-                }
-                int bps = 0;
-                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, k_coarse_cycle, 256, 0));
-                g.coarse_grid = (unsigned)(std::max(1, std::min(bps, 2)) * ctx->sm_count);
-                g.lc = bps > 0 ? lc : -1;
-            }
         }
         if (g.max_nb > (1 << 20)) {
             ctx->err = "bottom level too large for shared-memory staging";
@@ -816,12 +574,9 @@ int build_tiles(dfl_ctx *ctx) {
     if (ctx->nsub <= kSubTab) {
         ctx->subtab.n = ctx->nsub;
         ctx->subtab.rows_per_tile = rpt;
-        int64_t gacc = 0;
         for (int s = 0; s <= ctx->nsub; ++s) {
             ctx->subtab.sub_off[s] = ctx->sub_off[s];
             ctx->subtab.tile_start[s] = subt[s];
-            ctx->subtab.group_start[s] = gacc;
-            if (s < ctx->nsub) gacc += cdiv(subt[s + 1] - subt[s], kFinGroup);
         }
     }
     return DFL_OK;

@@ -485,10 +485,6 @@ int basis_az(const dfl_csr *A, int k, const double *zext, const int32_t *owner,
 // ---------------------------------------------------------------------------
 // C ABI
 
-struct dfl_matrix {
-    dfl::Csr m;
-};
-
 extern "C" {
 
 int dfl_abi_version(void) { return DFLB200_ABI_VERSION; }

@@ -58,3 +58,8 @@ struct dfl_hier {
     std::shared_ptr<dfl::Hierarchy> sp = std::make_shared<dfl::Hierarchy>();
     dfl::Hierarchy &h = *sp;
 };
+
+// the opaque host CSR handle of the C ABI (dfl_matrix_shape / _copy / _free)
+struct dfl_matrix {
+    dfl::Csr m;
+};

@@ -31,16 +31,7 @@ constexpr int kEllUnroll = 8;     // slice widths up to this are fully unrolled
 #define DFL_ELL_BATCH 8
 #endif
 
-enum { FMT_ELL = 0, FMT_CSR = 1, FMT_CODE = 2, FMT_CLASS = 3, FMT_PCODE = 4, FMT_SCODE = 5 };
-
-// FMT_SCODE ("gap/value-coded SELL"): long-row matrices with <= 255 distinct
-// values whose consecutive columns in a row differ by < 65536 -- the
-// restriction R = P^T of a structured problem (150^3: 9 values, 28 entries
-// per row, gaps <= 22.5K).  SELL-32 slices (rows sorted by length inside 1024-row
-// windows, slot -> row permutation); per slot the first column (int32); per
-// entry a 16-bit column gap and an 8-bit value code, column-major inside the
-// slice.  3 bytes per entry instead of 12; the running column is summed
-// along the row; CSR order, no FMA: bit-identical.
+enum { FMT_ELL = 0, FMT_CSR = 1, FMT_CODE = 2, FMT_CLASS = 3, FMT_PCODE = 4 };
 
 // FMT_PCODE ("delta/value-coded rows"): matrices with <= 7 entries per row,
 // column-sorted rows whose columns lie within 65535 of the row's first one and
@@ -80,25 +71,10 @@ struct ClassTab {
 // operator has 7 -- and 8 bytes per row instead of 12 per entry.
 constexpr unsigned kCodePad = 255u;
 
-// row tiles of one matrix for the TMA-pipelined kernels (spmv_pipe.cuh):
-// rows [row0, row1), entries [e0, e0 + ecnt) of the value / index arrays
-// (aligned to 4 entries = 16 B for the bulk-copy engine)
-struct Pipe {
-    const int64_t *row0 = nullptr;
-    const int64_t *row1 = nullptr;
-    const int64_t *e0 = nullptr;
-    const int *ecnt = nullptr;
-    int64_t ntiles = 0;
-    int cap = 0;     // max entries of a tile (stage capacity)
-    int stages = 0;  // 0: pipeline unavailable for this matrix
-};
-
 struct DMat {
-    Pipe pipe;
     int fmt = FMT_ELL;
     int ell_w = 0;            // > 0: every slice has this width (no slice_off lookup)
     int group = 1;            // CSR-vector lanes per row
-    int keep = 0;             // CSR small enough to stay L2-resident across cycles: loads with an evict-last policy
     int64_t nrows = 0, ncols = 0, nnz = 0, stored = 0;
     const int64_t *slice_off = nullptr;  // ELL: nslices + 1 element offsets
     const int *ptr = nullptr;            // CSR row pointer
@@ -111,10 +87,6 @@ struct DMat {
     // FMT_CLASS
     const uint8_t *cls = nullptr;        // class of every row
     int class_id = -1;                   // index of the ClassTab in the context
-    // FMT_SCODE (with slice_off, perm, pc_c0 per slot, pc_tab[<=256])
-    const uint16_t *sc_gap = nullptr;
-    const uint8_t *sc_code = nullptr;
-    int sc_ntab = 0;
     // FMT_PCODE
     const int *pc_c0 = nullptr;          // first column of every row
     const uint32_t *pc_d = nullptr;      // 3 x nrows: 16-bit deltas of entries 1..6 (SoA)
@@ -123,11 +95,6 @@ struct DMat {
     const int *ctab_delta = nullptr;     // column - row of each code
     const double *ctab_val = nullptr;    // value of each code
     int ncodes = 0;
-    // value-coded ELL ("VELL"): 1-byte value codes in the layout of val, the
-    // distinct values in vtab (<= 255); index arrays unchanged
-    const uint8_t *vcode = nullptr;
-    const double *vtab = nullptr;
-    int nvtab = 0;
 };
 
 // run-time state of one Krylov solve (device resident)
@@ -143,17 +110,9 @@ struct KState {
 // depends on (griddepcontrol.wait: full completion and memory flush of the
 // previous kernel in the stream; a no-op when launched without the PDL
 // attribute), so the launch of a kernel overlaps the drain of the one before
-// it.  With DFL_PDL_TRIGGER=1 kernels also signal launch_dependents at entry
-// (the next grid becomes resident during this one's last wave) -- measured
-// slower for the V-cycle (profiles/r01/README.md), so off by default.
-#ifndef DFL_PDL_TRIGGER
-#define DFL_PDL_TRIGGER 0  // early trigger measured: V-cycle graph 345 vs 324 us
-#endif
-#if DFL_PDL_TRIGGER
-#define DFL_PDL_ENTRY asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory")
-#else
+// it.  (An early launch_dependents trigger was measured slower for the
+// V-cycle: 345 vs 324 us per graph, profiles/r01/README.md.)
 #define DFL_PDL_ENTRY asm volatile("griddepcontrol.wait;" ::: "memory")
-#endif
 
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
@@ -161,27 +120,7 @@ __device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(
 
 template <class T>
 __device__ __forceinline__ T ld_stream(const T *p) { return __ldcs(p); }
-// evict-last loads for the coarse-level matrices (they fit in L2 next to the
-// gathered vectors while the fine-level streams pass through evict-first)
-__device__ __forceinline__ uint64_t l2_keep_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-__device__ __forceinline__ int ld_keep(const int *p, uint64_t pol) {
-    int v;
-    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ double ld_keep(const double *p, uint64_t pol) {
-    double v;
-    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
-    return v;
-}
 __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
-#ifndef DFL_SLICE_PREFETCH
-#define DFL_SLICE_PREFETCH 0  // measured slower (L0 restriction 43.4 -> 46.0 us)
-#endif
 
 // ---------------------------------------------------------------------------
 // gather functors: the value an entry multiplies
@@ -329,10 +268,7 @@ __device__ __forceinline__ double ell_slice_w(const DMat &A, int64_t off, const 
     return acc;
 }
 
-#ifndef DFL_SLICE_CHUNK
-#define DFL_SLICE_CHUNK 4
-#endif
-constexpr int kChunk = DFL_SLICE_CHUNK;
+constexpr int kChunk = 4;  // entries of a sliced row whose loads are batched
 
 // chunk of w <= kChunk entries of a sliced row, accumulated into acc in order
 template <class G>
@@ -352,10 +288,6 @@ __device__ __forceinline__ double ell_chunk(const DMat &A, int64_t o, int w, dou
     return acc;
 }
 
-#ifndef DFL_SLICE_PIPE
-#define DFL_SLICE_PIPE 0  // register double buffer: measured neutral (profiles/r01/README.md)
-#endif
-
 template <class G>
 __device__ __forceinline__ double ell_row_sliced(const DMat &A, int64_t row, const G &g) {
     const int64_t s = row >> 5;
@@ -363,61 +295,10 @@ __device__ __forceinline__ double ell_row_sliced(const DMat &A, int64_t row, con
     const int width = (int)((__ldg(A.slice_off + s + 1) - off) >> 5);
     const int64_t o = off + (row & 31);
     double acc = 0.0;
-#if DFL_SLICE_PIPE
-    // register double buffer: chunk k+1's column / value loads are in flight
-    // while chunk k's gathers run, so DRAM sees this row's stream continuously
-    // (same sequential summation order as below: bit-identical)
-    int c[kChunk];
-    double v[kChunk];
-#pragma unroll
-    for (int k = 0; k < kChunk; ++k)
-        if (k < width) {
-            c[k] = ld_stream(A.col + o + 32 * k);
-            v[k] = ld_stream(A.val + o + 32 * k);
-        }
     for (int k0 = 0; k0 < width; k0 += kChunk) {
-        const int k1 = k0 + kChunk;
-        int cn[kChunk];
-        double vn[kChunk];
-#pragma unroll
-        for (int k = 0; k < kChunk; ++k)
-            if (k1 + k < width) {
-                cn[k] = ld_stream(A.col + o + 32 * (k1 + k));
-                vn[k] = ld_stream(A.val + o + 32 * (k1 + k));
-            }
-        double xv[kChunk];
-#pragma unroll
-        for (int k = 0; k < kChunk; ++k)
-            if (k0 + k < width) xv[k] = g(c[k]);
-#pragma unroll
-        for (int k = 0; k < kChunk; ++k)
-            if (k0 + k < width) acc = add_rn(acc, mul_rn(v[k], xv[k]));
-#pragma unroll
-        for (int k = 0; k < kChunk; ++k) {
-            c[k] = cn[k];
-            v[k] = vn[k];
-        }
-    }
-    return acc;
-#else
-    for (int k0 = 0; k0 < width; k0 += kChunk) {
-#if DFL_SLICE_PREFETCH
-        // long rows: pull the next chunk of the matrix stream into L2 while this
-        // one's gathers run, so the next chunk's loads are L2 hits
-        if (k0 + kChunk < width) {
-            const int nk = min(kChunk, width - k0 - kChunk);
-#pragma unroll
-            for (int k = 0; k < kChunk; ++k)
-                if (k < nk) {
-                    prefetch_l2(A.col + o + 32 * (k0 + kChunk + k));
-                    prefetch_l2(A.val + o + 32 * (k0 + kChunk + k));
-                }
-        }
-#endif
         acc = ell_chunk(A, o + 32 * k0, min(kChunk, width - k0), acc, g);
     }
     return acc;
-#endif
 }
 
 template <int W, class G>
@@ -446,20 +327,14 @@ __device__ __forceinline__ double csr_row(const DMat &A, int64_t row, int sub, c
     double acc = 0.0;
     if (row < A.nrows) {
         const int b = __ldg(A.ptr + row), e = __ldg(A.ptr + row + 1);
-        const uint64_t pol = A.keep ? l2_keep_policy() : 0;
         for (int k0 = b + sub; k0 < e; k0 += kCsrUnroll * G) {
             int c[kCsrUnroll];
             double v[kCsrUnroll], xv[kCsrUnroll];
 #pragma unroll
             for (int u = 0; u < kCsrUnroll; ++u)
                 if (k0 + u * G < e) {
-                    if (A.keep) {
-                        c[u] = ld_keep(A.col + k0 + u * G, pol);
-                        v[u] = ld_keep(A.val + k0 + u * G, pol);
-                    } else {
-                        c[u] = ld_stream(A.col + k0 + u * G);
-                        v[u] = ld_stream(A.val + k0 + u * G);
-                    }
+                    c[u] = ld_stream(A.col + k0 + u * G);
+                    v[u] = ld_stream(A.val + k0 + u * G);
                 }
 #pragma unroll
             for (int u = 0; u < kCsrUnroll; ++u)
@@ -539,87 +414,6 @@ __device__ __forceinline__ double block_sum_t(double (&v)[NV], double *smem /* 3
 
 __device__ __forceinline__ bool skip(const KState *st) { return st != nullptr && st->done; }
 
-// ---------------------------------------------------------------------------
-// Grid finish (single rank): the scalar step that consumes a reduction runs in
-// the last block of the kernel that produced the partials, instead of in a
-// separate single-block launch.  Blocks are grouped in runs of kFinGroup; the
-// last block of a group (atomic ticket) sums the group's partials in index
-// order, the last group sums the group sums in index order -- the result does
-// not depend on which block finishes last (deterministic).
-// tick[0] counts finished groups, tick[1 + g] the blocks of group g; every
-// counter is reset by the block that completes it, so they are zero between
-// launches.
-constexpr int kFinGroup = 64;
-enum { ACT_NONE = 0, ACT_PQ = 1, ACT_RR = 2, ACT_RZ = 3 };
-
-struct Fin {
-    unsigned *tick = nullptr;  // nullptr: plain partials, no finish
-    double *gpart = nullptr;   // one sum per group (x NV)
-    KState *st = nullptr;
-    int act = ACT_NONE;
-    int use_if = 0;            // ACT_PQ: set the refresh IF condition
-    cudaGraphConditionalHandle hif = 0;
-};
-
-// Release / acquire at GPU scope.  The block's partial stores are ordered
-// before thread 0's release by the barrier in front of it (cumulativity), so
-// one thread fences per block, with acq_rel rather than the sequentially
-// consistent fence of __threadfence().
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
-
-// Block b of group g (blocks [gb0, gb0 + gs)) hands in its NV values (thread
-// j < NV holds value j).  Returns true, in every thread of the one block that
-// completes the last group; the group sums are then in gpart[0 .. ng*NV).
-template <int NV>
-__device__ __forceinline__ bool fin_arrive(unsigned *tick, double *part, double *gpart, int64_t b, double v,
-                                           unsigned g, int64_t gb0, unsigned gs, unsigned ng) {
-    __shared__ int s_last;
-    if ((int)threadIdx.x < NV) part[b * NV + threadIdx.x] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        fence_acq_rel_gpu();
-        const bool last = atomicAdd(tick + 1 + g, 1u) == gs - 1;
-        if (last) fence_acq_rel_gpu();
-        s_last = last;
-    }
-    __syncthreads();
-    if (!s_last) return false;
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            double a = lane < (int)gs ? __ldcg(part + (gb0 + lane) * NV + j) : 0.0;
-            if (lane + 32 < (int)gs) a += __ldcg(part + (gb0 + lane + 32) * NV + j);
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-            if (lane == 0) gpart[(int64_t)g * NV + j] = a;
-        }
-        if (lane == 0) {
-            tick[1 + g] = 0u;
-            fence_acq_rel_gpu();
-            const bool last = atomicAdd(tick, 1u) == ng - 1;
-            if (last) {
-                tick[0] = 0u;
-                fence_acq_rel_gpu();
-            }
-            s_last = last;
-        }
-    }
-    __syncthreads();
-    return s_last != 0;
-}
-
-// sum of group sums [g0, g1) of value j, fixed order; valid in lane 0 of warp 0
-template <int NV>
-__device__ __forceinline__ double fin_total(const double *gpart, int64_t g0, int64_t g1, int j) {
-    const int lane = threadIdx.x & 31;
-    double a = 0.0;
-    for (int64_t q = g0 + lane; q < g1; q += 32) a += __ldcg(gpart + q * NV + j);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o);
-    return a;
-}
-
 // the CG scalar steps of krylov.py:119-143 (also used by the single-block
 // kernels of ctx_cg.cu, which call them with the reduced value)
 __device__ __forceinline__ void cg_step_pq(KState *st, double pq) {  // iters += 1; alpha
@@ -651,35 +445,10 @@ __device__ __forceinline__ void cg_step_rz(KState *st, double rz) {  // beta
     st->rz = rz;
 }
 
-__device__ __forceinline__ void fin_action(const Fin &f, double tot) {
-    KState *st = f.st;
-    if (st->done) return;  // as the single-block kernels: nothing after the loop ended
-    if (f.act == ACT_PQ) {
-        cg_step_pq(st, tot);
-        if (f.use_if) cudaGraphSetConditional(f.hif, (!st->done && st->refresh_now) ? 1u : 0u);
-    } else if (f.act == ACT_RR) {
-        cg_step_rr(st, tot);
-    } else if (f.act == ACT_RZ) {
-        cg_step_rz(st, tot);
-    }
-}
-
 // end of a row / vector kernel with one dot partial per block (block_sum<1>
-// result in thread 0's v): plain partial, or partial + grid finish
-__device__ __forceinline__ void dot_out(const Fin &f, double *part, double v) {
-    if (!f.tick) {
-        if (threadIdx.x == 0) part[blockIdx.x] = v;
-        return;
-    }
-    const unsigned g = blockIdx.x / kFinGroup;
-    const unsigned ng = (gridDim.x + kFinGroup - 1) / kFinGroup;
-    const unsigned gs = min((unsigned)kFinGroup, gridDim.x - g * kFinGroup);
-    if (fin_arrive<1>(f.tick, part, f.gpart, blockIdx.x, v, g, (int64_t)g * kFinGroup, gs, ng)) {
-        if (threadIdx.x < 32) {
-            const double tot = fin_total<1>(f.gpart, 0, ng, 0);
-            if (threadIdx.x == 0) fin_action(f, tot);
-        }
-    }
+// result in thread 0's v)
+__device__ __forceinline__ void dot_out(double *part, double v) {
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -698,7 +467,6 @@ struct RowArgs {
     double *out;
     double *dot_part;  // POST: per-block r.out partials (nullptr: none)
     const KState *st;
-    Fin fin{};         // POST with dot: grid finish (single rank)
 };
 
 template <int MODE>
@@ -748,101 +516,9 @@ __global__ void __launch_bounds__(kBlock, W == 0 ? DFL_ELL_MINB0 : DFL_ELL_MINB)
         __shared__ double sm[32];
         double v[1] = {dot};
         block_sum<1>(v, sm);
-        dot_out(a.fin, a.dot_part, v[0]);
+        dot_out(a.dot_part, v[0]);
     }
 }
-
-// value-coded ELL row: value of entry e is vt[vcode[e]]
-template <class G>
-__device__ __forceinline__ double vell_row(const DMat &A, int64_t slot, int W, const G &g, const double *vt) {
-    const int64_t s = slot >> 5;
-    int64_t off;
-    int width;
-    if (A.ell_w > 0) {
-        width = A.ell_w;
-        off = s * 32 * (int64_t)width;
-    } else {
-        off = __ldg(A.slice_off + s);
-        width = (int)((__ldg(A.slice_off + s + 1) - off) >> 5);
-    }
-    off += slot & 31;
-    double acc = 0.0;
-    for (int k0 = 0; k0 < width; k0 += 8) {
-        int c[8];
-        unsigned v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (k0 + k < width) {
-                c[k] = ld_stream(A.col + off + 32 * (k0 + k));
-                v[k] = ld_stream(A.vcode + off + 32 * (k0 + k));
-            }
-        double xv[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (k0 + k < width) xv[k] = g(c[k]);
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-            if (k0 + k < width) acc = add_rn(acc, mul_rn(vt[v[k]], xv[k]));
-    }
-    return acc;
-}
-
-// value-coded ELL row kernel: grid-stride, value table staged once per block
-template <int MODE, bool DOT>
-__global__ void __launch_bounds__(kBlock) k_vell(DMat A, RowArgs a) {
-    DFL_PDL_ENTRY;
-    __shared__ double vt[256];
-    for (int t = threadIdx.x; t < A.nvtab; t += blockDim.x) vt[t] = A.vtab[t];
-    __syncthreads();
-    double dot = 0.0;
-    for (int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x; j < A.nrows; j += (int64_t)gridDim.x * kBlock) {
-        const int64_t i = A.perm ? (int64_t)__ldg(A.perm + j) : j;
-        const double ax = vell_row(A, j, 0, GatherX{MODE == MODE_RESID ? a.r : a.x}, vt);
-        const double y = epilogue<MODE>(a, i, ax);
-        a.out[i] = y;
-        if (DOT) dot += __ldg(a.r + i) * y;
-    }
-    if (DOT) {
-        __shared__ double sm[32];
-        double v[1] = {dot};
-        block_sum<1>(v, sm);
-        dot_out(a.fin, a.dot_part, v[0]);
-    }
-}
-
-// FMT_CODE row kernel, grid-stride (the code table is staged once per block;
-// the next rows' codes are requested before the table load completes).
-// MODE_RESID: t = r - A (w .* r) with the products w_j * r_j rounded at the
-// gather (a.x == nullptr) or read from a.x = w .* r (k_wr, DFL_WR_SPLIT=1);
-// either way the reference's arithmetic exactly.  DOT: one partial per block.
-template <int MODE, bool DOT>
-__global__ void __launch_bounds__(kBlock) k_code(DMat A, RowArgs a) {
-    DFL_PDL_ENTRY;
-    __shared__ int sd[256];
-    __shared__ double sv[256];
-    const int64_t stride = (int64_t)gridDim.x * kBlock;
-    int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    uint2 cw = i < A.nrows ? __ldcs(A.codes + i) : make_uint2(~0u, ~0u);
-    load_codes(A, sd, sv);
-    double dot = 0.0;
-    for (; i < A.nrows; i += stride) {
-        const int64_t inext = i + stride;
-        const uint2 cn = inext < A.nrows ? __ldcs(A.codes + inext) : make_uint2(~0u, ~0u);
-        const double ax = (MODE == MODE_RESID && a.x == nullptr) ? code_row_w(cw, i, GatherWR{a.w, a.r}, sd, sv)
-                                                                 : code_row_w(cw, i, GatherX{a.x}, sd, sv);
-        const double y = epilogue<MODE>(a, i, ax);
-        a.out[i] = y;
-        if (DOT) dot += __ldg(a.r + i) * y;
-        cw = cn;
-    }
-    if (DOT) {
-        __shared__ double sm[32];
-        double v[1] = {dot};
-        block_sum<1>(v, sm);
-        dot_out(a.fin, a.dot_part, v[0]);
-    }
-}
-
 
 // FMT_CODE row kernel, software-pipelined: the codes and the own-row operands
 // of the next row are loaded one iteration ahead, and the leading edge of its
@@ -908,7 +584,7 @@ __global__ void __launch_bounds__(kBlock) k_codep(DMat A, RowArgs a) {
         __shared__ double sm[32];
         double v[1] = {dot};
         block_sum<1>(v, sm);
-        dot_out(a.fin, a.dot_part, v[0]);
+        dot_out(a.dot_part, v[0]);
     }
 }
 
@@ -1003,7 +679,7 @@ __global__ void __launch_bounds__(kBlock, MODE == MODE_RESID ? DFL_CLASS_RESID_M
         __shared__ double sm[32];
         double v[1] = {dot};
         block_sum<1>(v, sm);
-        dot_out(a.fin, a.dot_part, v[0]);
+        dot_out(a.dot_part, v[0]);
     }
 }
 
@@ -1049,78 +725,8 @@ __global__ void __launch_bounds__(kBlock) k_pcode(DMat A, RowArgs a) {
         __shared__ double sm[32];
         double v[1] = {dot};
         block_sum<1>(v, sm);
-        dot_out(a.fin, a.dot_part, v[0]);
+        dot_out(a.dot_part, v[0]);
     }
-}
-
-constexpr unsigned kScPad = 255u;  // value code of the slice padding (skipped)
-#ifndef DFL_SC_CHUNK
-#define DFL_SC_CHUNK 8
-#endif
-#ifndef DFL_SC_MINB
-#define DFL_SC_MINB 6
-#endif
-
-// FMT_SCODE row kernel: one thread per slot
-template <int MODE, bool DOT>
-__global__ void __launch_bounds__(kBlock, DFL_SC_MINB) k_scode(DMat A, RowArgs a) {
-    DFL_PDL_ENTRY;
-    __shared__ double tab[256];
-    const int64_t j = (int64_t)blockIdx.x * kBlock + threadIdx.x;  // storage slot
-    const bool valid = j < A.nrows;
-    int64_t off = 0;
-    int width = 0, col = 0;
-    if (valid) {
-        const int64_t s = j >> 5;
-        off = __ldg(A.slice_off + s);
-        width = (int)((__ldg(A.slice_off + s + 1) - off) >> 5);
-        off += j & 31;
-        col = __ldcs(A.pc_c0 + j);
-    }
-    for (int t = threadIdx.x; t < A.sc_ntab; t += kBlock) tab[t] = A.pc_tab[t];
-    __syncthreads();
-    double dot = 0.0;
-    if (valid) {
-        const int64_t i = A.perm ? (int64_t)__ldg(A.perm + j) : j;  // matrix row
-        const double *x = MODE == MODE_RESID ? a.r : a.x;
-        double acc = 0.0;
-        for (int k0 = 0; k0 < width; k0 += DFL_SC_CHUNK) {
-            unsigned g[DFL_SC_CHUNK], c[DFL_SC_CHUNK];
-#pragma unroll
-            for (int k = 0; k < DFL_SC_CHUNK; ++k)
-                if (k0 + k < width) {
-                    g[k] = __ldcs(A.sc_gap + off + 32 * (k0 + k));
-                    c[k] = __ldcs(A.sc_code + off + 32 * (k0 + k));
-                }
-            double xv[DFL_SC_CHUNK];
-#pragma unroll
-            for (int k = 0; k < DFL_SC_CHUNK; ++k)
-                if (k0 + k < width && c[k] != kScPad) {
-                    col += (int)g[k];
-                    xv[k] = __ldg(x + col);
-                }
-#pragma unroll
-            for (int k = 0; k < DFL_SC_CHUNK; ++k)
-                if (k0 + k < width && c[k] != kScPad) acc = add_rn(acc, mul_rn(tab[c[k]], xv[k]));
-        }
-        const double y = epilogue<MODE>(a, i, acc);
-        a.out[i] = y;
-        if (DOT) dot = __ldg(a.r + i) * y;
-    }
-    if (DOT) {
-        __shared__ double sm[32];
-        double v[1] = {dot};
-        block_sum<1>(v, sm);
-        dot_out(a.fin, a.dot_part, v[0]);
-    }
-}
-
-// wr = w .* r  (the relaxation x = w r of amg.py:193/195, rounded as there)
-static __global__ void __launch_bounds__(kBlock) k_wr(const double *__restrict__ w, const double *__restrict__ r, double *wr,
-                                               int64_t n) {
-    DFL_PDL_ENTRY;
-    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    if (i < n) wr[i] = mul_rn(w[i], r[i]);
 }
 
 template <int G, int MODE, bool DOT>
@@ -1144,7 +750,7 @@ __global__ void __launch_bounds__(kBlock, DFL_CSR_MINB) k_csr(DMat A, RowArgs a)
         __shared__ double sm[32];
         double v[1] = {dot};
         block_sum<1>(v, sm);
-        dot_out(a.fin, a.dot_part, v[0]);
+        dot_out(a.dot_part, v[0]);
     }
 }
 
@@ -1207,7 +813,6 @@ struct SubTable {
     int rows_per_tile = 0;
     int64_t sub_off[kSubTab + 1];
     int64_t tile_start[kSubTab + 1];
-    int64_t group_start[kSubTab + 1];  // grid-finish groups of kFinGroup tiles, per subdomain
 };
 
 
@@ -1239,15 +844,6 @@ struct OpArgs {
     const KState *st;
     int need_refresh;       // 1: skip unless st->refresh_now
     const uint8_t *skip_rows = nullptr;  // halo overlap: rows with ghost columns are done later
-    // grid finish of Z'y (single rank, SubTable tiles): the last block sums the
-    // tile partials per subdomain into t and, with Einv, solves t2 = E^-1 t
-    unsigned *tick = nullptr;
-    double *gpart = nullptr;
-    double *t = nullptr;
-    const double *Einv = nullptr;
-    double *t2 = nullptr;
-    int64_t K = 0;
-    int64_t first_col = 0;
     int64_t pf = 0;  // FMT_CLASS: L2 prefetch distance in rows (0: none)
 };
 
@@ -1268,45 +864,6 @@ __device__ __forceinline__ void op_zt(const OpArgs &a, int64_t i, bool valid, do
     if ((int)threadIdx.x < a.k) a.zt_part[slot * a.k + threadIdx.x] = tot;
 }
 
-// Z'y partials of tile t with the grid finish (OpArgs::tick set): partials
-// at stride NV; the last block writes t and t2 = E^-1 t (deflation.py:230-233)
-template <int NV>
-__device__ __forceinline__ void op_zt_fin(const OpArgs &a, const SubTable &S, int64_t i, bool valid, double y,
-                                          int64_t t, int s) {
-    __shared__ double sm[32 * NV];
-    double acc[NV];
-#pragma unroll
-    for (int c = 0; c < NV; ++c) acc[c] = 0.0;
-    if (valid) {
-        acc[0] = y;
-#pragma unroll
-        for (int c = 1; c < NV; ++c)
-            if (c < a.k) acc[c] = __ldg(a.zcols + (int64_t)(c - 1) * a.n + i) * y;
-    }
-    const double tot = block_sum_t<NV>(acc, sm);
-    const int64_t lt = t - S.tile_start[s];
-    const int64_t ntl = S.tile_start[s + 1] - S.tile_start[s];
-    const unsigned g = (unsigned)(S.group_start[s] + lt / kFinGroup);
-    const int64_t gb0 = S.tile_start[s] + (lt / kFinGroup) * kFinGroup;
-    const unsigned gs = (unsigned)min((int64_t)kFinGroup, ntl - (lt / kFinGroup) * kFinGroup);
-    const unsigned ng = (unsigned)S.group_start[S.n];
-    if (!fin_arrive<NV>(a.tick, a.zt_part, a.gpart, t, tot, g, gb0, gs, ng)) return;
-    if (threadIdx.x < 32) {
-        for (int q = 0; q < S.n * a.k; ++q) {
-            const int sq = q / a.k, c = q % a.k;
-            const double v = fin_total<NV>(a.gpart, S.group_start[sq], S.group_start[sq + 1], c);
-            if (threadIdx.x == 0) a.t[a.first_col + q] = v;
-        }
-    }
-    __syncthreads();
-    if (a.Einv == nullptr) return;
-    for (int64_t r = threadIdx.x; r < a.K; r += blockDim.x) {
-        double acc2 = 0.0;
-        for (int64_t j = 0; j < a.K; ++j) acc2 = fma(a.Einv[r * a.K + j], __ldcg(a.t + j), acc2);
-        a.t2[r] = acc2;
-    }
-}
-
 template <int OPMODE, int W, int NV>
 __global__ void __launch_bounds__(kBlock) k_op_ell(DMat A, Tiles T, const __grid_constant__ SubTable S, OpArgs a) {
     DFL_PDL_ENTRY;
@@ -1323,10 +880,7 @@ __global__ void __launch_bounds__(kBlock) k_op_ell(DMat A, Tiles T, const __grid
         a.y[i] = y;
     }
     if (a.k > 0) {
-        if (a.tick)
-            op_zt_fin<NV>(a, S, i, valid, y, t, sub);
-        else
-            op_zt<NV>(a, i, valid, y, t);
+        op_zt<NV>(a, i, valid, y, t);
     }
 }
 
@@ -1350,10 +904,7 @@ __global__ void __launch_bounds__(kBlock) k_op_code(DMat A, Tiles T, const __gri
         a.y[i] = y;
     }
     if (a.k > 0) {
-        if (a.tick)
-            op_zt_fin<NV>(a, S, i, valid, y, t, sub);
-        else
-            op_zt<NV>(a, i, valid, y, t);
+        op_zt<NV>(a, i, valid, y, t);
     }
 }
 
@@ -1386,10 +937,7 @@ __global__ void __launch_bounds__(kBlock, DFL_OPCLASS_MINB) k_op_class(DMat A, T
         a.y[i] = y;
     }
     if (a.k > 0) {
-        if (a.tick)
-            op_zt_fin<NV>(a, S, i, valid, y, t, sub);
-        else
-            op_zt<NV>(a, i, valid, y, t);
+        op_zt<NV>(a, i, valid, y, t);
     }
 }
 
@@ -1565,7 +1113,6 @@ struct ProjArgs {
     int dotmode;        // 0: none, 1: dot(dotv, out), 2: dot(out, out)
     const KState *st;
     int need_refresh;   // 1: only when refresh_now, 0: always, -1: only when !refresh_now
-    Fin fin;            // dotmode != 0: grid finish (single rank)
 };
 
 // t2 is read through the read-only path (every thread of a subdomain reads the
@@ -1622,7 +1169,7 @@ __global__ void __launch_bounds__(kBlock) k_project(ProjArgs a) {
         __shared__ double sm[32];
         double v[1] = {dot};
         block_sum<1>(v, sm);
-        dot_out(a.fin, a.dot_part, v[0]);
+        dot_out(a.dot_part, v[0]);
     }
 }
 
@@ -1698,73 +1245,11 @@ static __global__ void k_reduce(const double *part, int64_t nparts, double *out)
     if (threadIdx.x == 0) *out = s;
 }
 
-// Projection + CG update in one cooperative kernel (single rank, DFL_FUSE_PU=1):
-// q = w - AZ t2 with p.q partials (as k_project<0>), a grid barrier, then every
-// block reduces the partials itself, block 0 records the scalar step of
-// krylov.py:119-126 (cg_step_pq, refresh IF condition), and all blocks apply
-// x += alpha p, r -= alpha q (+ r.r partials) while p and q are still in L2
-// (as k_cg_update).  The KState fields are read before the barrier, so no
-// block sees block 0's update.  pq_part: the p.q partials (a buffer of their
-// own: the r.r partials reuse a.dot_part while slower blocks still reduce).
-template <int KZ>
-__global__ void __launch_bounds__(kBlock, 6) k_proj_update(ProjArgs a, double *x, double *r, double *pq_part,
-                                                        KState *st, int use_if, cudaGraphConditionalHandle hif) {
-    DFL_PDL_ENTRY;
-    __shared__ int s_done, s_iters, s_every;
-    __shared__ double s_rz;
-    if (threadIdx.x == 0) {
-        s_done = st->done;
-        s_iters = st->iters;
-        s_every = st->refresh_every;
-        s_rz = st->rz;
-    }
-    __syncthreads();
-    if (s_done) return;  // uniform across the grid: no block reaches the barrier
-    double dot = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * kBlock) {
-        double q = a.in[i];
-        if (a.azd) q = sub_rn(q, az_row<KZ>(a, i));
-        a.out[i] = q;
-        dot += __ldg(a.dotv + i) * q;
-    }
-    {
-        __shared__ double sm[32];
-        double v[1] = {dot};
-        block_sum<1>(v, sm);
-        if (threadIdx.x == 0) pq_part[blockIdx.x] = v[0];
-    }
-    cooperative_groups::this_grid().sync();
-    const double pq = reduce_parts(pq_part, gridDim.x);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        cg_step_pq(st, pq);
-        if (use_if) cudaGraphSetConditional(hif, (!st->done && st->refresh_now) ? 1u : 0u);
-    }
-    if (pq <= 0.0 || !isfinite(pq)) return;  // curvature breakdown: no update (cg_step_pq)
-    const double alpha = s_rz / pq;
-    const bool refresh = ((s_iters + 1) % s_every) == 0;
-    double rr = 0.0;
-    for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * kBlock) {
-        const double pi = a.dotv[i];
-        x[i] = add_rn(x[i], mul_rn(alpha, pi));
-        if (!refresh) {
-            const double ri = sub_rn(r[i], mul_rn(alpha, a.out[i]));
-            r[i] = ri;
-            rr += ri * ri;
-        }
-    }
-    if (!refresh) {
-        __shared__ double sm2[32];
-        double v[1] = {rr};
-        block_sum<1>(v, sm2);
-        if (threadIdx.x == 0) a.dot_part[blockIdx.x] = v[0];
-    }
-}
-
 // CG update (krylov.py:127-131): x += alpha p;  r -= alpha q  (+ r.r partial)
 // On refresh iterations only x is updated here (r comes from the refresh path).
 static __global__ void __launch_bounds__(kBlock) k_cg_update(double *x, double *r, const double *__restrict__ p,
                                                       const double *__restrict__ q, int64_t n, double *part,
-                                                      const KState *st, Fin fin) {
+                                                      const KState *st) {
     DFL_PDL_ENTRY;
     if (skip(st)) return;
     const double alpha = st->alpha;
@@ -1783,7 +1268,7 @@ static __global__ void __launch_bounds__(kBlock) k_cg_update(double *x, double *
         __shared__ double sm[32];
         double v[1] = {dot};
         block_sum<1>(v, sm);
-        dot_out(fin, part, v[0]);
+        dot_out(part, v[0]);
     }
 }
 

@@ -57,6 +57,7 @@ _STATUS = {
     -6: ConfigError,
     -7: DeviceError,
     -8: DeviceError,
+    -9: ParseError,
 }
 
 

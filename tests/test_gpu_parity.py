@@ -66,10 +66,9 @@ def test_spmv_class_coded_bitwise(variant):
 def test_spmv_transfer_operators_coded_bitwise(level, which, monkeypatch):
     """The smoothed prolongation P of a structured problem (<= 7 entries, <= 15
     distinct values: FMT_PCODE delta/value-coded rows at level 0) and the
-    restriction R = P^T (long rows, 9 values: FMT_SCODE gap/value-coded SELL,
-    100^3 so that it has >= 100K rows) are bit-identical to spmv_rows; the
+    restriction R = P^T (long rows: SELL-32-1024, one thread per row in CSR
+    order, 100^3 so that it has >= 100K rows) are bit-identical to spmv_rows; the
     generic fallbacks at level 1 (multi-lane CSR for R) agree to rounding."""
-    monkeypatch.setenv("DFL_SCODE", "1")  # opt-in format, read at context creation
     p = problems.poisson3d(100 if which == "R" and level == 0 else 20)
     A = nat.CsrArrays(p.matrix.nrows, p.matrix.ncols, p.matrix.row_ptr, p.matrix.col_idx, p.matrix.values)
     h = nat.Hierarchy(A, nat.AmgOptions(0.08, 2 / 3, 0.8, nat.DFL_RELAX["spai0"], 25, 500))
