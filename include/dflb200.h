@@ -130,6 +130,7 @@ typedef struct {
     double h2d_seconds;
     double d2h_seconds;
     int64_t kernel_launches;    /* kernels of this library launched by the solve */
+    double breakdown_value;     /* CG: the p'Ap / r'z that broke down (krylov.py:124,140) */
 } dfl_report;
 
 /* structured test problems (problems.py make_problem; reference problems.py:143-171 for the
@@ -269,6 +270,13 @@ DFL_API int dfl_ctx_finalize(dfl_ctx *ctx);
 DFL_API int64_t dfl_ctx_device_bytes(const dfl_ctx *ctx);
 
 /* ---- solve phase ------------------------------------------------------------------- */
+/* Stream ordering for device-pointer inputs (DFL_PTR_DEVICE): the context
+ * works on a private stream, so a b (or x0) just written by work queued on
+ * another stream must be ordered first: dfl_ctx_wait_stream(ctx, s) makes
+ * the context's next operations wait for everything queued on the CUDA
+ * stream s (a cudaStream_t; NULL = the legacy default stream).  dfl_solve and
+ * the unit operations return only after their outputs are complete. */
+DFL_API int dfl_ctx_wait_stream(dfl_ctx *ctx, void *stream);
 DFL_API int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *x, int ptr_kind,
               dfl_report *rep);
 

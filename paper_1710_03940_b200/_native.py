@@ -55,14 +55,14 @@ class BlockParams(ctypes.Structure):
 class BlockReport(ctypes.Structure):
     _fields_ = [("iterations", c_i32), ("converged", c_i32), ("relative_residual", c_dbl),
                 ("solve_seconds", c_dbl), ("velocity_iterations", c_i64), ("pressure_iterations", c_i64),
-                ("kernel_launches", c_i64)]
+                ("kernel_launches", c_i64), ("breakdown_value", c_dbl)]
 
 
 class Report(ctypes.Structure):
     _fields_ = [("iterations", c_i32), ("converged", c_i32), ("breakdown", c_i32), ("device_loop", c_i32),
                 ("bnorm", c_dbl), ("resnorm", c_dbl), ("relative_residual", c_dbl),
                 ("solve_seconds", c_dbl), ("h2d_seconds", c_dbl), ("d2h_seconds", c_dbl),
-                ("kernel_launches", c_i64)]
+                ("kernel_launches", c_i64), ("breakdown_value", c_dbl)]
 
 
 _lib = None
@@ -151,6 +151,7 @@ def lib():
         "dfl_ctx_set_inexact": ([c_vp, c_vp, c_dbl], c_i32),
         "dfl_ctx_device_bytes": ([c_vp], c_i64),
         "dfl_solve": ([c_vp, P(SolveParams), c_vp, c_vp, c_i32, P(Report)], c_i32),
+        "dfl_ctx_wait_stream": ([c_vp, c_vp], c_i32),
         "dfl_host_alloc": ([c_i64], c_vp),
         "dfl_host_free": ([c_vp], None),
         "dfl_op_apply": ([c_vp, c_vp, c_vp, c_i32], c_i32),
@@ -375,6 +376,10 @@ class DeviceContext:
     def device_bytes(self) -> int:
         return lib().dfl_ctx_device_bytes(self.h)
 
+    def wait_stream(self, stream: int | None):
+        """Order the context after the work queued on CUDA stream `stream` (a cudaStream_t)."""
+        self._c(lib().dfl_ctx_wait_stream(self.h, c_vp(stream or 0)))
+
     def solve(self, params: SolveParams, b, x, ptr_kind: int = PTR_HOST) -> Report:
         rep = Report()
         bp = _ptr(b) if ptr_kind == PTR_HOST else c_vp(b)
@@ -452,8 +457,14 @@ def spmv_device(A: CsrArrays, x: np.ndarray, device: int = 0) -> np.ndarray:
     return y
 
 
-def breakdown_string(code: int) -> str:
-    return (lib().dfl_breakdown_string(code) or b"").decode()
+def breakdown_string(code: int, value: float | None = None) -> str:
+    """The reference's breakdown note; CG's carry the scalar (krylov.py:124,140)."""
+    s = (lib().dfl_breakdown_string(code) or b"").decode()
+    if value is not None and code == 1:  # DFL_BRK_CURVATURE
+        return f"{s} = {value:g}"
+    if value is not None and code == 2:  # DFL_BRK_RZ
+        return f"{s} to {value:g}"
+    return s
 
 
 class DeviceBlock:

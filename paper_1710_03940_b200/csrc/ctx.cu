@@ -409,6 +409,18 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
     return DFL_OK;
 }
 
+int dfl_ctx_wait_stream(dfl_ctx *ctx, void *stream) {
+    if (!ctx) return DFL_E_STATE;
+    CK(cudaSetDevice(ctx->device));
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventRecord(e, (cudaStream_t)stream));
+    const cudaError_t w = cudaStreamWaitEvent(ctx->st, e, 0);
+    cudaEventDestroy(e);
+    CK(w);
+    return DFL_OK;
+}
+
 int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *x, int ptr_kind, dfl_report *rep) {
     RC(ready(ctx));
     if (!p || !rep) return DFL_E_STATE;
@@ -482,6 +494,7 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     rep->device_loop = (use_graph || (p->solver == DFL_SOLVER_BICGSTAB2 && dev_loop)) ? 1 : 0;
     rep->bnorm = s.bnorm;
     rep->resnorm = s.resnorm;
+    rep->breakdown_value = s.brk_val;
     rep->solve_seconds = ms_solve * 1e-3;
     rep->h2d_seconds = ms_h2d * 1e-3;
     rep->d2h_seconds = ms_d2h * 1e-3;

@@ -105,6 +105,7 @@ __global__ void k_cg_rrz(KState *st, const double *gath, int nranks) {
     }
     if (rz == 0.0 || !isfinite(rz)) {
         st->breakdown = DFL_BRK_RZ;
+        st->brk_val = rz;
         st->done = 1;
         return;
     }

@@ -211,6 +211,7 @@ struct dfl_ctx {
     int gm_restart = 0;
     std::vector<double *> gmV, gmZ;
     const double **gmVp = nullptr, **gmZp = nullptr;  // device pointer arrays
+    int gm_ld = 0;  // GMRES slot stride (>= restart + 1)
     double *gm_h = nullptr, *gm_e = nullptr, *gm_y = nullptr, *gm_part = nullptr, *gm_loc = nullptr,
            *gm_gath = nullptr, *h_gm = nullptr;
     double *scal = nullptr;     // [0..7] local reduced scalars

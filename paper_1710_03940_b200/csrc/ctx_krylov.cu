@@ -285,11 +285,10 @@ int bicg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
 // on the host in IEEE double exactly as the reference's Python; one host
 // round trip per Arnoldi step.
 
-static constexpr int kGmLd = 128;  // max restart + 1
-
+// Hessenberg column / dot-slot stride: >= restart + 1 (buffers grow with M)
 static int gm_alloc(dfl_ctx *ctx, int restart, bool flexible) {
-    if (restart < 1 || restart + 1 > kGmLd) {
-        ctx->err = "solver.M (GMRES restart) must be in [1, " + std::to_string(kGmLd - 1) + "]";
+    if (restart < 1) {  // krylov.py:374-375
+        ctx->err = "restart length must be positive, got " + std::to_string(restart);
         return DFL_E_CONFIG;
     }
     RC(bicg_alloc(ctx));  // zx
@@ -306,16 +305,20 @@ static int gm_alloc(dfl_ctx *ctx, int restart, bool flexible) {
             CK(cudaMemset(z, 0, sizeof(double) * nx));
             ctx->gmZ.push_back(z);
         }
-    if (!ctx->gmVp) {
-        RC(dalloc(ctx, (double **)&ctx->gmVp, kGmLd));
-        RC(dalloc(ctx, (double **)&ctx->gmZp, kGmLd));
-        RC(dalloc(ctx, &ctx->gm_h, kGmLd));
-        RC(dalloc(ctx, &ctx->gm_e, kGmLd));
-        RC(dalloc(ctx, &ctx->gm_y, kGmLd));
-        RC(dalloc(ctx, &ctx->gm_loc, kGmLd));
-        RC(dalloc(ctx, &ctx->gm_gath, (int64_t)kGmLd * ctx->nranks));
-        RC(dalloc(ctx, &ctx->gm_part, (int64_t)kGmLd * 4 * ctx->sm_count));
-        CK(cudaMallocHost(&ctx->h_gm, 4 * kGmLd * sizeof(double)));
+    if (ctx->gm_ld < restart + 1) {
+        int ld = 128;
+        while (ld < restart + 1) ld *= 2;
+        if (ctx->h_gm) cudaFreeHost(ctx->h_gm);
+        RC(dalloc(ctx, (double **)&ctx->gmVp, ld));
+        RC(dalloc(ctx, (double **)&ctx->gmZp, ld));
+        RC(dalloc(ctx, &ctx->gm_h, ld));
+        RC(dalloc(ctx, &ctx->gm_e, ld));
+        RC(dalloc(ctx, &ctx->gm_y, ld));
+        RC(dalloc(ctx, &ctx->gm_loc, ld));
+        RC(dalloc(ctx, &ctx->gm_gath, (int64_t)ld * ctx->nranks));
+        RC(dalloc(ctx, &ctx->gm_part, (int64_t)ld * 4 * ctx->sm_count));
+        CK(cudaMallocHost(&ctx->h_gm, 4 * (size_t)ld * sizeof(double)));
+        ctx->gm_ld = ld;
     }
     CK(cudaMemcpy((void *)ctx->gmVp, ctx->gmV.data(), sizeof(double *) * ctx->gmV.size(), cudaMemcpyHostToDevice));
     if (!ctx->gmZ.empty())
@@ -328,16 +331,16 @@ static int gm_alloc(dfl_ctx *ctx, int restart, bool flexible) {
 static int gm_vdots(dfl_ctx *ctx, int nvec, const double *w, double *dev_out) {
     const unsigned gx = (unsigned)std::min<int64_t>(std::max<int64_t>(1, ctx->nblk), 4 * ctx->sm_count);
     const dim3 grid(gx, (unsigned)cdiv(nvec, kVecGroup));
-    launch_k(ctx->st, k_vdots, grid, kBlock, 0, ctx->gmVp, nvec, w, ctx->n, ctx->gm_part, kGmLd);
+    launch_k(ctx->st, k_vdots, grid, kBlock, 0, ctx->gmVp, nvec, w, ctx->n, ctx->gm_part, ctx->gm_ld);
     ctx->launches++;
     if (!multi(ctx)) {
-        launch_k(ctx->st, k_vreduce, nvec, 1024, 0, ctx->gm_part, gx, kGmLd, dev_out);
+        launch_k(ctx->st, k_vreduce, nvec, 1024, 0, ctx->gm_part, gx, ctx->gm_ld, dev_out);
         ctx->launches++;
         return DFL_OK;
     }
-    launch_k(ctx->st, k_vreduce, nvec, 1024, 0, ctx->gm_part, gx, kGmLd, ctx->gm_loc);
-    RC(comm_allgather(ctx, ctx->gm_loc, ctx->gm_gath, kGmLd));
-    launch_k(ctx->st, k_rank_sum, 1, kGmLd, 0, ctx->gm_gath, ctx->nranks, kGmLd, nvec, dev_out);
+    launch_k(ctx->st, k_vreduce, nvec, 1024, 0, ctx->gm_part, gx, ctx->gm_ld, ctx->gm_loc);
+    RC(comm_allgather(ctx, ctx->gm_loc, ctx->gm_gath, ctx->gm_ld));
+    launch_k(ctx->st, k_rank_sum, (unsigned)cdiv(nvec, 256), 256, 0, ctx->gm_gath, ctx->nranks, ctx->gm_ld, nvec, dev_out);
     ctx->launches += 2;
     return DFL_OK;
 }
@@ -360,8 +363,7 @@ static int gm_residual(dfl_ctx *ctx, bool defl, double *resnorm) {
 
 int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KState &out) {
     const bool defl = p->deflated != 0;
-    const int M = p->restart > 0 ? p->restart : 50;
-    RC(gm_alloc(ctx, M, flexible));
+    const int M = p->restart;
     const int64_t n = ctx->n;
     const unsigned nb = (unsigned)ctx->nblk;
     const unsigned gx = (unsigned)std::min<int64_t>(std::max<int64_t>(1, ctx->nblk), 4 * ctx->sm_count);
@@ -377,6 +379,7 @@ int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KSta
         out.converged = 1;
         return DFL_OK;
     }
+    RC(gm_alloc(ctx, M, flexible));  // b != 0: the restart length is checked here, as krylov.py:370-375
     if (defl) {
         RC(project_dev(ctx, ctx->b, ctx->bp, nullptr, 0));
     } else {
@@ -430,12 +433,12 @@ int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KSta
             ctx->launches += 2;
             RC(global_dots(ctx, ctx->dpart, gx, 1, false, val));
             CK(cudaMemcpyAsync(ctx->h_gm, ctx->gm_h, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, ctx->st));
-            CK(cudaMemcpyAsync(ctx->h_gm + kGmLd, ctx->gm_e, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost,
+            CK(cudaMemcpyAsync(ctx->h_gm + ctx->gm_ld, ctx->gm_e, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost,
                                ctx->st));
             CK(cudaStreamSynchronize(ctx->st));
             for (int i = 0; i <= j; ++i) {
                 h(i, j) = ctx->h_gm[i];
-                h(i, j) += ctx->h_gm[kGmLd + i];
+                h(i, j) += ctx->h_gm[ctx->gm_ld + i];
             }
             const double hj1 = std::sqrt(std::max(val[0], 0.0));
             h(j + 1, j) = hj1;

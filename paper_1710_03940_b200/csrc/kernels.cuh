@@ -104,6 +104,7 @@ struct KState {
     int iters, done, converged, breakdown, maxiter, refresh_every, refresh_now, pad;
     // bicgstab2 scalars
     double rho0, rho1, omega, gamma_div;
+    double brk_val;  // the scalar that broke down (p'Ap or r'z), for the report string
 };
 
 // Programmatic dependent launch: every kernel first waits for the grid it
@@ -421,6 +422,7 @@ __device__ __forceinline__ void cg_step_pq(KState *st, double pq) {  // iters +=
     st->pq = pq;
     if (pq <= 0.0 || !isfinite(pq)) {
         st->breakdown = DFL_BRK_CURVATURE;
+        st->brk_val = pq;
         st->done = 1;
         return;
     }
@@ -438,6 +440,7 @@ __device__ __forceinline__ void cg_step_rr(KState *st, double rr) {  // converge
 __device__ __forceinline__ void cg_step_rz(KState *st, double rz) {  // beta
     if (rz == 0.0 || !isfinite(rz)) {
         st->breakdown = DFL_BRK_RZ;
+        st->brk_val = rz;
         st->done = 1;
         return;
     }
@@ -1321,10 +1324,10 @@ static __global__ void k_gather(const double *__restrict__ src, const int *__res
 // sum rank-gathered scalars in rank order: out[v] = sum_q g[q*stride + v]
 static __global__ void k_rank_sum(const double *g, int nranks, int stride, int nv, double *out) {
     DFL_PDL_ENTRY;
-    const int v = threadIdx.x;
+    const int v = blockIdx.x * blockDim.x + threadIdx.x;
     if (v >= nv) return;
     double acc = 0.0;
-    for (int q = 0; q < nranks; ++q) acc += g[q * stride + v];
+    for (int q = 0; q < nranks; ++q) acc += g[(int64_t)q * stride + v];
     out[v] = acc;
 }
 

@@ -230,7 +230,7 @@ class DeflatedSolver:
         # x comes back in the layout of b: global in, global out; a rank's
         # own rows in, its own rows out (no gather)
         x = x_local if np.shape(b)[0] == self.n_local and self.n_local != self.n else self._global(x_local)
-        brk = nat.breakdown_string(rep.breakdown) if rep.breakdown else None
+        brk = nat.breakdown_string(rep.breakdown, rep.breakdown_value) if rep.breakdown else None
         report = {
             "solver": name,
             "deflation": self.basis.kind if self.deflated else None,
@@ -276,9 +276,21 @@ def _params(solver: "DeflatedSolver", maxiter=None):
     )
 
 
-def solve_device(solver: "DeflatedSolver", b_ptr: int, x_ptr: int):
+def solve_device(solver: "DeflatedSolver", b_ptr: int, x_ptr: int, stream: int | None = None):
     """Solve with this rank's b and x already in device memory (raw CUDA
-    pointers, e.g. ``torch.Tensor.data_ptr()``); returns the native report."""
+    pointers, e.g. ``torch.Tensor.data_ptr()``); returns the native report.
+
+    The solve is ordered after the work queued on `stream` (a cudaStream_t;
+    default: torch's current stream when torch is loaded, so a b written by a
+    torch kernel is complete before it is read).  x is complete on return."""
+    if stream is None:
+        import sys
+
+        torch = sys.modules.get("torch")
+        if torch is not None and torch.cuda.is_available():
+            stream = torch.cuda.current_stream(solver.device).cuda_stream
+    if stream is not None:
+        solver._ctx.wait_stream(stream)
     return solver._ctx.solve(_params(solver), b_ptr, x_ptr, nat.PTR_DEVICE)
 
 

@@ -473,5 +473,9 @@ def test_cg_curvature_breakdown_on_indefinite_matrix(diag):
     assert not rep["converged"] and not ro["converged"]
     assert rep["breakdown"] and "curvature" in rep["breakdown"]
     assert ro["breakdown"] and "curvature" in ro["breakdown"]
+    # the reference's string carries the scalar: "non-positive curvature p'Ap = {pAp:g}"
+    head = "non-positive curvature p'Ap = "
+    assert rep["breakdown"].startswith(head) and ro["breakdown"].startswith(head), (rep["breakdown"], ro["breakdown"])
+    assert float(rep["breakdown"][len(head):]) == pytest.approx(float(ro["breakdown"][len(head):]), rel=1e-5, abs=1e-12)
     assert rep["iterations"] == ro["iterations"]
     assert np.allclose(x, xo, rtol=1e-12, atol=1e-14)
