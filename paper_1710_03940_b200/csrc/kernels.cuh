@@ -933,14 +933,28 @@ __global__ void __launch_bounds__(kBlock, DFL_OPCLASS_MINB) k_op_class(DMat A, T
         }
     }
     const bool valid = i < r1 && !(a.skip_rows && a.skip_rows[i]);
+    // every load of the row that does not depend on its gathers goes out
+    // first: class byte, b, and the Z columns of the epilogue (a third of
+    // the kernel's DRAM bytes), so they overlap the class byte -> gather chain
+    const int c = valid ? (int)__ldcs(A.cls + i) : 0;
+    const double bi = (OPMODE == 1 && valid) ? __ldg(a.b + i) : 0.0;
+    double z[NV];
+#pragma unroll
+    for (int q = 1; q < NV; ++q) z[q] = (valid && q < a.k) ? __ldcs(a.zcols + (int64_t)(q - 1) * a.n + i) : 0.0;
     double y = 0.0;
     if (valid) {
-        const double ax = class_row(C, __ldcs(A.cls + i), i, GatherX{a.x});
-        y = OPMODE == 1 ? sub_rn(__ldg(a.b + i), ax) : ax;
+        const double ax = class_row(C, c, i, GatherX{a.x});
+        y = OPMODE == 1 ? sub_rn(bi, ax) : ax;
         a.y[i] = y;
     }
     if (a.k > 0) {
-        op_zt<NV>(a, i, valid, y, t);
+        __shared__ double sm[32 * NV];
+        double acc[NV];
+        acc[0] = valid ? y : 0.0;
+#pragma unroll
+        for (int q = 1; q < NV; ++q) acc[q] = z[q] * y;
+        const double tot = block_sum_t<NV>(acc, sm);
+        if ((int)threadIdx.x < a.k) a.zt_part[t * a.k + threadIdx.x] = tot;
     }
 }
 
@@ -997,18 +1011,16 @@ static __global__ void __launch_bounds__(kBlock) k_zt_vec(Tiles T, const double 
                                                    int k, double *zt_part) {
     DFL_PDL_ENTRY;
     const int64_t t = blockIdx.x;
-    const int64_t i = T.row0[t] + threadIdx.x;
-    const bool valid = i < T.row1[t];
     __shared__ double sm[32 * kKmax];
     double acc[kKmax];
 #pragma unroll
     for (int c = 0; c < kKmax; ++c) acc[c] = 0.0;
-    if (valid) {
+    for (int64_t i = T.row0[t] + threadIdx.x; i < T.row1[t]; i += blockDim.x) {  // tiles may be wider than the block
         const double y = v[i];
-        acc[0] = y;
+        acc[0] += y;
 #pragma unroll
         for (int c = 1; c < kKmax; ++c)
-            if (c < k) acc[c] = __ldg(zcols + (int64_t)(c - 1) * n + i) * y;
+            if (c < k) acc[c] += __ldg(zcols + (int64_t)(c - 1) * n + i) * y;
     }
     block_sum<kKmax>(acc, sm);
     if (threadIdx.x == 0)
@@ -1184,12 +1196,12 @@ static __global__ void __launch_bounds__(kBlock) k_lift(Tiles T, const int *tile
                                                  double *out, int add_y) {
     DFL_PDL_ENTRY;
     const int64_t t = blockIdx.x;
-    const int64_t i = T.row0[t] + threadIdx.x;
-    if (i >= T.row1[t]) return;
     const int64_t base = (first_col + (int64_t)tile_sub[t] * k);
-    double acc = add_rn(0.0, mul_rn(1.0, t2[base]));
-    for (int c = 1; c < k; ++c) acc = add_rn(acc, mul_rn(zcols[(int64_t)(c - 1) * n + i], t2[base + c]));
-    out[i] = add_y ? add_rn(y[i], acc) : acc;
+    for (int64_t i = T.row0[t] + threadIdx.x; i < T.row1[t]; i += blockDim.x) {
+        double acc = add_rn(0.0, mul_rn(1.0, t2[base]));
+        for (int c = 1; c < k; ++c) acc = add_rn(acc, mul_rn(zcols[(int64_t)(c - 1) * n + i], t2[base + c]));
+        out[i] = add_y ? add_rn(y[i], acc) : acc;
+    }
 }
 
 // ---------------------------------------------------------------------------
