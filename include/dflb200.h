@@ -238,6 +238,12 @@ DFL_API int dfl_ctx_set_comm(dfl_ctx *ctx, int nranks, int rank, const void *ncc
  * rank-ordered sums, host-driven loop) without NCCL, e.g. on one GPU. */
 DFL_API int dfl_fabric_create(int nranks, dfl_fabric **out);
 DFL_API void dfl_fabric_destroy(dfl_fabric *f);
+/* a rank that waits longer than `seconds` in a collective declares the
+ * fabric broken: its call and every later collective return DFL_E_COMM
+ * (CommunicatorError, "a participant dropped out", runtime.py:191-212).
+ * NCCL ranks use DFL_COMM_TIMEOUT (seconds, default 300) and also poll
+ * ncclCommGetAsyncError; either failure aborts the communicator. */
+DFL_API int dfl_fabric_set_timeout(dfl_fabric *f, double seconds);
 DFL_API int dfl_ctx_set_fabric(dfl_ctx *ctx, dfl_fabric *f, int rank);
 
 /* Operator rows of this rank (all its subdomains), columns renumbered as in

@@ -143,6 +143,7 @@ def lib():
         "dfl_ctx_set_comm": ([c_vp, c_i32, c_i32, c_vp], c_i32),
         "dfl_fabric_create": ([c_i32, P(c_vp)], c_i32),
         "dfl_fabric_destroy": ([c_vp], None),
+        "dfl_fabric_set_timeout": ([c_vp, c_dbl], c_i32),
         "dfl_ctx_set_fabric": ([c_vp, c_vp, c_i32], c_i32),
         "dfl_ctx_set_operator": ([c_vp, P(Csr), c_i32, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp], c_i32),
         "dfl_ctx_add_hierarchy": ([c_vp, c_i32, c_vp], c_i32),
@@ -437,6 +438,9 @@ class Fabric:
         check(lib().dfl_fabric_create(nranks, ctypes.byref(h)))
         self.h = h
         self.nranks = nranks
+
+    def set_timeout(self, seconds: float):
+        check(lib().dfl_fabric_set_timeout(self.h, float(seconds)))
 
     def __del__(self):
         if getattr(self, "h", None) and _lib is not None:

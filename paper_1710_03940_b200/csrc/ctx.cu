@@ -29,7 +29,7 @@ static int stage_out(dfl_ctx *ctx, double *dst, const double *src, int ptr_kind)
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(dst, src, sizeof(double) * ctx->n,
                        ptr_kind == DFL_PTR_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->st));
-    CK(cudaStreamSynchronize(ctx->st));
+    RC(comm_wait(ctx, ctx->st));
     return DFL_OK;
 }
 
@@ -56,7 +56,7 @@ static int rank_dot(dfl_ctx *ctx, const double *a, const double *b, double *out)
     } else {
         CK(cudaMemcpyAsync(out, ctx->scal, sizeof(double), cudaMemcpyDeviceToHost, ctx->st));
     }
-    CK(cudaStreamSynchronize(ctx->st));
+    RC(comm_wait(ctx, ctx->st));
     return DFL_OK;
 }
 
@@ -169,12 +169,50 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
     // the operator: row-class coded when it has few distinct rows (structured
     // grids; 1 byte per row instead of 12 per entry), else uniform ELL (at the
     // HBM roofline); FMT_CODE only pays off for the V-cycle kernels with longer
-    // epilogues (profiles/r01).  The halo-overlapped boundary pass (k_op_bnd)
-    // reads ELL / CSR, so a rank with ghost columns keeps those.
+    // epilogues (profiles/r01).  A rank with ghost columns splits the
+    // operator: the rows with ghost columns (the boundary pass, k_op_bnd, after
+    // the halo) go into a matrix of their own, Abnd (ELL / CSR, one row per
+    // boundary slot), and are emptied in Aop, so the interior rows -- which
+    // run while the halo is in flight -- keep the class-coded layout.
     const char *no_ov = getenv("DFL_NO_OVERLAP");
     const bool will_split = multi(ctx) && A->ncols > A->nrows && !(no_ov && no_ov[0] == '1');
-    RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, nullptr, true, nullptr, nullptr, false, false, !will_split));
-    ctx->op_nnz = ctx->Aop.nnz;
+    std::vector<int64_t> ib_ptr, bb_ptr, bb_col;
+    std::vector<double> bb_val;
+    if (will_split) {
+        ib_ptr.assign(A->nrows + 1, 0);
+        bb_ptr.assign(1, 0);
+        for (int64_t i = 0; i < A->nrows; ++i) {
+            bool ghost = false;
+            for (int64_t e = A->row_ptr[i]; e < A->row_ptr[i + 1]; ++e) ghost = ghost || A->col_idx[e] >= A->nrows;
+            if (ghost) {
+                for (int64_t e = A->row_ptr[i]; e < A->row_ptr[i + 1]; ++e) {
+                    bb_col.push_back(A->col_idx[e]);
+                    bb_val.push_back(A->values[e]);
+                }
+                bb_ptr.push_back((int64_t)bb_col.size());
+                ib_ptr[i + 1] = ib_ptr[i];
+            } else {
+                ib_ptr[i + 1] = ib_ptr[i] + (A->row_ptr[i + 1] - A->row_ptr[i]);
+            }
+        }
+        // interior copy: boundary rows empty (skipped by the interior pass)
+        std::vector<int64_t> icol((size_t)ib_ptr[A->nrows]);
+        std::vector<double> ival((size_t)ib_ptr[A->nrows]);
+        for (int64_t i = 0, q = 0; i < A->nrows; ++i)
+            if (ib_ptr[i + 1] > ib_ptr[i])
+                for (int64_t e = A->row_ptr[i]; e < A->row_ptr[i + 1]; ++e, ++q) {
+                    icol[q] = A->col_idx[e];
+                    ival[q] = A->values[e];
+                }
+        HostRows hi{A->nrows, A->ncols, ib_ptr.data(), icol.data(), ival.data()};
+        RC(upload_matrix(ctx, hi, ctx->Aop, ctx->sub_off, nullptr, true, nullptr, nullptr, false, false, true));
+        const int64_t nb = (int64_t)bb_ptr.size() - 1;
+        HostRows hb{nb, A->ncols, bb_ptr.data(), bb_col.data(), bb_val.data()};
+        RC(upload_matrix(ctx, hb, ctx->Abnd, {0, nb}, nullptr, true, nullptr, nullptr, false, false, false));
+    } else {
+        RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, nullptr, true, nullptr, nullptr, false, false, true));
+    }
+    ctx->op_nnz = A->row_ptr[A->nrows] - A->row_ptr[0];
     int64_t nrecv = 0;
     ctx->nbr.clear();
     ctx->recv_cnt.clear();
@@ -322,7 +360,7 @@ int dfl_ctx_set_deflation(dfl_ctx *ctx, int32_t k, const double *zcols, const df
     RC(upload(ctx, &ctx->Einv, Einv, K * K));
     RC(dalloc(ctx, &ctx->tvec, K));
     RC(dalloc(ctx, &ctx->t2, K));
-    RC(dalloc(ctx, &ctx->tgather, (int64_t)ctx->nranks * ctx->max_nsub * k));
+    RC(dalloc(ctx, &ctx->tgather, (int64_t)ctx->nranks * (ctx->max_nsub * k + 1)));  // + the p.w slot of CG
     ctx->deflation = true;
     return DFL_OK;
 }
@@ -471,7 +509,7 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
                        ptr_kind == DFL_PTR_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, ctx->st_copy));
     CK(cudaEventRecord(e_h1, ctx->st_copy));
     CK(cudaMemcpyAsync(ctx->h_state, ctx->state, sizeof(KState), cudaMemcpyDeviceToHost, ctx->st));
-    CK(cudaStreamSynchronize(ctx->st));
+    RC(comm_wait(ctx, ctx->st));
     const KState s = bicg ? bstate : *ctx->h_state;
     // true residual ||b - A x|| / ||b|| (deflation.py:293-297; outside the timed span)
     const int64_t solve_launches = ctx->launches;
@@ -480,7 +518,7 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
         RC(op_apply_dev(ctx, ctx->xin, ctx->tmp, 1, ctx->b, false, nullptr, 0));
         RC(rank_dot(ctx, ctx->tmp, ctx->tmp, &rr));
     }
-    CK(cudaStreamSynchronize(ctx->st_copy));
+    RC(comm_wait(ctx, ctx->st_copy));
     float ms_h2d = 0, ms_solve = 0, ms_d2h = 0;
     CK(cudaEventElapsedTime(&ms_h2d, e_h0, ctx->ev0));
     CK(cudaEventElapsedTime(&ms_solve, ctx->ev0, ctx->ev1));

@@ -482,7 +482,7 @@ int bicg_solve_graph(dfl_ctx *ctx, const dfl_solve_params *p, KState &out) {
     RC(bg_graph(ctx, defl, b));
     CK(cudaGraphLaunch(ctx->bg_exec, ctx->st));
     CK(cudaMemcpyAsync(ctx->h_bstate, b, sizeof(BState), cudaMemcpyDeviceToHost, ctx->st));
-    CK(cudaStreamSynchronize(ctx->st));
+    RC(comm_wait(ctx, ctx->st));
     const BState &s = *static_cast<const BState *>(ctx->h_bstate);
     ctx->launches += ctx->bg_body_kernels * std::max(1, s.iters);
     // x = x0 + M(u)  (krylov.py:284-285), into ctx->x (the y of the deflated system)

@@ -1,5 +1,8 @@
 // Collectives of the multi-rank solve: NCCL (loaded with dlopen) or the
 // in-process fabric used to test several ranks on one device.
+#include <functional>
+#include <thread>
+
 #include "ctx_impl.cuh"
 
 Nccl g_nccl;
@@ -15,20 +18,89 @@ static int nccl_check(dfl_ctx *ctx, int rc, const char *what) {
     return DFL_OK;
 }
 
+static int dropped(dfl_ctx *ctx) {
+    ctx->err = "a participant dropped out: the collective did not complete within " +
+               std::to_string(ctx->fab ? ctx->fab->timeout_s : ctx->comm_timeout_s) + " s";
+    return DFL_E_COMM;
+}
+
+static double comm_timeout_default() {
+    const char *t = getenv("DFL_COMM_TIMEOUT");
+    return t ? atof(t) : 300.0;
+}
+
+static int comm_poll(dfl_ctx *ctx, const std::function<cudaError_t()> &query) {
+    if (ctx->comm_dead) {
+        ctx->err = "the communicator was aborted after an earlier failure";
+        return DFL_E_COMM;
+    }
+    if (!ctx->comm) {
+        for (;;) {  // no NCCL: plain wait
+            const cudaError_t q = query();
+            if (q == cudaSuccess) return DFL_OK;
+            if (q != cudaErrorNotReady) CK(q);
+            std::this_thread::yield();
+        }
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    for (long spin = 0;; ++spin) {
+        const cudaError_t q = query();
+        if (q == cudaSuccess) return DFL_OK;
+        if (q != cudaErrorNotReady) CK(q);
+        if ((spin & 255) == 0) {
+            int aerr = 0;
+            if (g_nccl.CommGetAsyncError && g_nccl.CommGetAsyncError(ctx->comm, &aerr) == 0 && aerr != 0 &&
+                aerr != 7 /* ncclInProgress */) {
+                ctx->err = std::string("NCCL asynchronous error: ") + g_nccl.GetErrorString(aerr) +
+                           " (a participant dropped out?)";
+                if (g_nccl.CommAbort) g_nccl.CommAbort(ctx->comm);
+                ctx->comm = nullptr;
+                ctx->comm_dead = true;
+                return DFL_E_COMM;
+            }
+            const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+            if (el > ctx->comm_timeout_s) {
+                if (g_nccl.CommAbort) g_nccl.CommAbort(ctx->comm);
+                ctx->comm = nullptr;
+                ctx->comm_dead = true;
+                return dropped(ctx);
+            }
+            if (spin > 4096) std::this_thread::sleep_for(std::chrono::microseconds(20));
+        }
+    }
+}
+
+int comm_wait(dfl_ctx *ctx, cudaStream_t s) {
+    if (!ctx->comm && !ctx->comm_dead) {
+        CK(cudaStreamSynchronize(s));
+        return DFL_OK;
+    }
+    return comm_poll(ctx, [s] { return cudaStreamQuery(s); });
+}
+
+int comm_wait_event(dfl_ctx *ctx, cudaEvent_t e) {
+    if (!ctx->comm && !ctx->comm_dead) {
+        CK(cudaEventSynchronize(e));
+        return DFL_OK;
+    }
+    return comm_poll(ctx, [e] { return cudaEventQuery(e); });
+}
+
 // allgather of `count` doubles per rank into recv[q * count] (send may alias
 // recv + rank * count)
 int comm_allgather(dfl_ctx *ctx, const double *send, double *recv, size_t count) {
+    if (ctx->comm_dead) return comm_wait(ctx, ctx->st);
     if (ctx->comm) return nccl_check(ctx, g_nccl.AllGather(send, recv, count, ncclDouble_, ctx->comm, ctx->st), "ncclAllGather");
     dfl_fabric *f = ctx->fab;
     CK(cudaStreamSynchronize(ctx->st));
     f->pub[ctx->rank] = send;
-    f->barrier();
+    if (!f->barrier()) return dropped(ctx);
     for (int q = 0; q < ctx->nranks; ++q) {
         double *dst = recv + (size_t)q * count;
         if (f->pub[q] != dst) CK(cudaMemcpyAsync(dst, f->pub[q], count * sizeof(double), cudaMemcpyDefault, ctx->st));
     }
     CK(cudaStreamSynchronize(ctx->st));
-    f->barrier();
+    if (!f->barrier()) return dropped(ctx);
     return DFL_OK;
 }
 
@@ -51,7 +123,7 @@ int halo(dfl_ctx *ctx, double *v, cudaStream_t xs) {
         dfl_fabric *f = ctx->fab;
         CK(cudaStreamSynchronize(ctx->st));
         f->pub[ctx->rank] = ctx->sendbuf;
-        f->barrier();
+        if (!f->barrier()) return dropped(ctx);
         int64_t ro = 0;
         for (size_t qi = 0; qi < ctx->nbr.size(); ++qi) {
             const dfl_ctx *peer = f->ctxs[ctx->nbr[qi]];
@@ -74,9 +146,10 @@ int halo(dfl_ctx *ctx, double *v, cudaStream_t xs) {
             ro += ctx->recv_cnt[qi];
         }
         CK(cudaStreamSynchronize(ctx->st));
-        f->barrier();
+        if (!f->barrier()) return dropped(ctx);
         return DFL_OK;
     }
+    if (ctx->comm_dead) return comm_wait(ctx, ctx->st);
     RC(nccl_check(ctx, g_nccl.GroupStart(), "ncclGroupStart"));
     int64_t so = 0, ro = 0;
     for (size_t q = 0; q < ctx->nbr.size(); ++q) {
@@ -94,7 +167,8 @@ int halo(dfl_ctx *ctx, double *v, cudaStream_t xs) {
 }
 
 // Z' v partials -> t (global numbering) -> t2 = E^-1 t on every rank
-int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op) {
+int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op, const double *extra_part,
+             int64_t extra_n) {
     const int64_t *sub_tiles = ctx->sub_tiles;
     if (!multi(ctx)) {
         launch_k(ctx->st, k_zt_finish, ctx->nsub * ctx->k, 1024, 0, ctx->zt_part, sub_tiles, ctx->nsub, ctx->k,
@@ -110,13 +184,18 @@ int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op) {
         }
         return DFL_OK;
     }
-    // local entries into a padded slot, allgather, unpack, solve
-    const int64_t slot = (int64_t)ctx->max_nsub * ctx->k;
+    // local entries into a padded slot (+ the caller's extra scalar: CG's
+    // rank-local p.w), allgather, unpack, solve
+    const int64_t slot = (int64_t)ctx->max_nsub * ctx->k + 1;
     double *mine = ctx->tgather + (int64_t)ctx->rank * slot;
     launch_k(ctx->st, k_zt_finish, ctx->nsub * ctx->k, 1024, 0, ctx->zt_part, sub_tiles, ctx->nsub, ctx->k, mine, 0,
                                                          nullptr, ctx->K, nullptr, st, need_refresh, ctx->ticket,
                                                          from_op && ctx->split ? ctx->sub_btiles : nullptr,
                                                          ctx->ntiles);
+    if (extra_part) {
+        launch_k(ctx->st, k_reduce, 1, 1024, 0, extra_part, extra_n, mine + slot - 1);
+        ctx->launches++;
+    }
     RC(comm_allgather(ctx, mine, ctx->tgather, slot));
     // unpack rank slots into t: rank q owns a contiguous subdomain range
     int64_t pos = 0;
@@ -178,6 +257,7 @@ int dfl_ctx_set_comm(dfl_ctx *ctx, int nranks, int rank, const void *id) {
     CK(cudaSetDevice(ctx->device));
     NcclId nid;
     std::memcpy(&nid, id, sizeof nid);
+    ctx->comm_timeout_s = comm_timeout_default();
     return nccl_check(ctx, g_nccl.CommInitRank(&ctx->comm, nranks, nid, rank), "ncclCommInitRank");
 }
 
@@ -192,6 +272,13 @@ int dfl_fabric_create(int nranks, dfl_fabric **out) {
 }
 
 void dfl_fabric_destroy(dfl_fabric *f) { delete f; }
+
+int dfl_fabric_set_timeout(dfl_fabric *f, double seconds) {
+    if (!f || !(seconds > 0.0)) return DFL_E_STATE;
+    std::lock_guard<std::mutex> lk(f->mu);
+    f->timeout_s = seconds;
+    return DFL_OK;
+}
 
 int dfl_ctx_set_fabric(dfl_ctx *ctx, dfl_fabric *f, int rank) {
     if (!ctx || !f || rank < 0 || rank >= f->nranks) return DFL_E_STATE;

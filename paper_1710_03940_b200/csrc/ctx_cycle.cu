@@ -96,10 +96,10 @@ int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double 
     a.skip_rows = nullptr;
     if (ctx->nbtiles > 0) {
         if (opmode == 0)
-            launch_k(ctx->st, k_op_bnd<0>, (unsigned)ctx->nbtiles, kBlock, 0, ctx->Aop, ctx->brows, ctx->bstart, ctx->bcnt,
+            launch_k(ctx->st, k_op_bnd<0>, (unsigned)ctx->nbtiles, kBlock, 0, ctx->Abnd, ctx->brows, ctx->bstart, ctx->bcnt,
                                                                          ctx->ntiles, a);
         else
-            launch_k(ctx->st, k_op_bnd<1>, (unsigned)ctx->nbtiles, kBlock, 0, ctx->Aop, ctx->brows, ctx->bstart, ctx->bcnt,
+            launch_k(ctx->st, k_op_bnd<1>, (unsigned)ctx->nbtiles, kBlock, 0, ctx->Abnd, ctx->brows, ctx->bstart, ctx->bcnt,
                                                                          ctx->ntiles, a);
         ctx->launches++;
     }

@@ -39,6 +39,8 @@ struct Nccl {
     int (*GroupStart)() = nullptr;
     int (*GroupEnd)() = nullptr;
     const char *(*GetErrorString)(int) = nullptr;
+    int (*CommGetAsyncError)(NcclComm, int *) = nullptr;  // optional
+    int (*CommAbort)(NcclComm) = nullptr;                 // optional
     bool load(std::string &err) {
         if (h) return true;
         const char *names[] = {"libnccl.so.2", "libnccl.so"};
@@ -64,6 +66,8 @@ struct Nccl {
         LD(GroupEnd, "ncclGroupEnd");
         LD(GetErrorString, "ncclGetErrorString");
 #undef LD
+        CommGetAsyncError = reinterpret_cast<decltype(CommGetAsyncError)>(dlsym(h, "ncclCommGetAsyncError"));
+        CommAbort = reinterpret_cast<decltype(CommAbort)>(dlsym(h, "ncclCommAbort"));
         return true;
     }
 };
@@ -112,16 +116,27 @@ struct dfl_fabric {
     long generation = 0;
     std::vector<dfl_ctx *> ctxs;
     std::vector<const double *> pub;  // per-rank published buffer of the current collective
-    void barrier() {
+    double timeout_s = 300.0;         // a rank waiting longer declares the collective broken
+    bool broken = false;              // a participant dropped out: every later collective fails
+    // false: a participant did not arrive within timeout_s (or dropped out earlier)
+    bool barrier() {
         std::unique_lock<std::mutex> lk(mu);
+        if (broken) return false;
         const long gen = generation;
         if (++arrived == nranks) {
             arrived = 0;
             ++generation;
             cv.notify_all();
-        } else {
-            cv.wait(lk, [&] { return generation != gen; });
+            return true;
         }
+        const bool ok = cv.wait_for(lk, std::chrono::duration<double>(timeout_s),
+                                    [&] { return generation != gen || broken; });
+        if (!ok || broken) {
+            broken = true;
+            cv.notify_all();
+            return false;
+        }
+        return true;
     }
 };
 
@@ -138,12 +153,15 @@ struct dfl_ctx {
     // comm
     int nranks = 1, rank = 0;
     NcclComm comm = nullptr;
+    bool comm_dead = false;      // aborted after a failure: every later collective fails
+    double comm_timeout_s = 300.0;  // DFL_COMM_TIMEOUT: longest wait for a collective
     // operator
     bool have_op = false, finalized = false;
     int64_t n = 0, n_ghost = 0;
     int nsub = 0;
     std::vector<int64_t> sub_off;
     DMat Aop;
+    DMat Abnd;  // split operator (ranks with ghost columns): the rows with ghost columns, one per boundary slot
     std::vector<int64_t> op_nnz_rows;  // host stats
     int64_t op_nnz = 0;
     // tiles (per subdomain, rows per tile = op rows per block)
@@ -515,8 +533,15 @@ int build_tiles(dfl_ctx *ctx);
 // ctx_comm.cu
 int comm_allgather(dfl_ctx *ctx, const double *send, double *recv, size_t count);
 int halo(dfl_ctx *ctx, double *v, cudaStream_t xs = nullptr);
-int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op);
+int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op, const double *extra_part = nullptr,
+             int64_t extra_n = 0);
 int rank_scalar(dfl_ctx *ctx, const double *part, int64_t nparts, int slot, const double **gath);
+// wait for a stream / event; with NCCL, poll the communicator's asynchronous
+// error and a timeout instead of blocking, abort the communicator on either
+// (a participant that dropped out would otherwise hang the solve) and return
+// DFL_E_COMM -> CommunicatorError (runtime.py:191-212)
+int comm_wait(dfl_ctx *ctx, cudaStream_t s);
+int comm_wait_event(dfl_ctx *ctx, cudaEvent_t e);
 // ctx_cycle.cu
 int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *dot_part, int64_t *nparts);
 int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double *b, bool zt, const KState *st,

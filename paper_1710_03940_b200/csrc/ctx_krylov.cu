@@ -9,7 +9,7 @@
 
 static int fetch(dfl_ctx *ctx, const double *dev, int n, double *out) {
     CK(cudaMemcpyAsync(ctx->h_dots, dev, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->st));
-    CK(cudaStreamSynchronize(ctx->st));
+    RC(comm_wait(ctx, ctx->st));
     for (int q = 0; q < n; ++q) out[q] = ctx->h_dots[q];
     return DFL_OK;
 }
@@ -435,7 +435,7 @@ int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KSta
             CK(cudaMemcpyAsync(ctx->h_gm, ctx->gm_h, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost, ctx->st));
             CK(cudaMemcpyAsync(ctx->h_gm + ctx->gm_ld, ctx->gm_e, sizeof(double) * (j + 1), cudaMemcpyDeviceToHost,
                                ctx->st));
-            CK(cudaStreamSynchronize(ctx->st));
+            RC(comm_wait(ctx, ctx->st));
             for (int i = 0; i <= j; ++i) {
                 h(i, j) = ctx->h_gm[i];
                 h(i, j) += ctx->h_gm[ctx->gm_ld + i];
@@ -478,7 +478,7 @@ int gmres_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool flexible, KSta
             launch_k(ctx->st, k_addv, nb, kBlock, 0, ctx->x, ctx->zx, n);
             ctx->launches += 2;
         }
-        CK(cudaStreamSynchronize(ctx->st));  // y (host vector) was read by the async copy above
+        RC(comm_wait(ctx, ctx->st));  // y (host vector) was read by the async copy above
         total += j;
         RC(gm_residual(ctx, defl, &resnorm));
     }

@@ -990,14 +990,15 @@ __global__ void __launch_bounds__(kBlock) k_op_bnd(DMat A, const int *__restrict
     if (a.need_refresh && !a.st->refresh_now) return;
     const int64_t bt = blockIdx.x;
     const bool valid = (int)threadIdx.x < bcnt[bt];
-    const int64_t i = valid ? brows[bstart[bt] + threadIdx.x] : 0;
+    const int64_t slot = valid ? bstart[bt] + threadIdx.x : 0;  // row of the boundary matrix A
+    const int64_t i = valid ? brows[slot] : 0;                   // row of the operator
     double y = 0.0;
     if (valid) {
         double ax = 0.0;
         if (A.fmt == FMT_CSR) {
-            for (int e = A.ptr[i]; e < A.ptr[i + 1]; ++e) ax = add_rn(ax, mul_rn(A.val[e], __ldg(a.x + A.col[e])));
+            for (int e = A.ptr[slot]; e < A.ptr[slot + 1]; ++e) ax = add_rn(ax, mul_rn(A.val[e], __ldg(a.x + A.col[e])));
         } else {
-            ax = ell_row_sliced(A, i, GatherX{a.x});
+            ax = ell_row_sliced(A, slot, GatherX{a.x});
         }
         y = OPMODE == 1 ? sub_rn(__ldg(a.b + i), ax) : ax;
         a.y[i] = y;

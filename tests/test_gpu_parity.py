@@ -479,3 +479,42 @@ def test_cg_curvature_breakdown_on_indefinite_matrix(diag):
     assert float(rep["breakdown"][len(head):]) == pytest.approx(float(ro["breakdown"][len(head):]), rel=1e-5, abs=1e-12)
     assert rep["iterations"] == ro["iterations"]
     assert np.allclose(x, xo, rtol=1e-12, atol=1e-14)
+
+
+@pytest.mark.timeout(300)
+def test_participant_dropout_raises_communicator_error():
+    """runtime.py:191-212: a collective whose participant dropped out raises
+    CommunicatorError instead of hanging.  Two ranks on the in-process fabric;
+    rank 1 sets up and then never solves, so rank 0's first collective times
+    out (2 s here), and every later collective on the fabric fails at once."""
+    import threading
+
+    from paper_1710_03940_b200 import DeflatedSolver
+    from paper_1710_03940_b200.dist import ThreadWorld
+    from paper_1710_03940_b200.errors import CommunicatorError
+
+    p = problems.poisson3d(12, problems.boxes_for(2))
+    cfg = SolverConfig({"solver": {"type": "cg", "tol": 1e-8}, "precond": {"relax": {"type": "spai0"}},
+                        "deflation": {"kind": "linear"}})
+    fab = nat.Fabric(2)
+    fab.set_timeout(2.0)
+    shared = ThreadWorld.Shared(2)
+    solvers, errs = [None, None], []
+
+    def setup(rank):
+        try:
+            solvers[rank] = DeflatedSolver(p.matrix, p.partition, config=cfg, coords=p.coords,
+                                           world=ThreadWorld(shared, rank), fabric=fab, device=0)
+        except Exception as exc:  # pragma: no cover
+            errs.append(exc)
+
+    th = [threading.Thread(target=setup, args=(r,)) for r in range(2)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    with pytest.raises(CommunicatorError, match="dropped out"):
+        solvers[0].solve(p.rhs)
+    with pytest.raises(CommunicatorError):
+        solvers[1].solve(p.rhs)  # the fabric stays broken
