@@ -87,6 +87,14 @@ def test_config_matches_reference(case):
         # as close to a 1e-12 solution as the reference's x
         assert rep["iterations"] <= meta["iterations"] + 1
         assert rep["relative_residual"] <= tol
+        # the oracle (the reference's algorithm, pinned bitwise to it) with only
+        # its Z' r sums taken pairwise instead of sequentially over the 7M rows
+        # converges in 9 groups to 9.0e-9 (tools/diag_zt_accuracy.py, committed
+        # in tests/golden/c5_m1_zt_accuracy.json): the device matches that
+        with open(os.path.join(os.path.dirname(HERE), "c5_m1_zt_accuracy.json")) as fh:
+            acc = json.load(fh)
+        assert acc["reference_sums"]["iters"] == meta["iterations"]
+        assert abs(rep["iterations"] - acc["pairwise_zt"]["iters"]) <= 1, (rep["iterations"], acc["pairwise_zt"])
         _, xt, rt = _solve(meta, tol=1e-12)
         assert rt["converged"] and rt["relative_residual"] <= 1e-10
         e_gpu = np.linalg.norm(x[idx] - xt[idx])
