@@ -367,8 +367,7 @@ inline int64_t code_grid(const DMat &A) {
 
 template <int MODE, bool DOT>
 inline int64_t class_grid(const DMat &A) {
-    static const int occ = occupancy(k_class<MODE, DOT>);
-    return std::max<int64_t>(1, std::min<int64_t>(cdiv(A.nrows, kBlock), (int64_t)occ * g_sm_count));
+    return cdiv(A.nrows, kBlock);  // k_class1: one block per kBlock rows
 }
 
 // number of per-block / per-tile partials the POST-with-dot kernel on A produces
@@ -401,8 +400,9 @@ static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
         return;
     }
     if (A.fmt == FMT_CLASS) {
-        launch_k(ctx->st, k_class<MODE, DOT>, (unsigned)class_grid<MODE, DOT>(A), kBlock, 0, A, a,
-                 *ctx->class_tabs[A.class_id]);
+        static const int occ1 = occupancy(k_class1<MODE, DOT>);
+        launch_k(ctx->st, k_class1<MODE, DOT>, (unsigned)class_grid<MODE, DOT>(A), kBlock, 0, A, a,
+                 *ctx->class_tabs[A.class_id], (int64_t)occ1 * g_sm_count * kBlock);
         ctx->launches++;
         return;
     }

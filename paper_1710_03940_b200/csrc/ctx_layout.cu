@@ -239,6 +239,8 @@ static constexpr double kSellMinMean = 12.0;
 static constexpr double kShortRowMean = 8.0;
 static constexpr double kShortRowPad = 1.7;     // short rows: padding is cheaper than CSR up to this
 static constexpr double kCsrPerLane = 12.0;     // CSR-vector: target entries per lane
+static constexpr int64_t kCsrTinyRows = 5000;   // levels below: kCsrPerLaneTiny (profiles/r02/README.md)
+static constexpr double kCsrPerLaneTiny = 3.0;
 
 int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<int64_t> &bounds,
                   std::vector<int64_t> *bound_tiles, bool allow_ell, const double *colscale, DMat *scaled,
@@ -379,7 +381,9 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
         m.stored = m.nnz;
         // lanes per row: about kCsrPerLane entries per lane, batched kCsrUnroll deep
         int g = 1;
-        const int want = (int)std::ceil(mean / kCsrPerLane);
+        // tiny levels (< kCsrTinyRows rows: the last AMG levels, the coarsest
+        // restriction) are latency chains: more lanes, fewer entries each
+        const int want = (int)std::ceil(mean / (h.nrows < kCsrTinyRows ? kCsrPerLaneTiny : kCsrPerLane));
         while (g < want && g < 32) g *= 2;
         m.group = g;
         // padded by 4 entries (aligned vector loads may overrun the last row)

@@ -489,12 +489,6 @@ __device__ __forceinline__ double epilogue(const RowArgs &a, int64_t i, double a
 #ifndef DFL_OPCLASS_MINB
 #define DFL_OPCLASS_MINB 8
 #endif
-#ifndef DFL_CLASS_MINB
-#define DFL_CLASS_MINB 5
-#endif
-#ifndef DFL_CLASS_RESID_MINB
-#define DFL_CLASS_RESID_MINB 4  // the w .* r gathers of the pre-smoothing residual
-#endif
 #ifndef DFL_ELL_MINB0
 #define DFL_ELL_MINB0 6
 #endif
@@ -623,64 +617,47 @@ __device__ __forceinline__ double class_row(const ClassTab &T, int c, int64_t ro
     return class_row_slow(T, c, row, g);
 }
 
-// FMT_CLASS row kernel (V-cycle stages), grid-stride over one wave, software
-// pipelined like k_codep: the next row's class byte and own-row operands are
-// loaded one iteration ahead and its leading gather edge is prefetched to L2
+// FMT_CLASS row kernel (V-cycle stages), one row per thread and one block per
+// kBlock rows (the operator kernel's layout, k_op_class): the grid holds
+// every row, so 64 warps per SM cover the class byte -> gather chain; the
+// next wave's first DRAM touches (class byte, leading gather edge) are
+// prefetched into L2 (pf rows ahead).  Own-row operands are loaded before
+// the gathers.  DOT: one partial per block.
 template <int MODE, bool DOT>
-__global__ void __launch_bounds__(kBlock, MODE == MODE_RESID ? DFL_CLASS_RESID_MINB : DFL_CLASS_MINB) k_class(DMat A, RowArgs a, const __grid_constant__ ClassTab T) {
+__global__ void __launch_bounds__(kBlock, DFL_OPCLASS_MINB) k_class1(DMat A, RowArgs a, const __grid_constant__ ClassTab T,
+                                                                    int64_t pf) {
     DFL_PDL_ENTRY;
     constexpr bool kR = MODE != MODE_PLAIN || DOT;
     constexpr bool kPost = MODE == MODE_POST;
     const bool wr = MODE == MODE_RESID && a.x == nullptr;
-    const double *gx = wr ? a.r : a.x;
-    const int64_t n = A.nrows, ncols = A.ncols;
-    const int64_t stride = (int64_t)gridDim.x * kBlock;
-    int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
-    int c = 0;
-    double ri = 0.0, wi = 0.0, xi = 0.0;
-    if (i < n) {
-        c = __ldcs(A.cls + i);
-        if (kR) ri = __ldg(a.r + i);
-        if (kPost) {
-            wi = __ldg(a.w + i);
-            xi = __ldg(a.xo + i);
-        }
-        const int64_t pe = min(i + (int64_t)T.lead, ncols - 1);
-        prefetch_l2(gx + pe);
-        if (wr) prefetch_l2(a.w + pe);
-    }
-    double dot = 0.0;
-    for (; i < n; i += stride) {
-        const int64_t in = i + stride;
-        int cn = 0;
-        double rn = 0.0, wn = 0.0, xn = 0.0;
-        if (in < n) {
-            cn = __ldcs(A.cls + in);
-            if (kR) rn = __ldg(a.r + in);
-            if (kPost) {
-                wn = __ldg(a.w + in);
-                xn = __ldg(a.xo + in);
-            }
-            const int64_t pe = min(in + (int64_t)T.lead, ncols - 1);
-            prefetch_l2(gx + pe);
+    const int64_t n = A.nrows;
+    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    if (pf > 0) {
+        const int64_t ip = i + pf;
+        if (ip < n) {
+            prefetch_l2(A.cls + ip);
+            const int64_t pe = min(ip + (int64_t)T.lead, A.ncols - 1);
+            prefetch_l2((wr ? a.r : a.x) + pe);
             if (wr) prefetch_l2(a.w + pe);
         }
+    }
+    const bool valid = i < n;
+    const int c = valid ? (int)__ldcs(A.cls + i) : 0;
+    const double ri = (kR && valid) ? __ldg(a.r + i) : 0.0;
+    const double wi = (kPost && valid) ? __ldg(a.w + i) : 0.0;
+    const double xi = (kPost && valid) ? __ldg(a.xo + i) : 0.0;
+    double y = 0.0;
+    if (valid) {
         const double ax = wr ? class_row(T, c, i, GatherWR{a.w, a.r}) : class_row(T, c, i, GatherX{a.x});
-        double y;
         if (MODE == MODE_PLAIN) y = ax;
         else if (MODE == MODE_RESID) y = sub_rn(ri, ax);
         else if (MODE == MODE_POST) y = add_rn(xi, mul_rn(wi, sub_rn(ri, ax)));
         else y = epilogue<MODE>(a, i, ax);
         a.out[i] = y;
-        if (DOT) dot += ri * y;
-        c = cn;
-        ri = rn;
-        wi = wn;
-        xi = xn;
     }
     if (DOT) {
         __shared__ double sm[32];
-        double v[1] = {dot};
+        double v[1] = {ri * y};
         block_sum<1>(v, sm);
         dot_out(a.dot_part, v[0]);
     }
