@@ -44,19 +44,20 @@ def up_to_date() -> bool:
 def build(force: bool = False, verbose: bool = False, out: str | None = None) -> str:
     if out is None and not force and up_to_date():
         return LIB
-    os.makedirs(BUILD, exist_ok=True)
+    bdir = BUILD if out is None else os.path.join(REPO, "build", os.path.basename(out) + ".obj")
+    os.makedirs(bdir, exist_ok=True)
     nvcc = _nvcc()
     run = lambda cmd: subprocess.run(cmd, check=True, stdout=None if verbose else subprocess.DEVNULL)
     # only the C ABI of include/dflb200.h (DFL_API) is exported
     jobs = []
     for f in CXX_SOURCES:
-        o = os.path.join(BUILD, f + ".o")
+        o = os.path.join(bdir, f + ".o")
         jobs.append((o, ["g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-ffp-contract=off", "-fno-fast-math",
                          "-fvisibility=hidden", "-I", os.path.join(REPO, "include"), "-c", os.path.join(CSRC, f),
                          "-o", o]))
     extra = os.environ.get("DFL_NVCC_FLAGS", "").split()
     for f in CU_SOURCES:
-        o = os.path.join(BUILD, f + ".o")
+        o = os.path.join(bdir, f + ".o")
         jobs.append((o, [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", *extra,
                          "-Xcompiler", "-ffp-contract=off", "-Xcompiler", "-fvisibility=hidden",
                          "-I", os.path.join(REPO, "include"), "-c", os.path.join(CSRC, f), "-o", o]))

@@ -269,7 +269,10 @@ __device__ __forceinline__ double ell_slice_w(const DMat &A, int64_t off, const 
     return acc;
 }
 
-constexpr int kChunk = 4;  // entries of a sliced row whose loads are batched
+#ifndef DFL_SLICE_CHUNK
+#define DFL_SLICE_CHUNK 4
+#endif
+constexpr int kChunk = DFL_SLICE_CHUNK;  // entries of a sliced row whose loads are batched
 
 // chunk of w <= kChunk entries of a sliced row, accumulated into acc in order
 template <class G>
