@@ -28,6 +28,10 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+def _cuda_include() -> str:
+    return os.path.join(os.path.dirname(os.path.dirname(_nvcc())), "include")  # NVTX 3 headers
+
+
 def _sources():
     hdrs = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".hpp", ".h"))]
     hdrs.append(os.path.join(REPO, "include", "dflb200.h"))
@@ -53,7 +57,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None) ->
     for f in CXX_SOURCES:
         o = os.path.join(bdir, f + ".o")
         jobs.append((o, ["g++", "-O3", "-std=c++17", "-fPIC", "-pthread", "-ffp-contract=off", "-fno-fast-math",
-                         "-fvisibility=hidden", "-I", os.path.join(REPO, "include"), "-c", os.path.join(CSRC, f),
+                         "-fvisibility=hidden", "-I", os.path.join(REPO, "include"), "-I", _cuda_include(),
+                         "-c", os.path.join(CSRC, f),
                          "-o", o]))
     extra = os.environ.get("DFL_NVCC_FLAGS", "").split()
     for f in CU_SOURCES:

@@ -391,6 +391,7 @@ int dfl_ctx_set_inexact(dfl_ctx *ctx, const double *E, double coarse_tol) {
 }
 
 int dfl_ctx_finalize(dfl_ctx *ctx) {
+    dfl::NvtxRange nv("dfl.upload");
     if (!ctx) return DFL_E_STATE;
     if (!ctx->have_op) {
         ctx->err = "no operator uploaded";
@@ -460,6 +461,7 @@ int dfl_ctx_wait_stream(dfl_ctx *ctx, void *stream) {
 }
 
 int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *x, int ptr_kind, dfl_report *rep) {
+    dfl::NvtxRange nv("dfl.solve");
     RC(ready(ctx));
     if (!p || !rep) return DFL_E_STATE;
     if (p->solver < DFL_SOLVER_CG || p->solver > DFL_SOLVER_FGMRES) {
@@ -487,17 +489,20 @@ int dfl_solve(dfl_ctx *ctx, const dfl_solve_params *p, const double *b, double *
     const bool use_graph = !bicg && !multi(ctx) && !(ng && ng[0] == '1');
     KState bstate{};
     const bool dev_loop = !multi(ctx) && !(ng && ng[0] == '1');  // device-side Krylov loops (single rank)
-    if (p->solver == DFL_SOLVER_BICGSTAB2) {
-        if (dev_loop)
-            RC(bicg_solve_graph(ctx, p, bstate));
-        else
-            RC(bicg_solve_dev(ctx, p, bstate));
-        RC(lift_dev(ctx, p));
-    } else if (p->solver == DFL_SOLVER_GMRES || p->solver == DFL_SOLVER_FGMRES) {
-        RC(gmres_solve_dev(ctx, p, p->solver == DFL_SOLVER_FGMRES, bstate));
-        RC(lift_dev(ctx, p));
-    } else {
-        RC(cg_solve_dev(ctx, p, use_graph));
+    {
+        dfl::NvtxRange kr("dfl.solve.krylov");
+        if (p->solver == DFL_SOLVER_BICGSTAB2) {
+            if (dev_loop)
+                RC(bicg_solve_graph(ctx, p, bstate));
+            else
+                RC(bicg_solve_dev(ctx, p, bstate));
+            RC(lift_dev(ctx, p));
+        } else if (p->solver == DFL_SOLVER_GMRES || p->solver == DFL_SOLVER_FGMRES) {
+            RC(gmres_solve_dev(ctx, p, p->solver == DFL_SOLVER_FGMRES, bstate));
+            RC(lift_dev(ctx, p));
+        } else {
+            RC(cg_solve_dev(ctx, p, use_graph));
+        }
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(ctx->ev1, ctx->st));

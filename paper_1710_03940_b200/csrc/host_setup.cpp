@@ -491,6 +491,7 @@ int dfl_abi_version(void) { return DFLB200_ABI_VERSION; }
 const char *dfl_last_setup_error(void) { return dfl::setup_error(); }
 
 int dfl_hier_build(const dfl_csr *A, const dfl_amg_options *opts, dfl_hier **out) {
+    dfl::NvtxRange nv("dfl.setup.hierarchy");
     if (!A || !opts || !out) return DFL_E_STATE;
     *out = nullptr;
     if (A->nrows != A->ncols) {
@@ -566,6 +567,7 @@ void dfl_hier_free(dfl_hier *h) { delete h; }
 int dfl_basis_az(const dfl_csr *A, int32_t k, const double *zext, const int32_t *owner,
                  const int32_t *rowsub, int64_t K, int32_t sub0, int32_t nsub, int32_t keep_zeros,
                  dfl_matrix **AZ, double *E_rows) {
+    dfl::NvtxRange nv("dfl.setup.basis");
     if (!A || !zext || !owner || !rowsub || !AZ || !E_rows || k < 1) return DFL_E_STATE;
     auto *m = new dfl_matrix;
     int rc = dfl::basis_az(A, k, zext, owner, rowsub, K, sub0, nsub, keep_zeros, m->m, E_rows);

@@ -8,8 +8,18 @@
 #include <vector>
 
 #include "../../include/dflb200.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace dfl {
+
+// NVTX range for the phases of setup and solve (header-only NVTX 3: no cost
+// unless a profiler injects itself, nsys / ncu --nvtx show the ranges)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 struct Csr {
     int64_t nrows = 0, ncols = 0;
