@@ -350,7 +350,8 @@ def b200_arm(args, ws, rank, local):
             "achieved": gbs(op_fmt, op_ms), "peak": peak, "unit": "GB/s", "frac": gbs(op_fmt, op_ms) / peak,
             "traffic": traffic, "bytes_per_launch": op_fmt, "ms_per_launch": op_ms,
             "bytes_definition": "bytes the stored layout must move once: 1 class byte per row + x read once "
-                                "+ y written once + the k-1 Z columns read by the Z'y epilogue (DESIGN.md §4)",
+                                "+ y written once + the k-1 Z columns read by the Z'y epilogue, dictionary-coded: "
+                                "2 B per value + the tables (DESIGN.md §4)",
             "timing": "cold L2 (256 MB written before each launch), CUDA events around each launch; "
                       f"warm back-to-back: {op_warm_ms * 1e3:.1f} us",
             "peak_source": peak_src,

@@ -17,6 +17,7 @@ bool g_use_pcode = true;      // DFL_NO_PCODE=1: no delta/value-coded rows (P)
 bool g_no_sell = false;       // DFL_NO_SELL=1: long-row matrices as CSR-vector instead of SELL
 bool g_pdl = true;            // DFL_NO_PDL=1: plain launches instead of programmatic dependent launch
 bool g_nccl_graph = false;    // DFL_NCCL_GRAPH=1: several NCCL ranks replay the captured CG body
+bool g_use_zdict = true;      // DFL_NO_ZDICT=1: Z / AZ columns read dense instead of dictionary-coded
 int g_sm_count = 148;
 
 static int stage_in(dfl_ctx *ctx, double *dst, const double *src, int ptr_kind) {
@@ -102,6 +103,7 @@ int dfl_ctx_create(int device, dfl_ctx **out) {
         g_no_sell = on("DFL_NO_SELL");
         g_pdl = !on("DFL_NO_PDL");
         g_nccl_graph = on("DFL_NCCL_GRAPH");
+        g_use_zdict = !on("DFL_NO_ZDICT");
     }
     if (e != cudaSuccess) {
         dfl::set_setup_error(std::string("CUDA context creation failed: ") + cudaGetErrorString(e));
@@ -298,6 +300,45 @@ int dfl_ctx_add_hierarchy(dfl_ctx *ctx, int32_t sub, const dfl_hier *h) {
     return DFL_OK;
 }
 
+// Lossless dictionary coding of dense per-row columns (the Z and AZ columns
+// of the hot loop): every column's distinct values (by bit pattern) go to a
+// table, each row stores one uint16 index per column, `stride` indices per
+// row (row-major, one vector load).  Linear deflation on a grid has a few
+// hundred distinct values per column (coordinates repeat along the other
+// axes), so 2 bytes replace 8 per value.  Returns false (caller keeps the
+// dense columns) if a column has more than 65536 distinct values.
+static bool dict_code(const double *cols, int ncol, int64_t n, int stride, std::vector<uint16_t> &codes,
+                      std::vector<double> &tab, int *off) {
+    constexpr int kBits = 17;
+    constexpr uint64_t kSlots = 1ull << kBits;  // load factor <= 1/2 at 65536 values
+    codes.assign((size_t)n * stride, 0);
+    tab.clear();
+    std::vector<uint64_t> key(kSlots);
+    std::vector<int32_t> idx(kSlots);
+    for (int c = 0; c < ncol; ++c) {
+        off[c] = (int)tab.size();
+        std::fill(idx.begin(), idx.end(), -1);
+        int cnt = 0;
+        const double *col = cols + (size_t)c * n;
+        for (int64_t i = 0; i < n; ++i) {
+            uint64_t b;
+            std::memcpy(&b, col + i, 8);
+            uint64_t h = (b * 0x9E3779B97F4A7C15ull) >> (64 - kBits);
+            while (idx[h] >= 0 && key[h] != b) h = (h + 1) & (kSlots - 1);
+            if (idx[h] < 0) {
+                if (cnt == 65536) return false;
+                key[h] = b;
+                idx[h] = cnt++;
+                tab.push_back(col[i]);
+            }
+            codes[(size_t)i * stride + c] = (uint16_t)idx[h];
+        }
+    }
+    return true;
+}
+
+static int code_stride(int ncol) { return ncol <= 1 ? 1 : ncol <= 2 ? 2 : ncol <= 4 ? 4 : 8; }
+
 int dfl_ctx_set_deflation(dfl_ctx *ctx, int32_t k, const double *zcols, const dfl_csr *AZ, int64_t K,
                           const double *Einv, int32_t first_sub) {
     if (!ctx || !AZ || !Einv) return DFL_E_STATE;
@@ -351,6 +392,23 @@ int dfl_ctx_set_deflation(dfl_ctx *ctx, int32_t k, const double *zcols, const df
     ctx->az_nnz = AZ->row_ptr[n];
     ctx->ax_nnz = (int64_t)xcol.size();
     RC(upload(ctx, &ctx->azd, azd.data(), (int64_t)azd.size()));
+    ctx->zcode = nullptr;
+    ctx->acode = nullptr;
+    if (g_use_zdict && n > 0) {
+        std::vector<uint16_t> codes;
+        std::vector<double> tab;
+        if (k > 1 && dict_code(zc.data(), k - 1, n, code_stride(k - 1), codes, tab, ctx->ztab_off)) {
+            ctx->zs = code_stride(k - 1);
+            RC(upload(ctx, &ctx->zcode, codes.data(), (int64_t)codes.size()));
+            RC(upload(ctx, &ctx->ztab, tab.data(), (int64_t)tab.size()));
+            ctx->ztab_n = (int64_t)tab.size();
+        }
+        if (dict_code(azd.data(), k, n, code_stride(k), codes, tab, ctx->atab_off)) {
+            RC(upload(ctx, &ctx->acode, codes.data(), (int64_t)codes.size()));
+            RC(upload(ctx, &ctx->atab, tab.data(), (int64_t)tab.size()));
+            ctx->atab_n = (int64_t)tab.size();
+        }
+    }
     if (ctx->ax_nnz > 0) {
         RC(upload(ctx, &ctx->ax_ptr, xptr.data(), n + 1));
         RC(upload(ctx, &ctx->ax_col, xcol.data(), ctx->ax_nnz));
@@ -434,6 +492,11 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
     const int64_t dslots = std::max({ctx->nblk, vparts, kDotStride * std::max<int64_t>(ctx->nblk, 4 * ctx->sm_count)});
     RC(dalloc(ctx, &ctx->dpart, dslots + 64));
     RC(dalloc(ctx, &ctx->zt_part, (ctx->ntiles + ctx->nbtiles) * kKmax + 64));
+    // ~512 tiles per k_zt_finish block: enough blocks that the partial reads
+    // of a 10^6-row subdomain are spread over the GPU, few enough that the
+    // last block's chunk sum stays short
+    ctx->zt_chunks = (int)std::max<int64_t>(1, std::min<int64_t>(kZtMaxChunks, ctx->ntiles / std::max(1, ctx->nsub) / 512));
+    RC(dalloc(ctx, &ctx->zt_scratch, (int64_t)ctx->nsub * kKmax * kZtMaxChunks + 64));
     RC(dalloc(ctx, &ctx->scal, 16));
     RC(dalloc(ctx, &ctx->sgather, (int64_t)8 * ctx->nranks));
     RC(dalloc(ctx, &ctx->state, 1));

@@ -171,11 +171,9 @@ int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op, con
              int64_t extra_n) {
     const int64_t *sub_tiles = ctx->sub_tiles;
     if (!multi(ctx)) {
-        launch_k(ctx->st, k_zt_finish, ctx->nsub * ctx->k, 1024, 0, ctx->zt_part, sub_tiles, ctx->nsub, ctx->k,
-                                                             ctx->tvec, 0, ctx->inexact ? nullptr : ctx->Einv,
-                                                             ctx->K, ctx->t2, st, need_refresh, ctx->ticket,
-                                                             from_op && ctx->split ? ctx->sub_btiles : nullptr,
-                                                             ctx->ntiles);
+        launch_k(ctx->st, k_zt_finish, dim3(ctx->zt_chunks, ctx->nsub), 256, 0, ctx->zt_part, sub_tiles, ctx->nsub,
+                 ctx->k, ctx->tvec, 0, ctx->inexact ? nullptr : ctx->Einv, ctx->K, ctx->t2, st, need_refresh,
+                 ctx->ticket, ctx->zt_scratch, from_op && ctx->split ? ctx->sub_btiles : nullptr, ctx->ntiles);
         ctx->launches++;
         if (ctx->inexact) {
             launch_k(ctx->st, k_egmres, 1, 256, 0, ctx->Edense, (int)ctx->K, ctx->tvec, ctx->t2, ctx->coarse_tol,
@@ -188,10 +186,9 @@ int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op, con
     // rank-local p.w), allgather, unpack, solve
     const int64_t slot = (int64_t)ctx->max_nsub * ctx->k + 1;
     double *mine = ctx->tgather + (int64_t)ctx->rank * slot;
-    launch_k(ctx->st, k_zt_finish, ctx->nsub * ctx->k, 1024, 0, ctx->zt_part, sub_tiles, ctx->nsub, ctx->k, mine, 0,
-                                                         nullptr, ctx->K, nullptr, st, need_refresh, ctx->ticket,
-                                                         from_op && ctx->split ? ctx->sub_btiles : nullptr,
-                                                         ctx->ntiles);
+    launch_k(ctx->st, k_zt_finish, dim3(ctx->zt_chunks, ctx->nsub), 256, 0, ctx->zt_part, sub_tiles, ctx->nsub,
+             ctx->k, mine, 0, nullptr, ctx->K, nullptr, st, need_refresh, ctx->ticket, ctx->zt_scratch,
+             from_op && ctx->split ? ctx->sub_btiles : nullptr, ctx->ntiles);
     if (extra_part) {
         launch_k(ctx->st, k_reduce, 1, 1024, 0, extra_part, extra_n, mine + slot - 1);
         ctx->launches++;

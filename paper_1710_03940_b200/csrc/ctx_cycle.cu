@@ -72,6 +72,12 @@ int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *d
 int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double *b, bool zt,
                         const KState *st, int need_refresh) {
     OpArgs a{xin, b, y, ctx->zcols, ctx->n, zt ? ctx->k : 0, ctx->zt_part, st, need_refresh};
+    if (ctx->zcode) {
+        a.zcode = ctx->zcode;
+        a.ztab = ctx->ztab;
+        a.zs = ctx->zs;
+        for (int c = 0; c < kKmax; ++c) a.ztab_off[c] = ctx->ztab_off[c];
+    }
     if (!ctx->split) {
         RC(halo(ctx, xin));
         if (opmode == 0)
@@ -196,10 +202,20 @@ int dfl_ctx_time(dfl_ctx *ctx, int what_flags, int reps, double *ms, double *byt
     if ((what == 0 || what == 4) && fmt_bytes) {
         // the stored layout's bytes: each stored matrix byte once, x read once, y written once
         *bytes = mat(ctx->Aop) + 8.0 * (ctx->n + ctx->n_ghost) + 8.0 * ctx->n;
-        if (what == 4 && ctx->deflation) *bytes += 8.0 * (ctx->k - 1) * ctx->n;  // Z columns 1..k-1
+        if (what == 4 && ctx->deflation) {  // Z columns 1..k-1: dictionary indices + tables, or dense
+            *bytes += ctx->zcode ? 2.0 * ctx->zs * ctx->n + 8.0 * ctx->ztab_n : 8.0 * (ctx->k - 1) * ctx->n;
+        }
     } else if (what == 0 || what == 4) {
         *bytes = 12.0 * ctx->op_nnz + 4.0 * (ctx->n + 1) + 8.0 * (ctx->n + ctx->n_ghost) + 8.0 * ctx->n;
         if (what == 4 && ctx->deflation) *bytes += 8.0 * (ctx->k - 1) * ctx->n;  // Z columns 1..k-1
+    } else if (what == 5 && fmt_bytes) {
+        // w, p read, q written + the own-block AZ (dictionary indices + tables, or dense) + extras
+        *bytes = 24.0 * ctx->n;
+        if (ctx->deflation) {
+            const int ks = ctx->k <= 1 ? 1 : ctx->k <= 2 ? 2 : ctx->k <= 4 ? 4 : 8;
+            *bytes += ctx->acode ? 2.0 * ks * ctx->n + 8.0 * ctx->atab_n : 8.0 * ctx->k * ctx->n;
+            if (ctx->ax_nnz) *bytes += 12.0 * ctx->ax_nnz + 4.0 * (ctx->n + 1);
+        }
     } else if (what == 5) {
         // w, p read, q written + AZ (CSR fp64/int32, as uploaded)
         *bytes = 24.0 * ctx->n + (ctx->deflation ? 12.0 * ctx->az_nnz + 4.0 * (ctx->n + 1) : 0.0);

@@ -74,7 +74,7 @@ struct Nccl {
 extern Nccl g_nccl;
 
 // profiling / layout knobs (defined in ctx.cu, read at context creation)
-extern bool g_use_code, g_use_class, g_use_pcode, g_no_sell, g_pdl, g_nccl_graph;
+extern bool g_use_code, g_use_class, g_use_pcode, g_no_sell, g_pdl, g_nccl_graph, g_use_zdict;
 extern int g_sm_count;
 
 // ---------------------------------------------------------------------------
@@ -197,6 +197,15 @@ struct dfl_ctx {
     int first_sub = 0;
     double *zcols = nullptr;
     double *azd = nullptr;                  // own-block AZ values, k x n column-major
+    // dictionary-coded copies read by the hot loop (nullptr: > 65536 distinct values, dense)
+    uint16_t *zcode = nullptr;              // Z columns 1..k-1: zs uint16 per row
+    double *ztab = nullptr;
+    int ztab_off[kKmax] = {};
+    int zs = 0;
+    int64_t ztab_n = 0, atab_n = 0;         // table entries (all columns)
+    uint16_t *acode = nullptr;              // AZ own block: code_stride(k) uint16 per row
+    double *atab = nullptr;
+    int atab_off[kKmax] = {};
     int *ax_ptr = nullptr, *ax_col = nullptr;  // AZ entries outside the own block (nullptr: none)
     double *ax_val = nullptr;
     int64_t az_nnz = 0, ax_nnz = 0;
@@ -209,6 +218,8 @@ struct dfl_ctx {
     double coarse_tol = 1e-2;
     double *tvec = nullptr, *t2 = nullptr;
     double *zt_part = nullptr;
+    double *zt_scratch = nullptr;  // k_zt_finish chunk partials (nsub * zt_chunks * k)
+    int zt_chunks = 1;             // k_zt_finish blocks per subdomain
     double *tgather = nullptr;  // nranks * maxsub * k
     unsigned int *ticket = nullptr;
     cudaStream_t st_if = nullptr;  // capture stream of the refresh IF body
@@ -435,7 +446,12 @@ static void launch_op_nv(dfl_ctx *ctx, const OpArgs &a, unsigned grid) {
         static const int occ = occupancy(k_op_class<OPMODE, NV>);
         OpArgs b = a;
         b.pf = (int64_t)occ * g_sm_count * kBlock;  // next-wave L2 prefetch distance
-        launch_k(ctx->st, k_op_class<OPMODE, NV>, grid, kBlock, 0, A, ctx->tiles, S, b, *ctx->class_tabs[A.class_id]);
+        if (a.zcode && a.k > 1)
+            launch_k(ctx->st, k_op_class<OPMODE, NV, true>, grid, kBlock, 0, A, ctx->tiles, S, b,
+                     *ctx->class_tabs[A.class_id]);
+        else
+            launch_k(ctx->st, k_op_class<OPMODE, NV>, grid, kBlock, 0, A, ctx->tiles, S, b,
+                     *ctx->class_tabs[A.class_id]);
         return;
     }
     if (A.fmt == FMT_CODE) {
@@ -492,6 +508,9 @@ inline ProjArgs proj_args(dfl_ctx *ctx, const double *in, double *out, const KSt
         a.ax_ptr = ctx->ax_ptr;
         a.ax_col = ctx->ax_col;
         a.ax_val = ctx->ax_val;
+        a.acode = ctx->acode;
+        a.atab = ctx->atab;
+        for (int c = 0; c < kKmax; ++c) a.atab_off[c] = ctx->atab_off[c];
         a.sub_off = ctx->sub_off_d;
         a.nsub = ctx->nsub;
         a.k = ctx->k;

@@ -857,7 +857,32 @@ struct OpArgs {
     int need_refresh;       // 1: skip unless st->refresh_now
     const uint8_t *skip_rows = nullptr;  // halo overlap: rows with ghost columns are done later
     int64_t pf = 0;  // FMT_CLASS: L2 prefetch distance in rows (0: none)
+    // Z columns dictionary-coded (nullptr: dense zcols): zs uint16 per row,
+    // column q-1 of the row indexes ztab + ztab_off[q-1]
+    const uint16_t *zcode = nullptr;
+    const double *ztab = nullptr;
+    int zs = 0;
+    int ztab_off[kKmax] = {};
 };
+
+// the uint16 dictionary indices of row i (S per row: one vector load)
+__device__ __forceinline__ void load_codes(const uint16_t *codes, int S, int64_t i, uint32_t (&w)[4]) {
+    w[0] = w[1] = w[2] = w[3] = 0u;
+    if (S == 4) {
+        const uint2 v = __ldcs(reinterpret_cast<const uint2 *>(codes) + i);
+        w[0] = v.x, w[1] = v.y;
+    } else if (S == 8) {
+        const uint4 v = __ldcs(reinterpret_cast<const uint4 *>(codes) + i);
+        w[0] = v.x, w[1] = v.y, w[2] = v.z, w[3] = v.w;
+    } else if (S == 2) {
+        w[0] = __ldcs(reinterpret_cast<const unsigned int *>(codes) + i);
+    } else {
+        w[0] = __ldcs(reinterpret_cast<const unsigned short *>(codes) + i);
+    }
+}
+__device__ __forceinline__ int code_at(const uint32_t (&w)[4], int c) {
+    return (int)((w[c >> 1] >> ((c & 1) * 16)) & 0xffffu);
+}
 
 // Z'y partials of one tile: thread c < k writes column c (NV >= k, power of two)
 template <int NV>
@@ -868,9 +893,17 @@ __device__ __forceinline__ void op_zt(const OpArgs &a, int64_t i, bool valid, do
     for (int c = 0; c < NV; ++c) acc[c] = 0.0;
     if (valid) {
         acc[0] = y;
+        if (a.zcode) {
+            uint32_t w[4];
+            load_codes(a.zcode, a.zs, i, w);
 #pragma unroll
-        for (int c = 1; c < NV; ++c)
-            if (c < a.k) acc[c] = __ldg(a.zcols + (int64_t)(c - 1) * a.n + i) * y;
+            for (int c = 1; c < NV; ++c)
+                if (c < a.k) acc[c] = __ldg(a.ztab + a.ztab_off[c - 1] + code_at(w, c - 1)) * y;
+        } else {
+#pragma unroll
+            for (int c = 1; c < NV; ++c)
+                if (c < a.k) acc[c] = __ldg(a.zcols + (int64_t)(c - 1) * a.n + i) * y;
+        }
     }
     const double tot = block_sum_t<NV>(acc, sm);
     if ((int)threadIdx.x < a.k) a.zt_part[slot * a.k + threadIdx.x] = tot;
@@ -925,7 +958,7 @@ __global__ void __launch_bounds__(kBlock) k_op_code(DMat A, Tiles T, const __gri
 // leading gather edge x[i + lead]) are prefetched into L2 one wave ahead
 // (a.pf rows: the resident rows of the whole GPU), so the blocks of the next
 // wave find them there.
-template <int OPMODE, int NV>
+template <int OPMODE, int NV, bool ZC = false>
 __global__ void __launch_bounds__(kBlock, DFL_OPCLASS_MINB) k_op_class(DMat A, Tiles T, const __grid_constant__ SubTable S,
                                                                       OpArgs a, const __grid_constant__ ClassTab C) {
     DFL_PDL_ENTRY;
@@ -948,8 +981,13 @@ __global__ void __launch_bounds__(kBlock, DFL_OPCLASS_MINB) k_op_class(DMat A, T
     const int c = valid ? (int)__ldcs(A.cls + i) : 0;
     const double bi = (OPMODE == 1 && valid) ? __ldg(a.b + i) : 0.0;
     double z[NV];
+    uint32_t zw[4] = {0u, 0u, 0u, 0u};
+    if (ZC) {
+        if (valid && a.k > 1) load_codes(a.zcode, a.zs, i, zw);
+    } else {
 #pragma unroll
-    for (int q = 1; q < NV; ++q) z[q] = (valid && q < a.k) ? __ldcs(a.zcols + (int64_t)(q - 1) * a.n + i) : 0.0;
+        for (int q = 1; q < NV; ++q) z[q] = (valid && q < a.k) ? __ldcs(a.zcols + (int64_t)(q - 1) * a.n + i) : 0.0;
+    }
     double y = 0.0;
     if (valid) {
         const double ax = class_row(C, c, i, GatherX{a.x});
@@ -957,6 +995,11 @@ __global__ void __launch_bounds__(kBlock, DFL_OPCLASS_MINB) k_op_class(DMat A, T
         a.y[i] = y;
     }
     if (a.k > 0) {
+        if (ZC) {  // table entries: L1 hits (a few hundred values per column)
+#pragma unroll
+            for (int q = 1; q < NV; ++q)
+                z[q] = (valid && q < a.k) ? __ldg(a.ztab + a.ztab_off[q - 1] + code_at(zw, q - 1)) : 0.0;
+        }
         __shared__ double sm[32 * NV];
         double acc[NV];
         acc[0] = valid ? y : 0.0;
@@ -1040,61 +1083,80 @@ static __global__ void __launch_bounds__(kBlock) k_zt_vec(Tiles T, const double 
 }
 
 // Sum tile partials per local subdomain -> t (global coarse numbering at
-// first_col); one block per coarse value, fixed-order strided sums + tree.
-// The last block to finish (atomic ticket) then solves t2 = E^{-1} t with
-// the replicated inverse (Einv == nullptr: skip, multi-rank path).
-static __global__ void __launch_bounds__(1024) k_zt_finish(const double *__restrict__ zt_part,
+// first_col), then (Einv != nullptr) t2 = E^{-1} t with the replicated
+// inverse.  Grid (G, nsub): block (g, s) reads chunk g of subdomain s's tile
+// partials -- one contiguous, coalesced range of the row-major zt_part (tile
+// t, value c at t * k + c); thread i of the first (blockDim / k) * k always
+// sees value i % k -- reduces them per value with a fixed-shape tree and
+// writes scratch[(s * G + g) * k + c].  The last block (atomic ticket) adds
+// the chunks in chunk order (deterministic) and applies E^{-1}.
+constexpr int kZtMaxChunks = 64;
+static __global__ void __launch_bounds__(256) k_zt_finish(const double *__restrict__ zt_part,
                                                    const int64_t *__restrict__ sub_tiles, int nsub, int k,
                                                    double *t_out, int64_t first_col, const double *Einv,
                                                    int64_t K, double *t2, const KState *st, int need_refresh,
-                                                   unsigned int *ticket, const int64_t *sub_tiles2 = nullptr,
-                                                   int64_t toff2 = 0) {
+                                                   unsigned int *ticket, double *scratch,
+                                                   const int64_t *sub_tiles2 = nullptr, int64_t toff2 = 0) {
     DFL_PDL_ENTRY;
     if (skip(st)) return;
     if (need_refresh && !st->refresh_now) return;
-    const int v = blockIdx.x;
-    const int s = v / k, c = v % k;
-    const int64_t t0 = sub_tiles[s], t1 = sub_tiles[s + 1];
-    // four independent accumulators: the strided loads of a thread are in
-    // flight together instead of one L2 round trip per tile (fixed order:
-    // deterministic)
-    const int64_t bs = blockDim.x;
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    int64_t t = t0 + threadIdx.x;
-    for (; t + 3 * bs < t1; t += 4 * bs) {
-        a0 += zt_part[t * k + c];
-        a1 += zt_part[(t + bs) * k + c];
-        a2 += zt_part[(t + 2 * bs) * k + c];
-        a3 += zt_part[(t + 3 * bs) * k + c];
+    const int g = blockIdx.x, G = gridDim.x, s = blockIdx.y;
+    const int nt = (int)(blockDim.x / k) * k;
+    const int i = threadIdx.x;
+    __shared__ double sm[256];
+    double acc = 0.0;
+    if (i < nt) {
+        const int64_t t0 = sub_tiles[s], t1 = sub_tiles[s + 1];
+        const int64_t e0 = (t0 + (t1 - t0) * g / G) * k, e1 = (t0 + (t1 - t0) * (g + 1) / G) * k;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+        int64_t e = e0 + i;
+        for (; e + 3 * nt < e1; e += 4 * nt) {
+            a0 += zt_part[e];
+            a1 += zt_part[e + nt];
+            a2 += zt_part[e + 2 * nt];
+            a3 += zt_part[e + 3 * nt];
+        }
+        for (; e < e1; e += nt) a0 += zt_part[e];
+        acc = (a0 + a1) + (a2 + a3);
+        if (sub_tiles2 && g == G - 1)  // boundary-row tiles of the halo-overlapped operator
+            for (int64_t e2 = (toff2 + sub_tiles2[s]) * k + i; e2 < (toff2 + sub_tiles2[s + 1]) * k; e2 += nt)
+                acc += zt_part[e2];
     }
-    for (; t < t1; t += bs) a0 += zt_part[t * k + c];
-    double acc = (a0 + a1) + (a2 + a3);
-    if (sub_tiles2)  // boundary-row tiles of the halo-overlapped operator
-        for (int64_t t2i = toff2 + sub_tiles2[s] + threadIdx.x; t2i < toff2 + sub_tiles2[s + 1]; t2i += bs)
-            acc += zt_part[t2i * k + c];
-    __shared__ double sm[32];
-    double val[1] = {acc};
-    block_sum<1>(val, sm);
-    if (Einv == nullptr) {
-        if (threadIdx.x == 0) t_out[first_col + v] = val[0];
-        return;
+    sm[i] = acc;
+    __syncthreads();
+    for (int ng = nt / k; ng > 1;) {  // groups of k lanes, halved each step
+        const int half = (ng + 1) / 2;
+        if (i < (ng - half) * k) sm[i] += sm[i + half * k];
+        __syncthreads();
+        ng = half;
     }
     __shared__ bool last;
-    if (threadIdx.x == 0) {
-        t_out[first_col + v] = val[0];
+    if (i < k) scratch[((int64_t)s * G + g) * k + i] = sm[i];
+    __syncthreads();
+    if (i == 0) {
         __threadfence();
-        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        last = atomicAdd(ticket, 1u) == gridDim.x * gridDim.y - 1;
     }
     __syncthreads();
     if (!last) return;
     __threadfence();
-    const volatile double *tv = t_out;
-    for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
-        double a = 0.0;
-        for (int64_t j = 0; j < K; ++j) a = fma(Einv[i * K + j], tv[j], a);
-        t2[i] = a;
+    const volatile double *sc = scratch;
+    for (int v = i; v < nsub * k; v += blockDim.x) {
+        const int vs = v / k, vc = v % k;
+        double tot = 0.0;
+        for (int j = 0; j < G; ++j) tot += sc[((int64_t)vs * G + j) * k + vc];
+        t_out[first_col + v] = tot;
     }
-    if (threadIdx.x == 0) *ticket = 0u;
+    if (Einv != nullptr) {
+        __syncthreads();
+        const volatile double *tv = t_out;
+        for (int64_t r = i; r < K; r += blockDim.x) {
+            double a = 0.0;
+            for (int64_t j = 0; j < K; ++j) a = fma(Einv[r * K + j], tv[j], a);
+            t2[r] = a;
+        }
+    }
+    if (i == 0) *ticket = 0u;
 }
 
 // t2 = E^{-1} t (multi-rank path, after the allgather of t)
@@ -1120,6 +1182,9 @@ static __global__ void k_esolve(const double *Einv, int64_t K, const double *t, 
 // leaves it unchanged, so the result equals the CSR sum bit for bit.
 struct ProjArgs {
     const double *azd;     // k x n own-block values (nullptr: no deflation term)
+    const uint16_t *acode; // the same values dictionary-coded (code_stride(k) per row), nullptr: read azd
+    const double *atab;
+    int atab_off[kKmax];
     const int *ax_ptr;     // extras (n + 1 row pointer), nullptr: none
     const int *ax_col;
     const double *ax_val;
@@ -1146,9 +1211,17 @@ struct ProjArgs {
 template <int KZ>
 __device__ __forceinline__ double az_row(const ProjArgs &a, int64_t i) {
     double v[KZ];
+    if (a.acode) {
+        uint32_t w[4];
+        load_codes(a.acode, KZ, i, w);
 #pragma unroll
-    for (int c = 0; c < KZ; ++c)
-        if (c < a.k) v[c] = __ldcs(a.azd + (int64_t)c * a.n + i);
+        for (int c = 0; c < KZ; ++c)
+            if (c < a.k) v[c] = __ldg(a.atab + a.atab_off[c] + code_at(w, c));
+    } else {
+#pragma unroll
+        for (int c = 0; c < KZ; ++c)
+            if (c < a.k) v[c] = __ldcs(a.azd + (int64_t)c * a.n + i);
+    }
     int s = 0;
     if (a.nsub > 1) {  // subdomain of row i: last s with sub_off[s] <= i
         int lo = 0, hi = a.nsub - 1;
