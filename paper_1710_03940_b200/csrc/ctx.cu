@@ -120,7 +120,8 @@ void dfl_ctx_destroy(dfl_ctx *ctx) {
     if (ctx->st) cudaStreamSynchronize(ctx->st);
     if (ctx->loop_exec) cudaGraphExecDestroy(ctx->loop_exec);
     if (ctx->bg_exec) cudaGraphExecDestroy(ctx->bg_exec);
-    if (ctx->body_exec) cudaGraphExecDestroy(ctx->body_exec);
+    for (auto &e : ctx->body_exec)
+        if (e) cudaGraphExecDestroy(e);
     if (ctx->h_state2) cudaFreeHost(ctx->h_state2);
     for (cudaEvent_t e : ctx->ev_it)
         if (e) cudaEventDestroy(e);
@@ -358,6 +359,11 @@ int dfl_ctx_set_deflation(dfl_ctx *ctx, int32_t k, const double *zcols, const df
     ctx->rank_nsub.assign(ctx->nranks, 0);
     for (int q = 0; q < ctx->nranks; ++q) ctx->rank_nsub[q] = m / ctx->nranks + (q < m % ctx->nranks ? 1 : 0);
     ctx->max_nsub = *std::max_element(ctx->rank_nsub.begin(), ctx->rank_nsub.end());
+    {
+        std::vector<int64_t> rc(ctx->nranks);
+        for (int q = 0; q < ctx->nranks; ++q) rc[q] = (int64_t)ctx->rank_nsub[q] * k;
+        RC(upload(ctx, &ctx->rank_cnt_d, rc.data(), (int64_t)ctx->nranks));
+    }
     if (ctx->rank_nsub[ctx->rank] != ctx->nsub) {
         ctx->err = "rank owns " + std::to_string(ctx->nsub) + " subdomains, placement expects " +
                    std::to_string(ctx->rank_nsub[ctx->rank]);

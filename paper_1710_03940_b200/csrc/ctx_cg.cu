@@ -195,7 +195,10 @@ static int capture_refresh_if(dfl_ctx *ctx, bool deflated, cudaGraphConditionalH
     return DFL_OK;
 }
 
-static int cg_body(dfl_ctx *ctx, bool deflated, const CgGraph &G) {
+// refresh: -1 = decided on the device (IF node / predicated kernels), 0 / 1 =
+// the caller knows whether this iteration refreshes (host-driven loops:
+// iteration it refreshes iff (it + 1) % refresh_every == 0, krylov.py:128)
+static int cg_body(dfl_ctx *ctx, bool deflated, const CgGraph &G, int refresh = -1) {
     KState *st = ctx->state;
     const double *gath;
     const bool single = !multi(ctx);
@@ -206,15 +209,18 @@ static int cg_body(dfl_ctx *ctx, bool deflated, const CgGraph &G) {
         // so the rank's p.w rides in the Z'w allgather and the iteration needs
         // two collectives besides the halo (Z'w + p.w, then r.r + r.z).  A
         // separate dot pass measured faster than a fifth value slot in the
-        // operator kernel's epilogue (10.9 vs 11.2 ms, 1-rank NCCL, 150^3).
+        // operator kernel's epilogue (10.9 vs 11.2 ms, 1-rank NCCL, 150^3), and
+        // as fast as a warp-sum epilogue next to the Z'y tree (10.02 vs 9.98 ms)
         launch_k(ctx->st, k_dot, (unsigned)ctx->vgrid, kBlock, 0, (const double *)ctx->p, (const double *)ctx->w,
                  ctx->n, ctx->dpart, (const KState *)st);
         ctx->launches++;
-        RC(zt_to_t2(ctx, st, 0, true, ctx->dpart, ctx->vgrid));
-        const int64_t slot = (int64_t)ctx->max_nsub * ctx->k + 1;
-        launch_k(ctx->st, k_cg_pq_fold, 1, 32, 0, st, (const double *)ctx->tgather, ctx->nranks, slot,
-                 (const double *)ctx->tvec, (const double *)ctx->t2, ctx->K);
-        ctx->launches++;
+        RC(zt_to_t2(ctx, st, 0, true, ctx->dpart, ctx->vgrid, st));
+        if (ctx->inexact) {  // t2 from the inner GMRES: fold after it
+            const int64_t slot = (int64_t)ctx->max_nsub * ctx->k + 1;
+            launch_k(ctx->st, k_cg_pq_fold, 1, 32, 0, st, (const double *)ctx->tgather, ctx->nranks, slot,
+                     (const double *)ctx->tvec, (const double *)ctx->t2, ctx->K);
+            ctx->launches++;
+        }
         ProjArgs a = proj_args(ctx, ctx->w, ctx->w, st);
         launch_project<0>(ctx, a);
     } else {
@@ -229,25 +235,31 @@ static int cg_body(dfl_ctx *ctx, bool deflated, const CgGraph &G) {
         launch_k(ctx->st, k_cg_pq, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, gath, ctx->nranks, G.use_if, G.hif);
         ctx->launches++;
     }
-    // x += alpha p ; r -= alpha q (regular iterations)
+    // x += alpha p ; r -= alpha q (regular iterations); several ranks: the
+    // update's last block also sums r.r into the allgather slot
     launch_k(ctx->st, k_cg_update, (unsigned)ctx->vgrid, kBlock, 0, ctx->x, ctx->r, ctx->p, ctx->w, ctx->n,
-             ctx->dpart, st);
+             ctx->dpart, (const KState *)st, single ? nullptr : ctx->scal + 0, ctx->ticket + 1);
     ctx->launches++;
     // refresh iterations: r = b' - project(A x)   (krylov.py:128-129)
-    if (G.use_if)
+    if (refresh == 0) {
+    } else if (G.use_if) {
         RC(capture_refresh_if(ctx, deflated, G.hif));
-    else
+    } else {
         RC(cg_refresh(ctx, deflated, 1));
+    }
     int64_t np = 0;
     if (!single) {
         // one collective for r.r and r.z: the V-cycle runs before the
         // convergence test (its result is discarded on the last iteration)
-        launch_k(ctx->st, k_reduce, 1, 1024, 0, ctx->dpart, ctx->vgrid, ctx->scal + 0);
+        if (refresh != 0) {  // r.r of the refreshed residual (the update skipped its own)
+            launch_k(ctx->st, k_reduce, 1, 1024, 0, ctx->dpart, ctx->vgrid, ctx->scal + 0);
+            ctx->launches++;
+        }
         RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
         launch_k(ctx->st, k_reduce, 1, 1024, 0, ctx->dpart, np, ctx->scal + 1);
         RC(comm_allgather(ctx, ctx->scal, ctx->sgather, 8));
         launch_k(ctx->st, k_cg_rrz, 1, 32, 0, st, ctx->sgather, ctx->nranks);
-        ctx->launches += 3;
+        ctx->launches += 2;
     } else {
         launch_k(ctx->st, k_cg_rr, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, nullptr, 1);
         ctx->launches++;
@@ -306,28 +318,32 @@ static int build_loop_graph(dfl_ctx *ctx, bool deflated) {
     return DFL_OK;
 }
 
-// the CG body as a plain graph (several NCCL ranks: no conditional nodes)
+// the CG body as plain graphs (several NCCL ranks: no conditional nodes),
+// one without and one with the residual refresh
 static int build_body_graph(dfl_ctx *ctx, bool deflated) {
     const int key = deflated ? 1 : 0;
-    if (ctx->body_exec && ctx->body_key == key) return DFL_OK;
-    if (ctx->body_exec) {
-        cudaGraphExecDestroy(ctx->body_exec);
-        ctx->body_exec = nullptr;
-    }
+    if (ctx->body_exec[0] && ctx->body_key == key) return DFL_OK;
+    for (auto &e : ctx->body_exec)
+        if (e) {
+            cudaGraphExecDestroy(e);
+            e = nullptr;
+        }
     if (!ctx->h_state2) CK(cudaMallocHost(&ctx->h_state2, 2 * sizeof(KState)));
     for (int q = 0; q < 2; ++q)
         if (!ctx->ev_it[q]) CK(cudaEventCreateWithFlags(&ctx->ev_it[q], cudaEventDisableTiming));
-    CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
-    const int64_t before = ctx->launches;
-    int rc = cg_body(ctx, deflated, CgGraph{});
-    cudaGraph_t g = nullptr;
-    cudaError_t ce = cudaStreamEndCapture(ctx->st, &g);
-    if (rc != DFL_OK) return rc;
-    CK(ce);
-    ctx->body_graph_kernels = ctx->launches - before;
-    ctx->launches = before;
-    CK(cudaGraphInstantiate(&ctx->body_exec, g, 0));
-    cudaGraphDestroy(g);
+    for (int refresh = 0; refresh < 2; ++refresh) {
+        CK(cudaStreamBeginCapture(ctx->st, cudaStreamCaptureModeThreadLocal));
+        const int64_t before = ctx->launches;
+        int rc = cg_body(ctx, deflated, CgGraph{}, refresh);
+        cudaGraph_t g = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(ctx->st, &g);
+        if (rc != DFL_OK) return rc;
+        CK(ce);
+        ctx->body_graph_kernels[refresh] = ctx->launches - before;
+        ctx->launches = before;
+        CK(cudaGraphInstantiate(&ctx->body_exec[refresh], g, 0));
+        cudaGraphDestroy(g);
+    }
     ctx->body_key = key;
     return DFL_OK;
 }
@@ -390,10 +406,11 @@ int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
         // always has the next iteration queued.  The extra iteration after the
         // last one skips its updates (KState.done) on every rank alike.
         RC(build_body_graph(ctx, defl));
-        int64_t replays = 0;
+        const int R = std::max(1, p->refresh_every);
         for (int it = 0;; ++it) {
-            CK(cudaGraphLaunch(ctx->body_exec, ctx->st));
-            ++replays;
+            const int rf = (it + 1) % R == 0 ? 1 : 0;
+            CK(cudaGraphLaunch(ctx->body_exec[rf], ctx->st));
+            ctx->launches += ctx->body_graph_kernels[rf];
             CK(cudaMemcpyAsync(ctx->h_state2 + (it & 1), st, sizeof(KState), cudaMemcpyDeviceToHost, ctx->st));
             CK(cudaEventRecord(ctx->ev_it[it & 1], ctx->st));
             if (it > 0) {
@@ -401,7 +418,6 @@ int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
                 if (ctx->h_state2[(it - 1) & 1].done) break;
             }
         }
-        ctx->launches += ctx->body_graph_kernels * replays;
     } else {
         // several ranks: host-driven, but the host reads `done` one iteration
         // late, so iteration it+1 (kernels and collectives) is already queued
@@ -412,8 +428,9 @@ int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
         if (!ctx->h_state2) CK(cudaMallocHost(&ctx->h_state2, 2 * sizeof(KState)));
         for (int q = 0; q < 2; ++q)
             if (!ctx->ev_it[q]) CK(cudaEventCreateWithFlags(&ctx->ev_it[q], cudaEventDisableTiming));
+        const int R = std::max(1, p->refresh_every);
         for (int it = 0;; ++it) {
-            RC(cg_body(ctx, defl, CgGraph{}));
+            RC(cg_body(ctx, defl, CgGraph{}, (it + 1) % R == 0 ? 1 : 0));
             CK(cudaMemcpyAsync(ctx->h_state2 + (it & 1), st, sizeof(KState), cudaMemcpyDeviceToHost, ctx->st));
             CK(cudaEventRecord(ctx->ev_it[it & 1], ctx->st));
             if (it > 0) {

@@ -168,12 +168,13 @@ int halo(dfl_ctx *ctx, double *v, cudaStream_t xs) {
 
 // Z' v partials -> t (global numbering) -> t2 = E^-1 t on every rank
 int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op, const double *extra_part,
-             int64_t extra_n) {
+             int64_t extra_n, KState *fold) {
     const int64_t *sub_tiles = ctx->sub_tiles;
     if (!multi(ctx)) {
         launch_k(ctx->st, k_zt_finish, dim3(ctx->zt_chunks, ctx->nsub), 256, 0, ctx->zt_part, sub_tiles, ctx->nsub,
                  ctx->k, ctx->tvec, 0, ctx->inexact ? nullptr : ctx->Einv, ctx->K, ctx->t2, st, need_refresh,
-                 ctx->ticket, ctx->zt_scratch, from_op && ctx->split ? ctx->sub_btiles : nullptr, ctx->ntiles);
+                 ctx->ticket, ctx->zt_scratch, from_op && ctx->split ? ctx->sub_btiles : nullptr, ctx->ntiles,
+                 (const double *)nullptr, (int64_t)0, (double *)nullptr);
         ctx->launches++;
         if (ctx->inexact) {
             launch_k(ctx->st, k_egmres, 1, 256, 0, ctx->Edense, (int)ctx->K, ctx->tvec, ctx->t2, ctx->coarse_tol,
@@ -186,28 +187,23 @@ int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op, con
     // rank-local p.w), allgather, unpack, solve
     const int64_t slot = (int64_t)ctx->max_nsub * ctx->k + 1;
     double *mine = ctx->tgather + (int64_t)ctx->rank * slot;
+    // the finish kernel's last block also sums the caller's partials into the slot's last entry
     launch_k(ctx->st, k_zt_finish, dim3(ctx->zt_chunks, ctx->nsub), 256, 0, ctx->zt_part, sub_tiles, ctx->nsub,
              ctx->k, mine, 0, nullptr, ctx->K, nullptr, st, need_refresh, ctx->ticket, ctx->zt_scratch,
-             from_op && ctx->split ? ctx->sub_btiles : nullptr, ctx->ntiles);
-    if (extra_part) {
-        launch_k(ctx->st, k_reduce, 1, 1024, 0, extra_part, extra_n, mine + slot - 1);
+             from_op && ctx->split ? ctx->sub_btiles : nullptr, ctx->ntiles, extra_part, extra_n,
+             extra_part ? mine + slot - 1 : nullptr);
+    RC(comm_allgather(ctx, mine, ctx->tgather, slot));
+    // unpack the rank slots into t (rank q owns a contiguous subdomain range),
+    // t2 = E^-1 t and (CG) the folded p.q, in one single-block kernel
+    launch_k(ctx->st, k_unpack, 1, 256, 0, (const double *)ctx->tgather, ctx->nranks, slot,
+             (const int64_t *)ctx->rank_cnt_d, ctx->tvec, ctx->inexact ? nullptr : (const double *)ctx->Einv, ctx->K,
+             ctx->t2, st, need_refresh, ctx->inexact ? nullptr : fold);
+    ctx->launches += 2;
+    if (ctx->inexact) {
+        launch_k(ctx->st, k_egmres, 1, 256, 0, ctx->Edense, (int)ctx->K, ctx->tvec, ctx->t2, ctx->coarse_tol,
+                 ctx->egm_scr, st, need_refresh);
         ctx->launches++;
     }
-    RC(comm_allgather(ctx, mine, ctx->tgather, slot));
-    // unpack rank slots into t: rank q owns a contiguous subdomain range
-    int64_t pos = 0;
-    for (int q = 0; q < ctx->nranks; ++q) {
-        const int64_t cnt = (int64_t)ctx->rank_nsub[q] * ctx->k;
-        if (cnt > 0) CK(cudaMemcpyAsync(ctx->tvec + pos, ctx->tgather + q * slot, cnt * sizeof(double),
-                                        cudaMemcpyDeviceToDevice, ctx->st));
-        pos += cnt;
-    }
-    if (ctx->inexact)
-        launch_k(ctx->st, k_egmres, 1, 256, 0, ctx->Edense, (int)ctx->K, ctx->tvec, ctx->t2, ctx->coarse_tol, ctx->egm_scr,
-                                         st, need_refresh);
-    else
-        launch_k(ctx->st, k_esolve, 1, 256, 0, ctx->Einv, ctx->K, ctx->tvec, ctx->t2, st, need_refresh);
-    ctx->launches += 2;
     return DFL_OK;
 }
 

@@ -198,6 +198,7 @@ struct dfl_ctx {
     double *zcols = nullptr;
     double *azd = nullptr;                  // own-block AZ values, k x n column-major
     // dictionary-coded copies read by the hot loop (nullptr: > 65536 distinct values, dense)
+    int64_t *rank_cnt_d = nullptr;          // coarse values per rank (rank_nsub * k), device
     uint16_t *zcode = nullptr;              // Z columns 1..k-1: zs uint16 per row
     double *ztab = nullptr;
     int ztab_off[kKmax] = {};
@@ -252,9 +253,9 @@ struct dfl_ctx {
     int loop_key = -1;
     int64_t body_kernels = 0;
     // several NCCL ranks: the CG body replayed as a graph, done read one iteration late
-    cudaGraphExec_t body_exec = nullptr;
+    cudaGraphExec_t body_exec[2] = {nullptr, nullptr};  // [refresh iteration]
     int body_key = -1;
-    int64_t body_graph_kernels = 0;
+    int64_t body_graph_kernels[2] = {0, 0};
     KState *h_state2 = nullptr;  // pinned, 2
     cudaEvent_t ev_it[2] = {nullptr, nullptr};
     // BiCGStab(2) device loop (ctx_bicg.cu)
@@ -552,8 +553,10 @@ int build_tiles(dfl_ctx *ctx);
 // ctx_comm.cu
 int comm_allgather(dfl_ctx *ctx, const double *send, double *recv, size_t count);
 int halo(dfl_ctx *ctx, double *v, cudaStream_t xs = nullptr);
+// fold (several ranks, CG, exact E^-1): also pAp = p.w - t.E^-1 t and the alpha step
+// (the rank's p.w partials in extra_part)
 int zt_to_t2(dfl_ctx *ctx, const KState *st, int need_refresh, bool from_op, const double *extra_part = nullptr,
-             int64_t extra_n = 0);
+             int64_t extra_n = 0, KState *fold = nullptr);
 int rank_scalar(dfl_ctx *ctx, const double *part, int64_t nparts, int slot, const double **gath);
 // wait for a stream / event; with NCCL, poll the communicator's asynchronous
 // error and a timeout instead of blocking, abort the communicator on either

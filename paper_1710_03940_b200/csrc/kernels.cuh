@@ -1082,6 +1082,28 @@ static __global__ void __launch_bounds__(kBlock) k_zt_vec(Tiles T, const double 
             if (c < k) zt_part[t * k + c] = acc[c];
 }
 
+// deterministic sum of nparts partials (one block; read through L2: the
+// partials may come from other blocks of the calling kernel)
+__device__ __forceinline__ double reduce_parts(const double *part, int64_t nparts) {
+    __shared__ double sm[32];
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    const int64_t step = blockDim.x;
+    int64_t j = threadIdx.x;
+    for (; j + 3 * step < nparts; j += 4 * step) {
+        a0 += __ldcg(part + j);
+        a1 += __ldcg(part + j + step);
+        a2 += __ldcg(part + j + 2 * step);
+        a3 += __ldcg(part + j + 3 * step);
+    }
+    for (; j < nparts; j += step) a0 += __ldcg(part + j);
+    double v[1] = {(a0 + a1) + (a2 + a3)};
+    block_sum<1>(v, sm);
+    __shared__ double total;
+    if (threadIdx.x == 0) total = v[0];
+    __syncthreads();
+    return total;
+}
+
 // Sum tile partials per local subdomain -> t (global coarse numbering at
 // first_col), then (Einv != nullptr) t2 = E^{-1} t with the replicated
 // inverse.  Grid (G, nsub): block (g, s) reads chunk g of subdomain s's tile
@@ -1096,7 +1118,9 @@ static __global__ void __launch_bounds__(256) k_zt_finish(const double *__restri
                                                    double *t_out, int64_t first_col, const double *Einv,
                                                    int64_t K, double *t2, const KState *st, int need_refresh,
                                                    unsigned int *ticket, double *scratch,
-                                                   const int64_t *sub_tiles2 = nullptr, int64_t toff2 = 0) {
+                                                   const int64_t *sub_tiles2 = nullptr, int64_t toff2 = 0,
+                                                   const double *extra_part = nullptr, int64_t extra_n = 0,
+                                                   double *extra_out = nullptr) {
     DFL_PDL_ENTRY;
     if (skip(st)) return;
     if (need_refresh && !st->refresh_now) return;
@@ -1156,7 +1180,46 @@ static __global__ void __launch_bounds__(256) k_zt_finish(const double *__restri
             t2[r] = a;
         }
     }
+    if (extra_part != nullptr) {  // the caller's per-block partials (CG: rank-local p.w)
+        const double e = reduce_parts(extra_part, extra_n);
+        if (i == 0) *extra_out = e;
+    }
     if (i == 0) *ticket = 0u;
+}
+
+// several ranks: unpack the allgathered rank slots (tg + q * slot, cnt[q]
+// values each) into t, t2 = E^{-1} t (Einv != nullptr), and for deflated CG
+// (fold_st != nullptr) pAp = sum_q (p.w)_q - t . t2 in rank / index order (the
+// rank-local p.w rides in the last entry of every slot; A symmetric:
+// p'AZ t2 = (Z'Ap)' t2) followed by the alpha step.  One block.
+static __global__ void __launch_bounds__(256) k_unpack(const double *tg, int nranks, int64_t slot,
+                                                const int64_t *__restrict__ cnt, double *t, const double *Einv,
+                                                int64_t K, double *t2, const KState *st, int need_refresh,
+                                                KState *fold_st) {
+    DFL_PDL_ENTRY;
+    if (skip(st)) return;
+    if (need_refresh && !st->refresh_now) return;
+    int64_t pos = 0;
+    for (int q = 0; q < nranks; ++q) {
+        const int64_t c = cnt[q];
+        for (int64_t j = threadIdx.x; j < c; j += blockDim.x) t[pos + j] = tg[(int64_t)q * slot + j];
+        pos += c;
+    }
+    if (Einv == nullptr) return;
+    __syncthreads();
+    for (int64_t r = threadIdx.x; r < K; r += blockDim.x) {
+        double a = 0.0;
+        for (int64_t j = 0; j < K; ++j) a = fma(Einv[r * K + j], t[j], a);
+        t2[r] = a;
+    }
+    if (fold_st == nullptr) return;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    double pw = 0.0;
+    for (int q = 0; q < nranks; ++q) pw += tg[(int64_t)q * slot + slot - 1];
+    double tt = 0.0;
+    for (int64_t j = 0; j < K; ++j) tt += t[j] * t2[j];
+    cg_step_pq(fold_st, pw - tt);
 }
 
 // t2 = E^{-1} t (multi-rank path, after the allgather of t)
@@ -1303,27 +1366,6 @@ static __global__ void __launch_bounds__(kBlock) k_dot(const double *__restrict_
     if (threadIdx.x == 0) part[blockIdx.x] = v[0];
 }
 
-// deterministic sum of nparts partials -> out[slot]  (one block)
-__device__ __forceinline__ double reduce_parts(const double *part, int64_t nparts) {
-    __shared__ double sm[32];
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    const int64_t step = blockDim.x;
-    int64_t j = threadIdx.x;
-    for (; j + 3 * step < nparts; j += 4 * step) {
-        a0 += part[j];
-        a1 += part[j + step];
-        a2 += part[j + 2 * step];
-        a3 += part[j + 3 * step];
-    }
-    for (; j < nparts; j += step) a0 += part[j];
-    double v[1] = {(a0 + a1) + (a2 + a3)};
-    block_sum<1>(v, sm);
-    __shared__ double total;
-    if (threadIdx.x == 0) total = v[0];
-    __syncthreads();
-    return total;
-}
-
 // deterministic sum of part[0], part[ld], part[2 ld], ... (one block)
 __device__ __forceinline__ double reduce_parts_strided(const double *part, int64_t nparts, int ld) {
     __shared__ double sm[32];
@@ -1347,7 +1389,8 @@ static __global__ void k_reduce(const double *part, int64_t nparts, double *out)
 // On refresh iterations only x is updated here (r comes from the refresh path).
 static __global__ void __launch_bounds__(kBlock) k_cg_update(double *x, double *r, const double *__restrict__ p,
                                                       const double *__restrict__ q, int64_t n, double *part,
-                                                      const KState *st) {
+                                                      const KState *st, double *rr_out = nullptr,
+                                                      unsigned int *ticket = nullptr) {
     DFL_PDL_ENTRY;
     if (skip(st)) return;
     const double alpha = st->alpha;
@@ -1367,6 +1410,21 @@ static __global__ void __launch_bounds__(kBlock) k_cg_update(double *x, double *
         double v[1] = {dot};
         block_sum<1>(v, sm);
         dot_out(part, v[0]);
+        if (rr_out != nullptr) {  // several ranks: the last block sums the partials for the allgather
+            __shared__ bool last;
+            if (threadIdx.x == 0) {
+                __threadfence();
+                last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+            }
+            __syncthreads();
+            if (!last) return;
+            __threadfence();
+            const double rr = reduce_parts(part, gridDim.x);
+            if (threadIdx.x == 0) {
+                *rr_out = rr;
+                *ticket = 0u;
+            }
+        }
     }
 }
 
