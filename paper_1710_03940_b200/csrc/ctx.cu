@@ -403,8 +403,10 @@ int dfl_ctx_set_deflation(dfl_ctx *ctx, int32_t k, const double *zcols, const df
     if (g_use_zdict && n > 0) {
         std::vector<uint16_t> codes;
         std::vector<double> tab;
-        if (k > 1 && dict_code(zc.data(), k - 1, n, code_stride(k - 1), codes, tab, ctx->ztab_off)) {
-            ctx->zs = code_stride(k - 1);
+        // row stride code_stride(k) (the operator kernel's Z'y width NV: a
+        // compile-time stride there), columns 1..k-1 in its first k-1 slots
+        if (k > 1 && dict_code(zc.data(), k - 1, n, code_stride(k), codes, tab, ctx->ztab_off)) {
+            ctx->zs = code_stride(k);
             RC(upload(ctx, &ctx->zcode, codes.data(), (int64_t)codes.size()));
             RC(upload(ctx, &ctx->ztab, tab.data(), (int64_t)tab.size()));
             ctx->ztab_n = (int64_t)tab.size();

@@ -413,8 +413,13 @@ static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
     }
     if (A.fmt == FMT_CLASS) {
         static const int occ1 = occupancy(k_class1<MODE, DOT>);
+#ifdef DFL_NO_PF
+        const int64_t pf = 0;
+#else
+        const int64_t pf = (int64_t)occ1 * g_sm_count * kBlock;  // next-wave L2 prefetch distance
+#endif
         launch_k(ctx->st, k_class1<MODE, DOT>, (unsigned)class_grid<MODE, DOT>(A), kBlock, 0, A, a,
-                 *ctx->class_tabs[A.class_id], (int64_t)occ1 * g_sm_count * kBlock);
+                 *ctx->class_tabs[A.class_id], pf);
         ctx->launches++;
         return;
     }
@@ -447,6 +452,9 @@ static void launch_op_nv(dfl_ctx *ctx, const OpArgs &a, unsigned grid) {
         static const int occ = occupancy(k_op_class<OPMODE, NV>);
         OpArgs b = a;
         b.pf = (int64_t)occ * g_sm_count * kBlock;  // next-wave L2 prefetch distance
+#ifdef DFL_NO_PF
+        b.pf = 0;
+#endif
         if (a.zcode && a.k > 1)
             launch_k(ctx->st, k_op_class<OPMODE, NV, true>, grid, kBlock, 0, A, ctx->tiles, S, b,
                      *ctx->class_tabs[A.class_id]);

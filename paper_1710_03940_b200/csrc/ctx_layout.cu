@@ -115,7 +115,9 @@ static int try_upload_class(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) 
     int64_t best = -1;
     for (auto &kv : count)
         if (kv.second > best) best = kv.second, dom = kv.first;
-    const bool have_dom = dom.len <= 7;
+    // the masked dominant-row sum adds dval * 0.0 for absent entries: finite values only
+    bool have_dom = dom.len <= 7;
+    for (int k = 0; k < dom.len && have_dom; ++k) have_dom = std::isfinite(dom.v[k]);
     // pass 2: masks for subsets of the dominant row, generic classes for the rest
     std::unordered_map<Row, int, RH> dict;
     std::vector<Row> rows;

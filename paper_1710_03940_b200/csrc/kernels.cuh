@@ -128,12 +128,19 @@ __device__ __forceinline__ void prefetch_l2(const void *p) { asm volatile("prefe
 struct GatherX {
     const double *__restrict__ x;
     __device__ __forceinline__ double operator()(int c) const { return __ldg(x + c); }
+    // entry at row + d, the row's base address formed once by the caller
+    __device__ __forceinline__ double at(const GatherX &b, int d) const { return __ldg(b.x + d); }
+    __device__ __forceinline__ GatherX shift(int64_t row) const { return GatherX{x + row}; }
 };
 // relaxation applied on the fly: (w * r)[c]  (amg.py:193/195 then matvec)
 struct GatherWR {
     const double *__restrict__ w;
     const double *__restrict__ r;
     __device__ __forceinline__ double operator()(int c) const { return mul_rn(__ldg(w + c), __ldg(r + c)); }
+    __device__ __forceinline__ double at(const GatherWR &b, int d) const {
+        return mul_rn(__ldg(b.w + d), __ldg(b.r + d));
+    }
+    __device__ __forceinline__ GatherWR shift(int64_t row) const { return GatherWR{w + row, r + row}; }
 };
 
 // code table into shared memory (called by all threads of the block)
@@ -629,17 +636,22 @@ __device__ __forceinline__ double class_row_slow(const ClassTab &T, int c, int64
     return acc;
 }
 
+// Dominant-row path: absent entries load nothing and contribute
+// dval * 0.0 = +-0, which leaves the running sum unchanged bit for bit (the sum
+// starts at +0 and round-to-nearest never produces -0 from it), so the sum
+// equals the CSR sum over the present entries without a select per entry;
+// the host keeps the path only for finite dominant values.  Unused table
+// slots (k >= dlen) hold 0.
 template <class G>
 __device__ __forceinline__ double class_row(const ClassTab &T, int c, int64_t row, const G &g) {
     if (c & 0x80) {
+        const G gr = g.shift(row);
         double xv[7];
 #pragma unroll
-        for (int k = 0; k < 7; ++k)
-            if ((c >> k) & 1) xv[k] = g((int)(row + T.ddelta[k]));
+        for (int k = 0; k < 7; ++k) xv[k] = ((c >> k) & 1) ? g.at(gr, T.ddelta[k]) : 0.0;
         double acc = 0.0;
 #pragma unroll
-        for (int k = 0; k < 7; ++k)
-            if ((c >> k) & 1) acc = add_rn(acc, mul_rn(T.dval[k], xv[k]));
+        for (int k = 0; k < 7; ++k) acc = add_rn(acc, mul_rn(T.dval[k], xv[k]));
         return acc;
     }
     return class_row_slow(T, c, row, g);
@@ -983,7 +995,7 @@ __global__ void __launch_bounds__(kBlock, DFL_OPCLASS_MINB) k_op_class(DMat A, T
     double z[NV];
     uint32_t zw[4] = {0u, 0u, 0u, 0u};
     if (ZC) {
-        if (valid && a.k > 1) load_codes(a.zcode, a.zs, i, zw);
+        if (valid && a.k > 1) load_codes(a.zcode, NV, i, zw);  // stride NV (host: code_stride(k))
     } else {
 #pragma unroll
         for (int q = 1; q < NV; ++q) z[q] = (valid && q < a.k) ? __ldcs(a.zcols + (int64_t)(q - 1) * a.n + i) : 0.0;
