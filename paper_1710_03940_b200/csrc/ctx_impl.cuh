@@ -364,9 +364,9 @@ inline int64_t nblocks_for(const DMat &A) { return cdiv(A.nrows, rows_per_block(
 // resident blocks per SM of a kBlock-thread kernel (grid-stride grids are
 // sized to one full wave: a second partial wave would double the tail)
 template <class K>
-inline int occupancy(K kernel) {
+inline int occupancy(K kernel, int threads = kBlock) {
     int b = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, kBlock, 0) != cudaSuccess) b = 1;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, 0) != cudaSuccess) b = 1;
     return std::max(1, b);
 }
 
@@ -412,13 +412,13 @@ static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
         return;
     }
     if (A.fmt == FMT_CLASS) {
-        static const int occ1 = occupancy(k_class1<MODE, DOT>);
+        static const int occ1 = occupancy(k_class1<MODE, DOT>, kBlock / kOpRpt);
 #ifdef DFL_NO_PF
         const int64_t pf = 0;
 #else
         const int64_t pf = (int64_t)occ1 * g_sm_count * kBlock;  // next-wave L2 prefetch distance
 #endif
-        launch_k(ctx->st, k_class1<MODE, DOT>, (unsigned)class_grid<MODE, DOT>(A), kBlock, 0, A, a,
+        launch_k(ctx->st, k_class1<MODE, DOT>, (unsigned)class_grid<MODE, DOT>(A), kBlock / kOpRpt, 0, A, a,
                  *ctx->class_tabs[A.class_id], pf);
         ctx->launches++;
         return;
@@ -449,17 +449,17 @@ static void launch_op_nv(dfl_ctx *ctx, const OpArgs &a, unsigned grid) {
     const DMat &A = ctx->Aop;
     const SubTable &S = ctx->subtab;
     if (A.fmt == FMT_CLASS) {
-        static const int occ = occupancy(k_op_class<OPMODE, NV>);
+        static const int occ = occupancy(k_op_class<OPMODE, NV, false>, kBlock / kOpRpt);
         OpArgs b = a;
-        b.pf = (int64_t)occ * g_sm_count * kBlock;  // next-wave L2 prefetch distance
+        b.pf = (int64_t)occ * g_sm_count * kBlock;  // next-wave L2 prefetch distance (rows)
 #ifdef DFL_NO_PF
         b.pf = 0;
 #endif
         if (a.zcode && a.k > 1)
-            launch_k(ctx->st, k_op_class<OPMODE, NV, true>, grid, kBlock, 0, A, ctx->tiles, S, b,
+            launch_k(ctx->st, k_op_class<OPMODE, NV, true>, grid, kBlock / kOpRpt, 0, A, ctx->tiles, S, b,
                      *ctx->class_tabs[A.class_id]);
         else
-            launch_k(ctx->st, k_op_class<OPMODE, NV>, grid, kBlock, 0, A, ctx->tiles, S, b,
+            launch_k(ctx->st, k_op_class<OPMODE, NV, false>, grid, kBlock / kOpRpt, 0, A, ctx->tiles, S, b,
                      *ctx->class_tabs[A.class_id]);
         return;
     }

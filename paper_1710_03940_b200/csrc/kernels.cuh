@@ -515,9 +515,6 @@ struct Own {
 #ifndef DFL_ELL_MINB
 #define DFL_ELL_MINB 1
 #endif
-#ifndef DFL_OPCLASS_MINB
-#define DFL_OPCLASS_MINB 8
-#endif
 #ifndef DFL_ELL_MINB0
 #define DFL_ELL_MINB0 6
 #endif
@@ -657,23 +654,35 @@ __device__ __forceinline__ double class_row(const ClassTab &T, int c, int64_t ro
     return class_row_slow(T, c, row, g);
 }
 
-// FMT_CLASS row kernel (V-cycle stages), one row per thread and one block per
-// kBlock rows (the operator kernel's layout, k_op_class): the grid holds
-// every row, so 64 warps per SM cover the class byte -> gather chain; the
-// next wave's first DRAM touches (class byte, leading gather edge) are
-// prefetched into L2 (pf rows ahead).  Own-row operands are loaded before
-// the gathers.  DOT: one partial per block.
-template <int MODE, bool DOT>
-__global__ void __launch_bounds__(kBlock, DFL_OPCLASS_MINB) k_class1(DMat A, RowArgs a, const __grid_constant__ ClassTab T,
-                                                                    int64_t pf) {
+// rows per thread of the class-coded row kernels (k_class1, k_op_class) and
+// their resident blocks per SM (DFL_OPCLASS2_MINB: 16 x 128 threads)
+#ifndef DFL_OP_RPT
+#define DFL_OP_RPT 2
+#endif
+constexpr int kOpRpt = DFL_OP_RPT;
+#ifndef DFL_OPCLASS2_MINB
+#define DFL_OPCLASS2_MINB 16
+#endif
+
+// FMT_CLASS row kernel (V-cycle stages): one block per kBlock rows, RPT rows
+// per thread (rows i0, i0 + kBlock / RPT, ...; k_op_class's layout), so the
+// per-thread fixed cost is paid once per RPT rows and their loads are in
+// flight together; the next wave's first DRAM touches (class byte, leading
+// gather edge) are prefetched into L2 (pf rows ahead).  Own-row operands are
+// loaded before the gathers.  DOT: one partial per block.
+template <int MODE, bool DOT, int RPT = kOpRpt>
+__global__ void __launch_bounds__(kBlock / RPT, DFL_OPCLASS2_MINB) k_class1(DMat A, RowArgs a,
+                                                                           const __grid_constant__ ClassTab T,
+                                                                           int64_t pf) {
     DFL_PDL_ENTRY;
+    constexpr int TB = kBlock / RPT;
     constexpr bool kR = MODE != MODE_PLAIN || DOT;
     constexpr bool kPost = MODE == MODE_POST;
     const bool wr = MODE == MODE_RESID && a.x == nullptr;
     const int64_t n = A.nrows;
-    const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
+    const int64_t i0 = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     if (pf > 0) {
-        const int64_t ip = i + pf;
+        const int64_t ip = i0 + pf;
         if (ip < n) {
             prefetch_l2(A.cls + ip);
             const int64_t pe = min(ip + (int64_t)T.lead, A.ncols - 1);
@@ -681,23 +690,35 @@ __global__ void __launch_bounds__(kBlock, DFL_OPCLASS_MINB) k_class1(DMat A, Row
             if (wr) prefetch_l2(a.w + pe);
         }
     }
-    const bool valid = i < n;
-    const int c = valid ? (int)__ldcs(A.cls + i) : 0;
-    const double ri = (kR && valid) ? __ldg(a.r + i) : 0.0;
-    const double wi = (kPost && valid) ? __ldg(a.w + i) : 0.0;
-    const double xi = (kPost && valid) ? __ldg(a.xo + i) : 0.0;
-    double y = 0.0;
-    if (valid) {
-        const double ax = wr ? class_row(T, c, i, GatherWR{a.w, a.r}) : class_row(T, c, i, GatherX{a.x});
-        if (MODE == MODE_PLAIN) y = ax;
-        else if (MODE == MODE_RESID) y = sub_rn(ri, ax);
-        else if (MODE == MODE_POST) y = add_rn(xi, mul_rn(wi, sub_rn(ri, ax)));
-        else y = epilogue<MODE>(a, i, ax);
-        a.out[i] = y;
+    int c[RPT];
+    double ri[RPT], wi[RPT], xi[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+        const int64_t i = i0 + u * TB;
+        const bool valid = i < n;
+        c[u] = valid ? (int)__ldcs(A.cls + i) : 0;
+        ri[u] = (kR && valid) ? __ldg(a.r + i) : 0.0;
+        wi[u] = (kPost && valid) ? __ldg(a.w + i) : 0.0;
+        xi[u] = (kPost && valid) ? __ldg(a.xo + i) : 0.0;
+    }
+    double dot = 0.0;
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+        const int64_t i = i0 + u * TB;
+        if (i < n) {
+            const double ax = wr ? class_row(T, c[u], i, GatherWR{a.w, a.r}) : class_row(T, c[u], i, GatherX{a.x});
+            double y;
+            if (MODE == MODE_PLAIN) y = ax;
+            else if (MODE == MODE_RESID) y = sub_rn(ri[u], ax);
+            else if (MODE == MODE_POST) y = add_rn(xi[u], mul_rn(wi[u], sub_rn(ri[u], ax)));
+            else y = epilogue<MODE>(a, i, ax);
+            a.out[i] = y;
+            if (DOT) dot += ri[u] * y;
+        }
     }
     if (DOT) {
         __shared__ double sm[32];
-        double v[1] = {ri * y};
+        double v[1] = {dot};
         block_sum<1>(v, sm);
         dot_out(a.dot_part, v[0]);
     }
@@ -965,58 +986,74 @@ __global__ void __launch_bounds__(kBlock) k_op_code(DMat A, Tiles T, const __gri
     }
 }
 
-// One row per thread, one tile per block.  The chain of a row is class byte
-// -> table -> gathers; both DRAM first touches in it (the class byte and the
-// leading gather edge x[i + lead]) are prefetched into L2 one wave ahead
-// (a.pf rows: the resident rows of the whole GPU), so the blocks of the next
-// wave find them there.
-template <int OPMODE, int NV, bool ZC = false>
-__global__ void __launch_bounds__(kBlock, DFL_OPCLASS_MINB) k_op_class(DMat A, Tiles T, const __grid_constant__ SubTable S,
-                                                                      OpArgs a, const __grid_constant__ ClassTab C) {
+// FMT_CLASS operator: one kBlock-row tile per block, RPT rows per thread
+// (rows i0 and i0 + kBlock / RPT, ...).  The chain of a row is class byte ->
+// table -> gathers; the per-thread fixed cost (tile bounds, prefetch, the Z'y
+// tree: about half of the kernel's instructions at one row per thread) is
+// paid once per RPT rows, and the RPT rows' loads are in flight together.
+// The next wave's first DRAM touches (class byte, leading gather edge) are
+// prefetched into L2 (a.pf rows ahead).
+template <int OPMODE, int NV, bool ZC, int RPT = kOpRpt>
+__global__ void __launch_bounds__(kBlock / RPT, DFL_OPCLASS2_MINB) k_op_class(DMat A, Tiles T,
+                                                                              const __grid_constant__ SubTable S,
+                                                                              OpArgs a,
+                                                                              const __grid_constant__ ClassTab C) {
     DFL_PDL_ENTRY;
     if (a.need_refresh && !a.st->refresh_now) return;
+    constexpr int TB = kBlock / RPT;
     const int64_t t = blockIdx.x;
     int64_t r0, r1;
-    const int sub = tile_rows(S, T, t, r0, r1);
-    const int64_t i = r0 + threadIdx.x;
+    tile_rows(S, T, t, r0, r1);
+    const int64_t i0 = r0 + threadIdx.x;
     if (a.pf > 0) {
-        const int64_t ip = i + a.pf;
+        const int64_t ip = i0 + a.pf;
         if (ip < A.nrows) {
             prefetch_l2(A.cls + ip);
             prefetch_l2(a.x + min(ip + (int64_t)C.lead, A.ncols - 1));
         }
     }
-    const bool valid = i < r1 && !(a.skip_rows && a.skip_rows[i]);
-    // every load of the row that does not depend on its gathers goes out
-    // first: class byte, b, and the Z columns of the epilogue (a third of
-    // the kernel's DRAM bytes), so they overlap the class byte -> gather chain
-    const int c = valid ? (int)__ldcs(A.cls + i) : 0;
-    const double bi = (OPMODE == 1 && valid) ? __ldg(a.b + i) : 0.0;
-    double z[NV];
-    uint32_t zw[4] = {0u, 0u, 0u, 0u};
-    if (ZC) {
-        if (valid && a.k > 1) load_codes(a.zcode, NV, i, zw);  // stride NV (host: code_stride(k))
-    } else {
+    bool valid[RPT];
+    int c[RPT];
+    double bi[RPT];
+    uint32_t zw[RPT][4];
 #pragma unroll
-        for (int q = 1; q < NV; ++q) z[q] = (valid && q < a.k) ? __ldcs(a.zcols + (int64_t)(q - 1) * a.n + i) : 0.0;
+    for (int u = 0; u < RPT; ++u) {
+        const int64_t i = i0 + u * TB;
+        valid[u] = i < r1 && !(a.skip_rows && a.skip_rows[i]);
+        c[u] = valid[u] ? (int)__ldcs(A.cls + i) : 0;
+        bi[u] = (OPMODE == 1 && valid[u]) ? __ldg(a.b + i) : 0.0;
+        zw[u][0] = zw[u][1] = zw[u][2] = zw[u][3] = 0u;
+        if (ZC && valid[u] && a.k > 1) load_codes(a.zcode, NV, i, zw[u]);
     }
-    double y = 0.0;
-    if (valid) {
-        const double ax = class_row(C, c, i, GatherX{a.x});
-        y = OPMODE == 1 ? sub_rn(bi, ax) : ax;
-        a.y[i] = y;
+    double y[RPT];
+#pragma unroll
+    for (int u = 0; u < RPT; ++u) {
+        const int64_t i = i0 + u * TB;
+        y[u] = 0.0;
+        if (valid[u]) {
+            const double ax = class_row(C, c[u], i, GatherX{a.x});
+            y[u] = OPMODE == 1 ? sub_rn(bi[u], ax) : ax;
+            a.y[i] = y[u];
+        }
     }
     if (a.k > 0) {
-        if (ZC) {  // table entries: L1 hits (a few hundred values per column)
-#pragma unroll
-            for (int q = 1; q < NV; ++q)
-                z[q] = (valid && q < a.k) ? __ldg(a.ztab + a.ztab_off[q - 1] + code_at(zw, q - 1)) : 0.0;
-        }
         __shared__ double sm[32 * NV];
         double acc[NV];
-        acc[0] = valid ? y : 0.0;
 #pragma unroll
-        for (int q = 1; q < NV; ++q) acc[q] = z[q] * y;
+        for (int q = 0; q < NV; ++q) acc[q] = 0.0;
+#pragma unroll
+        for (int u = 0; u < RPT; ++u) {
+            const int64_t i = i0 + u * TB;
+            acc[0] += valid[u] ? y[u] : 0.0;
+#pragma unroll
+            for (int q = 1; q < NV; ++q) {
+                double z = 0.0;
+                if (valid[u] && q < a.k)
+                    z = ZC ? __ldg(a.ztab + a.ztab_off[q - 1] + code_at(zw[u], q - 1))
+                           : __ldcs(a.zcols + (int64_t)(q - 1) * a.n + i);
+                acc[q] += z * y[u];
+            }
+        }
         const double tot = block_sum_t<NV>(acc, sm);
         if ((int)threadIdx.x < a.k) a.zt_part[t * a.k + threadIdx.x] = tot;
     }
