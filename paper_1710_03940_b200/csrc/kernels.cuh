@@ -1361,8 +1361,13 @@ __device__ __forceinline__ double az_row(const ProjArgs &a, int64_t i) {
 }
 
 // q = w - AZ t2 (+ dot partial p.q);  refresh variant: r = b' - (w - AZ t2) (+ r.r)
+// 6 resident blocks (40 registers): 20.4 vs 22.1 us at the compiler's 48
+// registers / 5 blocks (150^3, k = 4); 8 blocks spill, and so does KZ = 8 at 6
+#ifndef DFL_PROJ_MINB
+#define DFL_PROJ_MINB 6
+#endif
 template <int MODE, int KZ>
-__global__ void __launch_bounds__(kBlock) k_project(ProjArgs a) {
+__global__ void __launch_bounds__(kBlock, KZ > 4 ? 4 : DFL_PROJ_MINB) k_project(ProjArgs a) {
     DFL_PDL_ENTRY;
     if (skip(a.st)) return;
     if (a.need_refresh == 1 && !a.st->refresh_now) return;
