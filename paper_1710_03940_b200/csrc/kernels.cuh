@@ -1271,19 +1271,6 @@ static __global__ void __launch_bounds__(256) k_unpack(const double *tg, int nra
     cg_step_pq(fold_st, pw - tt);
 }
 
-// t2 = E^{-1} t (multi-rank path, after the allgather of t)
-static __global__ void k_esolve(const double *Einv, int64_t K, const double *t, double *t2, const KState *st,
-                         int need_refresh) {
-    DFL_PDL_ENTRY;
-    if (skip(st)) return;
-    if (need_refresh && !st->refresh_now) return;
-    for (int64_t i = threadIdx.x; i < K; i += blockDim.x) {
-        double acc = 0.0;
-        for (int64_t j = 0; j < K; ++j) acc = fma(Einv[i * K + j], t[j], acc);
-        t2[i] = acc;
-    }
-}
-
 // AZ storage (deflation.py:140-149): row i of AZ has its entries in the k
 // columns of its own subdomain (always present: a_ii z_i) plus, on rows next
 // to another subdomain, a few in that subdomain's columns.  The own block is
