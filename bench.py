@@ -318,6 +318,9 @@ def b200_arm(args, ws, rank, local):
     op_warm_ms, _ = solver._ctx.time(4, 30)
     plain_ms, plain_alg = solver._ctx.time(0 | flush, 30)
     _, plain_fmt = solver._ctx.time(0 | fmtb, 1)
+    rs_ms, rs_alg = solver._ctx.time(6 | flush, 30)  # the V-cycle's largest kernel (L0 restriction)
+    _, rs_fmt = solver._ctx.time(6 | fmtb, 1)
+    rs_warm_ms, _ = solver._ctx.time(6, 30)
     vc_trials = [solver._ctx.time(3, 20) for _ in range(3)]
     vc_ms, vc_alg = min(vc_trials)
     _, vc_fmt = solver._ctx.time(2, 1)
@@ -368,6 +371,12 @@ def b200_arm(args, ws, rank, local):
                             "csr_bytes_per_cycle": vc_alg, "csr_frac": gbs(vc_alg, vc_ms) / peak,
                             "timing": "CUDA graph replay, best of 3 x 20 (trials %s ms)"
                                       % [round(t[0], 4) for t in vc_trials]},
+        "restriction_roofline": {
+            "kernel": "finest-level restriction t -> R t (sliced ELL, int32 + fp64), the largest single kernel "
+                      "of the V-cycle at 150^3",
+            "bytes_per_launch": rs_fmt, "ms_per_launch": rs_ms, "achieved": gbs(rs_fmt, rs_ms),
+            "frac": gbs(rs_fmt, rs_ms) / peak, "csr_bytes_per_launch": rs_alg,
+            "timing": f"cold L2, CUDA events around each launch; warm back-to-back: {rs_warm_ms * 1e3:.1f} us"},
         "vcycle_breakdown_us": {lab: round(ms * 1e3, 1) for lab, ms in solver._ctx.profile_vcycle(5)},
         "clocks": clk.summary(),
     }

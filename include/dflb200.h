@@ -313,12 +313,14 @@ DFL_API int dfl_spmv_csr(const dfl_csr *A, const double *x, double *y, int devic
  *         3 = V-cycle captured once and replayed as a CUDA graph, as inside
  *             the solve (bytes as 1),
  *         4 = operator SpMV with the fused Z'y tile partials (as in CG),
- *         5 = projection q = w - AZ t2 with the fused p.q partials
+ *         5 = projection q = w - AZ t2 with the fused p.q partials,
+ *         6 = the finest level's restriction t -> R t (group 0; the V-cycle's
+ *             largest single kernel at 150^3)
  *   flags or-ed into what:
  *     DFL_TIME_FLUSH_L2: cold L2 before every launch (a 256 MB buffer is
  *         written in between; each launch timed by its own event pair) --
- *         for 0 / 4 / 5, whose working set would otherwise fit in L2;
- *     DFL_TIME_FORMAT_BYTES: for 0 / 4, return the bytes the stored layout
+ *         for 0 / 4 / 5 / 6, whose working set would otherwise fit in L2;
+ *     DFL_TIME_FORMAT_BYTES: for 0 / 4 / 5 / 6, return the bytes the stored layout
  *         must move (each stored matrix byte once, each vector read once and
  *         written once) instead of the CSR algorithmic bytes */
 #define DFL_TIME_FLUSH_L2 0x100

@@ -186,6 +186,13 @@ int dfl_ctx_time(dfl_ctx *ctx, int what_flags, int reps, double *ms, double *byt
             launch_project<0>(ctx, a);
             return DFL_OK;
         }
+        if (what == 6 && !ctx->groups.empty() && !ctx->groups[0].lv.empty()) {
+            VGroup &g = ctx->groups[0];
+            double *next = g.lv.size() > 1 ? g.lv[1].rv : g.rb;
+            RowArgs b{g.lv[0].t, nullptr, nullptr, nullptr, next, nullptr, nullptr};
+            launch_rows<MODE_PLAIN, false>(ctx, g.lv[0].R, b);
+            return DFL_OK;
+        }
         ctx->err = "unknown timing target";
         return DFL_E_CONFIG;
     };
@@ -216,6 +223,16 @@ int dfl_ctx_time(dfl_ctx *ctx, int what_flags, int reps, double *ms, double *byt
             *bytes += ctx->acode ? 2.0 * ks * ctx->n + 8.0 * ctx->atab_n : 8.0 * ctx->k * ctx->n;
             if (ctx->ax_nnz) *bytes += 12.0 * ctx->ax_nnz + 4.0 * (ctx->n + 1);
         }
+    } else if (what == 6) {
+        if (ctx->groups.empty() || ctx->groups[0].lv.empty()) {
+            ctx->err = "no smoothing level to time";
+            return DFL_E_CONFIG;
+        }
+        const VGroup &g = ctx->groups[0];
+        const DMat &R = g.lv[0].R;
+        const double n = (double)g.rows[0], nc = (double)g.rows[1];
+        // t read once, R t written once, plus R itself
+        *bytes = (fmt_bytes ? mat(R) : 12.0 * (double)g.nnzP[0] + 4.0 * (nc + 1)) + 8.0 * n + 8.0 * nc;
     } else if (what == 5) {
         // w, p read, q written + AZ (CSR fp64/int32, as uploaded)
         *bytes = 24.0 * ctx->n + (ctx->deflation ? 12.0 * ctx->az_nnz + 4.0 * (ctx->n + 1) : 0.0);
@@ -248,6 +265,10 @@ int dfl_ctx_time(dfl_ctx *ctx, int what_flags, int reps, double *ms, double *byt
     launch_k(ctx->st, k_fill, (unsigned)cdiv(ctx->n + ctx->n_ghost, kBlock), kBlock, 0, ctx->p, 1.0, ctx->n + ctx->n_ghost);
     launch_k(ctx->st, k_fill, (unsigned)ctx->nblk, kBlock, 0, ctx->r, 1.0, ctx->n);
     launch_k(ctx->st, k_fill, (unsigned)ctx->nblk, kBlock, 0, ctx->w, 1.0, ctx->n);
+    if (what == 6) {
+        const VGroup &g = ctx->groups[0];
+        launch_k(ctx->st, k_fill, (unsigned)cdiv(g.rows[0], kBlock), kBlock, 0, g.lv[0].t, 1.0, g.rows[0]);
+    }
     if (what == 3) {  // the V-cycle as the solve runs it: captured once, replayed as a CUDA graph
         double b = 0;
         double tmp = 0;
