@@ -177,17 +177,42 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
     // the halo) go into a matrix of their own, Abnd (ELL / CSR, one row per
     // boundary slot), and are emptied in Aop, so the interior rows -- which
     // run while the halo is in flight -- keep the class-coded layout.
+    //
+    // Several subdomains in one context: the rows coupling to another
+    // subdomain have irregular column offsets under a box ordering (300^3 as
+    // 2x2x2 boxes), so the whole operator does not class-code; they take the
+    // same boundary pass (here with no halo), the rest stays class-coded.
     const char *no_ov = getenv("DFL_NO_OVERLAP");
-    const bool will_split = multi(ctx) && A->ncols > A->nrows && !(no_ov && no_ov[0] == '1');
+    const bool overlap_ok = !(no_ov && no_ov[0] == '1');
+    std::vector<int> rowsub((size_t)A->nrows);
+    for (int s = 0; s < nsub; ++s)
+        for (int64_t i = sub_offsets[s]; i < sub_offsets[s + 1]; ++i) rowsub[(size_t)i] = s;
+    bool cross_rule = false;  // boundary rows also = rows coupling to another subdomain
+    auto is_bnd = [&](int64_t i) {
+        const int s = rowsub[(size_t)i];
+        for (int64_t e = A->row_ptr[i]; e < A->row_ptr[i + 1]; ++e) {
+            const int64_t c = A->col_idx[e];
+            if (c >= A->nrows) return true;
+            if (cross_rule && (c < sub_offsets[s] || c >= sub_offsets[s + 1])) return true;
+        }
+        return false;
+    };
+    bool will_split = multi(ctx) && A->ncols > A->nrows && overlap_ok;
+    if (!will_split && nsub > 1 && overlap_ok && g_use_class) {
+        RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, nullptr, true, nullptr, nullptr, false, false, true));
+        if (ctx->Aop.fmt != FMT_CLASS) will_split = true;  // retry with the coupling rows apart
+    }
+    if (will_split && nsub > 1) cross_rule = true;
     std::vector<int64_t> ib_ptr, bb_ptr, bb_col;
     std::vector<double> bb_val;
-    if (will_split) {
+    bool split_done = false;
+    if (!will_split && nsub > 1 && overlap_ok && g_use_class) {
+        split_done = true;  // the operator as a whole is class-coded already (uploaded above)
+    } else if (will_split) {
         ib_ptr.assign(A->nrows + 1, 0);
         bb_ptr.assign(1, 0);
         for (int64_t i = 0; i < A->nrows; ++i) {
-            bool ghost = false;
-            for (int64_t e = A->row_ptr[i]; e < A->row_ptr[i + 1]; ++e) ghost = ghost || A->col_idx[e] >= A->nrows;
-            if (ghost) {
+            if (is_bnd(i)) {
                 for (int64_t e = A->row_ptr[i]; e < A->row_ptr[i + 1]; ++e) {
                     bb_col.push_back(A->col_idx[e]);
                     bb_val.push_back(A->values[e]);
@@ -212,7 +237,12 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
         const int64_t nb = (int64_t)bb_ptr.size() - 1;
         HostRows hb{nb, A->ncols, bb_ptr.data(), bb_col.data(), bb_val.data()};
         RC(upload_matrix(ctx, hb, ctx->Abnd, {0, nb}, nullptr, true, nullptr, nullptr, false, false, false));
-    } else {
+        if (!multi(ctx) && ctx->Aop.fmt != FMT_CLASS) {
+            // one context: the split only pays when the interior class-codes
+            will_split = false;
+            RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, nullptr, true, nullptr, nullptr, false, false, true));
+        }
+    } else if (!split_done) {
         RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, nullptr, true, nullptr, nullptr, false, false, true));
     }
     ctx->op_nnz = A->row_ptr[A->nrows] - A->row_ptr[0];
@@ -243,21 +273,20 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
         RC(upload(ctx, &ctx->send_idx, si.data(), ctx->nsend));
         RC(dalloc(ctx, &ctx->sendbuf, ctx->nsend));
     }
-    // rows with ghost columns (multi-rank only): second pass of the operator
+    // boundary rows (ghost columns; with several subdomains also the rows
+    // coupling to another one): second pass of the operator
     ctx->split = false;
-    if (multi(ctx) && ctx->n_ghost > 0 && !(getenv("DFL_NO_OVERLAP") && getenv("DFL_NO_OVERLAP")[0] == '1')) {
+    if (will_split) {
         std::vector<uint8_t> flag(ctx->n, 0);
         std::vector<int> rows, bs, bc;
         std::vector<int64_t> sbt{0};
         for (int s = 0; s < nsub; ++s) {
             const size_t first = rows.size();
             for (int64_t i = sub_offsets[s]; i < sub_offsets[s + 1]; ++i)
-                for (int64_t e = A->row_ptr[i]; e < A->row_ptr[i + 1]; ++e)
-                    if (A->col_idx[e] >= ctx->n) {
-                        flag[i] = 1;
-                        rows.push_back((int)i);
-                        break;
-                    }
+                if (is_bnd(i)) {
+                    flag[i] = 1;
+                    rows.push_back((int)i);
+                }
             for (size_t j = first; j < rows.size(); j += kBlock) {
                 bs.push_back((int)j);
                 bc.push_back((int)std::min<size_t>(kBlock, rows.size() - j));
@@ -419,6 +448,9 @@ int dfl_ctx_set_deflation(dfl_ctx *ctx, int32_t k, const double *zcols, const df
     }
     if (ctx->ax_nnz > 0) {
         RC(upload(ctx, &ctx->ax_ptr, xptr.data(), n + 1));
+        std::vector<uint8_t> xf((size_t)n, 0);
+        for (int64_t i = 0; i < n; ++i) xf[(size_t)i] = xptr[i + 1] > xptr[i] ? 1 : 0;
+        RC(upload(ctx, &ctx->ax_flag, xf.data(), n));
         RC(upload(ctx, &ctx->ax_col, xcol.data(), ctx->ax_nnz));
         RC(upload(ctx, &ctx->ax_val, xval.data(), ctx->ax_nnz));
     }

@@ -95,7 +95,7 @@ int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double 
         launch_op<0>(ctx, a);
     else
         launch_op<1>(ctx, a);
-    if (!ctx->fab) {
+    if (!ctx->fab && multi(ctx) && !ctx->nbr.empty()) {  // the exchange ran on st2
         CK(cudaEventRecord(ctx->ev_halo, ctx->st2));
         CK(cudaStreamWaitEvent(ctx->st, ctx->ev_halo, 0));
     }

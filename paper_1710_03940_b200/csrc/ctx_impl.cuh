@@ -208,6 +208,7 @@ struct dfl_ctx {
     double *atab = nullptr;
     int atab_off[kKmax] = {};
     int *ax_ptr = nullptr, *ax_col = nullptr;  // AZ entries outside the own block (nullptr: none)
+    uint8_t *ax_flag = nullptr;             // rows with such entries
     double *ax_val = nullptr;
     int64_t az_nnz = 0, ax_nnz = 0;
     int64_t *sub_off_d = nullptr;           // nsub + 1 local row offsets
@@ -515,6 +516,7 @@ inline ProjArgs proj_args(dfl_ctx *ctx, const double *in, double *out, const KSt
     if (ctx->deflation) {
         a.azd = ctx->azd;
         a.ax_ptr = ctx->ax_ptr;
+        a.ax_flag = ctx->ax_flag;
         a.ax_col = ctx->ax_col;
         a.ax_val = ctx->ax_val;
         a.acode = ctx->acode;

@@ -1285,6 +1285,7 @@ struct ProjArgs {
     const double *atab;
     int atab_off[kKmax];
     const int *ax_ptr;     // extras (n + 1 row pointer), nullptr: none
+    const uint8_t *ax_flag;  // 1 on the rows that have extras (read instead of ax_ptr on every row)
     const int *ax_col;
     const double *ax_val;
     const int64_t *sub_off;  // nsub + 1 local row offsets (device)
@@ -1308,7 +1309,7 @@ struct ProjArgs {
 // same k values: L1 broadcast), so no shared-memory staging and no barrier
 // stands in front of the streaming loads
 template <int KZ>
-__device__ __forceinline__ double az_row(const ProjArgs &a, int64_t i) {
+__device__ __forceinline__ double az_row(const ProjArgs &a, int64_t i, int s) {
     double v[KZ];
     if (a.acode) {
         uint32_t w[4];
@@ -1321,20 +1322,11 @@ __device__ __forceinline__ double az_row(const ProjArgs &a, int64_t i) {
         for (int c = 0; c < KZ; ++c)
             if (c < a.k) v[c] = __ldcs(a.azd + (int64_t)c * a.n + i);
     }
-    int s = 0;
-    if (a.nsub > 1) {  // subdomain of row i: last s with sub_off[s] <= i
-        int lo = 0, hi = a.nsub - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (__ldg(a.sub_off + mid) <= i) lo = mid; else hi = mid - 1;
-        }
-        s = lo;
-    }
     const double *t2o = a.t2 + a.own_base + (int64_t)s * a.k;
     const int64_t own0 = a.own_base + (int64_t)s * a.k;
     double acc = 0.0;
     int e = 0, e1 = 0;
-    if (a.ax_ptr) {
+    if (a.ax_ptr && __ldg(a.ax_flag + i)) {
         e = __ldg(a.ax_ptr + i);
         e1 = __ldg(a.ax_ptr + i + 1);
         for (; e < e1 && __ldg(a.ax_col + e) < own0; ++e)
@@ -1359,9 +1351,13 @@ __global__ void __launch_bounds__(kBlock, KZ > 4 ? 4 : DFL_PROJ_MINB) k_project(
     if (skip(a.st)) return;
     if (a.need_refresh == 1 && !a.st->refresh_now) return;
     double dot = 0.0;  // grid-stride (grid = ctx->vgrid): one partial per block
+    // subdomain of the thread's rows (increasing): a cursor over sub_off
+    int s = 0;
+    int64_t snext = a.nsub > 1 ? __ldg(a.sub_off + 1) : INT64_MAX;
     for (int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x; i < a.n; i += (int64_t)gridDim.x * kBlock) {
+        while (i >= snext) snext = (++s + 1 < a.nsub) ? __ldg(a.sub_off + s + 1) : INT64_MAX;
         double q = a.in[i];
-        if (a.azd) q = sub_rn(q, az_row<KZ>(a, i));
+        if (a.azd) q = sub_rn(q, az_row<KZ>(a, i, s));
         if (MODE == 1) q = sub_rn(__ldg(a.base + i), q);
         a.out[i] = q;
         if (a.dotmode == 1) dot += __ldg(a.dotv + i) * q;
