@@ -197,22 +197,32 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
         }
         return false;
     };
+    //
+    // Rows of rare classes (a matrix with more than kMaxClass distinct
+    // non-dominant rows, e.g. jump coefficients: 242 distinct rows, the 64
+    // most frequent cover 99.8% of them) take the boundary pass too.
     bool will_split = multi(ctx) && A->ncols > A->nrows && overlap_ok;
-    if (!will_split && nsub > 1 && overlap_ok && g_use_class) {
+    bool full_class = false, full_uploaded = false;
+    if (!will_split && overlap_ok && g_use_class) {
         RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, nullptr, true, nullptr, nullptr, false, false, true));
-        if (ctx->Aop.fmt != FMT_CLASS) will_split = true;  // retry with the coupling rows apart
+        full_uploaded = true;
+        full_class = ctx->Aop.fmt == FMT_CLASS;
+        if (!full_class && nsub > 1) will_split = true;  // retry with the coupling rows apart
     }
     if (will_split && nsub > 1) cross_rule = true;
+    std::vector<uint8_t> exc;
+    auto is_bnd2 = [&](int64_t i) { return (!exc.empty() && exc[(size_t)i]) || is_bnd(i); };
     std::vector<int64_t> ib_ptr, bb_ptr, bb_col;
     std::vector<double> bb_val;
-    bool split_done = false;
-    if (!will_split && nsub > 1 && overlap_ok && g_use_class) {
-        split_done = true;  // the operator as a whole is class-coded already (uploaded above)
-    } else if (will_split) {
+    // interior copy (boundary rows emptied: skipped by the interior pass) +
+    // the boundary rows' own matrix; true if the interior class-codes
+    auto build_split = [&](bool &interior_class) -> int {
         ib_ptr.assign(A->nrows + 1, 0);
         bb_ptr.assign(1, 0);
+        bb_col.clear();
+        bb_val.clear();
         for (int64_t i = 0; i < A->nrows; ++i) {
-            if (is_bnd(i)) {
+            if (is_bnd2(i)) {
                 for (int64_t e = A->row_ptr[i]; e < A->row_ptr[i + 1]; ++e) {
                     bb_col.push_back(A->col_idx[e]);
                     bb_val.push_back(A->values[e]);
@@ -223,7 +233,6 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
                 ib_ptr[i + 1] = ib_ptr[i] + (A->row_ptr[i + 1] - A->row_ptr[i]);
             }
         }
-        // interior copy: boundary rows empty (skipped by the interior pass)
         std::vector<int64_t> icol((size_t)ib_ptr[A->nrows]);
         std::vector<double> ival((size_t)ib_ptr[A->nrows]);
         for (int64_t i = 0, q = 0; i < A->nrows; ++i)
@@ -237,14 +246,33 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
         const int64_t nb = (int64_t)bb_ptr.size() - 1;
         HostRows hb{nb, A->ncols, bb_ptr.data(), bb_col.data(), bb_val.data()};
         RC(upload_matrix(ctx, hb, ctx->Abnd, {0, nb}, nullptr, true, nullptr, nullptr, false, false, false));
-        if (!multi(ctx) && ctx->Aop.fmt != FMT_CLASS) {
+        interior_class = ctx->Aop.fmt == FMT_CLASS;
+        return DFL_OK;
+    };
+    if (!full_class) {
+        bool interior_class = false;
+        if (will_split) RC(build_split(interior_class));
+        if (!interior_class && overlap_ok && g_use_class) {
+            // second attempt: the rows of rare classes into the boundary pass as well
+            exc = class_exceptions(h, [&](int64_t i) { return is_bnd(i); });
+            if (!exc.empty()) {
+                will_split = true;
+                RC(build_split(interior_class));
+            }
+        }
+        if (will_split && !multi(ctx) && !interior_class) {
             // one context: the split only pays when the interior class-codes
             will_split = false;
+            exc.clear();
+            RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, nullptr, true, nullptr, nullptr, false, false, true));
+        } else if (!will_split && !full_uploaded) {
             RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, nullptr, true, nullptr, nullptr, false, false, true));
         }
-    } else if (!split_done) {
-        RC(upload_matrix(ctx, h, ctx->Aop, ctx->sub_off, nullptr, true, nullptr, nullptr, false, false, true));
     }
+    if (getenv("DFL_SETUP_VERBOSE"))
+        fprintf(stderr, "dfl: operator fmt %d (class %d), split %d, exception rows %lld, boundary rows %lld\n",
+                ctx->Aop.fmt, (int)full_class, (int)will_split,
+                (long long)std::count(exc.begin(), exc.end(), (uint8_t)1), (long long)(bb_ptr.empty() ? 0 : bb_ptr.size() - 1));
     ctx->op_nnz = A->row_ptr[A->nrows] - A->row_ptr[0];
     int64_t nrecv = 0;
     ctx->nbr.clear();
@@ -283,7 +311,7 @@ int dfl_ctx_set_operator(dfl_ctx *ctx, const dfl_csr *A, int32_t nsub, const int
         for (int s = 0; s < nsub; ++s) {
             const size_t first = rows.size();
             for (int64_t i = sub_offsets[s]; i < sub_offsets[s + 1]; ++i)
-                if (is_bnd(i)) {
+                if (is_bnd2(i)) {
                     flag[i] = 1;
                     rows.push_back((int)i);
                 }

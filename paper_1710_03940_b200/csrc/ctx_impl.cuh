@@ -8,6 +8,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <functional>
 #include <condition_variable>
 #include <memory>
 #include <mutex>
@@ -558,6 +559,7 @@ int upload_matrix(dfl_ctx *ctx, const HostRows &h, DMat &m, const std::vector<in
                   const double *colscale = nullptr, DMat *scaled = nullptr, bool allow_sell = true,
                   bool allow_code = true, bool allow_class = true);
 int build_groups(dfl_ctx *ctx);
+std::vector<uint8_t> class_exceptions(const HostRows &h, const std::function<bool(int64_t)> &skip);
 int build_tiles(dfl_ctx *ctx);
 
 // ctx_comm.cu

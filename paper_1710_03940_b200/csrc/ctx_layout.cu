@@ -61,43 +61,115 @@ static int try_upload_code(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) {
     return DFL_OK;
 }
 
+// a row as (column - row, value bits) pairs, <= 8 entries
+struct ClsRow {
+    int len = 0;
+    int d[8];
+    uint64_t v[8];
+    bool operator==(const ClsRow &o) const {
+        if (len != o.len) return false;
+        for (int k = 0; k < len; ++k)
+            if (d[k] != o.d[k] || v[k] != o.v[k]) return false;
+        return true;
+    }
+};
+struct ClsRowHash {
+    size_t operator()(const ClsRow &r) const {
+        uint64_t x = (uint64_t)r.len * 0x9e3779b97f4a7c15ull;
+        for (int k = 0; k < r.len; ++k)
+            x = (x ^ ((uint64_t)(uint32_t)r.d[k] * 0x100000001b3ull) ^ r.v[k]) * 0xff51afd7ed558ccdull;
+        return (size_t)x;
+    }
+};
+// deterministic order for ties of the dominant row (hash-map order is not)
+static bool cls_row_less(const ClsRow &a, const ClsRow &b) {
+    if (a.len != b.len) return a.len < b.len;
+    for (int k = 0; k < a.len; ++k) {
+        if (a.d[k] != b.d[k]) return a.d[k] < b.d[k];
+        if (a.v[k] != b.v[k]) return a.v[k] < b.v[k];
+    }
+    return false;
+}
+static bool cls_row_of(const HostRows &h, int64_t i, ClsRow &r) {
+    const int64_t b = h.ptr[i], e = h.ptr[i + 1];
+    if (e - b > 8) return false;
+    r.len = (int)(e - b);
+    for (int64_t k = b; k < e; ++k) {
+        const int64_t d = h.col[k] - i;
+        if (d < INT32_MIN || d > INT32_MAX) return false;
+        r.d[k - b] = (int)d;
+        std::memcpy(&r.v[k - b], &h.val[k], 8);
+    }
+    return true;
+}
+
+// Rows that keep a matrix from class-coding only because it has more than
+// kMaxClass generic rows: with the dominant row (and its subsets) and the
+// kMaxClass most frequent other rows coded, the rows of the rarer ones are
+// flagged (1 per row) for the operator's boundary pass.  Rows with
+// skip(i) are ignored (they are in that pass already).  Empty result: not
+// needed (the rows fit), or hopeless (> 4096 distinct rows, long rows, or
+// more than 5% of the rows would be flagged).
+std::vector<uint8_t> class_exceptions(const HostRows &h, const std::function<bool(int64_t)> &skip) {
+    std::unordered_map<ClsRow, int64_t, ClsRowHash> count;
+    ClsRow r;
+    for (int64_t i = 0; i < h.nrows; ++i) {
+        if (skip(i)) continue;
+        if (!cls_row_of(h, i, r)) return {};
+        auto it = count.find(r);
+        if (it == count.end()) {
+            if (count.size() >= 4096) return {};
+            count.emplace(r, 1);
+        } else {
+            it->second++;
+        }
+    }
+    ClsRow dom;
+    int64_t best = -1;
+    for (auto &kv : count)
+        if (kv.second > best || (kv.second == best && cls_row_less(kv.first, dom))) best = kv.second, dom = kv.first;
+    bool have_dom = dom.len <= 7;
+    for (int k = 0; k < dom.len && have_dom; ++k) have_dom = std::isfinite(*reinterpret_cast<const double *>(&dom.v[k]));
+    auto subset = [&](const ClsRow &x) {
+        if (!have_dom) return false;
+        int k = 0;
+        for (int e = 0; e < x.len; ++e) {
+            while (k < dom.len && dom.d[k] != x.d[e]) ++k;
+            if (k == dom.len || dom.v[k] != x.v[e]) return false;
+            ++k;
+        }
+        return true;
+    };
+    std::vector<std::pair<int64_t, const ClsRow *>> gen;
+    for (auto &kv : count)
+        if (!subset(kv.first)) gen.emplace_back(kv.second, &kv.first);
+    if ((int)gen.size() <= kMaxClass) return {};
+    std::sort(gen.begin(), gen.end(), [](const auto &a, const auto &b) { return a.first > b.first; });
+    std::unordered_map<ClsRow, int, ClsRowHash> rare;
+    int64_t nrare = 0;
+    for (size_t q = kMaxClass; q < gen.size(); ++q) {
+        rare.emplace(*gen[q].second, 1);
+        nrare += gen[q].first;
+    }
+    if (nrare * 20 > h.nrows) return {};
+    std::vector<uint8_t> flag((size_t)h.nrows, 0);
+    for (int64_t i = 0; i < h.nrows; ++i) {
+        if (skip(i)) continue;
+        cls_row_of(h, i, r);
+        if (rare.count(r)) flag[(size_t)i] = 1;
+    }
+    return flag;
+}
+
 // FMT_CLASS encoder (kernels.cuh ClassTab): the dominant row (most frequent,
 // <= 7 entries) and its subsets as presence masks, <= kMaxClass generic
 // classes for the rest, every row <= 8 entries.  ok = false leaves m
 // untouched for the next format.
 static int try_upload_class(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) {
     ok = false;
-    struct Row {
-        int len = 0;
-        int d[8];
-        uint64_t v[8];
-        bool operator==(const Row &o) const {
-            if (len != o.len) return false;
-            for (int k = 0; k < len; ++k)
-                if (d[k] != o.d[k] || v[k] != o.v[k]) return false;
-            return true;
-        }
-    };
-    struct RH {
-        size_t operator()(const Row &r) const {
-            uint64_t x = (uint64_t)r.len * 0x9e3779b97f4a7c15ull;
-            for (int k = 0; k < r.len; ++k)
-                x = (x ^ ((uint64_t)(uint32_t)r.d[k] * 0x100000001b3ull) ^ r.v[k]) * 0xff51afd7ed558ccdull;
-            return (size_t)x;
-        }
-    };
-    auto row_of = [&](int64_t i, Row &r) -> bool {
-        const int64_t b = h.ptr[i], e = h.ptr[i + 1];
-        if (e - b > 8) return false;
-        r.len = (int)(e - b);
-        for (int64_t k = b; k < e; ++k) {
-            const int64_t d = h.col[k] - i;
-            if (d < INT32_MIN || d > INT32_MAX) return false;
-            r.d[k - b] = (int)d;
-            std::memcpy(&r.v[k - b], &h.val[k], 8);
-        }
-        return true;
-    };
+    auto row_of = [&](int64_t i, ClsRow &r) -> bool { return cls_row_of(h, i, r); };
+    using Row = ClsRow;
+    using RH = ClsRowHash;
     // pass 1: the dominant row (count distinct rows, give up beyond a bound)
     std::unordered_map<Row, int64_t, RH> count;
     Row r;
@@ -114,7 +186,7 @@ static int try_upload_class(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) 
     Row dom;
     int64_t best = -1;
     for (auto &kv : count)
-        if (kv.second > best) best = kv.second, dom = kv.first;
+        if (kv.second > best || (kv.second == best && cls_row_less(kv.first, dom))) best = kv.second, dom = kv.first;
     // the masked dominant-row sum adds dval * 0.0 for absent entries: finite values only
     bool have_dom = dom.len <= 7;
     for (int k = 0; k < dom.len && have_dom; ++k) have_dom = std::isfinite(dom.v[k]);
