@@ -201,7 +201,7 @@ int dfl_ctx_time(dfl_ctx *ctx, int what_flags, int reps, double *ms, double *byt
         const double rows = (double)M.nrows;
         if (M.fmt == FMT_CODE) return 8.0 * rows;
         if (M.fmt == FMT_CLASS) return 1.0 * rows;
-        if (M.fmt == FMT_PCODE) return 20.0 * rows;
+        if (M.fmt == FMT_PCODE) return (M.pc_wide ? 24.0 : 20.0) * rows;
         if (M.fmt == FMT_CSR) return 12.0 * (double)M.nnz + 4.0 * (rows + 1);
         return 12.0 * (double)M.stored + (M.perm ? 4.0 * rows : 0.0) +
                (M.ell_w ? 0.0 : 8.0 * (rows / 32 + 1));

@@ -409,7 +409,10 @@ template <int MODE, bool DOT>
 static void launch_rows(dfl_ctx *ctx, const DMat &A, const RowArgs &a) {
     if (A.nrows == 0) return;
     if (A.fmt == FMT_PCODE) {
-        launch_k(ctx->st, k_pcode<MODE, DOT>, (unsigned)cdiv(A.nrows, kBlock), kBlock, 0, A, a);
+        if (A.pc_wide)
+            launch_k(ctx->st, k_pcode<MODE, DOT, true>, (unsigned)cdiv(A.nrows, kBlock), kBlock, 0, A, a);
+        else
+            launch_k(ctx->st, k_pcode<MODE, DOT>, (unsigned)cdiv(A.nrows, kBlock), kBlock, 0, A, a);
         ctx->launches++;
         return;
     }

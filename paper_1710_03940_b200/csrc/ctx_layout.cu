@@ -260,11 +260,13 @@ static int try_upload_pcode(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) 
     std::unordered_map<uint64_t, int> dict;
     std::vector<double> tab;
     std::vector<int> c0(n, 0);
-    std::vector<uint32_t> d((size_t)3 * n, 0u), v(n, 0u);
+    std::vector<uint32_t> d((size_t)3 * n, 0u);
+    std::vector<uint8_t> code((size_t)n * kPcMaxLen, 0);
+    std::vector<uint8_t> len((size_t)n, 0);
     for (int64_t i = 0; i < n; ++i) {
         const int64_t b = h.ptr[i], e = h.ptr[i + 1];
         if (e - b > kPcMaxLen) return DFL_OK;
-        uint32_t w = (uint32_t)(e - b);
+        len[(size_t)i] = (uint8_t)(e - b);
         if (e > b) c0[i] = (int)h.col[b];
         for (int64_t k = b; k < e; ++k) {
             const int64_t j = k - b;
@@ -277,22 +279,36 @@ static int try_upload_pcode(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) 
             std::memcpy(&bits, &h.val[k], 8);
             auto it = dict.find(bits);
             if (it == dict.end()) {
-                if (dict.size() >= 16) return DFL_OK;
+                if (dict.size() >= 256) return DFL_OK;
                 it = dict.emplace(bits, (int)tab.size()).first;
                 tab.push_back(h.val[k]);
             }
-            w |= (uint32_t)it->second << (3 + 4 * j);
+            code[(size_t)i * kPcMaxLen + j] = (uint8_t)it->second;
         }
-        v[i] = w;
     }
-    tab.resize(16, 0.0);
+    // up to 16 values: 4-bit codes in one word; else 8-bit codes in two
+    const bool wide = tab.size() > 16;
+    std::vector<uint32_t> v((size_t)(wide ? 2 : 1) * n, 0u);
+    for (int64_t i = 0; i < n; ++i) {
+        const uint8_t *c = &code[(size_t)i * kPcMaxLen];
+        uint32_t w = len[(size_t)i], w2 = 0;
+        for (int j = 0; j < len[(size_t)i]; ++j) {
+            if (!wide) w |= (uint32_t)c[j] << (3 + 4 * j);
+            else if (j < 3) w |= (uint32_t)c[j] << (8 * (j + 1));
+            else w2 |= (uint32_t)c[j] << (8 * (j - 3));
+        }
+        v[(size_t)i] = w;
+        if (wide) v[(size_t)(n + i)] = w2;
+    }
+    tab.resize(wide ? 256 : 16, 0.0);
     int *d_c0;
     uint32_t *d_d, *d_v;
     double *d_tab;
     RC(upload(ctx, &d_c0, c0.data(), std::max<int64_t>(1, n)));
     RC(upload(ctx, &d_d, d.data(), std::max<int64_t>(1, 3 * n)));
-    RC(upload(ctx, &d_v, v.data(), std::max<int64_t>(1, n)));
-    RC(upload(ctx, &d_tab, tab.data(), 16));
+    RC(upload(ctx, &d_v, v.data(), std::max<int64_t>(1, (int64_t)v.size())));
+    RC(upload(ctx, &d_tab, tab.data(), (int64_t)tab.size()));
+    m.pc_wide = wide ? 1 : 0;
     m.fmt = FMT_PCODE;
     m.stored = m.nnz;
     m.pc_c0 = d_c0;

@@ -91,7 +91,8 @@ struct DMat {
     const int *pc_c0 = nullptr;          // first column of every row
     const uint32_t *pc_d = nullptr;      // 3 x nrows: 16-bit deltas of entries 1..6 (SoA)
     const uint32_t *pc_v = nullptr;      // length | 4-bit value codes << (3 + 4k)
-    const double *pc_tab = nullptr;      // 16 values
+    const double *pc_tab = nullptr;      // 16 values (wide: up to 256)
+    int pc_wide = 0;                     // 8-bit value codes: pc_v = len | c0..c2 << 8.., pc_v + n = c3..c6
     const int *ctab_delta = nullptr;     // column - row of each code
     const double *ctab_val = nullptr;    // value of each code
     int ncodes = 0;
@@ -724,26 +725,30 @@ __global__ void __launch_bounds__(kBlock / RPT, DFL_OPCLASS2_MINB) k_class1(DMat
     }
 }
 
-// FMT_PCODE row kernel: one row per thread
-template <int MODE, bool DOT>
+// FMT_PCODE row kernel: one row per thread.  WIDE: 8-bit value codes (a
+// second code word per row, the table of <= 256 values read through L1)
+template <int MODE, bool DOT, bool WIDE = false>
 __global__ void __launch_bounds__(kBlock) k_pcode(DMat A, RowArgs a) {
     DFL_PDL_ENTRY;
     __shared__ double tab[16];
     const int64_t i = (int64_t)blockIdx.x * kBlock + threadIdx.x;
     const bool valid = i < A.nrows;
     int c0 = 0;
-    uint32_t d0 = 0, d1 = 0, d2 = 0, vw = 0;
+    uint32_t d0 = 0, d1 = 0, d2 = 0, vw = 0, vw2 = 0;
     Own<MODE, DOT> own;
     if (valid) {
         own.load(a, i);
         c0 = __ldcs(A.pc_c0 + i);
         vw = __ldcs(A.pc_v + i);
+        if (WIDE) vw2 = __ldcs(A.pc_v + A.nrows + i);
         d0 = __ldcs(A.pc_d + i);
         d1 = __ldcs(A.pc_d + A.nrows + i);
         d2 = __ldcs(A.pc_d + 2 * A.nrows + i);
     }
-    if (threadIdx.x < 16) tab[threadIdx.x] = A.pc_tab[threadIdx.x];
-    __syncthreads();
+    if (!WIDE) {
+        if (threadIdx.x < 16) tab[threadIdx.x] = A.pc_tab[threadIdx.x];
+        __syncthreads();
+    }
     double dot = 0.0;
     if (valid) {
         const int len = (int)(vw & 7u);
@@ -759,7 +764,11 @@ __global__ void __launch_bounds__(kBlock) k_pcode(DMat A, RowArgs a) {
         double acc = 0.0;
 #pragma unroll
         for (int k = 0; k < kPcMaxLen; ++k)
-            if (k < len) acc = add_rn(acc, mul_rn(tab[(vw >> (3 + 4 * k)) & 0xfu], xv[k]));
+            if (k < len) {
+                const double vk = WIDE ? __ldg(A.pc_tab + ((k < 3 ? vw >> (8 * (k + 1)) : vw2 >> (8 * (k - 3))) & 0xffu))
+                                       : tab[(vw >> (3 + 4 * k)) & 0xfu];
+                acc = add_rn(acc, mul_rn(vk, xv[k]));
+            }
         const double y = own.apply(acc);
         a.out[i] = y;
         if (DOT) dot = own.r * y;
