@@ -61,6 +61,22 @@ def test_spmv_class_coded_bitwise(variant):
     assert np.array_equal(y, ref)
 
 
+@pytest.mark.parametrize("case", ["boxes_m8", "jump_m1", "jump_m8"])
+def test_operator_boundary_pass_bitwise(case):
+    """The operator with rows moved to the boundary pass in one context: the
+    rows coupling box-ordered subdomains (2x2x2 boxes) and the rows of rare
+    classes (jump coefficients) -- every row still summed in CSR order."""
+    kind = "poisson" if case == "boxes_m8" else "jump"
+    m = 8 if case.endswith("m8") else 1
+    edge = 24 if kind == "poisson" else 64  # rare classes stay under 5% of the rows from ~48^3 on
+    p = problems.make_problem((edge, edge, edge), problems.boxes_for(m), kind)
+    s = _solver(p, m, {"solver": {"type": "cg"}, "precond": {"relax": {"type": "spai0"}},
+                       "deflation": {"kind": "linear"}})
+    x = np.random.default_rng(5).standard_normal(p.matrix.nrows)
+    ref = port.spmv(port.Csr(p.matrix.nrows, p.matrix.ncols, p.matrix.row_ptr, p.matrix.col_idx, p.matrix.values), x)
+    assert np.array_equal(s.op(x), ref)
+
+
 @pytest.mark.parametrize("level", [0, 1])
 @pytest.mark.parametrize("which", ["P", "R"])
 def test_spmv_transfer_operators_coded_bitwise(level, which, monkeypatch):
