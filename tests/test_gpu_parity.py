@@ -99,6 +99,20 @@ def test_spmv_transfer_operators_coded_bitwise(level, which, monkeypatch):
         np.testing.assert_allclose(y, ref, rtol=1e-13, atol=1e-13 * np.abs(ref).max())
 
 
+def test_spmv_prolongation_wide_codes_bitwise():
+    """Jump coefficients: the level-0 prolongation has more than 16 distinct
+    values (config #4: 50), so FMT_PCODE carries 8-bit value codes -- still
+    the CSR order of spmv_rows, bit for bit."""
+    p = problems.jump3d(32)
+    A = nat.CsrArrays(p.matrix.nrows, p.matrix.ncols, p.matrix.row_ptr, p.matrix.col_idx, p.matrix.values)
+    h = nat.Hierarchy(A, nat.AmgOptions(0.08, 2 / 3, 0.8, nat.DFL_RELAX["damped_jacobi"], 25, 500))
+    nr, nc, ptr, col, val = h.matrix(0, nat.LEVEL_P)
+    assert 16 < len(np.unique(val)) <= 256
+    P = nat.CsrArrays(nr, nc, ptr, col, val)
+    x = np.random.default_rng(12).standard_normal(nc)
+    assert np.array_equal(nat.spmv_device(P, x), port.spmv(port.Csr(nr, nc, ptr, col, val), x))
+
+
 def test_spmv_random_csr():
     rng = np.random.default_rng(3)
     n = 3000
