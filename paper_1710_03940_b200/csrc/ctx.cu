@@ -119,6 +119,7 @@ void dfl_ctx_destroy(dfl_ctx *ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->st) cudaStreamSynchronize(ctx->st);
     if (ctx->loop_exec) cudaGraphExecDestroy(ctx->loop_exec);
+    if (ctx->solve_exec) cudaGraphExecDestroy(ctx->solve_exec);
     if (ctx->bg_exec) cudaGraphExecDestroy(ctx->bg_exec);
     for (auto &e : ctx->body_exec)
         if (e) cudaGraphExecDestroy(e);

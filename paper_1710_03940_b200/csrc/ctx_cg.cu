@@ -278,46 +278,6 @@ static int cg_body(dfl_ctx *ctx, bool deflated, const CgGraph &G, int refresh = 
     return DFL_OK;
 }
 
-static int build_loop_graph(dfl_ctx *ctx, bool deflated) {
-    const int key = deflated ? 1 : 0;
-    if (ctx->loop_exec && ctx->loop_key == key) return DFL_OK;
-    if (ctx->loop_exec) {
-        cudaGraphExecDestroy(ctx->loop_exec);
-        ctx->loop_exec = nullptr;
-    }
-    cudaGraph_t g;
-    CK(cudaGraphCreate(&g, 0));
-    cudaGraphConditionalHandle h;
-    CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = h;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t node;
-    CK(cudaGraphAddNode(&node, g, nullptr, 0, &cp));
-    cudaGraph_t body = cp.conditional.phGraph_out[0];
-    CgGraph G;
-    G.use_cond = 1;
-    G.h = h;
-    const char *ni = getenv("DFL_NO_IF");
-    G.use_if = !(ni && ni[0] == '1');
-    if (G.use_if) CK(cudaGraphConditionalHandleCreate(&G.hif, body, 0, 0));
-    CK(cudaStreamBeginCaptureToGraph(ctx->st, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-    const int64_t before = ctx->launches;
-    int rc = cg_body(ctx, deflated, G);
-    cudaGraph_t captured = nullptr;
-    cudaError_t ce = cudaStreamEndCapture(ctx->st, &captured);
-    if (rc != DFL_OK) return rc;
-    CK(ce);
-    ctx->body_kernels = ctx->launches - before;
-    ctx->launches = before;
-    CK(cudaGraphInstantiate(&ctx->loop_exec, g, 0));
-    cudaGraphDestroy(g);
-    ctx->loop_key = key;
-    return DFL_OK;
-}
-
 // the CG body as plain graphs (several NCCL ranks: no conditional nodes),
 // one without and one with the residual refresh
 static int build_body_graph(dfl_ctx *ctx, bool deflated) {
@@ -350,7 +310,8 @@ static int build_body_graph(dfl_ctx *ctx, bool deflated) {
 
 // ---------------------------------------------------------------------------
 // the whole solve on the device: b, x in ctx->b / ctx->xin
-int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
+// x = 0, ||b||, b' = project(b), r, z = M r, p = z (krylov.py:101-117)
+static int cg_prologue(dfl_ctx *ctx, const dfl_solve_params *p) {
     KState *st = ctx->state;
     const bool defl = p->deflated != 0;
     const double *gath;
@@ -396,11 +357,94 @@ int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
     launch_k(ctx->st, k_cg_init_rz, 1, 1024, 0, st, ctx->dpart, np, gath, ctx->nranks);
     launch_k(ctx->st, k_copy, (unsigned)ctx->nblk, kBlock, 0, ctx->p, ctx->z, ctx->n);
     ctx->launches += 2;
-    // the loop
+    return DFL_OK;
+}
+
+// The whole single-rank solve as one CUDA graph: the prologue kernels, the
+// while-conditional node with the CG body (refresh IF node inside), and the
+// lift -- one launch per solve instead of ~45 host launches around the loop
+// graph.  Cached per (deflated, x0, tol, maxiter, refresh): k_cg_start bakes
+// them in.
+static int build_solve_graph(dfl_ctx *ctx, const dfl_solve_params *p) {
+    const bool defl = p->deflated != 0;
+    char key[160];
+    snprintf(key, sizeof key, "%d/%d/%.17g/%d/%d", (int)defl, (int)use_x0(ctx, p), p->tol, p->maxiter,
+             std::max(1, p->refresh_every));
+    if (ctx->solve_exec && ctx->solve_key == key) return DFL_OK;
+    if (ctx->solve_exec) {
+        cudaGraphExecDestroy(ctx->solve_exec);
+        ctx->solve_exec = nullptr;
+    }
+    if (!ctx->st_body) CK(cudaStreamCreateWithFlags(&ctx->st_body, cudaStreamNonBlocking));
+    cudaGraph_t g;
+    CK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    CK(cudaStreamBeginCaptureToGraph(ctx->st, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+    const int64_t before = ctx->launches;
+    int rc = cg_prologue(ctx, p);
+    cudaGraph_t body = nullptr;
+    if (rc == DFL_OK) {
+        cudaStreamCaptureStatus cs;
+        cudaGraph_t capg = nullptr;
+        const cudaGraphNode_t *deps = nullptr;
+        size_t nd = 0;
+        CK(cudaStreamGetCaptureInfo(ctx->st, &cs, nullptr, &capg, &deps, &nd));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t wnode;
+        CK(cudaGraphAddNode(&wnode, capg, deps, nd, &cp));
+        CK(cudaStreamUpdateCaptureDependencies(ctx->st, &wnode, 1, cudaStreamSetCaptureDependencies));
+        body = cp.conditional.phGraph_out[0];
+        CgGraph G;
+        G.use_cond = 1;
+        G.h = h;
+        const char *ni = getenv("DFL_NO_IF");
+        G.use_if = !(ni && ni[0] == '1');
+        if (G.use_if) CK(cudaGraphConditionalHandleCreate(&G.hif, body, 0, 0));
+        CK(cudaStreamBeginCaptureToGraph(ctx->st_body, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        cudaStream_t main = ctx->st;
+        ctx->st = ctx->st_body;
+        const int64_t b0 = ctx->launches;
+        rc = cg_body(ctx, defl, G);
+        ctx->body_kernels = ctx->launches - b0;
+        ctx->launches = b0;
+        ctx->st = main;
+        cudaGraph_t bg = nullptr;
+        const cudaError_t be = cudaStreamEndCapture(ctx->st_body, &bg);
+        if (rc == DFL_OK && be != cudaSuccess) rc = DFL_E_CUDA;
+        if (rc == DFL_OK) rc = lift_dev(ctx, p);
+    }
+    cudaGraph_t captured = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(ctx->st, &captured);
+    ctx->solve_fixed_kernels = ctx->launches - before;
+    ctx->launches = before;
+    if (rc != DFL_OK) {
+        cudaGraphDestroy(g);
+        return rc;
+    }
+    CK(ce);
+    CK(cudaGraphInstantiate(&ctx->solve_exec, g, 0));
+    cudaGraphDestroy(g);
+    ctx->solve_key = key;
+    return DFL_OK;
+}
+
+int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph) {
+    KState *st = ctx->state;
+    const bool defl = p->deflated != 0;
     if (use_graph) {
-        RC(build_loop_graph(ctx, defl));
-        CK(cudaGraphLaunch(ctx->loop_exec, ctx->st));
-    } else if (ctx->comm && g_nccl_graph) {
+        RC(build_solve_graph(ctx, p));
+        CK(cudaGraphLaunch(ctx->solve_exec, ctx->st));
+        ctx->launches += ctx->solve_fixed_kernels;
+        return DFL_OK;
+    }
+    RC(cg_prologue(ctx, p));
+    // the loop
+    if (ctx->comm && g_nccl_graph) {
         // NCCL ranks: the body (collectives included) captured once and replayed
         // per iteration; the host reads `done` one iteration late, so the GPU
         // always has the next iteration queued.  The extra iteration after the

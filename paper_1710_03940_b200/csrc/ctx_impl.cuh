@@ -253,6 +253,11 @@ struct dfl_ctx {
     // graph
     cudaGraphExec_t loop_exec = nullptr;
     int loop_key = -1;
+    // the whole single-rank CG solve (prologue, while loop, lift) as one graph
+    cudaGraphExec_t solve_exec = nullptr;
+    std::string solve_key;
+    int64_t solve_fixed_kernels = 0;
+    cudaStream_t st_body = nullptr;  // capture stream of the while body
     int64_t body_kernels = 0;
     // several NCCL ranks: the CG body replayed as a graph, done read one iteration late
     cudaGraphExec_t body_exec[2] = {nullptr, nullptr};  // [refresh iteration]
