@@ -189,7 +189,11 @@ static int try_upload_class(dfl_ctx *ctx, const HostRows &h, DMat &m, bool &ok) 
         if (kv.second > best || (kv.second == best && cls_row_less(kv.first, dom))) best = kv.second, dom = kv.first;
     // the masked dominant-row sum adds dval * 0.0 for absent entries: finite values only
     bool have_dom = dom.len <= 7;
-    for (int k = 0; k < dom.len && have_dom; ++k) have_dom = std::isfinite(dom.v[k]);
+    for (int k = 0; k < dom.len && have_dom; ++k) {
+        double v;
+        std::memcpy(&v, &dom.v[k], 8);  // v[] holds the value bits
+        have_dom = std::isfinite(v);
+    }
     // pass 2: masks for subsets of the dominant row, generic classes for the rest
     std::unordered_map<Row, int, RH> dict;
     std::vector<Row> rows;
