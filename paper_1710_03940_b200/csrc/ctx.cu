@@ -530,6 +530,13 @@ int dfl_ctx_finalize(dfl_ctx *ctx) {
             return DFL_E_STATE;
         }
     CK(cudaSetDevice(ctx->device));
+    // graphs captured against the previous buffers (a context finalized again)
+    if (ctx->solve_exec) cudaGraphExecDestroy(ctx->solve_exec), ctx->solve_exec = nullptr, ctx->solve_key.clear();
+    if (ctx->loop_exec) cudaGraphExecDestroy(ctx->loop_exec), ctx->loop_exec = nullptr, ctx->loop_key = -1;
+    if (ctx->bg_exec) cudaGraphExecDestroy(ctx->bg_exec), ctx->bg_exec = nullptr, ctx->bg_key = -1;
+    for (auto &e : ctx->body_exec)
+        if (e) cudaGraphExecDestroy(e), e = nullptr;
+    ctx->body_key = -1;
     RC(build_groups(ctx));
     ctx->pending.clear();
     ctx->pending.shrink_to_fit();
