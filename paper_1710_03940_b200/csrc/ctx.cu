@@ -754,11 +754,10 @@ int dfl_coarse_lift(dfl_ctx *ctx, const double *r, double *out, int ptr_kind) {
     }
     RC(stage_in(ctx, ctx->tmp, r, ptr_kind));
     launch_k(ctx->st, k_zt_vec, (unsigned)ctx->ntiles, kBlock, 0, ctx->tiles, ctx->tmp, ctx->zcols, ctx->n, ctx->k,
-                                                           ctx->zt_part);
+             ctx->zt_part, zcode_of(ctx));
     RC(zt_to_t2(ctx, nullptr, 0, false));
     launch_k(ctx->st, k_lift, (unsigned)ctx->ntiles, kBlock, 0, ctx->tiles, ctx->tile_sub, ctx->tmp, ctx->zcols, ctx->n,
-                                                         ctx->k, ctx->t2, (int64_t)ctx->first_sub * ctx->k,
-                                                         ctx->yout, 0);
+             ctx->k, ctx->t2, (int64_t)ctx->first_sub * ctx->k, ctx->yout, 0, zcode_of(ctx));
     return stage_out(ctx, out, ctx->yout, ptr_kind);
 }
 

@@ -382,7 +382,7 @@ int sweep(dfl_block *B, const SweepParams &sp, const double *b_u, const double *
         RC(vcycle(ctx, B->pt, B->pz, nullptr, nullptr, nullptr));
         k_lift<<<(unsigned)ctx->ntiles, kBlock, 0, ctx->st>>>(ctx->tiles, ctx->tile_sub, B->pz, ctx->zcols, ctx->n,
                                                               ctx->k, ctx->t2, (int64_t)ctx->first_sub * ctx->k, o,
-                                                              1);
+                                                              1, zcode_of(ctx));
         ctx->launches++;
         return DFL_OK;
     };

@@ -325,17 +325,19 @@ static int cg_prologue(dfl_ctx *ctx, const dfl_solve_params *p) {
                                       std::max(1, p->refresh_every));
     ctx->launches++;
     // b' = project(b) and ||b'||^2
+    // (without x0 the same kernel also writes r = b')
+    const bool x0 = use_x0(ctx, p);
     if (defl) {
-        RC(project_dev(ctx, ctx->b, ctx->bp, nullptr, 2));
+        RC(project_dev(ctx, ctx->b, ctx->bp, nullptr, 2, x0 ? nullptr : ctx->r));
     } else {
         ProjArgs a = proj_args(ctx, ctx->b, ctx->bp, nullptr);
         a.azd = nullptr;
         a.K = 0;
         a.dotmode = 2;
         a.dot_part = ctx->dpart;
+        a.out2 = x0 ? nullptr : ctx->r;
         launch_project<0>(ctx, a);
     }
-    const bool x0 = use_x0(ctx, p);
     if (x0) {  // x = x0 (unless b = 0), r = b - A x0 and ||r|| (krylov.py:108-109)
         launch_k(ctx->st, k_copy_live, (unsigned)ctx->nblk, kBlock, 0, ctx->x, (const double *)ctx->x0, ctx->n,
                  (const KState *)st);
@@ -347,10 +349,6 @@ static int cg_prologue(dfl_ctx *ctx, const dfl_solve_params *p) {
     RC(rank_scalar(ctx, ctx->dpart, ctx->vgrid, 0, &gath));
     launch_k(ctx->st, k_cg_init_r, 1, 1024, 0, st, ctx->dpart, ctx->vgrid, gath, ctx->nranks);
     ctx->launches++;
-    if (!x0) {
-        launch_k(ctx->st, k_copy, (unsigned)ctx->nblk, kBlock, 0, ctx->r, ctx->bp, ctx->n);
-        ctx->launches++;
-    }
     int64_t np = 0;
     RC(vcycle(ctx, ctx->r, ctx->z, st, ctx->dpart, &np));
     RC(rank_scalar(ctx, ctx->dpart, np, 0, &gath));

@@ -113,13 +113,15 @@ int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double 
 }
 
 // out = project(v) = v - AZ E^-1 Z' v   (deflation.py:230-233)
-int project_dev(dfl_ctx *ctx, const double *v, double *out, const KState *st, int dotmode) {
-    launch_k(ctx->st, k_zt_vec, (unsigned)ctx->ntiles, kBlock, 0, ctx->tiles, v, ctx->zcols, ctx->n, ctx->k, ctx->zt_part);
+int project_dev(dfl_ctx *ctx, const double *v, double *out, const KState *st, int dotmode, double *out2) {
+    launch_k(ctx->st, k_zt_vec, (unsigned)ctx->ntiles, kBlock, 0, ctx->tiles, v, ctx->zcols, ctx->n, ctx->k, ctx->zt_part,
+             zcode_of(ctx));
     ctx->launches++;
     RC(zt_to_t2(ctx, nullptr, 0, false));
     ProjArgs a = proj_args(ctx, v, out, st);
     a.dotmode = dotmode;
     a.dot_part = ctx->dpart;
+    a.out2 = out2;
     launch_project<0>(ctx, a);
     return DFL_OK;
 }
@@ -131,7 +133,7 @@ int lift_dev(dfl_ctx *ctx, const dfl_solve_params *p) {
         RC(zt_to_t2(ctx, nullptr, 0, true));
         launch_k(ctx->st, k_lift, (unsigned)ctx->ntiles, kBlock, 0, ctx->tiles, ctx->tile_sub, ctx->x, ctx->zcols, ctx->n,
                                                               ctx->k, ctx->t2, (int64_t)ctx->first_sub * ctx->k,
-                                                              ctx->xin, 1);
+                                                              ctx->xin, 1, zcode_of(ctx));
     } else {
         launch_k(ctx->st, k_copy, (unsigned)ctx->nblk, kBlock, 0, ctx->xin, ctx->x, ctx->n);
     }

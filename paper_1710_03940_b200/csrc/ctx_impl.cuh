@@ -517,6 +517,16 @@ static void launch_op(dfl_ctx *ctx, const OpArgs &a) {
 // cross-unit entry points (return DFL_OK or a DFL_E_* code, message in ctx->err)
 
 inline bool multi(const dfl_ctx *ctx) { return ctx->comm != nullptr || ctx->fab != nullptr; }
+inline ZCode zcode_of(const dfl_ctx *ctx) {
+    ZCode z;
+    if (ctx->zcode) {
+        z.code = ctx->zcode;
+        z.tab = ctx->ztab;
+        z.stride = ctx->zs;
+        for (int c = 0; c < kKmax; ++c) z.off[c] = ctx->ztab_off[c];
+    }
+    return z;
+}
 // the plain block-AMG Krylov path starts from x0 (krylov.py:108/275/383)
 inline bool use_x0(const dfl_ctx *ctx, const dfl_solve_params *p) { return p->x0_given && !p->deflated && ctx->x0; }
 
@@ -588,7 +598,7 @@ int comm_wait_event(dfl_ctx *ctx, cudaEvent_t e);
 int vcycle(dfl_ctx *ctx, const double *r, double *z, const KState *st, double *dot_part, int64_t *nparts);
 int op_apply_dev(dfl_ctx *ctx, double *xin, double *y, int opmode, const double *b, bool zt, const KState *st,
                  int need_refresh);
-int project_dev(dfl_ctx *ctx, const double *v, double *out, const KState *st, int dotmode);
+int project_dev(dfl_ctx *ctx, const double *v, double *out, const KState *st, int dotmode, double *out2 = nullptr);
 int lift_dev(dfl_ctx *ctx, const dfl_solve_params *p);
 // ctx_cg.cu / ctx_krylov.cu
 int cg_solve_dev(dfl_ctx *ctx, const dfl_solve_params *p, bool use_graph);

@@ -1117,9 +1117,23 @@ __global__ void __launch_bounds__(kBlock) k_op_bnd(DMat A, const int *__restrict
 }
 
 // Z' v partials without a product (project(b), coarse_lift(r))
+// the dictionary-coded Z columns (OpArgs::zcode) for the kernels outside the
+// operator; code == nullptr: read the dense columns
+struct ZCode {
+    const uint16_t *code = nullptr;
+    const double *tab = nullptr;
+    int stride = 0;
+    int off[kKmax] = {};
+};
+// Z column c (1..k-1) of row i
+__device__ __forceinline__ double zcol(const ZCode &zc, const double *zcols, int64_t n, int c, int64_t i,
+                                       const uint32_t (&w)[4]) {
+    return zc.code ? __ldg(zc.tab + zc.off[c - 1] + code_at(w, c - 1)) : __ldg(zcols + (int64_t)(c - 1) * n + i);
+}
+
 static __global__ void __launch_bounds__(kBlock) k_zt_vec(Tiles T, const double *__restrict__ v,
                                                    const double *__restrict__ zcols, int64_t n,
-                                                   int k, double *zt_part) {
+                                                   int k, double *zt_part, const ZCode zc) {
     DFL_PDL_ENTRY;
     const int64_t t = blockIdx.x;
     __shared__ double sm[32 * kKmax];
@@ -1128,10 +1142,12 @@ static __global__ void __launch_bounds__(kBlock) k_zt_vec(Tiles T, const double 
     for (int c = 0; c < kKmax; ++c) acc[c] = 0.0;
     for (int64_t i = T.row0[t] + threadIdx.x; i < T.row1[t]; i += blockDim.x) {  // tiles may be wider than the block
         const double y = v[i];
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        if (zc.code && k > 1) load_codes(zc.code, zc.stride, i, w);
         acc[0] += y;
 #pragma unroll
         for (int c = 1; c < kKmax; ++c)
-            if (c < k) acc[c] += __ldg(zcols + (int64_t)(c - 1) * n + i) * y;
+            if (c < k) acc[c] += zcol(zc, zcols, n, c, i, w) * y;
     }
     block_sum<kKmax>(acc, sm);
     if (threadIdx.x == 0)
@@ -1306,6 +1322,7 @@ struct ProjArgs {
     int64_t n;
     const double *in;   // w
     double *out;        // w - AZ t2   (may alias in)
+    double *out2;       // optional second copy of out (the CG prologue's r = b')
     const double *dotv; // dotmode 1: partial dot(dotv, out)
     const double *base; // MODE 1: out = base - (in - AZ t2)
     double *dot_part;
@@ -1369,6 +1386,7 @@ __global__ void __launch_bounds__(kBlock, KZ > 4 ? 4 : DFL_PROJ_MINB) k_project(
         if (a.azd) q = sub_rn(q, az_row<KZ>(a, i, s));
         if (MODE == 1) q = sub_rn(__ldg(a.base + i), q);
         a.out[i] = q;
+        if (a.out2) a.out2[i] = q;
         if (a.dotmode == 1) dot += __ldg(a.dotv + i) * q;
         if (a.dotmode == 2) dot += q * q;
     }
@@ -1385,13 +1403,15 @@ __global__ void __launch_bounds__(kBlock, KZ > 4 ? 4 : DFL_PROJ_MINB) k_project(
 static __global__ void __launch_bounds__(kBlock) k_lift(Tiles T, const int *tile_sub, const double *__restrict__ y,
                                                  const double *__restrict__ zcols, int64_t n, int k,
                                                  const double *__restrict__ t2, int64_t first_col,
-                                                 double *out, int add_y) {
+                                                 double *out, int add_y, const ZCode zc) {
     DFL_PDL_ENTRY;
     const int64_t t = blockIdx.x;
     const int64_t base = (first_col + (int64_t)tile_sub[t] * k);
     for (int64_t i = T.row0[t] + threadIdx.x; i < T.row1[t]; i += blockDim.x) {
+        uint32_t w[4] = {0u, 0u, 0u, 0u};
+        if (zc.code && k > 1) load_codes(zc.code, zc.stride, i, w);
         double acc = add_rn(0.0, mul_rn(1.0, t2[base]));
-        for (int c = 1; c < k; ++c) acc = add_rn(acc, mul_rn(zcols[(int64_t)(c - 1) * n + i], t2[base + c]));
+        for (int c = 1; c < k; ++c) acc = add_rn(acc, mul_rn(zcol(zc, zcols, n, c, i, w), t2[base + c]));
         out[i] = add_y ? add_rn(y[i], acc) : acc;
     }
 }
